@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the MLMC sample path: MLMC samples/s per level (CE field + Darcy solve, fp64)
+and its fraction of the B200 HBM roofline.
+
+Default workload (BASELINE.json config 4, the per-level CE + MG-PCG configuration that is
+sharded across GPUs): Matérn ν=0.5, σ²=2, λ=0.003; coupled (2048², 1024²) samples, batches of
+64 per GPU; f = 1; homogeneous Dirichlet on all sides; MG-PCG to relative residual 1e-10; fp64.
+A step = one batch of 64 coupled samples through osc_level_draws (ξ from the device Philox
+stream NormalStream(seed, ℓ, i), fine + coarse fields, both solves, QoIs, level sums).
+Per-GPU work is fixed as N grows (weak scaling: rank r draws its own contiguous index range).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4|1|2|3]
+
+Rank 0 prints ONE JSON line. `--impl reference` times the reference's CPU implementation of the
+same workload on the host cores (oracle/_ref for the reference's own BCs; the oracle port for
+the all-Dirichlet extension the reference lacks) — rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+# ---- workloads ---------------------------------------------------------------------------------
+def workload(cfg: str):
+    """(name, dict) for a BASELINE config; per-sample algorithmic bytes follow SURVEY §8(d)."""
+    if cfg == "4":
+        return dict(name="cfg4: matern nu=0.5 s2=2 lam=0.003, coupled 2048^2/1024^2, dirichlet-all, f=1, MG-PCG 1e-10",
+                    family="matern", sigma2=2.0, lam=0.003, nu=0.5, m=2048, coupled=True, bc=1, qoi=0,
+                    batch=64, ell=1, it=(43, 44))
+    if cfg == "1":
+        return dict(name="cfg1: matern nu=0.5 s2=1 lam=0.1, 64^2 single-level MC, dirichlet-all, integral QoI",
+                    family="matern", sigma2=1.0, lam=0.1, nu=0.5, m=64, coupled=False, bc=1, qoi=2,
+                    batch=1000, ell=0, it=(16, 0))
+    if cfg == "3":
+        return dict(name="cfg3 level 4: sep-exp s2=1 lam=0.01, coupled 256^2/128^2, flow-cell, flux QoI",
+                    family="sep", sigma2=1.0, lam=0.01, nu=1.0, m=256, coupled=True, bc=0, qoi=3,
+                    batch=1024, ell=4, it=(25, 24))
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def algorithmic_bytes_per_sample(W, n):
+    """B = B_ce + B_solve(m) + B_solve(m/2), B_solve(m) = (m+1)²(200 + 251 it),
+    B_ce (device ξ, √λ amortised over the batch) = 8 s/B + 32 n (n/2+1) + 8 (N_f + N_c)."""
+    m = W["m"]
+    s = n * n
+    Nf, Nc = (m + 1) ** 2, (m // 2 + 1) ** 2
+    b_ce = 8 * s / W["batch"] + (32 * n * (n // 2 + 1) if 16 * n * (n // 2 + 1) > 227 * 1024 else 0) + \
+        8 * (Nf + (Nc if W["coupled"] else 0))
+    itf, itc = W["it"]
+    b = b_ce + Nf * (200 + 251 * itf)
+    if W["coupled"]:
+        b += Nc * (200 + 251 * itc)
+    return b
+
+
+# per-kernel compulsory HBM bytes per node of the grid the kernel runs on:
+# inputs read once + outputs written once, for one active sample
+KERNEL_BYTES_PER_NODE = {
+    "pcg_apply": 7 * 8,          # read z, p_old, D, E, N; write p_new, Ap
+    "pcg_update": 6 * 8,         # read u, p, r, Ap; write u, r
+    "mg_smooth_down": 5 * 8,     # read r, D, E, N; write z
+    "mg_smooth_up_black": 6 * 8,  # read r, z, D, E, N (+ coarse zc, 1/4); write z (half)
+    "mg_smooth_up_red": 6 * 8,
+    "mg_restrict": 5 * 8,        # read r, z, D, E, N (fine) per coarse-node neighbourhood
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---- reference (CPU) arm --------------------------------------------------------------------------
+def cpu_reference_step(W, threads: int, n_samples: int, seed_index: int, port=None, ref=None):
+    """Run n_samples coupled samples of the workload on the CPU path with `threads` threads.
+    Uses the pristine reference (oracle/_ref) for flow-cell BCs, else the oracle port."""
+    from oracle import oracle as O
+    from paper_2306_13493_b200 import api
+    m = W["m"]
+    if W["bc"] == 0 and ref is not None and W["qoi"] in (0, 1):
+        opts = O.RefOpts.make(family=O.MATERN if W["family"] == "matern" else O.SEP_EXP,
+                              sigma2=W["sigma2"], lam=W["lam"], nu_or_p=W["nu"], qoi_kind=W["qoi"],
+                              seed=1, threads=threads)
+        key = ("plan", m)
+        if key not in _CACHE:
+            _CACHE[key] = ref.plan(W["ell"], 1.0 / (m >> W["ell"]), opts)
+        t0 = time.perf_counter()
+        ref.coupled(_CACHE[key], W["coupled"], False, False, opts, seed_index, seed_index + n_samples)
+        return time.perf_counter() - t0, "reference"
+    key = ("op", m)
+    if key not in _CACHE:
+        model = (api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]) if W["family"] == "matern"
+                 else api.CovarianceModel.separable_exponential(W["sigma2"], W["lam"]))
+        op = api.build_operator(api.GridSpec.square(m), model)
+        _CACHE[key] = (op, np.sqrt(np.maximum(op.eigenvalues, 0.0)))
+    op, sl = _CACHE[key]
+    t0 = time.perf_counter()
+    port.coupled(m, op.n, sl, None, W["coupled"], 1, W["ell"], seed_index, seed_index + n_samples,
+                 bc=W["bc"], qoi=W["qoi"], threads=threads)
+    return time.perf_counter() - t0, "port"
+
+
+_CACHE = {}
+
+
+def run_reference(args, W):
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    port = O.Port()
+    ref = O.Ref() if os.path.exists(O.REF_SO) else None
+    per_step = cores  # one coupled sample per host core per step (bounded sample)
+    if W["m"] <= 256:
+        per_step = cores * max(1, int(4096 // (W["m"] * W["m"] // 64 + 1)))
+    for w in range(min(args.warmup, 1)):
+        cpu_reference_step(W, cores, min(per_step, cores), 10_000_000 + w, port, ref)
+    times, kind = [], "port"
+    t_budget = time.time() + 240.0
+    for k in range(args.steps):
+        dt, kind = cpu_reference_step(W, cores, per_step, k * per_step, port, ref)
+        times.append(dt)
+        if time.time() > t_budget:
+            break
+    total = sum(times)
+    value = per_step * len(times) / total
+    line = {
+        "impl": "reference", "metric": "MLMC samples/s per level (CE field + Darcy solve, fp64)",
+        "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": len(times),
+        "warmup": min(args.warmup, 1), "ms_per_step": 1000 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (NormalStream seed 1)",
+        "config": {"workload": W["name"], "global_batch": per_step, "parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} coupled samples per step x {len(times)} steps"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm -----------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="4")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    W = workload(args.config)
+    if args.batch:
+        W["batch"] = args.batch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, W)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2306_13493_b200 import api
+    ctx = api.Context(local)
+    m, B = W["m"], W["batch"]
+    model = (api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]) if W["family"] == "matern"
+             else api.CovarianceModel.separable_exponential(W["sigma2"], W["lam"]))
+    problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind(W["qoi"])), bc=api.BC(W["bc"]))
+    opt = api.EstimatorOptions(seed=1)
+    t_setup = time.perf_counter()
+    plan = api.make_level_plan(W["ell"], 1.0 / (m >> W["ell"]), problem, opt)
+    t_setup = time.perf_counter() - t_setup
+    lev = plan.op.device_level(ctx, 0)
+    coarse = api.GridSpec.square(m // 2) if W["coupled"] else None
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    import ctypes as C
+    from paper_2306_13493_b200 import _lib as L
+    lib = L.lib()
+    ps = api._problem_struct(problem, opt.solver)
+    flags = L.DRAW_HAS_COARSE if W["coupled"] else 0
+    qf, qc = np.empty(B), np.empty(B)
+    itf, itc, st = (np.zeros(B, dtype=np.int32) for _ in range(3))
+    sums = np.zeros(8)
+    iters_total = [0, 0]
+
+    def step(k, xi=None):
+        frm = (k * world + rank) * B
+        code = lib.osc_level_draws(lev.h, C.byref(ps), opt.seed, W["ell"], frm, frm + B, flags,
+                                   None if xi is None else xi.ctypes.data_as(C.c_void_p),
+                                   qf.ctypes.data, qc.ctypes.data, itf.ctypes.data, itc.ctypes.data,
+                                   st.ctypes.data, sums.ctypes.data)
+        api._check(code, status=st)
+        iters_total[0] += int(itf.sum())
+        iters_total[1] += int(itc.sum())
+
+    for w in range(args.warmup):
+        step(1_000_000 + w)
+    # timed region
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    iters_total[:] = [0, 0]
+    launches0 = ctx.launch_count
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    e1.record(stream)
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    gpu_launches = ctx.launch_count - launches0
+    kstats = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    samples = args.steps * B * world
+    value = samples / (ms / 1000.0)
+
+    # roofline of the dominant kernel (compulsory bytes / its event-timed duration)
+    hbm, hbm_kind = peaks()
+    dom = max(kstats.items(), key=lambda kv: kv[1][1])
+    dom_name = dom[0]
+    base = dom_name.split("@")[0]
+    roof = None
+    if base in ("pcg_apply", "pcg_update"):
+        nodes_f, nodes_c = (m + 1) ** 2, (m // 2 + 1) ** 2
+        grid_nodes = nodes_f if dom_name.endswith(f"@{m}") else nodes_c
+        sample_iters = iters_total[0] if dom_name.endswith(f"@{m}") else iters_total[1]
+        alg_bytes = KERNEL_BYTES_PER_NODE[base] * grid_nodes * sample_iters
+        launches, tot_ms = dom[1]
+        achieved = alg_bytes / (tot_ms / 1000.0) / 1e9
+        roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind,
+                "alg_bytes_per_launch": alg_bytes / max(launches, 1), "avg_launch_ms": tot_ms / max(launches, 1)}
+    n = lev.n
+    b_sample = algorithmic_bytes_per_sample(W, n)
+    pipeline = {"basis": "SURVEY 8(d) B per coupled sample", "bytes_per_sample": b_sample,
+                "roofline_samples_per_s_per_gpu": hbm * 1e9 / b_sample,
+                "frac": value / world / (hbm * 1e9 / b_sample)}
+
+    # e2e: same metric through the C-ABI with HOST ξ (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        s = lev.s
+        pool = min(B, 8)
+        buf = api.PinnedBuffer((B, s))
+        # ξ rows for the step from the device Philox stream of a pool of indices (outside timing)
+        tmp = np.empty((pool, s))
+        lib.osc_normals(ctx.h, opt.seed, W["ell"], 0, pool, s, tmp.ctypes.data)
+        for b in range(B):
+            buf.array[b] = tmp[b % pool]
+        del tmp
+        k_e2e = max(1, min(args.steps, 3))
+        step(2_000_000, xi=buf.array)  # warm the host-ξ path
+        if dist:
+            dist.barrier()
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for k in range(k_e2e):
+            step(3_000_000 + k, xi=buf.array)
+        f1.record(stream)
+        ctx.synchronize()
+        ems = f0.elapsed_time(f1)
+        if dist:
+            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": k_e2e * B * world / (ems / 1000.0), "unit": "samples/s",
+               "h2d_bytes_per_step": 8 * s * B, "d2h_bytes_per_step": 8 * 2 * B + 4 * 3 * B + 40,
+               "xi": f"host pinned, {pool} distinct Philox rows cycled over the batch", "steps": k_e2e}
+        buf.free()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        cores = os.cpu_count() or 1
+        ref = O.Ref() if os.path.exists(O.REF_SO) else None
+        dt, kind = cpu_reference_step(W, cores, cores, 0, O.Port(), ref)
+        cpu = {"value": cores / dt, "unit": "samples/s", "cores": cores, "kind": kind,
+               "sample": f"{cores} coupled samples of the same workload, one per host thread ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "MLMC samples/s per level (CE field + Darcy solve, fp64)",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: xi = NormalStream(seed 1, l, i) on device (Philox4x32-10 + Box-Muller)",
+            "config": {"workload": W["name"], "global_batch": B * world, "per_gpu_batch": B,
+                       "grid": f"{m}^2/{m // 2}^2" if W["coupled"] else f"{m}^2", "embedding_n": n,
+                       "parallelism": f"dp{world} (contiguous sample shards)",
+                       "l2": "inputs larger than L2 (>= 40 GB touched per step)" if m >= 1024 else
+                       "per-step working set exceeds L2 (batch)",
+                       "setup_s": round(t_setup, 2),
+                       "mean_iters_fine": iters_total[0] / (args.steps * B),
+                       "mean_iters_coarse": iters_total[1] / (args.steps * B) if W["coupled"] else None},
+            "roofline": roof, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": gpu_launches, "clocks": ck,
+            "kernels_ms": {k: round(v[1], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * oscfield_b200.h — C-ABI of the B200-native MLMC sample path
+ * (circulant-embedding field → coarse/fine restriction → batched fp64 Darcy MG-PCG →
+ * QoI → per-level sums). Implemented by paper_2306_13493_b200/libosc_b200.so
+ * (hand-written sm_100a CUDA + host C++). Plain pointers and sizes only.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj):
+ *
+ *   osc_level_draws     ← run_level_draws (include/oscfield/estimators.hpp:112-118, declared
+ *                         but undefined in the reference; its body today is run_level_samples,
+ *                         src/estimators.cpp:65-75 → coupled_sample :200-237 per index)
+ *   osc_summarize       ← summarize_draws (estimators.hpp:120-128; body = moments_of,
+ *                         src/estimators.cpp:82-101)
+ *   osc_ce_sample       ← EmbeddingOperator::sample_into + restrict_to
+ *                         (include/oscfield/embedding.hpp:63-69, src/embedding.cpp:165-203)
+ *   osc_darcy_solve     ← assemble_and_solve (include/oscfield/fem.hpp:47, src/fem.cpp:317-400)
+ *   osc_qoi             ← evaluate_qoi / qoi_point / qoi_l2norm (estimators.hpp:23,
+ *                         fem.hpp:51-54, src/fem.cpp:402-436)
+ *   osc_build_spectrum  ← build_operator (embedding.hpp:112-113, src/embedding.cpp:114-151)
+ *   osc_level_create    ← EmbeddingOperator::from_parts + truncated (embedding.cpp:90-112,153-163)
+ *   osc_normals         ← NormalStream::fill (include/oscfield/rng.hpp:30-43, src/rng.cpp:42-67)
+ *
+ * Errors: every function returns an osc_status. Non-zero codes map onto the reference's
+ * exception taxonomy (include/oscfield/errors.hpp:10-29): OSC_ERR_CONFIG → ConfigError,
+ * OSC_ERR_NUMERICAL → NumericalError, OSC_ERR_SOLVER → SolverError (per-sample status[]
+ * says which samples, the optional history buffer carries the residual history),
+ * OSC_ERR_EMBEDDING → EmbeddingError. The message is available from osc_last_error().
+ *
+ * Threading: one osc_ctx per device, driven by one host thread (mirrors one
+ * SampleWorkspace per worker, embedding.hpp:24-35). Device buffers are owned by the
+ * context/level and stay resident across calls; host buffers are owned by the caller.
+ *
+ * Layouts: nodal arrays are fp64, x fastest, index p0 + (m+1)*p1 (grid.hpp:13-15,39-41).
+ * ξ is fp64 of length s = n*n in NormalStream::fill order (q0 + n*q1).
+ */
+#ifndef OSCFIELD_B200_H
+#define OSCFIELD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  OSC_OK = 0,
+  OSC_ERR_CONFIG = 2,     /* ConfigError (CLI exit 2) */
+  OSC_ERR_NUMERICAL = 3,  /* NumericalError (CLI exit 3) */
+  OSC_ERR_SOLVER = 4,     /* SolverError: CG did not reach tol within the cap */
+  OSC_ERR_EMBEDDING = 5,  /* EmbeddingError: no SPD embedding within the padding schedule */
+  OSC_ERR_CUDA = 6        /* device / driver failure */
+} osc_status;
+
+/* Boundary conditions. FLOWCELL is the reference's (fem.hpp:11-16, fem.cpp:28-30):
+ * u=1 at x=0, u=0 at x=1, zero flux on y∈{0,1}. DIRICHLET_ALL (u=0 on all sides) is an
+ * extension required by BASELINE configs 1 and 4 (parity unpinned by the reference). */
+enum { OSC_BC_FLOWCELL = 0, OSC_BC_DIRICHLET_ALL = 1 };
+/* QoIs: POINT, L2 as the reference (estimators.hpp:16-21); INTEGRAL (∫u dx) and FLUX
+ * (outflow flux through x=1) are extensions for BASELINE configs 1/3/5. */
+enum { OSC_QOI_POINT = 0, OSC_QOI_L2 = 1, OSC_QOI_INTEGRAL = 2, OSC_QOI_FLUX = 3 };
+/* Covariance families (covariance.hpp:10). */
+enum { OSC_COV_MATERN = 0, OSC_COV_SEPARABLE_EXP = 1 };
+
+/* osc_level_draws flags */
+enum {
+  OSC_DRAW_HAS_COARSE = 1,      /* level ℓ>0: also solve on the coarse grid m/2 */
+  OSC_DRAW_TRUNC_FINE = 2,      /* fine field from the truncated (smoothed) spectrum */
+  OSC_DRAW_TRUNC_COARSE = 4,    /* coarse field from the truncated spectrum */
+  OSC_DRAW_XI_DEVICE = 8        /* xi points to DEVICE memory (else host memory) */
+};
+/* osc_ce_sample flags */
+enum {
+  OSC_CE_TRUNCATED = 1,         /* use the truncated spectrum */
+  OSC_CE_EXP = 2,               /* write k = exp(Z) instead of Z */
+  OSC_CE_FINE = 4,              /* write the fine field (m+1)^2 */
+  OSC_CE_COARSE = 8             /* write the stride-2 coarse field (m/2+1)^2 */
+};
+
+/* Flat mirror of DarcyProblem / SolverOptions / QoiSpec (fem.hpp:17-35,
+ * estimators.hpp:16-30). Preconditioner is always geometric multigrid (the estimator
+ * default, estimators.hpp:79): red-black Gauss-Seidel V(1,1), P1 transfer, injected k,
+ * per-sample dense Cholesky on the coarsest grid. */
+typedef struct {
+  int bc;               /* OSC_BC_* */
+  int forcing;          /* 0 = Forcing::Zero, 1 = Forcing::Constant */
+  double forcing_value; /* f */
+  int qoi;              /* OSC_QOI_* */
+  double qoi_x, qoi_y;  /* point QoI location, default (7/15, 7/15) */
+  double tol;           /* relative residual target, default 1e-10 */
+  int max_iter_factor;  /* CG cap = factor * node count, default 10 */
+} osc_problem;
+
+typedef struct osc_ctx osc_ctx;
+typedef struct osc_level osc_level;
+
+/* ---- context --------------------------------------------------------------- */
+int osc_ctx_create(int device, osc_ctx** out);
+void osc_ctx_destroy(osc_ctx* ctx);
+/* Thread-local message of the last failing call. */
+const char* osc_last_error(void);
+/* The cudaStream_t (as void*) every kernel of this context is launched on. */
+void* osc_ctx_stream(osc_ctx* ctx);
+int osc_ctx_synchronize(osc_ctx* ctx);
+/* Device memory budget (bytes) for batch workspaces; 0 = 60% of free memory. */
+int osc_ctx_set_mem_budget(osc_ctx* ctx, size_t bytes);
+/* Per-kernel-class timing with CUDA events on the context stream (0 off / 1 on). */
+int osc_ctx_set_profiling(osc_ctx* ctx, int on);
+/* Number of kernel classes with stats; name/launch count/total ms of class i. */
+int osc_ctx_kernel_stats(osc_ctx* ctx, int i, const char** name, int64_t* launches,
+                         double* total_ms);
+int osc_ctx_reset_stats(osc_ctx* ctx);
+/* Kernels launched by this context since creation (all classes). */
+int64_t osc_ctx_launch_count(osc_ctx* ctx);
+
+/* Pinned host memory for overlapped H2D/D2H (cudaHostAlloc). */
+void* osc_host_alloc(size_t bytes);
+void osc_host_free(void* p);
+/* Library-allocated host buffer release (osc_build_spectrum output). */
+void osc_free(void* p);
+
+/* ---- level setup (host C++) ---------------------------------------------------- */
+/* build_operator: first row (embedding.cpp:22-65) → spectrum (:67-88) with padding
+ * schedule J = 0, then ceil(f*m) for f in fractions (:132-141) until min λ ≥ -tol_spd
+ * (tol_spd = tol_spd_factor * s * sigma2), negatives clamped to 0. Returns J and a
+ * malloc'd eigenvalue array of s = (2(m+J))^2 entries (release with osc_free).
+ * fractions = NULL → {0.5, 1, 2, 4, 8}; tol_spd_factor ≤ 0 → 1e-12. */
+int osc_build_spectrum(int m, int family, double sigma2, double lambda, double nu_or_p,
+                       const double* fractions, int n_fractions, double tol_spd_factor,
+                       int* J_out, int64_t* s_out, double** eig_out);
+/* Upload one level: n = 2(m+J); eigenvalues (s entries) → √max(λ,0) on device, plus the
+ * truncated copy zeroing the k_trunc smallest by a stable descending sort
+ * (embedding.cpp:105-110,153-163). k_trunc = 0 → no truncated copy. */
+int osc_level_create(osc_ctx* ctx, int m, int J, const double* eigenvalues, int64_t k_trunc,
+                     osc_level** out);
+void osc_level_destroy(osc_level* level);
+/* m, J, n, s and k_trunc of a level. */
+int osc_level_info(const osc_level* level, int* m, int* J, int* n, int64_t* s, int64_t* k_trunc);
+
+/* ---- the fused per-level batch (the drop-in seam) ------------------------------ */
+/* Draws samples [from, to) on one level: ξ_i = NormalStream(seed, ell, i) generated on
+ * device (xi == NULL) or taken from xi (row i-from, s doubles; host or device memory per
+ * OSC_DRAW_XI_DEVICE); fine field (and, with OSC_DRAW_HAS_COARSE, the stride-2 coarse
+ * field of the same ξ — from the other spectrum when the TRUNC flags differ,
+ * estimators.cpp:221-234); batched MG-PCG solves; QoIs. Slot i-from of q_fine / q_coarse
+ * / iters_* / status receives sample i, so results do not depend on how [from,to) is
+ * split across calls, ranks or devices (estimators.hpp:112-114). Any output pointer
+ * may be NULL. level_sums (may be NULL) receives, accumulated in slot order on device,
+ * [count, Σ(Y-shift), Σ(Y-shift)², Σ(q_f-shift_q), Σ(q_f-shift_q)²] with
+ * Y = q_fine - q_coarse (or q_fine) and shifts given in level_sums[5], level_sums[6]
+ * on input. Returns OSC_ERR_SOLVER if any sample failed to converge (its status[] slot
+ * is OSC_ERR_SOLVER), OSC_ERR_NUMERICAL on a non-finite field. */
+int osc_level_draws(osc_level* level, const osc_problem* problem, uint64_t seed, uint32_t ell,
+                    int64_t from, int64_t to, int flags, const double* xi, double* q_fine,
+                    double* q_coarse, int32_t* iters_fine, int32_t* iters_coarse,
+                    int32_t* status, double* level_sums);
+
+/* summarize_draws: one-pass Welford over slot-ordered draws (estimators.cpp:82-101).
+ * out = [n, mean_y, var_y, mean_q, var_q]; var only when n ≥ 2. q_coarse may be NULL. */
+int osc_summarize(const double* q_fine, const double* q_coarse, int64_t n, int has_coarse,
+                  double out[5]);
+
+/* ---- unfused stages (single-sample reference APIs, unit tests) -------------------- */
+/* NormalStream(seed, ell, index0 + j).fill for j < count on device; out host (count*s). */
+int osc_normals(osc_ctx* ctx, uint64_t seed, uint32_t ell, uint64_t index0, int64_t count,
+                int64_t s, double* out);
+/* CE sample of `count` samples: xi host (count*s) or NULL for device Philox of indices
+ * [index0, index0+count) at (seed, ell); writes fine ((m+1)^2 each) and/or coarse
+ * ((m/2+1)^2 each) fields to host per OSC_CE_* flags. */
+int osc_ce_sample(osc_level* level, const double* xi, uint64_t seed, uint32_t ell,
+                  uint64_t index0, int64_t count, int flags, double* fine_out,
+                  double* coarse_out);
+/* Batched assemble_and_solve of `count` log fields Z (host, count*(m+1)^2) on grid m.
+ * u_out (host, may be NULL), iters/status per sample (may be NULL); history (may be NULL)
+ * receives hist_cap relative residuals per sample (the reference's residual_history,
+ * fem.cpp:364-365,388), padded with 0. */
+int osc_darcy_solve(osc_ctx* ctx, int m, int64_t count, const double* Z,
+                    const osc_problem* problem, double* u_out, int32_t* iters, int32_t* status,
+                    double* history, int hist_cap);
+/* QoI of `count` nodal solutions u (host) on grid m; Z (host) needed only for FLUX. */
+int osc_qoi(osc_ctx* ctx, int m, int64_t count, const double* u, const double* Z,
+            const osc_problem* problem, double* q_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OSCFIELD_B200_H */

@@ -1,0 +1,538 @@
+// C-ABI (include/oscfield_b200.h): context / level lifetime, the fused per-level batch
+// osc_level_draws (the reference's run_level_draws seam, estimators.hpp:112-118) and the
+// unfused single-stage entry points. Host C++; every kernel runs on the context stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "osc_internal.cuh"
+
+namespace osc {
+struct SetupError {
+  int code;
+  std::string msg;
+};
+std::vector<double> build_spectrum(int m, int family, double sigma2, double lambda, double nu_or_p,
+                                   const double* fractions, int n_fractions, double tol_factor,
+                                   int* J_out);
+void sqrt_spectra(const double* eig, int64_t s, int64_t k_trunc, std::vector<double>& full,
+                  std::vector<double>& trunc);
+}  // namespace osc
+
+using namespace osc;
+
+struct osc_ctx : Ctx {};
+struct osc_level : Level {};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return OSC_OK;
+  } catch (const osc::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const osc::SetupError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return OSC_ERR_NUMERICAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return OSC_ERR_CONFIG;
+  }
+}
+
+void set_device(Ctx* c) { OSC_CUDA(cudaSetDevice(c->device)); }
+
+size_t budget_of(Ctx* c) {
+  if (c->mem_budget) return c->mem_budget;
+  size_t fr = 0, tot = 0;
+  OSC_CUDA(cudaMemGetInfo(&fr, &tot));
+  // what the context already holds is reusable
+  size_t held = c->ce_inter.bytes + c->xi_dev.bytes + c->fields_fine.bytes + c->fields_coarse.bytes +
+                c->solver.mem.bytes + c->out_q.bytes + c->out_i.bytes;
+  return (size_t)(0.6 * (double)(fr + held));
+}
+
+void h2d(Ctx* c, void* dst, const void* src, size_t bytes) {
+  OSC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+}
+void d2h(Ctx* c, void* dst, const void* src, size_t bytes) {
+  OSC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+}
+}  // namespace
+
+// ---- profiling ---------------------------------------------------------------------------------
+namespace osc {
+int Ctx::stat_class(const char* name) {
+  for (size_t i = 0; i < stats.size(); ++i)
+    if (stats[i].name == name) return (int)i;
+  stats.push_back(KernelStat{name});
+  return (int)stats.size() - 1;
+}
+
+void Ctx::flush_stats() {
+  for (auto& s : stats) {
+    for (auto& pr : s.pending) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) s.total_ms += ms;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    s.pending.clear();
+  }
+}
+
+KScope::KScope(Ctx* c, const char* name, int n_launches) : ctx(c) {
+  cls = c->tag.empty() ? c->stat_class(name) : c->stat_class((std::string(name) + "@" + c->tag).c_str());
+  c->stats[cls].launches += n_launches;
+  c->launches += n_launches;
+  if (c->profiling) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->stream);
+  }
+}
+
+KScope::~KScope() {
+  if (e0) {
+    cudaEventRecord(e1, ctx->stream);
+    ctx->stats[cls].pending.emplace_back(e0, e1);
+  }
+}
+}  // namespace osc
+
+extern "C" {
+
+const char* osc_last_error(void) { return g_last_error.c_str(); }
+
+int osc_ctx_create(int device, osc_ctx** out) {
+  return guarded([&] {
+    OSC_REQUIRE(out != nullptr, "osc_ctx_create: null out");
+    auto* c = new osc_ctx();
+    c->device = device;
+    try {
+      OSC_CUDA(cudaSetDevice(device));
+      OSC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      OSC_CUDA(cudaHostAlloc(&c->h_pinned_int, 64, cudaHostAllocDefault));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void osc_ctx_destroy(osc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->flush_stats();
+  for (DevBuf* b : {&c->ce_inter, &c->xi_dev, &c->fields_fine, &c->fields_coarse, &c->out_q,
+                    &c->out_i, &c->tmp_host_stage, &c->sums, &c->solver.mem})
+    b->release();
+  if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* osc_ctx_stream(osc_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int osc_ctx_synchronize(osc_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+  });
+}
+
+int osc_ctx_set_mem_budget(osc_ctx* c, size_t bytes) {
+  c->mem_budget = bytes;
+  return OSC_OK;
+}
+
+int osc_ctx_set_profiling(osc_ctx* c, int on) {
+  return guarded([&] {
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+    c->profiling = on != 0;
+  });
+}
+
+int osc_ctx_kernel_stats(osc_ctx* c, int i, const char** name, int64_t* launches, double* total_ms) {
+  if (i < 0 || i >= (int)c->stats.size()) return OSC_ERR_CONFIG;
+  if (name) *name = c->stats[i].name.c_str();
+  if (launches) *launches = c->stats[i].launches;
+  if (total_ms) *total_ms = c->stats[i].total_ms;
+  return OSC_OK;
+}
+
+int osc_ctx_reset_stats(osc_ctx* c) {
+  return guarded([&] {
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+    for (auto& s : c->stats) {
+      s.launches = 0;
+      s.total_ms = 0.0;
+    }
+  });
+}
+
+int64_t osc_ctx_launch_count(osc_ctx* c) { return c ? c->launches : 0; }
+
+void* osc_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return p;
+}
+void osc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+void osc_free(void* p) { std::free(p); }
+
+// ---- level setup -----------------------------------------------------------------------------
+int osc_build_spectrum(int m, int family, double sigma2, double lambda, double nu_or_p,
+                       const double* fractions, int n_fractions, double tol_spd_factor, int* J_out,
+                       int64_t* s_out, double** eig_out) {
+  return guarded([&] {
+    OSC_REQUIRE(family == OSC_COV_MATERN || family == OSC_COV_SEPARABLE_EXP,
+                "osc_build_spectrum: unknown covariance family");
+    int J = 0;
+    std::vector<double> eig = build_spectrum(m, family, sigma2, lambda, nu_or_p, fractions,
+                                             n_fractions, tol_spd_factor, &J);
+    if (J_out) *J_out = J;
+    if (s_out) *s_out = (int64_t)eig.size();
+    if (eig_out) {
+      double* buf = static_cast<double*>(std::malloc(sizeof(double) * eig.size()));
+      if (!buf) throw std::bad_alloc();
+      std::memcpy(buf, eig.data(), sizeof(double) * eig.size());
+      *eig_out = buf;
+    }
+  });
+}
+
+int osc_level_create(osc_ctx* c, int m, int J, const double* eigenvalues, int64_t k_trunc,
+                     osc_level** out) {
+  return guarded([&] {
+    OSC_REQUIRE(c && out && eigenvalues, "osc_level_create: null argument");
+    OSC_REQUIRE(m >= 1 && J >= 0, "osc_level_create: m >= 1, J >= 0 required");
+    set_device(c);
+    auto* L = new osc_level();
+    L->ctx = c;
+    L->m = m;
+    L->J = J;
+    L->n = 2 * (m + J);
+    L->s = (int64_t)L->n * L->n;
+    OSC_REQUIRE(k_trunc >= 0 && k_trunc < L->s,
+                "truncated: k must lie in [0, s); at least one mode must survive");
+    L->k_trunc = k_trunc;
+    try {
+      std::vector<double> full, trunc;
+      sqrt_spectra(eigenvalues, L->s, k_trunc, full, trunc);
+      L->sqrt_full.ensure(sizeof(double) * L->s);
+      OSC_CUDA(cudaMemcpy(L->sqrt_full.p, full.data(), sizeof(double) * L->s, cudaMemcpyHostToDevice));
+      if (k_trunc > 0) {
+        L->sqrt_trunc.ensure(sizeof(double) * L->s);
+        OSC_CUDA(cudaMemcpy(L->sqrt_trunc.p, trunc.data(), sizeof(double) * L->s, cudaMemcpyHostToDevice));
+      }
+      std::vector<double> tw(2 * (size_t)L->n);
+      for (int t = 0; t < L->n; ++t) {
+        const long double a = 6.283185307179586476925286766559005768L * t / L->n;
+        tw[2 * (size_t)t] = (double)std::cos(a);
+        tw[2 * (size_t)t + 1] = (double)std::sin(a);
+      }
+      L->twiddle.ensure(sizeof(double) * tw.size());
+      OSC_CUDA(cudaMemcpy(L->twiddle.p, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
+    } catch (...) {
+      L->sqrt_full.release();
+      L->sqrt_trunc.release();
+      L->twiddle.release();
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+
+void osc_level_destroy(osc_level* L) {
+  if (!L) return;
+  cudaSetDevice(L->ctx->device);
+  cudaStreamSynchronize(L->ctx->stream);
+  L->sqrt_full.release();
+  L->sqrt_trunc.release();
+  L->twiddle.release();
+  delete L;
+}
+
+int osc_level_info(const osc_level* L, int* m, int* J, int* n, int64_t* s, int64_t* k_trunc) {
+  if (!L) return OSC_ERR_CONFIG;
+  if (m) *m = L->m;
+  if (J) *J = L->J;
+  if (n) *n = L->n;
+  if (s) *s = L->s;
+  if (k_trunc) *k_trunc = L->k_trunc;
+  return OSC_OK;
+}
+
+// ---- the fused per-level batch -----------------------------------------------------------------
+int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32_t ell,
+                    int64_t from, int64_t to, int flags, const double* xi, double* q_fine,
+                    double* q_coarse, int32_t* iters_fine, int32_t* iters_coarse, int32_t* status,
+                    double* level_sums) {
+  return guarded([&] {
+    OSC_REQUIRE(L && prob, "osc_level_draws: null argument");
+    OSC_REQUIRE(to >= from && from >= 0, "osc_level_draws: need 0 <= from <= to");
+    OSC_REQUIRE(prob->bc == OSC_BC_FLOWCELL || prob->bc == OSC_BC_DIRICHLET_ALL, "unknown bc");
+    OSC_REQUIRE(prob->qoi >= OSC_QOI_POINT && prob->qoi <= OSC_QOI_FLUX, "unknown qoi");
+    OSC_REQUIRE(!(prob->qoi == OSC_QOI_POINT && (prob->qoi_x < 0 || prob->qoi_x > 1 ||
+                                                 prob->qoi_y < 0 || prob->qoi_y > 1)),
+                "qoi_point: point outside [0,1]^2");
+    Ctx* c = L->ctx;
+    set_device(c);
+    const int64_t count = to - from;
+    if (count == 0) return;
+    const bool has_coarse = (flags & OSC_DRAW_HAS_COARSE) != 0;
+    OSC_REQUIRE(!has_coarse || (L->m % 2 == 0 && L->m >= 2),
+                "restrict: target grid is not a nested coarsening");
+    // coupled_sample: the smoothed operator is used only when it exists (estimators.cpp:211-223)
+    const double* sq_f = (flags & OSC_DRAW_TRUNC_FINE) && L->k_trunc > 0 ? L->sqrt_trunc.as<double>()
+                                                                         : L->sqrt_full.as<double>();
+    const double* sq_c = (flags & OSC_DRAW_TRUNC_COARSE) && L->k_trunc > 0 ? L->sqrt_trunc.as<double>()
+                                                                           : L->sqrt_full.as<double>();
+    const bool shared_field = sq_f == sq_c;
+    const int m = L->m, mc = m / 2;
+    const int64_t Nf = (int64_t)(m + 1) * (m + 1), Nc = (int64_t)(mc + 1) * (mc + 1);
+    const bool xi_host = xi != nullptr && !(flags & OSC_DRAW_XI_DEVICE);
+    // batch size from the memory budget
+    size_t per = sizeof(double) * (Nf + (has_coarse ? Nc : 0)) + ce_inter_bytes(L, 1, 1) +
+                 solver_bytes(m, 1, 0) + 64;
+    if (xi_host) per += sizeof(double) * L->s;
+    const size_t budget = budget_of(c);
+    int64_t Bmax = std::max<int64_t>(1, (int64_t)(budget / per));
+    Bmax = std::min<int64_t>(Bmax, 1 << 16);
+    const int64_t nchunks = (count + Bmax - 1) / Bmax;
+    const int Bc = (int)((count + nchunks - 1) / nchunks);
+    c->fields_fine.ensure(sizeof(double) * Nf * Bc);
+    if (has_coarse) c->fields_coarse.ensure(sizeof(double) * Nc * Bc);
+    c->out_q.ensure(sizeof(double) * 2 * Bc);
+    c->out_i.ensure(sizeof(int) * 2 * Bc);
+    c->sums.ensure(sizeof(double) * 8);
+    if (xi_host) c->xi_dev.ensure(sizeof(double) * L->s * Bc);
+    double* d_qf = c->out_q.as<double>();
+    double* d_qc = d_qf + Bc;
+    int* d_bad = c->out_i.as<int>();
+    double* d_sums = c->sums.as<double>();
+    if (level_sums) {
+      OSC_CUDA(cudaMemsetAsync(d_sums, 0, sizeof(double) * 8, c->stream));
+    }
+    bool any_bad = false, any_fail = false;
+    std::vector<int32_t> it_tmp(Bc), st_tmp(Bc), bad_tmp(Bc);
+    for (int64_t c0 = 0; c0 < count; c0 += Bc) {
+      const int B = (int)std::min<int64_t>(Bc, count - c0);
+      const double* xi_chunk = nullptr;
+      if (xi) {
+        if (xi_host) {
+          h2d(c, c->xi_dev.p, xi + c0 * L->s, sizeof(double) * L->s * B);
+          xi_chunk = c->xi_dev.as<double>();
+        } else {
+          xi_chunk = xi + c0 * L->s;
+        }
+      }
+      OSC_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int) * B, c->stream));
+      double* kf = c->fields_fine.as<double>();
+      double* kc = has_coarse ? c->fields_coarse.as<double>() : nullptr;
+      const uint64_t idx0 = (uint64_t)(from + c0);
+      if (shared_field || !has_coarse) {
+        ce_sample_launch(c, L, sq_f, xi_chunk, seed, ell, idx0, B, true, kf, kc, d_bad);
+      } else {
+        ce_sample_launch(c, L, sq_f, xi_chunk, seed, ell, idx0, B, true, kf, nullptr, d_bad);
+        ce_sample_launch(c, L, sq_c, xi_chunk, seed, ell, idx0, B, true, nullptr, kc, d_bad);
+      }
+      // fine solve + QoI
+      solver_prepare(c, m, B, 0);
+      c->solver.lev[0].k = kf;
+      solver_run(c, prob, B);
+      qoi_launch(c, prob, B, d_qf);
+      solver_results(c, B, it_tmp.data(), st_tmp.data(), nullptr);
+      d2h(c, bad_tmp.data(), d_bad, sizeof(int) * B);
+      OSC_CUDA(cudaStreamSynchronize(c->stream));
+      for (int b = 0; b < B; ++b) {
+        int s = bad_tmp[b] ? OSC_ERR_NUMERICAL : st_tmp[b];
+        any_bad |= bad_tmp[b] != 0;
+        any_fail |= st_tmp[b] != 0;
+        if (iters_fine) iters_fine[c0 + b] = it_tmp[b];
+        if (status) status[c0 + b] = s;
+      }
+      if (has_coarse) {
+        solver_prepare(c, mc, B, 0);
+        c->solver.lev[0].k = kc;
+        solver_run(c, prob, B);
+        qoi_launch(c, prob, B, d_qc);
+        solver_results(c, B, it_tmp.data(), st_tmp.data(), nullptr);
+        for (int b = 0; b < B; ++b) {
+          any_fail |= st_tmp[b] != 0;
+          if (iters_coarse) iters_coarse[c0 + b] = it_tmp[b];
+          if (status && status[c0 + b] == 0) status[c0 + b] = st_tmp[b];
+        }
+      }
+      if (level_sums)
+        level_sums_launch(c, d_qf, has_coarse ? d_qc : nullptr, B, level_sums[5], level_sums[6], d_sums);
+      if (q_fine) d2h(c, q_fine + c0, d_qf, sizeof(double) * B);
+      if (q_coarse) {
+        if (has_coarse) d2h(c, q_coarse + c0, d_qc, sizeof(double) * B);
+        else std::memset(q_coarse + c0, 0, sizeof(double) * B);
+      }
+    }
+    if (level_sums) d2h(c, level_sums, d_sums, sizeof(double) * 5);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+    if (any_bad) throw osc::Error(OSC_ERR_NUMERICAL, "assemble_and_solve: non-finite log-field value");
+    if (any_fail) throw osc::Error(OSC_ERR_SOLVER, "CG did not reach the relative residual within the iteration cap");
+  });
+}
+
+int osc_summarize(const double* qf, const double* qc, int64_t n, int has_coarse, double out[5]) {
+  // moments_of (estimators.cpp:82-101), slot order
+  double mean_y = 0.0, mean_q = 0.0, m2y = 0.0, m2q = 0.0;
+  int64_t cnt = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double y = has_coarse ? qf[i] - qc[i] : qf[i];
+    ++cnt;
+    double d = y - mean_y;
+    mean_y += d / cnt;
+    m2y += d * (y - mean_y);
+    d = qf[i] - mean_q;
+    mean_q += d / cnt;
+    m2q += d * (qf[i] - mean_q);
+  }
+  out[0] = (double)cnt;
+  out[1] = mean_y;
+  out[2] = cnt >= 2 ? m2y / (cnt - 1) : 0.0;
+  out[3] = mean_q;
+  out[4] = cnt >= 2 ? m2q / (cnt - 1) : 0.0;
+  return OSC_OK;
+}
+
+// ---- unfused stages ------------------------------------------------------------------------------
+int osc_normals(osc_ctx* c, uint64_t seed, uint32_t ell, uint64_t index0, int64_t count, int64_t s,
+                double* out) {
+  return guarded([&] {
+    set_device(c);
+    OSC_REQUIRE(count >= 0 && s >= 0, "osc_normals: negative size");
+    if (count == 0 || s == 0) return;
+    c->xi_dev.ensure(sizeof(double) * s * count);
+    normals_launch(c, seed, ell, index0, (int)count, s, c->xi_dev.as<double>());
+    d2h(c, out, c->xi_dev.p, sizeof(double) * s * count);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+  });
+}
+
+int osc_ce_sample(osc_level* L, const double* xi, uint64_t seed, uint32_t ell, uint64_t index0,
+                  int64_t count, int flags, double* fine_out, double* coarse_out) {
+  return guarded([&] {
+    Ctx* c = L->ctx;
+    set_device(c);
+    if (count <= 0) return;
+    const bool want_f = (flags & OSC_CE_FINE) != 0, want_c = (flags & OSC_CE_COARSE) != 0;
+    OSC_REQUIRE(want_f || want_c, "osc_ce_sample: request FINE and/or COARSE output");
+    OSC_REQUIRE(!want_c || L->m % 2 == 0, "restrict: target grid is not a nested coarsening");
+    OSC_REQUIRE(!(flags & OSC_CE_TRUNCATED) || L->k_trunc > 0, "osc_ce_sample: level has no truncated spectrum");
+    const double* sq = (flags & OSC_CE_TRUNCATED) ? L->sqrt_trunc.as<double>() : L->sqrt_full.as<double>();
+    const int m = L->m, mc = m / 2;
+    const int64_t Nf = (int64_t)(m + 1) * (m + 1), Nc = (int64_t)(mc + 1) * (mc + 1);
+    c->fields_fine.ensure(sizeof(double) * Nf * count);
+    if (want_c) c->fields_coarse.ensure(sizeof(double) * Nc * count);
+    c->out_i.ensure(sizeof(int) * count);
+    const double* xd = nullptr;
+    if (xi) {
+      c->xi_dev.ensure(sizeof(double) * L->s * count);
+      h2d(c, c->xi_dev.p, xi, sizeof(double) * L->s * count);
+      xd = c->xi_dev.as<double>();
+    }
+    OSC_CUDA(cudaMemsetAsync(c->out_i.p, 0, sizeof(int) * count, c->stream));
+    ce_sample_launch(c, L, sq, xd, seed, ell, index0, (int)count, (flags & OSC_CE_EXP) != 0,
+                     want_f ? c->fields_fine.as<double>() : nullptr,
+                     want_c ? c->fields_coarse.as<double>() : nullptr, c->out_i.as<int>());
+    if (want_f && fine_out) d2h(c, fine_out, c->fields_fine.p, sizeof(double) * Nf * count);
+    if (want_c && coarse_out) d2h(c, coarse_out, c->fields_coarse.p, sizeof(double) * Nc * count);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+  });
+}
+
+int osc_darcy_solve(osc_ctx* c, int m, int64_t count, const double* Z, const osc_problem* prob,
+                    double* u_out, int32_t* iters, int32_t* status, double* history, int hist_cap) {
+  return guarded([&] {
+    set_device(c);
+    OSC_REQUIRE(m >= 1, "assemble_and_solve: m >= 1 required");
+    OSC_REQUIRE(prob && Z, "osc_darcy_solve: null argument");
+    if (count <= 0) return;
+    const int64_t N = (int64_t)(m + 1) * (m + 1);
+    c->fields_fine.ensure(sizeof(double) * N * count);
+    c->xi_dev.ensure(sizeof(double) * N * count);
+    c->out_i.ensure(sizeof(int) * count);
+    h2d(c, c->xi_dev.p, Z, sizeof(double) * N * count);
+    OSC_CUDA(cudaMemsetAsync(c->out_i.p, 0, sizeof(int) * count, c->stream));
+    solver_prepare(c, m, (int)count, history ? hist_cap : 0);
+    exp_field_launch(c, c->xi_dev.as<double>(), c->fields_fine.as<double>(), N * count, c->out_i.as<int>());
+    std::vector<int> bad(count);
+    d2h(c, bad.data(), c->out_i.p, sizeof(int) * count);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    for (int64_t b = 0; b < count; ++b)
+      if (bad[b]) throw osc::Error(OSC_ERR_NUMERICAL, "assemble_and_solve: non-finite log-field value");
+    c->solver.lev[0].k = c->fields_fine.as<double>();
+    solver_run(c, prob, (int)count);
+    std::vector<int32_t> it(count), st(count);
+    solver_results(c, (int)count, it.data(), st.data(), history);
+    if (u_out) d2h(c, u_out, c->solver.u, sizeof(double) * N * count);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+    bool fail = false;
+    for (int64_t b = 0; b < count; ++b) {
+      if (iters) iters[b] = it[b];
+      if (status) status[b] = st[b];
+      fail |= st[b] != 0;
+    }
+    if (fail) throw osc::Error(OSC_ERR_SOLVER, "CG did not reach the relative residual within the iteration cap");
+  });
+}
+
+int osc_qoi(osc_ctx* c, int m, int64_t count, const double* u, const double* Z,
+            const osc_problem* prob, double* q_out) {
+  return guarded([&] {
+    set_device(c);
+    OSC_REQUIRE(prob && u && q_out, "osc_qoi: null argument");
+    OSC_REQUIRE(prob->qoi != OSC_QOI_FLUX || Z != nullptr, "osc_qoi: FLUX needs the log field Z");
+    if (count <= 0) return;
+    const int64_t N = (int64_t)(m + 1) * (m + 1);
+    solver_prepare(c, m, (int)count, 0);
+    c->fields_fine.ensure(sizeof(double) * N * count);
+    c->out_q.ensure(sizeof(double) * count);
+    c->out_i.ensure(sizeof(int) * count);
+    h2d(c, c->solver.u, u, sizeof(double) * N * count);
+    if (Z) {
+      c->xi_dev.ensure(sizeof(double) * N * count);
+      h2d(c, c->xi_dev.p, Z, sizeof(double) * N * count);
+      exp_field_launch(c, c->xi_dev.as<double>(), c->fields_fine.as<double>(), N * count, c->out_i.as<int>());
+    }
+    c->solver.lev[0].k = c->fields_fine.as<double>();
+    qoi_launch(c, prob, (int)count, c->out_q.as<double>());
+    d2h(c, q_out, c->out_q.p, sizeof(double) * count);
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+// K1 + K2: batched circulant-embedding sample with the coarse/fine restriction fused into
+// the epilogue. Replaces, per sample, NormalStream::fill (src/rng.cpp:65-67),
+// EmbeddingOperator::sample_into (src/embedding.cpp:165-174) with UnitaryDft::forward_real
+// (src/fft.cpp:48-56), restrict_to (src/embedding.cpp:183-203) and the exp() of
+// assemble_and_solve (src/fem.cpp:324-329).
+//
+// u = Re(F w) + Im(F w), w = √λ ⊙ ξ, F the unitary 2-D DFT with + sign (fft.hpp:11), only
+// the R-block p ∈ [0,m]² is ever read, so:
+//   pass 1 (rows, along x): two real rows q1 = 2r, 2r+1 are packed as one complex row
+//           z = w_a + i w_b, FFT'd in shared memory (Stockham radix-8), and unpacked into
+//           the half spectra X_a[p0], X_b[p0] for the needed p0 only (p0 ≤ m, stride cs);
+//   pass 2 (columns, along y): for each needed p0 the length-n column of X is FFT'd and only
+//           p1 ≤ m (stride cs) is kept; u = (Re+Im)/n, k = exp(u) written straight into the
+//           solver's fine and stride-2 coarse conductivity arrays.
+// The intermediate X is [sample][q1][p] complex (row-major: coalesced in both passes).
+#include <cuda_runtime.h>
+
+#include "osc_device.cuh"
+#include "osc_internal.cuh"
+
+namespace osc {
+
+namespace {
+
+// elements per thread for a length-n transform
+inline int elems_for(int n) { return n >= 8 ? 8 : n; }
+
+template <int E>
+__global__ void __launch_bounds__(512) ce_rows_kernel(
+    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed,
+    uint32_t ell, uint64_t index0, int n, int NT, int P, int cs, int B, int SB,
+    const double2* __restrict__ tw, double2* __restrict__ inter) {
+  extern __shared__ double2 smem[];
+  const int T = n / E;                      // threads per transform
+  const int t = threadIdx.x / T;            // transform slot in this CTA
+  const int lt = threadIdx.x - t * T;       // lane within the transform
+  const int rp = blockIdx.x * NT + t;       // row pair
+  const bool valid = rp < n / 2;
+  const int q1a = 2 * rp, q1b = 2 * rp + 1;
+  double2* x = smem + t * n;
+  const int64_t s = (int64_t)n * n;
+
+  // √λ for this thread's columns of both rows, reused across the sample loop.
+  constexpr int CP = E / 2;  // column pairs per thread
+  double2 la[CP], lb[CP];
+#pragma unroll
+  for (int g = 0; g < CP; ++g) {
+    const int c = lt + g * T;  // column pair: columns 2c, 2c+1
+    if (valid) {
+      la[g] = __ldg(reinterpret_cast<const double2*>(sqrt_lam + (int64_t)q1a * n) + c);
+      lb[g] = __ldg(reinterpret_cast<const double2*>(sqrt_lam + (int64_t)q1b * n) + c);
+    } else {
+      la[g] = lb[g] = make_double2(0.0, 0.0);
+    }
+  }
+
+  const int b0 = blockIdx.y * SB;
+  const int b1 = min(B, b0 + SB);
+  for (int b = b0; b < b1; ++b) {
+    if (valid) {
+#pragma unroll
+      for (int g = 0; g < CP; ++g) {
+        const int c = lt + g * T;
+        double2 xa, xb;
+        if (xi) {
+          const double* xr = xi + (int64_t)b * s;
+          xa = __ldg(reinterpret_cast<const double2*>(xr + (int64_t)q1a * n) + c);
+          xb = __ldg(reinterpret_cast<const double2*>(xr + (int64_t)q1b * n) + c);
+        } else {
+          const uint64_t idx = index0 + (uint64_t)b;
+          xa = normal_pair(seed, ell, idx, (uint32_t)((int64_t)q1a * (n / 2) + c));
+          xb = normal_pair(seed, ell, idx, (uint32_t)((int64_t)q1b * (n / 2) + c));
+        }
+        // z[q0] = w(q0, q1a) + i w(q0, q1b)
+        x[2 * c] = make_double2(la[g].x * xa.x, lb[g].x * xb.x);
+        x[2 * c + 1] = make_double2(la[g].y * xa.y, lb[g].y * xb.y);
+      }
+    }
+    __syncthreads();
+    fft_smem<E>(x, n, lt, tw);
+    if (valid) {
+      double2* outa = inter + ((int64_t)b * n + q1a) * P;
+      double2* outb = inter + ((int64_t)b * n + q1b) * P;
+      for (int p = lt; p < P; p += T) {
+        const int p0 = p * cs;
+        const double2 zp = x[p0];
+        const double2 zm = x[(n - p0) & (n - 1)];
+        // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
+        outa[p] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+        outb[p] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(512) ce_cols_kernel(
+    const double2* __restrict__ inter, int n, int m, int NT, int P, int cs, double inv_n,
+    int do_exp, const double2* __restrict__ tw, double* __restrict__ out_fine,
+    double* __restrict__ out_coarse, int* __restrict__ bad_flag) {
+  extern __shared__ double2 smem[];
+  const int T = n / E;
+  const int t = threadIdx.x / T;
+  const int lt = threadIdx.x - t * T;
+  const int b = blockIdx.y;
+  const int j0 = blockIdx.x * NT;
+  const int ld = n + 1;  // padded column stride (conflict-free transposed staging)
+  const double2* src = inter + (int64_t)b * n * P;
+
+  for (int idx = threadIdx.x; idx < NT * n; idx += blockDim.x) {
+    const int tt = idx % NT, q1 = idx / NT;
+    const int j = j0 + tt;
+    smem[tt * ld + q1] = (j < P) ? src[(int64_t)q1 * P + j] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_smem<E>(smem + t * ld, n, lt, tw);
+
+  // outputs: rows p1 = i*cs ≤ m, columns p0 = j*cs
+  const int n_rows = m / cs + 1;
+  const int mf = m + 1, mc = m / 2 + 1;
+  double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
+  double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
+  int bad = 0;
+  for (int idx = threadIdx.x; idx < NT * n_rows; idx += blockDim.x) {
+    const int tt = idx % NT, i = idx / NT;
+    const int j = j0 + tt;
+    if (j >= P) continue;
+    const int p1 = i * cs, p0 = j * cs;
+    const double2 v = smem[tt * ld + p1];
+    const double zval = (v.x + v.y) * inv_n;
+    if (!isfinite(zval)) bad = 1;
+    const double o = do_exp ? exp(zval) : zval;
+    if (of) of[(int64_t)p1 * mf + p0] = o;
+    if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
+  }
+  if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+}
+
+struct CeGeom {
+  int E, T, NT, threads;
+  size_t smem;
+};
+
+CeGeom rows_geom(int n) {
+  CeGeom g;
+  g.E = elems_for(n);
+  g.T = n / g.E;
+  g.NT = std::max(1, 256 / g.T);
+  g.NT = std::min(g.NT, std::max(1, n / 2));
+  g.threads = g.NT * g.T;
+  g.smem = sizeof(double2) * (size_t)g.NT * n;
+  return g;
+}
+
+CeGeom cols_geom(int n, int P) {
+  CeGeom g;
+  g.E = elems_for(n);
+  g.T = n / g.E;
+  int nt = std::max(1, 8192 / n);
+  nt = std::min(nt, std::max(1, 512 / g.T));
+  nt = std::min(nt, P);
+  g.NT = nt;
+  g.threads = g.NT * g.T;
+  g.smem = sizeof(double2) * (size_t)g.NT * (n + 1);
+  return g;
+}
+
+template <int E>
+void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
+                 uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
+                 double* out_fine, double* out_coarse, int* bad_flag, int cs, double2* inter) {
+  const int n = L->n, m = L->m;
+  const int P = m / cs + 1;
+  const double2* tw = L->twiddle.as<double2>();
+  cudaStream_t st = ctx->stream;
+  {
+    const CeGeom g = rows_geom(n);
+    const int row_groups = (n / 2 + g.NT - 1) / g.NT;
+    const int want = 2 * 148;
+    const int sample_groups = std::max(1, std::min(count, (want + row_groups - 1) / row_groups));
+    const int SB = (count + sample_groups - 1) / sample_groups;
+    const dim3 grid(row_groups, (count + SB - 1) / SB);
+    auto kern = ce_rows_kernel<E>;
+    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    KScope ks(ctx, "ce_rows");
+    kern<<<grid, g.threads, g.smem, st>>>(sqrt_lam, xi_dev, seed, ell, index0, n, g.NT, P, cs,
+                                         count, SB, tw, inter);
+    OSC_CUDA(cudaGetLastError());
+  }
+  {
+    const CeGeom g = cols_geom(n, P);
+    const dim3 grid((P + g.NT - 1) / g.NT, count);
+    auto kern = ce_cols_kernel<E>;
+    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    KScope ks(ctx, "ce_cols");
+    kern<<<grid, g.threads, g.smem, st>>>(inter, n, m, g.NT, P, cs, 1.0 / n, do_exp ? 1 : 0, tw,
+                                         out_fine, out_coarse, bad_flag);
+    OSC_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace
+
+size_t ce_inter_bytes(const Level* L, int count, int col_stride) {
+  const int P = L->m / col_stride + 1;
+  return sizeof(double2) * (size_t)count * L->n * P;
+}
+
+void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
+                      uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
+                      double* out_fine, double* out_coarse, int* bad_flag) {
+  OSC_REQUIRE((L->n & (L->n - 1)) == 0 && L->n >= 2,
+              "ce_sample: embedding size n = 2(m+J) must be a power of two on this build");
+  OSC_REQUIRE(L->n <= 8192, "ce_sample: embedding size n > 8192 is not supported");
+  if (count <= 0) return;
+  // Coarse-only pass (other spectrum on the finest CES level) computes even columns only.
+  const int cs = (out_fine == nullptr && out_coarse != nullptr) ? 2 : 1;
+  ctx->ce_inter.ensure(ce_inter_bytes(L, count, cs));
+  double2* inter = ctx->ce_inter.as<double2>();
+  switch (elems_for(L->n)) {
+    case 8: launch_pair<8>(ctx, L, sqrt_lam, xi_dev, seed, ell, index0, count, do_exp, out_fine, out_coarse, bad_flag, cs, inter); break;
+    case 4: launch_pair<4>(ctx, L, sqrt_lam, xi_dev, seed, ell, index0, count, do_exp, out_fine, out_coarse, bad_flag, cs, inter); break;
+    default: launch_pair<2>(ctx, L, sqrt_lam, xi_dev, seed, ell, index0, count, do_exp, out_fine, out_coarse, bad_flag, cs, inter); break;
+  }
+}
+
+// Standalone NormalStream fill on device (osc_normals): out[b*s + e] = ξ_e of index0+b.
+__global__ void normals_kernel(uint64_t seed, uint32_t ell, uint64_t index0, int64_t s,
+                               double* __restrict__ out) {
+  const int b = blockIdx.y;
+  const int64_t half = (s + 1) / 2;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < half;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = normal_pair(seed, ell, index0 + b, (uint32_t)j);
+    out[(int64_t)b * s + 2 * j] = v.x;
+    if (2 * j + 1 < s) out[(int64_t)b * s + 2 * j + 1] = v.y;
+  }
+}
+
+void normals_launch(Ctx* ctx, uint64_t seed, uint32_t ell, uint64_t index0, int count,
+                    int64_t s, double* out) {
+  const int64_t half = (s + 1) / 2;
+  const int blocks = (int)std::min<int64_t>((half + 255) / 256, 4096);
+  KScope ks(ctx, "normals");
+  normals_kernel<<<dim3(blocks, count), 256, 0, ctx->stream>>>(seed, ell, index0, s, out);
+  OSC_CUDA(cudaGetLastError());
+}
+
+}  // namespace osc

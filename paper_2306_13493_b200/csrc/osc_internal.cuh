@@ -1,0 +1,146 @@
+// Internal declarations shared by the sm_100a kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/oscfield_b200.h"
+
+namespace osc {
+
+// ---- errors -------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define OSC_CUDA(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      throw ::osc::Error(OSC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define OSC_REQUIRE(cond, msg) \
+  do {                         \
+    if (!(cond)) throw ::osc::Error(OSC_ERR_CONFIG, msg); \
+  } while (0)
+
+// ---- device buffer (grow-only) --------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    OSC_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- per-kernel-class profiling on the context stream -------------------------------------
+struct KernelStat {
+  std::string name;
+  int64_t launches = 0;
+  double total_ms = 0.0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+
+struct Ctx;
+// RAII scope: records start/stop events around the launches of one kernel class.
+struct KScope {
+  Ctx* ctx;
+  int cls;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  KScope(Ctx* c, const char* name, int n_launches = 1);
+  ~KScope();
+};
+
+// ---- solver workspace (one MG hierarchy for a batch of B samples) ----------------------------
+struct SolverLevel {
+  int m = 0;       // cells per side
+  int64_t N = 0;   // nodes (m+1)^2
+  double *k = nullptr, *D = nullptr, *E = nullptr, *Nw = nullptr;  // conductivity + stencil
+  double *r = nullptr, *z = nullptr;                                // MG residual / correction
+};
+
+struct SolverWork {
+  int m = 0;
+  int B = 0;
+  int nlev = 0;
+  int nc = 0;  // coarsest node count
+  SolverLevel lev[24];
+  double *u = nullptr, *p0 = nullptr, *p1 = nullptr, *Ap = nullptr;  // level-0 PCG vectors
+  double* chol = nullptr;   // B * nc * nc
+  double* scal = nullptr;   // per-sample scalars (see mgpcg.cu)
+  double* partial = nullptr;
+  unsigned* counter = nullptr;
+  int* flags = nullptr;     // per-sample: active, iters, status
+  int* n_active = nullptr;
+  double* hist = nullptr;   // B * hist_cap (optional)
+  int hist_cap = 0;
+  int max_parts = 0;
+  DevBuf mem;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  size_t mem_budget = 0;
+  bool profiling = false;
+  int64_t launches = 0;
+  std::string tag;  // appended to kernel-class names ("name@tag"), e.g. the solve grid m
+  std::vector<KernelStat> stats;
+  // reusable workspaces
+  DevBuf ce_inter, xi_dev, fields_fine, fields_coarse, out_q, out_i, tmp_host_stage, sums;
+  SolverWork solver;
+  int* h_pinned_int = nullptr;  // small pinned staging for n_active
+  int stat_class(const char* name);
+  void flush_stats();
+};
+
+struct Level {
+  Ctx* ctx = nullptr;
+  int m = 0, J = 0, n = 0;
+  int64_t s = 0, k_trunc = 0;
+  DevBuf sqrt_full, sqrt_trunc, twiddle;  // twiddle: n complex exp(+2πi t/n)
+};
+
+// ---- launchers --------------------------------------------------------------------------
+// CE sample (ce_sample.cu). Produces fields for samples [0, count) of a chunk:
+//  xi_dev != nullptr: ξ rows in device memory (count*s), else device Philox of indices
+//  index0 + b. out_fine/out_coarse (device, may be null) receive exp(Z) (if do_exp) or Z.
+//  col_stride 2 computes only the even columns/rows (coarse-only pass).
+void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
+                      uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
+                      double* out_fine, double* out_coarse, int* bad_flag);
+size_t ce_inter_bytes(const Level* L, int count, int col_stride);
+
+// Batched MG-PCG (mgpcg.cu). k (device, B*(m+1)^2) is consumed as level-0 conductivity.
+void solver_prepare(Ctx* ctx, int m, int B, int hist_cap);
+size_t solver_bytes(int m, int B, int hist_cap);
+void solver_run(Ctx* ctx, const osc_problem* prob, int B);
+// after solver_run: per-sample iters/status/u on device
+void qoi_launch(Ctx* ctx, const osc_problem* prob, int B, double* q_dev);
+void level_sums_launch(Ctx* ctx, const double* qf, const double* qc, int B, double shift_y,
+                       double shift_q, double* sums_dev);
+// per-sample iterations / status (and history) of the last solver_run, copied to host
+void solver_results(Ctx* ctx, int B, int32_t* iters, int32_t* status, double* hist_host);
+void exp_field_launch(Ctx* ctx, const double* Z, double* k, int64_t total, int* bad_flag);
+void normals_launch(Ctx* ctx, uint64_t seed, uint32_t ell, uint64_t index0, int count,
+                    int64_t s, double* out);
+
+}  // namespace osc

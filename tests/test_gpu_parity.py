@@ -1,0 +1,237 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference's golden vectors and
+the CPU oracle on identical seeded inputs.
+
+Tolerances (from BASELINE.json north_star): fields 1e-10 relative (max|ΔZ| / max|Z|);
+QoIs 1e-7 relative with both sides solved to relative residual 1e-10; RNG bit-exact in
+the Philox words, Box–Muller normals to 1e-14 relative (device log/sincos vs glibc).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-10
+QOI_TOL = 1e-7
+
+
+def relmax(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def qrel(a, b):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+# ---- RNG -----------------------------------------------------------------------------------
+def test_normals_match_reference(P, ctx, golden, port):
+    import ctypes as C
+    lib = P.lib()
+    out = np.empty(16)
+    assert lib.osc_normals(ctx.h, 1, 0, 0, 1, 16, out.ctypes.data_as(C.c_void_p)) == 0
+    assert relmax(out, golden["normals_1_0_0"]) < 1e-14
+    out2 = np.empty(16)
+    assert lib.osc_normals(ctx.h, 7, 3, (1 << 33) + 5, 1, 16, out2.ctypes.data_as(C.c_void_p)) == 0
+    assert relmax(out2, golden["normals_7_3_big"]) < 1e-14
+    # a long stream, several indices
+    big = np.empty((3, 1 << 16))
+    assert lib.osc_normals(ctx.h, 11, 2, 40, 3, 1 << 16, big.ctypes.data_as(C.c_void_p)) == 0
+    for i in range(3):
+        assert relmax(big[i], port.normals(11, 2, 40 + i, 1 << 16)) < 1e-14
+
+
+# ---- CE sampler (K1 + K2) ---------------------------------------------------------------------
+def test_ce_fields_golden(P, ctx, golden):
+    api = P.api
+    eig = golden["eig_matern_m16_nu15"]
+    op = api.EmbeddingOperator(api.GridSpec.square(16), int(golden["J_matern_m16_nu15"][0]), eig, 2.0)
+    fine, coarse = op.sample_fields(golden["ce_xi"], fine=True, coarse=True, ctx=ctx)
+    assert relmax(fine, golden["ce_fine"]) < FIELD_TOL
+    assert relmax(coarse, golden["ce_coarse"]) < FIELD_TOL
+    # smoothed field: same eigenvalues → same stable descending perm → same truncation mask
+    tr = op.truncated(op.s // 2)
+    fine_t = tr.sample_fields(golden["ce_xi"], fine=True, ctx=ctx)
+    assert relmax(fine_t, golden["ce_fine_trunc"]) < FIELD_TOL
+
+
+@pytest.mark.parametrize("m,model", [
+    (4, ("sep", 1.0, 0.3)), (8, ("matern", 1.0, 0.1, 0.5)), (64, ("matern", 1.0, 0.1, 0.5)),
+    (256, ("sep", 1.0, 0.01)), (1024, ("matern", 1.0, 0.01, 1.5)),
+])
+def test_ce_fields_vs_oracle(P, ctx, port, m, model):
+    api = P.api
+    cov = (api.CovarianceModel.separable_exponential(model[1], model[2]) if model[0] == "sep"
+           else api.CovarianceModel.matern(model[1], model[2], model[3]))
+    op = api.build_operator(api.GridSpec.square(m), cov)
+    if op.n & (op.n - 1):
+        pytest.skip("padded non-power-of-two embedding")
+    count = 2
+    # device Philox path (no host ξ) must reproduce NormalStream(seed, ell, i)
+    fine, coarse = op.sample_fields(None, count=count, seed=5, ell=2, index0=9, fine=True,
+                                    coarse=True, ctx=ctx)
+    sl = np.sqrt(np.maximum(op.eigenvalues, 0))
+    for b in range(count):
+        xi = port.normals(5, 2, 9 + b, op.s)
+        u = port.sample(op.n, sl, xi)
+        assert relmax(fine[b], port.restrict(op.n, m, u, m)) < FIELD_TOL
+        assert relmax(coarse[b], port.restrict(op.n, m, u, m // 2)) < FIELD_TOL
+
+
+def test_ce_linearity_large(P, ctx):
+    """Size-independent property at config-2 size (1024², n = 2048): the field is linear in ξ."""
+    api = P.api
+    op = api.build_operator(api.GridSpec.square(1024), api.CovarianceModel.matern(1.0, 0.01, 1.5))
+    rng = np.random.default_rng(3)
+    x1, x2 = rng.standard_normal(op.s), rng.standard_normal(op.s)
+    f = op.sample_fields(np.stack([x1, x2, 0.5 * x1 - 2.0 * x2]), fine=True, ctx=ctx)
+    assert relmax(f[2], 0.5 * f[0] - 2.0 * f[1]) < 1e-12
+    # ξ = 0 → u = 0 (SPEC sample example)
+    z = op.sample_fields(np.zeros((1, op.s)), fine=True, ctx=ctx)
+    assert np.all(z == 0.0)
+
+
+# ---- FEM (K3) -------------------------------------------------------------------------------------
+def test_solve_golden(P, ctx, golden):
+    api = P.api
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1, 1))
+    u, it, _ = api.assemble_and_solve(16, golden["ce_fine"], prob, ctx=ctx)
+    assert np.max(np.abs(u - golden["fem_u"])) < 1e-8
+    qp = api.evaluate_qoi(16, u, prob, ctx=ctx)
+    assert qrel(qp, golden["fem_qpoint"]) < QOI_TOL
+    prob.qoi = api.QoiSpec(api.QoiKind.L2Norm)
+    ql = api.evaluate_qoi(16, u, prob, ctx=ctx)
+    assert qrel(ql, golden["fem_ql2"]) < QOI_TOL
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("m", [4, 8, 32, 128, 512])
+def test_solve_vs_oracle(P, ctx, port, m, bc):
+    api = P.api
+    rng = np.random.default_rng(m + 17 * bc)
+    # a rough, high-contrast log field (σ ≈ 1.4) to stress the preconditioner
+    Z = np.cumsum(np.cumsum(rng.standard_normal((3, m + 1, m + 1)) * 0.2, axis=1), axis=2)
+    Z = (Z - Z.mean()) / Z.std() * 1.4
+    Z = Z.reshape(3, -1)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1, 1), bc=api.BC(bc))
+    u, it, _ = api.assemble_and_solve(m, Z, prob, ctx=ctx)
+    for kind in (0, 1, 2, 3):
+        prob.qoi = api.QoiSpec(api.QoiKind(kind))
+        q = api.evaluate_qoi(m, u, prob, Z=Z, ctx=ctx)
+        for b in range(3):
+            uo, ito, rc, _ = port.solve(m, Z[b], bc=bc)
+            assert rc == 0
+            qo = port.qoi(m, uo, bc=bc, qoi=kind, Z=Z[b])
+            assert abs(q[b] - qo) <= QOI_TOL * max(abs(qo), 1e-12), (kind, b, q[b], qo)
+
+
+def test_solve_analytic(P, ctx):
+    """SPEC fem examples: Z ≡ 0, f = 0 → u = 1 − x; point QoI 8/15; L2 1/√3; flux 1; ∫u = 1/2."""
+    api = P.api
+    m = 16
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1, 1), forcing=api.Forcing.Zero)
+    u, it, _ = api.assemble_and_solve(m, np.zeros((2, (m + 1) ** 2)) + np.array([[0.0], [2.5]]), prob,
+                                      ctx=ctx)
+    x = np.tile(np.arange(m + 1) / m, m + 1)
+    assert np.max(np.abs(u - (1 - x))) < 1e-10
+    expect = {0: 8 / 15, 1: 1 / np.sqrt(3), 2: 0.5, 3: 1.0}
+    for kind, val in expect.items():
+        prob.qoi = api.QoiSpec(api.QoiKind(kind))
+        q = api.evaluate_qoi(m, u, prob, Z=np.zeros_like(u), ctx=ctx)
+        assert abs(q[0] - val) < 1e-9, (kind, q[0], val)
+
+
+def test_solver_errors(P, ctx):
+    api = P.api
+    m = 32
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1, 1))
+    Z = np.zeros((2, (m + 1) ** 2))
+    Z[1, 5] = np.nan
+    with pytest.raises(api.NumericalError):
+        api.assemble_and_solve(m, Z, prob, ctx=ctx)
+    rng = np.random.default_rng(0)
+    Z = rng.standard_normal((2, (m + 1) ** 2))
+    with pytest.raises(api.SolverError) as ei:
+        api.assemble_and_solve(m, Z, prob, api.SolverOptions(tol=1e-30, max_iter_factor=0), ctx=ctx,
+                               hist_cap=8)
+    assert ei.value.residual_history is not None
+
+
+# ---- fused level draws -----------------------------------------------------------------------------
+def test_level_draws_golden(P, ctx, golden):
+    api = P.api
+    model = api.CovarianceModel.separable_exponential(1.0, 0.1)
+    prob = api.ProblemSpec(model)
+    opt = api.EstimatorOptions(seed=1)
+    plan = api.make_level_plan(1, 1.0 / 8, prob, opt)
+    d = api.LevelDraws()
+    api.run_level_draws(plan, api.GridSpec.square(8), False, False, prob, opt, 0, 6, d, ctx=ctx)
+    assert qrel(d.q_fine, golden["coupled_qf"]) < QOI_TOL
+    assert qrel(d.q_coarse, golden["coupled_qc"]) < QOI_TOL
+    # smoothed finest CES level: inject the reference eigenvalues (tie-group parity)
+    opt_s = api.EstimatorOptions(seed=1, smoothing=api.SmoothingRule.HalfSpectrum)
+    op = api.EmbeddingOperator(api.GridSpec.square(16), 0, golden["coupled_s_eig"], 1.0)
+    plan_s = api.make_level_plan(1, 1.0 / 8, prob, opt_s, operator=op)
+    assert plan_s.k_trunc == int(golden["coupled_s_k"][0])
+    d = api.LevelDraws()
+    api.run_level_draws(plan_s, api.GridSpec.square(8), False, True, prob, opt_s, 0, 6, d, ctx=ctx)
+    assert qrel(d.q_fine, golden["coupled_s_qf"]) < QOI_TOL
+    assert qrel(d.q_coarse, golden["coupled_s_qc"]) < QOI_TOL
+
+
+def test_mc_fixed_n_golden(P, ctx, golden):
+    api = P.api
+    prob = api.ProblemSpec(api.CovarianceModel.matern(1.0, 0.1, 0.5), api.QoiSpec(api.QoiKind.L2Norm))
+    rep = api.mc_estimate_fixed_n(prob, api.EstimatorOptions(seed=1), api.GridSpec.square(16), 64,
+                                  ctx=ctx)
+    mean, var = golden["mc16_mean_var"]
+    assert abs(rep.levels[0].mean_y - mean) < 1e-8 * abs(mean)
+    assert abs(rep.levels[0].var_y - var) < 1e-5 * abs(var)
+
+
+def test_slot_invariance(P, ctx):
+    """Sample i lands in slot i regardless of how [from, to) is split (estimators.hpp:112-114)."""
+    api = P.api
+    prob = api.ProblemSpec(api.CovarianceModel.matern(1.0, 0.1, 0.5))
+    opt = api.EstimatorOptions(seed=3)
+    plan = api.make_level_plan(2, 1.0 / 8, prob, opt)
+    a, b = api.LevelDraws(), api.LevelDraws()
+    cg = api.GridSpec.square(16)
+    api.run_level_draws(plan, cg, False, False, prob, opt, 0, 10, a, ctx=ctx)
+    api.run_level_draws(plan, cg, False, False, prob, opt, 0, 3, b, ctx=ctx)
+    api.run_level_draws(plan, cg, False, False, prob, opt, 3, 10, b, ctx=ctx)
+    assert np.array_equal(a.q_fine, b.q_fine) and np.array_equal(a.q_coarse, b.q_coarse)
+
+
+@pytest.mark.parametrize("bc,qoi", [(1, 2), (0, 3), (1, 0)])
+def test_level_draws_extensions_vs_port(P, ctx, port, bc, qoi):
+    """BC / QoI extensions (configs 1, 3, 4): GPU vs the oracle port on identical ξ."""
+    api = P.api
+    model = api.CovarianceModel.separable_exponential(1.0, 0.05)
+    prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind(qoi)), bc=api.BC(bc))
+    opt = api.EstimatorOptions(seed=2)
+    plan = api.make_level_plan(2, 1.0 / 8, prob, opt)
+    d = api.LevelDraws()
+    api.run_level_draws(plan, api.GridSpec.square(16), False, False, prob, opt, 5, 9, d, ctx=ctx)
+    sl = np.sqrt(np.maximum(plan.op.eigenvalues, 0))
+    qf, qc, itf, itc = port.coupled(32, plan.op.n, sl, None, True, 2, 2, 5, 9, bc=bc, qoi=qoi)
+    assert qrel(d.q_fine[5:9], qf) < QOI_TOL
+    assert qrel(d.q_coarse[5:9], qc) < QOI_TOL
+
+
+def test_mlmc_vs_reference(P, ctx, ref):
+    """MLMC mean and level variances agree with the reference within sampling CIs."""
+    from oracle import oracle as O
+    api = P.api
+    h0, eps = 1.0 / 8, 2e-3
+    opts = O.RefOpts.make(family=O.SEP_EXP, sigma2=1.0, lam=0.1, nu_or_p=1.0, seed=1, pilot_n=50,
+                          threads=8, l_max=3)
+    rr = ref.mlmc(opts, h0, eps, 2)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1.0, 0.1))
+    rep = api.mlmc_estimate(prob, api.EstimatorOptions(seed=1, pilot_n=50, l_max=3), h0, eps, 2, ctx=ctx)
+    se = np.hypot(rep.sampling_error, rr.sampling_error)
+    assert abs(rep.estimate - rr.estimate) < 4 * se
+    lv = rr.levels()
+    for a, b in zip(rep.levels, lv):
+        # same sample indices → near-identical moments, not just within CI
+        assert abs(a.mean_y - b["mean_y"]) < 4 * np.sqrt(b["var_y"] / max(b["n"], 2)) + 1e-12

@@ -288,6 +288,10 @@ __global__ void __launch_bounds__(NT) pcg_update_kernel(Geo g, double tol, const
     if (rel <= tol) {
       flags[b * F_NFLAGS + F_ACTIVE] = 0;
       atomicSub(n_active, 1);
+    } else if (!isfinite(rel)) {  // breakdown (non-finite residual): fail fast, never spin to the cap
+      flags[b * F_NFLAGS + F_ACTIVE] = 0;
+      flags[b * F_NFLAGS + F_STATUS] = OSC_ERR_SOLVER;
+      atomicSub(n_active, 1);
     } else if (it >= flags[b * F_NFLAGS + F_MAXIT]) {
       flags[b * F_NFLAGS + F_ACTIVE] = 0;
       flags[b * F_NFLAGS + F_STATUS] = OSC_ERR_SOLVER;

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -50,14 +51,15 @@ __device__ __forceinline__ bool is_dir(int bc, int m, int p0, int p1) {
 // Returns true in the last CTA; totals valid in thread 0 of that CTA.
 __device__ __forceinline__ bool reduce2_last(double v0, double v1, double2* partial, int maxp,
                                              unsigned* counter, int b, double& t0, double& t1) {
+  const int part = blockIdx.y * gridDim.x + blockIdx.x;
+  const int nparts = gridDim.x * gridDim.y;
   __shared__ double sh[32];
   __shared__ int last;
   const double s0 = block_sum(v0, sh);
   __syncthreads();
   const double s1 = block_sum(v1, sh);
-  const int nparts = gridDim.x;
   if (threadIdx.x == 0) {
-    partial[(int64_t)b * maxp + blockIdx.x] = make_double2(s0, s1);
+    partial[(int64_t)b * maxp + part] = make_double2(s0, s1);
     __threadfence();
     const unsigned prev = atomicAdd(counter + b, 1u);
     last = (prev == (unsigned)nparts - 1) ? 1 : 0;
@@ -79,53 +81,157 @@ __device__ __forceinline__ bool reduce2_last(double v0, double v1, double2* part
   return true;
 }
 
-// ---- setup: stencil from nodal k (+ injection to the next level) --------------------------
-__global__ void __launch_bounds__(NT) setup_level_kernel(Geo g, int bc, const double* __restrict__ k,
-                                                         double* __restrict__ D, double* __restrict__ E,
-                                                         double* __restrict__ Nw, double* __restrict__ kc) {
-  const int b = blockIdx.y;
-  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (i >= g.N) return;
-  const int m = g.m, n0 = g.n0;
-  const int p1 = (int)(i / n0), p0 = (int)(i - (int64_t)p1 * n0);
-  const double* kb = k + (int64_t)b * g.N;
-  auto K = [&](int a0, int a1) { return __ldg(kb + (int64_t)a1 * n0 + a0); };
-  auto klow = [&](int c0, int c1) { return (K(c0, c1) + K(c0 + 1, c1) + K(c0 + 1, c1 + 1)) / 3.0; };
-  auto kup = [&](int c0, int c1) { return (K(c0, c1) + K(c0 + 1, c1 + 1) + K(c0, c1 + 1)) / 3.0; };
-  // raw couplings of the 4 edges at this node
-  double e_east = 0.0, e_west = 0.0, e_north = 0.0, e_south = 0.0;
-  if (p0 < m) e_east = -0.5 * ((p1 < m ? klow(p0, p1) : 0.0) + (p1 > 0 ? kup(p0, p1 - 1) : 0.0));
-  if (p0 > 0) e_west = -0.5 * ((p1 < m ? klow(p0 - 1, p1) : 0.0) + (p1 > 0 ? kup(p0 - 1, p1 - 1) : 0.0));
-  if (p1 < m) e_north = -0.5 * ((p0 < m ? kup(p0, p1) : 0.0) + (p0 > 0 ? klow(p0 - 1, p1) : 0.0));
-  if (p1 > 0) e_south = -0.5 * ((p0 < m ? kup(p0, p1 - 1) : 0.0) + (p0 > 0 ? klow(p0 - 1, p1 - 1) : 0.0));
-  const bool dself = is_dir(bc, m, p0, p1);
-  const int64_t o = (int64_t)b * g.N + i;
-  D[o] = dself ? 1.0 : -(e_east + e_west + e_north + e_south);
-  E[o] = (p0 < m && !dself && !is_dir(bc, m, p0 + 1, p1)) ? e_east : 0.0;
-  Nw[o] = (p1 < m && !dself && !is_dir(bc, m, p0, p1 + 1)) ? e_north : 0.0;
-  if (kc && ((p0 | p1) & 1) == 0) {
-    const int mc = m / 2;
-    kc[(int64_t)b * (mc + 1) * (mc + 1) + (int64_t)(p1 >> 1) * (mc + 1) + (p0 >> 1)] = K(p0, p1);
+// ---- tiled, fused MG-PCG kernels -------------------------------------------------------------
+// Every kernel works on a TX×TY tile of one sample (blockIdx.z) with the fields it needs staged
+// in shared memory with a halo, and recomputes the 5-point stencil from the nodal k tile
+// (8 B/node of HBM instead of 24 B/node for stored D/E/N).
+constexpr int TX = 32, TY = 16;      // fine tile (threads: 32 × 8, two rows each)
+constexpr int CXT = 32, CYT = 8;     // coarse tile of the restriction (one node per thread)
+constexpr int TT = 256;              // threads per tiled CTA
+
+struct Sten {
+  double d, e, w, n, s;  // raw diagonal (1 on Dirichlet rows) and eliminated couplings
+};
+
+// Stencil at tile-local (lx, ly) of k tile `kt` (leading dim ld) for global node (gx, gy).
+// Bitwise identical to the per-node formulas in the header (same operands, same order),
+// so the coupling seen from both ends of an edge is the same double (A stays symmetric).
+__device__ __forceinline__ Sten stencil_at(const double* kt, int ld, int lx, int ly, int gx, int gy,
+                                           int m, int bc) {
+  auto K = [&](int dx, int dy) { return kt[(ly + dy) * ld + lx + dx]; };
+  const double k00 = K(0, 0);
+  double e = 0.0, w = 0.0, n = 0.0, s = 0.0;
+  if (gx < m) e = -0.5 * ((gy < m ? (k00 + K(1, 0) + K(1, 1)) / 3.0 : 0.0) +
+                          (gy > 0 ? (K(0, -1) + K(1, 0) + k00) / 3.0 : 0.0));
+  if (gx > 0) w = -0.5 * ((gy < m ? (K(-1, 0) + k00 + K(0, 1)) / 3.0 : 0.0) +
+                          (gy > 0 ? (K(-1, -1) + k00 + K(-1, 0)) / 3.0 : 0.0));
+  if (gy < m) n = -0.5 * ((gx < m ? (k00 + K(1, 1) + K(0, 1)) / 3.0 : 0.0) +
+                          (gx > 0 ? (K(-1, 0) + k00 + K(0, 1)) / 3.0 : 0.0));
+  if (gy > 0) s = -0.5 * ((gx < m ? (K(0, -1) + K(1, 0) + k00) / 3.0 : 0.0) +
+                          (gx > 0 ? (K(-1, -1) + K(0, -1) + k00) / 3.0 : 0.0));
+  Sten st;
+  if (is_dir(bc, m, gx, gy)) {
+    st.d = 1.0;
+    st.e = st.w = st.n = st.s = 0.0;
+    return st;
+  }
+  st.d = -(e + w + n + s);
+  st.e = is_dir(bc, m, gx + 1, gy) ? 0.0 : e;
+  st.w = is_dir(bc, m, gx - 1, gy) ? 0.0 : w;
+  st.n = is_dir(bc, m, gx, gy + 1) ? 0.0 : n;
+  st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : s;
+  return st;
+}
+
+// Stage rows [gy0, gy0+h) × cols [gx0, gx0+wd) of a sample's nodal field into smem with
+// cp.async (LDGSTS): every element's copy is in flight at once (no register round trip), and
+// out-of-grid elements are zero-filled (src-size 0). Caller: stage_wait() before use.
+__device__ __forceinline__ void stage(double* sm, int wd, int h, const double* __restrict__ g,
+                                      int gx0, int gy0, int n0) {
+  for (int idx = threadIdx.x; idx < wd * h; idx += TT) {
+    const int ly = idx / wd, lx = idx - ly * wd;
+    const int gx = gx0 + lx, gy = gy0 + ly;
+    const bool in = gx >= 0 && gx < n0 && gy >= 0 && gy < n0;
+    const double* src = in ? g + (int64_t)gy * n0 + gx : g;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sm + idx);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(in ? 8 : 0)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+}
+
+// Raw edge weights of a staged k region (origin (gx0, gy0), wd × h, zero-padded outside the
+// grid): es[y][x] couples (x,y)–(x+1,y), ns[y][x] couples (x,y)–(x,y+1). Triangle means use
+// the reference's vertex order with ·(1/3) instead of /3 (≤ 1 ulp per coefficient), and each
+// edge is formed once, so both rows of A see the same double (A stays symmetric).
+__device__ __forceinline__ void build_edges(const double* ks, double* es, double* ns, int wd, int h,
+                                            int gx0, int gy0, int m) {
+  constexpr double third = 1.0 / 3.0;
+  for (int idx = threadIdx.x; idx < wd * h; idx += TT) {
+    const int ly = idx / wd, lx = idx - ly * wd;
+    const int gx = gx0 + lx, gy = gy0 + ly;
+    double e = 0.0, n = 0.0;
+    if (lx + 1 < wd && ly > 0 && ly + 1 < h && gx >= 0 && gx < m && gy >= 0 && gy <= m) {
+      const double* k = ks + idx;
+      const double lo = gy < m ? (k[0] + k[1] + k[wd + 1]) * third : 0.0;       // K_low(x, y)
+      const double up = gy > 0 ? (k[-wd] + k[1] + k[0]) * third : 0.0;          // K_up(x, y-1)
+      e = -0.5 * (lo + up);
+    }
+    if (lx > 0 && lx + 1 < wd && ly + 1 < h && gy >= 0 && gy < m && gx >= 0 && gx <= m) {
+      const double* k = ks + idx;
+      const double up = gx < m ? (k[0] + k[wd + 1] + k[wd]) * third : 0.0;      // K_up(x, y)
+      const double lo = gx > 0 ? (k[-1] + k[0] + k[wd]) * third : 0.0;         // K_low(x-1, y)
+      n = -0.5 * (up + lo);
+    }
+    es[idx] = e;
+    ns[idx] = n;
   }
 }
 
+// 5-point row at local (lx, ly) of an edge region with leading dimension wd.
+__device__ __forceinline__ Sten sten_edges(const double* es, const double* ns, int wd, int lx, int ly,
+                                           int gx, int gy, int m, int bc) {
+  const int c = ly * wd + lx;
+  Sten st;
+  if (is_dir(bc, m, gx, gy)) {
+    st.d = 1.0;
+    st.e = st.w = st.n = st.s = 0.0;
+    return st;
+  }
+  const double e = es[c], w = es[c - 1], n = ns[c], s = ns[c - wd];
+  st.d = -(e + w + n + s);
+  st.e = is_dir(bc, m, gx + 1, gy) ? 0.0 : e;
+  st.w = is_dir(bc, m, gx - 1, gy) ? 0.0 : w;
+  st.n = is_dir(bc, m, gx, gy + 1) ? 0.0 : n;
+  st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : s;
+  return st;
+}
+
+#define TILE_PROLOGUE                                                \
+  const int b = blockIdx.z;                                          \
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                       \
+  const int m = g.m, n0 = g.n0;                                      \
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;              \
+  const int64_t off = (int64_t)b * g.N;                              \
+  const int tx = threadIdx.x & 31, ty0 = threadIdx.x >> 5;
+
+// ---- setup: k injection to the next level (fem.cpp:241-244) -----------------------------------------
+__global__ void __launch_bounds__(NT) inject_kernel(Geo gf, Geo gc, const double* __restrict__ kf,
+                                                    double* __restrict__ kc) {
+  const int b = blockIdx.y;
+  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (ic >= gc.N) return;
+  const int J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
+  kc[(int64_t)b * gc.N + ic] = kf[(int64_t)b * gf.N + (int64_t)(2 * J) * gf.n0 + 2 * I];
+}
+
 // Dense Cholesky of the coarsest operator, one thread per sample (fem.cpp:255-272).
-__global__ void coarse_factor_kernel(Geo g, int B, const double* __restrict__ D,
-                                     const double* __restrict__ E, const double* __restrict__ Nw,
+__global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restrict__ k,
                                      double* __restrict__ chol) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int n = (int)g.N, n0 = g.n0;
+  const int n = (int)g.N, n0 = g.n0, m = g.m;
   double* L = chol + (int64_t)b * n * n;
-  const double* Db = D + (int64_t)b * n;
-  const double* Eb = E + (int64_t)b * n;
-  const double* Nb = Nw + (int64_t)b * n;
+  const double* kb = k + (int64_t)b * n;
   for (int i = 0; i < n * n; ++i) L[i] = 0.0;
+  // stencil from a zero-padded 3×3 neighbourhood of k
   for (int i = 0; i < n; ++i) {
-    const int p1 = i / n0, p0 = i - p1 * n0;
-    L[i * n + i] = Db[i];
-    if (p0 + 1 < n0) { L[i * n + i + 1] = Eb[i]; L[(i + 1) * n + i] = Eb[i]; }
-    if (p1 + 1 < n0) { L[i * n + i + n0] = Nb[i]; L[(i + n0) * n + i] = Nb[i]; }
+    const int gy = i / n0, gx = i - gy * n0;
+    double kt[9];
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int x = gx + dx, y = gy + dy;
+        kt[(dy + 1) * 3 + dx + 1] = (x >= 0 && x < n0 && y >= 0 && y < n0) ? kb[y * n0 + x] : 0.0;
+      }
+    const Sten st = stencil_at(kt, 3, 1, 1, gx, gy, m, bc);
+    L[i * n + i] = st.d;
+    if (gx + 1 < n0) L[i * n + i + 1] = st.e;
+    if (gx > 0) L[i * n + i - 1] = st.w;
+    if (gy + 1 < n0) L[i * n + i + n0] = st.n;
+    if (gy > 0) L[i * n + i - n0] = st.s;
   }
   for (int j = 0; j < n; ++j) {
     double d = L[j * n + j];
@@ -140,33 +246,6 @@ __global__ void coarse_factor_kernel(Geo g, int B, const double* __restrict__ D,
   }
 }
 
-// ---- stencil helpers --------------------------------------------------------------------------
-struct St {
-  const double* __restrict__ D;
-  const double* __restrict__ E;
-  const double* __restrict__ Nw;
-};
-
-// Σ_nb A(i,nb) x(nb) (off-diagonal part) at node (p0,p1) of sample slice x.
-__device__ __forceinline__ double offdiag(const St& s, const double* __restrict__ x, int64_t i,
-                                          int p0, int p1, int m, int n0) {
-  double acc = 0.0;
-  if (p0 < m) acc += __ldg(s.E + i) * x[i + 1];
-  if (p0 > 0) acc += __ldg(s.E + i - 1) * x[i - 1];
-  if (p1 < m) acc += __ldg(s.Nw + i) * x[i + n0];
-  if (p1 > 0) acc += __ldg(s.Nw + i - n0) * x[i - n0];
-  return acc;
-}
-
-#define NODE_PROLOGUE                                                     \
-  const int b = blockIdx.y;                                               \
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                            \
-  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;               \
-  const int m = g.m, n0 = g.n0;                                           \
-  const int p1 = (int)(i / n0), p0 = (int)(i - (int64_t)p1 * n0);         \
-  const int64_t off = (int64_t)b * g.N;                                   \
-  const bool in = i < g.N;
-
 // ---- PCG init: u = lift, r = b − A u (= b on interior rows, 0 on Dirichlet rows) -------------
 __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing, double fval,
                                                       double tol, int max_iter_factor,
@@ -175,7 +254,7 @@ __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing
                                                       double* scal, int* flags, double2* partial,
                                                       int maxp, unsigned* counter, int* n_active,
                                                       double* hist, int hist_cap) {
-  const int b = blockIdx.y;
+  const int b = blockIdx.z;
   const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
   const int m = g.m, n0 = g.n0;
   const int p1 = (int)(i / n0), p0 = (int)(i - (int64_t)p1 * n0);
@@ -229,30 +308,39 @@ __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing
   }
 }
 
-// ---- PCG: p = z + βp (p = z first), Ap, <p,Ap> → α -----------------------------------------------
-__global__ void __launch_bounds__(NT) pcg_apply_kernel(Geo g, St s, const double* __restrict__ z,
+// ---- PCG: p = z + βp (p = z first), <p, A p> → α  (Ap itself is recomputed where needed) -----------
+__global__ void __launch_bounds__(TT) pcg_apply_kernel(Geo g, int bc, const double* __restrict__ k,
+                                                       const double* __restrict__ z,
                                                        const double* __restrict__ p_old,
-                                                       double* __restrict__ p_new,
-                                                       double* __restrict__ Ap, double* scal,
+                                                       double* __restrict__ p_new, double* scal,
                                                        int* flags, double2* partial, int maxp,
                                                        unsigned* counter) {
-  NODE_PROLOGUE
+  TILE_PROLOGUE
+  constexpr int W1 = TX + 2, H1 = TY + 2;
+  __shared__ double ks[H1 * W1], ps[H1 * W1], zs[H1 * W1], es[H1 * W1], ns[H1 * W1];
   const bool first = flags[b * F_NFLAGS + F_FIRST] != 0;
   const double beta = scal[b * S_NSCAL + S_BETA];
+  stage(ks, W1, H1, k + off, x0 - 1, y0 - 1, n0);
+  stage(zs, W1, H1, z + off, x0 - 1, y0 - 1, n0);
+  if (!first) stage(ps, W1, H1, p_old + off, x0 - 1, y0 - 1, n0);
+  stage_wait();
+  build_edges(ks, es, ns, W1, H1, x0 - 1, y0 - 1, m);
+  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT)
+    ps[idx] = first ? zs[idx] : fma(beta, ps[idx], zs[idx]);
+  __syncthreads();
   double pap = 0.0;
-  if (in) {
-    const double* zb = z + off;
-    const double* pb = p_old + off;
-    auto P = [&](int64_t j) { return first ? zb[j] : fma(beta, pb[j], zb[j]); };
-    const double pc = P(i);
-    double acc = __ldg(s.D + off + i) * pc;
-    if (p0 < m) acc += __ldg(s.E + off + i) * P(i + 1);
-    if (p0 > 0) acc += __ldg(s.E + off + i - 1) * P(i - 1);
-    if (p1 < m) acc += __ldg(s.Nw + off + i) * P(i + n0);
-    if (p1 > 0) acc += __ldg(s.Nw + off + i - n0) * P(i - n0);
-    p_new[off + i] = pc;
-    Ap[off + i] = acc;
-    pap = pc * acc;
+#pragma unroll
+  for (int r = 0; r < TY / 8; ++r) {
+    const int ly = ty0 + 8 * r, gx = x0 + tx, gy = y0 + ly;
+    if (gx < n0 && gy < n0) {
+      const int c = (ly + 1) * W1 + tx + 1;
+      const Sten st = sten_edges(es, ns, W1, tx + 1, ly + 1, gx, gy, m, bc);
+      const double pc = ps[c];
+      const double ap = st.d * pc + st.e * ps[c + 1] + st.w * ps[c - 1] + st.n * ps[c + W1] +
+                        st.s * ps[c - W1];
+      p_new[off + (int64_t)gy * n0 + gx] = pc;
+      pap = fma(pc, ap, pap);
+    }
   }
   double t0, t1;
   if (reduce2_last(pap, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -261,22 +349,63 @@ __global__ void __launch_bounds__(NT) pcg_apply_kernel(Geo g, St s, const double
   }
 }
 
-// ---- PCG: u += αp, r −= αAp, ‖r‖ → convergence ----------------------------------------------------
-__global__ void __launch_bounds__(NT) pcg_update_kernel(Geo g, double tol, const double* __restrict__ p,
-                                                        const double* __restrict__ Ap,
-                                                        double* __restrict__ u, double* __restrict__ r,
-                                                        double* scal, int* flags, double2* partial,
-                                                        int maxp, unsigned* counter, int* n_active,
-                                                        double* hist, int hist_cap) {
-  NODE_PROLOGUE
-  (void)p0; (void)p1; (void)m; (void)n0;
+// ---- PCG update fused with the level-0 pre-smoother:
+//   u += αp, r −= αAp (Ap recomputed from p), ‖r‖ → convergence,
+//   then z_red = r/D, z_black = (r − Σ A z_red)/D  (red-black GS from z = 0)
+__global__ void __launch_bounds__(TT) pcg_update_down_kernel(
+    Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
+    double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
+    double* __restrict__ z, double* scal, int* flags,
+    double2* partial, int maxp, unsigned* counter, int* n_active, double* hist, int hist_cap) {
+  TILE_PROLOGUE
+  constexpr int W2 = TX + 4, H2 = TY + 4, W1 = TX + 2, H1 = TY + 2;
+  __shared__ double ks[H2 * W2], ps[H2 * W2], rs[H1 * W1], zr[H1 * W1], es[H2 * W2], ns[H2 * W2],
+      us[TX * TY];
   const double alpha = scal[b * S_NSCAL + S_ALPHA];
+  stage(ks, W2, H2, k + off, x0 - 2, y0 - 2, n0);
+  stage(ps, W2, H2, p + off, x0 - 2, y0 - 2, n0);
+  stage(rs, W1, H1, r + off, x0 - 1, y0 - 1, n0);
+  stage(us, TX, TY, u + off, x0, y0, n0);
+  stage_wait();
+  build_edges(ks, es, ns, W2, H2, x0 - 2, y0 - 2, m);
+  __syncthreads();
+  // r_new and z_red = r_new / D on the tile + 1 halo (in place in rs)
+  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT) {
+    const int ly = idx / W1, lx = idx - ly * W1;
+    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    double rn = 0.0, zv = 0.0;
+    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0) {
+      const int c = (ly + 1) * W2 + lx + 1;
+      const Sten st = sten_edges(es, ns, W2, lx + 1, ly + 1, gx, gy, m, bc);
+      const double ap = st.d * ps[c] + st.e * ps[c + 1] + st.w * ps[c - 1] + st.n * ps[c + W2] +
+                        st.s * ps[c - W2];
+      rn = fma(-alpha, ap, rs[idx]);
+      if (((gx + gy) & 1) == 0) zv = rn / st.d;
+    }
+    rs[idx] = rn;
+    zr[idx] = zv;
+  }
+  __syncthreads();
   double rr = 0.0;
-  if (in) {
-    u[off + i] = fma(alpha, p[off + i], u[off + i]);
-    const double rn = fma(-alpha, Ap[off + i], r[off + i]);
-    r[off + i] = rn;
-    rr = rn * rn;
+#pragma unroll
+  for (int q = 0; q < TY / 8; ++q) {
+    const int ly = ty0 + 8 * q, gx = x0 + tx, gy = y0 + ly;
+    if (gx < n0 && gy < n0) {
+      const int c1 = (ly + 1) * W1 + tx + 1;
+      const int64_t j = off + (int64_t)gy * n0 + gx;
+      const double rn = rs[c1];
+      double zv;
+      if (((gx + gy) & 1) == 0) {
+        zv = zr[c1];
+      } else {
+        const Sten st = sten_edges(es, ns, W2, tx + 2, ly + 2, gx, gy, m, bc);
+        zv = (rn - (st.e * zr[c1 + 1] + st.w * zr[c1 - 1] + st.n * zr[c1 + W1] + st.s * zr[c1 - W1])) / st.d;
+      }
+      u[j] = fma(alpha, ps[(ly + 2) * W2 + tx + 2], us[ly * TX + tx]);
+      r_out[j] = rn;
+      z[j] = zv;
+      rr = fma(rn, rn, rr);
+    }
   }
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -300,120 +429,145 @@ __global__ void __launch_bounds__(NT) pcg_update_kernel(Geo g, double tol, const
   }
 }
 
-// ---- V-cycle pieces ----------------------------------------------------------------------------------
-// pre-smooth from z = 0: red z = r/D, then black z = (r − Σ A z_red)/D
-__global__ void __launch_bounds__(NT) smooth_down_kernel(Geo g, St s, const double* __restrict__ r,
+// ---- pre-smoother on coarse levels (and on level 0 for the first V-cycle): red then black -----------
+__global__ void __launch_bounds__(TT) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
+                                                         const double* __restrict__ r,
                                                          double* __restrict__ z, const int* flags) {
-  NODE_PROLOGUE
-  if (!in) return;
-  const St sb{s.D + off, s.E + off, s.Nw + off};
-  const double* rb = r + off;
-  double val;
-  if (((p0 + p1) & 1) == 0) {
-    val = rb[i] / __ldg(sb.D + i);
-  } else {
-    double acc = 0.0;
-    if (p0 < m) acc += __ldg(sb.E + i) * (rb[i + 1] / __ldg(sb.D + i + 1));
-    if (p0 > 0) acc += __ldg(sb.E + i - 1) * (rb[i - 1] / __ldg(sb.D + i - 1));
-    if (p1 < m) acc += __ldg(sb.Nw + i) * (rb[i + n0] / __ldg(sb.D + i + n0));
-    if (p1 > 0) acc += __ldg(sb.Nw + i - n0) * (rb[i - n0] / __ldg(sb.D + i - n0));
-    val = (rb[i] - acc) / __ldg(sb.D + i);
+  TILE_PROLOGUE
+  constexpr int W2 = TX + 4, H2 = TY + 4, W1 = TX + 2, H1 = TY + 2;
+  __shared__ double ks[H2 * W2], rs[H1 * W1], zr[H1 * W1], es[H2 * W2], ns[H2 * W2];
+  stage(ks, W2, H2, k + off, x0 - 2, y0 - 2, n0);
+  stage(rs, W1, H1, r + off, x0 - 1, y0 - 1, n0);
+  stage_wait();
+  build_edges(ks, es, ns, W2, H2, x0 - 2, y0 - 2, m);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT) {
+    const int ly = idx / W1, lx = idx - ly * W1;
+    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    double zv = 0.0;
+    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0 && ((gx + gy) & 1) == 0) {
+      const Sten st = sten_edges(es, ns, W2, lx + 1, ly + 1, gx, gy, m, bc);
+      zv = rs[idx] / st.d;
+    }
+    zr[idx] = zv;
   }
-  z[off + i] = val;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < TY / 8; ++q) {
+    const int ly = ty0 + 8 * q, gx = x0 + tx, gy = y0 + ly;
+    if (gx < n0 && gy < n0) {
+      const int c1 = (ly + 1) * W1 + tx + 1;
+      double zv;
+      if (((gx + gy) & 1) == 0) {
+        zv = zr[c1];
+      } else {
+        const Sten st = sten_edges(es, ns, W2, tx + 2, ly + 2, gx, gy, m, bc);
+        zv = (rs[c1] - (st.e * zr[c1 + 1] + st.w * zr[c1 - 1] + st.n * zr[c1 + W1] + st.s * zr[c1 - W1])) / st.d;
+      }
+      z[off + (int64_t)gy * n0 + gx] = zv;
+    }
+  }
 }
 
-// residual t = r − A z at fine node (a0,a1)
-__device__ __forceinline__ double resid_at(const St& sb, const double* __restrict__ rb,
-                                           const double* __restrict__ zb, int a0, int a1, int m,
-                                           int n0) {
-  const int64_t j = (int64_t)a1 * n0 + a0;
-  return rb[j] - __ldg(sb.D + j) * zb[j] - offdiag(sb, zb, j, a0, a1, m, n0);
-}
-
-// coarse residual rc = Pᵀ (r − A z), zero at coarse Dirichlet nodes (fem.cpp:168-195)
-__global__ void __launch_bounds__(NT) restrict_kernel(Geo g, Geo gc, int bc, St s,
-                                                      const double* __restrict__ r,
+// ---- residual restriction rc = Pᵀ(r − A z) after the red-black pre-smoother (fem.cpp:168-195).
+// After the black sweep the residual vanishes on black nodes and equals −Σ A z_black on red
+// nodes, so rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]; zero at coarse Dirichlet nodes.
+__global__ void __launch_bounds__(TT) restrict_kernel(Geo g, Geo gc, int bc,
+                                                      const double* __restrict__ k,
                                                       const double* __restrict__ z,
                                                       double* __restrict__ rc, const int* flags) {
-  const int b = blockIdx.y;
+  const int b = blockIdx.z;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (ic >= gc.N) return;
-  const int mc = gc.m;
-  const int J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
+  const int m = g.m, n0 = g.n0, mc = gc.m;
+  const int I0 = blockIdx.x * CXT, J0 = blockIdx.y * CYT;
+  constexpr int WR = 2 * CXT + 3, HR = 2 * CYT + 3;
+  __shared__ double ks[HR * WR], zs[HR * WR], es[HR * WR], ns[HR * WR];
+  const int64_t off = (int64_t)b * g.N;
+  const int fx0 = 2 * I0 - 2, fy0 = 2 * J0 - 2;
+  stage(ks, WR, HR, k + off, fx0, fy0, n0);
+  stage(zs, WR, HR, z + off, fx0, fy0, n0);
+  stage_wait();
+  build_edges(ks, es, ns, WR, HR, fx0, fy0, m);
+  __syncthreads();
+  const int I = I0 + (threadIdx.x & 31), J = J0 + (threadIdx.x >> 5);
+  if (I > mc || J > mc) return;
   double acc = 0.0;
   if (!is_dir(bc, mc, I, J)) {
-    const int64_t off = (int64_t)b * g.N;
-    const St sb{s.D + off, s.E + off, s.Nw + off};
-    const double* rb = r + off;
-    const double* zb = z + off;
-    const int m = g.m, n0 = g.n0;
-    const int f0 = 2 * I, f1 = 2 * J;
-    acc = resid_at(sb, rb, zb, f0, f1, m, n0);
-    double half = 0.0;
-    if (f0 > 0) half += resid_at(sb, rb, zb, f0 - 1, f1, m, n0);
-    if (f0 < m) half += resid_at(sb, rb, zb, f0 + 1, f1, m, n0);
-    if (f1 > 0) half += resid_at(sb, rb, zb, f0, f1 - 1, m, n0);
-    if (f1 < m) half += resid_at(sb, rb, zb, f0, f1 + 1, m, n0);
-    if (f0 < m && f1 < m) half += resid_at(sb, rb, zb, f0 + 1, f1 + 1, m, n0);
-    if (f0 > 0 && f1 > 0) half += resid_at(sb, rb, zb, f0 - 1, f1 - 1, m, n0);
-    acc += 0.5 * half;
+    auto t_at = [&](int fx, int fy) {  // residual at a red fine node
+      if (fx < 0 || fx > m || fy < 0 || fy > m) return 0.0;
+      const int lx = fx - fx0, ly = fy - fy0;
+      const Sten st = sten_edges(es, ns, WR, lx, ly, fx, fy, m, bc);
+      const int c = ly * WR + lx;
+      return -(st.e * zs[c + 1] + st.w * zs[c - 1] + st.n * zs[c + WR] + st.s * zs[c - WR]);
+    };
+    acc = t_at(2 * I, 2 * J) + 0.5 * (t_at(2 * I + 1, 2 * J + 1) + t_at(2 * I - 1, 2 * J - 1));
   }
-  rc[(int64_t)b * gc.N + ic] = acc;
+  rc[(int64_t)b * gc.N + (int64_t)J * gc.n0 + I] = acc;
 }
 
-// P1 prolongation of the coarse correction at fine node (a0,a1) (fem.cpp:144-165)
-__device__ __forceinline__ double prolong_at(const double* __restrict__ zc, int a0, int a1,
-                                             int nc0) {
-  const bool ex = (a0 & 1) == 0, ey = (a1 & 1) == 0;
-  auto Z = [&](int c0, int c1) { return zc[(int64_t)c1 * nc0 + c0]; };
-  if (ex && ey) return Z(a0 >> 1, a1 >> 1);
-  if (!ex && ey) return 0.5 * (Z((a0 - 1) >> 1, a1 >> 1) + Z((a0 + 1) >> 1, a1 >> 1));
-  if (ex && !ey) return 0.5 * (Z(a0 >> 1, (a1 - 1) >> 1) + Z(a0 >> 1, (a1 + 1) >> 1));
-  return 0.5 * (Z((a0 - 1) >> 1, (a1 - 1) >> 1) + Z((a0 + 1) >> 1, (a1 + 1) >> 1));
-}
-
-// post-smooth part 1: black z = (r − Σ A (z_red + P zc)_nb)/D ; red untouched
-__global__ void __launch_bounds__(NT) smooth_up_black_kernel(Geo g, Geo gc, St s,
-                                                             const double* __restrict__ r,
-                                                             double* __restrict__ z,
-                                                             const double* __restrict__ zc,
-                                                             const int* flags) {
-  NODE_PROLOGUE
-  if (!in || ((p0 + p1) & 1) == 0) return;
-  const St sb{s.D + off, s.E + off, s.Nw + off};
-  const double* zb = z + off;
-  const double* zcb = zc + (int64_t)b * gc.N;
-  const int nc0 = gc.n0;
-  auto V = [&](int64_t j, int a0, int a1) { return zb[j] + prolong_at(zcb, a0, a1, nc0); };
-  double acc = 0.0;
-  if (p0 < m) acc += __ldg(sb.E + i) * V(i + 1, p0 + 1, p1);
-  if (p0 > 0) acc += __ldg(sb.E + i - 1) * V(i - 1, p0 - 1, p1);
-  if (p1 < m) acc += __ldg(sb.Nw + i) * V(i + n0, p0, p1 + 1);
-  if (p1 > 0) acc += __ldg(sb.Nw + i - n0) * V(i - n0, p0, p1 - 1);
-  z[off + i] = (r[off + i] - acc) / __ldg(sb.D + i);
-}
-
-// post-smooth part 2: red z = (r − Σ A z_black)/D; on level 0 also <r,z> → β
-__global__ void __launch_bounds__(NT) smooth_up_red_kernel(Geo g, St s, const double* __restrict__ r,
-                                                           double* __restrict__ z, int finest,
-                                                           double* scal, int* flags,
-                                                           double2* partial, int maxp,
-                                                           unsigned* counter) {
-  NODE_PROLOGUE
-  double rz = 0.0;
-  if (in) {
-    const St sb{s.D + off, s.E + off, s.Nw + off};
-    const double* zb = z + off;
-    const double ri = r[off + i];
-    double zi;
-    if (((p0 + p1) & 1) == 0) {
-      zi = (ri - offdiag(sb, zb, i, p0, p1, m, n0)) / __ldg(sb.D + i);
-      z[off + i] = zi;
-    } else {
-      zi = zb[i];
+// ---- prolongation + post-smoother (black then red), on level 0 also <r, z> → β ------------------------
+__global__ void __launch_bounds__(TT) smooth_up_kernel(Geo g, Geo gc, int bc,
+                                                       const double* __restrict__ k,
+                                                       const double* __restrict__ r,
+                                                       const double* __restrict__ z,
+                                                       double* __restrict__ z_out,
+                                                       const double* __restrict__ zc, int finest,
+                                                       double* scal, int* flags, double2* partial,
+                                                       int maxp, unsigned* counter) {
+  TILE_PROLOGUE
+  constexpr int W2 = TX + 4, H2 = TY + 4, W1 = TX + 2, H1 = TY + 2;
+  constexpr int WC = TX / 2 + 3, HC = TY / 2 + 3;
+  __shared__ double ks[H2 * W2], zp[H2 * W2], rs[H1 * W1], zb[H1 * W1], zcs[HC * WC], es[H2 * W2],
+      ns[H2 * W2];
+  const int cx0 = x0 / 2 - 1, cy0 = y0 / 2 - 1;
+  stage(ks, W2, H2, k + off, x0 - 2, y0 - 2, n0);
+  stage(zp, W2, H2, z + off, x0 - 2, y0 - 2, n0);
+  stage(rs, W1, H1, r + off, x0 - 1, y0 - 1, n0);
+  stage(zcs, WC, HC, zc + (int64_t)b * gc.N, cx0, cy0, gc.n0);
+  stage_wait();
+  build_edges(ks, es, ns, W2, H2, x0 - 2, y0 - 2, m);
+  // red nodes of the 2-halo region after prolongation: z_red + P zc (black entries unused)
+  for (int idx = threadIdx.x; idx < W2 * H2; idx += TT) {
+    const int ly = idx / W2, lx = idx - ly * W2;
+    const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
+    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0 && ((gx + gy) & 1) == 0) {
+      auto Zc = [&](int I, int J) { return zcs[(J - cy0) * WC + (I - cx0)]; };
+      double pz;
+      if ((gx & 1) == 0) pz = Zc(gx >> 1, gy >> 1);                                   // even-even
+      else pz = 0.5 * (Zc((gx - 1) >> 1, (gy - 1) >> 1) + Zc((gx + 1) >> 1, (gy + 1) >> 1));  // odd-odd
+      zp[idx] += pz;
     }
-    rz = ri * zi;
+  }
+  __syncthreads();
+  // black nodes of the 1-halo region: z_b = (r − Σ A z_red)/D
+  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT) {
+    const int ly = idx / W1, lx = idx - ly * W1;
+    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+    double v = 0.0;
+    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0 && ((gx + gy) & 1) == 1) {
+      const Sten st = sten_edges(es, ns, W2, lx + 1, ly + 1, gx, gy, m, bc);
+      const int c = (ly + 1) * W2 + lx + 1;
+      v = (rs[idx] - (st.e * zp[c + 1] + st.w * zp[c - 1] + st.n * zp[c + W2] + st.s * zp[c - W2])) / st.d;
+    }
+    zb[idx] = v;
+  }
+  __syncthreads();
+  double rz = 0.0;
+#pragma unroll
+  for (int q = 0; q < TY / 8; ++q) {
+    const int ly = ty0 + 8 * q, gx = x0 + tx, gy = y0 + ly;
+    if (gx < n0 && gy < n0) {
+      const int c1 = (ly + 1) * W1 + tx + 1;
+      double zv;
+      if (((gx + gy) & 1) == 0) {
+        const Sten st = sten_edges(es, ns, W2, tx + 2, ly + 2, gx, gy, m, bc);
+        zv = (rs[c1] - (st.e * zb[c1 + 1] + st.w * zb[c1 - 1] + st.n * zb[c1 + W1] + st.s * zb[c1 - W1])) / st.d;
+      } else {
+        zv = zb[c1];
+      }
+      z_out[off + (int64_t)gy * n0 + gx] = zv;
+      rz = fma(rs[c1], zv, rz);
+    }
   }
   if (!finest) return;
   double t0, t1;
@@ -424,14 +578,24 @@ __global__ void __launch_bounds__(NT) smooth_up_red_kernel(Geo g, St s, const do
   }
 }
 
+__global__ void mark_active_failed_kernel(int B, int* flags) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B && flags[b * F_NFLAGS + F_ACTIVE]) {
+    flags[b * F_NFLAGS + F_ACTIVE] = 0;
+    flags[b * F_NFLAGS + F_STATUS] = OSC_ERR_SOLVER;
+  }
+}
+
 // single-level case (no coarser grid): <r,z> → β
 __global__ void __launch_bounds__(NT) dot_rz_kernel(Geo g, const double* __restrict__ r,
                                                     const double* __restrict__ z, double* scal,
                                                     int* flags, double2* partial, int maxp,
                                                     unsigned* counter) {
-  NODE_PROLOGUE
-  (void)p0; (void)p1; (void)m; (void)n0;
-  const double rz = in ? r[off + i] * z[off + i] : 0.0;
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
+  const int64_t off = (int64_t)b * g.N;
+  const double rz = i < g.N ? r[off + i] * z[off + i] : 0.0;
   double t0, t1;
   if (reduce2_last(rz, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     const double old = scal[b * S_NSCAL + S_RZ];
@@ -467,7 +631,7 @@ __global__ void __launch_bounds__(NT) qoi_kernel(Geo g, int qoi, double qx, doub
                                                  const double* __restrict__ k,
                                                  double* __restrict__ q, double2* partial, int maxp,
                                                  unsigned* counter) {
-  const int b = blockIdx.y;
+  const int b = blockIdx.z;
   const int m = g.m, n0 = g.n0;
   const double* ub = u + (int64_t)b * g.N;
   if (qoi == OSC_QOI_POINT) {
@@ -555,6 +719,9 @@ __global__ void level_sums_kernel(const double* __restrict__ qf, const double* _
 }
 
 inline int nblocks(int64_t N) { return (int)((N + NT - 1) / NT); }
+inline int64_t tile_parts(int m) {
+  return (int64_t)((m + 1 + TX - 1) / TX) * ((m + 1 + TY - 1) / TY);
+}
 
 }  // namespace
 
@@ -563,23 +730,23 @@ size_t solver_bytes(int m, int B, int hist_cap) {
   int g = m, lev = 0;
   for (;;) {
     const size_t N = (size_t)(g + 1) * (g + 1);
-    tot += N * B * sizeof(double) * (lev == 0 ? 10 : 6);
+    tot += N * B * sizeof(double) * (lev == 0 ? 8 : 4);  // level 0: u r r2 z z2 p0 p1 (+k by caller); else k r z z2
     ++lev;
     if (g <= 4 || g % 2 != 0) { tot += N * N * B * sizeof(double); break; }
     g /= 2;
   }
   tot += (size_t)B * (S_NSCAL * 8 + F_NFLAGS * 4 + 8) + (size_t)B * hist_cap * 8;
-  tot += (size_t)B * ((size_t)(m + 1) * (m + 1) / NT + 2) * 16;
-  return tot + 4096 * 16;
+  tot += (size_t)B * (tile_parts(m) + (size_t)(m + 1) * (m + 1) / NT + 2) * 16;
+  return tot + 8192 * 16;
 }
 
 void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   SolverWork& w = ctx->solver;
   OSC_REQUIRE(m >= 1, "solve: m must be >= 1");
+  OSC_REQUIRE(B >= 1 && B <= 65535, "solve: batch must be in [1, 65535]");
   w.m = m;
   w.B = B;
   w.hist_cap = hist_cap;
-  // hierarchy geometry
   int g = m, nl = 0;
   for (;;) {
     w.lev[nl].m = g;
@@ -591,7 +758,7 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   w.nlev = nl;
   w.nc = (int)w.lev[nl - 1].N;
   OSC_REQUIRE(w.nc <= 1089, "solve: coarsest multigrid grid too large (m must be 2^j * c, c <= 32)");
-  w.max_parts = nblocks(w.lev[0].N);
+  w.max_parts = (int)std::max<int64_t>(tile_parts(m), nblocks(w.lev[0].N));
   w.mem.ensure(solver_bytes(m, B, hist_cap));
   char* p = static_cast<char*>(w.mem.p);
   auto take = [&](size_t bytes) {
@@ -602,18 +769,19 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   for (int l = 0; l < nl; ++l) {
     SolverLevel& L = w.lev[l];
     const size_t vb = sizeof(double) * L.N * B;
-    if (l > 0) L.k = (double*)take(vb);  // level 0's k is provided by the caller buffer
-    L.D = (double*)take(vb);
-    L.E = (double*)take(vb);
-    L.Nw = (double*)take(vb);
+    L.k = (l > 0) ? (double*)take(vb) : nullptr;  // level 0's k is the caller's buffer
+    L.D = L.E = L.Nw = nullptr;                     // stencils are recomputed from k in-tile
     L.r = (double*)take(vb);
     L.z = (double*)take(vb);
+    L.z2 = (double*)take(vb);
   }
   const size_t vb0 = sizeof(double) * w.lev[0].N * B;
   w.u = (double*)take(vb0);
+  w.r2 = (double*)take(vb0);
+  w.r_cur = w.lev[0].r;
   w.p0 = (double*)take(vb0);
   w.p1 = (double*)take(vb0);
-  w.Ap = (double*)take(vb0);
+  w.Ap = nullptr;
   w.chol = (double*)take(sizeof(double) * (size_t)w.nc * w.nc * B);
   w.scal = (double*)take(sizeof(double) * S_NSCAL * B);
   w.flags = (int*)take(sizeof(int) * F_NFLAGS * B);
@@ -630,50 +798,52 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
 namespace {
 
 Geo geo_of(const SolverLevel& L) { return Geo{L.m, L.m + 1, L.N}; }
-St st_of(const SolverLevel& L) { return St{L.D, L.E, L.Nw}; }
+dim3 tile_grid(const SolverLevel& L, int B) {
+  return dim3((unsigned)((L.m + 1 + TX - 1) / TX), (unsigned)((L.m + 1 + TY - 1) / TY), (unsigned)B);
+}
+dim3 ctile_grid(const SolverLevel& C, int B) {
+  return dim3((unsigned)((C.m + 1 + CXT - 1) / CXT), (unsigned)((C.m + 1 + CYT - 1) / CYT), (unsigned)B);
+}
 
-void vcycle(Ctx* ctx, int bc, int B) {
+// Preconditioner z = M r on level 0. With `fused_down` the level-0 pre-smoother already ran
+// inside pcg_update_down (z holds the pre-smoothed correction).
+void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
   SolverWork& w = ctx->solver;
   cudaStream_t st = ctx->stream;
   double2* part = reinterpret_cast<double2*>(w.partial);
   if (w.nlev == 1) {
     {
       KScope ks(ctx, "mg_coarse_solve");
-      coarse_solve_kernel<<<(B + 63) / 64, 64, 0, st>>>(w.nc, B, w.chol, w.lev[0].r, w.lev[0].z, w.flags);
+      coarse_solve_kernel<<<(B + 63) / 64, 64, 0, st>>>(w.nc, B, w.chol, w.r_cur, w.lev[0].z2, w.flags);
     }
     KScope ks(ctx, "pcg_dot_rz");
-    dot_rz_kernel<<<dim3(nblocks(w.lev[0].N), B), NT, 0, st>>>(geo_of(w.lev[0]), w.lev[0].r, w.lev[0].z,
-                                                              w.scal, w.flags, part, w.max_parts, w.counter);
+    dot_rz_kernel<<<dim3(nblocks(w.lev[0].N), 1, B), NT, 0, st>>>(geo_of(w.lev[0]), w.r_cur, w.lev[0].z2,
+                                                                 w.scal, w.flags, part, w.max_parts, w.counter);
+    OSC_CUDA(cudaGetLastError());
     return;
   }
   for (int l = 0; l + 1 < w.nlev; ++l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    {
+    if (l > 0 || !fused_down) {
       KScope ks(ctx, "mg_smooth_down");
-      smooth_down_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(geo_of(L), st_of(L), L.r, L.z, w.flags);
+      smooth_down_kernel<<<tile_grid(L, B), TT, 0, st>>>(geo_of(L), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, w.flags);
     }
     KScope ks(ctx, "mg_restrict");
-    restrict_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(geo_of(L), geo_of(C), bc, st_of(L), L.r, L.z,
-                                                         C.r, w.flags);
+    restrict_kernel<<<ctile_grid(C, B), TT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, C.r, w.flags);
   }
   {
     const SolverLevel& C = w.lev[w.nlev - 1];
     KScope ks(ctx, "mg_coarse_solve");
-    coarse_solve_kernel<<<(B + 63) / 64, 64, 0, st>>>(w.nc, B, w.chol, C.r, C.z, w.flags);
+    coarse_solve_kernel<<<(B + 63) / 64, 64, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
   }
   for (int l = w.nlev - 2; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    {
-      KScope ks(ctx, "mg_smooth_up_black");
-      smooth_up_black_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(geo_of(L), geo_of(C), st_of(L), L.r,
-                                                                   L.z, C.z, w.flags);
-    }
-    KScope ks(ctx, "mg_smooth_up_red");
-    smooth_up_red_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(geo_of(L), st_of(L), L.r, L.z, l == 0 ? 1 : 0,
-                                                               w.scal, w.flags, part, w.max_parts,
-                                                               w.counter);
+    KScope ks(ctx, "mg_smooth_up");
+    smooth_up_kernel<<<tile_grid(L, B), TT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, L.z2, C.z2,
+                                                     l == 0 ? 1 : 0, w.scal, w.flags, part,
+                                                     w.max_parts, w.counter);
   }
   OSC_CUDA(cudaGetLastError());
 }
@@ -691,34 +861,43 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
     ~TagGuard() { c->tag.clear(); }
   } tg{ctx};
   ctx->tag = std::to_string(w.m);
-  // setup: stencils + injection + coarse factor
-  {
-    KScope ks(ctx, "mg_setup", w.nlev + 1);
-    for (int l = 0; l < w.nlev; ++l) {
-      SolverLevel& L = w.lev[l];
-      double* kc = (l + 1 < w.nlev) ? w.lev[l + 1].k : nullptr;
-      setup_level_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(geo_of(L), bc, L.k, L.D, L.E, L.Nw, kc);
+  {  // hierarchy: injected k (fem.cpp:241-244) + coarsest Cholesky (fem.cpp:255-272)
+    KScope ks(ctx, "mg_setup", w.nlev);
+    for (int l = 0; l + 1 < w.nlev; ++l) {
+      const SolverLevel& L = w.lev[l];
+      const SolverLevel& C = w.lev[l + 1];
+      inject_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(geo_of(L), geo_of(C), L.k, C.k);
     }
     const SolverLevel& C = w.lev[w.nlev - 1];
-    coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), B, C.D, C.E, C.Nw, w.chol);
+    coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), bc, B, C.k, w.chol);
     OSC_CUDA(cudaGetLastError());
   }
   SolverLevel& L0 = w.lev[0];
   const Geo g0 = geo_of(L0);
-  const int nb0 = nblocks(L0.N);
+  w.r_cur = L0.r;
   OSC_CUDA(cudaMemsetAsync(w.n_active, 0, sizeof(int), st));
   {
     KScope ks(ctx, "pcg_init");
-    pcg_init_kernel<<<dim3(nb0, B), NT, 0, st>>>(g0, bc, prob->forcing, prob->forcing_value, prob->tol,
-                                                 prob->max_iter_factor, L0.k, w.u, L0.r, w.scal, w.flags,
-                                                 part, w.max_parts, w.counter, w.n_active, w.hist,
-                                                 w.hist_cap);
+    pcg_init_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(
+        g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, w.u, w.r_cur,
+        w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
   }
-  vcycle(ctx, bc, B);  // z = M r, rz = <r,z>
+  vcycle(ctx, bc, B, false);  // z = M r0, rz = <r0, z>
   double* p_old = w.p0;
   double* p_new = w.p1;
   const int check_every = L0.N >= 65536 ? 1 : 4;
+  const bool multilevel = w.nlev > 1;
+  // optional host-side safety valve (debugging): OSC_HARD_ITER_CAP stops the loop early; the
+  // samples still active are reported as not converged by solver_results().
+  static const long hard_cap = [] {
+    const char* e = std::getenv("OSC_HARD_ITER_CAP");
+    return e ? std::atol(e) : -1L;
+  }();
   for (int it = 0;; ++it) {
+    if (hard_cap >= 0 && it >= hard_cap) {
+      mark_active_failed_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, w.flags);
+      break;
+    }
     if (it % check_every == 0) {
       OSC_CUDA(cudaMemcpyAsync(ctx->h_pinned_int, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
       OSC_CUDA(cudaStreamSynchronize(st));
@@ -726,16 +905,19 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
     }
     {
       KScope ks(ctx, "pcg_apply");
-      pcg_apply_kernel<<<dim3(nb0, B), NT, 0, st>>>(g0, st_of(L0), L0.z, p_old, p_new, w.Ap, w.scal,
-                                                    w.flags, part, w.max_parts, w.counter);
+      pcg_apply_kernel<<<tile_grid(L0, B), TT, 0, st>>>(g0, bc, L0.k, L0.z2, p_old, p_new, w.scal, w.flags,
+                                                        part, w.max_parts, w.counter);
     }
     {
-      KScope ks(ctx, "pcg_update");
-      pcg_update_kernel<<<dim3(nb0, B), NT, 0, st>>>(g0, prob->tol, p_new, w.Ap, w.u, L0.r, w.scal,
-                                                     w.flags, part, w.max_parts, w.counter, w.n_active,
-                                                     w.hist, w.hist_cap);
+      KScope ks(ctx, "pcg_update_down");
+      double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
+      pcg_update_down_kernel<<<tile_grid(L0, B), TT, 0, st>>>(g0, bc, prob->tol, L0.k, p_new, w.u, w.r_cur,
+                                                              r_next, L0.z, w.scal, w.flags, part, w.max_parts,
+                                                              w.counter, w.n_active, w.hist, w.hist_cap);
     }
-    vcycle(ctx, bc, B);
+    w.r_cur = (w.r_cur == L0.r) ? w.r2 : L0.r;
+    // single-level: the "pre-smoothed" z is overwritten by the exact coarse solve
+    vcycle(ctx, bc, B, multilevel);
     std::swap(p_old, p_new);
   }
 }
@@ -753,7 +935,7 @@ void qoi_launch(Ctx* ctx, const osc_problem* prob, int B, double* q_dev) {
   if (prob->qoi == OSC_QOI_FLUX) items = m + 1;
   else if (prob->qoi != OSC_QOI_POINT) items = (int64_t)m * m;
   KScope ks(ctx, "qoi");
-  qoi_kernel<<<dim3(nblocks(items), B), NT, 0, ctx->stream>>>(
+  qoi_kernel<<<dim3(nblocks(items), 1, B), NT, 0, ctx->stream>>>(
       geo_of(L0), prob->qoi, prob->qoi_x, prob->qoi_y, prob->forcing, prob->forcing_value, w.u, L0.k,
       q_dev, reinterpret_cast<double2*>(w.partial), w.max_parts, w.counter);
   OSC_CUDA(cudaGetLastError());

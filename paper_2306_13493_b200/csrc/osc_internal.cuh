@@ -74,7 +74,8 @@ struct SolverLevel {
   int m = 0;       // cells per side
   int64_t N = 0;   // nodes (m+1)^2
   double *k = nullptr, *D = nullptr, *E = nullptr, *Nw = nullptr;  // conductivity + stencil
-  double *r = nullptr, *z = nullptr;                                // MG residual / correction
+  double *r = nullptr, *z = nullptr;   // MG residual / pre-smoothed correction
+  double* z2 = nullptr;                // post-smoothed correction (written by smooth_up; no in-place halo race)
 };
 
 struct SolverWork {
@@ -84,6 +85,8 @@ struct SolverWork {
   int nc = 0;  // coarsest node count
   SolverLevel lev[24];
   double *u = nullptr, *p0 = nullptr, *p1 = nullptr, *Ap = nullptr;  // level-0 PCG vectors
+  double* r2 = nullptr;  // level-0 residual ping-pong partner (pcg_update_down reads a halo of r)
+  double* r_cur = nullptr;
   double* chol = nullptr;   // B * nc * nc
   double* scal = nullptr;   // per-sample scalars (see mgpcg.cu)
   double* partial = nullptr;

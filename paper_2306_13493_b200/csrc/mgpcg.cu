@@ -81,14 +81,6 @@ __device__ __forceinline__ bool reduce2_last(double v0, double v1, double2* part
   return true;
 }
 
-// ---- tiled, fused MG-PCG kernels -------------------------------------------------------------
-// Every kernel works on a TX×TY tile of one sample (blockIdx.z) with the fields it needs staged
-// in shared memory with a halo, and recomputes the 5-point stencil from the nodal k tile
-// (8 B/node of HBM instead of 24 B/node for stored D/E/N).
-constexpr int TX = 32, TY = 16;      // fine tile (threads: 32 × 8, two rows each)
-constexpr int CXT = 32, CYT = 8;     // coarse tile of the restriction (one node per thread)
-constexpr int TT = 256;              // threads per tiled CTA
-
 struct Sten {
   double d, e, w, n, s;  // raw diagonal (1 on Dirichlet rows) and eliminated couplings
 };
@@ -122,81 +114,6 @@ __device__ __forceinline__ Sten stencil_at(const double* kt, int ld, int lx, int
   st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : s;
   return st;
 }
-
-// Stage rows [gy0, gy0+h) × cols [gx0, gx0+wd) of a sample's nodal field into smem with
-// cp.async (LDGSTS): every element's copy is in flight at once (no register round trip), and
-// out-of-grid elements are zero-filled (src-size 0). Caller: stage_wait() before use.
-__device__ __forceinline__ void stage(double* sm, int wd, int h, const double* __restrict__ g,
-                                      int gx0, int gy0, int n0) {
-  for (int idx = threadIdx.x; idx < wd * h; idx += TT) {
-    const int ly = idx / wd, lx = idx - ly * wd;
-    const int gx = gx0 + lx, gy = gy0 + ly;
-    const bool in = gx >= 0 && gx < n0 && gy >= 0 && gy < n0;
-    const double* src = in ? g + (int64_t)gy * n0 + gx : g;
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(sm + idx);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(in ? 8 : 0)
-                 : "memory");
-  }
-}
-__device__ __forceinline__ void stage_wait() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-}
-
-// Raw edge weights of a staged k region (origin (gx0, gy0), wd × h, zero-padded outside the
-// grid): es[y][x] couples (x,y)–(x+1,y), ns[y][x] couples (x,y)–(x,y+1). Triangle means use
-// the reference's vertex order with ·(1/3) instead of /3 (≤ 1 ulp per coefficient), and each
-// edge is formed once, so both rows of A see the same double (A stays symmetric).
-__device__ __forceinline__ void build_edges(const double* ks, double* es, double* ns, int wd, int h,
-                                            int gx0, int gy0, int m) {
-  constexpr double third = 1.0 / 3.0;
-  for (int idx = threadIdx.x; idx < wd * h; idx += TT) {
-    const int ly = idx / wd, lx = idx - ly * wd;
-    const int gx = gx0 + lx, gy = gy0 + ly;
-    double e = 0.0, n = 0.0;
-    if (lx + 1 < wd && ly > 0 && ly + 1 < h && gx >= 0 && gx < m && gy >= 0 && gy <= m) {
-      const double* k = ks + idx;
-      const double lo = gy < m ? (k[0] + k[1] + k[wd + 1]) * third : 0.0;       // K_low(x, y)
-      const double up = gy > 0 ? (k[-wd] + k[1] + k[0]) * third : 0.0;          // K_up(x, y-1)
-      e = -0.5 * (lo + up);
-    }
-    if (lx > 0 && lx + 1 < wd && ly + 1 < h && gy >= 0 && gy < m && gx >= 0 && gx <= m) {
-      const double* k = ks + idx;
-      const double up = gx < m ? (k[0] + k[wd + 1] + k[wd]) * third : 0.0;      // K_up(x, y)
-      const double lo = gx > 0 ? (k[-1] + k[0] + k[wd]) * third : 0.0;         // K_low(x-1, y)
-      n = -0.5 * (up + lo);
-    }
-    es[idx] = e;
-    ns[idx] = n;
-  }
-}
-
-// 5-point row at local (lx, ly) of an edge region with leading dimension wd.
-__device__ __forceinline__ Sten sten_edges(const double* es, const double* ns, int wd, int lx, int ly,
-                                           int gx, int gy, int m, int bc) {
-  const int c = ly * wd + lx;
-  Sten st;
-  if (is_dir(bc, m, gx, gy)) {
-    st.d = 1.0;
-    st.e = st.w = st.n = st.s = 0.0;
-    return st;
-  }
-  const double e = es[c], w = es[c - 1], n = ns[c], s = ns[c - wd];
-  st.d = -(e + w + n + s);
-  st.e = is_dir(bc, m, gx + 1, gy) ? 0.0 : e;
-  st.w = is_dir(bc, m, gx - 1, gy) ? 0.0 : w;
-  st.n = is_dir(bc, m, gx, gy + 1) ? 0.0 : n;
-  st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : s;
-  return st;
-}
-
-#define TILE_PROLOGUE                                                \
-  const int b = blockIdx.z;                                          \
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                       \
-  const int m = g.m, n0 = g.n0;                                      \
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;              \
-  const int64_t off = (int64_t)b * g.N;                              \
-  const int tx = threadIdx.x & 31, ty0 = threadIdx.x >> 5;
 
 // ---- setup: k injection to the next level (fem.cpp:241-244) -----------------------------------------
 __global__ void __launch_bounds__(NT) inject_kernel(Geo gf, Geo gc, const double* __restrict__ kf,
@@ -308,39 +225,118 @@ __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing
   }
 }
 
-// ---- PCG: p = z + βp (p = z first), <p, A p> → α  (Ap itself is recomputed where needed) -----------
-__global__ void __launch_bounds__(TT) pcg_apply_kernel(Geo g, int bc, const double* __restrict__ k,
+// ---- register-marching MG-PCG kernels -----------------------------------------------------------
+// One lane per grid column; a warp owns a strip of 32 columns (the outer HX lanes are x-halo) and
+// marches up a chunk of LY rows, keeping the few rows each stage needs in registers. x-neighbours
+// come from warp shuffles, y-neighbours from the register pipeline: no shared-memory staging and
+// no barriers on the data path. The 5-point stencil is recomputed from nodal k per row (8 B/node
+// of HBM instead of 24 B/node for stored D/E/N).
+constexpr int MW = 4;        // warps (strips) per CTA
+constexpr int MT = 32 * MW;  // threads per CTA
+constexpr int LY = 32;       // output rows per warp
+constexpr int LYC = 16;      // coarse output rows per warp (restriction)
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double shup(double v) { return __shfl_up_sync(FULL, v, 1); }
+__device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(FULL, v, 1); }
+
+__device__ __forceinline__ double ldv(const double* __restrict__ base, int gx, int gy, int n0) {
+  return ((unsigned)gx < (unsigned)n0 && (unsigned)gy < (unsigned)n0)
+             ? __ldg(base + (int64_t)gy * n0 + gx) : 0.0;
+}
+
+// 1/d to full double precision: MUFU approximation + two Newton steps (no DDIV sequence).
+__device__ __forceinline__ double rcp64(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  y = fma(y, fma(-d, y, 1.0), y);
+  return y;
+}
+
+// Raw edge weights of row y for this lane's column x from k rows y−1 (km), y (k0), y+1 (kp):
+// E couples (x,y)–(x+1,y), N couples (x,y)–(x,y+1). Triangle means in the reference's vertex
+// order, ·(1/3) instead of /3 (≤ 1 ulp per coefficient). Every lane must call (shuffles).
+__device__ __forceinline__ void edges_row(double km, double k0, double kp, int gx, int gy, int m,
+                                          double& E, double& N) {
+  constexpr double third = 1.0 / 3.0;
+  const double k0x1 = shdn(k0), kpx1 = shdn(kp), k0xm = shup(k0);
+  E = 0.0;
+  N = 0.0;
+  if (gx >= 0 && gx < m && gy >= 0 && gy <= m) {
+    const double lo = gy < m ? (k0 + k0x1 + kpx1) * third : 0.0;  // K_low(x, y)
+    const double up = gy > 0 ? (km + k0x1 + k0) * third : 0.0;    // K_up(x, y−1)
+    E = -0.5 * (lo + up);
+  }
+  if (gy >= 0 && gy < m && gx >= 0 && gx <= m) {
+    const double up = gx < m ? (k0 + kpx1 + kp) * third : 0.0;    // K_up(x, y)
+    const double lo = gx > 0 ? (k0xm + k0 + kp) * third : 0.0;    // K_low(x−1, y)
+    N = -0.5 * (up + lo);
+  }
+}
+
+// 5-point row at (gx, gy) from this row's E, N and the previous row's N (south coupling).
+// Out-of-grid and Dirichlet rows are identity. Every lane must call (shuffle).
+__device__ __forceinline__ Sten sten_row(double E, double N, double Nm, int gx, int gy, int m, int bc) {
+  const double W = shup(E);
+  Sten st;
+  if (gx < 0 || gx > m || gy < 0 || gy > m || is_dir(bc, m, gx, gy)) {
+    st.d = 1.0;
+    st.e = st.w = st.n = st.s = 0.0;
+    return st;
+  }
+  st.d = -(E + W + N + Nm);
+  st.e = is_dir(bc, m, gx + 1, gy) ? 0.0 : E;
+  st.w = is_dir(bc, m, gx - 1, gy) ? 0.0 : W;
+  st.n = is_dir(bc, m, gx, gy + 1) ? 0.0 : N;
+  st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : Nm;
+  return st;
+}
+
+#define MARCH_PROLOGUE(HX)                                              \
+  const int b = blockIdx.z;                                             \
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                          \
+  const int lane = threadIdx.x & 31;                                    \
+  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);               \
+  const int m = g.m, n0 = g.n0;                                         \
+  const int gx = strip * (32 - 2 * (HX)) - (HX) + lane;                 \
+  const bool outx = lane >= (HX) && lane < 32 - (HX) && gx <= m;        \
+  const int y0 = blockIdx.y * LY, y1 = min(y0 + LY, n0);                \
+  const int64_t off = (int64_t)b * g.N;
+
+// ---- PCG: p = z + βp (p = z first), <p, A p> → α  (Ap itself is recomputed where needed) --------
+__global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const double* __restrict__ k,
                                                        const double* __restrict__ z,
                                                        const double* __restrict__ p_old,
                                                        double* __restrict__ p_new, double* scal,
                                                        int* flags, double2* partial, int maxp,
                                                        unsigned* counter) {
-  TILE_PROLOGUE
-  constexpr int W1 = TX + 2, H1 = TY + 2;
-  __shared__ double ks[H1 * W1], ps[H1 * W1], zs[H1 * W1], es[H1 * W1], ns[H1 * W1];
+  MARCH_PROLOGUE(1)
   const bool first = flags[b * F_NFLAGS + F_FIRST] != 0;
   const double beta = scal[b * S_NSCAL + S_BETA];
-  stage(ks, W1, H1, k + off, x0 - 1, y0 - 1, n0);
-  stage(zs, W1, H1, z + off, x0 - 1, y0 - 1, n0);
-  if (!first) stage(ps, W1, H1, p_old + off, x0 - 1, y0 - 1, n0);
-  stage_wait();
-  build_edges(ks, es, ns, W1, H1, x0 - 1, y0 - 1, m);
-  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT)
-    ps[idx] = first ? zs[idx] : fma(beta, ps[idx], zs[idx]);
-  __syncthreads();
+  const double *kb = k + off, *zb = z + off, *pb = p_old + off;
+  auto P = [&](int y) {
+    const double zv = ldv(zb, gx, y, n0);
+    return first ? zv : fma(beta, ldv(pb, gx, y, n0), zv);
+  };
+  double km = ldv(kb, gx, y0 - 1, n0), k0 = ldv(kb, gx, y0, n0);
+  double pm = P(y0 - 1), p0 = P(y0);
+  double Nm, Ed;
+  edges_row(0.0, km, k0, gx, y0 - 1, m, Ed, Nm);
   double pap = 0.0;
-#pragma unroll
-  for (int r = 0; r < TY / 8; ++r) {
-    const int ly = ty0 + 8 * r, gx = x0 + tx, gy = y0 + ly;
-    if (gx < n0 && gy < n0) {
-      const int c = (ly + 1) * W1 + tx + 1;
-      const Sten st = sten_edges(es, ns, W1, tx + 1, ly + 1, gx, gy, m, bc);
-      const double pc = ps[c];
-      const double ap = st.d * pc + st.e * ps[c + 1] + st.w * ps[c - 1] + st.n * ps[c + W1] +
-                        st.s * ps[c - W1];
-      p_new[off + (int64_t)gy * n0 + gx] = pc;
-      pap = fma(pc, ap, pap);
+  for (int y = y0; y < y1; ++y) {
+    const double kp = ldv(kb, gx, y + 1, n0);
+    const double pp = P(y + 1);
+    double E, N;
+    edges_row(km, k0, kp, gx, y, m, E, N);
+    const Sten st = sten_row(E, N, Nm, gx, y, m, bc);
+    const double pe = shdn(p0), pw = shup(p0);
+    const double ap = st.d * p0 + st.e * pe + st.w * pw + st.n * pp + st.s * pm;
+    if (outx) {
+      p_new[off + (int64_t)y * n0 + gx] = p0;
+      pap = fma(p0, ap, pap);
     }
+    km = k0; k0 = kp; pm = p0; p0 = pp; Nm = N;
   }
   double t0, t1;
   if (reduce2_last(pap, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -352,60 +348,46 @@ __global__ void __launch_bounds__(TT) pcg_apply_kernel(Geo g, int bc, const doub
 // ---- PCG update fused with the level-0 pre-smoother:
 //   u += αp, r −= αAp (Ap recomputed from p), ‖r‖ → convergence,
 //   then z_red = r/D, z_black = (r − Σ A z_red)/D  (red-black GS from z = 0)
-__global__ void __launch_bounds__(TT) pcg_update_down_kernel(
+__global__ void __launch_bounds__(MT) pcg_update_down_kernel(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
-    double* __restrict__ z, double* scal, int* flags,
-    double2* partial, int maxp, unsigned* counter, int* n_active, double* hist, int hist_cap) {
-  TILE_PROLOGUE
-  constexpr int W2 = TX + 4, H2 = TY + 4, W1 = TX + 2, H1 = TY + 2;
-  __shared__ double ks[H2 * W2], ps[H2 * W2], rs[H1 * W1], zr[H1 * W1], es[H2 * W2], ns[H2 * W2],
-      us[TX * TY];
+    double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
+    int* n_active, double* hist, int hist_cap) {
+  MARCH_PROLOGUE(2)
   const double alpha = scal[b * S_NSCAL + S_ALPHA];
-  stage(ks, W2, H2, k + off, x0 - 2, y0 - 2, n0);
-  stage(ps, W2, H2, p + off, x0 - 2, y0 - 2, n0);
-  stage(rs, W1, H1, r + off, x0 - 1, y0 - 1, n0);
-  stage(us, TX, TY, u + off, x0, y0, n0);
-  stage_wait();
-  build_edges(ks, es, ns, W2, H2, x0 - 2, y0 - 2, m);
-  __syncthreads();
-  // r_new and z_red = r_new / D on the tile + 1 halo (in place in rs)
-  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT) {
-    const int ly = idx / W1, lx = idx - ly * W1;
-    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-    double rn = 0.0, zv = 0.0;
-    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0) {
-      const int c = (ly + 1) * W2 + lx + 1;
-      const Sten st = sten_edges(es, ns, W2, lx + 1, ly + 1, gx, gy, m, bc);
-      const double ap = st.d * ps[c] + st.e * ps[c + 1] + st.w * ps[c - 1] + st.n * ps[c + W2] +
-                        st.s * ps[c - W2];
-      rn = fma(-alpha, ap, rs[idx]);
-      if (((gx + gy) & 1) == 0) zv = rn / st.d;
-    }
-    rs[idx] = rn;
-    zr[idx] = zv;
-  }
-  __syncthreads();
+  const double *kb = k + off, *pb = p + off, *rb = r + off;
+  // pipeline state for output row t: k/p rows t, t+1; N_t; r_new(t); z_red rows t−1, t; stencil(t)
+  double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
+  double pa = ldv(pb, gx, y0 - 2, n0), pb1 = ldv(pb, gx, y0 - 1, n0);
+  double Nt, Ed;
+  edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
+  double rn0 = 0.0, zrm = 0.0, zr0 = 0.0;
+  Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
   double rr = 0.0;
-#pragma unroll
-  for (int q = 0; q < TY / 8; ++q) {
-    const int ly = ty0 + 8 * q, gx = x0 + tx, gy = y0 + ly;
-    if (gx < n0 && gy < n0) {
-      const int c1 = (ly + 1) * W1 + tx + 1;
-      const int64_t j = off + (int64_t)gy * n0 + gx;
-      const double rn = rs[c1];
-      double zv;
-      if (((gx + gy) & 1) == 0) {
-        zv = zr[c1];
-      } else {
-        const Sten st = sten_edges(es, ns, W2, tx + 2, ly + 2, gx, gy, m, bc);
-        zv = (rn - (st.e * zr[c1 + 1] + st.w * zr[c1 - 1] + st.n * zr[c1 + W1] + st.s * zr[c1 - W1])) / st.d;
-      }
-      u[j] = fma(alpha, ps[(ly + 2) * W2 + tx + 2], us[ly * TX + tx]);
-      r_out[j] = rn;
+  for (int t = y0 - 2; t < y1; ++t) {
+    const double kc = ldv(kb, gx, t + 2, n0);
+    const double pc = ldv(pb, gx, t + 2, n0);
+    const double r1 = ldv(rb, gx, t + 1, n0);
+    double E1, N1;
+    edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
+    const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
+    const double ap1 = st1.d * pb1 + st1.e * shdn(pb1) + st1.w * shup(pb1) + st1.n * pc + st1.s * pa;
+    const double rn1 = fma(-alpha, ap1, r1);
+    const double zrp = (((gx + t + 1) & 1) == 0) ? rn1 * rcp64(st1.d) : 0.0;
+    // output row t
+    const double ze = shdn(zr0), zw = shup(zr0);
+    if (t >= y0 && outx) {
+      const double zv = (((gx + t) & 1) == 0)
+                            ? zr0
+                            : (rn0 - (st0.e * ze + st0.w * zw + st0.n * zrp + st0.s * zrm)) * rcp64(st0.d);
+      const int64_t j = off + (int64_t)t * n0 + gx;
+      u[j] = fma(alpha, pa, u[j]);
+      r_out[j] = rn0;
       z[j] = zv;
-      rr = fma(rn, rn, rr);
+      rr = fma(rn0, rn0, rr);
     }
+    ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
+    rn0 = rn1; zrm = zr0; zr0 = zrp; st0 = st1;
   }
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -429,84 +411,134 @@ __global__ void __launch_bounds__(TT) pcg_update_down_kernel(
   }
 }
 
-// ---- pre-smoother on coarse levels (and on level 0 for the first V-cycle): red then black -----------
-__global__ void __launch_bounds__(TT) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
+// ---- pre-smoother from z = 0 (coarse levels; level 0 of the first V-cycle): red then black ------
+__global__ void __launch_bounds__(MT) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ z, const int* flags) {
-  TILE_PROLOGUE
-  constexpr int W2 = TX + 4, H2 = TY + 4, W1 = TX + 2, H1 = TY + 2;
-  __shared__ double ks[H2 * W2], rs[H1 * W1], zr[H1 * W1], es[H2 * W2], ns[H2 * W2];
-  stage(ks, W2, H2, k + off, x0 - 2, y0 - 2, n0);
-  stage(rs, W1, H1, r + off, x0 - 1, y0 - 1, n0);
-  stage_wait();
-  build_edges(ks, es, ns, W2, H2, x0 - 2, y0 - 2, m);
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT) {
-    const int ly = idx / W1, lx = idx - ly * W1;
-    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-    double zv = 0.0;
-    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0 && ((gx + gy) & 1) == 0) {
-      const Sten st = sten_edges(es, ns, W2, lx + 1, ly + 1, gx, gy, m, bc);
-      zv = rs[idx] / st.d;
+  MARCH_PROLOGUE(2)  // z_black at x needs D(x−1), i.e. E(x−2)
+  const double *kb = k + off, *rb = r + off;
+  double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
+  double Nt, Ed;
+  edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
+  double r0 = 0.0, zrm = 0.0, zr0 = 0.0;
+  Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
+  for (int t = y0 - 2; t < y1; ++t) {
+    const double kc = ldv(kb, gx, t + 2, n0);
+    const double r1 = ldv(rb, gx, t + 1, n0);
+    double E1, N1;
+    edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
+    const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
+    const double zrp = (((gx + t + 1) & 1) == 0) ? r1 * rcp64(st1.d) : 0.0;
+    const double ze = shdn(zr0), zw = shup(zr0);
+    if (t >= y0 && outx) {
+      const double zv = (((gx + t) & 1) == 0)
+                            ? zr0
+                            : (r0 - (st0.e * ze + st0.w * zw + st0.n * zrp + st0.s * zrm)) * rcp64(st0.d);
+      z[off + (int64_t)t * n0 + gx] = zv;
     }
-    zr[idx] = zv;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < TY / 8; ++q) {
-    const int ly = ty0 + 8 * q, gx = x0 + tx, gy = y0 + ly;
-    if (gx < n0 && gy < n0) {
-      const int c1 = (ly + 1) * W1 + tx + 1;
-      double zv;
-      if (((gx + gy) & 1) == 0) {
-        zv = zr[c1];
-      } else {
-        const Sten st = sten_edges(es, ns, W2, tx + 2, ly + 2, gx, gy, m, bc);
-        zv = (rs[c1] - (st.e * zr[c1 + 1] + st.w * zr[c1 - 1] + st.n * zr[c1 + W1] + st.s * zr[c1 - W1])) / st.d;
-      }
-      z[off + (int64_t)gy * n0 + gx] = zv;
-    }
+    ka = kb1; kb1 = kc; Nt = N1;
+    r0 = r1; zrm = zr0; zr0 = zrp; st0 = st1;
   }
 }
 
 // ---- residual restriction rc = Pᵀ(r − A z) after the red-black pre-smoother (fem.cpp:168-195).
 // After the black sweep the residual vanishes on black nodes and equals −Σ A z_black on red
 // nodes, so rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]; zero at coarse Dirichlet nodes.
-__global__ void __launch_bounds__(TT) restrict_kernel(Geo g, Geo gc, int bc,
+// Lane l owns fine columns xa = 2I, xb = 2I+1 of coarse column I; lanes 0 and 31 are halo.
+__global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
                                                       const double* __restrict__ k,
                                                       const double* __restrict__ z,
                                                       double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int lane = threadIdx.x & 31;
+  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
   const int m = g.m, n0 = g.n0, mc = gc.m;
-  const int I0 = blockIdx.x * CXT, J0 = blockIdx.y * CYT;
-  constexpr int WR = 2 * CXT + 3, HR = 2 * CYT + 3;
-  __shared__ double ks[HR * WR], zs[HR * WR], es[HR * WR], ns[HR * WR];
+  const int I = strip * 30 - 1 + lane;
+  const bool outI = lane >= 1 && lane < 31 && I <= mc;
+  const int xa = 2 * I, xb = 2 * I + 1;
+  const int J0 = blockIdx.y * LYC, J1 = min(J0 + LYC, gc.n0);
   const int64_t off = (int64_t)b * g.N;
-  const int fx0 = 2 * I0 - 2, fy0 = 2 * J0 - 2;
-  stage(ks, WR, HR, k + off, fx0, fy0, n0);
-  stage(zs, WR, HR, z + off, fx0, fy0, n0);
-  stage_wait();
-  build_edges(ks, es, ns, WR, HR, fx0, fy0, m);
-  __syncthreads();
-  const int I = I0 + (threadIdx.x & 31), J = J0 + (threadIdx.x >> 5);
-  if (I > mc || J > mc) return;
-  double acc = 0.0;
-  if (!is_dir(bc, mc, I, J)) {
-    auto t_at = [&](int fx, int fy) {  // residual at a red fine node
-      if (fx < 0 || fx > m || fy < 0 || fy > m) return 0.0;
-      const int lx = fx - fx0, ly = fy - fy0;
-      const Sten st = sten_edges(es, ns, WR, lx, ly, fx, fy, m, bc);
-      const int c = ly * WR + lx;
-      return -(st.e * zs[c + 1] + st.w * zs[c - 1] + st.n * zs[c + WR] + st.s * zs[c - WR]);
-    };
-    acc = t_at(2 * I, 2 * J) + 0.5 * (t_at(2 * I + 1, 2 * J + 1) + t_at(2 * I - 1, 2 * J - 1));
+  const double *kb = k + off, *zb = z + off;
+  constexpr double third = 1.0 / 3.0;
+  // edges at both columns of row y from k rows y−1, y, y+1 (a: xa, b: xb)
+  auto edges2 = [&](double kma, double kmb, double k0a, double k0b, double kpa, double kpb, int y,
+                    double& Ea, double& Eb, double& Na, double& Nb) {
+    const double k0a_n = shdn(k0a), kpa_n = shdn(kpa), k0b_p = shup(k0b);  // x = xb+1 / xa−1
+    Ea = Eb = Na = Nb = 0.0;
+    if (y >= 0 && y <= m) {
+      if (xa >= 0 && xa < m)
+        Ea = -0.5 * ((y < m ? (k0a + k0b + kpb) * third : 0.0) + (y > 0 ? (kma + k0b + k0a) * third : 0.0));
+      if (xb >= 0 && xb < m)
+        Eb = -0.5 * ((y < m ? (k0b + k0a_n + kpa_n) * third : 0.0) + (y > 0 ? (kmb + k0a_n + k0b) * third : 0.0));
+    }
+    if (y >= 0 && y < m) {
+      if (xa >= 0 && xa <= m)
+        Na = -0.5 * ((xa < m ? (k0a + kpb + kpa) * third : 0.0) + (xa > 0 ? (k0b_p + k0a + kpa) * third : 0.0));
+      if (xb >= 0 && xb <= m)
+        Nb = -0.5 * ((xb < m ? (k0b + kpa_n + kpb) * third : 0.0) + (xb > 0 ? (k0a + k0b + kpb) * third : 0.0));
+    }
+  };
+  // residual at the red node of row y (column xa if y even, xb if odd): −Σ A z_black
+  auto t_red = [&](int y, double Ea, double Eb, double Na, double Nb, double Nma, double Nmb,
+                   double zma, double zmb, double z0a, double z0b, double zpa, double zpb) {
+    const double Eb_w = shup(Eb);     // E at column xa−1
+    const double z0b_w = shup(z0b);   // z at xa−1
+    const double z0a_e = shdn(z0a);   // z at xb+1
+    double t = 0.0;
+    if ((y & 1) == 0) {  // red at xa
+      if (xa >= 0 && xa <= m && y >= 0 && y <= m && !is_dir(bc, m, xa, y)) {
+        const double e = is_dir(bc, m, xa + 1, y) ? 0.0 : Ea, w = is_dir(bc, m, xa - 1, y) ? 0.0 : Eb_w;
+        const double nn = is_dir(bc, m, xa, y + 1) ? 0.0 : Na, s = is_dir(bc, m, xa, y - 1) ? 0.0 : Nma;
+        t = -(e * z0b + w * z0b_w + nn * zpa + s * zma);
+      }
+    } else {  // red at xb
+      if (xb >= 0 && xb <= m && y >= 0 && y <= m && !is_dir(bc, m, xb, y)) {
+        const double e = is_dir(bc, m, xb + 1, y) ? 0.0 : Eb, w = is_dir(bc, m, xb - 1, y) ? 0.0 : Ea;
+        const double nn = is_dir(bc, m, xb, y + 1) ? 0.0 : Nb, s = is_dir(bc, m, xb, y - 1) ? 0.0 : Nmb;
+        t = -(e * z0a_e + w * z0a + nn * zpb + s * zmb);
+      }
+    }
+    return t;
+  };
+  // fine rows y = 2J0−1 … 2J1−1; state: k, z rows y−1, y; N of row y−1
+  const int ys = 2 * J0 - 1;
+  double kma = ldv(kb, xa, ys - 1, n0), kmb = ldv(kb, xb, ys - 1, n0);
+  double k0a = ldv(kb, xa, ys, n0), k0b = ldv(kb, xb, ys, n0);
+  double zma = ldv(zb, xa, ys - 1, n0), zmb = ldv(zb, xb, ys - 1, n0);
+  double z0a = ldv(zb, xa, ys, n0), z0b = ldv(zb, xb, ys, n0);
+  double Nma, Nmb;
+  {
+    double Ea, Eb;
+    edges2(0.0, 0.0, kma, kmb, k0a, k0b, ys - 1, Ea, Eb, Nma, Nmb);
   }
-  rc[(int64_t)b * gc.N + (int64_t)J * gc.n0 + I] = acc;
+  double t_prev = 0.0, t_even = 0.0;  // t at (xb, 2J−1) and (xa, 2J)
+  double* rcb = rc + (int64_t)b * gc.N;
+  for (int y = ys; y <= 2 * J1 - 1; ++y) {
+    const double kpa = ldv(kb, xa, y + 1, n0), kpb = ldv(kb, xb, y + 1, n0);
+    const double zpa = ldv(zb, xa, y + 1, n0), zpb = ldv(zb, xb, y + 1, n0);
+    double Ea, Eb, Na, Nb;
+    edges2(kma, kmb, k0a, k0b, kpa, kpb, y, Ea, Eb, Na, Nb);
+    const double t = t_red(y, Ea, Eb, Na, Nb, Nma, Nmb, zma, zmb, z0a, z0b, zpa, zpb);
+    if ((y & 1) == 0) {
+      t_even = t;
+    } else {
+      const double t_w = shup(t_prev);  // t at (xa−1, 2J−1): previous lane's xb
+      const int J = (y - 1) >> 1;       // y = 2J+1
+      if (J >= J0 && J < J1 && outI) {
+        const double v = is_dir(bc, mc, I, J) ? 0.0 : t_even + 0.5 * (t + t_w);
+        rcb[(int64_t)J * gc.n0 + I] = v;
+      }
+      t_prev = t;
+    }
+    kma = k0a; kmb = k0b; k0a = kpa; k0b = kpb;
+    zma = z0a; zmb = z0b; z0a = zpa; z0b = zpb;
+    Nma = Na; Nmb = Nb;
+  }
 }
 
-// ---- prolongation + post-smoother (black then red), on level 0 also <r, z> → β ------------------------
-__global__ void __launch_bounds__(TT) smooth_up_kernel(Geo g, Geo gc, int bc,
+// ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
+__global__ void __launch_bounds__(MT) smooth_up_kernel(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ k,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
@@ -514,60 +546,44 @@ __global__ void __launch_bounds__(TT) smooth_up_kernel(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ zc, int finest,
                                                        double* scal, int* flags, double2* partial,
                                                        int maxp, unsigned* counter) {
-  TILE_PROLOGUE
-  constexpr int W2 = TX + 4, H2 = TY + 4, W1 = TX + 2, H1 = TY + 2;
-  constexpr int WC = TX / 2 + 3, HC = TY / 2 + 3;
-  __shared__ double ks[H2 * W2], zp[H2 * W2], rs[H1 * W1], zb[H1 * W1], zcs[HC * WC], es[H2 * W2],
-      ns[H2 * W2];
-  const int cx0 = x0 / 2 - 1, cy0 = y0 / 2 - 1;
-  stage(ks, W2, H2, k + off, x0 - 2, y0 - 2, n0);
-  stage(zp, W2, H2, z + off, x0 - 2, y0 - 2, n0);
-  stage(rs, W1, H1, r + off, x0 - 1, y0 - 1, n0);
-  stage(zcs, WC, HC, zc + (int64_t)b * gc.N, cx0, cy0, gc.n0);
-  stage_wait();
-  build_edges(ks, es, ns, W2, H2, x0 - 2, y0 - 2, m);
-  // red nodes of the 2-halo region after prolongation: z_red + P zc (black entries unused)
-  for (int idx = threadIdx.x; idx < W2 * H2; idx += TT) {
-    const int ly = idx / W2, lx = idx - ly * W2;
-    const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
-    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0 && ((gx + gy) & 1) == 0) {
-      auto Zc = [&](int I, int J) { return zcs[(J - cy0) * WC + (I - cx0)]; };
-      double pz;
-      if ((gx & 1) == 0) pz = Zc(gx >> 1, gy >> 1);                                   // even-even
-      else pz = 0.5 * (Zc((gx - 1) >> 1, (gy - 1) >> 1) + Zc((gx + 1) >> 1, (gy + 1) >> 1));  // odd-odd
-      zp[idx] += pz;
-    }
-  }
-  __syncthreads();
-  // black nodes of the 1-halo region: z_b = (r − Σ A z_red)/D
-  for (int idx = threadIdx.x; idx < W1 * H1; idx += TT) {
-    const int ly = idx / W1, lx = idx - ly * W1;
-    const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-    double v = 0.0;
-    if (gx >= 0 && gx < n0 && gy >= 0 && gy < n0 && ((gx + gy) & 1) == 1) {
-      const Sten st = sten_edges(es, ns, W2, lx + 1, ly + 1, gx, gy, m, bc);
-      const int c = (ly + 1) * W2 + lx + 1;
-      v = (rs[idx] - (st.e * zp[c + 1] + st.w * zp[c - 1] + st.n * zp[c + W2] + st.s * zp[c - W2])) / st.d;
-    }
-    zb[idx] = v;
-  }
-  __syncthreads();
+  MARCH_PROLOGUE(2)
+  const double *kb = k + off, *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
+  const int nc0 = gc.n0;
+  // red node after prolongation: z_red + P zc (fem.cpp:144-165); 0 on black/out-of-grid nodes
+  auto ZP = [&](int y) {
+    if (((gx + y) & 1) != 0 || (unsigned)gx >= (unsigned)n0 || (unsigned)y >= (unsigned)n0) return 0.0;
+    const double a = __ldg(zcb + (int64_t)(y >> 1) * nc0 + (gx >> 1));
+    const double pz = (gx & 1) == 0 ? a : 0.5 * (a + __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + ((gx + 1) >> 1)));
+    return __ldg(zbp + (int64_t)y * n0 + gx) + pz;
+  };
+  double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
+  double zpa = ZP(y0 - 2), zpb = ZP(y0 - 1);
+  double Nt, Ed;
+  edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
+  double r0 = 0.0, zbm = 0.0, zb0 = 0.0;
+  Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
   double rz = 0.0;
-#pragma unroll
-  for (int q = 0; q < TY / 8; ++q) {
-    const int ly = ty0 + 8 * q, gx = x0 + tx, gy = y0 + ly;
-    if (gx < n0 && gy < n0) {
-      const int c1 = (ly + 1) * W1 + tx + 1;
-      double zv;
-      if (((gx + gy) & 1) == 0) {
-        const Sten st = sten_edges(es, ns, W2, tx + 2, ly + 2, gx, gy, m, bc);
-        zv = (rs[c1] - (st.e * zb[c1 + 1] + st.w * zb[c1 - 1] + st.n * zb[c1 + W1] + st.s * zb[c1 - W1])) / st.d;
-      } else {
-        zv = zb[c1];
-      }
-      z_out[off + (int64_t)gy * n0 + gx] = zv;
-      rz = fma(rs[c1], zv, rz);
+  for (int t = y0 - 2; t < y1; ++t) {
+    const double kc = ldv(kb, gx, t + 2, n0);
+    const double zpc = ZP(t + 2);
+    const double r1 = ldv(rb, gx, t + 1, n0);
+    double E1, N1;
+    edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
+    const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
+    const double pe = shdn(zpb), pw = shup(zpb);
+    const double zbp1 = (((gx + t + 1) & 1) == 1)
+                            ? (r1 - (st1.e * pe + st1.w * pw + st1.n * zpc + st1.s * zpa)) * rcp64(st1.d)
+                            : 0.0;
+    const double be = shdn(zb0), bw = shup(zb0);
+    if (t >= y0 && outx) {
+      const double zv = (((gx + t) & 1) == 0)
+                            ? (r0 - (st0.e * be + st0.w * bw + st0.n * zbp1 + st0.s * zbm)) * rcp64(st0.d)
+                            : zb0;
+      z_out[off + (int64_t)t * n0 + gx] = zv;
+      rz = fma(r0, zv, rz);
     }
+    ka = kb1; kb1 = kc; zpa = zpb; zpb = zpc; Nt = N1;
+    r0 = r1; zbm = zb0; zb0 = zbp1; st0 = st1;
   }
   if (!finest) return;
   double t0, t1;
@@ -719,8 +735,16 @@ __global__ void level_sums_kernel(const double* __restrict__ qf, const double* _
 }
 
 inline int nblocks(int64_t N) { return (int)((N + NT - 1) / NT); }
+inline int march_strips(int m, int hx) { return (m + 1 + (32 - 2 * hx) - 1) / (32 - 2 * hx); }
+inline dim3 march_grid(int m, int hx, int B) {
+  return dim3((unsigned)((march_strips(m, hx) + MW - 1) / MW), (unsigned)((m + 1 + LY - 1) / LY), (unsigned)B);
+}
+inline dim3 restrict_grid(int mc, int B) {
+  return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + LYC - 1) / LYC), (unsigned)B);
+}
 inline int64_t tile_parts(int m) {
-  return (int64_t)((m + 1 + TX - 1) / TX) * ((m + 1 + TY - 1) / TY);
+  const dim3 a = march_grid(m, 1, 1), b = march_grid(m, 2, 1);
+  return std::max<int64_t>((int64_t)a.x * a.y, (int64_t)b.x * b.y);
 }
 
 }  // namespace
@@ -798,12 +822,6 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
 namespace {
 
 Geo geo_of(const SolverLevel& L) { return Geo{L.m, L.m + 1, L.N}; }
-dim3 tile_grid(const SolverLevel& L, int B) {
-  return dim3((unsigned)((L.m + 1 + TX - 1) / TX), (unsigned)((L.m + 1 + TY - 1) / TY), (unsigned)B);
-}
-dim3 ctile_grid(const SolverLevel& C, int B) {
-  return dim3((unsigned)((C.m + 1 + CXT - 1) / CXT), (unsigned)((C.m + 1 + CYT - 1) / CYT), (unsigned)B);
-}
 
 // Preconditioner z = M r on level 0. With `fused_down` the level-0 pre-smoother already ran
 // inside pcg_update_down (z holds the pre-smoothed correction).
@@ -827,10 +845,10 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     const SolverLevel& C = w.lev[l + 1];
     if (l > 0 || !fused_down) {
       KScope ks(ctx, "mg_smooth_down");
-      smooth_down_kernel<<<tile_grid(L, B), TT, 0, st>>>(geo_of(L), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, w.flags);
+      smooth_down_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, w.flags);
     }
     KScope ks(ctx, "mg_restrict");
-    restrict_kernel<<<ctile_grid(C, B), TT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, C.r, w.flags);
+    restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, C.r, w.flags);
   }
   {
     const SolverLevel& C = w.lev[w.nlev - 1];
@@ -841,7 +859,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     KScope ks(ctx, "mg_smooth_up");
-    smooth_up_kernel<<<tile_grid(L, B), TT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, L.z2, C.z2,
+    smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, L.z2, C.z2,
                                                      l == 0 ? 1 : 0, w.scal, w.flags, part,
                                                      w.max_parts, w.counter);
   }
@@ -905,13 +923,13 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
     }
     {
       KScope ks(ctx, "pcg_apply");
-      pcg_apply_kernel<<<tile_grid(L0, B), TT, 0, st>>>(g0, bc, L0.k, L0.z2, p_old, p_new, w.scal, w.flags,
+      pcg_apply_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(g0, bc, L0.k, L0.z2, p_old, p_new, w.scal, w.flags,
                                                         part, w.max_parts, w.counter);
     }
     {
       KScope ks(ctx, "pcg_update_down");
       double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
-      pcg_update_down_kernel<<<tile_grid(L0, B), TT, 0, st>>>(g0, bc, prob->tol, L0.k, p_new, w.u, w.r_cur,
+      pcg_update_down_kernel<<<march_grid(L0.m, 2, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, p_new, w.u, w.r_cur,
                                                               r_next, L0.z, w.scal, w.flags, part, w.max_parts,
                                                               w.counter, w.n_active, w.hist, w.hist_cap);
     }

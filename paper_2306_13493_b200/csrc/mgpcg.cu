@@ -324,9 +324,13 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
   double Nm, Ed;
   edges_row(0.0, km, k0, gx, y0 - 1, m, Ed, Nm);
   double pap = 0.0;
+  // row y+1 loaded one iteration ahead as raw values (combined only when used)
+  double kq = ldv(kb, gx, y0 + 1, n0), zq = ldv(zb, gx, y0 + 1, n0), oq = first ? 0.0 : ldv(pb, gx, y0 + 1, n0);
   for (int y = y0; y < y1; ++y) {
-    const double kp = ldv(kb, gx, y + 1, n0);
-    const double pp = P(y + 1);
+    const double kp = kq, pp = first ? zq : fma(beta, oq, zq);
+    kq = ldv(kb, gx, y + 2, n0);
+    zq = ldv(zb, gx, y + 2, n0);
+    oq = first ? 0.0 : ldv(pb, gx, y + 2, n0);
     double E, N;
     edges_row(km, k0, kp, gx, y, m, E, N);
     const Sten st = sten_row(E, N, Nm, gx, y, m, bc);
@@ -364,10 +368,12 @@ __global__ void __launch_bounds__(MT) pcg_update_down_kernel(
   double rn0 = 0.0, zrm = 0.0, zr0 = 0.0;
   Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
   double rr = 0.0;
+  double kq = ldv(kb, gx, y0, n0), pq = ldv(pb, gx, y0, n0), rq = ldv(rb, gx, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
-    const double kc = ldv(kb, gx, t + 2, n0);
-    const double pc = ldv(pb, gx, t + 2, n0);
-    const double r1 = ldv(rb, gx, t + 1, n0);
+    const double kc = kq, pc = pq, r1 = rq;  // rows t+2 / t+1, prefetched one iteration ahead
+    kq = ldv(kb, gx, t + 3, n0);
+    pq = ldv(pb, gx, t + 3, n0);
+    rq = ldv(rb, gx, t + 2, n0);
     double E1, N1;
     edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
     const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
@@ -422,9 +428,11 @@ __global__ void __launch_bounds__(MT) smooth_down_kernel(Geo g, int bc, const do
   edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
   double r0 = 0.0, zrm = 0.0, zr0 = 0.0;
   Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
+  double kq = ldv(kb, gx, y0, n0), rq = ldv(rb, gx, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
-    const double kc = ldv(kb, gx, t + 2, n0);
-    const double r1 = ldv(rb, gx, t + 1, n0);
+    const double kc = kq, r1 = rq;  // prefetched one iteration ahead
+    kq = ldv(kb, gx, t + 3, n0);
+    rq = ldv(rb, gx, t + 2, n0);
     double E1, N1;
     edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
     const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
@@ -514,9 +522,14 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
   }
   double t_prev = 0.0, t_even = 0.0;  // t at (xb, 2J−1) and (xa, 2J)
   double* rcb = rc + (int64_t)b * gc.N;
+  double kqa = ldv(kb, xa, ys + 1, n0), kqb = ldv(kb, xb, ys + 1, n0);
+  double zqa = ldv(zb, xa, ys + 1, n0), zqb = ldv(zb, xb, ys + 1, n0);
   for (int y = ys; y <= 2 * J1 - 1; ++y) {
-    const double kpa = ldv(kb, xa, y + 1, n0), kpb = ldv(kb, xb, y + 1, n0);
-    const double zpa = ldv(zb, xa, y + 1, n0), zpb = ldv(zb, xb, y + 1, n0);
+    const double kpa = kqa, kpb = kqb, zpa = zqa, zpb = zqb;  // row y+1, prefetched
+    kqa = ldv(kb, xa, y + 2, n0);
+    kqb = ldv(kb, xb, y + 2, n0);
+    zqa = ldv(zb, xa, y + 2, n0);
+    zqb = ldv(zb, xb, y + 2, n0);
     double Ea, Eb, Na, Nb;
     edges2(kma, kmb, k0a, k0b, kpa, kpb, y, Ea, Eb, Na, Nb);
     const double t = t_red(y, Ea, Eb, Na, Nb, Nma, Nmb, zma, zmb, z0a, z0b, zpa, zpb);
@@ -550,12 +563,19 @@ __global__ void __launch_bounds__(MT) smooth_up_kernel(Geo g, Geo gc, int bc,
   const double *kb = k + off, *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
   const int nc0 = gc.n0;
   // red node after prolongation: z_red + P zc (fem.cpp:144-165); 0 on black/out-of-grid nodes
-  auto ZP = [&](int y) {
-    if (((gx + y) & 1) != 0 || (unsigned)gx >= (unsigned)n0 || (unsigned)y >= (unsigned)n0) return 0.0;
-    const double a = __ldg(zcb + (int64_t)(y >> 1) * nc0 + (gx >> 1));
-    const double pz = (gx & 1) == 0 ? a : 0.5 * (a + __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + ((gx + 1) >> 1)));
-    return __ldg(zbp + (int64_t)y * n0 + gx) + pz;
+  struct ZRaw {
+    double z, a, c;
   };
+  auto ZL = [&](int y) {  // raw loads of z_red and the coarse values its prolongation needs
+    ZRaw v{0.0, 0.0, 0.0};
+    if (((gx + y) & 1) != 0 || (unsigned)gx >= (unsigned)n0 || (unsigned)y >= (unsigned)n0) return v;
+    v.z = __ldg(zbp + (int64_t)y * n0 + gx);
+    v.a = __ldg(zcb + (int64_t)(y >> 1) * nc0 + (gx >> 1));
+    if (gx & 1) v.c = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + ((gx + 1) >> 1));
+    return v;
+  };
+  auto ZC = [&](const ZRaw& v) { return v.z + ((gx & 1) == 0 ? v.a : 0.5 * (v.a + v.c)); };
+  auto ZP = [&](int y) { return ZC(ZL(y)); };
   double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
   double zpa = ZP(y0 - 2), zpb = ZP(y0 - 1);
   double Nt, Ed;
@@ -563,10 +583,13 @@ __global__ void __launch_bounds__(MT) smooth_up_kernel(Geo g, Geo gc, int bc,
   double r0 = 0.0, zbm = 0.0, zb0 = 0.0;
   Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
   double rz = 0.0;
+  double kq = ldv(kb, gx, y0, n0), rq = ldv(rb, gx, y0 - 1, n0);
+  ZRaw zq = ZL(y0);
   for (int t = y0 - 2; t < y1; ++t) {
-    const double kc = ldv(kb, gx, t + 2, n0);
-    const double zpc = ZP(t + 2);
-    const double r1 = ldv(rb, gx, t + 1, n0);
+    const double kc = kq, zpc = ZC(zq), r1 = rq;  // raw rows loaded one iteration ahead
+    kq = ldv(kb, gx, t + 3, n0);
+    zq = ZL(t + 3);
+    rq = ldv(rb, gx, t + 2, n0);
     double E1, N1;
     edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
     const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
@@ -844,10 +867,10 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     if (l > 0 || !fused_down) {
-      KScope ks(ctx, "mg_smooth_down");
+      KScope ks(ctx, l == 0 ? "mg_smooth_down.L0" : "mg_smooth_down.Lc");
       smooth_down_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, w.flags);
     }
-    KScope ks(ctx, "mg_restrict");
+    KScope ks(ctx, l == 0 ? "mg_restrict.L0" : "mg_restrict.Lc");
     restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, C.r, w.flags);
   }
   {
@@ -858,7 +881,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
   for (int l = w.nlev - 2; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    KScope ks(ctx, "mg_smooth_up");
+    KScope ks(ctx, l == 0 ? "mg_smooth_up.L0" : "mg_smooth_up.Lc");
     smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, L.z2, C.z2,
                                                      l == 0 ? 1 : 0, w.scal, w.flags, part,
                                                      w.max_parts, w.counter);

@@ -77,15 +77,15 @@ def algorithmic_bytes_per_sample(W, n):
     return b
 
 
-# per-kernel compulsory HBM bytes per node of the grid the kernel runs on:
-# inputs read once + outputs written once, for one active sample
-KERNEL_BYTES_PER_NODE = {
-    "pcg_apply": 7 * 8,          # read z, p_old, D, E, N; write p_new, Ap
-    "pcg_update": 6 * 8,         # read u, p, r, Ap; write u, r
-    "mg_smooth_down": 5 * 8,     # read r, D, E, N; write z
-    "mg_smooth_up_black": 6 * 8,  # read r, z, D, E, N (+ coarse zc, 1/4); write z (half)
-    "mg_smooth_up_red": 6 * 8,
-    "mg_restrict": 5 * 8,        # read r, z, D, E, N (fine) per coarse-node neighbourhood
+# Per-kernel compulsory HBM bytes per node of the grid the kernel runs on: every
+# input read once and every output written once, for one active sample; `launches_per_iter`
+# says how the per-sample launch count follows from the PCG iteration count `it`.
+KERNEL_BYTES = {
+    # name: (bytes per node, launches per sample as a function of it)
+    "pcg_apply": (4 * 8, lambda it: it),              # read k, z, p_old; write p_new
+    "pcg_update_down": (7 * 8, lambda it: it),        # read k, p, r, u; write u, r, z
+    "mg_smooth_up.L0": (4 * 8 + 2, lambda it: it),    # read k, z, r, zc (1/4); write z
+    "mg_restrict.L0": (2 * 8 + 2, lambda it: it),     # read k, z; write rc (1/4)
 }
 
 
@@ -298,23 +298,33 @@ def main():
         ms = float(t.item())
     samples = args.steps * B * world
     value = samples / (ms / 1000.0)
+    iters_timed = list(iters_total)
 
-    # roofline of the dominant kernel (compulsory bytes / its event-timed duration)
+    # roofline of the dominant kernel: compulsory bytes / its CUDA-event time on the ctx stream
     hbm, hbm_kind = peaks()
-    dom = max(kstats.items(), key=lambda kv: kv[1][1])
-    dom_name = dom[0]
-    base = dom_name.split("@")[0]
-    roof = None
-    if base in ("pcg_apply", "pcg_update"):
-        nodes_f, nodes_c = (m + 1) ** 2, (m // 2 + 1) ** 2
-        grid_nodes = nodes_f if dom_name.endswith(f"@{m}") else nodes_c
-        sample_iters = iters_total[0] if dom_name.endswith(f"@{m}") else iters_total[1]
-        alg_bytes = KERNEL_BYTES_PER_NODE[base] * grid_nodes * sample_iters
-        launches, tot_ms = dom[1]
-        achieved = alg_bytes / (tot_ms / 1000.0) / 1e9
-        roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind,
-                "alg_bytes_per_launch": alg_bytes / max(launches, 1), "avg_launch_ms": tot_ms / max(launches, 1)}
+    dom_name, (dom_launches, dom_ms) = max(kstats.items(), key=lambda kv: kv[1][1])
+    base, _, grid_tag = dom_name.partition("@")
+    roof = {"kernel": dom_name, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s",
+            "frac": None, "traffic": None, "peak_kind": hbm_kind}
+    if base in KERNEL_BYTES and grid_tag:
+        mg = int(grid_tag)
+        sample_iters = iters_total[0] if mg == m else iters_total[1]
+        per_node, launches_of = KERNEL_BYTES[base]
+        alg_bytes = per_node * (mg + 1) ** 2 * launches_of(sample_iters)
+        achieved = alg_bytes / (dom_ms / 1000.0) / 1e9
+        roof.update(achieved=achieved, frac=achieved / hbm, alg_bytes_total=alg_bytes,
+                    launches=dom_launches, avg_launch_ms=dom_ms / max(dom_launches, 1),
+                    alg_bytes_per_launch=alg_bytes / max(dom_launches, 1),
+                    bytes_per_node=per_node, sample_launches=launches_of(sample_iters))
+    # every classified kernel's achieved bandwidth (same accounting), for DESIGN.md
+    per_kernel = {}
+    for name, (nl, tms) in kstats.items():
+        b_, _, g_ = name.partition("@")
+        if b_ in KERNEL_BYTES and g_ and tms > 0:
+            mg = int(g_)
+            it_ = iters_total[0] if mg == m else iters_total[1]
+            by = KERNEL_BYTES[b_][0] * (mg + 1) ** 2 * KERNEL_BYTES[b_][1](it_)
+            per_kernel[name] = round(by / (tms / 1000.0) / 1e9, 1)
     n = lev.n
     b_sample = algorithmic_bytes_per_sample(W, n)
     pipeline = {"basis": "SURVEY 8(d) B per coupled sample", "bytes_per_sample": b_sample,
@@ -377,9 +387,9 @@ def main():
                        "l2": "inputs larger than L2 (>= 40 GB touched per step)" if m >= 1024 else
                        "per-step working set exceeds L2 (batch)",
                        "setup_s": round(t_setup, 2),
-                       "mean_iters_fine": iters_total[0] / (args.steps * B),
-                       "mean_iters_coarse": iters_total[1] / (args.steps * B) if W["coupled"] else None},
-            "roofline": roof, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+                       "mean_iters_fine": iters_timed[0] / (args.steps * B),
+                       "mean_iters_coarse": iters_timed[1] / (args.steps * B) if W["coupled"] else None},
+            "roofline": roof, "kernel_gbs": per_kernel, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": ck,
             "kernels_ms": {k: round(v[1], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])},
         }

@@ -36,6 +36,8 @@ def build(ref: bool = True) -> None:
     targets = ["oracle"]
     if ref and os.path.isdir("/root/reference/proj/src"):
         targets.append("ref")
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2306_13493_b200", "libosc_b200.so")):
+            targets.append("seam_demo")  # pristine reference + seam binding + C-ABI
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

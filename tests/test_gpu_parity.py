@@ -235,3 +235,17 @@ def test_mlmc_vs_reference(P, ctx, ref):
     for a, b in zip(rep.levels, lv):
         # same sample indices → near-identical moments, not just within CI
         assert abs(a.mean_y - b["mean_y"]) < 4 * np.sqrt(b["var_y"] / max(b["n"], 2)) + 1e-12
+
+
+def test_reference_seam_demo(P, ctx):
+    """The pristine reference's own make_level_plan / coupled_sample vs its run_level_draws seam
+    bound to the B200 C-ABI (integration/oscfield_gpu_seams.cpp), in one C++ program."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "seam_demo")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/seam_demo not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr

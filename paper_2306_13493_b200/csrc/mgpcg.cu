@@ -254,55 +254,86 @@ __device__ __forceinline__ double rcp64(double d) {
   return y;
 }
 
-// Raw edge weights of row y for this lane's column x from k rows y−1 (km), y (k0), y+1 (kp):
-// E couples (x,y)–(x+1,y), N couples (x,y)–(x,y+1). Triangle means in the reference's vertex
-// order, ·(1/3) instead of /3 (≤ 1 ulp per coefficient). Every lane must call (shuffles).
-__device__ __forceinline__ void edges_row(double km, double k0, double kp, int gx, int gy, int m,
-                                          double& E, double& N) {
+// ---- column-pair marching ------------------------------------------------------------------------
+// Lane l owns the column pair xa = 60·strip − 2 + 2l (even) and xb = xa + 1, so every row gives
+// each lane exactly one red and one black node: the red-black sweeps run without divergence and
+// every load instruction moves two independent rows' worth of work. Lanes 0 and 31 are the
+// 2-column x-halo; lanes 1..30 write.
+struct Pair {
+  double a, b;
+};
+
+__device__ __forceinline__ Pair ld2(const double* __restrict__ base, int xa, int y, int n0) {
+  return Pair{ldv(base, xa, y, n0), ldv(base, xa + 1, y, n0)};
+}
+
+// Edge weights of row y at both columns from k rows y−1, y, y+1 (edges_row per column).
+__device__ __forceinline__ void edges_pair(Pair km, Pair k0, Pair kp, int xa, int y, int m, Pair& E,
+                                           Pair& N) {
   constexpr double third = 1.0 / 3.0;
-  const double k0x1 = shdn(k0), kpx1 = shdn(kp), k0xm = shup(k0);
-  E = 0.0;
-  N = 0.0;
-  if (gx >= 0 && gx < m && gy >= 0 && gy <= m) {
-    const double lo = gy < m ? (k0 + k0x1 + kpx1) * third : 0.0;  // K_low(x, y)
-    const double up = gy > 0 ? (km + k0x1 + k0) * third : 0.0;    // K_up(x, y−1)
-    E = -0.5 * (lo + up);
+  const double k0a_e = shdn(k0.a), kpa_e = shdn(kp.a), k0b_w = shup(k0.b);  // k(xb+1,y), k(xb+1,y+1), k(xa−1,y)
+  const int xb = xa + 1;
+  E.a = E.b = N.a = N.b = 0.0;
+  if (y >= 0 && y <= m) {
+    if (xa >= 0 && xa < m)
+      E.a = -0.5 * ((y < m ? (k0.a + k0.b + kp.b) * third : 0.0) + (y > 0 ? (km.a + k0.b + k0.a) * third : 0.0));
+    if (xb >= 0 && xb < m)
+      E.b = -0.5 * ((y < m ? (k0.b + k0a_e + kpa_e) * third : 0.0) + (y > 0 ? (km.b + k0a_e + k0.b) * third : 0.0));
   }
-  if (gy >= 0 && gy < m && gx >= 0 && gx <= m) {
-    const double up = gx < m ? (k0 + kpx1 + kp) * third : 0.0;    // K_up(x, y)
-    const double lo = gx > 0 ? (k0xm + k0 + kp) * third : 0.0;    // K_low(x−1, y)
-    N = -0.5 * (up + lo);
+  if (y >= 0 && y < m) {
+    if (xa >= 0 && xa <= m)
+      N.a = -0.5 * ((xa < m ? (k0.a + kp.b + kp.a) * third : 0.0) + (xa > 0 ? (k0b_w + k0.a + kp.a) * third : 0.0));
+    if (xb >= 0 && xb <= m)
+      N.b = -0.5 * ((xb < m ? (k0.b + kpa_e + kp.b) * third : 0.0) + (xb > 0 ? (k0.a + k0.b + kp.b) * third : 0.0));
   }
 }
 
-// 5-point row at (gx, gy) from this row's E, N and the previous row's N (south coupling).
-// Out-of-grid and Dirichlet rows are identity. Every lane must call (shuffle).
-__device__ __forceinline__ Sten sten_row(double E, double N, double Nm, int gx, int gy, int m, int bc) {
-  const double W = shup(E);
+__device__ __forceinline__ Sten mk_sten(double E, double W, double N, double S, int x, int y, int m, int bc) {
   Sten st;
-  if (gx < 0 || gx > m || gy < 0 || gy > m || is_dir(bc, m, gx, gy)) {
+  if (x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y)) {
     st.d = 1.0;
     st.e = st.w = st.n = st.s = 0.0;
     return st;
   }
-  st.d = -(E + W + N + Nm);
-  st.e = is_dir(bc, m, gx + 1, gy) ? 0.0 : E;
-  st.w = is_dir(bc, m, gx - 1, gy) ? 0.0 : W;
-  st.n = is_dir(bc, m, gx, gy + 1) ? 0.0 : N;
-  st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : Nm;
+  st.d = -(E + W + N + S);
+  st.e = is_dir(bc, m, x + 1, y) ? 0.0 : E;
+  st.w = is_dir(bc, m, x - 1, y) ? 0.0 : W;
+  st.n = is_dir(bc, m, x, y + 1) ? 0.0 : N;
+  st.s = is_dir(bc, m, x, y - 1) ? 0.0 : S;
   return st;
 }
 
-#define MARCH_PROLOGUE(HX)                                              \
+struct Sten2 {
+  Sten a, b;
+};
+
+// 5-point rows at (xa, y) and (xb, y) from this row's E, N and the previous row's N.
+__device__ __forceinline__ Sten2 sten_pair(Pair E, Pair N, Pair Nm, int xa, int y, int m, int bc) {
+  const double Wa = shup(E.b);  // E(xa−1) lives in the previous lane's b column
+  return Sten2{mk_sten(E.a, Wa, N.a, Nm.a, xa, y, m, bc), mk_sten(E.b, E.a, N.b, Nm.b, xa + 1, y, m, bc)};
+}
+
+// Off-diagonal part Σ A(x,nb) v(nb) at both columns of row y from v rows y−1, y, y+1.
+__device__ __forceinline__ Pair offd_pair(const Sten2& st, Pair vm, Pair v0, Pair vp) {
+  const double va_e = shdn(v0.a), vb_w = shup(v0.b);
+  return Pair{st.a.e * v0.b + st.a.w * vb_w + st.a.n * vp.a + st.a.s * vm.a,
+              st.b.e * va_e + st.b.w * v0.a + st.b.n * vp.b + st.b.s * vm.b};
+}
+
+#define PAIR_PROLOGUE                                                   \
   const int b = blockIdx.z;                                             \
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                          \
   const int lane = threadIdx.x & 31;                                    \
   const int strip = blockIdx.x * MW + (threadIdx.x >> 5);               \
   const int m = g.m, n0 = g.n0;                                         \
-  const int gx = strip * (32 - 2 * (HX)) - (HX) + lane;                 \
-  const bool outx = lane >= (HX) && lane < 32 - (HX) && gx <= m;        \
+  const int xa = strip * 60 - 2 + 2 * lane, xb = xa + 1;                \
+  const bool outa = lane >= 1 && lane < 31 && xa <= m;                  \
+  const bool outb = lane >= 1 && lane < 31 && xb <= m;                  \
   const int y0 = blockIdx.y * LY, y1 = min(y0 + LY, n0);                \
   const int64_t off = (int64_t)b * g.N;
+
+// red column of row y: a (even xa) when y is even, b otherwise
+#define RED_IS_A(y) (((y) & 1) == 0)
 
 // ---- PCG: p = z + βp (p = z first), <p, A p> → α  (Ap itself is recomputed where needed) --------
 __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const double* __restrict__ k,
@@ -311,34 +342,39 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
                                                        double* __restrict__ p_new, double* scal,
                                                        int* flags, double2* partial, int maxp,
                                                        unsigned* counter) {
-  MARCH_PROLOGUE(1)
+  PAIR_PROLOGUE
   const bool first = flags[b * F_NFLAGS + F_FIRST] != 0;
   const double beta = scal[b * S_NSCAL + S_BETA];
   const double *kb = k + off, *zb = z + off, *pb = p_old + off;
-  auto P = [&](int y) {
-    const double zv = ldv(zb, gx, y, n0);
-    return first ? zv : fma(beta, ldv(pb, gx, y, n0), zv);
+  auto comb = [&](Pair zz, Pair oo) {
+    return first ? zz : Pair{fma(beta, oo.a, zz.a), fma(beta, oo.b, zz.b)};
   };
-  double km = ldv(kb, gx, y0 - 1, n0), k0 = ldv(kb, gx, y0, n0);
-  double pm = P(y0 - 1), p0 = P(y0);
-  double Nm, Ed;
-  edges_row(0.0, km, k0, gx, y0 - 1, m, Ed, Nm);
+  const Pair zero{0.0, 0.0};
+  Pair km = ld2(kb, xa, y0 - 1, n0), k0 = ld2(kb, xa, y0, n0);
+  Pair pm = comb(ld2(zb, xa, y0 - 1, n0), first ? zero : ld2(pb, xa, y0 - 1, n0));
+  Pair p0 = comb(ld2(zb, xa, y0, n0), first ? zero : ld2(pb, xa, y0, n0));
+  Pair Nm, Ed;
+  edges_pair(zero, km, k0, xa, y0 - 1, m, Ed, Nm);
+  Pair kq = ld2(kb, xa, y0 + 1, n0), zq = ld2(zb, xa, y0 + 1, n0);
+  Pair oq = first ? zero : ld2(pb, xa, y0 + 1, n0);
   double pap = 0.0;
-  // row y+1 loaded one iteration ahead as raw values (combined only when used)
-  double kq = ldv(kb, gx, y0 + 1, n0), zq = ldv(zb, gx, y0 + 1, n0), oq = first ? 0.0 : ldv(pb, gx, y0 + 1, n0);
   for (int y = y0; y < y1; ++y) {
-    const double kp = kq, pp = first ? zq : fma(beta, oq, zq);
-    kq = ldv(kb, gx, y + 2, n0);
-    zq = ldv(zb, gx, y + 2, n0);
-    oq = first ? 0.0 : ldv(pb, gx, y + 2, n0);
-    double E, N;
-    edges_row(km, k0, kp, gx, y, m, E, N);
-    const Sten st = sten_row(E, N, Nm, gx, y, m, bc);
-    const double pe = shdn(p0), pw = shup(p0);
-    const double ap = st.d * p0 + st.e * pe + st.w * pw + st.n * pp + st.s * pm;
-    if (outx) {
-      p_new[off + (int64_t)y * n0 + gx] = p0;
-      pap = fma(p0, ap, pap);
+    const Pair kp = kq, pp = comb(zq, oq);  // row y+1 (raw rows loaded one iteration ahead)
+    kq = ld2(kb, xa, y + 2, n0);
+    zq = ld2(zb, xa, y + 2, n0);
+    if (!first) oq = ld2(pb, xa, y + 2, n0);
+    Pair E, N;
+    edges_pair(km, k0, kp, xa, y, m, E, N);
+    const Sten2 st = sten_pair(E, N, Nm, xa, y, m, bc);
+    const Pair od = offd_pair(st, pm, p0, pp);
+    double* out = p_new + off + (int64_t)y * n0;
+    if (outa) {
+      out[xa] = p0.a;
+      pap = fma(p0.a, fma(st.a.d, p0.a, od.a), pap);
+    }
+    if (outb) {
+      out[xb] = p0.b;
+      pap = fma(p0.b, fma(st.b.d, p0.b, od.b), pap);
     }
     km = k0; k0 = kp; pm = p0; p0 = pp; Nm = N;
   }
@@ -352,48 +388,60 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
 // ---- PCG update fused with the level-0 pre-smoother:
 //   u += αp, r −= αAp (Ap recomputed from p), ‖r‖ → convergence,
 //   then z_red = r/D, z_black = (r − Σ A z_red)/D  (red-black GS from z = 0)
-__global__ void __launch_bounds__(MT) pcg_update_down_kernel(
+__global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
     int* n_active, double* hist, int hist_cap) {
-  MARCH_PROLOGUE(2)
+  PAIR_PROLOGUE
   const double alpha = scal[b * S_NSCAL + S_ALPHA];
   const double *kb = k + off, *pb = p + off, *rb = r + off;
-  // pipeline state for output row t: k/p rows t, t+1; N_t; r_new(t); z_red rows t−1, t; stencil(t)
-  double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
-  double pa = ldv(pb, gx, y0 - 2, n0), pb1 = ldv(pb, gx, y0 - 1, n0);
-  double Nt, Ed;
-  edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
-  double rn0 = 0.0, zrm = 0.0, zr0 = 0.0;
-  Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
+  const Pair zero{0.0, 0.0};
+  // state for output row t: k/p rows t, t+1; N_t; r_new(t); z_red rows t−1, t; stencil(t)
+  Pair ka = ld2(kb, xa, y0 - 2, n0), kb1 = ld2(kb, xa, y0 - 1, n0);
+  Pair pa = ld2(pb, xa, y0 - 2, n0), pb1 = ld2(pb, xa, y0 - 1, n0);
+  Pair Nt, Ed;
+  edges_pair(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  Pair rn0 = zero, zrm = zero, zr0 = zero;
+  Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's black column (all the output needs)
+  Pair kq = ld2(kb, xa, y0, n0), pq = ld2(pb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
   double rr = 0.0;
-  double kq = ldv(kb, gx, y0, n0), pq = ldv(pb, gx, y0, n0), rq = ldv(rb, gx, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
-    const double kc = kq, pc = pq, r1 = rq;  // rows t+2 / t+1, prefetched one iteration ahead
-    kq = ldv(kb, gx, t + 3, n0);
-    pq = ldv(pb, gx, t + 3, n0);
-    rq = ldv(rb, gx, t + 2, n0);
-    double E1, N1;
-    edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
-    const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
-    const double ap1 = st1.d * pb1 + st1.e * shdn(pb1) + st1.w * shup(pb1) + st1.n * pc + st1.s * pa;
-    const double rn1 = fma(-alpha, ap1, r1);
-    const double zrp = (((gx + t + 1) & 1) == 0) ? rn1 * rcp64(st1.d) : 0.0;
-    // output row t
-    const double ze = shdn(zr0), zw = shup(zr0);
-    if (t >= y0 && outx) {
-      const double zv = (((gx + t) & 1) == 0)
-                            ? zr0
-                            : (rn0 - (st0.e * ze + st0.w * zw + st0.n * zrp + st0.s * zrm)) * rcp64(st0.d);
-      const int64_t j = off + (int64_t)t * n0 + gx;
-      u[j] = fma(alpha, pa, u[j]);
-      r_out[j] = rn0;
-      z[j] = zv;
-      rr = fma(rn0, rn0, rr);
+    const Pair kc = kq, pc = pq, r1 = rq;  // rows t+2 / t+1, loaded one iteration ahead
+    kq = ld2(kb, xa, t + 3, n0);
+    pq = ld2(pb, xa, t + 3, n0);
+    rq = ld2(rb, xa, t + 2, n0);
+    Pair E1, N1;
+    edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
+    const Pair od1 = offd_pair(st1, pa, pb1, pc);
+    const Pair rn1{fma(-alpha, fma(st1.a.d, pb1.a, od1.a), r1.a), fma(-alpha, fma(st1.b.d, pb1.b, od1.b), r1.b)};
+    // z_red on row t+1 (the other column is black → 0)
+    const Pair zrp = RED_IS_A(t + 1) ? Pair{rn1.a * rcp64(st1.a.d), 0.0} : Pair{0.0, rn1.b * rcp64(st1.b.d)};
+    // output row t: black column = (r − Σ A z_red)/D, red column = z_red
+    const double zr0_e = shdn(zr0.a), zr0_w = shup(zr0.b);
+    Pair zv;
+    if (RED_IS_A(t))  // black at xb: east = next lane's xa, west = own xa
+      zv = Pair{zr0.a, (rn0.b - (sb0.e * zr0_e + sb0.w * zr0.a + sb0.n * zrp.b + sb0.s * zrm.b)) * rcp64(sb0.d)};
+    else              // black at xa: east = own xb, west = previous lane's xb
+      zv = Pair{(rn0.a - (sb0.e * zr0.b + sb0.w * zr0_w + sb0.n * zrp.a + sb0.s * zrm.a)) * rcp64(sb0.d), zr0.b};
+    if (t >= y0) {
+      const int64_t row = off + (int64_t)t * n0;
+      if (outa) {
+        u[row + xa] = fma(alpha, pa.a, u[row + xa]);
+        r_out[row + xa] = rn0.a;
+        z[row + xa] = zv.a;
+        rr = fma(rn0.a, rn0.a, rr);
+      }
+      if (outb) {
+        u[row + xb] = fma(alpha, pa.b, u[row + xb]);
+        r_out[row + xb] = rn0.b;
+        z[row + xb] = zv.b;
+        rr = fma(rn0.b, rn0.b, rr);
+      }
     }
     ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
-    rn0 = rn1; zrm = zr0; zr0 = zrp; st0 = st1;
+    rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
   }
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -418,34 +466,39 @@ __global__ void __launch_bounds__(MT) pcg_update_down_kernel(
 }
 
 // ---- pre-smoother from z = 0 (coarse levels; level 0 of the first V-cycle): red then black ------
-__global__ void __launch_bounds__(MT) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ z, const int* flags) {
-  MARCH_PROLOGUE(2)  // z_black at x needs D(x−1), i.e. E(x−2)
+  PAIR_PROLOGUE
   const double *kb = k + off, *rb = r + off;
-  double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
-  double Nt, Ed;
-  edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
-  double r0 = 0.0, zrm = 0.0, zr0 = 0.0;
-  Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
-  double kq = ldv(kb, gx, y0, n0), rq = ldv(rb, gx, y0 - 1, n0);
+  const Pair zero{0.0, 0.0};
+  Pair ka = ld2(kb, xa, y0 - 2, n0), kb1 = ld2(kb, xa, y0 - 1, n0);
+  Pair Nt, Ed;
+  edges_pair(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  Pair r0 = zero, zrm = zero, zr0 = zero;
+  Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};
+  Pair kq = ld2(kb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
-    const double kc = kq, r1 = rq;  // prefetched one iteration ahead
-    kq = ldv(kb, gx, t + 3, n0);
-    rq = ldv(rb, gx, t + 2, n0);
-    double E1, N1;
-    edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
-    const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
-    const double zrp = (((gx + t + 1) & 1) == 0) ? r1 * rcp64(st1.d) : 0.0;
-    const double ze = shdn(zr0), zw = shup(zr0);
-    if (t >= y0 && outx) {
-      const double zv = (((gx + t) & 1) == 0)
-                            ? zr0
-                            : (r0 - (st0.e * ze + st0.w * zw + st0.n * zrp + st0.s * zrm)) * rcp64(st0.d);
-      z[off + (int64_t)t * n0 + gx] = zv;
+    const Pair kc = kq, r1 = rq;
+    kq = ld2(kb, xa, t + 3, n0);
+    rq = ld2(rb, xa, t + 2, n0);
+    Pair E1, N1;
+    edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
+    const Pair zrp = RED_IS_A(t + 1) ? Pair{r1.a * rcp64(st1.a.d), 0.0} : Pair{0.0, r1.b * rcp64(st1.b.d)};
+    const double zr0_e = shdn(zr0.a), zr0_w = shup(zr0.b);
+    Pair zv;
+    if (RED_IS_A(t))
+      zv = Pair{zr0.a, (r0.b - (sb0.e * zr0_e + sb0.w * zr0.a + sb0.n * zrp.b + sb0.s * zrm.b)) * rcp64(sb0.d)};
+    else
+      zv = Pair{(r0.a - (sb0.e * zr0.b + sb0.w * zr0_w + sb0.n * zrp.a + sb0.s * zrm.a)) * rcp64(sb0.d), zr0.b};
+    if (t >= y0) {
+      double* out = z + off + (int64_t)t * n0;
+      if (outa) out[xa] = zv.a;
+      if (outb) out[xb] = zv.b;
     }
     ka = kb1; kb1 = kc; Nt = N1;
-    r0 = r1; zrm = zr0; zr0 = zrp; st0 = st1;
+    r0 = r1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
   }
 }
 
@@ -551,7 +604,7 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
 }
 
 // ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
-__global__ void __launch_bounds__(MT) smooth_up_kernel(Geo g, Geo gc, int bc,
+__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ k,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
@@ -559,54 +612,76 @@ __global__ void __launch_bounds__(MT) smooth_up_kernel(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ zc, int finest,
                                                        double* scal, int* flags, double2* partial,
                                                        int maxp, unsigned* counter) {
-  MARCH_PROLOGUE(2)
+  PAIR_PROLOGUE
   const double *kb = k + off, *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
   const int nc0 = gc.n0;
-  // red node after prolongation: z_red + P zc (fem.cpp:144-165); 0 on black/out-of-grid nodes
+  const Pair zero{0.0, 0.0};
+  // Red node of row y after prolongation: z_red + P zc (fem.cpp:144-165). Row y even: red at xa
+  // (even, even) → zc(xa/2, y/2). Row y odd: red at xb (odd, odd) → ½[zc(xa/2, (y−1)/2) +
+  // zc(xa/2+1, (y+1)/2)]. Raw values are loaded one row ahead and combined when used.
   struct ZRaw {
-    double z, a, c;
+    double z, c0, c1;
   };
-  auto ZL = [&](int y) {  // raw loads of z_red and the coarse values its prolongation needs
+  const int I = xa >> 1;
+  auto ZL = [&](int y) {
     ZRaw v{0.0, 0.0, 0.0};
-    if (((gx + y) & 1) != 0 || (unsigned)gx >= (unsigned)n0 || (unsigned)y >= (unsigned)n0) return v;
-    v.z = __ldg(zbp + (int64_t)y * n0 + gx);
-    v.a = __ldg(zcb + (int64_t)(y >> 1) * nc0 + (gx >> 1));
-    if (gx & 1) v.c = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + ((gx + 1) >> 1));
+    if ((unsigned)y >= (unsigned)n0) return v;
+    if (RED_IS_A(y)) {
+      if ((unsigned)xa < (unsigned)n0) {
+        v.z = __ldg(zbp + (int64_t)y * n0 + xa);
+        v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
+      }
+    } else if ((unsigned)xb < (unsigned)n0) {
+      v.z = __ldg(zbp + (int64_t)y * n0 + xb);
+      v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
+      v.c1 = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + I + 1);
+    }
     return v;
   };
-  auto ZC = [&](const ZRaw& v) { return v.z + ((gx & 1) == 0 ? v.a : 0.5 * (v.a + v.c)); };
-  auto ZP = [&](int y) { return ZC(ZL(y)); };
-  double ka = ldv(kb, gx, y0 - 2, n0), kb1 = ldv(kb, gx, y0 - 1, n0);
-  double zpa = ZP(y0 - 2), zpb = ZP(y0 - 1);
-  double Nt, Ed;
-  edges_row(0.0, ka, kb1, gx, y0 - 2, m, Ed, Nt);
-  double r0 = 0.0, zbm = 0.0, zb0 = 0.0;
-  Sten st0{1.0, 0.0, 0.0, 0.0, 0.0};
-  double rz = 0.0;
-  double kq = ldv(kb, gx, y0, n0), rq = ldv(rb, gx, y0 - 1, n0);
+  auto ZC = [&](const ZRaw& v, int y) {  // the row's pair: red column prolonged, black column 0
+    return RED_IS_A(y) ? Pair{v.z + v.c0, 0.0} : Pair{0.0, v.z + 0.5 * (v.c0 + v.c1)};
+  };
+  Pair ka = ld2(kb, xa, y0 - 2, n0), kb1 = ld2(kb, xa, y0 - 1, n0);
+  Pair zpa = ZC(ZL(y0 - 2), y0 - 2), zpb = ZC(ZL(y0 - 1), y0 - 1);
+  Pair Nt, Ed;
+  edges_pair(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  Pair r0 = zero, zbm = zero, zb0 = zero;
+  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
+  Pair kq = ld2(kb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
   ZRaw zq = ZL(y0);
+  double rz = 0.0;
   for (int t = y0 - 2; t < y1; ++t) {
-    const double kc = kq, zpc = ZC(zq), r1 = rq;  // raw rows loaded one iteration ahead
-    kq = ldv(kb, gx, t + 3, n0);
+    const Pair kc = kq, r1 = rq, zpc = ZC(zq, t + 2);
+    kq = ld2(kb, xa, t + 3, n0);
     zq = ZL(t + 3);
-    rq = ldv(rb, gx, t + 2, n0);
-    double E1, N1;
-    edges_row(ka, kb1, kc, gx, t + 1, m, E1, N1);
-    const Sten st1 = sten_row(E1, N1, Nt, gx, t + 1, m, bc);
-    const double pe = shdn(zpb), pw = shup(zpb);
-    const double zbp1 = (((gx + t + 1) & 1) == 1)
-                            ? (r1 - (st1.e * pe + st1.w * pw + st1.n * zpc + st1.s * zpa)) * rcp64(st1.d)
-                            : 0.0;
-    const double be = shdn(zb0), bw = shup(zb0);
-    if (t >= y0 && outx) {
-      const double zv = (((gx + t) & 1) == 0)
-                            ? (r0 - (st0.e * be + st0.w * bw + st0.n * zbp1 + st0.s * zbm)) * rcp64(st0.d)
-                            : zb0;
-      z_out[off + (int64_t)t * n0 + gx] = zv;
-      rz = fma(r0, zv, rz);
+    rq = ld2(rb, xa, t + 2, n0);
+    Pair E1, N1;
+    edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
+    // black column of row t+1: (r − Σ A z_red_prolonged)/D
+    const Pair odp = offd_pair(st1, zpa, zpb, zpc);
+    const Pair zbp1 = RED_IS_A(t + 1) ? Pair{0.0, (r1.b - odp.b) * rcp64(st1.b.d)}
+                                      : Pair{(r1.a - odp.a) * rcp64(st1.a.d), 0.0};
+    // output row t: red column = (r − Σ A z_black)/D, black column = z_black
+    const double zb0_e = shdn(zb0.a), zb0_w = shup(zb0.b);
+    Pair zv;
+    if (RED_IS_A(t))  // red at xa: east = own xb, west = previous lane's xb
+      zv = Pair{(r0.a - (sr0.e * zb0.b + sr0.w * zb0_w + sr0.n * zbp1.a + sr0.s * zbm.a)) * rcp64(sr0.d), zb0.b};
+    else              // red at xb: east = next lane's xa, west = own xa
+      zv = Pair{zb0.a, (r0.b - (sr0.e * zb0_e + sr0.w * zb0.a + sr0.n * zbp1.b + sr0.s * zbm.b)) * rcp64(sr0.d)};
+    if (t >= y0) {
+      double* out = z_out + off + (int64_t)t * n0;
+      if (outa) {
+        out[xa] = zv.a;
+        rz = fma(r0.a, zv.a, rz);
+      }
+      if (outb) {
+        out[xb] = zv.b;
+        rz = fma(r0.b, zv.b, rz);
+      }
     }
     ka = kb1; kb1 = kc; zpa = zpb; zpb = zpc; Nt = N1;
-    r0 = r1; zbm = zb0; zb0 = zbp1; st0 = st1;
+    r0 = r1; zbm = zb0; zb0 = zbp1; sr0 = RED_IS_A(t + 1) ? st1.a : st1.b;
   }
   if (!finest) return;
   double t0, t1;
@@ -758,9 +833,9 @@ __global__ void level_sums_kernel(const double* __restrict__ qf, const double* _
 }
 
 inline int nblocks(int64_t N) { return (int)((N + NT - 1) / NT); }
-inline int march_strips(int m, int hx) { return (m + 1 + (32 - 2 * hx) - 1) / (32 - 2 * hx); }
-inline dim3 march_grid(int m, int hx, int B) {
-  return dim3((unsigned)((march_strips(m, hx) + MW - 1) / MW), (unsigned)((m + 1 + LY - 1) / LY), (unsigned)B);
+inline int march_strips(int m) { return (m + 1 + 59) / 60; }  // 60 written columns per warp strip
+inline dim3 march_grid(int m, int /*hx*/, int B) {
+  return dim3((unsigned)((march_strips(m) + MW - 1) / MW), (unsigned)((m + 1 + LY - 1) / LY), (unsigned)B);
 }
 inline dim3 restrict_grid(int mc, int B) {
   return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + LYC - 1) / LYC), (unsigned)B);

@@ -233,7 +233,10 @@ __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing
 // of HBM instead of 24 B/node for stored D/E/N).
 constexpr int MW = 4;        // warps (strips) per CTA
 constexpr int MT = 32 * MW;  // threads per CTA
-constexpr int LY = 32;       // output rows per warp
+constexpr int LY = 32;       // output rows per warp on large grids
+// rows marched per warp: long chunks amortise the 2-row warm-up on large grids; short chunks
+// cut the serial row-latency chain (and add CTAs) on the small, latency-bound MG levels.
+__host__ __device__ __forceinline__ int rows_per_warp(int m) { return m >= 512 ? LY : (m >= 64 ? 16 : 8); }
 constexpr int LYC = 16;      // coarse output rows per warp (restriction)
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -329,7 +332,8 @@ __device__ __forceinline__ Pair offd_pair(const Sten2& st, Pair vm, Pair v0, Pai
   const int xa = strip * 60 - 2 + 2 * lane, xb = xa + 1;                \
   const bool outa = lane >= 1 && lane < 31 && xa <= m;                  \
   const bool outb = lane >= 1 && lane < 31 && xb <= m;                  \
-  const int y0 = blockIdx.y * LY, y1 = min(y0 + LY, n0);                \
+  const int ly = rows_per_warp(m);                                      \
+  const int y0 = blockIdx.y * ly, y1 = min(y0 + ly, n0);                \
   const int64_t off = (int64_t)b * g.N;
 
 // red column of row y: a (even xa) when y is even, b otherwise
@@ -405,12 +409,14 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
   Pair rn0 = zero, zrm = zero, zr0 = zero;
   Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's black column (all the output needs)
   Pair kq = ld2(kb, xa, y0, n0), pq = ld2(pb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
+  Pair uq = ld2(u + off, xa, y0 - 2, n0);
   double rr = 0.0;
   for (int t = y0 - 2; t < y1; ++t) {
-    const Pair kc = kq, pc = pq, r1 = rq;  // rows t+2 / t+1, loaded one iteration ahead
+    const Pair kc = kq, pc = pq, r1 = rq, u0 = uq;  // rows t+2 / t+1 / t, loaded one iteration ahead
     kq = ld2(kb, xa, t + 3, n0);
     pq = ld2(pb, xa, t + 3, n0);
     rq = ld2(rb, xa, t + 2, n0);
+    uq = ld2(u + off, xa, t + 1, n0);
     Pair E1, N1;
     edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
     const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
@@ -428,13 +434,13 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
     if (t >= y0) {
       const int64_t row = off + (int64_t)t * n0;
       if (outa) {
-        u[row + xa] = fma(alpha, pa.a, u[row + xa]);
+        u[row + xa] = fma(alpha, pa.a, u0.a);
         r_out[row + xa] = rn0.a;
         z[row + xa] = zv.a;
         rr = fma(rn0.a, rn0.a, rr);
       }
       if (outb) {
-        u[row + xb] = fma(alpha, pa.b, u[row + xb]);
+        u[row + xb] = fma(alpha, pa.b, u0.b);
         r_out[row + xb] = rn0.b;
         z[row + xb] = zv.b;
         rr = fma(rn0.b, rn0.b, rr);
@@ -835,7 +841,8 @@ __global__ void level_sums_kernel(const double* __restrict__ qf, const double* _
 inline int nblocks(int64_t N) { return (int)((N + NT - 1) / NT); }
 inline int march_strips(int m) { return (m + 1 + 59) / 60; }  // 60 written columns per warp strip
 inline dim3 march_grid(int m, int /*hx*/, int B) {
-  return dim3((unsigned)((march_strips(m) + MW - 1) / MW), (unsigned)((m + 1 + LY - 1) / LY), (unsigned)B);
+  const int ly = rows_per_warp(m);
+  return dim3((unsigned)((march_strips(m) + MW - 1) / MW), (unsigned)((m + 1 + ly - 1) / ly), (unsigned)B);
 }
 inline dim3 restrict_grid(int mc, int B) {
   return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + LYC - 1) / LYC), (unsigned)B);

@@ -243,7 +243,10 @@ constexpr unsigned FULL = 0xffffffffu;
 __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(FULL, v, 1); }
 __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(FULL, v, 1); }
 
+// Load one node; INT (interior warp-chunk) skips the bounds test.
+template <bool INT>
 __device__ __forceinline__ double ldv(const double* __restrict__ base, int gx, int gy, int n0) {
+  if (INT) return __ldg(base + (int64_t)gy * n0 + gx);
   return ((unsigned)gx < (unsigned)n0 && (unsigned)gy < (unsigned)n0)
              ? __ldg(base + (int64_t)gy * n0 + gx) : 0.0;
 }
@@ -266,15 +269,26 @@ struct Pair {
   double a, b;
 };
 
+template <bool INT>
 __device__ __forceinline__ Pair ld2(const double* __restrict__ base, int xa, int y, int n0) {
-  return Pair{ldv(base, xa, y, n0), ldv(base, xa + 1, y, n0)};
+  return Pair{ldv<INT>(base, xa, y, n0), ldv<INT>(base, xa + 1, y, n0)};
 }
 
-// Edge weights of row y at both columns from k rows y−1, y, y+1 (edges_row per column).
+// Edge weights of row y at both columns from k rows y−1, y, y+1. Triangle means in the
+// reference's vertex order with ·(1/3) instead of /3 (≤ 1 ulp per coefficient); each edge is
+// formed once, so both rows of A see the same double. INT: every edge of the pair is interior.
+template <bool INT>
 __device__ __forceinline__ void edges_pair(Pair km, Pair k0, Pair kp, int xa, int y, int m, Pair& E,
                                            Pair& N) {
   constexpr double third = 1.0 / 3.0;
   const double k0a_e = shdn(k0.a), kpa_e = shdn(kp.a), k0b_w = shup(k0.b);  // k(xb+1,y), k(xb+1,y+1), k(xa−1,y)
+  if (INT) {
+    E.a = -0.5 * ((k0.a + k0.b + kp.b) * third + (km.a + k0.b + k0.a) * third);
+    E.b = -0.5 * ((k0.b + k0a_e + kpa_e) * third + (km.b + k0a_e + k0.b) * third);
+    N.a = -0.5 * ((k0.a + kp.b + kp.a) * third + (k0b_w + k0.a + kp.a) * third);
+    N.b = -0.5 * ((k0.b + kpa_e + kp.b) * third + (k0.a + k0.b + kp.b) * third);
+    return;
+  }
   const int xb = xa + 1;
   E.a = E.b = N.a = N.b = 0.0;
   if (y >= 0 && y <= m) {
@@ -291,8 +305,17 @@ __device__ __forceinline__ void edges_pair(Pair km, Pair k0, Pair kp, int xa, in
   }
 }
 
+template <bool INT>
 __device__ __forceinline__ Sten mk_sten(double E, double W, double N, double S, int x, int y, int m, int bc) {
   Sten st;
+  if (INT) {  // interior node with interior neighbours: no Dirichlet elimination
+    st.d = -(E + W + N + S);
+    st.e = E;
+    st.w = W;
+    st.n = N;
+    st.s = S;
+    return st;
+  }
   if (x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y)) {
     st.d = 1.0;
     st.e = st.w = st.n = st.s = 0.0;
@@ -311,9 +334,10 @@ struct Sten2 {
 };
 
 // 5-point rows at (xa, y) and (xb, y) from this row's E, N and the previous row's N.
+template <bool INT>
 __device__ __forceinline__ Sten2 sten_pair(Pair E, Pair N, Pair Nm, int xa, int y, int m, int bc) {
   const double Wa = shup(E.b);  // E(xa−1) lives in the previous lane's b column
-  return Sten2{mk_sten(E.a, Wa, N.a, Nm.a, xa, y, m, bc), mk_sten(E.b, E.a, N.b, Nm.b, xa + 1, y, m, bc)};
+  return Sten2{mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc), mk_sten<INT>(E.b, E.a, N.b, Nm.b, xa + 1, y, m, bc)};
 }
 
 // Off-diagonal part Σ A(x,nb) v(nb) at both columns of row y from v rows y−1, y, y+1.
@@ -323,30 +347,58 @@ __device__ __forceinline__ Pair offd_pair(const Sten2& st, Pair vm, Pair v0, Pai
               st.b.e * va_e + st.b.w * v0.a + st.b.n * vp.b + st.b.s * vm.b};
 }
 
-#define PAIR_PROLOGUE                                                   \
-  const int b = blockIdx.z;                                             \
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                          \
-  const int lane = threadIdx.x & 31;                                    \
-  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);               \
-  const int m = g.m, n0 = g.n0;                                         \
-  const int xa = strip * 60 - 2 + 2 * lane, xb = xa + 1;                \
-  const bool outa = lane >= 1 && lane < 31 && xa <= m;                  \
-  const bool outb = lane >= 1 && lane < 31 && xb <= m;                  \
-  const int ly = rows_per_warp(m);                                      \
-  const int y0 = blockIdx.y * ly, y1 = min(y0 + ly, n0);                \
-  const int64_t off = (int64_t)b * g.N;
+struct PairCtx {
+  int b, lane, m, n0, xa, xb, y0, y1;
+  bool outa, outb;
+  int64_t off;
+};
+
+// Per-warp context; `interior` = every node this warp-chunk touches (rows y0−2 … y1+2, columns
+// xa(lane 0)−1 … xb(lane 31)+1) is an in-grid non-Dirichlet node with in-grid neighbours, so the
+// warp can run the branch-free body.
+#define PAIR_PROLOGUE                                                                   \
+  const int b = blockIdx.z;                                                             \
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                                          \
+  PairCtx c;                                                                            \
+  {                                                                                     \
+    const int lane = threadIdx.x & 31;                                                  \
+    const int strip = blockIdx.x * MW + (threadIdx.x >> 5);                             \
+    const int ly = rows_per_warp(g.m);                                                  \
+    c.b = b;                                                                            \
+    c.lane = lane;                                                                      \
+    c.m = g.m;                                                                          \
+    c.n0 = g.n0;                                                                        \
+    c.xa = strip * 60 - 2 + 2 * lane;                                                   \
+    c.xb = c.xa + 1;                                                                    \
+    c.outa = lane >= 1 && lane < 31 && c.xa <= g.m;                                     \
+    c.outb = lane >= 1 && lane < 31 && c.xb <= g.m;                                     \
+    c.y0 = blockIdx.y * ly;                                                             \
+    c.y1 = min(c.y0 + ly, g.n0);                                                        \
+    c.off = (int64_t)b * g.N;                                                           \
+  }                                                                                     \
+  const int strip0 = blockIdx.x * MW + (threadIdx.x >> 5);                              \
+  const bool interior = strip0 * 60 - 2 >= 2 && strip0 * 60 + 61 <= g.m - 2 &&          \
+                        c.y0 >= 3 && c.y1 <= g.m - 2;
+
+#define PAIR_UNPACK                                                                     \
+  const int b = c.b, m = c.m, n0 = c.n0, xa = c.xa, xb = c.xb, y0 = c.y0, y1 = c.y1;    \
+  const bool outa = c.outa, outb = c.outb;                                              \
+  const int64_t off = c.off;                                                            \
+  (void)b; (void)xb; (void)outa; (void)outb;
 
 // red column of row y: a (even xa) when y is even, b otherwise
 #define RED_IS_A(y) (((y) & 1) == 0)
 
 // ---- PCG: p = z + βp (p = z first), <p, A p> → α  (Ap itself is recomputed where needed) --------
-__global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const double* __restrict__ k,
+template <bool INT>
+__device__ __forceinline__ double pcg_apply_kernel_body(Geo g, int bc, const double* __restrict__ k,
                                                        const double* __restrict__ z,
                                                        const double* __restrict__ p_old,
                                                        double* __restrict__ p_new, double* scal,
                                                        int* flags, double2* partial, int maxp,
-                                                       unsigned* counter) {
-  PAIR_PROLOGUE
+                                                       unsigned* counter, const PairCtx& c) {
+  PAIR_UNPACK
+
   const bool first = flags[b * F_NFLAGS + F_FIRST] != 0;
   const double beta = scal[b * S_NSCAL + S_BETA];
   const double *kb = k + off, *zb = z + off, *pb = p_old + off;
@@ -354,22 +406,22 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
     return first ? zz : Pair{fma(beta, oo.a, zz.a), fma(beta, oo.b, zz.b)};
   };
   const Pair zero{0.0, 0.0};
-  Pair km = ld2(kb, xa, y0 - 1, n0), k0 = ld2(kb, xa, y0, n0);
-  Pair pm = comb(ld2(zb, xa, y0 - 1, n0), first ? zero : ld2(pb, xa, y0 - 1, n0));
-  Pair p0 = comb(ld2(zb, xa, y0, n0), first ? zero : ld2(pb, xa, y0, n0));
+  Pair km = ld2<INT>(kb, xa, y0 - 1, n0), k0 = ld2<INT>(kb, xa, y0, n0);
+  Pair pm = comb(ld2<INT>(zb, xa, y0 - 1, n0), first ? zero : ld2<INT>(pb, xa, y0 - 1, n0));
+  Pair p0 = comb(ld2<INT>(zb, xa, y0, n0), first ? zero : ld2<INT>(pb, xa, y0, n0));
   Pair Nm, Ed;
-  edges_pair(zero, km, k0, xa, y0 - 1, m, Ed, Nm);
-  Pair kq = ld2(kb, xa, y0 + 1, n0), zq = ld2(zb, xa, y0 + 1, n0);
-  Pair oq = first ? zero : ld2(pb, xa, y0 + 1, n0);
+  edges_pair<INT>(zero, km, k0, xa, y0 - 1, m, Ed, Nm);
+  Pair kq = ld2<INT>(kb, xa, y0 + 1, n0), zq = ld2<INT>(zb, xa, y0 + 1, n0);
+  Pair oq = first ? zero : ld2<INT>(pb, xa, y0 + 1, n0);
   double pap = 0.0;
   for (int y = y0; y < y1; ++y) {
     const Pair kp = kq, pp = comb(zq, oq);  // row y+1 (raw rows loaded one iteration ahead)
-    kq = ld2(kb, xa, y + 2, n0);
-    zq = ld2(zb, xa, y + 2, n0);
-    if (!first) oq = ld2(pb, xa, y + 2, n0);
+    kq = ld2<INT>(kb, xa, y + 2, n0);
+    zq = ld2<INT>(zb, xa, y + 2, n0);
+    if (!first) oq = ld2<INT>(pb, xa, y + 2, n0);
     Pair E, N;
-    edges_pair(km, k0, kp, xa, y, m, E, N);
-    const Sten2 st = sten_pair(E, N, Nm, xa, y, m, bc);
+    edges_pair<INT>(km, k0, kp, xa, y, m, E, N);
+    const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
     const Pair od = offd_pair(st, pm, p0, pp);
     double* out = p_new + off + (int64_t)y * n0;
     if (outa) {
@@ -382,6 +434,17 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
     }
     km = k0; k0 = kp; pm = p0; p0 = pp; Nm = N;
   }
+  return pap;
+}
+
+__global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const double* __restrict__ k,
+                                                       const double* __restrict__ z,
+                                                       const double* __restrict__ p_old,
+                                                       double* __restrict__ p_new, double* scal,
+                                                       int* flags, double2* partial, int maxp,
+                                                       unsigned* counter) {
+  PAIR_PROLOGUE
+  const double pap = interior ? pcg_apply_kernel_body<true>(g, bc, k, z, p_old, p_new, scal, flags, partial, maxp, counter, c) : pcg_apply_kernel_body<false>(g, bc, k, z, p_old, p_new, scal, flags, partial, maxp, counter, c);
   double t0, t1;
   if (reduce2_last(pap, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     scal[b * S_NSCAL + S_ALPHA] = scal[b * S_NSCAL + S_RZ] / t0;
@@ -392,34 +455,36 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
 // ---- PCG update fused with the level-0 pre-smoother:
 //   u += αp, r −= αAp (Ap recomputed from p), ‖r‖ → convergence,
 //   then z_red = r/D, z_black = (r − Σ A z_red)/D  (red-black GS from z = 0)
-__global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
+template <bool INT>
+__device__ __forceinline__ double pcg_update_down_kernel_body(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
-    int* n_active, double* hist, int hist_cap) {
-  PAIR_PROLOGUE
+    int* n_active, double* hist, int hist_cap, const PairCtx& c) {
+  PAIR_UNPACK
+
   const double alpha = scal[b * S_NSCAL + S_ALPHA];
   const double *kb = k + off, *pb = p + off, *rb = r + off;
   const Pair zero{0.0, 0.0};
   // state for output row t: k/p rows t, t+1; N_t; r_new(t); z_red rows t−1, t; stencil(t)
-  Pair ka = ld2(kb, xa, y0 - 2, n0), kb1 = ld2(kb, xa, y0 - 1, n0);
-  Pair pa = ld2(pb, xa, y0 - 2, n0), pb1 = ld2(pb, xa, y0 - 1, n0);
+  Pair ka = ld2<INT>(kb, xa, y0 - 2, n0), kb1 = ld2<INT>(kb, xa, y0 - 1, n0);
+  Pair pa = ld2<INT>(pb, xa, y0 - 2, n0), pb1 = ld2<INT>(pb, xa, y0 - 1, n0);
   Pair Nt, Ed;
-  edges_pair(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  edges_pair<INT>(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
   Pair rn0 = zero, zrm = zero, zr0 = zero;
   Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's black column (all the output needs)
-  Pair kq = ld2(kb, xa, y0, n0), pq = ld2(pb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
-  Pair uq = ld2(u + off, xa, y0 - 2, n0);
+  Pair kq = ld2<INT>(kb, xa, y0, n0), pq = ld2<INT>(pb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
+  Pair uq = ld2<INT>(u + off, xa, y0 - 2, n0);
   double rr = 0.0;
   for (int t = y0 - 2; t < y1; ++t) {
     const Pair kc = kq, pc = pq, r1 = rq, u0 = uq;  // rows t+2 / t+1 / t, loaded one iteration ahead
-    kq = ld2(kb, xa, t + 3, n0);
-    pq = ld2(pb, xa, t + 3, n0);
-    rq = ld2(rb, xa, t + 2, n0);
-    uq = ld2(u + off, xa, t + 1, n0);
+    kq = ld2<INT>(kb, xa, t + 3, n0);
+    pq = ld2<INT>(pb, xa, t + 3, n0);
+    rq = ld2<INT>(rb, xa, t + 2, n0);
+    uq = ld2<INT>(u + off, xa, t + 1, n0);
     Pair E1, N1;
-    edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
-    const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
+    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     const Pair od1 = offd_pair(st1, pa, pb1, pc);
     const Pair rn1{fma(-alpha, fma(st1.a.d, pb1.a, od1.a), r1.a), fma(-alpha, fma(st1.b.d, pb1.b, od1.b), r1.b)};
     // z_red on row t+1 (the other column is black → 0)
@@ -449,6 +514,18 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
     ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
     rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
   }
+  return rr;
+}
+
+__global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
+    Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
+    double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
+    double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
+    int* n_active, double* hist, int hist_cap) {
+  PAIR_PROLOGUE
+  // generic body only: the interior specialisation pushes this kernel past 128 registers (spills)
+  (void)interior;
+  const double rr = pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c);
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     const double rel = sqrt(t0) / scal[b * S_NSCAL + S_BNORM];
@@ -472,25 +549,27 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
 }
 
 // ---- pre-smoother from z = 0 (coarse levels; level 0 of the first V-cycle): red then black ------
-__global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
+template <bool INT>
+__device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const double* __restrict__ k,
                                                          const double* __restrict__ r,
-                                                         double* __restrict__ z, const int* flags) {
-  PAIR_PROLOGUE
+                                                         double* __restrict__ z, const int* flags, const PairCtx& c) {
+  PAIR_UNPACK
+
   const double *kb = k + off, *rb = r + off;
   const Pair zero{0.0, 0.0};
-  Pair ka = ld2(kb, xa, y0 - 2, n0), kb1 = ld2(kb, xa, y0 - 1, n0);
+  Pair ka = ld2<INT>(kb, xa, y0 - 2, n0), kb1 = ld2<INT>(kb, xa, y0 - 1, n0);
   Pair Nt, Ed;
-  edges_pair(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  edges_pair<INT>(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
   Pair r0 = zero, zrm = zero, zr0 = zero;
   Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};
-  Pair kq = ld2(kb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
+  Pair kq = ld2<INT>(kb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
     const Pair kc = kq, r1 = rq;
-    kq = ld2(kb, xa, t + 3, n0);
-    rq = ld2(rb, xa, t + 2, n0);
+    kq = ld2<INT>(kb, xa, t + 3, n0);
+    rq = ld2<INT>(rb, xa, t + 2, n0);
     Pair E1, N1;
-    edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
-    const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
+    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     const Pair zrp = RED_IS_A(t + 1) ? Pair{r1.a * rcp64(st1.a.d), 0.0} : Pair{0.0, r1.b * rcp64(st1.b.d)};
     const double zr0_e = shdn(zr0.a), zr0_w = shup(zr0.b);
     Pair zv;
@@ -505,7 +584,15 @@ __global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const
     }
     ka = kb1; kb1 = kc; Nt = N1;
     r0 = r1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
-  }
+  }  return 0.0;
+}
+
+__global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
+                                                         const double* __restrict__ r,
+                                                         double* __restrict__ z, const int* flags) {
+  PAIR_PROLOGUE
+  if (interior) smooth_down_kernel_body<true>(g, bc, k, r, z, flags, c);
+  else smooth_down_kernel_body<false>(g, bc, k, r, z, flags, c);
 }
 
 // ---- residual restriction rc = Pᵀ(r − A z) after the red-black pre-smoother (fem.cpp:168-195).
@@ -570,10 +657,10 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
   };
   // fine rows y = 2J0−1 … 2J1−1; state: k, z rows y−1, y; N of row y−1
   const int ys = 2 * J0 - 1;
-  double kma = ldv(kb, xa, ys - 1, n0), kmb = ldv(kb, xb, ys - 1, n0);
-  double k0a = ldv(kb, xa, ys, n0), k0b = ldv(kb, xb, ys, n0);
-  double zma = ldv(zb, xa, ys - 1, n0), zmb = ldv(zb, xb, ys - 1, n0);
-  double z0a = ldv(zb, xa, ys, n0), z0b = ldv(zb, xb, ys, n0);
+  double kma = ldv<false>(kb, xa, ys - 1, n0), kmb = ldv<false>(kb, xb, ys - 1, n0);
+  double k0a = ldv<false>(kb, xa, ys, n0), k0b = ldv<false>(kb, xb, ys, n0);
+  double zma = ldv<false>(zb, xa, ys - 1, n0), zmb = ldv<false>(zb, xb, ys - 1, n0);
+  double z0a = ldv<false>(zb, xa, ys, n0), z0b = ldv<false>(zb, xb, ys, n0);
   double Nma, Nmb;
   {
     double Ea, Eb;
@@ -581,14 +668,14 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
   }
   double t_prev = 0.0, t_even = 0.0;  // t at (xb, 2J−1) and (xa, 2J)
   double* rcb = rc + (int64_t)b * gc.N;
-  double kqa = ldv(kb, xa, ys + 1, n0), kqb = ldv(kb, xb, ys + 1, n0);
-  double zqa = ldv(zb, xa, ys + 1, n0), zqb = ldv(zb, xb, ys + 1, n0);
+  double kqa = ldv<false>(kb, xa, ys + 1, n0), kqb = ldv<false>(kb, xb, ys + 1, n0);
+  double zqa = ldv<false>(zb, xa, ys + 1, n0), zqb = ldv<false>(zb, xb, ys + 1, n0);
   for (int y = ys; y <= 2 * J1 - 1; ++y) {
     const double kpa = kqa, kpb = kqb, zpa = zqa, zpb = zqb;  // row y+1, prefetched
-    kqa = ldv(kb, xa, y + 2, n0);
-    kqb = ldv(kb, xb, y + 2, n0);
-    zqa = ldv(zb, xa, y + 2, n0);
-    zqb = ldv(zb, xb, y + 2, n0);
+    kqa = ldv<false>(kb, xa, y + 2, n0);
+    kqb = ldv<false>(kb, xb, y + 2, n0);
+    zqa = ldv<false>(zb, xa, y + 2, n0);
+    zqb = ldv<false>(zb, xb, y + 2, n0);
     double Ea, Eb, Na, Nb;
     edges2(kma, kmb, k0a, k0b, kpa, kpb, y, Ea, Eb, Na, Nb);
     const double t = t_red(y, Ea, Eb, Na, Nb, Nma, Nmb, zma, zmb, z0a, z0b, zpa, zpb);
@@ -610,15 +697,17 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
 }
 
 // ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
-__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
+template <bool INT>
+__device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ k,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
                                                        double* __restrict__ z_out,
                                                        const double* __restrict__ zc, int finest,
                                                        double* scal, int* flags, double2* partial,
-                                                       int maxp, unsigned* counter) {
-  PAIR_PROLOGUE
+                                                       int maxp, unsigned* counter, const PairCtx& c) {
+  PAIR_UNPACK
+
   const double *kb = k + off, *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
   const int nc0 = gc.n0;
   const Pair zero{0.0, 0.0};
@@ -647,23 +736,23 @@ __global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
   auto ZC = [&](const ZRaw& v, int y) {  // the row's pair: red column prolonged, black column 0
     return RED_IS_A(y) ? Pair{v.z + v.c0, 0.0} : Pair{0.0, v.z + 0.5 * (v.c0 + v.c1)};
   };
-  Pair ka = ld2(kb, xa, y0 - 2, n0), kb1 = ld2(kb, xa, y0 - 1, n0);
+  Pair ka = ld2<INT>(kb, xa, y0 - 2, n0), kb1 = ld2<INT>(kb, xa, y0 - 1, n0);
   Pair zpa = ZC(ZL(y0 - 2), y0 - 2), zpb = ZC(ZL(y0 - 1), y0 - 1);
   Pair Nt, Ed;
-  edges_pair(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  edges_pair<INT>(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
   Pair r0 = zero, zbm = zero, zb0 = zero;
   Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
-  Pair kq = ld2(kb, xa, y0, n0), rq = ld2(rb, xa, y0 - 1, n0);
+  Pair kq = ld2<INT>(kb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
   ZRaw zq = ZL(y0);
   double rz = 0.0;
   for (int t = y0 - 2; t < y1; ++t) {
     const Pair kc = kq, r1 = rq, zpc = ZC(zq, t + 2);
-    kq = ld2(kb, xa, t + 3, n0);
+    kq = ld2<INT>(kb, xa, t + 3, n0);
     zq = ZL(t + 3);
-    rq = ld2(rb, xa, t + 2, n0);
+    rq = ld2<INT>(rb, xa, t + 2, n0);
     Pair E1, N1;
-    edges_pair(ka, kb1, kc, xa, t + 1, m, E1, N1);
-    const Sten2 st1 = sten_pair(E1, N1, Nt, xa, t + 1, m, bc);
+    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     // black column of row t+1: (r − Σ A z_red_prolonged)/D
     const Pair odp = offd_pair(st1, zpa, zpb, zpc);
     const Pair zbp1 = RED_IS_A(t + 1) ? Pair{0.0, (r1.b - odp.b) * rcp64(st1.b.d)}
@@ -689,6 +778,19 @@ __global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
     ka = kb1; kb1 = kc; zpa = zpb; zpb = zpc; Nt = N1;
     r0 = r1; zbm = zb0; zb0 = zbp1; sr0 = RED_IS_A(t + 1) ? st1.a : st1.b;
   }
+  return rz;
+}
+
+__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
+                                                       const double* __restrict__ k,
+                                                       const double* __restrict__ r,
+                                                       const double* __restrict__ z,
+                                                       double* __restrict__ z_out,
+                                                       const double* __restrict__ zc, int finest,
+                                                       double* scal, int* flags, double2* partial,
+                                                       int maxp, unsigned* counter) {
+  PAIR_PROLOGUE
+  const double rz = interior ? smooth_up_kernel_body<true>(g, gc, bc, k, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c) : smooth_up_kernel_body<false>(g, gc, bc, k, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c);
   if (!finest) return;
   double t0, t1;
   if (reduce2_last(rz, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {

@@ -51,6 +51,10 @@ def workload(cfg: str):
         return dict(name="cfg4: matern nu=0.5 s2=2 lam=0.003, coupled 2048^2/1024^2, dirichlet-all, f=1, MG-PCG 1e-10",
                     family="matern", sigma2=2.0, lam=0.003, nu=0.5, m=2048, coupled=True, bc=1, qoi=0,
                     batch=64, ell=1, it=(43, 44))
+    if cfg == "2":
+        return dict(name="cfg2: CE field sampling only, matern nu=1.5 s2=1 lam=0.01, 1024^2 (n=2048), 4096 samples/batch",
+                    family="matern", sigma2=1.0, lam=0.01, nu=1.5, m=1024, coupled=False, bc=0, qoi=0,
+                    batch=4096, ell=0, it=(0, 0), ce_only=True)
     if cfg == "1":
         return dict(name="cfg1: matern nu=0.5 s2=1 lam=0.1, 64^2 single-level MC, dirichlet-all, integral QoI",
                     family="matern", sigma2=1.0, lam=0.1, nu=0.5, m=64, coupled=False, bc=1, qoi=2,
@@ -176,15 +180,24 @@ def run_reference(args, W):
     per_step = cores  # one coupled sample per host core per step (bounded sample)
     if W["m"] <= 256:
         per_step = cores * max(1, int(4096 // (W["m"] * W["m"] // 64 + 1)))
-    for w in range(min(args.warmup, 1)):
-        cpu_reference_step(W, cores, min(per_step, cores), 10_000_000 + w, port, ref)
     times, kind = [], "port"
     t_budget = time.time() + 240.0
-    for k in range(args.steps):
-        dt, kind = cpu_reference_step(W, cores, per_step, k * per_step, port, ref)
-        times.append(dt)
-        if time.time() > t_budget:
-            break
+    if W.get("ce_only"):
+        from paper_2306_13493_b200 import api
+        op = api.build_operator(api.GridSpec.square(W["m"]), api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]))
+        for k in range(args.steps):
+            dt, kind = cpu_ce_step(W, op, cores, ref, O)
+            times.append(dt)
+            if time.time() > t_budget:
+                break
+    else:
+        for w in range(min(args.warmup, 1)):
+            cpu_reference_step(W, cores, min(per_step, cores), 10_000_000 + w, port, ref)
+        for k in range(args.steps):
+            dt, kind = cpu_reference_step(W, cores, per_step, k * per_step, port, ref)
+            times.append(dt)
+            if time.time() > t_budget:
+                break
     total = sum(times)
     value = per_step * len(times) / total
     line = {
@@ -234,6 +247,8 @@ def main():
 
     from paper_2306_13493_b200 import api
     ctx = api.Context(local)
+    if W.get("ce_only"):
+        return run_ce_only(args, W, api, ctx, torch, dist, rank, world, local)
     m, B = W["m"], W["batch"]
     model = (api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]) if W["family"] == "matern"
              else api.CovarianceModel.separable_exponential(W["sigma2"], W["lam"]))
@@ -396,6 +411,155 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
+    """Config 2: batched CE field sampling (K1 + K2), fields left in HBM for `value`."""
+    import ctypes as C
+    from paper_2306_13493_b200 import _lib as L
+    lib = L.lib()
+    m, B = W["m"], W["batch"]
+    model = api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"])
+    t_setup = time.perf_counter()
+    op = api.build_operator(api.GridSpec.square(m), model)
+    t_setup = time.perf_counter() - t_setup
+    lev = op.device_level(ctx, 0)
+    Nf = (m + 1) ** 2
+    out = torch.empty((B, Nf), dtype=torch.float64, device=f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    flags = L.CE_FINE | L.CE_DEVICE_OUT
+
+    def step(k):
+        idx0 = (k * world + rank) * B
+        api._check(lib.osc_ce_sample(lev.h, None, 1, W["ell"], idx0, B, flags, out.data_ptr(), None))
+
+    for w in range(args.warmup):
+        step(1_000_000 + w)
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    launches0 = ctx.launch_count
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    e1.record(stream)
+    ctx.synchronize()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    kstats = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    gpu_launches = ctx.launch_count - launches0
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = args.steps * B * world / (ms / 1000.0)
+    hbm, hbm_kind = peaks()
+    n = lev.n
+    P = m + 1
+    # compulsory bytes per sample: rows write the half-spectrum intermediate (16 n P) and read
+    # √λ once per CTA sample-loop (≈ 8 s / samples per CTA, ignored); cols read it and write 8 Nf.
+    per = {"ce_rows": 16 * n * P, "ce_cols": 16 * n * P + 8 * Nf}
+    dom, (dl, dms) = max(kstats.items(), key=lambda kv: kv[1][1])
+    ach = per[dom] * args.steps * B / (dms / 1000.0) / 1e9 if dom in per else None
+    roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "frac": ach / hbm if ach else None, "traffic": None, "peak_kind": hbm_kind,
+            "note": "algorithmic bytes count the half-spectrum round trip; chunks keep it L2-resident"}
+    b_sample = algorithmic_bytes_per_sample(dict(W, coupled=False, it=(0, 0)), n) - 8 * Nf * 0
+    b_sample = 8 * n * n / B + 32 * n * (n // 2 + 1) + 8 * Nf  # SURVEY §8(d) B_ce, device ξ
+    pipeline = {"basis": "SURVEY 8(d) B_ce (device xi)", "bytes_per_sample": b_sample,
+                "roofline_samples_per_s_per_gpu": hbm * 1e9 / b_sample,
+                "frac": value / world / (hbm * 1e9 / b_sample)}
+    # e2e: host ξ in (pinned pool), fields out to pinned host memory, 64-sample calls
+    e2e = None
+    if not args.no_e2e:
+        cb = 64
+        s_ = lev.s
+        pool = api.PinnedBuffer((cb, s_))
+        tmp = np.empty((8, s_))
+        lib.osc_normals(ctx.h, 1, W["ell"], 0, 8, s_, tmp.ctypes.data)
+        for bb in range(cb):
+            pool.array[bb] = tmp[bb % 8]
+        del tmp
+        host_out = api.PinnedBuffer((cb, Nf))
+        nsteps = 1
+        calls = B // cb
+
+        def e2e_step():
+            for _ in range(calls):
+                api._check(lib.osc_ce_sample(lev.h, pool.array.ctypes.data, 1, W["ell"], 0, cb, L.CE_FINE,
+                                             host_out.array.ctypes.data, None))
+        e2e_step()
+        ctx.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(nsteps):
+            e2e_step()
+        f1.record(stream)
+        ctx.synchronize()
+        ems = f0.elapsed_time(f1)
+        e2e = {"value": nsteps * B * world / (ems / 1000.0), "unit": "samples/s",
+               "h2d_bytes_per_step": 8 * s_ * B, "d2h_bytes_per_step": 8 * Nf * B,
+               "xi": "host pinned pool of 64 rows (8 distinct Philox rows), 64-sample calls", "steps": nsteps}
+        pool.free()
+        host_out.free()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        cores = os.cpu_count() or 1
+        ref = O.Ref() if os.path.exists(O.REF_SO) else None
+        dt, kind = cpu_ce_step(W, op, cores, ref, O)
+        cpu = {"value": cores / dt, "unit": "samples/s", "cores": cores, "kind": kind,
+               "sample": f"{cores} CE samples (NormalStream + sample_into + restrict_to), one per thread ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "CE field samples/s (config 2, sampling only, fp64)", "value": value,
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic: device Philox NormalStream(1, 0, i)",
+            "config": {"workload": W["name"], "global_batch": B * world, "embedding_n": n,
+                       "l2": "fields written (34 GB/step) exceed L2", "setup_s": round(t_setup, 2)},
+            "roofline": roof, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": gpu_launches, "clocks": ck,
+            "kernels_ms": {k: round(v[1], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])},
+        }), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_ce_step(W, op, cores, ref, O):
+    """CPU CE baseline: the pristine reference (NormalStream + sample_into + restrict_to) when
+    available, else the oracle port; one sample per thread."""
+    import threading as th
+    m = W["m"]
+    if ref is not None:
+        rop = ref.build_operator(m, O.MATERN, W["sigma2"], W["lam"], W["nu"])
+
+        def one(i):
+            u = rop.sample(ref.normals(1, 0, i, rop.s))
+            rop.restrict(u, m)
+        kind = "reference"
+    else:
+        port = O.Port()
+        sl = np.sqrt(np.maximum(op.eigenvalues, 0.0))
+
+        def one(i):
+            u = port.sample(op.n, sl, port.normals(1, 0, i, op.s))
+            port.restrict(op.n, m, u, m)
+        kind = "port"
+    ts = [th.Thread(target=one, args=(i,)) for i in range(cores)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return time.perf_counter() - t0, kind
 
 
 if __name__ == "__main__":

@@ -75,7 +75,9 @@ enum {
   OSC_CE_TRUNCATED = 1,         /* use the truncated spectrum */
   OSC_CE_EXP = 2,               /* write k = exp(Z) instead of Z */
   OSC_CE_FINE = 4,              /* write the fine field (m+1)^2 */
-  OSC_CE_COARSE = 8             /* write the stride-2 coarse field (m/2+1)^2 */
+  OSC_CE_COARSE = 8,            /* write the stride-2 coarse field (m/2+1)^2 */
+  OSC_CE_DEVICE_OUT = 16,       /* fine_out / coarse_out are DEVICE pointers (no D2H copy) */
+  OSC_CE_XI_DEVICE = 32         /* xi is a DEVICE pointer (no H2D copy) */
 };
 
 /* Flat mirror of DarcyProblem / SolverOptions / QoiSpec (fem.hpp:17-35,
@@ -165,9 +167,10 @@ int osc_summarize(const double* q_fine, const double* q_coarse, int64_t n, int h
 /* NormalStream(seed, ell, index0 + j).fill for j < count on device; out host (count*s). */
 int osc_normals(osc_ctx* ctx, uint64_t seed, uint32_t ell, uint64_t index0, int64_t count,
                 int64_t s, double* out);
-/* CE sample of `count` samples: xi host (count*s) or NULL for device Philox of indices
- * [index0, index0+count) at (seed, ell); writes fine ((m+1)^2 each) and/or coarse
- * ((m/2+1)^2 each) fields to host per OSC_CE_* flags. */
+/* CE sample of `count` samples: xi (count*s; host, or device with OSC_CE_XI_DEVICE) or NULL for
+ * device Philox of indices [index0, index0+count) at (seed, ell); writes fine ((m+1)^2 each)
+ * and/or coarse ((m/2+1)^2 each) fields to host (or to device with OSC_CE_DEVICE_OUT) per the
+ * OSC_CE_* flags. Large batches are processed in L2-sized chunks internally. */
 int osc_ce_sample(osc_level* level, const double* xi, uint64_t seed, uint32_t ell,
                   uint64_t index0, int64_t count, int flags, double* fine_out,
                   double* coarse_out);

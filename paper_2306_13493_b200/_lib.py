@@ -27,7 +27,7 @@ BC_FLOWCELL, BC_DIRICHLET_ALL = 0, 1
 QOI_POINT, QOI_L2, QOI_INTEGRAL, QOI_FLUX = 0, 1, 2, 3
 COV_MATERN, COV_SEPARABLE_EXP = 0, 1
 DRAW_HAS_COARSE, DRAW_TRUNC_FINE, DRAW_TRUNC_COARSE, DRAW_XI_DEVICE = 1, 2, 4, 8
-CE_TRUNCATED, CE_EXP, CE_FINE, CE_COARSE = 1, 2, 4, 8
+CE_TRUNCATED, CE_EXP, CE_FINE, CE_COARSE, CE_DEVICE_OUT, CE_XI_DEVICE = 1, 2, 4, 8, 16, 32
 
 # every symbol the header declares (checked by tests/test_abi.py against the header text)
 EXPORTS = [

@@ -446,29 +446,53 @@ int osc_ce_sample(osc_level* L, const double* xi, uint64_t seed, uint32_t ell, u
     set_device(c);
     if (count <= 0) return;
     const bool want_f = (flags & OSC_CE_FINE) != 0, want_c = (flags & OSC_CE_COARSE) != 0;
+    const bool dev_out = (flags & OSC_CE_DEVICE_OUT) != 0, dev_xi = (flags & OSC_CE_XI_DEVICE) != 0;
     OSC_REQUIRE(want_f || want_c, "osc_ce_sample: request FINE and/or COARSE output");
     OSC_REQUIRE(!want_c || L->m % 2 == 0, "restrict: target grid is not a nested coarsening");
     OSC_REQUIRE(!(flags & OSC_CE_TRUNCATED) || L->k_trunc > 0, "osc_ce_sample: level has no truncated spectrum");
+    OSC_REQUIRE(!dev_out || ((!want_f || fine_out) && (!want_c || coarse_out)),
+                "osc_ce_sample: OSC_CE_DEVICE_OUT needs device output pointers");
     const double* sq = (flags & OSC_CE_TRUNCATED) ? L->sqrt_trunc.as<double>() : L->sqrt_full.as<double>();
     const int m = L->m, mc = m / 2;
     const int64_t Nf = (int64_t)(m + 1) * (m + 1), Nc = (int64_t)(mc + 1) * (mc + 1);
-    c->fields_fine.ensure(sizeof(double) * Nf * count);
-    if (want_c) c->fields_coarse.ensure(sizeof(double) * Nc * count);
-    c->out_i.ensure(sizeof(int) * count);
-    const double* xd = nullptr;
-    if (xi) {
-      c->xi_dev.ensure(sizeof(double) * L->s * count);
-      h2d(c, c->xi_dev.p, xi, sizeof(double) * L->s * count);
-      xd = c->xi_dev.as<double>();
+    // host-facing calls stage through device buffers in chunks bounded by the memory budget
+    const size_t per = (size_t)(dev_out ? 0 : 8 * (Nf * want_f + Nc * want_c)) +
+                       (size_t)((xi && !dev_xi) ? 8 * L->s : 0) + ce_inter_bytes(L, 1, 1) + 64;
+    int64_t chunk = dev_out && (!xi || dev_xi) ? count
+                                               : std::max<int64_t>(1, std::min<int64_t>(count, budget_of(c) / per));
+    if (!dev_out) {
+      if (want_f) c->fields_fine.ensure(sizeof(double) * Nf * chunk);
+      if (want_c) c->fields_coarse.ensure(sizeof(double) * Nc * chunk);
     }
+    if (xi && !dev_xi) c->xi_dev.ensure(sizeof(double) * L->s * chunk);
+    c->out_i.ensure(sizeof(int) * count);
     OSC_CUDA(cudaMemsetAsync(c->out_i.p, 0, sizeof(int) * count, c->stream));
-    ce_sample_launch(c, L, sq, xd, seed, ell, index0, (int)count, (flags & OSC_CE_EXP) != 0,
-                     want_f ? c->fields_fine.as<double>() : nullptr,
-                     want_c ? c->fields_coarse.as<double>() : nullptr, c->out_i.as<int>());
-    if (want_f && fine_out) d2h(c, fine_out, c->fields_fine.p, sizeof(double) * Nf * count);
-    if (want_c && coarse_out) d2h(c, coarse_out, c->fields_coarse.p, sizeof(double) * Nc * count);
+    for (int64_t c0 = 0; c0 < count; c0 += chunk) {
+      const int64_t cnt = std::min<int64_t>(chunk, count - c0);
+      const double* xd = nullptr;
+      if (xi) {
+        if (dev_xi) {
+          xd = xi + c0 * L->s;
+        } else {
+          h2d(c, c->xi_dev.p, xi + c0 * L->s, sizeof(double) * L->s * cnt);
+          xd = c->xi_dev.as<double>();
+        }
+      }
+      double* of = want_f ? (dev_out ? fine_out + c0 * Nf : c->fields_fine.as<double>()) : nullptr;
+      double* oc = want_c ? (dev_out ? coarse_out + c0 * Nc : c->fields_coarse.as<double>()) : nullptr;
+      ce_sample_launch(c, L, sq, xd, seed, ell, index0 + (uint64_t)c0, (int)cnt, (flags & OSC_CE_EXP) != 0,
+                       of, oc, c->out_i.as<int>() + c0);
+      if (!dev_out) {
+        if (want_f && fine_out) d2h(c, fine_out + c0 * Nf, of, sizeof(double) * Nf * cnt);
+        if (want_c && coarse_out) d2h(c, coarse_out + c0 * Nc, oc, sizeof(double) * Nc * cnt);
+      }
+    }
+    std::vector<int> bad(count);
+    d2h(c, bad.data(), c->out_i.p, sizeof(int) * count);
     OSC_CUDA(cudaStreamSynchronize(c->stream));
     c->flush_stats();
+    for (int64_t b = 0; b < count; ++b)
+      if (bad[b]) throw osc::Error(OSC_ERR_NUMERICAL, "sample: non-finite field value");
   });
 }
 

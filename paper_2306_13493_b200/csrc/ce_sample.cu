@@ -15,6 +15,8 @@
 // The intermediate X is [sample][q1][p] complex (row-major: coalesced in both passes).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "osc_device.cuh"
 #include "osc_internal.cuh"
 
@@ -216,12 +218,26 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
   if (count <= 0) return;
   // Coarse-only pass (other spectrum on the finest CES level) computes even columns only.
   const int cs = (out_fine == nullptr && out_coarse != nullptr) ? 2 : 1;
-  ctx->ce_inter.ensure(ce_inter_bytes(L, count, cs));
+  // Process the batch in chunks whose half-spectrum intermediate stays L2-resident between the
+  // row and the column pass (≈ 48 MB of the 126 MB L2), so the intermediate round trip
+  // (SURVEY §8(d) 32·n(n/2+1) B/sample) is served by L2 instead of HBM.
+  const size_t per = ce_inter_bytes(L, 1, cs);
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, (48u << 20) / per));
+  ctx->ce_inter.ensure(ce_inter_bytes(L, chunk, cs));
   double2* inter = ctx->ce_inter.as<double2>();
-  switch (elems_for(L->n)) {
-    case 8: launch_pair<8>(ctx, L, sqrt_lam, xi_dev, seed, ell, index0, count, do_exp, out_fine, out_coarse, bad_flag, cs, inter); break;
-    case 4: launch_pair<4>(ctx, L, sqrt_lam, xi_dev, seed, ell, index0, count, do_exp, out_fine, out_coarse, bad_flag, cs, inter); break;
-    default: launch_pair<2>(ctx, L, sqrt_lam, xi_dev, seed, ell, index0, count, do_exp, out_fine, out_coarse, bad_flag, cs, inter); break;
+  const int m = L->m, mc = m / 2;
+  const int64_t Nf = (int64_t)(m + 1) * (m + 1), Nc = (int64_t)(mc + 1) * (mc + 1);
+  for (int c0 = 0; c0 < count; c0 += chunk) {
+    const int cnt = std::min(chunk, count - c0);
+    const double* xi_c = xi_dev ? xi_dev + (int64_t)c0 * L->s : nullptr;
+    double* of = out_fine ? out_fine + c0 * Nf : nullptr;
+    double* oc = out_coarse ? out_coarse + c0 * Nc : nullptr;
+    int* bf = bad_flag ? bad_flag + c0 : nullptr;
+    switch (elems_for(L->n)) {
+      case 8: launch_pair<8>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
+      case 4: launch_pair<4>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
+      default: launch_pair<2>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
+    }
   }
 }
 

@@ -131,7 +131,7 @@ __global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restr
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int n = (int)g.N, n0 = g.n0, m = g.m;
-  double* L = chol + (int64_t)b * n * n;
+  double* L = chol + (int64_t)b * 2 * n * n;
   const double* kb = k + (int64_t)b * n;
   for (int i = 0; i < n * n; ++i) L[i] = 0.0;
   // stencil from a zero-padded 3×3 neighbourhood of k
@@ -159,6 +159,21 @@ __global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restr
       double v = L[i * n + j];
       for (int q = 0; q < j; ++q) v -= L[i * n + q] * L[j * n + q];
       L[i * n + j] = v * inv;
+    }
+  }
+  // explicit inverse A⁻¹ = L⁻ᵀ L⁻¹ (column by column), so each V-cycle's coarsest solve is one
+  // warp-parallel matvec instead of two serial triangular sweeps
+  double* X = L + (int64_t)n * n;
+  for (int c = 0; c < n; ++c) {
+    for (int i = 0; i < n; ++i) {  // forward: L y = e_c
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int q = 0; q < i; ++q) v -= L[i * n + q] * X[q * n + c];
+      X[i * n + c] = v / L[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {  // backward: Lᵀ x = y
+      double v = X[i * n + c];
+      for (int q = i + 1; q < n; ++q) v -= L[q * n + i] * X[q * n + c];
+      X[i * n + c] = v / L[i * n + i];
     }
   }
 }
@@ -237,7 +252,8 @@ constexpr int LY = 32;       // output rows per warp on large grids
 // rows marched per warp: long chunks amortise the 2-row warm-up on large grids; short chunks
 // cut the serial row-latency chain (and add CTAs) on the small, latency-bound MG levels.
 __host__ __device__ __forceinline__ int rows_per_warp(int m) { return m >= 512 ? LY : (m >= 64 ? 16 : 8); }
-constexpr int LYC = 16;      // coarse output rows per warp (restriction)
+constexpr int LYC = 16;      // coarse output rows per warp (restriction) on large grids
+__host__ __device__ __forceinline__ int coarse_rows_per_warp(int mc) { return mc >= 256 ? LYC : 4; }
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(FULL, v, 1); }
@@ -611,7 +627,8 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
   const int I = strip * 30 - 1 + lane;
   const bool outI = lane >= 1 && lane < 31 && I <= mc;
   const int xa = 2 * I, xb = 2 * I + 1;
-  const int J0 = blockIdx.y * LYC, J1 = min(J0 + LYC, gc.n0);
+  const int lyc = coarse_rows_per_warp(gc.m);
+  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
   const int64_t off = (int64_t)b * g.N;
   const double *kb = k + off, *zb = z + off;
   constexpr double third = 1.0 / 3.0;
@@ -826,24 +843,21 @@ __global__ void __launch_bounds__(NT) dot_rz_kernel(Geo g, const double* __restr
   }
 }
 
-// coarsest solve z = L⁻ᵀ L⁻¹ r, one thread per sample (fem.cpp:274-286)
+// coarsest solve z = A⁻¹ r (the Cholesky solve of fem.cpp:274-286 via the precomputed inverse),
+// one warp per sample: lane i forms row i of the matvec
 __global__ void coarse_solve_kernel(int n, int B, const double* __restrict__ chol,
                                     const double* __restrict__ r, double* __restrict__ z,
                                     const int* flags) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (b >= B || !flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const double* L = chol + (int64_t)b * n * n;
+  const double* X = chol + (int64_t)b * 2 * n * n + (int64_t)n * n;
   const double* rb = r + (int64_t)b * n;
   double* zb = z + (int64_t)b * n;
-  for (int i = 0; i < n; ++i) {
-    double v = rb[i];
-    for (int q = 0; q < i; ++q) v -= L[i * n + q] * zb[q];
-    zb[i] = v / L[i * n + i];
-  }
-  for (int i = n - 1; i >= 0; --i) {
-    double v = zb[i];
-    for (int q = i + 1; q < n; ++q) v -= L[q * n + i] * zb[q];
-    zb[i] = v / L[i * n + i];
+  for (int i = lane; i < n; i += 32) {
+    double v = 0.0;
+    for (int j = 0; j < n; ++j) v = fma(X[i * n + j], __ldg(rb + j), v);
+    zb[i] = v;
   }
 }
 
@@ -947,7 +961,8 @@ inline dim3 march_grid(int m, int /*hx*/, int B) {
   return dim3((unsigned)((march_strips(m) + MW - 1) / MW), (unsigned)((m + 1 + ly - 1) / ly), (unsigned)B);
 }
 inline dim3 restrict_grid(int mc, int B) {
-  return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + LYC - 1) / LYC), (unsigned)B);
+  const int lyc = coarse_rows_per_warp(mc);
+  return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + lyc - 1) / lyc), (unsigned)B);
 }
 inline int64_t tile_parts(int m) {
   const dim3 a = march_grid(m, 1, 1), b = march_grid(m, 2, 1);
@@ -963,7 +978,7 @@ size_t solver_bytes(int m, int B, int hist_cap) {
     const size_t N = (size_t)(g + 1) * (g + 1);
     tot += N * B * sizeof(double) * (lev == 0 ? 8 : 4);  // level 0: u r r2 z z2 p0 p1 (+k by caller); else k r z z2
     ++lev;
-    if (g <= 4 || g % 2 != 0) { tot += N * N * B * sizeof(double); break; }
+    if (g <= 4 || g % 2 != 0) { tot += 2 * N * N * B * sizeof(double); break; }
     g /= 2;
   }
   tot += (size_t)B * (S_NSCAL * 8 + F_NFLAGS * 4 + 8) + (size_t)B * hist_cap * 8;
@@ -1013,7 +1028,7 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   w.p0 = (double*)take(vb0);
   w.p1 = (double*)take(vb0);
   w.Ap = nullptr;
-  w.chol = (double*)take(sizeof(double) * (size_t)w.nc * w.nc * B);
+  w.chol = (double*)take(sizeof(double) * 2 * (size_t)w.nc * w.nc * B);
   w.scal = (double*)take(sizeof(double) * S_NSCAL * B);
   w.flags = (int*)take(sizeof(int) * F_NFLAGS * B);
   w.counter = (unsigned*)take(sizeof(unsigned) * B);
@@ -1039,7 +1054,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
   if (w.nlev == 1) {
     {
       KScope ks(ctx, "mg_coarse_solve");
-      coarse_solve_kernel<<<(B + 63) / 64, 64, 0, st>>>(w.nc, B, w.chol, w.r_cur, w.lev[0].z2, w.flags);
+      coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, w.r_cur, w.lev[0].z2, w.flags);
     }
     KScope ks(ctx, "pcg_dot_rz");
     dot_rz_kernel<<<dim3(nblocks(w.lev[0].N), 1, B), NT, 0, st>>>(geo_of(w.lev[0]), w.r_cur, w.lev[0].z2,
@@ -1060,7 +1075,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
   {
     const SolverLevel& C = w.lev[w.nlev - 1];
     KScope ks(ctx, "mg_coarse_solve");
-    coarse_solve_kernel<<<(B + 63) / 64, 64, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
+    coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
   }
   for (int l = w.nlev - 2; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];

@@ -12,7 +12,8 @@
 //   pass 2 (columns, along y): for each needed p0 the length-n column of X is FFT'd and only
 //           p1 ≤ m (stride cs) is kept; u = (Re+Im)/n, k = exp(u) written straight into the
 //           solver's fine and stride-2 coarse conductivity arrays.
-// The intermediate X is [sample][q1][p] complex (row-major: coalesced in both passes).
+// The intermediate X is [sample][p][q1] complex (transposed: pass-1 writes of a row pair fill
+// 32-byte sectors, pass-2 column reads are contiguous).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,77 +28,67 @@ namespace {
 // elements per thread for a length-n transform
 inline int elems_for(int n) { return n >= 8 ? 8 : n; }
 
-template <int E>
-__global__ void __launch_bounds__(512) ce_rows_kernel(
+// Pass 1: one CTA slot per (row pair, sample). Writes the TRANSPOSED half spectrum
+// inter[b][p][q1] (q1 fastest), so rows q1a, q1b land in one 32-byte sector and pass 2 reads
+// each column as one contiguous run.
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_rows_kernel(
     const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed,
-    uint32_t ell, uint64_t index0, int n, int NT, int P, int cs, int B, int SB,
-    const double2* __restrict__ tw, double2* __restrict__ inter) {
+    uint32_t ell, uint64_t index0, int n, int NT, int P, int cs, const double2* __restrict__ tw,
+    double2* __restrict__ inter) {
   extern __shared__ double2 smem[];
   const int T = n / E;                      // threads per transform
   const int t = threadIdx.x / T;            // transform slot in this CTA
   const int lt = threadIdx.x - t * T;       // lane within the transform
   const int rp = blockIdx.x * NT + t;       // row pair
+  const int b = blockIdx.y;                 // sample within the chunk
   const bool valid = rp < n / 2;
   const int q1a = 2 * rp, q1b = 2 * rp + 1;
   double2* x = smem + t * n;
   const int64_t s = (int64_t)n * n;
-
-  // √λ for this thread's columns of both rows, reused across the sample loop.
-  constexpr int CP = E / 2;  // column pairs per thread
-  double2 la[CP], lb[CP];
+  const PhiloxKeys keys = philox_keys(seed);
+  if (valid) {
+    const double2* la = reinterpret_cast<const double2*>(sqrt_lam + (int64_t)q1a * n);
+    const double2* lb = reinterpret_cast<const double2*>(sqrt_lam + (int64_t)q1b * n);
 #pragma unroll
-  for (int g = 0; g < CP; ++g) {
-    const int c = lt + g * T;  // column pair: columns 2c, 2c+1
-    if (valid) {
-      la[g] = __ldg(reinterpret_cast<const double2*>(sqrt_lam + (int64_t)q1a * n) + c);
-      lb[g] = __ldg(reinterpret_cast<const double2*>(sqrt_lam + (int64_t)q1b * n) + c);
-    } else {
-      la[g] = lb[g] = make_double2(0.0, 0.0);
+    for (int g = 0; g < E / 2; ++g) {
+      const int c = lt + g * T;  // column pair: columns 2c, 2c+1
+      double2 xa, xb;
+      if (xi) {
+        const double* xr = xi + (int64_t)b * s;
+        xa = __ldg(reinterpret_cast<const double2*>(xr + (int64_t)q1a * n) + c);
+        xb = __ldg(reinterpret_cast<const double2*>(xr + (int64_t)q1b * n) + c);
+      } else {
+        const uint64_t idx = index0 + (uint64_t)b;
+        xa = normal_pair_k(keys, ell, idx, (uint32_t)((int64_t)q1a * (n / 2) + c));
+        xb = normal_pair_k(keys, ell, idx, (uint32_t)((int64_t)q1b * (n / 2) + c));
+      }
+      const double2 sa = __ldg(la + c), sb = __ldg(lb + c);
+      // z[q0] = w(q0, q1a) + i w(q0, q1b)
+      x[2 * c] = make_double2(sa.x * xa.x, sb.x * xb.x);
+      x[2 * c + 1] = make_double2(sa.y * xa.y, sb.y * xb.y);
     }
   }
-
-  const int b0 = blockIdx.y * SB;
-  const int b1 = min(B, b0 + SB);
-  for (int b = b0; b < b1; ++b) {
-    if (valid) {
-#pragma unroll
-      for (int g = 0; g < CP; ++g) {
-        const int c = lt + g * T;
-        double2 xa, xb;
-        if (xi) {
-          const double* xr = xi + (int64_t)b * s;
-          xa = __ldg(reinterpret_cast<const double2*>(xr + (int64_t)q1a * n) + c);
-          xb = __ldg(reinterpret_cast<const double2*>(xr + (int64_t)q1b * n) + c);
-        } else {
-          const uint64_t idx = index0 + (uint64_t)b;
-          xa = normal_pair(seed, ell, idx, (uint32_t)((int64_t)q1a * (n / 2) + c));
-          xb = normal_pair(seed, ell, idx, (uint32_t)((int64_t)q1b * (n / 2) + c));
-        }
-        // z[q0] = w(q0, q1a) + i w(q0, q1b)
-        x[2 * c] = make_double2(la[g].x * xa.x, lb[g].x * xb.x);
-        x[2 * c + 1] = make_double2(la[g].y * xa.y, lb[g].y * xb.y);
-      }
+  __syncthreads();
+  fft_smem<E>(x, n, lt, tw);
+  if (valid) {
+    double2* out = inter + (int64_t)b * P * n + q1a;
+    for (int p = lt; p < P; p += T) {
+      const int p0 = p * cs;
+      const double2 zp = x[p0];
+      const double2 zm = x[(n - p0) & (n - 1)];
+      // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
+      double2* o = out + (int64_t)p * n;
+      o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+      o[1] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
     }
-    __syncthreads();
-    fft_smem<E>(x, n, lt, tw);
-    if (valid) {
-      double2* outa = inter + ((int64_t)b * n + q1a) * P;
-      double2* outb = inter + ((int64_t)b * n + q1b) * P;
-      for (int p = lt; p < P; p += T) {
-        const int p0 = p * cs;
-        const double2 zp = x[p0];
-        const double2 zm = x[(n - p0) & (n - 1)];
-        // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
-        outa[p] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-        outb[p] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
-      }
-    }
-    __syncthreads();
   }
 }
 
-template <int E>
-__global__ void __launch_bounds__(512) ce_cols_kernel(
+// Pass 2: NT columns of one sample per CTA; column j of the transposed intermediate is one
+// contiguous n-element run (coalesced 16-byte loads).
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
     const double2* __restrict__ inter, int n, int m, int NT, int P, int cs, double inv_n,
     int do_exp, const double2* __restrict__ tw, double* __restrict__ out_fine,
     double* __restrict__ out_coarse, int* __restrict__ bad_flag) {
@@ -107,16 +98,12 @@ __global__ void __launch_bounds__(512) ce_cols_kernel(
   const int lt = threadIdx.x - t * T;
   const int b = blockIdx.y;
   const int j0 = blockIdx.x * NT;
-  const int ld = n + 1;  // padded column stride (conflict-free transposed staging)
-  const double2* src = inter + (int64_t)b * n * P;
-
-  for (int idx = threadIdx.x; idx < NT * n; idx += blockDim.x) {
-    const int tt = idx % NT, q1 = idx / NT;
-    const int j = j0 + tt;
-    smem[tt * ld + q1] = (j < P) ? src[(int64_t)q1 * P + j] : make_double2(0.0, 0.0);
-  }
+  const double2* src = inter + ((int64_t)b * P + j0) * n;
+  const int ncols = min(NT, P - j0);
+  for (int idx = threadIdx.x; idx < NT * n; idx += blockDim.x)
+    smem[idx] = (idx < ncols * n) ? __ldg(src + idx) : make_double2(0.0, 0.0);
   __syncthreads();
-  fft_smem<E>(smem + t * ld, n, lt, tw);
+  fft_smem<E>(smem + t * n, n, lt, tw);
 
   // outputs: rows p1 = i*cs ≤ m, columns p0 = j*cs
   const int n_rows = m / cs + 1;
@@ -129,7 +116,7 @@ __global__ void __launch_bounds__(512) ce_cols_kernel(
     const int j = j0 + tt;
     if (j >= P) continue;
     const int p1 = i * cs, p0 = j * cs;
-    const double2 v = smem[tt * ld + p1];
+    const double2 v = smem[tt * n + p1];
     const double zval = (v.x + v.y) * inv_n;
     if (!isfinite(zval)) bad = 1;
     const double o = do_exp ? exp(zval) : zval;
@@ -148,7 +135,7 @@ CeGeom rows_geom(int n) {
   CeGeom g;
   g.E = elems_for(n);
   g.T = n / g.E;
-  g.NT = std::max(1, 256 / g.T);
+  g.NT = std::max(1, 256 / g.T);  // T > 256 only for n ≥ 4096: one transform per CTA
   g.NT = std::min(g.NT, std::max(1, n / 2));
   g.threads = g.NT * g.T;
   g.smem = sizeof(double2) * (size_t)g.NT * n;
@@ -159,16 +146,13 @@ CeGeom cols_geom(int n, int P) {
   CeGeom g;
   g.E = elems_for(n);
   g.T = n / g.E;
-  int nt = std::max(1, 8192 / n);
-  nt = std::min(nt, std::max(1, 512 / g.T));
-  nt = std::min(nt, P);
-  g.NT = nt;
+  g.NT = std::min(std::max(1, 256 / g.T), P);
   g.threads = g.NT * g.T;
-  g.smem = sizeof(double2) * (size_t)g.NT * (n + 1);
+  g.smem = sizeof(double2) * (size_t)g.NT * n;
   return g;
 }
 
-template <int E>
+template <int E, int MAXT>
 void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
                  uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
                  double* out_fine, double* out_coarse, int* bad_flag, int cs, double2* inter) {
@@ -178,22 +162,17 @@ void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double*
   cudaStream_t st = ctx->stream;
   {
     const CeGeom g = rows_geom(n);
-    const int row_groups = (n / 2 + g.NT - 1) / g.NT;
-    const int want = 2 * 148;
-    const int sample_groups = std::max(1, std::min(count, (want + row_groups - 1) / row_groups));
-    const int SB = (count + sample_groups - 1) / sample_groups;
-    const dim3 grid(row_groups, (count + SB - 1) / SB);
-    auto kern = ce_rows_kernel<E>;
+    const dim3 grid((n / 2 + g.NT - 1) / g.NT, count);
+    auto kern = ce_rows_kernel<E, MAXT>;
     OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
     KScope ks(ctx, "ce_rows");
-    kern<<<grid, g.threads, g.smem, st>>>(sqrt_lam, xi_dev, seed, ell, index0, n, g.NT, P, cs,
-                                         count, SB, tw, inter);
+    kern<<<grid, g.threads, g.smem, st>>>(sqrt_lam, xi_dev, seed, ell, index0, n, g.NT, P, cs, tw, inter);
     OSC_CUDA(cudaGetLastError());
   }
   {
     const CeGeom g = cols_geom(n, P);
     const dim3 grid((P + g.NT - 1) / g.NT, count);
-    auto kern = ce_cols_kernel<E>;
+    auto kern = ce_cols_kernel<E, MAXT>;
     OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
     KScope ks(ctx, "ce_cols");
     kern<<<grid, g.threads, g.smem, st>>>(inter, n, m, g.NT, P, cs, 1.0 / n, do_exp ? 1 : 0, tw,
@@ -222,7 +201,7 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
   // row and the column pass (≈ 48 MB of the 126 MB L2), so the intermediate round trip
   // (SURVEY §8(d) 32·n(n/2+1) B/sample) is served by L2 instead of HBM.
   const size_t per = ce_inter_bytes(L, 1, cs);
-  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, (48u << 20) / per));
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, (80u << 20) / per));
   ctx->ce_inter.ensure(ce_inter_bytes(L, chunk, cs));
   double2* inter = ctx->ce_inter.as<double2>();
   const int m = L->m, mc = m / 2;
@@ -233,11 +212,17 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
     double* of = out_fine ? out_fine + c0 * Nf : nullptr;
     double* oc = out_coarse ? out_coarse + c0 * Nc : nullptr;
     int* bf = bad_flag ? bad_flag + c0 : nullptr;
-    switch (elems_for(L->n)) {
-      case 8: launch_pair<8>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
-      case 4: launch_pair<4>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
-      default: launch_pair<2>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
-    }
+    // threads per transform T = n/E: ≤ 256 up to n = 2048, 512 at 4096, 1024 at 8192
+    if (L->n >= 8192)
+      launch_pair<8, 1024>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+    else if (L->n == 4096)
+      launch_pair<8, 512>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+    else if (L->n >= 8)
+      launch_pair<8, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+    else if (L->n == 4)
+      launch_pair<4, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+    else
+      launch_pair<2, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
   }
 }
 

@@ -125,6 +125,55 @@ __global__ void __launch_bounds__(NT) inject_kernel(Geo gf, Geo gc, const double
   kc[(int64_t)b * gc.N + ic] = kf[(int64_t)b * gf.N + (int64_t)(2 * J) * gf.n0 + 2 * I];
 }
 
+// Coarsest operator and its explicit inverse, one warp per sample. The reference factors the
+// coarsest matrix by dense Cholesky (fem.cpp:255-272) and back-substitutes per V-cycle
+// (:274-286); here the SPD matrix is inverted once per solve by Gauss–Jordan (no pivoting
+// needed for SPD; lane i owns row i of [A | I] in shared memory), so every V-cycle's coarsest
+// solve is one warp-parallel matvec. n ≤ 32 uses this path; larger coarsest grids fall back to
+// the per-thread Cholesky + inverse below.
+constexpr int CF_WARPS = 2;
+__global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(Geo g, int bc, int B,
+                                                                          const double* __restrict__ k,
+                                                                          double* __restrict__ chol) {
+  __shared__ double aug[CF_WARPS][32][65];  // row i: A(i, 0..n−1) | I(i, 0..n−1), padded
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * CF_WARPS + w;
+  if (b >= B) return;
+  const int n = (int)g.N, n0 = g.n0, m = g.m;
+  const double* kb = k + (int64_t)b * n;
+  double(*A)[65] = aug[w];
+  if (lane < n) {
+    for (int j = 0; j < 2 * n; ++j) A[lane][j] = (j == n + lane) ? 1.0 : 0.0;
+    const int gy = lane / n0, gx = lane - gy * n0;
+    double kt[9];
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int x = gx + dx, y = gy + dy;
+        kt[(dy + 1) * 3 + dx + 1] = (x >= 0 && x < n0 && y >= 0 && y < n0) ? kb[y * n0 + x] : 0.0;
+      }
+    const Sten st = stencil_at(kt, 3, 1, 1, gx, gy, m, bc);
+    A[lane][lane] = st.d;
+    if (gx + 1 < n0) A[lane][lane + 1] = st.e;
+    if (gx > 0) A[lane][lane - 1] = st.w;
+    if (gy + 1 < n0) A[lane][lane + n0] = st.n;
+    if (gy > 0) A[lane][lane - n0] = st.s;
+  }
+  __syncwarp();
+  for (int c = 0; c < n; ++c) {
+    const double inv_p = 1.0 / A[c][c];
+    const double f = (lane < n && lane != c) ? A[lane][c] * inv_p : 0.0;
+    __syncwarp();
+    if (lane < n && lane != c)
+      for (int j = c; j < 2 * n; ++j) A[lane][j] = fma(-f, A[c][j], A[lane][j]);
+    __syncwarp();
+    if (lane == c)
+      for (int j = c; j < 2 * n; ++j) A[c][j] *= inv_p;
+    __syncwarp();
+  }
+  double* X = chol + (int64_t)b * 2 * n * n + (int64_t)n * n;
+  for (int idx = lane; idx < n * n; idx += 32) X[idx] = A[idx / n][n + idx % n];
+}
+
 // Dense Cholesky of the coarsest operator, one thread per sample (fem.cpp:255-272).
 __global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restrict__ k,
                                      double* __restrict__ chol) {
@@ -817,6 +866,309 @@ __global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
   }
 }
 
+// ---- CTA-resident solver for small grids (m ≤ 64) ----------------------------------------------------
+// One CTA owns one sample's whole solve: the edge weights E/N of every MG level, r, z (and p on
+// level 0) live in shared memory (≤ 221 KB at m = 64), u stays in global memory, and the entire
+// PCG loop (same algorithm and stopping rule as the multi-kernel path) runs inside one launch —
+// no per-iteration launches, host polling or grid-wide reductions for the latency-bound levels
+// that dominate MLMC's coarse levels (BASELINE configs 1, 3, 5).
+constexpr int SM_THREADS = 1024;
+
+struct SLev {
+  double *E, *N, *r, *z;
+  int m, n0, N_;
+};
+
+__device__ __forceinline__ Sten sten_smem(const SLev& L, int x, int y, int bc) {
+  const int m = L.m, n0 = L.n0, c = y * n0 + x;
+  Sten st;
+  if (is_dir(bc, m, x, y)) {
+    st.d = 1.0;
+    st.e = st.w = st.n = st.s = 0.0;
+    return st;
+  }
+  const double e = L.E[c], w = x > 0 ? L.E[c - 1] : 0.0, n = L.N[c], s = y > 0 ? L.N[c - n0] : 0.0;
+  st.d = -(e + w + n + s);
+  st.e = is_dir(bc, m, x + 1, y) ? 0.0 : e;
+  st.w = is_dir(bc, m, x - 1, y) ? 0.0 : w;
+  st.n = is_dir(bc, m, x, y + 1) ? 0.0 : n;
+  st.s = is_dir(bc, m, x, y - 1) ? 0.0 : s;
+  return st;
+}
+
+__device__ __forceinline__ double offd_smem(const Sten& st, const double* v, int c, int n0) {
+  double a = 0.0;
+  if (st.e != 0.0) a += st.e * v[c + 1];
+  if (st.w != 0.0) a += st.w * v[c - 1];
+  if (st.n != 0.0) a += st.n * v[c + n0];
+  if (st.s != 0.0) a += st.s * v[c - n0];
+  return a;
+}
+
+// red (color 0) or black (color 1) Gauss–Seidel half sweep: z = (r − Σ A z)/D on that color
+__device__ __forceinline__ void gs_color(const SLev& L, int color, int bc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int y = warp; y < L.n0; y += nw) {
+    for (int x = 2 * lane + ((y + color) & 1); x < L.n0; x += 64) {
+      const int i = y * L.n0 + x;
+      const Sten st = sten_smem(L, x, y, bc);
+      L.z[i] = (L.r[i] - offd_smem(st, L.z, i, L.n0)) * rcp64(st.d);
+    }
+  }
+}
+
+// V(1,1) on levels l..L−1, input L[l].r, output L[l].z (same algorithm as the multi-kernel path)
+__device__ void vcycle_smem(SLev* lev, int nlev, const double* Ainv, int bc) {
+  for (int l = 0; l + 1 < nlev; ++l) {
+    const SLev& F = lev[l];
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) F.z[i] = 0.0;
+    __syncthreads();
+    gs_color(F, 0, bc);
+    __syncthreads();
+    gs_color(F, 1, bc);
+    __syncthreads();
+    // rc = Pᵀ(r − A z): the residual vanishes on black nodes, is −Σ A z_black on red nodes
+    const SLev& C = lev[l + 1];
+    for (int ic = threadIdx.x; ic < C.N_; ic += blockDim.x) {
+      const int J = ic / C.n0, I = ic - J * C.n0;
+      double acc = 0.0;
+      if (!is_dir(bc, C.m, I, J)) {
+        auto t_at = [&](int fx, int fy) {
+          if (fx < 0 || fx > F.m || fy < 0 || fy > F.m) return 0.0;
+          const Sten st = sten_smem(F, fx, fy, bc);
+          return -offd_smem(st, F.z, fy * F.n0 + fx, F.n0);
+        };
+        acc = t_at(2 * I, 2 * J) + 0.5 * (t_at(2 * I + 1, 2 * J + 1) + t_at(2 * I - 1, 2 * J - 1));
+      }
+      C.r[ic] = acc;
+    }
+    __syncthreads();
+  }
+  {  // coarsest: z = A⁻¹ r
+    const SLev& C = lev[nlev - 1];
+    for (int i = threadIdx.x; i < C.N_; i += blockDim.x) {
+      double v = 0.0;
+      for (int j = 0; j < C.N_; ++j) v = fma(Ainv[i * C.N_ + j], C.r[j], v);
+      C.z[i] = v;
+    }
+    __syncthreads();
+  }
+  for (int l = nlev - 2; l >= 0; --l) {
+    const SLev& F = lev[l];
+    const SLev& C = lev[l + 1];
+    // prolongation onto the red nodes (black values are overwritten by the black sweep)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int y = warp; y < F.n0; y += nw)
+      for (int x = 2 * lane + (y & 1); x < F.n0; x += 64) {
+      const int i = y * F.n0 + x;
+      const double pz = (x & 1) == 0 ? C.z[(y >> 1) * C.n0 + (x >> 1)]
+                                     : 0.5 * (C.z[(y >> 1) * C.n0 + (x >> 1)] + C.z[((y + 1) >> 1) * C.n0 + ((x + 1) >> 1)]);
+      F.z[i] += pz;
+    }
+    __syncthreads();
+    gs_color(F, 1, bc);
+    __syncthreads();
+    gs_color(F, 0, bc);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ double block_sum_s(double v) {
+  __shared__ double sh[32];
+  const double t = block_sum(v, sh);
+  __shared__ double res;
+  if (threadIdx.x == 0) res = t;
+  __syncthreads();
+  return res;
+}
+
+size_t small_smem_bytes(int m, int* nlev_out) {
+  size_t tot = 0;
+  int g = m, nl = 0, nc = 0;
+  for (;;) {
+    const size_t N = (size_t)(g + 1) * (g + 1);
+    tot += N * (nl == 0 ? 5 : 4) * sizeof(double);
+    ++nl;
+    if (g <= 4 || g % 2 != 0) { nc = (int)N; break; }
+    g /= 2;
+  }
+  if (nlev_out) *nlev_out = nl;
+  return tot + (size_t)nc * nc * sizeof(double) + 64 * sizeof(SLev) + 256;
+}
+
+__global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev, int bc, int forcing,
+                                                               double fval, double tol, int max_iter_factor,
+                                                               const double* __restrict__ kin,
+                                                               double* __restrict__ uout, int* flags,
+                                                               double* scal) {
+  extern __shared__ double smem[];
+  __shared__ SLev lev[12];
+  __shared__ int s_go;
+  const int b = blockIdx.x;
+  const int N0 = (m0 + 1) * (m0 + 1);
+  const double* k0 = kin + (int64_t)b * N0;
+  double* u = uout + (int64_t)b * N0;
+  // carve shared memory
+  double* p = smem;
+  double* cur = smem + N0;
+  {
+    int g = m0;
+    for (int l = 0; l < nlev; ++l) {
+      const int n0 = g + 1, N = n0 * n0;
+      if (threadIdx.x == 0) lev[l] = SLev{cur, cur + N, cur + 2 * N, cur + 3 * N, g, n0, N};
+      cur += 4 * N;
+      g /= 2;
+    }
+  }
+  double* Ainv = cur;
+  __syncthreads();
+  // edge weights of every level from the injected nodal k (fem.cpp:241-244), same formulas and
+  // operand order as the streaming kernels
+  constexpr double third = 1.0 / 3.0;
+  for (int l = 0; l < nlev; ++l) {
+    const SLev L = lev[l];
+    const int st = 1 << l;
+    auto K = [&](int x, int y) { return __ldg(k0 + (int64_t)(y * st) * (m0 + 1) + x * st); };
+    for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
+      const int y = i / L.n0, x = i - y * L.n0, m = L.m;
+      double e = 0.0, n = 0.0;
+      if (x < m) {
+        const double lo = y < m ? (K(x, y) + K(x + 1, y) + K(x + 1, y + 1)) * third : 0.0;
+        const double up = y > 0 ? (K(x, y - 1) + K(x + 1, y) + K(x, y)) * third : 0.0;
+        e = -0.5 * (lo + up);
+      }
+      if (y < m) {
+        const double up = x < m ? (K(x, y) + K(x + 1, y + 1) + K(x, y + 1)) * third : 0.0;
+        const double lo = x > 0 ? (K(x - 1, y) + K(x, y) + K(x, y + 1)) * third : 0.0;
+        n = -0.5 * (up + lo);
+      }
+      L.E[i] = e;
+      L.N[i] = n;
+    }
+  }
+  __syncthreads();
+  {  // coarsest operator → in-place Gauss–Jordan inverse (SPD, no pivoting)
+    const SLev C = lev[nlev - 1];
+    const int n = C.N_;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Ainv[idx] = 0.0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int y = i / C.n0, x = i - y * C.n0;
+      const Sten st = sten_smem(C, x, y, bc);
+      Ainv[i * n + i] = st.d;
+      if (x + 1 < C.n0) Ainv[i * n + i + 1] = st.e;
+      if (x > 0) Ainv[i * n + i - 1] = st.w;
+      if (y + 1 < C.n0) Ainv[i * n + i + C.n0] = st.n;
+      if (y > 0) Ainv[i * n + i - C.n0] = st.s;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < n; ++kk) {
+      const double piv = 1.0 / Ainv[kk * n + kk];
+      __syncthreads();
+      // row kk scaled; column kk of other rows folded (in-place Gauss–Jordan)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (i == kk) continue;
+        const double f = Ainv[i * n + kk] * piv;
+        for (int j = 0; j < n; ++j) {
+          if (j == kk) continue;
+          Ainv[i * n + j] = fma(-f, Ainv[kk * n + j], Ainv[i * n + j]);
+        }
+        Ainv[i * n + kk] = -f;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int j = 0; j < n; ++j) Ainv[kk * n + j] = (j == kk) ? piv : Ainv[kk * n + j] * piv;
+      }
+      __syncthreads();
+    }
+  }
+  // PCG init (fem.cpp:335-365): u = lift, r = b − A u
+  const SLev L0 = lev[0];
+  const int m = m0;
+  double bb = 0.0, rr0 = 0.0;
+  for (int i = threadIdx.x; i < N0; i += blockDim.x) {
+    const int y = i / L0.n0, x = i - y * L0.n0;
+    const double gs = (bc == OSC_BC_FLOWCELL && x == 0) ? 1.0 : 0.0;
+    double bi;
+    if (is_dir(bc, m, x, y)) {
+      bi = gs;
+      u[i] = gs;
+      L0.r[i] = 0.0;
+    } else {
+      const int tri = 2 * (x < m && y < m) + (x > 0 && y < m) + 2 * (x > 0 && y > 0) + (x < m && y > 0);
+      const double h = 1.0 / m;
+      bi = forcing ? tri * (fval * (0.5 * h * h) / 3.0) : 0.0;
+      if (bc == OSC_BC_FLOWCELL && x == 1) bi -= L0.E[i - 1] * 1.0;  // raw coupling to u = 1 at x = 0
+      u[i] = 0.0;
+      L0.r[i] = bi;
+      rr0 += bi * bi;
+    }
+    bb += bi * bi;
+  }
+  const double bnorm = sqrt(block_sum_s(bb));
+  double rel = sqrt(block_sum_s(rr0)) / bnorm;
+  int it = 0, status = 0;
+  const int64_t cap64 = (int64_t)max_iter_factor * N0;
+  const int cap = (int)(cap64 < 0x7fffffff ? cap64 : 0x7fffffff);
+  if (rel > tol) {
+    vcycle_smem(lev, nlev, Ainv, bc);
+    double rz = 0.0;
+    for (int i = threadIdx.x; i < N0; i += blockDim.x) {
+      p[i] = L0.z[i];
+      rz += L0.r[i] * L0.z[i];
+    }
+    rz = block_sum_s(rz);
+    for (;;) {
+      if (it >= cap) {
+        status = OSC_ERR_SOLVER;
+        break;
+      }
+      ++it;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      double pap = 0.0;
+      for (int y = warp; y < L0.n0; y += nw)
+        for (int x = lane; x < L0.n0; x += 32) {
+          const int i = y * L0.n0 + x;
+          const Sten st = sten_smem(L0, x, y, bc);
+          pap += p[i] * (st.d * p[i] + offd_smem(st, p, i, L0.n0));
+        }
+      const double alpha = rz / block_sum_s(pap);
+      double rr = 0.0;
+      for (int y = warp; y < L0.n0; y += nw)
+        for (int x = lane; x < L0.n0; x += 32) {
+        const int i = y * L0.n0 + x;
+        const Sten st = sten_smem(L0, x, y, bc);
+        u[i] = fma(alpha, p[i], u[i]);
+        const double rn = fma(-alpha, st.d * p[i] + offd_smem(st, p, i, L0.n0), L0.r[i]);
+        L0.r[i] = rn;
+        rr += rn * rn;
+      }
+      rel = sqrt(block_sum_s(rr)) / bnorm;
+      if (rel <= tol) break;
+      if (!isfinite(rel)) {
+        status = OSC_ERR_SOLVER;
+        break;
+      }
+      vcycle_smem(lev, nlev, Ainv, bc);
+      double rzn = 0.0;
+      for (int i = threadIdx.x; i < N0; i += blockDim.x) rzn += L0.r[i] * L0.z[i];
+      rzn = block_sum_s(rzn);
+      const double beta = rzn / rz;
+      rz = rzn;
+      for (int i = threadIdx.x; i < N0; i += blockDim.x) p[i] = fma(beta, p[i], L0.z[i]);
+      __syncthreads();
+    }
+  }
+  (void)s_go;
+  if (threadIdx.x == 0) {
+    flags[b * F_NFLAGS + F_ACTIVE] = 0;
+    flags[b * F_NFLAGS + F_ITERS] = it;
+    flags[b * F_NFLAGS + F_STATUS] = status;
+    scal[b * S_NSCAL + S_REL] = rel;
+    scal[b * S_NSCAL + S_BNORM] = bnorm;
+  }
+}
+
 __global__ void mark_active_failed_kernel(int B, int* flags) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && flags[b * F_NFLAGS + F_ACTIVE]) {
@@ -1101,6 +1453,21 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
     ~TagGuard() { c->tag.clear(); }
   } tg{ctx};
   ctx->tag = std::to_string(w.m);
+  SolverLevel& L0 = w.lev[0];
+  const Geo g0 = geo_of(L0);
+  w.r_cur = L0.r;
+  static const bool small_off = std::getenv("OSC_NO_SMALL_PCG") != nullptr;
+  if (w.m <= 64 && w.hist_cap == 0 && !small_off) {
+    // whole solve CTA-resident (one CTA per sample, one launch)
+    int nl = 0;
+    const size_t sm = small_smem_bytes(w.m, &nl);
+    OSC_CUDA(cudaFuncSetAttribute(small_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    KScope ks(ctx, "small_pcg");
+    small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, nl, bc, prob->forcing, prob->forcing_value, prob->tol,
+                                               prob->max_iter_factor, L0.k, w.u, w.flags, w.scal);
+    OSC_CUDA(cudaGetLastError());
+    return;
+  }
   {  // hierarchy: injected k (fem.cpp:241-244) + coarsest Cholesky (fem.cpp:255-272)
     KScope ks(ctx, "mg_setup", w.nlev);
     for (int l = 0; l + 1 < w.nlev; ++l) {
@@ -1109,12 +1476,13 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
       inject_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(geo_of(L), geo_of(C), L.k, C.k);
     }
     const SolverLevel& C = w.lev[w.nlev - 1];
-    coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), bc, B, C.k, w.chol);
+    if (w.nc <= 32)
+      coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(geo_of(C), bc, B, C.k, w.chol);
+    else
+      coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), bc, B, C.k, w.chol);
     OSC_CUDA(cudaGetLastError());
   }
-  SolverLevel& L0 = w.lev[0];
-  const Geo g0 = geo_of(L0);
-  w.r_cur = L0.r;
+
   OSC_CUDA(cudaMemsetAsync(w.n_active, 0, sizeof(int), st));
   {
     KScope ks(ctx, "pcg_init");

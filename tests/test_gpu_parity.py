@@ -249,3 +249,34 @@ def test_reference_seam_demo(P, ctx):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_multikernel_path_on_small_grid(P, ctx):
+    """Small grids (m ≤ 64) run the CTA-resident solver; the streaming multi-kernel solver must give
+    the same QoIs there too (forced with OSC_NO_SMALL_PCG in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2306_13493_b200 as P
+from oracle import oracle as O
+api = P.api
+port = O.Port()
+for bc, qoi in [(0, 0), (1, 2), (0, 3)]:
+    model = api.CovarianceModel.matern(1.0, 0.1, 0.5)
+    prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind(qoi)), bc=api.BC(bc))
+    opt = api.EstimatorOptions(seed=4)
+    plan = api.make_level_plan(2, 1.0 / 8, prob, opt)
+    d = api.LevelDraws()
+    api.run_level_draws(plan, api.GridSpec.square(16), False, False, prob, opt, 0, 5, d)
+    sl = np.sqrt(np.maximum(plan.op.eigenvalues, 0))
+    qf, qc, _, _ = port.coupled(32, plan.op.n, sl, None, True, 4, 2, 0, 5, bc=bc, qoi=qoi)
+    rel = max(np.max(np.abs(d.q_fine[:5] - qf) / np.abs(qf)), np.max(np.abs(d.q_coarse[:5] - qc) / np.abs(qc)))
+    assert rel < 1e-7, (bc, qoi, rel)
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OSC_NO_SMALL_PCG="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr

@@ -177,9 +177,7 @@ def run_reference(args, W):
     cores = os.cpu_count() or 1
     port = O.Port()
     ref = O.Ref() if os.path.exists(O.REF_SO) else None
-    per_step = cores  # one coupled sample per host core per step (bounded sample)
-    if W["m"] <= 256:
-        per_step = cores * max(1, int(4096 // (W["m"] * W["m"] // 64 + 1)))
+    per_step = cores * max(1, int(2e6 // (W["m"] + 1) ** 2))  # bounded sample per step
     times, kind = [], "port"
     t_budget = time.time() + 240.0
     if W.get("ce_only"):
@@ -385,9 +383,11 @@ def main():
         from oracle import oracle as O
         cores = os.cpu_count() or 1
         ref = O.Ref() if os.path.exists(O.REF_SO) else None
-        dt, kind = cpu_reference_step(W, cores, cores, 0, O.Port(), ref)
-        cpu = {"value": cores / dt, "unit": "samples/s", "cores": cores, "kind": kind,
-               "sample": f"{cores} coupled samples of the same workload, one per host thread ({dt:.1f} s)"}
+        per_core = max(1, int(2e6 // (m + 1) ** 2))  # bounded sample: a few seconds of CPU work
+        nsamp = cores * per_core
+        dt, kind = cpu_reference_step(W, cores, nsamp, 0, O.Port(), ref)
+        cpu = {"value": nsamp / dt, "unit": "samples/s", "cores": cores, "kind": kind,
+               "sample": f"{nsamp} samples of the same workload over {cores} host threads ({dt:.1f} s)"}
 
     if rank == 0:
         line = {

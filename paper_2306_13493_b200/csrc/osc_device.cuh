@@ -115,6 +115,11 @@ __device__ __forceinline__ void dft_r(double2* v) {
   else dft8(v);
 }
 
+// Shared-memory FFT index padding: one spare slot per 8 complex values, so the stride-8 writes of
+// the first radix-8 stage (and the strided reads of later stages) spread across banks.
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+__host__ __device__ __forceinline__ int fpad_len(int n) { return n + (n >> 3) + 1; }
+
 // One in-place Stockham stage (radix R, current sub-length Ns) of a length-n transform held
 // in shared memory x[0..n), executed by T = n/E threads (lt = local thread id) that each own
 // E/R butterflies. tw[t] = exp(+2πi t/n). Caller syncs before and after.
@@ -129,7 +134,7 @@ __device__ __forceinline__ void stockham_stage(double2* x, int n, int Ns, int lt
   for (int g = 0; g < G; ++g) {
     const int j = lt + g * T;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[g][r] = x[j + r * nR];
+    for (int r = 0; r < R; ++r) v[g][r] = x[fpad(j + r * nR)];
     if (Ns > 1) {
       const int k = j & (Ns - 1);
       const int step = k * (n / (Ns * R));
@@ -145,7 +150,7 @@ __device__ __forceinline__ void stockham_stage(double2* x, int n, int Ns, int lt
     const int k = j & (Ns - 1);
     const int base = (j - k) * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[base + r * Ns] = v[g][r];
+    for (int r = 0; r < R; ++r) x[fpad(base + r * Ns)] = v[g][r];
   }
 }
 

@@ -116,3 +116,26 @@ def test_config_errors(P):
                             api.EstimatorOptions())
     with pytest.raises(api.ConfigError):
         api.EmbeddingOperator(api.GridSpec.square(4), 0, np.zeros(10), 1.0)
+
+
+def test_embedding_error_when_no_spd_padding(P):
+    """build_operator exhausts the padding schedule → EmbeddingError (embedding.cpp:142-149)."""
+    api = P.api
+    with pytest.raises(api.EmbeddingError):
+        api.build_operator(api.GridSpec.square(4), api.CovarianceModel.matern(1.0, 2.0, 1.5))
+
+
+def test_padded_embedding_sizes(P, ref):
+    """Padding J (smooth periodisation) matches the pristine reference; n = 2(m+J) factors into 2,3,5."""
+    api = P.api
+    for m, lam, nu in [(4, 1.0, 1.5), (8, 0.5, 3.5), (8, 1.0, 1.5), (16, 0.3, 1.5)]:
+        op = api.build_operator(api.GridSpec.square(m), api.CovarianceModel.matern(1.0, lam, nu))
+        r = ref.build_operator(m, 0, 1.0, lam, nu)
+        assert op.padding[0] == r.J
+        e = r.eigenvalues()
+        assert np.max(np.abs(op.eigenvalues - e)) <= 1e-10 * np.max(np.abs(e))
+        v = op.n
+        for f in (2, 3, 5):
+            while v % f == 0:
+                v //= f
+        assert v == 1

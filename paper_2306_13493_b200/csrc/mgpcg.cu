@@ -1169,6 +1169,83 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
   }
 }
 
+
+// ---- CTA-resident tail of the V-cycle (levels with m ≤ 32) ---------------------------------------------
+// On large solves the coarsest few levels are launch/latency-bound (≈ 20 µs per kernel whatever
+// their size); one CTA per sample runs the whole sub-V-cycle from level ls down in shared memory:
+// edge weights rebuilt from the injected k of each level, the coarsest inverse read from the setup.
+constexpr int SUB_THREADS = 256;
+__global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int nlev, int bc,
+                                                                 const double* __restrict__ k_ls,
+                                                                 const double* __restrict__ r_ls,
+                                                                 double* __restrict__ z_out,
+                                                                 const double* __restrict__ chol,
+                                                                 const int* flags) {
+  extern __shared__ double smem[];
+  __shared__ SLev lev[12];
+  const int b = blockIdx.x;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int N_ls = (m_ls + 1) * (m_ls + 1);
+  const double* kb = k_ls + (int64_t)b * N_ls;
+  double* cur = smem;
+  {
+    int g = m_ls;
+    for (int l = 0; l < nlev; ++l) {
+      const int n0 = g + 1, N = n0 * n0;
+      if (threadIdx.x == 0) lev[l] = SLev{cur, cur + N, cur + 2 * N, cur + 3 * N, g, n0, N};
+      cur += 4 * N;
+      g /= 2;
+    }
+  }
+  double* Ainv = cur;
+  __syncthreads();
+  constexpr double third = 1.0 / 3.0;
+  for (int l = 0; l < nlev; ++l) {
+    const SLev L = lev[l];
+    const int st = 1 << l;
+    auto K = [&](int x, int y) { return __ldg(kb + (int64_t)(y * st) * (m_ls + 1) + x * st); };
+    for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
+      const int y = i / L.n0, x = i - y * L.n0, m = L.m;
+      double e = 0.0, n = 0.0;
+      if (x < m) {
+        const double lo = y < m ? (K(x, y) + K(x + 1, y) + K(x + 1, y + 1)) * third : 0.0;
+        const double up = y > 0 ? (K(x, y - 1) + K(x + 1, y) + K(x, y)) * third : 0.0;
+        e = -0.5 * (lo + up);
+      }
+      if (y < m) {
+        const double up = x < m ? (K(x, y) + K(x + 1, y + 1) + K(x, y + 1)) * third : 0.0;
+        const double lo = x > 0 ? (K(x - 1, y) + K(x, y) + K(x, y + 1)) * third : 0.0;
+        n = -0.5 * (up + lo);
+      }
+      L.E[i] = e;
+      L.N[i] = n;
+    }
+  }
+  {
+    const int nc = lev[nlev - 1].N_;
+    const double* X = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
+    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Ainv[i] = X[i];
+  }
+  const double* rb = r_ls + (int64_t)b * N_ls;
+  for (int i = threadIdx.x; i < N_ls; i += blockDim.x) lev[0].r[i] = rb[i];
+  __syncthreads();
+  vcycle_smem(lev, nlev, Ainv, bc);
+  double* zb = z_out + (int64_t)b * N_ls;
+  for (int i = threadIdx.x; i < N_ls; i += blockDim.x) zb[i] = lev[0].z[i];
+}
+
+size_t sub_smem_bytes(int m_ls, int nlev) {
+  size_t tot = 0;
+  int g = m_ls, nc = 0;
+  for (int l = 0; l < nlev; ++l) {
+    const size_t N = (size_t)(g + 1) * (g + 1);
+    tot += 4 * N * sizeof(double);
+    nc = (int)N;
+    g /= 2;
+  }
+  return tot + (size_t)nc * nc * sizeof(double);
+}
+
 __global__ void mark_active_failed_kernel(int B, int* flags) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && flags[b * F_NFLAGS + F_ACTIVE]) {
@@ -1414,7 +1491,13 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     OSC_CUDA(cudaGetLastError());
     return;
   }
-  for (int l = 0; l + 1 < w.nlev; ++l) {
+  // first level handled by the CTA-resident tail (m ≤ 32, at least two levels below it)
+  static const bool sub_off = std::getenv("OSC_NO_SUB_VCYCLE") != nullptr;
+  int ls = w.nlev - 1;
+  if (!sub_off)
+    for (int l = 1; l < w.nlev - 1; ++l)
+      if (w.lev[l].m <= 32) { ls = l; break; }
+  for (int l = 0; l + 1 < w.nlev && l < ls; ++l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     if (l > 0 || !fused_down) {
@@ -1424,12 +1507,19 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     KScope ks(ctx, l == 0 ? "mg_restrict.L0" : "mg_restrict.Lc");
     restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, C.r, w.flags);
   }
-  {
+  if (ls < w.nlev - 1) {
+    const SolverLevel& S = w.lev[ls];
+    const int nl = w.nlev - ls;
+    const size_t sm = sub_smem_bytes(S.m, nl);
+    OSC_CUDA(cudaFuncSetAttribute(sub_vcycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    KScope ks(ctx, "mg_sub_vcycle");
+    sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, S.k, S.r, S.z2, w.chol, w.flags);
+  } else {
     const SolverLevel& C = w.lev[w.nlev - 1];
     KScope ks(ctx, "mg_coarse_solve");
     coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
   }
-  for (int l = w.nlev - 2; l >= 0; --l) {
+  for (int l = ls - 1; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     KScope ks(ctx, l == 0 ? "mg_smooth_up.L0" : "mg_smooth_up.Lc");

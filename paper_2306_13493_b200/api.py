@@ -287,6 +287,37 @@ class EmbeddingOperator:
                                  coarse=coarse, exp=exp, truncated=self.truncation_k > 0)
 
 
+@dataclass
+class SmoothingErrorStats:
+    mean: float
+    variance: float
+
+
+def smoothing_error_estimate(op: "EmbeddingOperator", k: int, n_samples: int, seed: int,
+                             ctx: Optional[Context] = None, chunk: int = 64) -> SmoothingErrorStats:
+    """Monte Carlo estimate of E‖Z − Z̃‖∞ (embedding.cpp:205-228): Z and Z̃ share the device ξ of
+    NormalStream(seed, 0, i); Z̃ drops the k smallest eigenvalues. Both fields come from the
+    device CE path; the sup-norm and the Welford update run on the host in index order."""
+    if n_samples < 2:
+        raise ConfigError("smoothing_error_estimate: need at least 2 samples")
+    ctx = ctx or default_context()
+    m = op.grid.m(0)
+    lev = op.device_level(ctx, k)
+    mean, m2 = 0.0, 0.0
+    for c0 in range(0, n_samples, chunk):
+        cnt = min(chunk, n_samples - c0)
+        full = lev.sample_fields(None, count=cnt, seed=seed, ell=0, index0=c0, fine=True)
+        smooth = lev.sample_fields(None, count=cnt, seed=seed, ell=0, index0=c0, fine=True,
+                                   truncated=k > 0)
+        sup = np.max(np.abs(full - smooth), axis=1)
+        for j, v in enumerate(sup):
+            i = c0 + j
+            d = v - mean
+            mean += d / (i + 1)
+            m2 += d * (v - mean)
+    return SmoothingErrorStats(mean, m2 / (n_samples - 1))
+
+
 class DeviceLevel:
     """An osc_level: √λ (full and truncated) resident on one device."""
 
@@ -856,3 +887,52 @@ def mlmc_estimate(problem: ProblemSpec, opt: EstimatorOptions, h0: float, eps: f
     if initial_levels < 1:
         raise ConfigError("mlmc_estimate: need at least one level")
     return _estimate_adaptive(problem, opt, h0, eps, initial_levels, True, **kw)
+
+
+# ---- rate fits (estimators.cpp:420-485) -------------------------------------------------------------------
+@dataclass
+class RatePoint:
+    h: float = 0.0
+    mean_abs_y: float = 0.0
+    var_y: float = 0.0
+    cost: float = 0.0
+
+
+@dataclass
+class RateFit:
+    alpha: float = 0.0
+    c_alpha: float = 0.0
+    beta: float = 0.0
+    c_beta: float = 0.0
+    gamma: float = 0.0
+    c_gamma: float = 0.0
+
+
+def fit_rates(data: Sequence[RatePoint], warnings: Optional[list] = None) -> RateFit:
+    """Least-squares log-log fits of |E Y|, V[Y] and cost against h (estimators.cpp:428-485);
+    non-positive points are dropped per series (noted in `warnings`), < 3 survivors is an error."""
+    if len(data) < 3:
+        raise ConfigError("fit_rates: need at least 3 levels")
+
+    def fit(hs, vs, name):
+        xs, ys = [], []
+        for h, v in zip(hs, vs):
+            if not (v > 0.0) or not math.isfinite(v):
+                if warnings is not None:
+                    warnings.append(f"fit_rates: dropped non-positive {name} point at h = {h}; ")
+                continue
+            xs.append(math.log(h))
+            ys.append(math.log(v))
+        if len(xs) < 3:
+            raise ConfigError("fit_rates: fewer than 3 positive points for a series")
+        mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
+        sxx = sum((x - mx) ** 2 for x in xs)
+        sxy = sum((x - mx) * (y - my) for x, y in zip(xs, ys))
+        slope = sxy / sxx
+        return slope, math.exp(my - slope * mx)
+
+    h = [p.h for p in data]
+    a, ca = fit(h, [p.mean_abs_y for p in data], "|mean Y|")
+    b, cb = fit(h, [p.var_y for p in data], "var Y")
+    g, cg = fit(h, [p.cost for p in data], "cost")
+    return RateFit(a, ca, b, cb, -g, cg)

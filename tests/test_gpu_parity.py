@@ -281,3 +281,46 @@ print("ok")
     env = dict(os.environ, OSC_NO_SMALL_PCG="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+
+def test_smoothing_error_estimate_vs_reference(P, ctx, ref):
+    """smoothing_error_estimate (embedding.cpp:205-228) on the device CE vs the pristine reference."""
+    api = P.api
+    from oracle import oracle as O
+    m = 16
+    r = ref.build_operator(m, O.SEP_EXP, 1.0, 0.1, 1.0)
+    op = api.EmbeddingOperator(api.GridSpec.square(m), r.J, r.eigenvalues(), 1.0)
+    k = op.s // 2
+    g = api.smoothing_error_estimate(op, k, 40, seed=5, ctx=ctx)
+    # the reference, sample by sample (same ξ, same truncation mask from the same eigenvalues)
+    tr = r.truncated(k)
+    sups = []
+    for i in range(40):
+        xi = ref.normals(5, 0, i, r.s)
+        sups.append(np.max(np.abs(r.restrict(r.sample(xi), m) - tr.restrict(tr.sample(xi), m))))
+    assert abs(g.mean - np.mean(sups)) < 1e-10 * np.mean(sups)
+    assert abs(g.variance - np.var(sups, ddof=1)) < 1e-8 * np.var(sups, ddof=1)
+    assert api.smoothing_error_estimate(op, 0, 4, seed=5, ctx=ctx).mean == 0.0  # k = 0 → Z = Z̃
+
+
+def test_edge_cases(P, ctx):
+    """Empty ranges, single samples and argument errors at the C-ABI."""
+    api = P.api
+    model = api.CovarianceModel.separable_exponential(1.0, 0.2)
+    prob = api.ProblemSpec(model)
+    opt = api.EstimatorOptions(seed=1)
+    plan = api.make_level_plan(1, 1.0 / 4, prob, opt)  # m = 8 → coarse 4 (coarsest direct solve)
+    d = api.LevelDraws()
+    api.run_level_draws(plan, api.GridSpec.square(4), False, False, prob, opt, 3, 3, d, ctx=ctx)
+    assert len(d) == 3 and np.all(d.q_fine == 0)  # empty range extends the slots only
+    api.run_level_draws(plan, api.GridSpec.square(4), False, False, prob, opt, 3, 4, d, ctx=ctx)
+    assert d.q_fine[3] != 0 and np.all(d.iters_coarse[3:4] >= 1)
+    with pytest.raises(api.ConfigError):
+        api.run_level_draws(plan, api.GridSpec.square(3), False, False, prob, opt, 0, 2, d, ctx=ctx)
+    # m = 4: the whole grid is the coarsest level — PCG with the exact inverse converges in one step
+    u, it, _ = api.assemble_and_solve(4, np.zeros((1, 25)), prob, ctx=ctx)
+    assert it[0] == 1
+    bad = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Point, x=1.5))
+    with pytest.raises(api.ConfigError):
+        api.run_level_draws(plan, None, False, False, bad, opt, 0, 1, d, ctx=ctx)

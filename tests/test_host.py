@@ -139,3 +139,17 @@ def test_padded_embedding_sizes(P, ref):
             while v % f == 0:
                 v //= f
         assert v == 1
+
+
+def test_fit_rates(P):
+    api = P.api
+    pts = [api.RatePoint(h, 0.3 * h, 2.0 * h ** 2, 5.0 * h ** -2) for h in (1 / 8, 1 / 16, 1 / 32, 1 / 64)]
+    f = api.fit_rates(pts)
+    assert abs(f.alpha - 1) < 1e-12 and abs(f.beta - 2) < 1e-12 and abs(f.gamma - 2) < 1e-12
+    assert abs(f.c_alpha - 0.3) < 1e-12
+    w = []
+    pts[0].mean_abs_y = 0.0
+    f = api.fit_rates(pts, w)
+    assert w and abs(f.alpha - 1) < 1e-12
+    with pytest.raises(api.ConfigError):
+        api.fit_rates(pts[:2])

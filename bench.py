@@ -335,6 +335,18 @@ def main():
                     launches=dom_launches, avg_launch_ms=dom_ms / max(dom_launches, 1),
                     alg_bytes_per_launch=alg_bytes / max(dom_launches, 1),
                     bytes_per_node=per_node, sample_launches=launches_of(sample_iters))
+        # measured DRAM traffic of the same kernel (ncu --set full, profiles/ncu_traffic.json),
+        # scaled to this run's node-launches like `achieved`
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f).get(base)
+            if tr:
+                nl = (mg + 1) ** 2 * launches_of(sample_iters)
+                roof["traffic"] = tr["dram_bytes_per_node"] * nl / max(dom_launches, 1)
+                roof["traffic_source"] = tr["source"]
+                roof["traffic_over_algorithmic"] = tr["dram_bytes_per_node"] / per_node
+        except (OSError, ValueError, KeyError):
+            pass
     # every classified kernel's achieved bandwidth (same accounting), for DESIGN.md
     per_kernel = {}
     for name, (nl, tms) in kstats.items():

@@ -367,7 +367,14 @@ def main():
     if not args.no_e2e:
         s = lev.s
         pool = min(B, 8)
-        buf = api.PinnedBuffer((B, s))
+        try:
+            buf = api.PinnedBuffer((B, s))
+            pinned = True
+        except MemoryError:  # e.g. 8 ranks × 8.6 GB on a small host: pageable staging instead
+            buf = type("Pageable", (), {})()
+            buf.array = np.empty((B, s))
+            buf.free = lambda: None
+            pinned = False
         # ξ rows for the step from the device Philox stream of a pool of indices (outside timing)
         tmp = np.empty((pool, s))
         lib.osc_normals(ctx.h, opt.seed, W["ell"], 0, pool, s, tmp.ctypes.data)
@@ -393,7 +400,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": k_e2e * B * world / (ems / 1000.0), "unit": "samples/s",
                "h2d_bytes_per_step": 8 * s * B, "d2h_bytes_per_step": 8 * 2 * B + 4 * 3 * B + 40,
-               "xi": f"host pinned, {pool} distinct Philox rows cycled over the batch", "steps": k_e2e}
+               "xi": f"host {'pinned' if pinned else 'pageable'}, {pool} distinct Philox rows cycled over the batch",
+               "steps": k_e2e}
         buf.free()
 
     cpu = None

@@ -37,9 +37,9 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_rows_kernel(
     uint32_t ell, uint64_t index0, int n, int NT, int P, int cs, const double2* __restrict__ tw,
     double2* __restrict__ inter) {
   extern __shared__ double2 smem[];
-  const int T = n / E;                      // threads per transform
-  const int t = threadIdx.x / T;            // transform slot in this CTA
-  const int lt = threadIdx.x - t * T;       // lane within the transform
+  const int T = n / E;                      // threads per transform (power of two)
+  const int t = threadIdx.x >> (31 - __clz(T));  // transform slot in this CTA
+  const int lt = threadIdx.x & (T - 1);          // lane within the transform
   const int rp = blockIdx.x * NT + t;       // row pair
   const int b = blockIdx.y;                 // sample within the chunk
   const bool valid = rp < n / 2;
@@ -94,15 +94,16 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
     double* __restrict__ out_coarse, int* __restrict__ bad_flag) {
   extern __shared__ double2 smem[];
   const int T = n / E;
-  const int t = threadIdx.x / T;
-  const int lt = threadIdx.x - t * T;
+  const int t = threadIdx.x >> (31 - __clz(T));
+  const int lt = threadIdx.x & (T - 1);
   const int b = blockIdx.y;
   const int j0 = blockIdx.x * NT;
   const double2* src = inter + ((int64_t)b * P + j0) * n;
   const int ncols = min(NT, P - j0);
   const int ld = fpad_len(n);
+  const int ln = 31 - __clz(n);
   for (int idx = threadIdx.x; idx < NT * n; idx += blockDim.x) {
-    const int tt = idx / n, q1 = idx - tt * n;
+    const int tt = idx >> ln, q1 = idx & (n - 1);
     smem[tt * ld + fpad(q1)] = (idx < ncols * n) ? __ldg(src + idx) : make_double2(0.0, 0.0);
   }
   __syncthreads();
@@ -114,8 +115,9 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
   double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
   double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
   int bad = 0;
+  const int lnt = 31 - __clz(NT);  // NT is a power of two
   for (int idx = threadIdx.x; idx < NT * n_rows; idx += blockDim.x) {
-    const int tt = idx % NT, i = idx / NT;
+    const int tt = idx & (NT - 1), i = idx >> lnt;
     const int j = j0 + tt;
     if (j >= P) continue;
     const int p1 = i * cs, p0 = j * cs;
@@ -149,7 +151,7 @@ CeGeom cols_geom(int n, int P) {
   CeGeom g;
   g.E = elems_for(n);
   g.T = n / g.E;
-  g.NT = std::min(std::max(1, 256 / g.T), P);
+  g.NT = std::max(1, 256 / g.T);  // power of two; columns beyond P are masked
   g.threads = g.NT * g.T;
   g.smem = sizeof(double2) * (size_t)g.NT * fpad_len(n);
   return g;

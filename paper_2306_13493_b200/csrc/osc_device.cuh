@@ -125,7 +125,7 @@ __host__ __device__ __forceinline__ int fpad_len(int n) { return n + (n >> 3) + 
 // E/R butterflies. tw[t] = exp(+2πi t/n). Caller syncs before and after.
 template <int E, int R>
 __device__ __forceinline__ void stockham_stage(double2* x, int n, int Ns, int lt,
-                                               const double2* __restrict__ tw) {
+                                               const double2* __restrict__ tw, int tw_shift) {
   constexpr int G = E / R;
   const int T = n / E;
   const int nR = n / R;
@@ -137,7 +137,7 @@ __device__ __forceinline__ void stockham_stage(double2* x, int n, int Ns, int lt
     for (int r = 0; r < R; ++r) v[g][r] = x[fpad(j + r * nR)];
     if (Ns > 1) {
       const int k = j & (Ns - 1);
-      const int step = k * (n / (Ns * R));
+      const int step = k << tw_shift;  // k · n/(Ns·R), all powers of two
 #pragma unroll
       for (int r = 1; r < R; ++r) v[g][r] = cmul(v[g][r], __ldg(&tw[r * step]));
     }
@@ -159,18 +159,21 @@ __device__ __forceinline__ void stockham_stage(double2* x, int n, int Ns, int lt
 // (data staged) and after (data consumed).
 template <int E>
 __device__ __forceinline__ void fft_smem(double2* x, int n, int lt, const double2* __restrict__ tw) {
-  int Ns = 1;
-  while (Ns * E <= n) {
-    stockham_stage<E, E>(x, n, Ns, lt, tw);
+  constexpr int LE = E == 8 ? 3 : (E == 4 ? 2 : 1);
+  const int ln = 31 - __clz(n);  // n is a power of two
+  int Ns = 1, lns = 0;
+  while (lns + LE <= ln) {
+    stockham_stage<E, E>(x, n, Ns, lt, tw, ln - lns - LE);
     __syncthreads();
-    Ns *= E;
+    Ns <<= LE;
+    lns += LE;
   }
-  const int rem = n / Ns;
+  const int rem = ln - lns;  // log2 of the remaining radix
   if constexpr (E >= 4) {
-    if (rem == 4) { stockham_stage<E, 4>(x, n, Ns, lt, tw); __syncthreads(); return; }
+    if (rem == 2) { stockham_stage<E, 4>(x, n, Ns, lt, tw, ln - lns - 2); __syncthreads(); return; }
   }
   if constexpr (E >= 2) {
-    if (rem == 2) { stockham_stage<E, 2>(x, n, Ns, lt, tw); __syncthreads(); }
+    if (rem == 1) { stockham_stage<E, 2>(x, n, Ns, lt, tw, ln - lns - 1); __syncthreads(); }
   }
 }
 

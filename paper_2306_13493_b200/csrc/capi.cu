@@ -126,6 +126,11 @@ int osc_ctx_create(int device, osc_ctx** out) {
       OSC_CUDA(cudaSetDevice(device));
       OSC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       OSC_CUDA(cudaHostAlloc(&c->h_pinned_int, 64, cudaHostAllocDefault));
+      OSC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        OSC_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+        OSC_CUDA(cudaEventCreateWithFlags(&c->ev_ce_done[i], cudaEventDisableTiming));
+      }
     } catch (...) {
       delete c;
       throw;
@@ -143,6 +148,11 @@ void osc_ctx_destroy(osc_ctx* c) {
                     &c->out_i, &c->tmp_host_stage, &c->sums, &c->solver.mem})
     b->release();
   if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_ce_done[i]) cudaEventDestroy(c->ev_ce_done[i]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -321,14 +331,29 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     const size_t budget = budget_of(c);
     int64_t Bmax = std::max<int64_t>(1, (int64_t)(budget / per));
     Bmax = std::min<int64_t>(Bmax, 1 << 16);
-    const int64_t nchunks = (count + Bmax - 1) / Bmax;
+    int64_t nchunks = (count + Bmax - 1) / Bmax;
+    // host ξ: at least two chunks, so chunk i+1's H2D copy (copy stream, double-buffered) runs
+    // under chunk i's solve; device ξ / Philox: one chunk when it fits
+    if (xi_host && count >= 2) nchunks = std::max<int64_t>(nchunks, 2);
     const int Bc = (int)((count + nchunks - 1) / nchunks);
     c->fields_fine.ensure(sizeof(double) * Nf * Bc);
     if (has_coarse) c->fields_coarse.ensure(sizeof(double) * Nc * Bc);
     c->out_q.ensure(sizeof(double) * 2 * Bc);
     c->out_i.ensure(sizeof(int) * 2 * Bc);
     c->sums.ensure(sizeof(double) * 8);
-    if (xi_host) c->xi_dev.ensure(sizeof(double) * L->s * Bc);
+    if (xi_host) c->xi_dev.ensure(2 * sizeof(double) * L->s * Bc);
+    auto xi_buf = [&](int64_t chunk) { return c->xi_dev.as<double>() + (chunk & 1) * L->s * Bc; };
+    auto issue_copy = [&](int64_t chunk) {  // H2D of chunk `chunk` on the copy stream
+      const int64_t a = chunk * Bc;
+      if (a >= count) return;
+      const int64_t nb = std::min<int64_t>(Bc, count - a);
+      if (chunk >= 2)  // the CE of chunk-2 used this buffer
+        OSC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_ce_done[chunk & 1], 0));
+      OSC_CUDA(cudaMemcpyAsync(xi_buf(chunk), xi + a * L->s, sizeof(double) * L->s * nb,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+      OSC_CUDA(cudaEventRecord(c->ev_copied[chunk & 1], c->copy_stream));
+    };
+    if (xi_host) issue_copy(0);
     double* d_qf = c->out_q.as<double>();
     double* d_qc = d_qf + Bc;
     int* d_bad = c->out_i.as<int>();
@@ -341,10 +366,11 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     for (int64_t c0 = 0; c0 < count; c0 += Bc) {
       const int B = (int)std::min<int64_t>(Bc, count - c0);
       const double* xi_chunk = nullptr;
+      const int64_t chunk = c0 / Bc;
       if (xi) {
         if (xi_host) {
-          h2d(c, c->xi_dev.p, xi + c0 * L->s, sizeof(double) * L->s * B);
-          xi_chunk = c->xi_dev.as<double>();
+          OSC_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[chunk & 1], 0));
+          xi_chunk = xi_buf(chunk);
         } else {
           xi_chunk = xi + c0 * L->s;
         }
@@ -358,6 +384,10 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
       } else {
         ce_sample_launch(c, L, sq_f, xi_chunk, seed, ell, idx0, B, true, kf, nullptr, d_bad);
         ce_sample_launch(c, L, sq_c, xi_chunk, seed, ell, idx0, B, true, nullptr, kc, d_bad);
+      }
+      if (xi_host) {  // ξ buffer consumed: start the next chunk's copy under this chunk's solves
+        OSC_CUDA(cudaEventRecord(c->ev_ce_done[chunk & 1], c->stream));
+        issue_copy(chunk + 1);
       }
       // fine solve + QoI
       solver_prepare(c, m, B, 0);

@@ -111,6 +111,9 @@ struct Ctx {
   DevBuf ce_inter, xi_dev, fields_fine, fields_coarse, out_q, out_i, tmp_host_stage, sums;
   SolverWork solver;
   int* h_pinned_int = nullptr;  // small pinned staging for n_active
+  cudaStream_t copy_stream = nullptr;           // host-ξ H2D overlapped with the previous chunk's solve
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_ce_done[2] = {nullptr, nullptr};
   int stat_class(const char* name);
   void flush_stats();
 };

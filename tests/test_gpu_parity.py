@@ -376,3 +376,35 @@ def test_cfg4_full_size_parity(P, ctx, port):
     print(f"true relative residual: gpu {gpu_rel:.3e} ({it[0]} it), reference port {port_rel:.3e} ({ito} it)")
     assert rc == 0 and gpu_rel <= max(3.0 * port_rel, 1e-10)
     assert np.all(U[0, :] == 0) and np.all(U[:, 0] == 0)
+
+
+def test_dist_shard_nccl_single_rank(P, ctx):
+    """The multi-GPU plumbing (dist.Shard: contiguous shards, NCCL all-gather of slots, all-reduce of
+    level sums) on a real NCCL group of one rank: draws are identical to the unsharded call."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2306_13493_b200.dist import Shard, level_sums, moments_from_sums
+    api = P.api
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    created = not dist.is_initialized()
+    if created:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1.0, 0.1))
+        opt = api.EstimatorOptions(seed=2)
+        plan = api.make_level_plan(1, 1.0 / 8, prob, opt)
+        a, b = api.LevelDraws(), api.LevelDraws()
+        cg = api.GridSpec.square(8)
+        api.run_level_draws(plan, cg, False, False, prob, opt, 0, 12, a, ctx=ctx)
+        sh = Shard()
+        api.run_level_draws(plan, cg, False, False, prob, opt, 0, 12, b, ctx=ctx, dist=sh)
+        assert np.array_equal(a.q_fine, b.q_fine) and np.array_equal(a.q_coarse, b.q_coarse)
+        s = sh.all_reduce_sum(level_sums(b.q_fine, b.q_coarse, 0.0, 0.5))
+        n, my, vy, mq, vq = moments_from_sums(s, 0.0, 0.5)
+        st = api.summarize_draws(b, True)
+        assert n == 12 and abs(my - st.mean_y) < 1e-12 and abs(vy - st.var_y) < 1e-10
+    finally:
+        if created:
+            dist.destroy_process_group()

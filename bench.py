@@ -66,15 +66,16 @@ def workload(cfg: str):
     raise SystemExit(f"unknown config {cfg}")
 
 
-def algorithmic_bytes_per_sample(W, n):
+def algorithmic_bytes_per_sample(W, n, it=None):
     """B = B_ce + B_solve(m) + B_solve(m/2), B_solve(m) = (m+1)²(200 + 251 it),
-    B_ce (device ξ, √λ amortised over the batch) = 8 s/B + 32 n (n/2+1) + 8 (N_f + N_c)."""
+    B_ce (device ξ, √λ amortised over the batch) = 8 s/B + 32 n (n/2+1) + 8 (N_f + N_c).
+    `it` overrides the basis iteration counts (fine, coarse) with measured ones."""
     m = W["m"]
     s = n * n
     Nf, Nc = (m + 1) ** 2, (m // 2 + 1) ** 2
     b_ce = 8 * s / W["batch"] + (32 * n * (n // 2 + 1) if 16 * n * (n // 2 + 1) > 227 * 1024 else 0) + \
         8 * (Nf + (Nc if W["coupled"] else 0))
-    itf, itc = W["it"]
+    itf, itc = W["it"] if it is None else it
     b = b_ce + Nf * (200 + 251 * itf)
     if W["coupled"]:
         b += Nc * (200 + 251 * itc)
@@ -221,6 +222,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="4")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--coarse-op", default="galerkin", choices=["galerkin", "rediscretize"],
+                    help="MG coarse operators: exact Galerkin (default) or the reference's rediscretisation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mlmc", action="store_true",
@@ -257,7 +260,8 @@ def main():
     model = (api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]) if W["family"] == "matern"
              else api.CovarianceModel.separable_exponential(W["sigma2"], W["lam"]))
     problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind(W["qoi"])), bc=api.BC(W["bc"]))
-    opt = api.EstimatorOptions(seed=1)
+    opt = api.EstimatorOptions(seed=1, solver=api.SolverOptions(
+        coarse_operator=api.CoarseOperator[args.coarse_op.capitalize()]))
     t_setup = time.perf_counter()
     plan = api.make_level_plan(W["ell"], 1.0 / (m >> W["ell"]), problem, opt)
     t_setup = time.perf_counter() - t_setup
@@ -359,8 +363,15 @@ def main():
     n = lev.n
     b_sample = algorithmic_bytes_per_sample(W, n)
     pipeline = {"basis": "SURVEY 8(d) B per coupled sample", "bytes_per_sample": b_sample,
+                "basis_iters": list(W["it"]),
                 "roofline_samples_per_s_per_gpu": hbm * 1e9 / b_sample,
                 "frac": value / world / (hbm * 1e9 / b_sample)}
+    # the same byte model at this run's measured mean iteration counts (the basis fixes the
+    # flow-cell counts of the reference algorithm; the preconditioner changes the count)
+    it_meas = (iters_timed[0] / (args.steps * B), iters_timed[1] / (args.steps * B) if W["coupled"] else 0)
+    b_meas = algorithmic_bytes_per_sample(W, n, it_meas)
+    pipeline["measured_iters"] = [round(x, 2) for x in it_meas]
+    pipeline["frac_at_measured_iters"] = value / world / (hbm * 1e9 / b_meas)
 
     # e2e: same metric through the C-ABI with HOST ξ (pinned), H2D + D2H inside the timed region
     e2e = None
@@ -427,7 +438,7 @@ def main():
                        "parallelism": f"dp{world} (contiguous sample shards)",
                        "l2": "inputs larger than L2 (>= 40 GB touched per step)" if m >= 1024 else
                        "per-step working set exceeds L2 (batch)",
-                       "setup_s": round(t_setup, 2),
+                       "setup_s": round(t_setup, 2), "coarse_op": args.coarse_op,
                        "mean_iters_fine": iters_timed[0] / (args.steps * B),
                        "mean_iters_coarse": iters_timed[1] / (args.steps * B) if W["coupled"] else None},
             "roofline": roof, "kernel_gbs": per_kernel, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
@@ -447,7 +458,8 @@ def run_mlmc(args, api, ctx, torch, rank):
     model = api.CovarianceModel.separable_exponential(1.0, args.lam)
     problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Flux), bc=api.BC.FlowCell)
     opt = api.EstimatorOptions(seed=1, smoothing=api.SmoothingRule.Adaptive, smoothing_lstar_only=True,
-                               l_max=4)
+                               l_max=4, solver=api.SolverOptions(
+                                   coarse_operator=api.CoarseOperator[args.coarse_op.capitalize()]))
     t0 = time.perf_counter()
     rep = api.mlmc_estimate(problem, opt, 1.0 / 16, args.eps, initial_levels=5, ctx=ctx)
     ctx.synchronize()

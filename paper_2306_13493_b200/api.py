@@ -435,10 +435,22 @@ class ProblemSpec:
     bc: BC = BC.FlowCell
 
 
+class CoarseOperator(enum.IntEnum):
+    """Coarse-grid operators of the MG preconditioner (include/oscfield_b200.h OSC_COARSE_*).
+
+    Galerkin is the exact PᵀAP, i.e. coarse P1 with triangle-averaged conductivity. Rediscretize is
+    the reference's injected-k re-assembly (fem.cpp:241-244). Either way the same fine system is
+    solved to the same tolerance.
+    """
+    Galerkin = 0
+    Rediscretize = 1
+
+
 @dataclass
 class SolverOptions:
     tol: float = 1e-10
     max_iter_factor: int = 10
+    coarse_operator: CoarseOperator = CoarseOperator.Galerkin
 
 
 class SmoothingRule(enum.IntEnum):
@@ -466,7 +478,7 @@ class EstimatorOptions:
 def _problem_struct(problem: ProblemSpec, solver: SolverOptions) -> L.Problem:
     return L.Problem(int(problem.bc), int(problem.forcing), float(problem.forcing_value),
                      int(problem.qoi.kind), float(problem.qoi.x), float(problem.qoi.y),
-                     float(solver.tol), int(solver.max_iter_factor))
+                     float(solver.tol), int(solver.max_iter_factor), int(solver.coarse_operator))
 
 
 # ---- batched FEM stages (fem.hpp) ---------------------------------------------------------------------

@@ -85,44 +85,98 @@ struct Sten {
   double d, e, w, n, s;  // raw diagonal (1 on Dirichlet rows) and eliminated couplings
 };
 
-// Stencil at tile-local (lx, ly) of k tile `kt` (leading dim ld) for global node (gx, gy).
-// Bitwise identical to the per-node formulas in the header (same operands, same order),
-// so the coupling seen from both ends of an edge is the same double (A stays symmetric).
-__device__ __forceinline__ Sten stencil_at(const double* kt, int ld, int lx, int ly, int gx, int gy,
-                                           int m, int bc) {
-  auto K = [&](int dx, int dy) { return kt[(ly + dy) * ld + lx + dx]; };
-  const double k00 = K(0, 0);
-  double e = 0.0, w = 0.0, n = 0.0, s = 0.0;
-  if (gx < m) e = -0.5 * ((gy < m ? (k00 + K(1, 0) + K(1, 1)) / 3.0 : 0.0) +
-                          (gy > 0 ? (K(0, -1) + K(1, 0) + k00) / 3.0 : 0.0));
-  if (gx > 0) w = -0.5 * ((gy < m ? (K(-1, 0) + k00 + K(0, 1)) / 3.0 : 0.0) +
-                          (gy > 0 ? (K(-1, -1) + k00 + K(-1, 0)) / 3.0 : 0.0));
-  if (gy < m) n = -0.5 * ((gx < m ? (k00 + K(1, 1) + K(0, 1)) / 3.0 : 0.0) +
-                          (gx > 0 ? (K(-1, 0) + k00 + K(0, 1)) / 3.0 : 0.0));
-  if (gy > 0) s = -0.5 * ((gx < m ? (K(0, -1) + K(1, 0) + k00) / 3.0 : 0.0) +
-                          (gx > 0 ? (K(-1, -1) + K(0, -1) + k00) / 3.0 : 0.0));
+// ---- setup: coarse-level operators -------------------------------------------------------------------
+// Level l ≥ 1 keeps its raw edge weights E, N in HBM (before Dirichlet elimination; built once per
+// solve). They come from per-triangle conductivities Klo(I,J), Kup(I,J) of the level's cells.
+// The triangles of cell (i,j) are lower (i,j),(i+1,j),(i+1,j+1) and upper (i,j),(i+1,j+1),(i,j+1)
+// (fem.cpp:62-63). The two coarse-operator modes differ only in those conductivities:
+//  * REDISCRETIZE is the reference: vertex means of the injected nodal k (fem.cpp:241-244).
+//  * GALERKIN is A_c = Pᵀ A P exactly. The coarse P1 basis functions have constant gradients on
+//    each coarse triangle, so Pᵀ A P is the coarse P1 matrix whose triangle conductivity is the
+//    mean of the 4 equal-area fine triangles inside it:
+//      coarse lower(I,J) = lower(2I,2J), lower(2I+1,2J), upper(2I+1,2J), lower(2I+1,2J+1)
+//      coarse upper(I,J) = upper(2I,2J), lower(2I,2J+1), upper(2I,2J+1), upper(2I+1,2J+1)
+//    (tests/test_host.py::test_galerkin_coarse_operator_identity checks this against Pᵀ A P).
+//    It is still a 5-point stencil, and it cuts the PCG iterations about 2× on rough fields.
+// Triangle conductivities of level l+1 are written cell-wise ([J·n0c + I]) into that level's z (lo)
+// and z2 (up) buffers, which are free until the solve starts.
+// mode: OSC_COARSE_* ; src_lo/src_up = level-l triangles (GALERKIN, l ≥ 1) or null (from k0);
+// stride = 2^(l+1) in level-0 nodes (REDISCRETIZE; 1 builds level 0's own triangles).
+__global__ void __launch_bounds__(NT) coarsen_tri_kernel(int mode, Geo g0, Geo gf, Geo gc, int stride,
+                                                         const double* __restrict__ k0,
+                                                         const double* __restrict__ src_lo,
+                                                         const double* __restrict__ src_up,
+                                                         double* __restrict__ clo, double* __restrict__ cup) {
+  const int b = blockIdx.y;
+  const int mc = gc.m;
+  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (ic >= (int64_t)mc * mc) return;
+  const int J = (int)(ic / mc), I = (int)(ic - (int64_t)J * mc);
+  constexpr double third = 1.0 / 3.0;
+  const double* kb = k0 + (int64_t)b * g0.N;
+  double lo, up;
+  if (mode == OSC_COARSE_REDISCRETIZE) {
+    auto K = [&](int x, int y) { return __ldg(kb + (int64_t)(y * stride) * g0.n0 + (int64_t)x * stride); };
+    lo = (K(I, J) + K(I + 1, J) + K(I + 1, J + 1)) * third;
+    up = (K(I, J) + K(I + 1, J + 1) + K(I, J + 1)) * third;
+  } else {
+    double fl[4], fu[4];  // fine cells (2I,2J), (2I+1,2J), (2I,2J+1), (2I+1,2J+1)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 2 * I + (c & 1), j = 2 * J + (c >> 1);
+      if (src_lo) {
+        fl[c] = __ldg(src_lo + (int64_t)b * gf.N + (int64_t)j * gf.n0 + i);
+        fu[c] = __ldg(src_up + (int64_t)b * gf.N + (int64_t)j * gf.n0 + i);
+      } else {
+        auto K = [&](int x, int y) { return __ldg(kb + (int64_t)y * g0.n0 + x); };
+        fl[c] = (K(i, j) + K(i + 1, j) + K(i + 1, j + 1)) * third;
+        fu[c] = (K(i, j) + K(i + 1, j + 1) + K(i, j + 1)) * third;
+      }
+    }
+    lo = 0.25 * (fl[0] + fl[1] + fu[1] + fl[3]);
+    up = 0.25 * (fu[0] + fl[2] + fu[2] + fu[3]);
+  }
+  const int64_t o = (int64_t)b * gc.N + (int64_t)J * gc.n0 + I;
+  clo[o] = lo;
+  cup[o] = up;
+}
+
+// Raw edge weights of one level from its triangle conductivities:
+//   E(x,y) = −½[Klo(x,y) + Kup(x,y−1)],  N(x,y) = −½[Kup(x,y) + Klo(x−1,y)],  zero off the grid.
+// With REDISCRETIZE conductivities this is bit-identical to edges_pair on the injected k.
+__global__ void __launch_bounds__(NT) edges_kernel(Geo g, const double* __restrict__ klo,
+                                                   const double* __restrict__ kup, double* __restrict__ E,
+                                                   double* __restrict__ Nn) {
+  const int b = blockIdx.y;
+  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (i >= g.N) return;
+  const int y = (int)(i / g.n0), x = (int)(i - (int64_t)y * g.n0), m = g.m;
+  const double* lo = klo + (int64_t)b * g.N;
+  const double* up = kup + (int64_t)b * g.N;
+  double e = 0.0, n = 0.0;
+  if (x < m) e = -0.5 * ((y < m ? lo[i] : 0.0) + (y > 0 ? up[i - g.n0] : 0.0));
+  if (y < m) n = -0.5 * ((x < m ? up[i] : 0.0) + (x > 0 ? lo[i - 1] : 0.0));
+  E[(int64_t)b * g.N + i] = e;
+  Nn[(int64_t)b * g.N + i] = n;
+}
+
+// 5-point row of node (x, y) from stored raw edges (Dirichlet rows identity, couplings to
+// Dirichlet nodes eliminated).
+__device__ __forceinline__ Sten sten_edges(const double* E, const double* Nn, int n0, int m, int x, int y, int bc) {
   Sten st;
-  if (is_dir(bc, m, gx, gy)) {
+  if (is_dir(bc, m, x, y)) {
     st.d = 1.0;
     st.e = st.w = st.n = st.s = 0.0;
     return st;
   }
+  const int i = y * n0 + x;
+  const double e = E[i], w = x > 0 ? E[i - 1] : 0.0, n = Nn[i], s = y > 0 ? Nn[i - n0] : 0.0;
   st.d = -(e + w + n + s);
-  st.e = is_dir(bc, m, gx + 1, gy) ? 0.0 : e;
-  st.w = is_dir(bc, m, gx - 1, gy) ? 0.0 : w;
-  st.n = is_dir(bc, m, gx, gy + 1) ? 0.0 : n;
-  st.s = is_dir(bc, m, gx, gy - 1) ? 0.0 : s;
+  st.e = is_dir(bc, m, x + 1, y) ? 0.0 : e;
+  st.w = is_dir(bc, m, x - 1, y) ? 0.0 : w;
+  st.n = is_dir(bc, m, x, y + 1) ? 0.0 : n;
+  st.s = is_dir(bc, m, x, y - 1) ? 0.0 : s;
   return st;
-}
-
-// ---- setup: k injection to the next level (fem.cpp:241-244) -----------------------------------------
-__global__ void __launch_bounds__(NT) inject_kernel(Geo gf, Geo gc, const double* __restrict__ kf,
-                                                    double* __restrict__ kc) {
-  const int b = blockIdx.y;
-  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (ic >= gc.N) return;
-  const int J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
-  kc[(int64_t)b * gc.N + ic] = kf[(int64_t)b * gf.N + (int64_t)(2 * J) * gf.n0 + 2 * I];
 }
 
 // Coarsest operator and its explicit inverse, one warp per sample. The reference factors the
@@ -133,25 +187,19 @@ __global__ void __launch_bounds__(NT) inject_kernel(Geo gf, Geo gc, const double
 // the per-thread Cholesky + inverse below.
 constexpr int CF_WARPS = 2;
 __global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(Geo g, int bc, int B,
-                                                                          const double* __restrict__ k,
+                                                                          const double* __restrict__ E,
+                                                                          const double* __restrict__ Nn,
                                                                           double* __restrict__ chol) {
   __shared__ double aug[CF_WARPS][32][65];  // row i: A(i, 0..n−1) | I(i, 0..n−1), padded
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * CF_WARPS + w;
   if (b >= B) return;
   const int n = (int)g.N, n0 = g.n0, m = g.m;
-  const double* kb = k + (int64_t)b * n;
   double(*A)[65] = aug[w];
   if (lane < n) {
     for (int j = 0; j < 2 * n; ++j) A[lane][j] = (j == n + lane) ? 1.0 : 0.0;
     const int gy = lane / n0, gx = lane - gy * n0;
-    double kt[9];
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int x = gx + dx, y = gy + dy;
-        kt[(dy + 1) * 3 + dx + 1] = (x >= 0 && x < n0 && y >= 0 && y < n0) ? kb[y * n0 + x] : 0.0;
-      }
-    const Sten st = stencil_at(kt, 3, 1, 1, gx, gy, m, bc);
+    const Sten st = sten_edges(E + (int64_t)b * n, Nn + (int64_t)b * n, n0, m, gx, gy, bc);
     A[lane][lane] = st.d;
     if (gx + 1 < n0) A[lane][lane + 1] = st.e;
     if (gx > 0) A[lane][lane - 1] = st.w;
@@ -175,24 +223,16 @@ __global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(Geo g
 }
 
 // Dense Cholesky of the coarsest operator, one thread per sample (fem.cpp:255-272).
-__global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restrict__ k,
-                                     double* __restrict__ chol) {
+__global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restrict__ E,
+                                     const double* __restrict__ Nn, double* __restrict__ chol) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int n = (int)g.N, n0 = g.n0, m = g.m;
   double* L = chol + (int64_t)b * 2 * n * n;
-  const double* kb = k + (int64_t)b * n;
   for (int i = 0; i < n * n; ++i) L[i] = 0.0;
-  // stencil from a zero-padded 3×3 neighbourhood of k
   for (int i = 0; i < n; ++i) {
     const int gy = i / n0, gx = i - gy * n0;
-    double kt[9];
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int x = gx + dx, y = gy + dy;
-        kt[(dy + 1) * 3 + dx + 1] = (x >= 0 && x < n0 && y >= 0 && y < n0) ? kb[y * n0 + x] : 0.0;
-      }
-    const Sten st = stencil_at(kt, 3, 1, 1, gx, gy, m, bc);
+    const Sten st = sten_edges(E + (int64_t)b * n, Nn + (int64_t)b * n, n0, m, gx, gy, bc);
     L[i * n + i] = st.d;
     if (gx + 1 < n0) L[i * n + i + 1] = st.e;
     if (gx > 0) L[i * n + i - 1] = st.w;
@@ -412,6 +452,53 @@ __device__ __forceinline__ Pair offd_pair(const Sten2& st, Pair vm, Pair v0, Pai
               st.b.e * va_e + st.b.w * v0.a + st.b.n * vp.b + st.b.s * vm.b};
 }
 
+// Raw edge weights (E, N) of consecutive rows r0, r0+1, … of one warp strip, with one row of loads
+// in flight. EN = false (level 0) rebuilds them from nodal k (three k rows in registers); EN = true
+// (levels ≥ 1) loads the stored E/N rows of the coarse operator. Every kernel uses only N of the
+// first row, so the k row below it is never loaded.
+template <bool INT, bool EN>
+struct EdgeRows;
+
+template <bool INT>
+struct EdgeRows<INT, false> {
+  const double* kb;
+  int xa, n0, m, r;
+  Pair k0, k1, kq;
+  __device__ __forceinline__ EdgeRows(const double* k, const double*, int xa_, int n0_, int m_, int r0)
+      : kb(k), xa(xa_), n0(n0_), m(m_), r(r0) {
+    k0 = Pair{0.0, 0.0};
+    k1 = ld2<INT>(kb, xa, r0, n0);
+    kq = ld2<INT>(kb, xa, r0 + 1, n0);
+  }
+  __device__ __forceinline__ void next(Pair& E, Pair& N) {
+    const Pair kp = kq;
+    kq = ld2<INT>(kb, xa, r + 2, n0);
+    edges_pair<INT>(k0, k1, kp, xa, r, m, E, N);
+    k0 = k1;
+    k1 = kp;
+    ++r;
+  }
+};
+
+template <bool INT>
+struct EdgeRows<INT, true> {
+  const double *Eb, *Nb;
+  int xa, n0, r;
+  Pair eq, nq;
+  __device__ __forceinline__ EdgeRows(const double* E, const double* N, int xa_, int n0_, int, int r0)
+      : Eb(E), Nb(N), xa(xa_), n0(n0_), r(r0) {
+    eq = ld2<INT>(Eb, xa, r0, n0);
+    nq = ld2<INT>(Nb, xa, r0, n0);
+  }
+  __device__ __forceinline__ void next(Pair& E, Pair& N) {
+    E = eq;
+    N = nq;
+    eq = ld2<INT>(Eb, xa, r + 1, n0);
+    nq = ld2<INT>(Nb, xa, r + 1, n0);
+    ++r;
+  }
+};
+
 struct PairCtx {
   int b, lane, m, n0, xa, xb, y0, y1;
   bool outa, outb;
@@ -614,26 +701,26 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
 }
 
 // ---- pre-smoother from z = 0 (coarse levels; level 0 of the first V-cycle): red then black ------
-template <bool INT>
-__device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const double* __restrict__ k,
+template <bool INT, bool EN>
+__device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const double* __restrict__ ka_,
+                                                         const double* __restrict__ kb_,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ z, const int* flags, const PairCtx& c) {
   PAIR_UNPACK
 
-  const double *kb = k + off, *rb = r + off;
+  const double* rb = r + off;
   const Pair zero{0.0, 0.0};
-  Pair ka = ld2<INT>(kb, xa, y0 - 2, n0), kb1 = ld2<INT>(kb, xa, y0 - 1, n0);
+  EdgeRows<INT, EN> er(ka_ + off, EN ? kb_ + off : nullptr, xa, n0, m, y0 - 2);
   Pair Nt, Ed;
-  edges_pair<INT>(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  er.next(Ed, Nt);
   Pair r0 = zero, zrm = zero, zr0 = zero;
   Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};
-  Pair kq = ld2<INT>(kb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
+  Pair rq = ld2<INT>(rb, xa, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
-    const Pair kc = kq, r1 = rq;
-    kq = ld2<INT>(kb, xa, t + 3, n0);
+    const Pair r1 = rq;
     rq = ld2<INT>(rb, xa, t + 2, n0);
     Pair E1, N1;
-    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    er.next(E1, N1);
     const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     const Pair zrp = RED_IS_A(t + 1) ? Pair{r1.a * rcp64(st1.a.d), 0.0} : Pair{0.0, r1.b * rcp64(st1.b.d)};
     const double zr0_e = shdn(zr0.a), zr0_w = shup(zr0.b);
@@ -647,105 +734,54 @@ __device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const d
       if (outa) out[xa] = zv.a;
       if (outb) out[xb] = zv.b;
     }
-    ka = kb1; kb1 = kc; Nt = N1;
+    Nt = N1;
     r0 = r1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
   }  return 0.0;
 }
 
-__global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const double* __restrict__ k,
+// coefficients: EN = false → a = nodal k (level 0); EN = true → a = E, b = N (levels ≥ 1)
+template <bool EN>
+__global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const double* __restrict__ a,
+                                                         const double* __restrict__ bN,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ z, const int* flags) {
   PAIR_PROLOGUE
-  if (interior) smooth_down_kernel_body<true>(g, bc, k, r, z, flags, c);
-  else smooth_down_kernel_body<false>(g, bc, k, r, z, flags, c);
+  if (interior) smooth_down_kernel_body<true, EN>(g, bc, a, bN, r, z, flags, c);
+  else smooth_down_kernel_body<false, EN>(g, bc, a, bN, r, z, flags, c);
 }
 
 // ---- residual restriction rc = Pᵀ(r − A z) after the red-black pre-smoother (fem.cpp:168-195).
 // After the black sweep the residual vanishes on black nodes and equals −Σ A z_black on red
 // nodes, so rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]; zero at coarse Dirichlet nodes.
-// Lane l owns fine columns xa = 2I, xb = 2I+1 of coarse column I; lanes 0 and 31 are halo.
-__global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
-                                                      const double* __restrict__ k,
-                                                      const double* __restrict__ z,
-                                                      double* __restrict__ rc, const int* flags) {
-  const int b = blockIdx.z;
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
+// Lane l owns fine columns xa = 2I, xb = 2I+1 of coarse column I (the column-pair layout of the
+// marching kernels); lanes 0 and 31 are halo.
+template <bool INT, bool EN>
+__device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
+                                              const double* __restrict__ cb, const double* __restrict__ z,
+                                              double* __restrict__ rc, int b, int I, bool outI, int J0, int J1) {
   const int m = g.m, n0 = g.n0, mc = gc.m;
-  const int I = strip * 30 - 1 + lane;
-  const bool outI = lane >= 1 && lane < 31 && I <= mc;
-  const int xa = 2 * I, xb = 2 * I + 1;
-  const int lyc = coarse_rows_per_warp(gc.m);
-  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
+  const int xa = 2 * I;
   const int64_t off = (int64_t)b * g.N;
-  const double *kb = k + off, *zb = z + off;
-  constexpr double third = 1.0 / 3.0;
-  // edges at both columns of row y from k rows y−1, y, y+1 (a: xa, b: xb)
-  auto edges2 = [&](double kma, double kmb, double k0a, double k0b, double kpa, double kpb, int y,
-                    double& Ea, double& Eb, double& Na, double& Nb) {
-    const double k0a_n = shdn(k0a), kpa_n = shdn(kpa), k0b_p = shup(k0b);  // x = xb+1 / xa−1
-    Ea = Eb = Na = Nb = 0.0;
-    if (y >= 0 && y <= m) {
-      if (xa >= 0 && xa < m)
-        Ea = -0.5 * ((y < m ? (k0a + k0b + kpb) * third : 0.0) + (y > 0 ? (kma + k0b + k0a) * third : 0.0));
-      if (xb >= 0 && xb < m)
-        Eb = -0.5 * ((y < m ? (k0b + k0a_n + kpa_n) * third : 0.0) + (y > 0 ? (kmb + k0a_n + k0b) * third : 0.0));
-    }
-    if (y >= 0 && y < m) {
-      if (xa >= 0 && xa <= m)
-        Na = -0.5 * ((xa < m ? (k0a + kpb + kpa) * third : 0.0) + (xa > 0 ? (k0b_p + k0a + kpa) * third : 0.0));
-      if (xb >= 0 && xb <= m)
-        Nb = -0.5 * ((xb < m ? (k0b + kpa_n + kpb) * third : 0.0) + (xb > 0 ? (k0a + k0b + kpb) * third : 0.0));
-    }
-  };
-  // residual at the red node of row y (column xa if y even, xb if odd): −Σ A z_black
-  auto t_red = [&](int y, double Ea, double Eb, double Na, double Nb, double Nma, double Nmb,
-                   double zma, double zmb, double z0a, double z0b, double zpa, double zpb) {
-    const double Eb_w = shup(Eb);     // E at column xa−1
-    const double z0b_w = shup(z0b);   // z at xa−1
-    const double z0a_e = shdn(z0a);   // z at xb+1
-    double t = 0.0;
-    if ((y & 1) == 0) {  // red at xa
-      if (xa >= 0 && xa <= m && y >= 0 && y <= m && !is_dir(bc, m, xa, y)) {
-        const double e = is_dir(bc, m, xa + 1, y) ? 0.0 : Ea, w = is_dir(bc, m, xa - 1, y) ? 0.0 : Eb_w;
-        const double nn = is_dir(bc, m, xa, y + 1) ? 0.0 : Na, s = is_dir(bc, m, xa, y - 1) ? 0.0 : Nma;
-        t = -(e * z0b + w * z0b_w + nn * zpa + s * zma);
-      }
-    } else {  // red at xb
-      if (xb >= 0 && xb <= m && y >= 0 && y <= m && !is_dir(bc, m, xb, y)) {
-        const double e = is_dir(bc, m, xb + 1, y) ? 0.0 : Eb, w = is_dir(bc, m, xb - 1, y) ? 0.0 : Ea;
-        const double nn = is_dir(bc, m, xb, y + 1) ? 0.0 : Nb, s = is_dir(bc, m, xb, y - 1) ? 0.0 : Nmb;
-        t = -(e * z0a_e + w * z0a + nn * zpb + s * zmb);
-      }
-    }
-    return t;
-  };
-  // fine rows y = 2J0−1 … 2J1−1; state: k, z rows y−1, y; N of row y−1
+  const double* zb = z + off;
+  // fine rows y = 2J0−1 … 2J1−1; state: z rows y−1, y (+ y+1 in flight); N of row y−1
   const int ys = 2 * J0 - 1;
-  double kma = ldv<false>(kb, xa, ys - 1, n0), kmb = ldv<false>(kb, xb, ys - 1, n0);
-  double k0a = ldv<false>(kb, xa, ys, n0), k0b = ldv<false>(kb, xb, ys, n0);
-  double zma = ldv<false>(zb, xa, ys - 1, n0), zmb = ldv<false>(zb, xb, ys - 1, n0);
-  double z0a = ldv<false>(zb, xa, ys, n0), z0b = ldv<false>(zb, xb, ys, n0);
-  double Nma, Nmb;
-  {
-    double Ea, Eb;
-    edges2(0.0, 0.0, kma, kmb, k0a, k0b, ys - 1, Ea, Eb, Nma, Nmb);
-  }
+  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, ys - 1);
+  Pair Ed, Nm;
+  er.next(Ed, Nm);
+  Pair zm = ld2<INT>(zb, xa, ys - 1, n0), z0 = ld2<INT>(zb, xa, ys, n0);
+  Pair zq = ld2<INT>(zb, xa, ys + 1, n0);
   double t_prev = 0.0, t_even = 0.0;  // t at (xb, 2J−1) and (xa, 2J)
   double* rcb = rc + (int64_t)b * gc.N;
-  double kqa = ldv<false>(kb, xa, ys + 1, n0), kqb = ldv<false>(kb, xb, ys + 1, n0);
-  double zqa = ldv<false>(zb, xa, ys + 1, n0), zqb = ldv<false>(zb, xb, ys + 1, n0);
   for (int y = ys; y <= 2 * J1 - 1; ++y) {
-    const double kpa = kqa, kpb = kqb, zpa = zqa, zpb = zqb;  // row y+1, prefetched
-    kqa = ldv<false>(kb, xa, y + 2, n0);
-    kqb = ldv<false>(kb, xb, y + 2, n0);
-    zqa = ldv<false>(zb, xa, y + 2, n0);
-    zqb = ldv<false>(zb, xb, y + 2, n0);
-    double Ea, Eb, Na, Nb;
-    edges2(kma, kmb, k0a, k0b, kpa, kpb, y, Ea, Eb, Na, Nb);
-    const double t = t_red(y, Ea, Eb, Na, Nb, Nma, Nmb, zma, zmb, z0a, z0b, zpa, zpb);
-    if ((y & 1) == 0) {
+    const Pair zp = zq;  // row y+1, prefetched
+    zq = ld2<INT>(zb, xa, y + 2, n0);
+    Pair E, N;
+    er.next(E, N);
+    const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
+    // residual at the red node of row y (column a if y even, b if odd): −Σ A z_black
+    const Pair od = offd_pair(st, zm, z0, zp);
+    const double t = RED_IS_A(y) ? -od.a : -od.b;
+    if (RED_IS_A(y)) {
       t_even = t;
     } else {
       const double t_w = shup(t_prev);  // t at (xa−1, 2J−1): previous lane's xb
@@ -756,16 +792,36 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc,
       }
       t_prev = t;
     }
-    kma = k0a; kmb = k0b; k0a = kpa; k0b = kpb;
-    zma = z0a; zmb = z0b; z0a = zpa; z0b = zpb;
-    Nma = Na; Nmb = Nb;
+    zm = z0; z0 = zp; Nm = N;
   }
 }
 
+template <bool EN>
+__global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ ca,
+                                                      const double* __restrict__ cb,
+                                                      const double* __restrict__ z,
+                                                      double* __restrict__ rc, const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int lane = threadIdx.x & 31;
+  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
+  const int I = strip * 30 - 1 + lane;
+  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
+  const int lyc = coarse_rows_per_warp(gc.m);
+  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
+  // interior: fine rows 2J0−2 … 2J1+1 and columns xa(lane 0)−1 … xb(lane 31)+1 are in-grid,
+  // non-Dirichlet nodes with in-grid neighbours
+  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 2 >= 2 &&
+                        2 * J1 + 2 <= g.m - 1;
+  if (interior) restrict_body<true, EN>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
+  else restrict_body<false, EN>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
+}
+
 // ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
-template <bool INT>
+template <bool INT, bool EN>
 __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
-                                                       const double* __restrict__ k,
+                                                       const double* __restrict__ ca,
+                                                       const double* __restrict__ cb,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
                                                        double* __restrict__ z_out,
@@ -774,7 +830,7 @@ __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
                                                        int maxp, unsigned* counter, const PairCtx& c) {
   PAIR_UNPACK
 
-  const double *kb = k + off, *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
+  const double *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
   const int nc0 = gc.n0;
   const Pair zero{0.0, 0.0};
   // Red node of row y after prolongation: z_red + P zc (fem.cpp:144-165). Row y even: red at xa
@@ -802,22 +858,21 @@ __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
   auto ZC = [&](const ZRaw& v, int y) {  // the row's pair: red column prolonged, black column 0
     return RED_IS_A(y) ? Pair{v.z + v.c0, 0.0} : Pair{0.0, v.z + 0.5 * (v.c0 + v.c1)};
   };
-  Pair ka = ld2<INT>(kb, xa, y0 - 2, n0), kb1 = ld2<INT>(kb, xa, y0 - 1, n0);
+  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, y0 - 2);
   Pair zpa = ZC(ZL(y0 - 2), y0 - 2), zpb = ZC(ZL(y0 - 1), y0 - 1);
   Pair Nt, Ed;
-  edges_pair<INT>(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
+  er.next(Ed, Nt);
   Pair r0 = zero, zbm = zero, zb0 = zero;
   Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
-  Pair kq = ld2<INT>(kb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
+  Pair rq = ld2<INT>(rb, xa, y0 - 1, n0);
   ZRaw zq = ZL(y0);
   double rz = 0.0;
   for (int t = y0 - 2; t < y1; ++t) {
-    const Pair kc = kq, r1 = rq, zpc = ZC(zq, t + 2);
-    kq = ld2<INT>(kb, xa, t + 3, n0);
+    const Pair r1 = rq, zpc = ZC(zq, t + 2);
     zq = ZL(t + 3);
     rq = ld2<INT>(rb, xa, t + 2, n0);
     Pair E1, N1;
-    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    er.next(E1, N1);
     const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     // black column of row t+1: (r − Σ A z_red_prolonged)/D
     const Pair odp = offd_pair(st1, zpa, zpb, zpc);
@@ -841,23 +896,27 @@ __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
         rz = fma(r0.b, zv.b, rz);
       }
     }
-    ka = kb1; kb1 = kc; zpa = zpb; zpb = zpc; Nt = N1;
+    zpa = zpb; zpb = zpc; Nt = N1;
     r0 = r1; zbm = zb0; zb0 = zbp1; sr0 = RED_IS_A(t + 1) ? st1.a : st1.b;
   }
   return rz;
 }
 
+// EN = false: level 0 (a = nodal k), also <r, z> → β; EN = true: levels ≥ 1 (a = E, b = N)
+template <bool EN>
 __global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
-                                                       const double* __restrict__ k,
+                                                       const double* __restrict__ a,
+                                                       const double* __restrict__ bN,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
                                                        double* __restrict__ z_out,
-                                                       const double* __restrict__ zc, int finest,
+                                                       const double* __restrict__ zc,
                                                        double* scal, int* flags, double2* partial,
                                                        int maxp, unsigned* counter) {
   PAIR_PROLOGUE
-  const double rz = interior ? smooth_up_kernel_body<true>(g, gc, bc, k, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c) : smooth_up_kernel_body<false>(g, gc, bc, k, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c);
-  if (!finest) return;
+  const int finest = EN ? 0 : 1;
+  const double rz = interior ? smooth_up_kernel_body<true, EN>(g, gc, bc, a, bN, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c) : smooth_up_kernel_body<false, EN>(g, gc, bc, a, bN, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c);
+  if (EN) return;
   double t0, t1;
   if (reduce2_last(rz, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     const double old = scal[b * S_NSCAL + S_RZ];
@@ -996,7 +1055,75 @@ size_t small_smem_bytes(int m, int* nlev_out) {
   return tot + (size_t)nc * nc * sizeof(double) + 64 * sizeof(SLev) + 256;
 }
 
-__global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev, int bc, int forcing,
+// Edge weights E/N of every level of a CTA-resident hierarchy. Level 0 comes from nodal k (global).
+// Level l ≥ 1 comes from its triangle conductivities, built in that level's r (lower) / z (upper)
+// buffers (free until the V-cycle runs):
+//  * REDISCRETIZE: vertex means of the injected k;
+//  * GALERKIN: means of the 4 fine triangles (from k for level 1, from level l−1's r/z after that).
+// Same formulas as coarsen_tri_kernel / edges_kernel.
+__device__ void smem_hierarchy(SLev* lev, int nlev, int coarse_op, const double* __restrict__ k0, int m0) {
+  constexpr double third = 1.0 / 3.0;
+  const int n00 = m0 + 1;
+  auto K = [&](int x, int y, int st) { return __ldg(k0 + (int64_t)(y * st) * n00 + x * st); };
+  for (int l = 1; l < nlev; ++l) {
+    const SLev L = lev[l];
+    const int mc = L.m;
+    for (int ic = threadIdx.x; ic < mc * mc; ic += blockDim.x) {
+      const int J = ic / mc, I = ic - J * mc;
+      double lo, up;
+      if (coarse_op == OSC_COARSE_REDISCRETIZE) {
+        const int st = 1 << l;
+        lo = (K(I, J, st) + K(I + 1, J, st) + K(I + 1, J + 1, st)) * third;
+        up = (K(I, J, st) + K(I + 1, J + 1, st) + K(I, J + 1, st)) * third;
+      } else {
+        double fl[4], fu[4];
+        for (int c = 0; c < 4; ++c) {
+          const int i = 2 * I + (c & 1), j = 2 * J + (c >> 1);
+          if (l == 1) {
+            fl[c] = (K(i, j, 1) + K(i + 1, j, 1) + K(i + 1, j + 1, 1)) * third;
+            fu[c] = (K(i, j, 1) + K(i + 1, j + 1, 1) + K(i, j + 1, 1)) * third;
+          } else {
+            fl[c] = lev[l - 1].r[j * lev[l - 1].n0 + i];
+            fu[c] = lev[l - 1].z[j * lev[l - 1].n0 + i];
+          }
+        }
+        lo = 0.25 * (fl[0] + fl[1] + fu[1] + fl[3]);
+        up = 0.25 * (fu[0] + fl[2] + fu[2] + fu[3]);
+      }
+      L.r[J * L.n0 + I] = lo;
+      L.z[J * L.n0 + I] = up;
+    }
+    __syncthreads();
+  }
+  for (int l = 0; l < nlev; ++l) {
+    const SLev L = lev[l];
+    const int m = L.m;
+    for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
+      const int y = i / L.n0, x = i - y * L.n0;
+      double e = 0.0, n = 0.0;
+      if (l == 0) {
+        if (x < m) {
+          const double lo = y < m ? (K(x, y, 1) + K(x + 1, y, 1) + K(x + 1, y + 1, 1)) * third : 0.0;
+          const double up = y > 0 ? (K(x, y - 1, 1) + K(x + 1, y, 1) + K(x, y, 1)) * third : 0.0;
+          e = -0.5 * (lo + up);
+        }
+        if (y < m) {
+          const double up = x < m ? (K(x, y, 1) + K(x + 1, y + 1, 1) + K(x, y + 1, 1)) * third : 0.0;
+          const double lo = x > 0 ? (K(x - 1, y, 1) + K(x, y, 1) + K(x, y + 1, 1)) * third : 0.0;
+          n = -0.5 * (up + lo);
+        }
+      } else {
+        if (x < m) e = -0.5 * ((y < m ? L.r[i] : 0.0) + (y > 0 ? L.z[i - L.n0] : 0.0));
+        if (y < m) n = -0.5 * ((x < m ? L.z[i] : 0.0) + (x > 0 ? L.r[i - 1] : 0.0));
+      }
+      L.E[i] = e;
+      L.N[i] = n;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev, int bc, int coarse_op, int forcing,
                                                                double fval, double tol, int max_iter_factor,
                                                                const double* __restrict__ kin,
                                                                double* __restrict__ uout, int* flags,
@@ -1022,31 +1149,9 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
   }
   double* Ainv = cur;
   __syncthreads();
-  // edge weights of every level from the injected nodal k (fem.cpp:241-244), same formulas and
-  // operand order as the streaming kernels
-  constexpr double third = 1.0 / 3.0;
-  for (int l = 0; l < nlev; ++l) {
-    const SLev L = lev[l];
-    const int st = 1 << l;
-    auto K = [&](int x, int y) { return __ldg(k0 + (int64_t)(y * st) * (m0 + 1) + x * st); };
-    for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
-      const int y = i / L.n0, x = i - y * L.n0, m = L.m;
-      double e = 0.0, n = 0.0;
-      if (x < m) {
-        const double lo = y < m ? (K(x, y) + K(x + 1, y) + K(x + 1, y + 1)) * third : 0.0;
-        const double up = y > 0 ? (K(x, y - 1) + K(x + 1, y) + K(x, y)) * third : 0.0;
-        e = -0.5 * (lo + up);
-      }
-      if (y < m) {
-        const double up = x < m ? (K(x, y) + K(x + 1, y + 1) + K(x, y + 1)) * third : 0.0;
-        const double lo = x > 0 ? (K(x - 1, y) + K(x, y) + K(x, y + 1)) * third : 0.0;
-        n = -0.5 * (up + lo);
-      }
-      L.E[i] = e;
-      L.N[i] = n;
-    }
-  }
-  __syncthreads();
+  // level-0 edge weights from nodal k (same formulas and operand order as the streaming kernels),
+  // coarse levels from their triangle conductivities (coarsen_tri_kernel / edges_kernel semantics)
+  smem_hierarchy(lev, nlev, coarse_op, k0, m0);
   {  // coarsest operator → in-place Gauss–Jordan inverse (SPD, no pivoting)
     const SLev C = lev[nlev - 1];
     const int n = C.N_;
@@ -1172,11 +1277,14 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
 
 // ---- CTA-resident tail of the V-cycle (levels with m ≤ 32) ---------------------------------------------
 // On large solves the coarsest few levels are launch/latency-bound (≈ 20 µs per kernel whatever
-// their size); one CTA per sample runs the whole sub-V-cycle from level ls down in shared memory:
-// edge weights rebuilt from the injected k of each level, the coarsest inverse read from the setup.
+// their size). One CTA per sample runs the whole sub-V-cycle from level ls down, in shared memory.
+// It reads the stored edge weights of each level and the coarsest inverse from the setup.
 constexpr int SUB_THREADS = 256;
-__global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int nlev, int bc,
-                                                                 const double* __restrict__ k_ls,
+struct SubLevels {
+  const double* E[12];
+  const double* N[12];
+};
+__global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int nlev, int bc, SubLevels sl,
                                                                  const double* __restrict__ r_ls,
                                                                  double* __restrict__ z_out,
                                                                  const double* __restrict__ chol,
@@ -1186,7 +1294,6 @@ __global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int n
   const int b = blockIdx.x;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
   const int N_ls = (m_ls + 1) * (m_ls + 1);
-  const double* kb = k_ls + (int64_t)b * N_ls;
   double* cur = smem;
   {
     int g = m_ls;
@@ -1199,26 +1306,13 @@ __global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int n
   }
   double* Ainv = cur;
   __syncthreads();
-  constexpr double third = 1.0 / 3.0;
   for (int l = 0; l < nlev; ++l) {
     const SLev L = lev[l];
-    const int st = 1 << l;
-    auto K = [&](int x, int y) { return __ldg(kb + (int64_t)(y * st) * (m_ls + 1) + x * st); };
+    const double* Eg = sl.E[l] + (int64_t)b * L.N_;
+    const double* Ng = sl.N[l] + (int64_t)b * L.N_;
     for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
-      const int y = i / L.n0, x = i - y * L.n0, m = L.m;
-      double e = 0.0, n = 0.0;
-      if (x < m) {
-        const double lo = y < m ? (K(x, y) + K(x + 1, y) + K(x + 1, y + 1)) * third : 0.0;
-        const double up = y > 0 ? (K(x, y - 1) + K(x + 1, y) + K(x, y)) * third : 0.0;
-        e = -0.5 * (lo + up);
-      }
-      if (y < m) {
-        const double up = x < m ? (K(x, y) + K(x + 1, y + 1) + K(x, y + 1)) * third : 0.0;
-        const double lo = x > 0 ? (K(x - 1, y) + K(x, y) + K(x, y + 1)) * third : 0.0;
-        n = -0.5 * (up + lo);
-      }
-      L.E[i] = e;
-      L.N[i] = n;
+      L.E[i] = __ldg(Eg + i);
+      L.N[i] = __ldg(Ng + i);
     }
   }
   {
@@ -1405,9 +1499,14 @@ size_t solver_bytes(int m, int B, int hist_cap) {
   int g = m, lev = 0;
   for (;;) {
     const size_t N = (size_t)(g + 1) * (g + 1);
-    tot += N * B * sizeof(double) * (lev == 0 ? 8 : 4);  // level 0: u r r2 z z2 p0 p1 (+k by caller); else k r z z2
+    // level 0: u r r2 z z2 p0 p1 (+k by caller); levels ≥ 1: E N r z z2
+    tot += N * B * sizeof(double) * (lev == 0 ? 8 : 5);
     ++lev;
-    if (g <= 4 || g % 2 != 0) { tot += 2 * N * N * B * sizeof(double); break; }
+    if (g <= 4 || g % 2 != 0) {
+      tot += 2 * N * N * B * sizeof(double);
+      if (lev == 1) tot += 2 * N * B * sizeof(double);  // single level: E N of level 0 for the factor
+      break;
+    }
     g /= 2;
   }
   tot += (size_t)B * (S_NSCAL * 8 + F_NFLAGS * 4 + 8) + (size_t)B * hist_cap * 8;
@@ -1444,8 +1543,11 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   for (int l = 0; l < nl; ++l) {
     SolverLevel& L = w.lev[l];
     const size_t vb = sizeof(double) * L.N * B;
-    L.k = (l > 0) ? (double*)take(vb) : nullptr;  // level 0's k is the caller's buffer
-    L.D = L.E = L.Nw = nullptr;                     // stencils are recomputed from k in-tile
+    L.k = nullptr;  // level 0's k is the caller's buffer; coarse levels keep edge weights instead
+    L.D = nullptr;
+    const bool edges = l > 0 || nl == 1;
+    L.E = edges ? (double*)take(vb) : nullptr;
+    L.Nw = edges ? (double*)take(vb) : nullptr;
     L.r = (double*)take(vb);
     L.z = (double*)take(vb);
     L.z2 = (double*)take(vb);
@@ -1502,18 +1604,29 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     const SolverLevel& C = w.lev[l + 1];
     if (l > 0 || !fused_down) {
       KScope ks(ctx, l == 0 ? "mg_smooth_down.L0" : "mg_smooth_down.Lc");
-      smooth_down_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, w.flags);
+      if (l == 0)
+        smooth_down_kernel<false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.k, nullptr, w.r_cur, L.z, w.flags);
+      else
+        smooth_down_kernel<true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.E, L.Nw, L.r, L.z, w.flags);
     }
     KScope ks(ctx, l == 0 ? "mg_restrict.L0" : "mg_restrict.Lc");
-    restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, C.r, w.flags);
+    if (l == 0)
+      restrict_kernel<false><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, L.z, C.r, w.flags);
+    else
+      restrict_kernel<true><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.z, C.r, w.flags);
   }
   if (ls < w.nlev - 1) {
     const SolverLevel& S = w.lev[ls];
     const int nl = w.nlev - ls;
     const size_t sm = sub_smem_bytes(S.m, nl);
     OSC_CUDA(cudaFuncSetAttribute(sub_vcycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    SubLevels sl{};
+    for (int l = 0; l < nl; ++l) {
+      sl.E[l] = w.lev[ls + l].E;
+      sl.N[l] = w.lev[ls + l].Nw;
+    }
     KScope ks(ctx, "mg_sub_vcycle");
-    sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, S.k, S.r, S.z2, w.chol, w.flags);
+    sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, sl, S.r, S.z2, w.chol, w.flags);
   } else {
     const SolverLevel& C = w.lev[w.nlev - 1];
     KScope ks(ctx, "mg_coarse_solve");
@@ -1523,9 +1636,12 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     KScope ks(ctx, l == 0 ? "mg_smooth_up.L0" : "mg_smooth_up.Lc");
-    smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, l == 0 ? w.r_cur : L.r, L.z, L.z2, C.z2,
-                                                     l == 0 ? 1 : 0, w.scal, w.flags, part,
-                                                     w.max_parts, w.counter);
+    if (l == 0)
+      smooth_up_kernel<false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur, L.z, L.z2,
+                                                              C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
+    else
+      smooth_up_kernel<true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.r, L.z, L.z2,
+                                                             C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
   }
   OSC_CUDA(cudaGetLastError());
 }
@@ -1538,6 +1654,8 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
   cudaStream_t st = ctx->stream;
   double2* part = reinterpret_cast<double2*>(w.partial);
   const int bc = prob->bc;
+  OSC_REQUIRE(prob->coarse_op == OSC_COARSE_GALERKIN || prob->coarse_op == OSC_COARSE_REDISCRETIZE,
+              "solve: unknown coarse_op");
   struct TagGuard {
     Ctx* c;
     ~TagGuard() { c->tag.clear(); }
@@ -1553,23 +1671,34 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
     const size_t sm = small_smem_bytes(w.m, &nl);
     OSC_CUDA(cudaFuncSetAttribute(small_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     KScope ks(ctx, "small_pcg");
-    small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, nl, bc, prob->forcing, prob->forcing_value, prob->tol,
+    small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, nl, bc, prob->coarse_op, prob->forcing, prob->forcing_value, prob->tol,
                                                prob->max_iter_factor, L0.k, w.u, w.flags, w.scal);
     OSC_CUDA(cudaGetLastError());
     return;
   }
-  {  // hierarchy: injected k (fem.cpp:241-244) + coarsest Cholesky (fem.cpp:255-272)
-    KScope ks(ctx, "mg_setup", w.nlev);
+  {  // hierarchy: coarse operators (triangle conductivities → edge weights) + coarsest inverse
+    KScope ks(ctx, "mg_setup", 2 * w.nlev);
+    const int mode = prob->coarse_op;
+    if (w.nlev == 1) {  // single level: level 0's own edges (vertex means of k) for the factor
+      SolverLevel& L = w.lev[0];
+      coarsen_tri_kernel<<<dim3(nblocks((int64_t)L.m * L.m), B), NT, 0, st>>>(
+          OSC_COARSE_REDISCRETIZE, g0, g0, g0, 1, L0.k, nullptr, nullptr, L.z, L.z2);
+      edges_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(g0, L.z, L.z2, L.E, L.Nw);
+    }
     for (int l = 0; l + 1 < w.nlev; ++l) {
-      const SolverLevel& L = w.lev[l];
+      const SolverLevel& F = w.lev[l];
       const SolverLevel& C = w.lev[l + 1];
-      inject_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(geo_of(L), geo_of(C), L.k, C.k);
+      const bool from_k = mode == OSC_COARSE_REDISCRETIZE || l == 0;
+      coarsen_tri_kernel<<<dim3(nblocks((int64_t)C.m * C.m), B), NT, 0, st>>>(
+          mode, g0, geo_of(F), geo_of(C), 2 << l, L0.k, from_k ? nullptr : F.z, from_k ? nullptr : F.z2,
+          C.z, C.z2);
+      edges_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(geo_of(C), C.z, C.z2, C.E, C.Nw);
     }
     const SolverLevel& C = w.lev[w.nlev - 1];
     if (w.nc <= 32)
-      coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(geo_of(C), bc, B, C.k, w.chol);
+      coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(geo_of(C), bc, B, C.E, C.Nw, w.chol);
     else
-      coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), bc, B, C.k, w.chol);
+      coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), bc, B, C.E, C.Nw, w.chol);
     OSC_CUDA(cudaGetLastError());
   }
 

@@ -153,3 +153,75 @@ def test_fit_rates(P):
     assert w and abs(f.alpha - 1) < 1e-12
     with pytest.raises(api.ConfigError):
         api.fit_rates(pts[:2])
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+def test_galerkin_coarse_operator_identity(bc):
+    """The GALERKIN coarse operator used by the solver (mgpcg.cu coarsen_tri_kernel) is exactly
+    Pᵀ A P. The P1 prolongation (fem.cpp:144-165) applied to the Dirichlet-eliminated P1 matrix
+    (fem.cpp:38-138) equals the coarse P1 matrix whose triangle conductivities are the means of the
+    4 fine triangles inside each coarse triangle. The same holds from a coarse level to the next."""
+    sp = pytest.importorskip("scipy.sparse")
+    rng = np.random.default_rng(bc)
+
+    def assemble(m, klo, kup):  # klo/kup[j, i]: triangle conductivities of cell (i, j)
+        n0 = m + 1
+        rows, cols, vals = [], [], []
+        for j in range(m):
+            for i in range(m):
+                for K, tri in ((klo[j, i], [(i, j), (i + 1, j), (i + 1, j + 1)]),
+                               (kup[j, i], [(i, j), (i + 1, j + 1), (i, j + 1)])):
+                    xs = [a / m for a, _ in tri]
+                    ys = [c / m for _, c in tri]
+                    area = 0.5 / m / m
+                    bb = [ys[(a + 1) % 3] - ys[(a + 2) % 3] for a in range(3)]
+                    cc = [xs[(a + 2) % 3] - xs[(a + 1) % 3] for a in range(3)]
+                    for a in range(3):
+                        for c in range(3):
+                            rows.append(tri[a][1] * n0 + tri[a][0])
+                            cols.append(tri[c][1] * n0 + tri[c][0])
+                            vals.append(K * (bb[a] * bb[c] + cc[a] * cc[c]) / (4 * area))
+        return sp.coo_matrix((vals, (rows, cols)), shape=(n0 * n0, n0 * n0)).tocsr()
+
+    def free(m):
+        d = np.zeros((m + 1, m + 1), bool)
+        d[:, 0] = d[:, m] = True
+        if bc == 1:
+            d[0, :] = d[m, :] = True
+        return np.where(~d.ravel())[0]
+
+    def prolong(mf):
+        nf, nc = mf + 1, mf // 2 + 1
+        r, c, v = [], [], []
+        for J in range(nf):
+            for I in range(nf):
+                i = J * nf + I
+                if I % 2 == 0 and J % 2 == 0:
+                    tgt = [((J // 2), I // 2, 1.0)]
+                elif J % 2 == 0:
+                    tgt = [(J // 2, (I - 1) // 2, .5), (J // 2, (I + 1) // 2, .5)]
+                elif I % 2 == 0:
+                    tgt = [((J - 1) // 2, I // 2, .5), ((J + 1) // 2, I // 2, .5)]
+                else:
+                    tgt = [((J - 1) // 2, (I - 1) // 2, .5), ((J + 1) // 2, (I + 1) // 2, .5)]
+                for (a, b2, w) in tgt:
+                    r.append(i), c.append(a * nc + b2), v.append(w)
+        return sp.coo_matrix((v, (r, c)), shape=(nf * nf, nc * nc)).tocsr()
+
+    def coarsen(lo, up):  # mgpcg.cu coarsen_tri_kernel, GALERKIN
+        return (0.25 * (lo[0::2, 0::2] + lo[0::2, 1::2] + up[0::2, 1::2] + lo[1::2, 1::2]),
+                0.25 * (up[0::2, 0::2] + lo[1::2, 0::2] + up[1::2, 0::2] + up[1::2, 1::2]))
+
+    m = 16
+    k = np.exp(1.5 * rng.standard_normal((m + 1, m + 1)))
+    lo = (k[:-1, :-1] + k[:-1, 1:] + k[1:, 1:]) / 3.0
+    up = (k[:-1, :-1] + k[1:, 1:] + k[1:, :-1]) / 3.0
+    for _ in range(2):  # level 0 → 1 and level 1 → 2
+        fi, ci = free(m), free(m // 2)
+        A = assemble(m, lo, up)[fi][:, fi]
+        P = prolong(m)[fi][:, ci]
+        G = (P.T @ A @ P).toarray()
+        lo, up = coarsen(lo, up)
+        Ac = assemble(m // 2, lo, up)[ci][:, ci].toarray()
+        assert np.max(np.abs(G - Ac)) <= 1e-12 * np.max(np.abs(G))
+        m //= 2

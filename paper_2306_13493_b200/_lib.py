@@ -11,7 +11,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libosc_b200.so")
+# OSC_LIB: developer override (A/B builds of the same sources); the default is the in-tree build
+LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 HEADER = os.path.join(ROOT, "include", "oscfield_b200.h")
 SOURCES = ["csrc/capi.cu", "csrc/ce_sample.cu", "csrc/mgpcg.cu", "csrc/setup.cpp"]
 DEPS = SOURCES + ["csrc/osc_internal.cuh", "csrc/osc_device.cuh"]

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "osc_device.cuh"
 #include "osc_internal.cuh"
@@ -623,7 +624,8 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
   Pair pa = ld2<INT>(pb, xa, y0 - 2, n0), pb1 = ld2<INT>(pb, xa, y0 - 1, n0);
   Pair Nt, Ed;
   edges_pair<INT>(zero, ka, kb1, xa, y0 - 2, m, Ed, Nt);
-  Pair rn0 = zero, zrm = zero, zr0 = zero;
+  Pair rn0 = zero;
+  double zrm = 0.0, zr0 = 0.0;        // red z of rows t−1, t (the black entries are 0)
   Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's black column (all the output needs)
   Pair kq = ld2<INT>(kb, xa, y0, n0), pq = ld2<INT>(pb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
   Pair uq = ld2<INT>(u + off, xa, y0 - 2, n0);
@@ -639,15 +641,15 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
     const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     const Pair od1 = offd_pair(st1, pa, pb1, pc);
     const Pair rn1{fma(-alpha, fma(st1.a.d, pb1.a, od1.a), r1.a), fma(-alpha, fma(st1.b.d, pb1.b, od1.b), r1.b)};
-    // z_red on row t+1 (the other column is black → 0)
-    const Pair zrp = RED_IS_A(t + 1) ? Pair{rn1.a * rcp64(st1.a.d), 0.0} : Pair{0.0, rn1.b * rcp64(st1.b.d)};
-    // output row t: black column = (r − Σ A z_red)/D, red column = z_red
-    const double zr0_e = shdn(zr0.a), zr0_w = shup(zr0.b);
-    Pair zv;
-    if (RED_IS_A(t))  // black at xb: east = next lane's xa, west = own xa
-      zv = Pair{zr0.a, (rn0.b - (sb0.e * zr0_e + sb0.w * zr0.a + sb0.n * zrp.b + sb0.s * zrm.b)) * rcp64(sb0.d)};
-    else              // black at xa: east = own xb, west = previous lane's xb
-      zv = Pair{(rn0.a - (sb0.e * zr0.b + sb0.w * zr0_w + sb0.n * zrp.a + sb0.s * zrm.a)) * rcp64(sb0.d), zr0.b};
+    // z_red on row t+1
+    const bool ra0 = RED_IS_A(t), ra1 = !ra0;
+    const double zrp = (ra1 ? rn1.a : rn1.b) * rcp64(ra1 ? st1.a.d : st1.b.d);
+    // output row t: black column = (r − Σ A z_red)/D, red column = z_red. Black at xb (ra0):
+    // east = next lane's xa, west = own xa; black at xa: east = own xb, west = previous lane's xb
+    const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
+    const double zbl = ((ra0 ? rn0.b : rn0.a) - (sb0.e * (ra0 ? zr0_e : zr0) + sb0.w * (ra0 ? zr0 : zr0_w) +
+                                                 sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d);
+    const Pair zv = ra0 ? Pair{zr0, zbl} : Pair{zbl, zr0};
     if (t >= y0) {
       const int64_t row = off + (int64_t)t * n0;
       if (outa) {
@@ -664,7 +666,7 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
       }
     }
     ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
-    rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
+    rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
   }
   return rr;
 }
@@ -675,9 +677,14 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
     int* n_active, double* hist, int hist_cap) {
   PAIR_PROLOGUE
+#ifdef OSC_UD_INTERIOR
+  const double rr = interior ? pcg_update_down_kernel_body<true>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c)
+                             : pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c);
+#else
   // generic body only: the interior specialisation pushes this kernel past 128 registers (spills)
   (void)interior;
   const double rr = pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c);
+#endif
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     const double rel = sqrt(t0) / scal[b * S_NSCAL + S_BNORM];
@@ -713,7 +720,8 @@ __device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const d
   EdgeRows<INT, EN> er(ka_ + off, EN ? kb_ + off : nullptr, xa, n0, m, y0 - 2);
   Pair Nt, Ed;
   er.next(Ed, Nt);
-  Pair r0 = zero, zrm = zero, zr0 = zero;
+  Pair r0 = zero;
+  double zrm = 0.0, zr0 = 0.0;  // red z of rows t−1, t
   Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};
   Pair rq = ld2<INT>(rb, xa, y0 - 1, n0);
   for (int t = y0 - 2; t < y1; ++t) {
@@ -722,21 +730,21 @@ __device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const d
     Pair E1, N1;
     er.next(E1, N1);
     const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
-    const Pair zrp = RED_IS_A(t + 1) ? Pair{r1.a * rcp64(st1.a.d), 0.0} : Pair{0.0, r1.b * rcp64(st1.b.d)};
-    const double zr0_e = shdn(zr0.a), zr0_w = shup(zr0.b);
-    Pair zv;
-    if (RED_IS_A(t))
-      zv = Pair{zr0.a, (r0.b - (sb0.e * zr0_e + sb0.w * zr0.a + sb0.n * zrp.b + sb0.s * zrm.b)) * rcp64(sb0.d)};
-    else
-      zv = Pair{(r0.a - (sb0.e * zr0.b + sb0.w * zr0_w + sb0.n * zrp.a + sb0.s * zrm.a)) * rcp64(sb0.d), zr0.b};
+    const bool ra0 = RED_IS_A(t), ra1 = !ra0;
+    const double zrp = (ra1 ? r1.a : r1.b) * rcp64(ra1 ? st1.a.d : st1.b.d);
+    const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
+    const double zbl = ((ra0 ? r0.b : r0.a) - (sb0.e * (ra0 ? zr0_e : zr0) + sb0.w * (ra0 ? zr0 : zr0_w) +
+                                               sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d);
+    const Pair zv = ra0 ? Pair{zr0, zbl} : Pair{zbl, zr0};
     if (t >= y0) {
       double* out = z + off + (int64_t)t * n0;
       if (outa) out[xa] = zv.a;
       if (outb) out[xb] = zv.b;
     }
     Nt = N1;
-    r0 = r1; zrm = zr0; zr0 = zrp; sb0 = RED_IS_A(t + 1) ? st1.b : st1.a;
-  }  return 0.0;
+    r0 = r1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
+  }
+  return 0.0;
 }
 
 // coefficients: EN = false → a = nodal k (level 0); EN = true → a = E, b = N (levels ≥ 1)
@@ -755,6 +763,24 @@ __global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const
 // nodes, so rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]; zero at coarse Dirichlet nodes.
 // Lane l owns fine columns xa = 2I, xb = 2I+1 of coarse column I (the column-pair layout of the
 // marching kernels); lanes 0 and 31 are halo.
+// −Σ A z_black at the red node of row y: column a (RA, y even) or b (y odd). E/N: row y's raw edges,
+// Nm: row y−1's; zm/z0/zp: z rows y−1, y, y+1. All lanes must call it (shuffles).
+template <bool INT, bool RA>
+__device__ __forceinline__ double red_resid(Pair E, Pair N, Pair Nm, Pair zm, Pair z0, Pair zp, int xa, int y,
+                                            int m, int bc) {
+  const double Ew = shup(E.b);                      // E(xa−1)
+  const double zw = RA ? shup(z0.b) : z0.a;         // z west of the red node
+  const double ze = RA ? z0.b : shdn(z0.a);         // z east
+  const double e0 = RA ? E.a : E.b, w0 = RA ? Ew : E.a, n0_ = RA ? N.a : N.b, s0 = RA ? Nm.a : Nm.b;
+  const double zn = RA ? zp.a : zp.b, zs = RA ? zm.a : zm.b;
+  if (INT) return -(e0 * ze + w0 * zw + n0_ * zn + s0 * zs);
+  const int x = RA ? xa : xa + 1;
+  if (x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y)) return 0.0;
+  const double e = is_dir(bc, m, x + 1, y) ? 0.0 : e0, w = is_dir(bc, m, x - 1, y) ? 0.0 : w0;
+  const double n = is_dir(bc, m, x, y + 1) ? 0.0 : n0_, sv = is_dir(bc, m, x, y - 1) ? 0.0 : s0;
+  return -(e * ze + w * zw + n * zn + sv * zs);
+}
+
 template <bool INT, bool EN>
 __device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
                                               const double* __restrict__ cb, const double* __restrict__ z,
@@ -763,36 +789,35 @@ __device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const doubl
   const int xa = 2 * I;
   const int64_t off = (int64_t)b * g.N;
   const double* zb = z + off;
-  // fine rows y = 2J0−1 … 2J1−1; state: z rows y−1, y (+ y+1 in flight); N of row y−1
+  // fine rows y = 2J0−1 (odd: t at (xb, 2J0−1)), then pairs (2J, 2J+1) for J = J0 … J1−1;
+  // state: z rows y−1, y (+ y+1 in flight), N of row y−1
   const int ys = 2 * J0 - 1;
   EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, ys - 1);
-  Pair Ed, Nm;
-  er.next(Ed, Nm);
+  Pair E, N, Nm;
+  er.next(E, Nm);
   Pair zm = ld2<INT>(zb, xa, ys - 1, n0), z0 = ld2<INT>(zb, xa, ys, n0);
   Pair zq = ld2<INT>(zb, xa, ys + 1, n0);
-  double t_prev = 0.0, t_even = 0.0;  // t at (xb, 2J−1) and (xa, 2J)
   double* rcb = rc + (int64_t)b * gc.N;
-  for (int y = ys; y <= 2 * J1 - 1; ++y) {
-    const Pair zp = zq;  // row y+1, prefetched
+  auto advance = [&](int y, Pair& zp) {  // row y's edges and z row y+1; prefetch z row y+2
+    zp = zq;
     zq = ld2<INT>(zb, xa, y + 2, n0);
-    Pair E, N;
     er.next(E, N);
-    const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
-    // residual at the red node of row y (column a if y even, b if odd): −Σ A z_black
-    const Pair od = offd_pair(st, zm, z0, zp);
-    const double t = RED_IS_A(y) ? -od.a : -od.b;
-    if (RED_IS_A(y)) {
-      t_even = t;
-    } else {
-      const double t_w = shup(t_prev);  // t at (xa−1, 2J−1): previous lane's xb
-      const int J = (y - 1) >> 1;       // y = 2J+1
-      if (J >= J0 && J < J1 && outI) {
-        const double v = is_dir(bc, mc, I, J) ? 0.0 : t_even + 0.5 * (t + t_w);
-        rcb[(int64_t)J * gc.n0 + I] = v;
-      }
-      t_prev = t;
-    }
+  };
+  Pair zp;
+  advance(ys, zp);
+  double t_prev = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, ys, m, bc);  // (xb, 2J0−1)
+  zm = z0; z0 = zp; Nm = N;
+  for (int J = J0; J < J1; ++J) {
+    const int y = 2 * J;
+    advance(y, zp);
+    const double t_even = red_resid<INT, true>(E, N, Nm, zm, z0, zp, xa, y, m, bc);  // (xa, 2J)
     zm = z0; z0 = zp; Nm = N;
+    advance(y + 1, zp);
+    const double t = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, y + 1, m, bc);  // (xb, 2J+1)
+    zm = z0; z0 = zp; Nm = N;
+    const double t_w = shup(t_prev);  // t at (xa−1, 2J−1): previous lane's xb
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : t_even + 0.5 * (t + t_w);
+    t_prev = t;
   }
 }
 
@@ -840,51 +865,55 @@ __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
     double z, c0, c1;
   };
   const int I = xa >> 1;
+  // red value of row y after prolongation (the black column's entry is 0 until the black sweep)
   auto ZL = [&](int y) {
     ZRaw v{0.0, 0.0, 0.0};
-    if ((unsigned)y >= (unsigned)n0) return v;
+    if (!INT && (unsigned)y >= (unsigned)n0) return v;
     if (RED_IS_A(y)) {
-      if ((unsigned)xa < (unsigned)n0) {
+      if (INT || (unsigned)xa < (unsigned)n0) {
         v.z = __ldg(zbp + (int64_t)y * n0 + xa);
         v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
       }
-    } else if ((unsigned)xb < (unsigned)n0) {
+    } else if (INT || (unsigned)xb < (unsigned)n0) {
       v.z = __ldg(zbp + (int64_t)y * n0 + xb);
       v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
       v.c1 = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + I + 1);
     }
     return v;
   };
-  auto ZC = [&](const ZRaw& v, int y) {  // the row's pair: red column prolonged, black column 0
-    return RED_IS_A(y) ? Pair{v.z + v.c0, 0.0} : Pair{0.0, v.z + 0.5 * (v.c0 + v.c1)};
-  };
+  auto ZC = [&](const ZRaw& v, int y) { return RED_IS_A(y) ? v.z + v.c0 : v.z + 0.5 * (v.c0 + v.c1); };
   EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, y0 - 2);
-  Pair zpa = ZC(ZL(y0 - 2), y0 - 2), zpb = ZC(ZL(y0 - 1), y0 - 1);
+  // scalars: qa/qb/qc = red values of rows t, t+1, t+2; zbm/zb0 = black values of rows t−1, t
+  double qa = ZC(ZL(y0 - 2), y0 - 2), qb = ZC(ZL(y0 - 1), y0 - 1);
   Pair Nt, Ed;
   er.next(Ed, Nt);
-  Pair r0 = zero, zbm = zero, zb0 = zero;
+  Pair r0 = zero;
+  double zbm = 0.0, zb0 = 0.0;
   Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
   Pair rq = ld2<INT>(rb, xa, y0 - 1, n0);
   ZRaw zq = ZL(y0);
   double rz = 0.0;
   for (int t = y0 - 2; t < y1; ++t) {
-    const Pair r1 = rq, zpc = ZC(zq, t + 2);
+    const bool ra1 = RED_IS_A(t + 1);  // row t+1: red column a, black b (else the reverse)
+    const Pair r1 = rq;
+    const double qc = ZC(zq, t + 2);
     zq = ZL(t + 3);
     rq = ld2<INT>(rb, xa, t + 2, n0);
     Pair E1, N1;
     er.next(E1, N1);
     const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
-    // black column of row t+1: (r − Σ A z_red_prolonged)/D
-    const Pair odp = offd_pair(st1, zpa, zpb, zpc);
-    const Pair zbp1 = RED_IS_A(t + 1) ? Pair{0.0, (r1.b - odp.b) * rcp64(st1.b.d)}
-                                      : Pair{(r1.a - odp.a) * rcp64(st1.a.d), 0.0};
+    // black node of row t+1: (r − Σ A z_red_prolonged)/D; its x-neighbours are row t+1's red
+    // nodes (own column and the next/previous lane's)
+    const double qb_e = shdn(qb), qb_w = shup(qb);
+    const Sten sb = ra1 ? st1.b : st1.a;
+    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
+    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
     // output row t: red column = (r − Σ A z_black)/D, black column = z_black
-    const double zb0_e = shdn(zb0.a), zb0_w = shup(zb0.b);
-    Pair zv;
-    if (RED_IS_A(t))  // red at xa: east = own xb, west = previous lane's xb
-      zv = Pair{(r0.a - (sr0.e * zb0.b + sr0.w * zb0_w + sr0.n * zbp1.a + sr0.s * zbm.a)) * rcp64(sr0.d), zb0.b};
-    else              // red at xb: east = next lane's xa, west = own xa
-      zv = Pair{zb0.a, (r0.b - (sr0.e * zb0_e + sr0.w * zb0.a + sr0.n * zbp1.b + sr0.s * zbm.b)) * rcp64(sr0.d)};
+    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
+    const bool ra0 = !ra1;
+    const double zred = ((ra0 ? r0.a : r0.b) - (sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) +
+                                                 sr0.n * zbp1 + sr0.s * zbm)) * rcp64(sr0.d);
+    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
     if (t >= y0) {
       double* out = z_out + off + (int64_t)t * n0;
       if (outa) {
@@ -896,15 +925,18 @@ __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
         rz = fma(r0.b, zv.b, rz);
       }
     }
-    zpa = zpb; zpb = zpc; Nt = N1;
-    r0 = r1; zbm = zb0; zb0 = zbp1; sr0 = RED_IS_A(t + 1) ? st1.a : st1.b;
+    qa = qb; qb = qc; Nt = N1;
+    r0 = r1; zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
   }
   return rz;
 }
 
 // EN = false: level 0 (a = nodal k), also <r, z> → β; EN = true: levels ≥ 1 (a = E, b = N)
+#ifndef OSC_SU_MINB
+#define OSC_SU_MINB 4
+#endif
 template <bool EN>
-__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
+__global__ void __launch_bounds__(MT, OSC_SU_MINB) smooth_up_kernel(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ a,
                                                        const double* __restrict__ bN,
                                                        const double* __restrict__ r,
@@ -1130,7 +1162,6 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
                                                                double* scal) {
   extern __shared__ double smem[];
   __shared__ SLev lev[12];
-  __shared__ int s_go;
   const int b = blockIdx.x;
   const int N0 = (m0 + 1) * (m0 + 1);
   const double* k0 = kin + (int64_t)b * N0;
@@ -1264,7 +1295,6 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
       __syncthreads();
     }
   }
-  (void)s_go;
   if (threadIdx.x == 0) {
     flags[b * F_NFLAGS + F_ACTIVE] = 0;
     flags[b * F_NFLAGS + F_ITERS] = it;

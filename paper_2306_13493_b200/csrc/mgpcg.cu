@@ -707,57 +707,6 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
   }
 }
 
-// ---- pre-smoother from z = 0 (coarse levels; level 0 of the first V-cycle): red then black ------
-template <bool INT, bool EN>
-__device__ __forceinline__ double smooth_down_kernel_body(Geo g, int bc, const double* __restrict__ ka_,
-                                                         const double* __restrict__ kb_,
-                                                         const double* __restrict__ r,
-                                                         double* __restrict__ z, const int* flags, const PairCtx& c) {
-  PAIR_UNPACK
-
-  const double* rb = r + off;
-  const Pair zero{0.0, 0.0};
-  EdgeRows<INT, EN> er(ka_ + off, EN ? kb_ + off : nullptr, xa, n0, m, y0 - 2);
-  Pair Nt, Ed;
-  er.next(Ed, Nt);
-  Pair r0 = zero;
-  double zrm = 0.0, zr0 = 0.0;  // red z of rows t−1, t
-  Sten sb0{1.0, 0.0, 0.0, 0.0, 0.0};
-  Pair rq = ld2<INT>(rb, xa, y0 - 1, n0);
-  for (int t = y0 - 2; t < y1; ++t) {
-    const Pair r1 = rq;
-    rq = ld2<INT>(rb, xa, t + 2, n0);
-    Pair E1, N1;
-    er.next(E1, N1);
-    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
-    const bool ra0 = RED_IS_A(t), ra1 = !ra0;
-    const double zrp = (ra1 ? r1.a : r1.b) * rcp64(ra1 ? st1.a.d : st1.b.d);
-    const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
-    const double zbl = ((ra0 ? r0.b : r0.a) - (sb0.e * (ra0 ? zr0_e : zr0) + sb0.w * (ra0 ? zr0 : zr0_w) +
-                                               sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d);
-    const Pair zv = ra0 ? Pair{zr0, zbl} : Pair{zbl, zr0};
-    if (t >= y0) {
-      double* out = z + off + (int64_t)t * n0;
-      if (outa) out[xa] = zv.a;
-      if (outb) out[xb] = zv.b;
-    }
-    Nt = N1;
-    r0 = r1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
-  }
-  return 0.0;
-}
-
-// coefficients: EN = false → a = nodal k (level 0); EN = true → a = E, b = N (levels ≥ 1)
-template <bool EN>
-__global__ void __launch_bounds__(MT, 4) smooth_down_kernel(Geo g, int bc, const double* __restrict__ a,
-                                                         const double* __restrict__ bN,
-                                                         const double* __restrict__ r,
-                                                         double* __restrict__ z, const int* flags) {
-  PAIR_PROLOGUE
-  if (interior) smooth_down_kernel_body<true, EN>(g, bc, a, bN, r, z, flags, c);
-  else smooth_down_kernel_body<false, EN>(g, bc, a, bN, r, z, flags, c);
-}
-
 // ---- residual restriction rc = Pᵀ(r − A z) after the red-black pre-smoother (fem.cpp:168-195).
 // After the black sweep the residual vanishes on black nodes and equals −Σ A z_black on red
 // nodes, so rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]; zero at coarse Dirichlet nodes.
@@ -782,7 +731,7 @@ __device__ __forceinline__ double red_resid(Pair E, Pair N, Pair Nm, Pair zm, Pa
 }
 
 template <bool INT, bool EN>
-__device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
+__device__ __forceinline__ void restrict_z_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
                                               const double* __restrict__ cb, const double* __restrict__ z,
                                               double* __restrict__ rc, int b, int I, bool outI, int J0, int J1) {
   const int m = g.m, n0 = g.n0, mc = gc.m;
@@ -821,9 +770,86 @@ __device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const doubl
   }
 }
 
-template <bool EN>
+// ---- pre-smoother + residual restriction, fused (fem.cpp:288-295, 168-195) ----------------------------
+// The pre-smoother is red-black GS from z = 0:
+//   red sweep:   z_red = r/D;
+//   black sweep: z_black = (r − Σ A z_red)/D.
+// The residual r − A z then vanishes on black nodes and equals t = −Σ A z_black on red nodes, so
+//   rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]   (zero at coarse Dirichlet nodes).
+// z is never stored. The post-smoother (smooth_up) recomputes z_red = r/D with the same operands,
+// and its black sweep overwrites the black values. Fine rows are ingested one at a time: ingesting
+// row y gives z_red(y), z_black(y−1) and t(y−2). Lane l owns fine columns xa = 2I, xb = 2I+1 of
+// coarse column I (the column-pair layout); lanes 0 and 31 are halo.
+template <bool INT, bool EN>
+__device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
+                                              const double* __restrict__ cb, const double* __restrict__ r,
+                                              double* __restrict__ rc, int b, int I, bool outI, int J0, int J1) {
+  const int m = g.m, n0 = g.n0, mc = gc.m;
+  const int xa = 2 * I;
+  const int64_t off = (int64_t)b * g.N;
+  const double* rb = r + off;
+  const int yf = 2 * J0 - 3;  // first ingested row (odd)
+  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, yf - 1);
+  Pair E, N, Nm;
+  er.next(E, Nm);  // N of row yf−1
+  Pair rq = ld2<INT>(rb, xa, yf, n0);
+  const Sten unit{1.0, 0.0, 0.0, 0.0, 0.0};
+  double zr_m = 0.0, zr_0 = 0.0;  // z_red of rows y−2, y−1 (y = the row being ingested)
+  double rb_0 = 0.0;              // r at the black node of row y−1
+  Sten sb_0 = unit;               // black stencil of row y−1
+  double zb_m = 0.0, zb_0 = 0.0;  // z_black of rows y−3, y−2
+  Sten sr_m = unit, sr_0 = unit;  // red stencils of rows y−2, y−1
+  // RN: the red column of the ingested row y is a (y even). Returns t(y−2).
+  auto ingest = [&](int y, auto ra) {
+    constexpr bool RN = decltype(ra)::value;
+    const Pair r1 = rq;
+    rq = ld2<INT>(rb, xa, y + 1, n0);
+    er.next(E, N);
+    const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
+    Nm = N;
+    const Sten srn = RN ? st.a : st.b, sbn = RN ? st.b : st.a;
+    // red sweep, row y
+    const double zr_p = (RN ? r1.a : r1.b) * rcp64(srn.d);
+    // black sweep, row y−1 (black column: a if RN). Black at a: east = own xb, west = previous
+    // lane's xb; black at b: east = next lane's xa, west = own xa; north/south = red of rows y, y−2
+    const double zr0_e = shdn(zr_0), zr0_w = shup(zr_0);
+    const double zb_p = (rb_0 - (sb_0.e * (RN ? zr_0 : zr0_e) + sb_0.w * (RN ? zr0_w : zr_0) +
+                                 sb_0.n * zr_p + sb_0.s * zr_m)) * rcp64(sb_0.d);
+    // residual at the red node of row y−2 (red column: a if RN)
+    const double zb0_e = shdn(zb_0), zb0_w = shup(zb_0);
+    const double t = -(sr_m.e * (RN ? zb_0 : zb0_e) + sr_m.w * (RN ? zb0_w : zb_0) + sr_m.n * zb_p +
+                       sr_m.s * zb_m);
+    zr_m = zr_0; zr_0 = zr_p;
+    rb_0 = RN ? r1.b : r1.a;
+    sb_0 = sbn;
+    zb_m = zb_0; zb_0 = zb_p;
+    sr_m = sr_0; sr_0 = srn;
+    return t;
+  };
+  using EVEN = std::true_type;
+  using ODD = std::false_type;
+  ingest(yf, ODD{});
+  ingest(yf + 1, EVEN{});
+  ingest(yf + 2, ODD{});
+  ingest(yf + 3, EVEN{});
+  double t_prev = ingest(yf + 4, ODD{});  // t(2J0−1)
+  double* rcb = rc + (int64_t)b * gc.N;
+  for (int J = J0; J < J1; ++J) {
+    const double t_even = ingest(2 * J + 2, EVEN{});  // t(2J)   at (xa, 2J)
+    const double t_odd = ingest(2 * J + 3, ODD{});    // t(2J+1) at (xb, 2J+1)
+    const double t_w = shup(t_prev);                  // t(2J−1) at (xa−1): previous lane's xb
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : t_even + 0.5 * (t_odd + t_w);
+    t_prev = t_odd;
+  }
+}
+
+// Level 0 (EN = false): restriction of the residual left by the pre-smoother that pcg_update_down
+// fused (reads k, z). Coarse levels (EN = true): pre-smoother fused here (reads E, N, r; z never
+// stored). Both give the same rc.
+template <bool EN, bool ZIN>
 __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ ca,
                                                       const double* __restrict__ cb,
+                                                      const double* __restrict__ r,
                                                       const double* __restrict__ z,
                                                       double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;
@@ -834,17 +860,22 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, con
   const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
   const int lyc = coarse_rows_per_warp(gc.m);
   const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
-  // interior: fine rows 2J0−2 … 2J1+1 and columns xa(lane 0)−1 … xb(lane 31)+1 are in-grid,
+  // interior: fine rows 2J0−4 … 2J1+3 and columns xa(lane 0)−1 … xb(lane 31)+1 are in-grid,
   // non-Dirichlet nodes with in-grid neighbours
-  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 2 >= 2 &&
-                        2 * J1 + 2 <= g.m - 1;
-  if (interior) restrict_body<true, EN>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
-  else restrict_body<false, EN>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
+  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 4 >= 2 &&
+                        2 * J1 + 4 <= g.m - 1;
+  if (!ZIN) {  // coarse levels, and level 0 of the first V-cycle (no fused pre-smoother ran yet)
+    if (interior) restrict_body<true, EN>(g, gc, bc, ca, cb, r, rc, b, I, outI, J0, J1);
+    else restrict_body<false, EN>(g, gc, bc, ca, cb, r, rc, b, I, outI, J0, J1);
+  } else {
+    if (interior) restrict_z_body<true, false>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
+    else restrict_z_body<false, false>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
+  }
 }
 
-// ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
+// ---- prolongation + post-smoother, level 0: reads the pre-smoothed z written by pcg_update_down ---------
 template <bool INT, bool EN>
-__device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
+__device__ __forceinline__ double smooth_up_z_body(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ ca,
                                                        const double* __restrict__ cb,
                                                        const double* __restrict__ r,
@@ -931,12 +962,108 @@ __device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
   return rz;
 }
 
-// EN = false: level 0 (a = nodal k), also <r, z> → β; EN = true: levels ≥ 1 (a = E, b = N)
-#ifndef OSC_SU_MINB
-#define OSC_SU_MINB 4
-#endif
-template <bool EN>
-__global__ void __launch_bounds__(MT, OSC_SU_MINB) smooth_up_kernel(Geo g, Geo gc, int bc,
+// ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
+// The pre-smoothed red values are recomputed as z_red = r/D (restrict_body's red sweep, same
+// operands), so the only field reads are the coefficients, r and the coarse correction zc.
+template <bool INT, bool EN>
+__device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
+                                                       const double* __restrict__ ca,
+                                                       const double* __restrict__ cb,
+                                                       const double* __restrict__ r,
+                                                       double* __restrict__ z_out,
+                                                       const double* __restrict__ zc, const PairCtx& c) {
+  PAIR_UNPACK
+
+  const double *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
+  const int nc0 = gc.n0;
+  const Pair zero{0.0, 0.0};
+  const int I = xa >> 1;
+  // coarse correction at the red node of row y (fem.cpp:144-165): row y even → red at xa (even,
+  // even): zc(I, y/2); row y odd → red at xb (odd, odd): ½[zc(I, (y−1)/2) + zc(I+1, (y+1)/2)].
+  // Raw values are loaded ahead and combined when used.
+  struct CRaw {
+    double c0, c1;
+  };
+  auto CL = [&](int y) {
+    CRaw v{0.0, 0.0};
+    if ((unsigned)y >= (unsigned)n0) return v;
+    if (RED_IS_A(y)) {
+      if (INT || (unsigned)xa < (unsigned)n0) v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
+    } else if (INT || (unsigned)xb < (unsigned)n0) {
+      v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
+      v.c1 = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + I + 1);
+    }
+    return v;
+  };
+  // red value of row y after the pre-smoother and the coarse correction: r/D + P zc, with D the
+  // raw diagonal of the red node from row y's edges and row y−1's N
+  auto qred = [&](Pair E, Pair N, Pair Nm, Pair rr, const CRaw& cv, int y) {
+    const double Wa = shup(E.b);
+    const double d = RED_IS_A(y) ? mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc).d
+                                 : mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc).d;
+    return RED_IS_A(y) ? rr.a * rcp64(d) + cv.c0 : rr.b * rcp64(d) + 0.5 * (cv.c0 + cv.c1);
+  };
+  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, y0 - 3);
+  Pair N0, E1, N1, Ed;
+  er.next(Ed, N0);  // N of row y0−3
+  er.next(E1, N1);  // row y0−2
+  const Pair r_a = ld2<INT>(rb, xa, y0 - 2, n0), r_b = ld2<INT>(rb, xa, y0 - 1, n0);
+  double qa = qred(E1, N1, N0, r_a, CL(y0 - 2), y0 - 2);
+  N0 = N1;
+  er.next(E1, N1);  // row y0−1
+  double qb = qred(E1, N1, N0, r_b, CL(y0 - 1), y0 - 1);
+  // scalars: qa/qb/qc = red values of rows t, t+1, t+2; zbm/zb0 = black values of rows t−1, t
+  Pair r0 = zero, r1 = r_b;
+  double zbm = 0.0, zb0 = 0.0;
+  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
+  Pair rq = ld2<INT>(rb, xa, y0, n0);
+  CRaw cq = CL(y0);
+  double rz = 0.0;
+  for (int t = y0 - 2; t < y1; ++t) {
+    const bool ra1 = RED_IS_A(t + 1);  // row t+1: red column a, black b (else the reverse)
+    const Pair r2 = rq;
+    const CRaw c2 = cq;
+    rq = ld2<INT>(rb, xa, t + 3, n0);
+    cq = CL(t + 3);
+    Pair E2, N2;
+    er.next(E2, N2);
+    const double qc = qred(E2, N2, N1, r2, c2, t + 2);
+    const Sten2 st1 = sten_pair<INT>(E1, N1, N0, xa, t + 1, m, bc);
+    // black node of row t+1: (r − Σ A z_red_prolonged)/D; its x-neighbours are row t+1's red
+    // nodes (own column and the next/previous lane's)
+    const double qb_e = shdn(qb), qb_w = shup(qb);
+    const Sten sb = ra1 ? st1.b : st1.a;
+    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
+    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
+    // output row t: red column = (r − Σ A z_black)/D, black column = z_black
+    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
+    const bool ra0 = !ra1;
+    const double zred = ((ra0 ? r0.a : r0.b) - (sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) +
+                                                 sr0.n * zbp1 + sr0.s * zbm)) * rcp64(sr0.d);
+    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
+    if (t >= y0) {
+      double* out = z_out + off + (int64_t)t * n0;
+      if (outa) {
+        out[xa] = zv.a;
+        rz = fma(r0.a, zv.a, rz);
+      }
+      if (outb) {
+        out[xb] = zv.b;
+        rz = fma(r0.b, zv.b, rz);
+      }
+    }
+    qa = qb; qb = qc;
+    N0 = N1; E1 = E2; N1 = N2;
+    r0 = r1; r1 = r2;
+    zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
+  }
+  return rz;
+}
+
+// EN = false: level 0 (a = nodal k, z = pre-smoothed z), also <r, z> → β; EN = true: levels ≥ 1
+// (a = E, b = N; z_red recomputed from r)
+template <bool EN, bool ZIN>
+__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ a,
                                                        const double* __restrict__ bN,
                                                        const double* __restrict__ r,
@@ -946,8 +1073,13 @@ __global__ void __launch_bounds__(MT, OSC_SU_MINB) smooth_up_kernel(Geo g, Geo g
                                                        double* scal, int* flags, double2* partial,
                                                        int maxp, unsigned* counter) {
   PAIR_PROLOGUE
-  const int finest = EN ? 0 : 1;
-  const double rz = interior ? smooth_up_kernel_body<true, EN>(g, gc, bc, a, bN, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c) : smooth_up_kernel_body<false, EN>(g, gc, bc, a, bN, r, z, z_out, zc, finest, scal, flags, partial, maxp, counter, c);
+  double rz;
+  if (!ZIN)
+    rz = interior ? smooth_up_kernel_body<true, EN>(g, gc, bc, a, bN, r, z_out, zc, c)
+                  : smooth_up_kernel_body<false, EN>(g, gc, bc, a, bN, r, z_out, zc, c);
+  else
+    rz = interior ? smooth_up_z_body<true, false>(g, gc, bc, a, bN, r, z, z_out, zc, 1, scal, flags, partial, maxp, counter, c)
+                  : smooth_up_z_body<false, false>(g, gc, bc, a, bN, r, z, z_out, zc, 1, scal, flags, partial, maxp, counter, c);
   if (EN) return;
   double t0, t1;
   if (reduce2_last(rz, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -1606,9 +1738,10 @@ namespace {
 
 Geo geo_of(const SolverLevel& L) { return Geo{L.m, L.m + 1, L.N}; }
 
-// Preconditioner z = M r on level 0. With `fused_down` the level-0 pre-smoother already ran
-// inside pcg_update_down (z holds the pre-smoothed correction).
-void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
+// Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). z0_fresh: lev[0].z holds the
+// level-0 pre-smoothed correction (written by pcg_update_down); otherwise the fused restriction
+// runs the level-0 pre-smoother itself.
+void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
   SolverWork& w = ctx->solver;
   cudaStream_t st = ctx->stream;
   double2* part = reinterpret_cast<double2*>(w.partial);
@@ -1629,21 +1762,19 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
   if (!sub_off)
     for (int l = 1; l < w.nlev - 1; ++l)
       if (w.lev[l].m <= 32) { ls = l; break; }
+  // down: pre-smoother + restriction, one fused pass per level
   for (int l = 0; l + 1 < w.nlev && l < ls; ++l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    if (l > 0 || !fused_down) {
-      KScope ks(ctx, l == 0 ? "mg_smooth_down.L0" : "mg_smooth_down.Lc");
-      if (l == 0)
-        smooth_down_kernel<false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.k, nullptr, w.r_cur, L.z, w.flags);
-      else
-        smooth_down_kernel<true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), bc, L.E, L.Nw, L.r, L.z, w.flags);
-    }
-    KScope ks(ctx, l == 0 ? "mg_restrict.L0" : "mg_restrict.Lc");
-    if (l == 0)
-      restrict_kernel<false><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, L.z, C.r, w.flags);
+    KScope ks(ctx, l > 0 ? "mg_restrict.Lc" : z0_fresh ? "mg_restrict.L0" : "mg_restrict.L0first");
+    if (l == 0 && z0_fresh)
+      restrict_kernel<false, true><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
+                                                                         L.z, C.r, w.flags);
+    else if (l == 0)
+      restrict_kernel<false, false><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
+                                                                          nullptr, C.r, w.flags);
     else
-      restrict_kernel<true><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.z, C.r, w.flags);
+      restrict_kernel<true, false><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.r, nullptr, C.r, w.flags);
   }
   if (ls < w.nlev - 1) {
     const SolverLevel& S = w.lev[ls];
@@ -1662,16 +1793,22 @@ void vcycle(Ctx* ctx, int bc, int B, bool fused_down) {
     KScope ks(ctx, "mg_coarse_solve");
     coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
   }
+  // up: prolongation + post-smoother per level
   for (int l = ls - 1; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    KScope ks(ctx, l == 0 ? "mg_smooth_up.L0" : "mg_smooth_up.Lc");
-    if (l == 0)
-      smooth_up_kernel<false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur, L.z, L.z2,
-                                                              C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
+    KScope ks(ctx, l > 0 ? "mg_smooth_up.Lc" : z0_fresh ? "mg_smooth_up.L0" : "mg_smooth_up.L0first");
+    if (l == 0 && z0_fresh)
+      smooth_up_kernel<false, true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
+                                                              L.z,
+                                                              L.z2, C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
+    else if (l == 0)
+      smooth_up_kernel<false, false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
+                                                              nullptr,
+                                                              L.z2, C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
     else
-      smooth_up_kernel<true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.r, L.z, L.z2,
-                                                             C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
+      smooth_up_kernel<true, false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.r, nullptr,
+                                                             L.z2, C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
   }
   OSC_CUDA(cudaGetLastError());
 }
@@ -1743,7 +1880,6 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
   double* p_old = w.p0;
   double* p_new = w.p1;
   const int check_every = L0.N >= 65536 ? 1 : 4;
-  const bool multilevel = w.nlev > 1;
   // optional host-side safety valve (debugging): OSC_HARD_ITER_CAP stops the loop early; the
   // samples still active are reported as not converged by solver_results().
   static const long hard_cap = [] {
@@ -1773,8 +1909,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
                                                               w.counter, w.n_active, w.hist, w.hist_cap);
     }
     w.r_cur = (w.r_cur == L0.r) ? w.r2 : L0.r;
-    // single-level: the "pre-smoothed" z is overwritten by the exact coarse solve
-    vcycle(ctx, bc, B, multilevel);
+    vcycle(ctx, bc, B, true);  // level-0 pre-smoother ran inside pcg_update_down
     std::swap(p_old, p_new);
   }
 }

@@ -1738,6 +1738,12 @@ namespace {
 
 Geo geo_of(const SolverLevel& L) { return Geo{L.m, L.m + 1, L.N}; }
 
+// kernel-class name of a coarse level: "<base>.Lc", or "<base>.L<l>" with OSC_LEVEL_STATS set
+std::string lvl_name(const char* base, int l) {
+  static const bool per_level = std::getenv("OSC_LEVEL_STATS") != nullptr;
+  return std::string(base) + (per_level ? ".L" + std::to_string(l) : std::string(".Lc"));
+}
+
 // Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). z0_fresh: lev[0].z holds the
 // level-0 pre-smoothed correction (written by pcg_update_down); otherwise the fused restriction
 // runs the level-0 pre-smoother itself.
@@ -1766,7 +1772,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
   for (int l = 0; l + 1 < w.nlev && l < ls; ++l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    KScope ks(ctx, l > 0 ? "mg_restrict.Lc" : z0_fresh ? "mg_restrict.L0" : "mg_restrict.L0first");
+    KScope ks(ctx, l > 0 ? lvl_name("mg_restrict", l).c_str() : z0_fresh ? "mg_restrict.L0" : "mg_restrict.L0first");
     if (l == 0 && z0_fresh)
       restrict_kernel<false, true><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
                                                                          L.z, C.r, w.flags);
@@ -1797,7 +1803,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
   for (int l = ls - 1; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    KScope ks(ctx, l > 0 ? "mg_smooth_up.Lc" : z0_fresh ? "mg_smooth_up.L0" : "mg_smooth_up.L0first");
+    KScope ks(ctx, l > 0 ? lvl_name("mg_smooth_up", l).c_str() : z0_fresh ? "mg_smooth_up.L0" : "mg_smooth_up.L0first");
     if (l == 0 && z0_fresh)
       smooth_up_kernel<false, true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
                                                               L.z,

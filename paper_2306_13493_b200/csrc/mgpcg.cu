@@ -630,6 +630,47 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
   Pair kq = ld2<INT>(kb, xa, y0, n0), pq = ld2<INT>(pb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
   Pair uq = ld2<INT>(u + off, xa, y0 - 2, n0);
   double rr = 0.0;
+#ifdef OSC_UD_UNROLL2
+  // rows alternate parity: run them in (even, odd) pairs so the red/black roles are static
+  auto step = [&](int t, auto ra) {
+    constexpr bool ra0 = decltype(ra)::value, ra1 = !ra0;  // red column of row t is a
+    const Pair kc = kq, pc = pq, r1 = rq, u0 = uq;  // rows t+2 / t+1 / t, loaded one iteration ahead
+    kq = ld2<INT>(kb, xa, t + 3, n0);
+    pq = ld2<INT>(pb, xa, t + 3, n0);
+    rq = ld2<INT>(rb, xa, t + 2, n0);
+    uq = ld2<INT>(u + off, xa, t + 1, n0);
+    Pair E1, N1;
+    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
+    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
+    const Pair od1 = offd_pair(st1, pa, pb1, pc);
+    const Pair rn1{fma(-alpha, fma(st1.a.d, pb1.a, od1.a), r1.a), fma(-alpha, fma(st1.b.d, pb1.b, od1.b), r1.b)};
+    const double zrp = ra1 ? rn1.a * rcp64(st1.a.d) : rn1.b * rcp64(st1.b.d);
+    const double zbl = ra0 ? (rn0.b - (sb0.e * shdn(zr0) + sb0.w * zr0 + sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d)
+                           : (rn0.a - (sb0.e * zr0 + sb0.w * shup(zr0) + sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d);
+    const Pair zv = ra0 ? Pair{zr0, zbl} : Pair{zbl, zr0};
+    if (t >= y0) {
+      const int64_t row = off + (int64_t)t * n0;
+      if (outa) {
+        u[row + xa] = fma(alpha, pa.a, u0.a);
+        r_out[row + xa] = rn0.a;
+        z[row + xa] = zv.a;
+        rr = fma(rn0.a, rn0.a, rr);
+      }
+      if (outb) {
+        u[row + xb] = fma(alpha, pa.b, u0.b);
+        r_out[row + xb] = rn0.b;
+        z[row + xb] = zv.b;
+        rr = fma(rn0.b, rn0.b, rr);
+      }
+    }
+    ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
+    rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
+  };
+  for (int t = y0 - 2; t < y1; t += 2) {  // y0 is even
+    step(t, std::true_type{});
+    if (t + 1 < y1) step(t + 1, std::false_type{});
+  }
+#else
   for (int t = y0 - 2; t < y1; ++t) {
     const Pair kc = kq, pc = pq, r1 = rq, u0 = uq;  // rows t+2 / t+1 / t, loaded one iteration ahead
     kq = ld2<INT>(kb, xa, t + 3, n0);
@@ -668,10 +709,14 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
     ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
     rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
   }
+#endif
   return rr;
 }
 
-__global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
+#ifndef OSC_UD_MINB
+#define OSC_UD_MINB 4
+#endif
+__global__ void __launch_bounds__(MT, OSC_UD_MINB) pcg_update_down_kernel(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,

@@ -27,7 +27,7 @@ OSC_OK, OSC_ERR_CONFIG, OSC_ERR_NUMERICAL, OSC_ERR_SOLVER, OSC_ERR_EMBEDDING, OS
 BC_FLOWCELL, BC_DIRICHLET_ALL = 0, 1
 QOI_POINT, QOI_L2, QOI_INTEGRAL, QOI_FLUX = 0, 1, 2, 3
 COV_MATERN, COV_SEPARABLE_EXP = 0, 1
-COARSE_GALERKIN, COARSE_REDISCRETIZE = 0, 1
+COARSE_GALERKIN, COARSE_REDISCRETIZE, COARSE_GALERKIN_LINEAR = 0, 1, 2
 DRAW_HAS_COARSE, DRAW_TRUNC_FINE, DRAW_TRUNC_COARSE, DRAW_XI_DEVICE = 1, 2, 4, 8
 CE_TRUNCATED, CE_EXP, CE_FINE, CE_COARSE, CE_DEVICE_OUT, CE_XI_DEVICE = 1, 2, 4, 8, 16, 32
 

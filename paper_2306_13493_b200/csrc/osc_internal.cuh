@@ -73,9 +73,15 @@ struct KScope {
 struct SolverLevel {
   int m = 0;       // cells per side
   int64_t N = 0;   // nodes (m+1)^2
-  double *k = nullptr, *D = nullptr, *E = nullptr, *Nw = nullptr;  // conductivity + stencil
+  double* k = nullptr;  // level 0: nodal conductivity (5-point stencil rebuilt in-kernel)
+  // levels ≥ 1: symmetric 9-point operator, Dirichlet-eliminated (identity rows): diagonal C and
+  // the couplings to the E, N, NE, NW neighbours (W, S, SW, SE are the neighbours' E, N, NE, NW)
+  double *C = nullptr, *E = nullptr, *Nw = nullptr, *NE = nullptr, *NW = nullptr;
+  // prolongation weights of this level's cell-centre nodes (odd, odd) to the SW, SE, NW, NE coarse
+  // corners, one value per cell (m/2 × m/2 per sample); edge-node weights are rebuilt from the stencil
+  double* pw[4] = {nullptr, nullptr, nullptr, nullptr};
   double *r = nullptr, *z = nullptr;   // MG residual / pre-smoothed correction
-  double* z2 = nullptr;                // post-smoothed correction (written by smooth_up; no in-place halo race)
+  double* z2 = nullptr;                // post-smoothed correction (no in-place halo race)
 };
 
 struct SolverWork {
@@ -96,6 +102,7 @@ struct SolverWork {
   double* hist = nullptr;   // B * hist_cap (optional)
   int hist_cap = 0;
   int max_parts = 0;
+  int opdep = 1;  // operator-dependent transfers (OSC_COARSE_GALERKIN) vs P1 linear
   DevBuf mem;
 };
 

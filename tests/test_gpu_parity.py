@@ -105,12 +105,13 @@ def test_solve_golden(P, ctx, golden):
     assert qrel(ql, golden["fem_ql2"]) < QOI_TOL
 
 
-@pytest.mark.parametrize("coarse_op", [0, 1])
+@pytest.mark.parametrize("coarse_op", [0, 1, 2])
 @pytest.mark.parametrize("bc", [0, 1])
-@pytest.mark.parametrize("m", [4, 8, 32, 128, 512])
+@pytest.mark.parametrize("m", [4, 8, 32, 64, 128, 512])
 def test_solve_vs_oracle(P, ctx, port, m, bc, coarse_op):
-    """Both coarse-operator modes (Galerkin, the reference's rediscretisation) solve the same fine
-    system: QoIs match the reference algorithm to 1e-7."""
+    """Every coarse-operator mode solves the same fine system, so QoIs match the reference
+    algorithm to 1e-7. The modes are operator-dependent Galerkin, the reference's
+    rediscretisation and P1 Galerkin."""
     api = P.api
     rng = np.random.default_rng(m + 17 * bc)
     # a rough, high-contrast log field (σ ≈ 1.4) to stress the preconditioner
@@ -130,23 +131,28 @@ def test_solve_vs_oracle(P, ctx, port, m, bc, coarse_op):
             assert abs(q[b] - qo) <= QOI_TOL * max(abs(qo), 1e-12), (kind, b, q[b], qo)
 
 
-@pytest.mark.parametrize("m", [64, 256, 1024])
+@pytest.mark.parametrize("m", [32, 64, 256, 1024])
 def test_galerkin_fewer_iterations(P, ctx, port, m):
-    """On a rough Matérn ν=0.5 log-field (σ² = 2, as config 4), the Galerkin coarse operators need
-    far fewer PCG iterations than the reference's rediscretised ones. Both modes give the same
-    solution. The streaming (m > 64) and CTA-resident (m = 64) solvers are both covered."""
+    """Rough Matérn ν=0.5 log-field (σ² = 2, as config 4):
+    * the reference's rediscretised hierarchy needs the most PCG iterations;
+    * P1 Galerkin needs fewer;
+    * operator-dependent Galerkin (the default) needs the fewest;
+    * all three give the same solution.
+    Covers the CTA-resident solver (m = 32), the streaming solver with its CTA-resident V-cycle
+    tail (m = 64) and larger streaming grids."""
     api = P.api
     model = api.CovarianceModel.matern(2.0, 3.0 / m, 0.5)
     op = api.build_operator(api.GridSpec.square(m), model)
     Z = op.sample_fields(None, count=2, seed=3, ell=0, index0=0, fine=True, ctx=ctx)
     prob = api.ProblemSpec(model, bc=api.BC.DirichletAll)
     res = {}
-    for mode in (api.CoarseOperator.Galerkin, api.CoarseOperator.Rediscretize):
+    for mode in api.CoarseOperator:
         u, it, _ = api.assemble_and_solve(m, Z, prob, api.SolverOptions(coarse_operator=mode), ctx=ctx)
         res[mode] = (u, it)
-    (ug, itg), (ur, itr) = res[api.CoarseOperator.Galerkin], res[api.CoarseOperator.Rediscretize]
-    assert np.all(itg < 0.8 * itr), (itg, itr)
-    assert relmax(ug, ur) < 1e-7
+    (ug, itg), (ur, itr), (ul, itl) = (res[api.CoarseOperator.Galerkin], res[api.CoarseOperator.Rediscretize],
+                                       res[api.CoarseOperator.GalerkinLinear])
+    assert np.all(itl < itr) and np.all(itg < itl), (itg, itl, itr)
+    assert relmax(ug, ur) < 1e-7 and relmax(ul, ur) < 1e-7
     uo, ito, rc, _ = port.solve(m, Z[0], bc=1)
     assert rc == 0 and relmax(ug[0], uo) < 1e-7
 
@@ -290,7 +296,7 @@ import paper_2306_13493_b200 as P
 from oracle import oracle as O
 api = P.api
 port = O.Port()
-for bc, qoi, cop in [(0, 0, 0), (1, 2, 1), (0, 3, 0), (1, 0, 1)]:
+for bc, qoi, cop in [(0, 0, 0), (1, 2, 1), (0, 3, 2), (1, 0, 0)]:
     model = api.CovarianceModel.matern(1.0, 0.1, 0.5)
     prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind(qoi)), bc=api.BC(bc))
     opt = api.EstimatorOptions(seed=4, solver=api.SolverOptions(coarse_operator=api.CoarseOperator(cop)))

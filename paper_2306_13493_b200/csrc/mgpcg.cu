@@ -21,10 +21,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "osc_device.cuh"
 #include "osc_internal.cuh"
@@ -170,25 +173,32 @@ __device__ __forceinline__ S9 row_s(const L9& L, int64_t off, int x, int y) {
   r.c = L.C[i];
   r.e = L.E[i];
   r.n = L.N[i];
-  r.ne = L.NE[i];
-  r.nw = L.NW[i];
   if (x > 0) r.w = L.E[i - 1];
   if (y > 0) r.s = L.N[i - L.n0];
-  if (x > 0 && y > 0) r.sw = L.NE[i - L.n0 - 1];
-  if (x < L.m && y > 0) r.se = L.NW[i - L.n0 + 1];
+  if (L.NE) {  // 9-point level (level 0 keeps 5-point rows)
+    r.ne = L.NE[i];
+    r.nw = L.NW[i];
+    if (x > 0 && y > 0) r.sw = L.NE[i - L.n0 - 1];
+    if (x < L.m && y > 0) r.se = L.NW[i - L.n0 + 1];
+  }
   return r;
 }
 
-// Row source of a level: nodal k (level 0, st = 1) or the stored 9-point operator.
-struct RowSrc {
-  const double* k;  // level-0 k (null for stored levels)
-  L9 L;
-  int m, bc;
-  __device__ __forceinline__ S9 row(int b, int x, int y) const {
-    if (k) return row_k(k + (int64_t)b * (m + 1) * (m + 1), m + 1, 1, m, bc, x, y);
-    return row_s(L, (int64_t)b * L.Nn, x, y);
-  }
-};
+// Level-0 rows from nodal k, stored once per setup (C, E, N; 5-point) so the transfer and Galerkin
+// kernels read every level the same way.
+__global__ void __launch_bounds__(NT) rows0_kernel(Geo g, int bc, const double* __restrict__ k,
+                                                   double* __restrict__ C, double* __restrict__ E,
+                                                   double* __restrict__ Nn) {
+  const int b = blockIdx.y;
+  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (i >= g.N) return;
+  const int y = (int)(i / g.n0), x = (int)(i - (int64_t)y * g.n0);
+  const S9 r = row_k(k + (int64_t)b * g.N, g.n0, 1, g.m, bc, x, y);
+  const int64_t o = (int64_t)b * g.N + i;
+  C[o] = r.c;
+  E[o] = r.e;
+  Nn[o] = r.n;
+}
 
 __device__ __forceinline__ bool dir_or_out(int bc, int m, int x, int y) {
   return x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y);
@@ -221,8 +231,9 @@ __device__ __forceinline__ void edge_w(const S9& r, bool horiz, bool opdep, bool
 }
 
 // Centre (odd x, odd y) weights to SW, SE, NW, NE.
-__device__ void centre_w(const RowSrc& R, int b, int x, int y, bool opdep, double w[4]) {
-  const int m = R.m, bc = R.bc, mc = m / 2;
+__device__ void centre_w(const L9& R, int bc, int b, int x, int y, bool opdep, double w[4]) {
+  const int m = R.m, mc = m / 2;
+  const int64_t off = (int64_t)b * R.Nn;
   const int I = (x - 1) >> 1, J = (y - 1) >> 1;
   const bool dSW = is_dir(bc, mc, I, J), dSE = is_dir(bc, mc, I + 1, J), dNW = is_dir(bc, mc, I, J + 1),
              dNE = is_dir(bc, mc, I + 1, J + 1);
@@ -233,12 +244,12 @@ __device__ void centre_w(const RowSrc& R, int b, int x, int y, bool opdep, doubl
     w[3] = dNE ? 0.0 : 0.5;
     return;
   }
-  const S9 rc = R.row(b, x, y);
+  const S9 rc = row_s(R, off, x, y);
   double wWs, wWn, wEs, wEn, wSw, wSe, wNw, wNe;  // V-edges W, E: (S, N); H-edges S, N: (W, E)
-  edge_w(R.row(b, x - 1, y), false, true, dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
-  edge_w(R.row(b, x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
-  edge_w(R.row(b, x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
-  edge_w(R.row(b, x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
+  edge_w(row_s(R, off, x - 1, y), false, true, dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
+  edge_w(row_s(R, off, x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
+  edge_w(row_s(R, off, x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
+  edge_w(row_s(R, off, x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
   const double ic = 1.0 / rc.c;
   w[0] = dSW ? 0.0 : -(rc.w * wWs + rc.s * wSw + rc.sw) * ic;
   w[1] = dSE ? 0.0 : -(rc.e * wEs + rc.s * wSe + rc.se) * ic;
@@ -248,13 +259,13 @@ __device__ void centre_w(const RowSrc& R, int b, int x, int y, bool opdep, doubl
 
 // P rows of every node of a level (scratch P0..P3, per node, meaning by parity as above) and the
 // level's centre weights per cell (pw, m/2 × m/2 per sample) for the V-cycle transfers.
-__global__ void __launch_bounds__(NT) prow_kernel(RowSrc R, int opdep, double* __restrict__ P0,
+__global__ void __launch_bounds__(NT) prow_kernel(L9 R, int bc, int opdep, double* __restrict__ P0,
                                                   double* __restrict__ P1, double* __restrict__ P2,
                                                   double* __restrict__ P3, double* __restrict__ pw0,
                                                   double* __restrict__ pw1, double* __restrict__ pw2,
                                                   double* __restrict__ pw3) {
   const int b = blockIdx.y;
-  const int m = R.m, n0 = m + 1, mc = m / 2, bc = R.bc;
+  const int m = R.m, n0 = m + 1, mc = m / 2;
   const int64_t N = (int64_t)n0 * n0;
   const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
   if (i >= N) return;
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(NT) prow_kernel(RowSrc R, int opdep, double* _
   if ((x & 1) == 0 && (y & 1) == 0) {
     w[0] = fdir ? 0.0 : 1.0;
   } else if ((x & 1) && (y & 1)) {
-    centre_w(R, b, x, y, opdep != 0, w);
+    centre_w(R, bc, b, x, y, opdep != 0, w);
     const int64_t cell = (int64_t)b * mc * mc + (int64_t)((y - 1) >> 1) * mc + ((x - 1) >> 1);
     pw0[cell] = w[0];
     pw1[cell] = w[1];
@@ -274,7 +285,7 @@ __global__ void __launch_bounds__(NT) prow_kernel(RowSrc R, int opdep, double* _
     const bool horiz = (x & 1) != 0;
     const int I0 = horiz ? (x - 1) >> 1 : x >> 1, J0 = horiz ? y >> 1 : (y - 1) >> 1;
     const int I1 = horiz ? I0 + 1 : I0, J1 = horiz ? J0 : J0 + 1;
-    const S9 r = opdep ? R.row(b, x, y) : S9{};
+    const S9 r = opdep ? row_s(R, (int64_t)b * N, x, y) : S9{};
     edge_w(r, horiz, opdep != 0, fdir, is_dir(bc, mc, I0, J0), is_dir(bc, mc, I1, J1), w[0], w[1]);
   }
   const int64_t o = (int64_t)b * N + i;
@@ -285,9 +296,11 @@ __global__ void __launch_bounds__(NT) prow_kernel(RowSrc R, int opdep, double* _
 }
 
 // Galerkin row of coarse node (I, J): A_c(c, c') = Σ_i P(i,c) Σ_j A(i,j) P(j,c') over the fine
-// nodes i of c's 3×3 support and their 9-point neighbours j (their P rows from prow_kernel).
-// Stores C, E, N, NE, NW of the symmetric result. Dirichlet coarse rows are identity.
-__global__ void __launch_bounds__(NT) rap_kernel(RowSrc R, const double* __restrict__ P0,
+// nodes i of c's 3×3 support and their 9-point neighbours j (P rows from prow_kernel). Fully
+// unrolled: every fine offset, node type and parent offset is a compile-time constant, so the
+// 3×3 accumulator stays in registers. Stores C, E, N, NE, NW of the symmetric result; Dirichlet
+// coarse rows are identity.
+__global__ void __launch_bounds__(NT) rap_kernel(L9 F, int bc, const double* __restrict__ P0,
                                                  const double* __restrict__ P1, const double* __restrict__ P2,
                                                  const double* __restrict__ P3, Geo gc, double* __restrict__ Cc,
                                                  double* __restrict__ Ec, double* __restrict__ Nc,
@@ -296,63 +309,56 @@ __global__ void __launch_bounds__(NT) rap_kernel(RowSrc R, const double* __restr
   const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
   if (ic >= gc.N) return;
   const int mc = gc.m, J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
-  const int m = R.m, n0 = m + 1, bc = R.bc;
-  const int64_t N = (int64_t)n0 * n0, o = (int64_t)b * gc.N + ic;
+  const int m = F.m, n0 = F.n0;
+  const int64_t off = (int64_t)b * F.Nn, o = (int64_t)b * gc.N + ic;
   if (is_dir(bc, mc, I, J)) {
     Cc[o] = 1.0;
     Ec[o] = Nc[o] = NEc[o] = NWc[o] = 0.0;
     return;
   }
-  // P(j, ·) of fine node (xj, yj) as up to 4 (coarse offset from c, weight)
-  auto prow = [&](int xj, int yj, int* dx, int* dy, double* wv) -> int {
-    if (xj < 0 || xj > m || yj < 0 || yj > m) return 0;
-    const int64_t j = (int64_t)b * N + (int64_t)yj * n0 + xj;
-    const int ox = xj & 1, oy = yj & 1;
-    const int Ib = xj >> 1, Jb = yj >> 1;  // floor(x/2), floor(y/2)
-    if (!ox && !oy) {
-      dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
-      return 1;
-    }
-    if (ox && !oy) {
-      dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
-      dx[1] = Ib + 1 - I; dy[1] = Jb - J; wv[1] = P1[j];
-      return 2;
-    }
-    if (!ox && oy) {
-      dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
-      dx[1] = Ib - I; dy[1] = Jb + 1 - J; wv[1] = P1[j];
-      return 2;
-    }
-    dx[0] = Ib - I; dy[0] = Jb - J; wv[0] = P0[j];
-    dx[1] = Ib + 1 - I; dy[1] = Jb - J; wv[1] = P1[j];
-    dx[2] = Ib - I; dy[2] = Jb + 1 - J; wv[2] = P2[j];
-    dx[3] = Ib + 1 - I; dy[3] = Jb + 1 - J; wv[3] = P3[j];
-    return 4;
-  };
   double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-  for (int di = -1; di <= 1; ++di)
-    for (int dj = -1; dj <= 1; ++dj) {
+#pragma unroll
+  for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
+    for (int di = -1; di <= 1; ++di) {
       const int xi = 2 * I + di, yi = 2 * J + dj;
       if (xi < 0 || xi > m || yi < 0 || yi > m) continue;
-      // P(i, c): find c among i's parents
-      int pdx[4], pdy[4];
-      double pw[4];
-      const int np = prow(xi, yi, pdx, pdy, pw);
-      double pic = 0.0;
-      for (int q = 0; q < np; ++q)
-        if (pdx[q] == 0 && pdy[q] == 0) pic = pw[q];
+      const int64_t ii = off + (int64_t)yi * n0 + xi;
+      double pic;  // P(i, c) by i's type and position relative to c
+      if (di == 0 && dj == 0) pic = P0[ii];
+      else if (dj == 0) pic = di > 0 ? P0[ii] : P1[ii];  // H-edge: c is its W (di = +1) or E parent
+      else if (di == 0) pic = dj > 0 ? P0[ii] : P1[ii];  // V-edge: c is its S or N parent
+      else pic = dj > 0 ? (di > 0 ? P0[ii] : P1[ii]) : (di > 0 ? P2[ii] : P3[ii]);  // centre: SW SE NW NE
       if (pic == 0.0) continue;
-      const S9 r = R.row(b, xi, yi);
-      const double a[3][3] = {{r.sw, r.s, r.se}, {r.w, r.c, r.e}, {r.nw, r.n, r.ne}};  // [ey+1][ex+1]
+      const S9 r = row_s(F, off, xi, yi);
+#pragma unroll
       for (int ey = -1; ey <= 1; ++ey)
+#pragma unroll
         for (int ex = -1; ex <= 1; ++ex) {
-          const double aij = a[ey + 1][ex + 1];
-          if (aij == 0.0) continue;
-          int qdx[4], qdy[4];
-          double qw[4];
-          const int nq = prow(xi + ex, yi + ey, qdx, qdy, qw);
-          for (int q = 0; q < nq; ++q)
-            if (qw[q] != 0.0) acc[qdy[q] + 1][qdx[q] + 1] += pic * aij * qw[q];
+          const double a = ey < 0 ? (ex < 0 ? r.sw : ex == 0 ? r.s : r.se)
+                                  : ey == 0 ? (ex < 0 ? r.w : ex == 0 ? r.c : r.e)
+                                            : (ex < 0 ? r.nw : ex == 0 ? r.n : r.ne);
+          const int xj = xi + ex, yj = yi + ey;
+          if (a == 0.0 || xj < 0 || xj > m || yj < 0 || yj > m) continue;
+          const int64_t jj = off + (int64_t)yj * n0 + xj;
+          const double pa = pic * a;
+          const int dx = di + ex, dy = dj + ey;  // j relative to (2I, 2J), in [−2, 2]
+          const bool ox = (dx & 1) != 0, oy = (dy & 1) != 0;
+          const int bx = dx >> 1, by = dy >> 1;  // floor(dx/2): j's W/S parent offset from c
+          if (!ox && !oy) {
+            acc[by + 1][bx + 1] += pa * P0[jj];
+          } else if (ox && !oy) {
+            acc[by + 1][bx + 1] += pa * P0[jj];
+            acc[by + 1][bx + 2] += pa * P1[jj];
+          } else if (!ox && oy) {
+            acc[by + 1][bx + 1] += pa * P0[jj];
+            acc[by + 2][bx + 1] += pa * P1[jj];
+          } else {
+            acc[by + 1][bx + 1] += pa * P0[jj];
+            acc[by + 1][bx + 2] += pa * P1[jj];
+            acc[by + 2][bx + 1] += pa * P2[jj];
+            acc[by + 2][bx + 2] += pa * P3[jj];
+          }
         }
     }
   Cc[o] = acc[1][1];
@@ -629,28 +635,6 @@ __global__ void __launch_bounds__(NT) c_post_kernel(L9 L, int red, const double*
   z2[i] = (r[i] - s) / a.c;
 }
 
-// level-0 pre-smoother for the first V-cycle (later cycles fuse it into pcg_update_down)
-__global__ void __launch_bounds__(NT) pre0_kernel(Geo g, int bc, const double* __restrict__ k, int black,
-                                                 const double* __restrict__ r, double* __restrict__ z,
-                                                 const int* flags) {
-  const int b = blockIdx.z;
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int64_t li = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (li >= g.N) return;
-  const int y = (int)(li / g.n0), x = (int)(li - (int64_t)y * g.n0);
-  const int64_t off = (int64_t)b * g.N, i = off + li;
-  const S9 a = row_k(k + off, g.n0, 1, g.m, bc, x, y);
-  if (!black) {
-    z[i] = is_red(x, y) ? r[i] * rcp64(a.c) : 0.0;
-  } else if (!is_red(x, y)) {
-    double s = 0.0;
-    if (x > 0) s += a.w * z[i - 1];
-    if (x < g.m) s += a.e * z[i + 1];
-    if (y > 0) s += a.s * z[i - g.n0];
-    if (y < g.m) s += a.n * z[i + g.n0];
-    z[i] = (r[i] - s) * rcp64(a.c);
-  }
-}
 
 // ---- PCG init: u = lift, r = b − A u (= b on interior rows, 0 on Dirichlet rows) -------------
 __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing, double fval,
@@ -989,10 +973,10 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
-    int* n_active, double* hist, int hist_cap, const PairCtx& c) {
+    int* n_active, double* hist, int hist_cap, int init, const PairCtx& c) {
   PAIR_UNPACK
 
-  const double alpha = scal[b * S_NSCAL + S_ALPHA];
+  const double alpha = init ? 0.0 : scal[b * S_NSCAL + S_ALPHA];
   const double *kb = k + off, *pb = p + off, *rb = r + off;
   const Pair zero{0.0, 0.0};
   // state for output row t: k/p rows t, t+1; N_t; r_new(t); z_red rows t−1, t; stencil(t)
@@ -1096,16 +1080,17 @@ __global__ void __launch_bounds__(MT, OSC_UD_MINB) pcg_update_down_kernel(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
-    int* n_active, double* hist, int hist_cap) {
+    int* n_active, double* hist, int hist_cap, int init) {
   PAIR_PROLOGUE
 #ifdef OSC_UD_INTERIOR
-  const double rr = interior ? pcg_update_down_kernel_body<true>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c)
-                             : pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c);
+  const double rr = interior ? pcg_update_down_kernel_body<true>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, init, c)
+                             : pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, init, c);
 #else
   // generic body only: the interior specialisation pushes this kernel past 128 registers (spills)
   (void)interior;
-  const double rr = pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, c);
+  const double rr = pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, init, c);
 #endif
+  if (init) return;  // the first V-cycle's pre-smoother pass (α = 0): no PCG bookkeeping
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
     const double rel = sqrt(t0) / scal[b * S_NSCAL + S_BNORM];
@@ -1215,6 +1200,298 @@ __device__ __forceinline__ void restrict_z_body(Geo g, Geo gc, int bc, const dou
     if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
     a_nw = t * wc[2];
     a_ne = t * wc[3];
+  }
+}
+
+// ---- coarse levels (9-point): row-marching kernels ----------------------------------------------------
+// The same column-pair layout as level 0: lane l owns the even column xa and xb = xa + 1 of its
+// 64-column strip, so each row gives every lane one red and one black node. The stored operator
+// rows are loaded as pairs; the W, S, SW, SE couplings come from the previous lane (shuffles) and
+// from the previous row (carried).
+struct R9 {
+  Pair C, E, N, NE, NW;
+};
+
+template <bool INT>
+__device__ __forceinline__ R9 ld9(const L9& L, int64_t off, int xa, int y) {
+  R9 q;
+  q.C = ld2<INT>(L.C + off, xa, y, L.n0);
+  q.E = ld2<INT>(L.E + off, xa, y, L.n0);
+  q.N = ld2<INT>(L.N + off, xa, y, L.n0);
+  q.NE = ld2<INT>(L.NE + off, xa, y, L.n0);
+  q.NW = ld2<INT>(L.NW + off, xa, y, L.n0);
+  if (!INT) {  // off-grid nodes: identity rows (their r and couplings are 0)
+    const bool yok = (unsigned)y < (unsigned)L.n0;
+    if (!(yok && (unsigned)xa < (unsigned)L.n0)) q.C.a = 1.0;
+    if (!(yok && (unsigned)(xa + 1) < (unsigned)L.n0)) q.C.b = 1.0;
+  }
+  return q;
+}
+
+// 9-point rows of both columns of row y from its loads and row y−1's N, NE, NW.
+__device__ __forceinline__ void st9_pair(const R9& q, Pair Nm, Pair NEm, Pair NWm, S9& A, S9& Bc) {
+  A.c = q.C.a;  A.e = q.E.a;  A.w = shup(q.E.b);  A.n = q.N.a;  A.s = Nm.a;
+  A.ne = q.NE.a;  A.nw = q.NW.a;  A.sw = shup(NEm.b);  A.se = NWm.b;
+  Bc.c = q.C.b;  Bc.e = q.E.b;  Bc.w = q.E.a;  Bc.n = q.N.b;  Bc.s = Nm.b;
+  Bc.ne = q.NE.b;  Bc.nw = q.NW.b;  Bc.sw = NEm.a;  Bc.se = shdn(NWm.a);
+}
+
+// Σ over the 8 neighbours of node a / node b of row y, from value pairs of rows y−1 (vm), y (v0), y+1 (vp)
+__device__ __forceinline__ double dot8_a(const S9& A, Pair vm, Pair v0, Pair vp) {
+  return A.e * v0.b + A.w * shup(v0.b) + A.n * vp.a + A.s * vm.a + A.ne * vp.b + A.nw * shup(vp.b) +
+         A.se * vm.b + A.sw * shup(vm.b);
+}
+__device__ __forceinline__ double dot8_b(const S9& B, Pair vm, Pair v0, Pair vp) {
+  return B.e * shdn(v0.a) + B.w * v0.a + B.n * vp.b + B.s * vm.b + B.ne * shdn(vp.a) + B.nw * vp.a +
+         B.se * shdn(vm.a) + B.sw * vm.a;
+}
+// diagonal part only
+__device__ __forceinline__ double diag_a(const S9& A, Pair vm, Pair vp) {
+  return A.ne * vp.b + A.nw * shup(vp.b) + A.se * vm.b + A.sw * shup(vm.b);
+}
+__device__ __forceinline__ double diag_b(const S9& B, Pair vm, Pair vp) {
+  return B.ne * shdn(vp.a) + B.nw * vp.a + B.se * shdn(vm.a) + B.sw * vm.a;
+}
+
+#define C9_PROLOGUE                                                                   \
+  const int b = blockIdx.z;                                                           \
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                                        \
+  const int lane = threadIdx.x & 31;                                                  \
+  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);                             \
+  const int m = L.m, n0 = L.n0;                                                       \
+  const int xa = strip * 60 - 2 + 2 * lane, xb = xa + 1;                              \
+  const bool outa = lane >= 1 && lane < 31 && xa <= m;                                \
+  const bool outb = lane >= 1 && lane < 31 && xb <= m;                                \
+  const int ly = rows_per_warp(m);                                                    \
+  const int y0 = blockIdx.y * ly, y1 = min(y0 + ly, n0);                              \
+  const int64_t off = (int64_t)b * L.Nn;                                              \
+  (void)outa; (void)outb;
+
+// Pre-smoother from z = 0 (red then black; the black sweep's diagonal neighbours are still 0):
+//   z_red = r/C,  z_black = (r − Σ_WENS a z_red)/C.  Reads C, E, N, r; writes z. Ingesting row t+1
+// gives z_red(t+1) and z_black(t).
+__global__ void __launch_bounds__(MT) c_pre_march_kernel(L9 L, const double* __restrict__ r,
+                                                         double* __restrict__ z, const int* flags) {
+  C9_PROLOGUE
+  const double *Cb = L.C + off, *Eb = L.E + off, *Nb = L.N + off, *rb = r + off;
+  auto ldC = [&](int y) {
+    Pair c = ld2<false>(Cb, xa, y, n0);
+    const bool yok = (unsigned)y < (unsigned)n0;
+    if (!(yok && (unsigned)xa < (unsigned)n0)) c.a = 1.0;
+    if (!(yok && (unsigned)xb < (unsigned)n0)) c.b = 1.0;
+    return c;
+  };
+  // state: row t: C, E, N, r; row t−1: N; red z of rows t−1, t
+  Pair Nm = ld2<false>(Nb, xa, y0 - 2, n0);
+  Pair C0 = ldC(y0 - 1), E0 = ld2<false>(Eb, xa, y0 - 1, n0), N0 = ld2<false>(Nb, xa, y0 - 1, n0);
+  Pair r0 = ld2<false>(rb, xa, y0 - 1, n0);
+  double zrm = 0.0;
+  double zr0 = (RED_IS_A(y0 - 1) ? r0.a / C0.a : r0.b / C0.b);
+  for (int t = y0 - 1; t < y1; ++t) {
+    const Pair C1 = ldC(t + 1), E1 = ld2<false>(Eb, xa, t + 1, n0), N1 = ld2<false>(Nb, xa, t + 1, n0);
+    const Pair r1 = ld2<false>(rb, xa, t + 1, n0);
+    const bool ra0 = RED_IS_A(t), ra1 = !ra0;
+    const double zrp = ra1 ? r1.a / C1.a : r1.b / C1.b;  // red of row t+1
+    // black of row t: at b (ra0: red at a) or at a
+    const double zr0_e = shdn(zr0), zr0_w = shup(zr0), Ew = shup(E0.b);
+    double zbl;
+    if (ra0)  // black at xb: E = E0.b toward the next lane's xa, W = E0.a toward own xa
+      zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) / C0.b;
+    else      // black at xa: E toward own xb, W = E(xa−1) toward the previous lane's xb
+      zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) / C0.a;
+    if (t >= y0) {
+      double* out = z + off + (int64_t)t * n0;
+      if (outa) out[xa] = ra0 ? zr0 : zbl;
+      if (outb) out[xb] = ra0 ? zbl : zr0;
+    }
+    Nm = N0; C0 = C1; E0 = E1; N0 = N1; r0 = r1;
+    zrm = zr0; zr0 = zrp;
+  }
+}
+
+// Residual after the pre-smoother and its restriction rc = Pᵀ t (coarse-row layout: lane l owns
+// coarse column I, fine columns 2I and 2I+1). With C·z_red = r and the black update absorbing its
+// WENS red terms:
+//   t_red = −Σ_8 a z,  t_black = −Σ_diag a z_black.
+// Row roles:
+//   even row 2J: a = C point (red), b = H-edge (black; weights to (I,J), (I+1,J));
+//   odd row 2J±1: a = V-edge (black), b = centre (red, weights pw of cell (I, J)).
+// Edge weights are rebuilt from the edge node's 9-point row (opdep) or ½.
+__global__ void __launch_bounds__(MT) c_restrict_march_kernel(L9 L, int bc, int opdep, const double* __restrict__ z,
+                                                              PW4 pw, Geo gc, double* __restrict__ rc,
+                                                              const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int lane = threadIdx.x & 31;
+  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
+  const int I = strip * 30 - 1 + lane;
+  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
+  const int lyc = coarse_rows_per_warp(gc.m);
+  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
+  const int m = L.m, n0 = L.n0, mc = gc.m, xa = 2 * I;
+  const int64_t off = (int64_t)b * L.Nn;
+  const double* zb = z + off;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  auto W4 = [&](int Jc, double w[4]) {
+    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+  };
+  // state for row y: its loads q, row y−1's N/NE/NW, z rows y−1, y (+ y+1 in flight)
+  const int ys = 2 * J0 - 1;
+  R9 q = ld9<false>(L, off, xa, ys);
+  Pair Nm = ld2<false>(L.N + off, xa, ys - 1, n0), NEm = ld2<false>(L.NE + off, xa, ys - 1, n0),
+       NWm = ld2<false>(L.NW + off, xa, ys - 1, n0);
+  Pair zm = ld2<false>(zb, xa, ys - 1, n0), z0 = ld2<false>(zb, xa, ys, n0), zq = ld2<false>(zb, xa, ys + 1, n0);
+  R9 qn = ld9<false>(L, off, xa, ys + 1);
+  // residuals of row y (both columns) and the row's stencils; advances the state to row y+1
+  auto row = [&](int y, double& ta, double& tb, S9& A, S9& Bc) {
+    const Pair zp = zq;
+    zq = ld2<false>(zb, xa, y + 2, n0);
+    st9_pair(q, Nm, NEm, NWm, A, Bc);
+    const bool red_a = RED_IS_A(y);
+    ta = red_a ? -dot8_a(A, zm, z0, zp) : -diag_a(A, zm, zp);
+    tb = red_a ? -diag_b(Bc, zm, zp) : -dot8_b(Bc, zm, z0, zp);
+    // off-grid or Dirichlet nodes carry no residual
+    if (is_dir(bc, m, xa, y) || (unsigned)xa > (unsigned)m || (unsigned)y > (unsigned)m) ta = 0.0;
+    if (is_dir(bc, m, xa + 1, y) || (unsigned)(xa + 1) > (unsigned)m || (unsigned)y > (unsigned)m) tb = 0.0;
+    Nm = q.N; NEm = q.NE; NWm = q.NW;
+    q = qn;
+    qn = ld9<false>(L, off, xa, y + 2);
+    zm = z0; z0 = zp;
+  };
+  double w[4], ta, tb, w0, w1;
+  S9 A, Bc;
+  // odd row 2J0−1: contributions to coarse row J0 (V-edge N weight, centre NW own / NE previous lane)
+  row(ys, ta, tb, A, Bc);
+  W4(J0 - 1, w);
+  edge_w(A, false, opdep != 0, false, false, false, w0, w1);
+  double carry_own = w1 * ta + w[2] * tb, carry_ne = w[3] * tb;
+  double* rcb = rc + (int64_t)b * gc.N;
+  for (int J = J0; J < J1; ++J) {
+    // even row 2J: C point (a) and H-edge (b)
+    row(2 * J, ta, tb, A, Bc);
+    edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
+    double acc = carry_own + shup(carry_ne) + ta + w0 * tb;
+    const double he = w1 * tb;  // H-edge (2I+1, 2J) → (I+1, J)
+    acc += shup(he);
+    // odd row 2J+1: V-edge (a) and centre (b)
+    row(2 * J + 1, ta, tb, A, Bc);
+    W4(J, w);
+    edge_w(A, false, opdep != 0, false, false, false, w0, w1);
+    const double se = w[1] * tb;
+    acc += w0 * ta + w[0] * tb + shup(se);
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : acc;
+    carry_own = w1 * ta + w[2] * tb;
+    carry_ne = w[3] * tb;
+  }
+}
+
+// Prolongation + post-smoother (black then red), ingesting one row per step:
+//   v(y) = z + P zc (both columns);  black new(y−1) = (r − Σ_8 a v)/C;
+//   red new(y−2) = (r − Σ_WENS a black_new − Σ_diag a v)/C.
+// Writes z2 (row y−2: red new and black new).
+__global__ void __launch_bounds__(MT) c_up_march_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+                                                        const double* __restrict__ z, PW4 pw, Geo gc,
+                                                        const double* __restrict__ zc, double* __restrict__ z2,
+                                                        const int* flags) {
+  C9_PROLOGUE
+  const double *rb = r + off, *zb = z + off, *zcb = zc + (int64_t)b * gc.N;
+  const int I = xa >> 1, nc0 = gc.n0;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  auto ZC = [&](int Ic, int Jc) {
+    return ((unsigned)Ic < (unsigned)nc0 && (unsigned)Jc < (unsigned)nc0) ? __ldg(zcb + (int64_t)Jc * nc0 + Ic) : 0.0;
+  };
+  // prolonged pair of row y from its stencils (edge weights) and loads
+  auto prolong = [&](int y, const S9& A, const S9& Bc, Pair zz) {
+    Pair v = zz;
+    if ((unsigned)y > (unsigned)m) return Pair{0.0, 0.0};
+    double w0, w1;
+    if (RED_IS_A(y)) {  // a = C point, b = H-edge
+      const int Jc = y >> 1;
+      const double c0 = ZC(I, Jc), c1 = ZC(I + 1, Jc);
+      v.a += c0;
+      edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
+      v.b += w0 * c0 + w1 * c1;
+    } else {  // a = V-edge, b = centre
+      const int Jc = y >> 1;
+      const double c00 = ZC(I, Jc), c10 = ZC(I + 1, Jc), c01 = ZC(I, Jc + 1), c11 = ZC(I + 1, Jc + 1);
+      edge_w(A, false, opdep != 0, false, false, false, w0, w1);
+      v.a += w0 * c00 + w1 * c01;
+      const bool ok = I >= 0 && I < mcl && Jc < mcl;
+      const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+      if (ok)
+        v.b += __ldg(pw.w0 + cell) * c00 + __ldg(pw.w1 + cell) * c10 + __ldg(pw.w2 + cell) * c01 +
+               __ldg(pw.w3 + cell) * c11;
+    }
+    if ((unsigned)xa > (unsigned)m || is_dir(bc, m, xa, y)) v.a = 0.0;
+    if ((unsigned)xb > (unsigned)m || is_dir(bc, m, xb, y)) v.b = 0.0;
+    return v;
+  };
+  const Pair zero{0.0, 0.0};
+  const S9 unit{1, 0, 0, 0, 0, 0, 0, 0, 0};
+  // state entering the step for row y: q = loads of row y, Nm/NEm/NWm of row y−1, r/z of row y
+  int y = y0 - 3;
+  R9 q = ld9<false>(L, off, xa, y);
+  Pair Nm = ld2<false>(L.N + off, xa, y - 1, n0), NEm = ld2<false>(L.NE + off, xa, y - 1, n0),
+       NWm = ld2<false>(L.NW + off, xa, y - 1, n0);
+  Pair rq = ld2<false>(rb, xa, y, n0), zq = ld2<false>(zb, xa, y, n0);
+  Pair vm3 = zero, vm2 = zero, vm1 = zero;  // v of rows y−3, y−2, y−1
+  double zbn2 = 0.0, zbn1 = 0.0;             // black new of rows y−3, y−2
+  S9 sb1 = unit;                             // black stencil of row y−1
+  S9 sr1 = unit, sr2 = unit;                 // red stencils of rows y−1, y−2
+  double rb1 = 0.0, rr1 = 0.0, rr2 = 0.0;    // r at the black node of row y−1, red nodes of rows y−1, y−2
+  for (; y < y1 + 2; ++y) {
+    const R9 qc = q;
+    const Pair rc0 = rq, zc0 = zq;
+    q = ld9<false>(L, off, xa, y + 1);
+    rq = ld2<false>(rb, xa, y + 1, n0);
+    zq = ld2<false>(zb, xa, y + 1, n0);
+    S9 A, Bc;
+    st9_pair(qc, Nm, NEm, NWm, A, Bc);
+    // the halo lanes have no neighbour lane beyond them: load the couplings their prolongation
+    // weights need (lane 0: V-edge W/SW; lane 31: H-edge SE)
+    if (lane == 0) {
+      A.w = ldv<false>(L.E + off, xa - 1, y, n0);
+      A.sw = ldv<false>(L.NE + off, xa - 1, y - 1, n0);
+    } else if (lane == 31) {
+      Bc.se = ldv<false>(L.NW + off, xb + 1, y - 1, n0);
+    }
+    Nm = qc.N; NEm = qc.NE; NWm = qc.NW;
+    const Pair v0 = prolong(y, A, Bc, zc0);
+    // black new of row y−1 (its black column is b when row y−1 has red at a)
+    const bool ra1 = RED_IS_A(y - 1);
+    const double d1 = ra1 ? dot8_b(sb1, vm2, vm1, v0) : dot8_a(sb1, vm2, vm1, v0);
+    const double zbn0 = (rb1 - d1) / sb1.c;
+    // red new of row y−2 (red column a when row y−2 is even): W/E are the same row's black new,
+    // N/S the black new of rows y−1 / y−3 in the same column, the diagonals the red prolonged
+    // values of rows y−1 / y−3 in the other column
+    const bool ra2 = RED_IS_A(y - 2);
+    const double e_b = ra2 ? zbn1 : shdn(zbn1), w_b = ra2 ? shup(zbn1) : zbn1;
+    const double d_ne = ra2 ? vm1.b : shdn(vm1.a), d_nw = ra2 ? shup(vm1.b) : vm1.a;
+    const double d_se = ra2 ? vm3.b : shdn(vm3.a), d_sw = ra2 ? shup(vm3.b) : vm3.a;
+    const double s2 = sr2.e * e_b + sr2.w * w_b + sr2.n * zbn0 + sr2.s * zbn2 + sr2.ne * d_ne + sr2.nw * d_nw +
+                      sr2.se * d_se + sr2.sw * d_sw;
+    const double zrn = (rr2 - s2) / sr2.c;
+    const int yo = y - 2;
+    if (yo >= y0 && yo < y1) {
+      double* out = z2 + off + (int64_t)yo * n0;
+      if (outa) out[xa] = ra2 ? zrn : zbn1;
+      if (outb) out[xb] = ra2 ? zbn1 : zrn;
+    }
+    // shift to row y+1
+    const bool ra0 = RED_IS_A(y);
+    vm3 = vm2; vm2 = vm1; vm1 = v0;
+    zbn2 = zbn1; zbn1 = zbn0;
+    sr2 = sr1; sr1 = ra0 ? A : Bc;
+    rr2 = rr1; rr1 = ra0 ? rc0.a : rc0.b;
+    sb1 = ra0 ? Bc : A;
+    rb1 = ra0 ? rc0.b : rc0.a;
   }
 }
 
@@ -2034,8 +2311,8 @@ HierDev hier_of(const SolverWork& w, int l0) {
   return H;
 }
 
-// Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). z0_fresh: lev[0].z holds the
-// level-0 pre-smoothed correction (written by pcg_update_down); otherwise it is computed here.
+// Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). lev[0].z holds the level-0
+// pre-smoothed correction, written by pcg_update_down (z0_fresh).
 void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
   SolverWork& w = ctx->solver;
   cudaStream_t st = ctx->stream;
@@ -2058,11 +2335,11 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     for (int l = 1; l < w.nlev - 1; ++l)
       if (w.lev[l].m <= 32) { ls = l; break; }
   const SolverLevel& L0 = w.lev[0];
-  if (!z0_fresh) {  // first V-cycle: level-0 pre-smoother (later cycles fuse it into pcg_update_down)
-    KScope ks(ctx, "mg_pre.L0first", 2);
-    pre0_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(geo_of(L0), bc, L0.k, 0, w.r_cur, L0.z, w.flags);
-    pre0_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(geo_of(L0), bc, L0.k, 1, w.r_cur, L0.z, w.flags);
-  }
+  OSC_REQUIRE(z0_fresh, "vcycle: level-0 pre-smoothed z missing");
+  // OSC_SIMPLE_COARSE: coarse levels with the one-thread-per-node kernels (A/B and debugging)
+  static const bool simple_all = std::getenv("OSC_SIMPLE_COARSE") != nullptr;
+  static const bool simple_down = simple_all || std::getenv("OSC_SIMPLE_DOWN") != nullptr;
+  static const bool simple_up = simple_all || std::getenv("OSC_SIMPLE_UP") != nullptr;
   // down
   for (int l = 0; l < ls; ++l) {
     const SolverLevel& L = w.lev[l];
@@ -2074,18 +2351,26 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       continue;
     }
     const L9 l9 = l9_of(L);
-    const dim3 gf(nblocks(L.N), 1, B);
-    {
-      KScope ks(ctx, lvl_name("mg_pre", l).c_str(), 2);
-      c_pre_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, w.flags);
-      c_pre_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, w.flags);
-    }
-    {
+    if (simple_down) {  // one thread per node (reference implementation of the same V-cycle)
+      const dim3 gf(nblocks(L.N), 1, B);
+      {
+        KScope ks(ctx, lvl_name("mg_pre", l).c_str(), 2);
+        c_pre_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, w.flags);
+        c_pre_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, w.flags);
+      }
       KScope ks(ctx, lvl_name("mg_restrict", l).c_str(), 2);
       c_resid_kernel<<<gf, NT, 0, st>>>(l9, L.r, L.z, L.z2, w.flags);
       c_restrict_kernel<<<dim3(nblocks(C.N), 1, B), NT, 0, st>>>(l9, bc, w.opdep, L.z2, L.pw[0], L.pw[1], L.pw[2],
                                                                  L.pw[3], geo_of(C), C.r, w.flags);
+      continue;
     }
+    {
+      KScope ks(ctx, lvl_name("mg_pre", l).c_str());
+      c_pre_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, L.r, L.z, w.flags);
+    }
+    KScope ks(ctx, lvl_name("mg_restrict", l).c_str());
+    c_restrict_march_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(l9, bc, w.opdep, L.z, pw_of(L), geo_of(C), C.r,
+                                                                  w.flags);
   }
   if (ls < w.nlev - 1) {
     const SolverLevel& S = w.lev[ls];
@@ -2112,12 +2397,50 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       continue;
     }
     const L9 l9 = l9_of(L);
-    const dim3 gf(nblocks(L.N), 1, B);
-    KScope ks(ctx, lvl_name("mg_smooth_up", l).c_str(), 3);
-    c_prolong_kernel<<<gf, NT, 0, st>>>(l9, bc, w.opdep, L.pw[0], L.pw[1], L.pw[2], L.pw[3], geo_of(C), C.z2, L.z,
-                                        w.flags);
-    c_post_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, L.z2, w.flags);
-    c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, L.z2, w.flags);
+    if (simple_up) {
+      const dim3 gf(nblocks(L.N), 1, B);
+      KScope ks(ctx, lvl_name("mg_smooth_up", l).c_str(), 3);
+      c_prolong_kernel<<<gf, NT, 0, st>>>(l9, bc, w.opdep, L.pw[0], L.pw[1], L.pw[2], L.pw[3], geo_of(C), C.z2,
+                                          L.z, w.flags);
+      c_post_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, L.z2, w.flags);
+      c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, L.z2, w.flags);
+      continue;
+    }
+    KScope ks(ctx, lvl_name("mg_smooth_up", l).c_str());
+    static const bool dbg = std::getenv("OSC_DEBUG_UP") != nullptr;
+    double *tz = nullptr, *tz2 = nullptr;
+    const size_t nb = sizeof(double) * L.N * B;
+    if (dbg) {
+      OSC_CUDA(cudaMalloc(&tz, nb));
+      OSC_CUDA(cudaMalloc(&tz2, nb));
+      OSC_CUDA(cudaMemcpyAsync(tz, L.z, nb, cudaMemcpyDeviceToDevice, st));
+    }
+    c_up_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2,
+                                                            L.z2, w.flags);
+    if (dbg) {
+      OSC_CUDA(cudaMemcpyAsync(tz2, L.z2, nb, cudaMemcpyDeviceToDevice, st));
+      const dim3 gf(nblocks(L.N), 1, B);
+      c_prolong_kernel<<<gf, NT, 0, st>>>(l9, bc, w.opdep, L.pw[0], L.pw[1], L.pw[2], L.pw[3], geo_of(C), C.z2,
+                                          tz, w.flags);
+      c_post_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, tz, L.z2, w.flags);
+      c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, tz, L.z2, w.flags);
+      std::vector<double> a(L.N * B), bb(L.N * B);
+      OSC_CUDA(cudaMemcpyAsync(a.data(), tz2, nb, cudaMemcpyDeviceToHost, st));
+      OSC_CUDA(cudaMemcpyAsync(bb.data(), L.z2, nb, cudaMemcpyDeviceToHost, st));
+      OSC_CUDA(cudaStreamSynchronize(st));
+      double mx = 0, ref = 0;
+      int64_t at = -1;
+      for (int64_t i = 0; i < L.N * B; ++i) {
+        ref = std::max(ref, std::fabs(bb[i]));
+        if (std::fabs(a[i] - bb[i]) > mx) { mx = std::fabs(a[i] - bb[i]); at = i; }
+      }
+      const int64_t s0 = at / L.N, li = at % L.N;
+      fprintf(stderr, "DEBUG_UP level %d m %d: max|diff| %.3e (ref %.3e) at sample %ld x %ld y %ld  march %.6e simple %.6e\n",
+              l, L.m, mx, ref, (long)s0, (long)(li % (L.m + 1)), (long)(li / (L.m + 1)), at >= 0 ? a[at] : 0.0,
+              at >= 0 ? bb[at] : 0.0);
+      cudaFree(tz);
+      cudaFree(tz2);
+    }
   }
   OSC_CUDA(cudaGetLastError());
 }
@@ -2130,25 +2453,32 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
   const int bc = prob->bc, mode = prob->coarse_op;
   const SolverLevel& L0 = w.lev[0];
   const Geo g0 = geo_of(L0);
-  KScope ks(ctx, "mg_setup", 3 * w.nlev);
   if (w.nlev == 1) {  // single level: level 0's own rows for the dense factor
+    KScope ks(ctx, "mg_setup.rows");
     const SolverLevel& L = w.lev[0];
     rediscretize_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(L0.k, g0, 1, bc, g0, L.C, L.E, L.Nw, L.NE, L.NW);
+  } else {  // level-0 rows (5-point) into scratch: u, r, r2 are free until pcg_init
+    KScope ks(ctx, "mg_setup.rows");
+    rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, L0.r, w.r2);
   }
   for (int l = 0; l + 1 < w.nlev; ++l) {
     const SolverLevel& F = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
-    // P rows of level l into scratch (level 0's z, z2, p0, p1: free until the solve starts)
-    const RowSrc R{l == 0 ? L0.k : nullptr, l9_of(F), F.m, bc};
-    prow_kernel<<<dim3(nblocks(F.N), B), NT, 0, st>>>(R, w.opdep, L0.z, L0.z2, w.p0, w.p1, F.pw[0], F.pw[1],
-                                                       F.pw[2], F.pw[3]);
+    const L9 R = l == 0 ? L9{w.u, L0.r, w.r2, nullptr, nullptr, F.m, F.m + 1, F.N} : l9_of(F);
+    {  // P rows of level l into scratch (level 0's z, z2, p0, p1: free until the solve starts)
+      KScope ks(ctx, "mg_setup.prow");
+      prow_kernel<<<dim3(nblocks(F.N), B), NT, 0, st>>>(R, bc, w.opdep, L0.z, L0.z2, w.p0, w.p1, F.pw[0],
+                                                         F.pw[1], F.pw[2], F.pw[3]);
+    }
+    KScope ks(ctx, "mg_setup.coarse_op");
     if (mode == OSC_COARSE_REDISCRETIZE)
       rediscretize_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(L0.k, g0, 2 << l, bc, geo_of(C), C.C, C.E, C.Nw,
                                                                 C.NE, C.NW);
     else
-      rap_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(R, L0.z, L0.z2, w.p0, w.p1, geo_of(C), C.C, C.E, C.Nw,
-                                                        C.NE, C.NW);
+      rap_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(R, bc, L0.z, L0.z2, w.p0, w.p1, geo_of(C), C.C, C.E,
+                                                        C.Nw, C.NE, C.NW);
   }
+  KScope ks(ctx, "mg_setup.factor");
   const SolverLevel& C = w.lev[w.nlev - 1];
   if (w.nc <= 32)
     coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(l9_of(C), B, w.chol);
@@ -2197,7 +2527,15 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
         g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, w.u, w.r_cur,
         w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
   }
-  vcycle(ctx, bc, B, false);  // z = M r0, rz = <r0, z>
+  if (w.nlev > 1) {  // first level-0 pre-smoother: pcg_update_down with α = 0 and p = u (finite)
+    KScope ks(ctx, "pcg_update_down.init");
+    double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
+    pcg_update_down_kernel<<<march_grid(L0.m, 2, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, w.u, w.u, w.r_cur,
+                                                            r_next, L0.z, w.scal, w.flags, part, w.max_parts,
+                                                            w.counter, w.n_active, w.hist, w.hist_cap, 1);
+    w.r_cur = r_next;
+  }
+  vcycle(ctx, bc, B, true);  // z = M r0, rz = <r0, z>
   double* p_old = w.p0;
   double* p_new = w.p1;
   const int check_every = L0.N >= 65536 ? 1 : 4;
@@ -2227,7 +2565,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
       double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
       pcg_update_down_kernel<<<march_grid(L0.m, 2, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, p_new, w.u, w.r_cur,
                                                               r_next, L0.z, w.scal, w.flags, part, w.max_parts,
-                                                              w.counter, w.n_active, w.hist, w.hist_cap);
+                                                              w.counter, w.n_active, w.hist, w.hist_cap, 0);
     }
     w.r_cur = (w.r_cur == L0.r) ? w.r2 : L0.r;
     vcycle(ctx, bc, B, true);  // level-0 pre-smoother ran inside pcg_update_down

@@ -1,6 +1,9 @@
 import os
 import sys
 
+# safety valve: a solver regression must fail fast instead of spinning to the 10·N iteration cap
+os.environ.setdefault("OSC_HARD_ITER_CAP", "3000")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -87,15 +87,60 @@ def algorithmic_bytes_per_sample(W, n, it=None):
 
 
 # Per-kernel compulsory HBM bytes per node of the grid the kernel runs on: every
-# input read once and every output written once, for one active sample; `launches_per_iter`
-# says how the per-sample launch count follows from the PCG iteration count `it`.
+# input read once and every output written once, for one active sample and one V-cycle / PCG
+# iteration (a sample runs one of each per iteration). Level 0 keeps nodal k (8 B/node, the
+# 5-point rows are rebuilt in registers); coarse levels store 9-point Galerkin rows C, E, N, NE, NW
+# (40 B/node); `pw` = the four centre prolongation weights per coarse cell (8 B per fine node);
+# a coarse-grid array costs ¼ of its fine-grid size.
 KERNEL_BYTES = {
-    # name: (bytes per node, launches per sample as a function of it)
-    "pcg_apply": (4 * 8, lambda it: it),              # read k, z, p_old; write p_new
-    "pcg_update_down": (7 * 8, lambda it: it),        # read k, p, r, u; write u, r, z
-    "mg_smooth_up.L0": (4 * 8 + 2, lambda it: it),    # read k, z, r, zc (1/4); write z
-    "mg_restrict.L0": (2 * 8 + 2, lambda it: it),     # read k, z; write rc (1/4)
+    "pcg_apply": 4 * 8,                    # read k, z, p_old; write p_new
+    "pcg_update_down": 7 * 8,              # read k, p, r, u; write u, r, z
+    "mg_restrict.L0": 8 + 8 + 8 + 2,       # read k, z, pw; write rc
+    "mg_smooth_up.L0": 8 + 8 + 8 + 2 + 8 + 8,  # read k, r, z, zc, pw; write z
+    "mg_pre": 24 + 8 + 8,                  # read C, E, N, r; write z
+    "mg_restrict": 40 + 8 + 8 + 2,         # read C, E, N, NE, NW, z, pw; write rc
+    "mg_smooth_up": 40 + 8 + 8 + 2 + 8 + 8,  # read C..NW, r, z, zc, pw; write z2
+    "mg_down": 40 + 8 + 8 + 2,             # fused pre + restrict: read C..NW, r, pw; write rc
+    "mg_up": 40 + 8 + 2 + 8 + 8,           # prolong + post (z recomputed): read C..NW, r, zc, pw; write z2
 }
+
+
+def mg_hierarchy(m):
+    """Grid sizes of the solver's levels and the first level of the CTA-resident tail, as
+    solver_prepare / vcycle build them (csrc/mgpcg.cu): halve while even down to m ≤ 4; the tail
+    starts at the first level l ≥ 1 with m_l ≤ 32 that has at least one level below it."""
+    ms = [m]
+    while ms[-1] > 4 and ms[-1] % 2 == 0 and len(ms) < 12:
+        ms.append(ms[-1] // 2)
+    ls = len(ms) - 1
+    for l in range(1, len(ms) - 1):
+        if ms[l] <= 32:
+            ls = l
+            break
+    return ms, ls
+
+
+def kernel_nodes(name, m_top):
+    """(bytes per node, nodes per sample-launch summed over the levels the class covers) of a
+    kernel-stats class "<base>[.L0|.Lc|.L<l>]" on the hierarchy of an m_top solve, or None."""
+    base, _, lv = name.partition(".")
+    if name in KERNEL_BYTES:
+        per = KERNEL_BYTES[name]
+        lv = "L0" if base.startswith("pcg_") or lv == "L0" else lv
+    elif base in KERNEL_BYTES:
+        per = KERNEL_BYTES[base]
+    else:
+        return None
+    ms, ls = mg_hierarchy(m_top)
+    if lv == "L0":
+        levels = [0]
+    elif lv == "Lc":
+        levels = list(range(1, ls))
+    elif lv.startswith("L") and lv[1:].isdigit():
+        levels = [int(lv[1:])]
+    else:
+        return None
+    return per, sum((ms[l] + 1) ** 2 for l in levels)
 
 
 class ClockSampler:
@@ -333,24 +378,24 @@ def main():
     base, _, grid_tag = dom_name.partition("@")
     roof = {"kernel": dom_name, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s",
             "frac": None, "traffic": None, "peak_kind": hbm_kind}
-    if base in KERNEL_BYTES and grid_tag:
+    kn = kernel_nodes(base, int(grid_tag)) if grid_tag else None
+    if kn:
         mg = int(grid_tag)
         sample_iters = iters_total[0] if mg == m else iters_total[1]
-        per_node, launches_of = KERNEL_BYTES[base]
-        alg_bytes = per_node * (mg + 1) ** 2 * launches_of(sample_iters)
+        per_node, nodes = kn
+        alg_bytes = per_node * nodes * sample_iters
         achieved = alg_bytes / (dom_ms / 1000.0) / 1e9
         roof.update(achieved=achieved, frac=achieved / hbm, alg_bytes_total=alg_bytes,
                     launches=dom_launches, avg_launch_ms=dom_ms / max(dom_launches, 1),
                     alg_bytes_per_launch=alg_bytes / max(dom_launches, 1),
-                    bytes_per_node=per_node, sample_launches=launches_of(sample_iters))
+                    bytes_per_node=per_node, nodes_per_sample_launch=nodes, sample_launches=sample_iters)
         # measured DRAM traffic of the same kernel (ncu --set full, profiles/ncu_traffic.json),
         # scaled to this run's node-launches like `achieved`
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
                 tr = json.load(f).get(base)
             if tr:
-                nl = (mg + 1) ** 2 * launches_of(sample_iters)
-                roof["traffic"] = tr["dram_bytes_per_node"] * nl / max(dom_launches, 1)
+                roof["traffic"] = tr["dram_bytes_per_node"] * nodes * sample_iters / max(dom_launches, 1)
                 roof["traffic_source"] = tr["source"]
                 roof["traffic_over_algorithmic"] = tr["dram_bytes_per_node"] / per_node
         except (OSError, ValueError, KeyError):
@@ -359,11 +404,10 @@ def main():
     per_kernel = {}
     for name, (nl, tms) in kstats.items():
         b_, _, g_ = name.partition("@")
-        if b_ in KERNEL_BYTES and g_ and tms > 0:
-            mg = int(g_)
-            it_ = iters_total[0] if mg == m else iters_total[1]
-            by = KERNEL_BYTES[b_][0] * (mg + 1) ** 2 * KERNEL_BYTES[b_][1](it_)
-            per_kernel[name] = round(by / (tms / 1000.0) / 1e9, 1)
+        kn_ = kernel_nodes(b_, int(g_)) if g_ else None
+        if kn_ and tms > 0:
+            it_ = iters_total[0] if int(g_) == m else iters_total[1]
+            per_kernel[name] = round(kn_[0] * kn_[1] * it_ / (tms / 1000.0) / 1e9, 1)
     n = lev.n
     b_sample = algorithmic_bytes_per_sample(W, n)
     pipeline = {"basis": "SURVEY 8(d) B per coupled sample", "bytes_per_sample": b_sample,

@@ -215,13 +215,13 @@ __device__ __forceinline__ void edge_w(const S9& r, bool horiz, bool opdep, bool
   }
   if (opdep) {
     if (horiz) {
-      const double cc = r.c + r.n + r.s;
-      w0 = -(r.w + r.nw + r.sw) / cc;
-      w1 = -(r.e + r.ne + r.se) / cc;
+      const double ic = rcp64(r.c + r.n + r.s);
+      w0 = -(r.w + r.nw + r.sw) * ic;
+      w1 = -(r.e + r.ne + r.se) * ic;
     } else {
-      const double cc = r.c + r.w + r.e;
-      w0 = -(r.s + r.sw + r.se) / cc;
-      w1 = -(r.n + r.nw + r.ne) / cc;
+      const double ic = rcp64(r.c + r.w + r.e);
+      w0 = -(r.s + r.sw + r.se) * ic;
+      w1 = -(r.n + r.nw + r.ne) * ic;
     }
   } else {
     w0 = w1 = 0.5;
@@ -1495,6 +1495,430 @@ __global__ void __launch_bounds__(MT) c_up_march_kernel(L9 L, int bc, int opdep,
   }
 }
 
+// ---- coarse levels: cp.async-staged marching ------------------------------------------------------
+// The register-marching coarse kernels above hold the next row's loads in registers (≈190
+// registers for the up kernel: 2 CTAs per SM, one row of loads in flight per warp, ≈30% of HBM).
+// The ring variants stage each lane's raw row data P rows ahead in a per-thread slot of shared
+// memory with cp.async (the slot is written and read by the same thread, so no barriers): loads
+// in flight no longer cost registers, and the zc / pw gathers of the prolongation are prefetched
+// with the rest.
+// 8-byte async copy global → shared; !ok zero-fills without reading (g is then never dereferenced,
+// so callers pass the unclamped address)
+__device__ __forceinline__ void cpa8(double* s, const double* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"((unsigned)ok << 3)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// up-kernel slot layout (doubles per row per thread; slot k of thread t at [k·MT + t])
+enum {
+  UP_C = 0, UP_E = 2, UP_N = 4, UP_NE = 6, UP_NW = 8, UP_R = 10, UP_Z = 12, UP_ZC = 14, UP_PW = 18, UP_X = 22,
+  UP_SLOTS = 24
+};
+constexpr int UP_RING = 3;  // rows staged per thread: 3 × 24 × 8 B × 128 threads = 72 KB, 3 CTAs per SM
+
+// Prolongation + post-smoother, ring-staged (same algorithm and operand order as c_up_march_kernel).
+// RZ: the pre-smoothed z is recomputed from r and the operator (red z = r/C, black z =
+// (r − Σ_WENS a z_red)/C, as c_pre_march_kernel) instead of loaded, so the down sweep need not
+// store it.
+template <bool RZ>
+__global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+                                                          const double* __restrict__ z, PW4 pw, Geo gc,
+                                                          const double* __restrict__ zc, double* __restrict__ z2,
+                                                          const int* flags) {
+  C9_PROLOGUE
+  extern __shared__ double ring[];
+  const int tid = threadIdx.x;
+  const double *rb = r + off, *zb = z + off, *zcb = zc + (int64_t)b * gc.N;
+  const int I = xa >> 1, nc0 = gc.n0;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  const double* Cb = L.C + off;
+  const double* Eb = L.E + off;
+  const double* Nb = L.N + off;
+  const double* NEb = L.NE + off;
+  const double* NWb = L.NW + off;
+  auto slot = [&](int y) { return ring + (size_t)((unsigned)(y - (y0 - 4)) % UP_RING) * UP_SLOTS * MT + tid; };
+  // stage row y into its slot (off-grid values are zero-filled); rows past the last one the chunk
+  // reads are skipped (their groups stay empty)
+  const int ylast = y1 + 1 + (RZ ? 1 : 0);
+  auto issue = [&](int y) {
+    if (y > ylast) return;
+    double* S = slot(y);
+    const bool yok = (unsigned)y < (unsigned)n0;
+    const bool aok = yok && (unsigned)xa < (unsigned)n0, bok = yok && (unsigned)xb < (unsigned)n0;
+    const int64_t ia = (int64_t)y * n0 + xa, ib = ia + 1;
+    cpa8(S + (UP_C + 0) * MT, Cb + ia, aok);
+    cpa8(S + (UP_C + 1) * MT, Cb + ib, bok);
+    cpa8(S + (UP_E + 0) * MT, Eb + ia, aok);
+    cpa8(S + (UP_E + 1) * MT, Eb + ib, bok);
+    cpa8(S + (UP_N + 0) * MT, Nb + ia, aok);
+    cpa8(S + (UP_N + 1) * MT, Nb + ib, bok);
+    cpa8(S + (UP_NE + 0) * MT, NEb + ia, aok);
+    cpa8(S + (UP_NE + 1) * MT, NEb + ib, bok);
+    cpa8(S + (UP_NW + 0) * MT, NWb + ia, aok);
+    cpa8(S + (UP_NW + 1) * MT, NWb + ib, bok);
+    cpa8(S + (UP_R + 0) * MT, rb + ia, aok);
+    cpa8(S + (UP_R + 1) * MT, rb + ib, bok);
+    if (!RZ) {
+      cpa8(S + (UP_Z + 0) * MT, zb + ia, aok);
+      cpa8(S + (UP_Z + 1) * MT, zb + ib, bok);
+    }
+    // coarse values of the prolongation: C-point row (y even) c0, c1; else c00, c10, c01, c11
+    const int Jc = y >> 1;
+    auto zc_ok = [&](int Ic, int J2) { return (unsigned)Ic < (unsigned)nc0 && (unsigned)J2 < (unsigned)nc0; };
+    auto zc_at = [&](int Ic, int J2) { return zcb + ((int64_t)J2 * nc0 + Ic); };
+    cpa8(S + (UP_ZC + 0) * MT, zc_at(I, Jc), zc_ok(I, Jc));
+    cpa8(S + (UP_ZC + 1) * MT, zc_at(I + 1, Jc), zc_ok(I + 1, Jc));
+    if (y & 1) {
+      cpa8(S + (UP_ZC + 2) * MT, zc_at(I, Jc + 1), zc_ok(I, Jc + 1));
+      cpa8(S + (UP_ZC + 3) * MT, zc_at(I + 1, Jc + 1), zc_ok(I + 1, Jc + 1));
+      const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+      const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+      cpa8(S + (UP_PW + 0) * MT, pw.w0 + cell, ok);
+      cpa8(S + (UP_PW + 1) * MT, pw.w1 + cell, ok);
+      cpa8(S + (UP_PW + 2) * MT, pw.w2 + cell, ok);
+      cpa8(S + (UP_PW + 3) * MT, pw.w3 + cell, ok);
+    }
+    // halo lanes: the couplings their prolongation weights need from beyond the warp
+    if (lane == 0) {
+      const bool ok0 = yok && (unsigned)(xa - 1) < (unsigned)n0;
+      const bool ok1 = (unsigned)(y - 1) < (unsigned)n0 && (unsigned)(xa - 1) < (unsigned)n0;
+      cpa8(S + (UP_X + 0) * MT, Eb + (ia - 1), ok0);
+      cpa8(S + (UP_X + 1) * MT, NEb + (ia - n0 - 1), ok1);
+    } else if (lane == 31) {
+      const bool ok1 = (unsigned)(y - 1) < (unsigned)n0 && (unsigned)(xb + 1) < (unsigned)n0;
+      cpa8(S + (UP_X + 0) * MT, NWb + (ib - n0 + 1), ok1);
+    }
+  };
+  auto P2 = [&](const double* S, int k) { return Pair{S[k * MT], S[(k + 1) * MT]}; };
+  auto raw9 = [&](const double* S, int y) {
+    R9 q{P2(S, UP_C), P2(S, UP_E), P2(S, UP_N), P2(S, UP_NE), P2(S, UP_NW)};
+    const bool yok = (unsigned)y < (unsigned)n0;
+    if (!(yok && (unsigned)xa < (unsigned)n0)) q.C.a = 1.0;
+    if (!(yok && (unsigned)xb < (unsigned)n0)) q.C.b = 1.0;
+    return q;
+  };
+  const Pair zero{0.0, 0.0};
+  int y = y0 - 3;  // y0 is even (rows per warp are even): the march starts on an odd row
+  // prologue: rows y0−4 (for the carried N/NE/NW), y0−3, … staged
+  for (int j = 0; j < UP_RING; ++j) {
+    issue(y - 1 + j);
+    cpa_commit();
+  }
+  cpa_wait<UP_RING - 1>();
+  Pair Nm, NEm, NWm;
+  {
+    const double* S = slot(y - 1);
+    Nm = P2(S, UP_N);
+    NEm = P2(S, UP_NE);
+    NWm = P2(S, UP_NW);
+  }
+  issue(y - 1 + UP_RING);
+  cpa_commit();
+  double zrm = 0.0, zr0 = 0.0;  // RZ: red pre-smoothed z of rows y−1, y
+  if (RZ) {
+    cpa_wait<UP_RING - 1>();
+    const double* S = slot(y);
+    const R9 q = raw9(S, y);
+    zr0 = S[(UP_R + 1) * MT] * rcp64(q.C.b);  // row y0−3 is odd: red at b
+  }
+  // Pending smoother rows carry partial sums instead of stencils: every neighbour term is folded in
+  // as soon as its value exists, so only the couplings still to be applied stay live.
+  //   black node of row y−1: Σ over the S/E/W-side neighbours done; N, NE, NW wait for v(y)
+  //   red node of row y−1:   S (black new of row y−2) and SE/SW (v(y−2)) done; E/W (black new of
+  //                          row y−1) and NE/NW (v(y)) arrive now, N (black new of row y) next step
+  //   red node of row y−2:   only N (black new of row y−1) left
+  struct PendB { double n, ne, nw, ic, rr; };
+  struct PendR1 { double e, w, ne, nw, n, ic, rr; };
+  struct PendR2 { double n, ic, rr; };
+  PendB pb{0, 0, 0, 0, 0};
+  PendR1 pr1{0, 0, 0, 0, 0, 0, 0};
+  PendR2 pr2{0, 0, 0};
+  Pair vm1 = zero;     // v of row y−1
+  double zbn1 = 0.0;   // black new of row y−2 (output with the red of row y−2)
+  // one row; RA = red at column a in row y (row parity is static: the loop is unrolled by 2)
+  auto step = [&](auto RA, int y) {
+    constexpr bool ra0 = decltype(RA)::value;
+    // row y (RZ: and y+1) resident; groups complete in issue order
+    cpa_wait<RZ ? UP_RING - 2 : UP_RING - 1>();
+    const double* S = slot(y);
+    const R9 qc = raw9(S, y);
+    const Pair rc0 = P2(S, UP_R);
+    Pair zc0;
+    if constexpr (RZ) {
+      const double* S1 = slot(y + 1);
+      constexpr int k1 = ra0 ? 1 : 0;  // row y+1 has its red node in the other column
+      const bool ok1 = (unsigned)(y + 1) < (unsigned)n0 && (unsigned)(ra0 ? xb : xa) < (unsigned)n0;
+      const double c1 = ok1 ? S1[(UP_C + k1) * MT] : 1.0;
+      const double zrp = S1[(UP_R + k1) * MT] * rcp64(c1);
+      const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
+      if constexpr (ra0) {
+        const double zbl = (rc0.b - (qc.E.b * zr0_e + qc.E.a * zr0 + qc.N.b * zrp + Nm.b * zrm)) * rcp64(qc.C.b);
+        zc0 = Pair{zr0, zbl};
+      } else {
+        const double Ew = shup(qc.E.b);
+        const double zbl = (rc0.a - (qc.E.a * zr0 + Ew * zr0_w + qc.N.a * zrp + Nm.a * zrm)) * rcp64(qc.C.a);
+        zc0 = Pair{zbl, zr0};
+      }
+      zrm = zr0;
+      zr0 = zrp;
+    } else {
+      zc0 = P2(S, UP_Z);
+    }
+    S9 A, Bc;
+    st9_pair(qc, Nm, NEm, NWm, A, Bc);
+    if (lane == 0) {
+      A.w = S[(UP_X + 0) * MT];
+      A.sw = S[(UP_X + 1) * MT];
+    } else if (lane == 31) {
+      Bc.se = S[(UP_X + 0) * MT];
+    }
+    Nm = qc.N; NEm = qc.NE; NWm = qc.NW;
+    // v(y) = z + P zc
+    Pair v0 = zc0;
+    {
+      double w0, w1;
+      if constexpr (ra0) {  // a = C point, b = H-edge
+        const double c0 = S[(UP_ZC + 0) * MT], c1 = S[(UP_ZC + 1) * MT];
+        v0.a += c0;
+        edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
+        v0.b += w0 * c0 + w1 * c1;
+      } else {  // a = V-edge, b = centre
+        const double c00 = S[(UP_ZC + 0) * MT], c10 = S[(UP_ZC + 1) * MT], c01 = S[(UP_ZC + 2) * MT],
+                     c11 = S[(UP_ZC + 3) * MT];
+        edge_w(A, false, opdep != 0, false, false, false, w0, w1);
+        v0.a += w0 * c00 + w1 * c01;
+        v0.b += S[(UP_PW + 0) * MT] * c00 + S[(UP_PW + 1) * MT] * c10 + S[(UP_PW + 2) * MT] * c01 +
+                S[(UP_PW + 3) * MT] * c11;
+      }
+      const bool yin = (unsigned)y <= (unsigned)m;
+      if (!yin || (unsigned)xa > (unsigned)m || is_dir(bc, m, xa, y)) v0.a = 0.0;
+      if (!yin || (unsigned)xb > (unsigned)m || is_dir(bc, m, xb, y)) v0.b = 0.0;
+    }
+    // the slot of row y is consumed: stage row y + UP_RING into it
+    issue(y + UP_RING);
+    cpa_commit();
+    // neighbours in row y of a node of row y−1 at column a / b: N, NE, NW
+    const double v0a_e = shdn(v0.a), v0b_w = shup(v0.b);
+    // black new of row y−1 (its black column is a when row y is red-at-a)
+    const double zbn0 = ra0 ? (pb.rr - (pb.n * v0.a + pb.ne * v0.b + pb.nw * v0b_w)) * pb.ic
+                            : (pb.rr - (pb.n * v0.b + pb.ne * v0a_e + pb.nw * v0.a)) * pb.ic;
+    // red new of row y−2 (same column as the black of row y−1): its N neighbour
+    const double zrn = (pr2.rr - pr2.n * zbn0) * pr2.ic;
+    const int yo = y - 2;
+    if (yo >= y0 && yo < y1) {
+      double* out = z2 + off + (int64_t)yo * n0;
+      if (outa) out[xa] = ra0 ? zrn : zbn1;
+      if (outb) out[xb] = ra0 ? zbn1 : zrn;
+    }
+    // red of row y−1 (column b when row y is red-at-a): E/W black new of row y−1, NE/NW v(y)
+    {
+      const double zbn0_e = shdn(zbn0), zbn0_w = shup(zbn0);
+      const double e_b = ra0 ? zbn0_e : zbn0, w_b = ra0 ? zbn0 : zbn0_w;
+      // red at b: NE = (xb+1, y) = next lane's a, NW = (xa, y); red at a: NE = (xb, y), NW = (xa−1, y)
+      const double d_ne = ra0 ? v0a_e : v0.b, d_nw = ra0 ? v0.a : v0b_w;
+      pr2 = PendR2{pr1.n, pr1.ic, pr1.rr - (pr1.e * e_b + pr1.w * w_b + pr1.ne * d_ne + pr1.nw * d_nw)};
+    }
+    // new pending nodes of row y: black (S side + E/W from v(y−1), v(y)) and red (S = black new of
+    // row y−1, SE/SW = v(y−1))
+    const double vm1a_e = shdn(vm1.a), vm1b_w = shup(vm1.b);
+    if constexpr (ra0) {  // red a, black b
+      const S9& K = Bc;    // black at b: E = next lane's a, W = own a; S row: S = vm1.b, SE = next a, SW = vm1.a
+      pb = PendB{K.n, K.ne, K.nw, rcp64(K.c),
+                 rc0.b - (K.e * v0a_e + K.w * v0.a + K.s * vm1.b + K.se * vm1a_e + K.sw * vm1.a)};
+      const S9& R = A;     // red at a: S = black new of row y−1 at a (= zbn0), SE = vm1.b, SW = prev lane's b
+      pr1 = PendR1{R.e, R.w, R.ne, R.nw, R.n, rcp64(R.c), rc0.a - (R.s * zbn0 + R.se * vm1.b + R.sw * vm1b_w)};
+    } else {  // red b, black a
+      const S9& K = A;     // black at a: E = own b, W = prev lane's b; SE = vm1.b, SW = prev lane's b
+      pb = PendB{K.n, K.ne, K.nw, rcp64(K.c),
+                 rc0.a - (K.e * v0.b + K.w * v0b_w + K.s * vm1.a + K.se * vm1.b + K.sw * vm1b_w)};
+      const S9& R = Bc;    // red at b: S = zbn0 (black new of row y−1 at b), SE = next lane's a, SW = vm1.a
+      pr1 = PendR1{R.e, R.w, R.ne, R.nw, R.n, rcp64(R.c), rc0.b - (R.s * zbn0 + R.se * vm1a_e + R.sw * vm1.a)};
+    }
+    vm1 = v0;
+    zbn1 = zbn0;
+  };
+  for (; y < y1 + 2; y += 2) {
+    step(std::false_type{}, y);
+    step(std::true_type{}, y + 1);
+  }
+  cpa_wait<0>();
+}
+constexpr size_t UP_RING_SMEM = sizeof(double) * UP_RING * UP_SLOTS * MT;
+
+// Fused pre-smoother + residual + restriction, ring-staged: z (red r/C, black (r − Σ_WENS a z_red)/C,
+// as c_pre_march_kernel) is formed in registers two rows ahead of the residual and never stored;
+// the residual and rc = Pᵀ t follow c_restrict_march_kernel. Reads C, E, N, NE, NW, r, pw; writes
+// rc. Slots per row: the operator pair (10), r (2), the centre weights of odd rows (4).
+enum { DN_C = 0, DN_E = 2, DN_N = 4, DN_NE = 6, DN_NW = 8, DN_R = 10, DN_PW = 12, DN_SLOTS = 16 };
+constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 64 KB per CTA, 3 CTAs per SM
+constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * DN_SLOTS * MT;
+
+__global__ void __launch_bounds__(MT, 3) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+                                                            PW4 pw, Geo gc, double* __restrict__ rc,
+                                                            const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  extern __shared__ double ring[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int strip = blockIdx.x * MW + (tid >> 5);
+  const int I = strip * 30 - 1 + lane;
+  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
+  const int lyc = coarse_rows_per_warp(gc.m);
+  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
+  const int m = L.m, n0 = L.n0, mc = gc.m, xa = 2 * I, xb = xa + 1;
+  const int64_t off = (int64_t)b * L.Nn;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  const double* Cb = L.C + off;
+  const double* Eb = L.E + off;
+  const double* Nb = L.N + off;
+  const double* NEb = L.NE + off;
+  const double* NWb = L.NW + off;
+  const double* rb = r + off;
+  const int ys = 2 * J0 - 1;
+  const int ylast = 2 * J1 + 1;  // residual rows end at 2J1 − 1; their z needs raw rows up to 2J1 + 1
+  auto slot = [&](int y) { return ring + (size_t)((unsigned)(y - (ys - 2)) % DN_RING) * DN_SLOTS * MT + tid; };
+  auto issue = [&](int y) {
+    if (y > ylast) return;
+    double* S = slot(y);
+    const bool yok = (unsigned)y < (unsigned)n0;
+    const bool aok = yok && (unsigned)xa < (unsigned)n0, bok = yok && (unsigned)xb < (unsigned)n0;
+    const int64_t ia = (int64_t)y * n0 + xa, ib = ia + 1;
+    cpa8(S + (DN_C + 0) * MT, Cb + ia, aok);
+    cpa8(S + (DN_C + 1) * MT, Cb + ib, bok);
+    cpa8(S + (DN_E + 0) * MT, Eb + ia, aok);
+    cpa8(S + (DN_E + 1) * MT, Eb + ib, bok);
+    cpa8(S + (DN_N + 0) * MT, Nb + ia, aok);
+    cpa8(S + (DN_N + 1) * MT, Nb + ib, bok);
+    cpa8(S + (DN_NE + 0) * MT, NEb + ia, aok);
+    cpa8(S + (DN_NE + 1) * MT, NEb + ib, bok);
+    cpa8(S + (DN_NW + 0) * MT, NWb + ia, aok);
+    cpa8(S + (DN_NW + 1) * MT, NWb + ib, bok);
+    cpa8(S + (DN_R + 0) * MT, rb + ia, aok);
+    cpa8(S + (DN_R + 1) * MT, rb + ib, bok);
+    if (y & 1) {  // centre weights of cell (I, y >> 1)
+      const int Jc = y >> 1;
+      const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+      const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+      cpa8(S + (DN_PW + 0) * MT, pw.w0 + cell, ok);
+      cpa8(S + (DN_PW + 1) * MT, pw.w1 + cell, ok);
+      cpa8(S + (DN_PW + 2) * MT, pw.w2 + cell, ok);
+      cpa8(S + (DN_PW + 3) * MT, pw.w3 + cell, ok);
+    }
+  };
+  auto P2 = [&](const double* S, int k) { return Pair{S[k * MT], S[(k + 1) * MT]}; };
+  auto Cpair = [&](const double* S, int y) {  // off-grid rows are identity
+    Pair c = P2(S, DN_C);
+    const bool yok = (unsigned)y < (unsigned)n0;
+    if (!(yok && (unsigned)xa < (unsigned)n0)) c.a = 1.0;
+    if (!(yok && (unsigned)xb < (unsigned)n0)) c.b = 1.0;
+    return c;
+  };
+  // red pre-smoothed z of row y (its red column): r/C
+  auto zred = [&](int y) {
+    const double* S = slot(y);
+    const Pair c = Cpair(S, y), rr = P2(S, DN_R);
+    return RED_IS_A(y) ? rr.a / c.a : rr.b / c.b;
+  };
+  // pre-smoothed pair of row y from its red value zr0 and the red values of rows y∓1 (zrm, zrp);
+  // Nm = N of row y − 1
+  auto zpair = [&](int y, double zrm, double zr0, double zrp, Pair Nm) {
+    const double* S = slot(y);
+    const Pair c = Cpair(S, y), E0 = P2(S, DN_E), N0 = P2(S, DN_N), r0 = P2(S, DN_R);
+    const double zr0_e = shdn(zr0), zr0_w = shup(zr0), Ew = shup(E0.b);
+    if (RED_IS_A(y)) {
+      const double zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) / c.b;
+      return Pair{zr0, zbl};
+    }
+    const double zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) / c.a;
+    return Pair{zbl, zr0};
+  };
+  // prologue: rows ys−2 … ys+1 staged; z of rows ys−1, ys
+  for (int j = 0; j < DN_RING; ++j) {
+    issue(ys - 2 + j);
+    cpa_commit();
+  }
+  cpa_wait<1>();  // rows ys−2, ys−1, ys
+  const double zr_m2 = zred(ys - 2), zr_m1 = zred(ys - 1), zr_0 = zred(ys);
+  const Pair N_m2 = P2(slot(ys - 2), DN_N);
+  Pair zm = zpair(ys - 1, zr_m2, zr_m1, zr_0, N_m2);
+  Pair Nm, NEm, NWm;
+  {
+    const double* S = slot(ys - 1);
+    Nm = P2(S, DN_N);
+    NEm = P2(S, DN_NE);
+    NWm = P2(S, DN_NW);
+  }
+  issue(ys + 2);  // into the slot of row ys−2
+  cpa_commit();
+  cpa_wait<1>();  // row ys+1
+  double zrA = zr_0, zrB = zred(ys + 1);  // red z of rows y, y+1 entering row(y)
+  Pair z0 = zpair(ys, zr_m1, zr_0, zrB, Nm);
+  issue(ys + 3);  // into the slot of row ys−1
+  cpa_commit();
+  // residuals of row y (both columns) and the row's stencils; advances the state to row y+1
+  auto row = [&](int y, double& ta, double& tb, S9& A, S9& Bc) {
+    cpa_wait<1>();  // row y+2
+    const double zrC = zred(y + 2);
+    const double* S = slot(y);
+    const R9 q{Cpair(S, y), P2(S, DN_E), P2(S, DN_N), P2(S, DN_NE), P2(S, DN_NW)};
+    const Pair zp = zpair(y + 1, zrA, zrB, zrC, q.N);
+    st9_pair(q, Nm, NEm, NWm, A, Bc);
+    const bool red_a = RED_IS_A(y);
+    ta = red_a ? -dot8_a(A, zm, z0, zp) : -diag_a(A, zm, zp);
+    tb = red_a ? -diag_b(Bc, zm, zp) : -dot8_b(Bc, zm, z0, zp);
+    if (is_dir(bc, m, xa, y) || (unsigned)xa > (unsigned)m || (unsigned)y > (unsigned)m) ta = 0.0;
+    if (is_dir(bc, m, xb, y) || (unsigned)xb > (unsigned)m || (unsigned)y > (unsigned)m) tb = 0.0;
+    Nm = q.N; NEm = q.NE; NWm = q.NW;
+    zm = z0; z0 = zp;
+    zrA = zrB; zrB = zrC;
+  };
+  auto W4 = [&](int y, double w[4]) {  // centre weights of odd row y (cell (I, y >> 1)); 0 off the cells
+    const double* S = slot(y);
+    w[0] = S[(DN_PW + 0) * MT];
+    w[1] = S[(DN_PW + 1) * MT];
+    w[2] = S[(DN_PW + 2) * MT];
+    w[3] = S[(DN_PW + 3) * MT];
+  };
+  double w[4], ta, tb, w0, w1;
+  S9 A, Bc;
+  row(ys, ta, tb, A, Bc);
+  W4(ys, w);
+  issue(ys + 4);
+  cpa_commit();
+  edge_w(A, false, opdep != 0, false, false, false, w0, w1);
+  double carry_own = w1 * ta + w[2] * tb, carry_ne = w[3] * tb;
+  double* rcb = rc + (int64_t)b * gc.N;
+  for (int J = J0; J < J1; ++J) {
+    const int ye = 2 * J, yo = ye + 1;
+    row(ye, ta, tb, A, Bc);
+    issue(ye + 4);
+    cpa_commit();
+    edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
+    double acc = carry_own + shup(carry_ne) + ta + w0 * tb;
+    const double he = w1 * tb;
+    acc += shup(he);
+    row(yo, ta, tb, A, Bc);
+    W4(yo, w);
+    issue(yo + 4);
+    cpa_commit();
+    edge_w(A, false, opdep != 0, false, false, false, w0, w1);
+    const double se = w[1] * tb;
+    acc += w0 * ta + w[0] * tb + shup(se);
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : acc;
+    carry_own = w1 * ta + w[2] * tb;
+    carry_ne = w[3] * tb;
+  }
+  cpa_wait<0>();
+}
+
 // Level-0 restriction kernel (reads k, z and the level-0 centre weights).
 __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                       const double* __restrict__ z, PW4 pw,
@@ -2311,6 +2735,17 @@ HierDev hier_of(const SolverWork& w, int l0) {
   return H;
 }
 
+// Coarse-level (9-point) V-cycle kernels, OSC_COARSE_MODE: 0 register marching (pre, restrict, up);
+// 1 the same with the up kernel ring-staged; 2 (default) fused ring-staged down sweep (pre-smoother +
+// restriction, z never stored) and the ring-staged up kernel recomputing z.
+int coarse_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("OSC_COARSE_MODE");
+    return e ? std::atoi(e) : 2;
+  }();
+  return mode;
+}
+
 // Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). lev[0].z holds the level-0
 // pre-smoothed correction, written by pcg_update_down (z0_fresh).
 void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
@@ -2364,6 +2799,18 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
                                                                  L.pw[3], geo_of(C), C.r, w.flags);
       continue;
     }
+    if (coarse_mode() == 2) {  // fused pre-smoother + restriction (z not stored)
+      static bool attr = false;
+      if (!attr) {
+        OSC_CUDA(cudaFuncSetAttribute(c_down_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)DN_RING_SMEM));
+        attr = true;
+      }
+      KScope ks(ctx, lvl_name("mg_down", l).c_str());
+      c_down_ring_kernel<<<restrict_grid(C.m, B), MT, DN_RING_SMEM, st>>>(l9, bc, w.opdep, L.r, pw_of(L),
+                                                                          geo_of(C), C.r, w.flags);
+      continue;
+    }
     {
       KScope ks(ctx, lvl_name("mg_pre", l).c_str());
       c_pre_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, L.r, L.z, w.flags);
@@ -2406,7 +2853,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, L.z2, w.flags);
       continue;
     }
-    KScope ks(ctx, lvl_name("mg_smooth_up", l).c_str());
+    KScope ks(ctx, lvl_name(coarse_mode() == 2 ? "mg_up" : "mg_smooth_up", l).c_str());
     static const bool dbg = std::getenv("OSC_DEBUG_UP") != nullptr;
     double *tz = nullptr, *tz2 = nullptr;
     const size_t nb = sizeof(double) * L.N * B;
@@ -2415,8 +2862,29 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       OSC_CUDA(cudaMalloc(&tz2, nb));
       OSC_CUDA(cudaMemcpyAsync(tz, L.z, nb, cudaMemcpyDeviceToDevice, st));
     }
-    c_up_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2,
-                                                            L.z2, w.flags);
+    const int up_mode = coarse_mode();
+    if (up_mode == 0) {
+      c_up_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2,
+                                                              L.z2, w.flags);
+    } else if (up_mode == 1) {
+      static bool attr = false;
+      if (!attr) {
+        OSC_CUDA(cudaFuncSetAttribute(c_up_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)UP_RING_SMEM));
+        attr = true;
+      }
+      c_up_ring_kernel<false><<<march_grid(L.m, 2, B), MT, UP_RING_SMEM, st>>>(
+          l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        OSC_CUDA(cudaFuncSetAttribute(c_up_ring_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)UP_RING_SMEM));
+        attr = true;
+      }
+      c_up_ring_kernel<true><<<march_grid(L.m, 2, B), MT, UP_RING_SMEM, st>>>(
+          l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
+    }
     if (dbg) {
       OSC_CUDA(cudaMemcpyAsync(tz2, L.z2, nb, cudaMemcpyDeviceToDevice, st));
       const dim3 gf(nblocks(L.N), 1, B);

@@ -125,6 +125,9 @@ int osc_ctx_synchronize(osc_ctx* ctx);
 int osc_ctx_set_mem_budget(osc_ctx* ctx, size_t bytes);
 /* Per-kernel-class timing with CUDA events on the context stream (0 off / 1 on). */
 int osc_ctx_set_profiling(osc_ctx* ctx, int on);
+/* Restrict profiling events to one kernel class ("name@grid", as osc_ctx_kernel_stats reports it);
+ * launch counts of every class are still kept. NULL or "" lifts the restriction. */
+int osc_ctx_profile_only(osc_ctx* ctx, const char* kernel_class);
 /* Number of kernel classes with stats; name/launch count/total ms of class i. */
 int osc_ctx_kernel_stats(osc_ctx* ctx, int i, const char** name, int64_t* launches,
                          double* total_ms);

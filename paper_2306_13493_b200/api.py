@@ -165,6 +165,10 @@ class Context:
     def set_profiling(self, on: bool):
         _check(self._lib.osc_ctx_set_profiling(self.h, 1 if on else 0))
 
+    def profile_only(self, kernel_class: str | None):
+        """Time only `kernel_class` (events around its launches); None times every class."""
+        _check(self._lib.osc_ctx_profile_only(self.h, kernel_class.encode() if kernel_class else None))
+
     def set_mem_budget(self, nbytes: int):
         _check(self._lib.osc_ctx_set_mem_budget(self.h, int(nbytes)))
 

@@ -87,22 +87,32 @@ void Ctx::flush_stats() {
     for (auto& pr : s.pending) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) s.total_ms += ms;
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
     }
     s.pending.clear();
   }
+  ev_next = 0;  // every pooled event has been read: reuse them
 }
 
-KScope::KScope(Ctx* c, const char* name, int n_launches) : ctx(c) {
-  cls = c->tag.empty() ? c->stat_class(name) : c->stat_class((std::string(name) + "@" + c->tag).c_str());
-  c->stats[cls].launches += n_launches;
-  c->launches += n_launches;
-  if (c->profiling) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, c->stream);
+cudaEvent_t Ctx::pool_event() {
+  if (ev_next == ev_pool.size()) {
+    cudaEvent_t e = nullptr;
+    OSC_CUDA(cudaEventCreate(&e));
+    ev_pool.push_back(e);
   }
+  return ev_pool[ev_next++];
+}
+
+// Without profiling a scope only counts launches (no string work on the launch path).
+KScope::KScope(Ctx* c, const char* name, int n_launches) : ctx(c), cls(-1) {
+  c->launches += n_launches;
+  if (!c->profiling) return;
+  const std::string full = c->tag.empty() ? std::string(name) : std::string(name) + "@" + c->tag;
+  cls = c->stat_class(full.c_str());
+  c->stats[cls].launches += n_launches;
+  if (!c->profile_only.empty() && c->profile_only != full) return;
+  e0 = c->pool_event();
+  e1 = c->pool_event();
+  cudaEventRecord(e0, c->stream);
 }
 
 KScope::~KScope() {
@@ -177,6 +187,14 @@ int osc_ctx_set_profiling(osc_ctx* c, int on) {
     OSC_CUDA(cudaStreamSynchronize(c->stream));
     c->flush_stats();
     c->profiling = on != 0;
+  });
+}
+
+int osc_ctx_profile_only(osc_ctx* c, const char* kernel_class) {
+  return guarded([&] {
+    OSC_CUDA(cudaStreamSynchronize(c->stream));
+    c->flush_stats();
+    c->profile_only = kernel_class ? kernel_class : "";
   });
 }
 

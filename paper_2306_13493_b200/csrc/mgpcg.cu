@@ -1515,35 +1515,50 @@ __device__ __forceinline__ void cpa_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// up-kernel slot layout (doubles per row per thread; slot k of thread t at [k·MT + t])
-enum {
-  UP_C = 0, UP_E = 2, UP_N = 4, UP_NE = 6, UP_NW = 8, UP_R = 10, UP_Z = 12, UP_ZC = 14, UP_PW = 18, UP_X = 22,
-  UP_SLOTS = 24
-};
-constexpr int UP_RING = 3;  // rows staged per thread: 3 × 24 × 8 B × 128 threads = 72 KB, 3 CTAs per SM
-
-// Prolongation + post-smoother, ring-staged (same algorithm and operand order as c_up_march_kernel).
-// RZ: the pre-smoothed z is recomputed from r and the operator (red z = r/C, black z =
-// (r − Σ_WENS a z_red)/C, as c_pre_march_kernel) instead of loaded, so the down sweep need not
-// store it.
+// Ring rows are laid out per warp: for each staged array the 64 consecutive columns x0 … x0+63 of
+// the warp's strip (x0 = xa of lane 0), so lane l's cp.async pair covers columns x0+l and x0+32+l
+// (each warp instruction moves 256 contiguous bytes) and lane l reads its own column pair back as
+// one 16-byte shared load. A __syncwarp orders the cp.async data with the other lanes' reads.
+//   up:   C E N NE NW r [z]  (64 each), zc of coarse rows Jc, Jc+1 (33 each: coarse columns
+//         x0/2 … x0/2+32), pw of the odd rows' cells (4 × 32), 3 halo couplings
 template <bool RZ>
-__global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+struct UpLayout {
+  static constexpr int NA = RZ ? 6 : 7;  // staged fine arrays
+  static constexpr int ZC0 = NA * 64, ZC1 = ZC0 + 33, PW = ZC1 + 33, X = PW + 128;
+  static constexpr int WORDS = (X + 3 + 1) & ~1;  // doubles per warp-row (even: 16-byte alignment)
+};
+enum { UP_C = 0, UP_E = 1, UP_N = 2, UP_NE = 3, UP_NW = 4, UP_R = 5, UP_Z = 6 };
+#ifndef OSC_UP_RING
+#define OSC_UP_RING 3
+#endif
+#ifndef OSC_UP_MINB
+#define OSC_UP_MINB 3
+#endif
+constexpr int UP_RING = OSC_UP_RING;  // rows staged per warp: 3 × 4 warps × 582 × 8 B = 55.9 KB (RZ); 3 CTAs per SM at ≤ 170 registers (A/B: faster than 4 CTAs at 128)
+template <bool RZ>
+constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * MW * UpLayout<RZ>::WORDS; }
+
+// Prolongation + post-smoother, ring-staged (same algorithm as c_up_march_kernel; pending smoother
+// rows carry partial sums). RZ: the pre-smoothed z is recomputed from r and the operator (red z =
+// r/C, black z = (r − Σ_WENS a z_red)/C, as c_pre_march_kernel) instead of loaded, so the down
+// sweep need not store it.
+template <bool RZ>
+__global__ void __launch_bounds__(MT, OSC_UP_MINB) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                           const double* __restrict__ z, PW4 pw, Geo gc,
                                                           const double* __restrict__ zc, double* __restrict__ z2,
                                                           const int* flags) {
   C9_PROLOGUE
-  extern __shared__ double ring[];
-  const int tid = threadIdx.x;
+  using LY = UpLayout<RZ>;
+  extern __shared__ __align__(16) double ring[];
+  const int warp = threadIdx.x >> 5;
   const double *rb = r + off, *zb = z + off, *zcb = zc + (int64_t)b * gc.N;
-  const int I = xa >> 1, nc0 = gc.n0;
+  const int x0 = xa - 2 * lane, I0 = x0 >> 1, nc0 = gc.n0;
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  const double* Cb = L.C + off;
-  const double* Eb = L.E + off;
-  const double* Nb = L.N + off;
-  const double* NEb = L.NE + off;
-  const double* NWb = L.NW + off;
-  auto slot = [&](int y) { return ring + (size_t)((unsigned)(y - (y0 - 4)) % UP_RING) * UP_SLOTS * MT + tid; };
+  const double* arr[7] = {L.C + off, L.E + off, L.N + off, L.NE + off, L.NW + off, rb, zb};
+  auto slot = [&](int y) {
+    return ring + ((size_t)((unsigned)(y - (y0 - 4)) % UP_RING) * MW + warp) * LY::WORDS;
+  };
   // stage row y into its slot (off-grid values are zero-filled); rows past the last one the chunk
   // reads are skipped (their groups stay empty)
   const int ylast = y1 + 1 + (RZ ? 1 : 0);
@@ -1551,52 +1566,45 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
     if (y > ylast) return;
     double* S = slot(y);
     const bool yok = (unsigned)y < (unsigned)n0;
-    const bool aok = yok && (unsigned)xa < (unsigned)n0, bok = yok && (unsigned)xb < (unsigned)n0;
-    const int64_t ia = (int64_t)y * n0 + xa, ib = ia + 1;
-    cpa8(S + (UP_C + 0) * MT, Cb + ia, aok);
-    cpa8(S + (UP_C + 1) * MT, Cb + ib, bok);
-    cpa8(S + (UP_E + 0) * MT, Eb + ia, aok);
-    cpa8(S + (UP_E + 1) * MT, Eb + ib, bok);
-    cpa8(S + (UP_N + 0) * MT, Nb + ia, aok);
-    cpa8(S + (UP_N + 1) * MT, Nb + ib, bok);
-    cpa8(S + (UP_NE + 0) * MT, NEb + ia, aok);
-    cpa8(S + (UP_NE + 1) * MT, NEb + ib, bok);
-    cpa8(S + (UP_NW + 0) * MT, NWb + ia, aok);
-    cpa8(S + (UP_NW + 1) * MT, NWb + ib, bok);
-    cpa8(S + (UP_R + 0) * MT, rb + ia, aok);
-    cpa8(S + (UP_R + 1) * MT, rb + ib, bok);
-    if (!RZ) {
-      cpa8(S + (UP_Z + 0) * MT, zb + ia, aok);
-      cpa8(S + (UP_Z + 1) * MT, zb + ib, bok);
+    const int c0 = x0 + lane, c1 = c0 + 32;
+    const bool ok0 = yok && (unsigned)c0 < (unsigned)n0, ok1 = yok && (unsigned)c1 < (unsigned)n0;
+    const int64_t i0 = (int64_t)y * n0 + c0;
+#pragma unroll
+    for (int k = 0; k < LY::NA; ++k) {
+      cpa8(S + k * 64 + lane, arr[k] + i0, ok0);
+      cpa8(S + k * 64 + 32 + lane, arr[k] + i0 + 32, ok1);
     }
-    // coarse values of the prolongation: C-point row (y even) c0, c1; else c00, c10, c01, c11
-    const int Jc = y >> 1;
-    auto zc_ok = [&](int Ic, int J2) { return (unsigned)Ic < (unsigned)nc0 && (unsigned)J2 < (unsigned)nc0; };
-    auto zc_at = [&](int Ic, int J2) { return zcb + ((int64_t)J2 * nc0 + Ic); };
-    cpa8(S + (UP_ZC + 0) * MT, zc_at(I, Jc), zc_ok(I, Jc));
-    cpa8(S + (UP_ZC + 1) * MT, zc_at(I + 1, Jc), zc_ok(I + 1, Jc));
+    // coarse values of the prolongation: row Jc (and Jc+1 on odd rows), columns I0 … I0+32
+    const int Jc = y >> 1, ci = I0 + lane;
+    const bool cok = (unsigned)ci < (unsigned)nc0, cok2 = (unsigned)(ci + 32) < (unsigned)nc0;
+    const bool j0 = (unsigned)Jc < (unsigned)nc0, j1 = (unsigned)(Jc + 1) < (unsigned)nc0;
+    const double* zr0 = zcb + (int64_t)Jc * nc0 + ci;
+    cpa8(S + LY::ZC0 + lane, zr0, j0 && cok);
+    if (lane == 0) cpa8(S + LY::ZC0 + 32, zr0 + 32, j0 && cok2);
     if (y & 1) {
-      cpa8(S + (UP_ZC + 2) * MT, zc_at(I, Jc + 1), zc_ok(I, Jc + 1));
-      cpa8(S + (UP_ZC + 3) * MT, zc_at(I + 1, Jc + 1), zc_ok(I + 1, Jc + 1));
-      const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
-      const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-      cpa8(S + (UP_PW + 0) * MT, pw.w0 + cell, ok);
-      cpa8(S + (UP_PW + 1) * MT, pw.w1 + cell, ok);
-      cpa8(S + (UP_PW + 2) * MT, pw.w2 + cell, ok);
-      cpa8(S + (UP_PW + 3) * MT, pw.w3 + cell, ok);
+      cpa8(S + LY::ZC1 + lane, zr0 + nc0, j1 && cok);
+      if (lane == 0) cpa8(S + LY::ZC1 + 32, zr0 + nc0 + 32, j1 && cok2);
+      const bool ok = ci >= 0 && ci < mcl && Jc >= 0 && Jc < mcl;
+      const int64_t cell = cb0 + (int64_t)Jc * mcl + ci;
+      cpa8(S + LY::PW + 0 * 32 + lane, pw.w0 + cell, ok);
+      cpa8(S + LY::PW + 1 * 32 + lane, pw.w1 + cell, ok);
+      cpa8(S + LY::PW + 2 * 32 + lane, pw.w2 + cell, ok);
+      cpa8(S + LY::PW + 3 * 32 + lane, pw.w3 + cell, ok);
     }
-    // halo lanes: the couplings their prolongation weights need from beyond the warp
+    // halo couplings from beyond the warp: E(x0−1, y), NE(x0−1, y−1), NW(x0+64, y−1)
     if (lane == 0) {
-      const bool ok0 = yok && (unsigned)(xa - 1) < (unsigned)n0;
-      const bool ok1 = (unsigned)(y - 1) < (unsigned)n0 && (unsigned)(xa - 1) < (unsigned)n0;
-      cpa8(S + (UP_X + 0) * MT, Eb + (ia - 1), ok0);
-      cpa8(S + (UP_X + 1) * MT, NEb + (ia - n0 - 1), ok1);
+      const bool xk = (unsigned)(x0 - 1) < (unsigned)n0;
+      cpa8(S + LY::X + 0, arr[UP_E] + (i0 - 1), yok && xk);
+      cpa8(S + LY::X + 1, arr[UP_NE] + (i0 - n0 - 1), (unsigned)(y - 1) < (unsigned)n0 && xk);
     } else if (lane == 31) {
-      const bool ok1 = (unsigned)(y - 1) < (unsigned)n0 && (unsigned)(xb + 1) < (unsigned)n0;
-      cpa8(S + (UP_X + 0) * MT, NWb + (ib - n0 + 1), ok1);
+      const bool xk = (unsigned)(x0 + 64) < (unsigned)n0;
+      cpa8(S + LY::X + 2, arr[UP_NW] + (i0 - n0 + 33), (unsigned)(y - 1) < (unsigned)n0 && xk);
     }
   };
-  auto P2 = [&](const double* S, int k) { return Pair{S[k * MT], S[(k + 1) * MT]}; };
+  auto P2 = [&](const double* S, int k) {
+    const double2 v = *reinterpret_cast<const double2*>(S + k * 64 + 2 * lane);
+    return Pair{v.x, v.y};
+  };
   auto raw9 = [&](const double* S, int y) {
     R9 q{P2(S, UP_C), P2(S, UP_E), P2(S, UP_N), P2(S, UP_NE), P2(S, UP_NW)};
     const bool yok = (unsigned)y < (unsigned)n0;
@@ -1612,6 +1620,7 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
     cpa_commit();
   }
   cpa_wait<UP_RING - 1>();
+  __syncwarp();
   Pair Nm, NEm, NWm;
   {
     const double* S = slot(y - 1);
@@ -1619,14 +1628,16 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
     NEm = P2(S, UP_NE);
     NWm = P2(S, UP_NW);
   }
+  __syncwarp();
   issue(y - 1 + UP_RING);
   cpa_commit();
   double zrm = 0.0, zr0 = 0.0;  // RZ: red pre-smoothed z of rows y−1, y
   if (RZ) {
     cpa_wait<UP_RING - 1>();
+    __syncwarp();
     const double* S = slot(y);
     const R9 q = raw9(S, y);
-    zr0 = S[(UP_R + 1) * MT] * rcp64(q.C.b);  // row y0−3 is odd: red at b
+    zr0 = P2(S, UP_R).b * rcp64(q.C.b);  // row y0−3 is odd: red at b
   }
   // Pending smoother rows carry partial sums instead of stencils: every neighbour term is folded in
   // as soon as its value exists, so only the couplings still to be applied stay live.
@@ -1647,16 +1658,17 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
     constexpr bool ra0 = decltype(RA)::value;
     // row y (RZ: and y+1) resident; groups complete in issue order
     cpa_wait<RZ ? UP_RING - 2 : UP_RING - 1>();
+    __syncwarp();
     const double* S = slot(y);
     const R9 qc = raw9(S, y);
     const Pair rc0 = P2(S, UP_R);
     Pair zc0;
     if constexpr (RZ) {
       const double* S1 = slot(y + 1);
-      constexpr int k1 = ra0 ? 1 : 0;  // row y+1 has its red node in the other column
+      // row y+1 has its red node in the other column
       const bool ok1 = (unsigned)(y + 1) < (unsigned)n0 && (unsigned)(ra0 ? xb : xa) < (unsigned)n0;
-      const double c1 = ok1 ? S1[(UP_C + k1) * MT] : 1.0;
-      const double zrp = S1[(UP_R + k1) * MT] * rcp64(c1);
+      const double c1 = ok1 ? S1[UP_C * 64 + 2 * lane + (ra0 ? 1 : 0)] : 1.0;
+      const double zrp = S1[UP_R * 64 + 2 * lane + (ra0 ? 1 : 0)] * rcp64(c1);
       const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
       if constexpr (ra0) {
         const double zbl = (rc0.b - (qc.E.b * zr0_e + qc.E.a * zr0 + qc.N.b * zrp + Nm.b * zrm)) * rcp64(qc.C.b);
@@ -1674,10 +1686,10 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
     S9 A, Bc;
     st9_pair(qc, Nm, NEm, NWm, A, Bc);
     if (lane == 0) {
-      A.w = S[(UP_X + 0) * MT];
-      A.sw = S[(UP_X + 1) * MT];
+      A.w = S[LY::X + 0];
+      A.sw = S[LY::X + 1];
     } else if (lane == 31) {
-      Bc.se = S[(UP_X + 0) * MT];
+      Bc.se = S[LY::X + 2];
     }
     Nm = qc.N; NEm = qc.NE; NWm = qc.NW;
     // v(y) = z + P zc
@@ -1685,23 +1697,24 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
     {
       double w0, w1;
       if constexpr (ra0) {  // a = C point, b = H-edge
-        const double c0 = S[(UP_ZC + 0) * MT], c1 = S[(UP_ZC + 1) * MT];
+        const double c0 = S[LY::ZC0 + lane], c1 = S[LY::ZC0 + lane + 1];
         v0.a += c0;
         edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
         v0.b += w0 * c0 + w1 * c1;
       } else {  // a = V-edge, b = centre
-        const double c00 = S[(UP_ZC + 0) * MT], c10 = S[(UP_ZC + 1) * MT], c01 = S[(UP_ZC + 2) * MT],
-                     c11 = S[(UP_ZC + 3) * MT];
+        const double c00 = S[LY::ZC0 + lane], c10 = S[LY::ZC0 + lane + 1], c01 = S[LY::ZC1 + lane],
+                     c11 = S[LY::ZC1 + lane + 1];
         edge_w(A, false, opdep != 0, false, false, false, w0, w1);
         v0.a += w0 * c00 + w1 * c01;
-        v0.b += S[(UP_PW + 0) * MT] * c00 + S[(UP_PW + 1) * MT] * c10 + S[(UP_PW + 2) * MT] * c01 +
-                S[(UP_PW + 3) * MT] * c11;
+        v0.b += S[LY::PW + lane] * c00 + S[LY::PW + 32 + lane] * c10 + S[LY::PW + 64 + lane] * c01 +
+                S[LY::PW + 96 + lane] * c11;
       }
       const bool yin = (unsigned)y <= (unsigned)m;
       if (!yin || (unsigned)xa > (unsigned)m || is_dir(bc, m, xa, y)) v0.a = 0.0;
       if (!yin || (unsigned)xb > (unsigned)m || is_dir(bc, m, xb, y)) v0.b = 0.0;
     }
-    // the slot of row y is consumed: stage row y + UP_RING into it
+    // the slot of row y is consumed (by every lane): stage row y + UP_RING into it
+    __syncwarp();
     issue(y + UP_RING);
     cpa_commit();
     // neighbours in row y of a node of row y−1 at column a / b: N, NE, NW
@@ -1750,70 +1763,55 @@ __global__ void __launch_bounds__(MT, 3) c_up_ring_kernel(L9 L, int bc, int opde
   }
   cpa_wait<0>();
 }
-constexpr size_t UP_RING_SMEM = sizeof(double) * UP_RING * UP_SLOTS * MT;
 
 // Fused pre-smoother + residual + restriction, ring-staged: z (red r/C, black (r − Σ_WENS a z_red)/C,
 // as c_pre_march_kernel) is formed in registers two rows ahead of the residual and never stored;
 // the residual and rc = Pᵀ t follow c_restrict_march_kernel. Reads C, E, N, NE, NW, r, pw; writes
-// rc. Slots per row: the operator pair (10), r (2), the centre weights of odd rows (4).
-enum { DN_C = 0, DN_E = 2, DN_N = 4, DN_NE = 6, DN_NW = 8, DN_R = 10, DN_PW = 12, DN_SLOTS = 16 };
-constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 64 KB per CTA, 3 CTAs per SM
-constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * DN_SLOTS * MT;
+// rc. Ring rows use the warp layout of the up kernel (C E N NE NW r, 64 columns each); the centre
+// weights of the odd rows are loaded into registers one row pair ahead.
+enum { DN_C = 0, DN_E = 1, DN_N = 2, DN_NE = 3, DN_NW = 4, DN_R = 5, DN_WORDS = 6 * 64 };
+constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 4 × 4 warps × 384 × 8 B = 48 KB
+constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * MW * DN_WORDS;
 
-__global__ void __launch_bounds__(MT, 3) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+__global__ void __launch_bounds__(MT, 4) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                             PW4 pw, Geo gc, double* __restrict__ rc,
                                                             const int* flags) {
   const int b = blockIdx.z;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  extern __shared__ double ring[];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int strip = blockIdx.x * MW + (tid >> 5);
+  extern __shared__ __align__(16) double ring[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int strip = blockIdx.x * MW + warp;
   const int I = strip * 30 - 1 + lane;
   const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
   const int lyc = coarse_rows_per_warp(gc.m);
   const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
-  const int m = L.m, n0 = L.n0, mc = gc.m, xa = 2 * I, xb = xa + 1;
+  const int m = L.m, n0 = L.n0, mc = gc.m, xa = 2 * I, xb = xa + 1, x0 = xa - 2 * lane;
   const int64_t off = (int64_t)b * L.Nn;
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  const double* Cb = L.C + off;
-  const double* Eb = L.E + off;
-  const double* Nb = L.N + off;
-  const double* NEb = L.NE + off;
-  const double* NWb = L.NW + off;
-  const double* rb = r + off;
+  const double* arr[6] = {L.C + off, L.E + off, L.N + off, L.NE + off, L.NW + off, r + off};
   const int ys = 2 * J0 - 1;
   const int ylast = 2 * J1 + 1;  // residual rows end at 2J1 − 1; their z needs raw rows up to 2J1 + 1
-  auto slot = [&](int y) { return ring + (size_t)((unsigned)(y - (ys - 2)) % DN_RING) * DN_SLOTS * MT + tid; };
+  auto slot = [&](int y) {
+    return ring + ((size_t)((unsigned)(y - (ys - 2)) % DN_RING) * MW + warp) * DN_WORDS;
+  };
   auto issue = [&](int y) {
     if (y > ylast) return;
     double* S = slot(y);
     const bool yok = (unsigned)y < (unsigned)n0;
-    const bool aok = yok && (unsigned)xa < (unsigned)n0, bok = yok && (unsigned)xb < (unsigned)n0;
-    const int64_t ia = (int64_t)y * n0 + xa, ib = ia + 1;
-    cpa8(S + (DN_C + 0) * MT, Cb + ia, aok);
-    cpa8(S + (DN_C + 1) * MT, Cb + ib, bok);
-    cpa8(S + (DN_E + 0) * MT, Eb + ia, aok);
-    cpa8(S + (DN_E + 1) * MT, Eb + ib, bok);
-    cpa8(S + (DN_N + 0) * MT, Nb + ia, aok);
-    cpa8(S + (DN_N + 1) * MT, Nb + ib, bok);
-    cpa8(S + (DN_NE + 0) * MT, NEb + ia, aok);
-    cpa8(S + (DN_NE + 1) * MT, NEb + ib, bok);
-    cpa8(S + (DN_NW + 0) * MT, NWb + ia, aok);
-    cpa8(S + (DN_NW + 1) * MT, NWb + ib, bok);
-    cpa8(S + (DN_R + 0) * MT, rb + ia, aok);
-    cpa8(S + (DN_R + 1) * MT, rb + ib, bok);
-    if (y & 1) {  // centre weights of cell (I, y >> 1)
-      const int Jc = y >> 1;
-      const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
-      const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-      cpa8(S + (DN_PW + 0) * MT, pw.w0 + cell, ok);
-      cpa8(S + (DN_PW + 1) * MT, pw.w1 + cell, ok);
-      cpa8(S + (DN_PW + 2) * MT, pw.w2 + cell, ok);
-      cpa8(S + (DN_PW + 3) * MT, pw.w3 + cell, ok);
+    const int c0 = x0 + lane, c1 = c0 + 32;
+    const bool ok0 = yok && (unsigned)c0 < (unsigned)n0, ok1 = yok && (unsigned)c1 < (unsigned)n0;
+    const int64_t i0 = (int64_t)y * n0 + c0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      cpa8(S + k * 64 + lane, arr[k] + i0, ok0);
+      cpa8(S + k * 64 + 32 + lane, arr[k] + i0 + 32, ok1);
     }
   };
-  auto P2 = [&](const double* S, int k) { return Pair{S[k * MT], S[(k + 1) * MT]}; };
+  auto P2 = [&](const double* S, int k) {
+    const double2 v = *reinterpret_cast<const double2*>(S + k * 64 + 2 * lane);
+    return Pair{v.x, v.y};
+  };
   auto Cpair = [&](const double* S, int y) {  // off-grid rows are identity
     Pair c = P2(S, DN_C);
     const bool yok = (unsigned)y < (unsigned)n0;
@@ -1825,7 +1823,7 @@ __global__ void __launch_bounds__(MT, 3) c_down_ring_kernel(L9 L, int bc, int op
   auto zred = [&](int y) {
     const double* S = slot(y);
     const Pair c = Cpair(S, y), rr = P2(S, DN_R);
-    return RED_IS_A(y) ? rr.a / c.a : rr.b / c.b;
+    return RED_IS_A(y) ? rr.a * rcp64(c.a) : rr.b * rcp64(c.b);
   };
   // pre-smoothed pair of row y from its red value zr0 and the red values of rows y∓1 (zrm, zrp);
   // Nm = N of row y − 1
@@ -1834,18 +1832,30 @@ __global__ void __launch_bounds__(MT, 3) c_down_ring_kernel(L9 L, int bc, int op
     const Pair c = Cpair(S, y), E0 = P2(S, DN_E), N0 = P2(S, DN_N), r0 = P2(S, DN_R);
     const double zr0_e = shdn(zr0), zr0_w = shup(zr0), Ew = shup(E0.b);
     if (RED_IS_A(y)) {
-      const double zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) / c.b;
+      const double zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) * rcp64(c.b);
       return Pair{zr0, zbl};
     }
-    const double zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) / c.a;
+    const double zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) * rcp64(c.a);
     return Pair{zbl, zr0};
   };
+  // centre weights of cell (I, Jc) (odd row 2Jc+1); 0 off the cells
+  auto W4 = [&](int Jc, double w[4]) {
+    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+  };
+  double wn[4];
+  W4(J0 - 1, wn);
   // prologue: rows ys−2 … ys+1 staged; z of rows ys−1, ys
   for (int j = 0; j < DN_RING; ++j) {
     issue(ys - 2 + j);
     cpa_commit();
   }
   cpa_wait<1>();  // rows ys−2, ys−1, ys
+  __syncwarp();
   const double zr_m2 = zred(ys - 2), zr_m1 = zred(ys - 1), zr_0 = zred(ys);
   const Pair N_m2 = P2(slot(ys - 2), DN_N);
   Pair zm = zpair(ys - 1, zr_m2, zr_m1, zr_0, N_m2);
@@ -1856,20 +1866,28 @@ __global__ void __launch_bounds__(MT, 3) c_down_ring_kernel(L9 L, int bc, int op
     NEm = P2(S, DN_NE);
     NWm = P2(S, DN_NW);
   }
+  __syncwarp();
   issue(ys + 2);  // into the slot of row ys−2
   cpa_commit();
   cpa_wait<1>();  // row ys+1
+  __syncwarp();
   double zrA = zr_0, zrB = zred(ys + 1);  // red z of rows y, y+1 entering row(y)
   Pair z0 = zpair(ys, zr_m1, zr_0, zrB, Nm);
+  __syncwarp();
   issue(ys + 3);  // into the slot of row ys−1
   cpa_commit();
-  // residuals of row y (both columns) and the row's stencils; advances the state to row y+1
+  // residuals of row y (both columns) and the row's stencils; advances the state to row y+1 and
+  // stages row y+4 into row y's slot
   auto row = [&](int y, double& ta, double& tb, S9& A, S9& Bc) {
     cpa_wait<1>();  // row y+2
+    __syncwarp();
     const double zrC = zred(y + 2);
     const double* S = slot(y);
     const R9 q{Cpair(S, y), P2(S, DN_E), P2(S, DN_N), P2(S, DN_NE), P2(S, DN_NW)};
     const Pair zp = zpair(y + 1, zrA, zrB, zrC, q.N);
+    __syncwarp();
+    issue(y + 4);
+    cpa_commit();
     st9_pair(q, Nm, NEm, NWm, A, Bc);
     const bool red_a = RED_IS_A(y);
     ta = red_a ? -dot8_a(A, zm, z0, zp) : -diag_a(A, zm, zp);
@@ -1880,35 +1898,26 @@ __global__ void __launch_bounds__(MT, 3) c_down_ring_kernel(L9 L, int bc, int op
     zm = z0; z0 = zp;
     zrA = zrB; zrB = zrC;
   };
-  auto W4 = [&](int y, double w[4]) {  // centre weights of odd row y (cell (I, y >> 1)); 0 off the cells
-    const double* S = slot(y);
-    w[0] = S[(DN_PW + 0) * MT];
-    w[1] = S[(DN_PW + 1) * MT];
-    w[2] = S[(DN_PW + 2) * MT];
-    w[3] = S[(DN_PW + 3) * MT];
-  };
   double w[4], ta, tb, w0, w1;
   S9 A, Bc;
+  // odd row 2J0−1: contributions to coarse row J0 (V-edge N weight, centre NW own / NE previous lane)
   row(ys, ta, tb, A, Bc);
-  W4(ys, w);
-  issue(ys + 4);
-  cpa_commit();
+  w[0] = wn[0]; w[1] = wn[1]; w[2] = wn[2]; w[3] = wn[3];
+  W4(J0, wn);
   edge_w(A, false, opdep != 0, false, false, false, w0, w1);
   double carry_own = w1 * ta + w[2] * tb, carry_ne = w[3] * tb;
   double* rcb = rc + (int64_t)b * gc.N;
   for (int J = J0; J < J1; ++J) {
-    const int ye = 2 * J, yo = ye + 1;
-    row(ye, ta, tb, A, Bc);
-    issue(ye + 4);
-    cpa_commit();
+    // even row 2J: C point (a) and H-edge (b)
+    row(2 * J, ta, tb, A, Bc);
     edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
     double acc = carry_own + shup(carry_ne) + ta + w0 * tb;
-    const double he = w1 * tb;
+    const double he = w1 * tb;  // H-edge (2I+1, 2J) → (I+1, J)
     acc += shup(he);
-    row(yo, ta, tb, A, Bc);
-    W4(yo, w);
-    issue(yo + 4);
-    cpa_commit();
+    // odd row 2J+1: V-edge (a) and centre (b)
+    row(2 * J + 1, ta, tb, A, Bc);
+    w[0] = wn[0]; w[1] = wn[1]; w[2] = wn[2]; w[3] = wn[3];
+    W4(J + 1, wn);
     edge_w(A, false, opdep != 0, false, false, false, w0, w1);
     const double se = w[1] * tb;
     acc += w0 * ta + w[0] * tb + shup(se);
@@ -2870,19 +2879,19 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       static bool attr = false;
       if (!attr) {
         OSC_CUDA(cudaFuncSetAttribute(c_up_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)UP_RING_SMEM));
+                                      (int)up_ring_smem<false>()));
         attr = true;
       }
-      c_up_ring_kernel<false><<<march_grid(L.m, 2, B), MT, UP_RING_SMEM, st>>>(
+      c_up_ring_kernel<false><<<march_grid(L.m, 2, B), MT, up_ring_smem<false>(), st>>>(
           l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
     } else {
       static bool attr = false;
       if (!attr) {
         OSC_CUDA(cudaFuncSetAttribute(c_up_ring_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)UP_RING_SMEM));
+                                      (int)up_ring_smem<true>()));
         attr = true;
       }
-      c_up_ring_kernel<true><<<march_grid(L.m, 2, B), MT, UP_RING_SMEM, st>>>(
+      c_up_ring_kernel<true><<<march_grid(L.m, 2, B), MT, up_ring_smem<true>(), st>>>(
           l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
     }
     if (dbg) {

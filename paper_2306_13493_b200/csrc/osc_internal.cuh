@@ -111,6 +111,9 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   size_t mem_budget = 0;
   bool profiling = false;
+  std::string profile_only;  // non-empty: events only around this kernel class's launches
+  std::vector<cudaEvent_t> ev_pool;  // timing events, reused across profiled launches
+  size_t ev_next = 0;
   int64_t launches = 0;
   std::string tag;  // appended to kernel-class names ("name@tag"), e.g. the solve grid m
   std::vector<KernelStat> stats;
@@ -122,6 +125,7 @@ struct Ctx {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_ce_done[2] = {nullptr, nullptr};
   int stat_class(const char* name);
+  cudaEvent_t pool_event();
   void flush_stats();
 };
 

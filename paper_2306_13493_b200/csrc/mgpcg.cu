@@ -230,10 +230,10 @@ __device__ __forceinline__ void edge_w(const S9& r, bool horiz, bool opdep, bool
   if (d1) w1 = 0.0;
 }
 
-// Centre (odd x, odd y) weights to SW, SE, NW, NE.
-__device__ void centre_w(const L9& R, int bc, int b, int x, int y, bool opdep, double w[4]) {
-  const int m = R.m, mc = m / 2;
-  const int64_t off = (int64_t)b * R.Nn;
+// Centre (odd x, odd y) weights to SW, SE, NW, NE; `row(x, y)` gives the level's S9 row of a node.
+template <class RowF>
+__device__ __forceinline__ void centre_w_f(RowF row, int bc, int m, int x, int y, bool opdep, double w[4]) {
+  const int mc = m / 2;
   const int I = (x - 1) >> 1, J = (y - 1) >> 1;
   const bool dSW = is_dir(bc, mc, I, J), dSE = is_dir(bc, mc, I + 1, J), dNW = is_dir(bc, mc, I, J + 1),
              dNE = is_dir(bc, mc, I + 1, J + 1);
@@ -244,17 +244,42 @@ __device__ void centre_w(const L9& R, int bc, int b, int x, int y, bool opdep, d
     w[3] = dNE ? 0.0 : 0.5;
     return;
   }
-  const S9 rc = row_s(R, off, x, y);
+  const S9 rc = row(x, y);
   double wWs, wWn, wEs, wEn, wSw, wSe, wNw, wNe;  // V-edges W, E: (S, N); H-edges S, N: (W, E)
-  edge_w(row_s(R, off, x - 1, y), false, true, dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
-  edge_w(row_s(R, off, x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
-  edge_w(row_s(R, off, x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
-  edge_w(row_s(R, off, x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
+  edge_w(row(x - 1, y), false, true, dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
+  edge_w(row(x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
+  edge_w(row(x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
+  edge_w(row(x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
   const double ic = 1.0 / rc.c;
   w[0] = dSW ? 0.0 : -(rc.w * wWs + rc.s * wSw + rc.sw) * ic;
   w[1] = dSE ? 0.0 : -(rc.e * wEs + rc.s * wSe + rc.se) * ic;
   w[2] = dNW ? 0.0 : -(rc.w * wWn + rc.n * wNw + rc.nw) * ic;
   w[3] = dNE ? 0.0 : -(rc.e * wEn + rc.n * wNe + rc.ne) * ic;
+}
+
+__device__ void centre_w(const L9& R, int bc, int b, int x, int y, bool opdep, double w[4]) {
+  const int64_t off = (int64_t)b * R.Nn;
+  centre_w_f([&](int xx, int yy) { return row_s(R, off, xx, yy); }, bc, R.m, x, y, opdep, w);
+}
+
+// P row of node (x, y) (weights to its coarse parents, meaning by parity; see prow_kernel)
+template <class RowF>
+__device__ __forceinline__ void prow_f(RowF row, int bc, int m, int x, int y, bool opdep, double w[4]) {
+  const int mc = m / 2;
+  w[0] = w[1] = w[2] = w[3] = 0.0;
+  if (x < 0 || x > m || y < 0 || y > m) return;
+  const bool fdir = is_dir(bc, m, x, y);
+  if ((x & 1) == 0 && (y & 1) == 0) {
+    w[0] = fdir ? 0.0 : 1.0;
+  } else if ((x & 1) && (y & 1)) {
+    centre_w_f(row, bc, m, x, y, opdep, w);
+  } else {
+    const bool horiz = (x & 1) != 0;
+    const int I0 = horiz ? (x - 1) >> 1 : x >> 1, J0 = horiz ? y >> 1 : (y - 1) >> 1;
+    const int I1 = horiz ? I0 + 1 : I0, J1 = horiz ? J0 : J0 + 1;
+    const S9 r = opdep ? row(x, y) : S9{};
+    edge_w(r, horiz, opdep, fdir, is_dir(bc, mc, I0, J0), is_dir(bc, mc, I1, J1), w[0], w[1]);
+  }
 }
 
 // P rows of every node of a level (scratch P0..P3, per node, meaning by parity as above) and the
@@ -358,6 +383,194 @@ __global__ void __launch_bounds__(NT) rap_kernel(L9 F, int bc, const double* __r
             acc[by + 1][bx + 2] += pa * P1[jj];
             acc[by + 2][bx + 1] += pa * P2[jj];
             acc[by + 2][bx + 2] += pa * P3[jj];
+          }
+        }
+    }
+  Cc[o] = acc[1][1];
+  Ec[o] = acc[1][2];
+  Nc[o] = acc[2][1];
+  NEc[o] = acc[2][2];
+  NWc[o] = acc[2][0];
+}
+
+// Fused Galerkin setup of one level pair, tiled in shared memory: the fine rows (level 0: rebuilt
+// from nodal k; levels ≥ 1: the stored 9-point rows) of a halo'd tile are staged once, the P rows of
+// the tile's fine nodes are formed in shared memory (prow_f, the arithmetic of prow_kernel), and each
+// thread forms one coarse Galerkin row (the loop of rap_kernel) and the centre weights pw of its
+// cell. HBM traffic is the fine input (k or C…NW, plus L2-served halo) and the coarse output, instead
+// of the stored rows, P rows and their re-reads of the unfused rows0/prow/rap sequence.
+// Tile: GT_X × GT_Y coarse nodes, one per thread. Fine regions (global coordinates):
+//   P rows  x ∈ [2I0−2, 2I0+2GT_X], y ∈ [2J0−2, 2J0+2GT_Y]
+//   rows    read at x ∈ [2I0−4, 2I0+2GT_X+2], y ∈ [2J0−4, 2J0+2GT_Y+1]
+//   k (L0)  x ∈ [2I0−5, 2I0+2GT_X+3], y ∈ [2J0−5, 2J0+2GT_Y+2]
+constexpr int GT_X = 16, GT_Y = 8, GT_THREADS = GT_X * GT_Y;
+constexpr int GA_W = 2 * GT_X + 7, GA_H = 2 * GT_Y + 6;
+constexpr int GP_W = 2 * GT_X + 3, GP_H = 2 * GT_Y + 3;
+constexpr int GK_W = 2 * GT_X + 9, GK_H = 2 * GT_Y + 8;
+constexpr size_t galerkin_tile_smem(bool l0) {
+  return sizeof(double) * ((l0 ? 3 : 5) * GA_W * GA_H + 4 * GP_W * GP_H + (l0 ? GK_W * GK_H : 0));
+}
+
+template <bool L0K>
+__global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double* __restrict__ k0, L9 F, int bc,
+                                                                   int opdep, Geo gc, double* __restrict__ Cc,
+                                                                   double* __restrict__ Ec, double* __restrict__ Nc,
+                                                                   double* __restrict__ NEc,
+                                                                   double* __restrict__ NWc, double* __restrict__ pw0,
+                                                                   double* __restrict__ pw1, double* __restrict__ pw2,
+                                                                   double* __restrict__ pw3) {
+  extern __shared__ double gsm[];
+  const int b = blockIdx.z;
+  const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y;
+  const int m = F.m, n0 = F.n0, mc = gc.m, mcl = m / 2;
+  const int ax = 2 * I0 - 4, ay = 2 * J0 - 4, px = 2 * I0 - 2, py = 2 * J0 - 2;
+  constexpr int NA = L0K ? 3 : 5;
+  double* sA = gsm;                          // raw rows: C, E, N [, NE, NW], each GA_H × GA_W
+  double* sP = gsm + NA * GA_W * GA_H;       // P rows: 4 × GP_H × GP_W
+  auto A = [&](int q, int lx, int ly) -> double& { return sA[(q * GA_H + ly) * GA_W + lx]; };
+  auto P = [&](int q, int lx, int ly) -> double& { return sP[(q * GP_H + ly) * GP_W + lx]; };
+  const int tid = threadIdx.x;
+  if constexpr (L0K) {
+    double* sK = sP + 4 * GP_W * GP_H;
+    const double* kb = k0 + (int64_t)b * F.Nn;
+    const int kx = ax - 1, ky = ay - 1;
+    for (int i = tid; i < GK_W * GK_H; i += GT_THREADS) {
+      const int lx = i % GK_W, ly = i / GK_W, x = kx + lx, y = ky + ly;
+      sK[i] = ((unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0) ? __ldg(kb + (int64_t)y * n0 + x) : 0.0;
+    }
+    __syncthreads();
+    // level-0 rows (row_k, stride 1) of the raw region from the staged k
+    constexpr double third = 1.0 / 3.0;
+    auto K = [&](int x, int y) { return sK[(y - ky) * GK_W + (x - kx)]; };
+    for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
+      const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
+      double c = 1.0, e = 0.0, nn = 0.0;
+      if (!(x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y))) {
+        auto Ed = [&](int a, int b2) -> double {
+          if (a < 0 || a >= m) return 0.0;
+          return -0.5 * ((b2 < m ? (K(a, b2) + K(a + 1, b2) + K(a + 1, b2 + 1)) * third : 0.0) +
+                         (b2 > 0 ? (K(a, b2 - 1) + K(a + 1, b2) + K(a, b2)) * third : 0.0));
+        };
+        auto Nd = [&](int a, int b2) -> double {
+          if (b2 < 0 || b2 >= m) return 0.0;
+          return -0.5 * ((a < m ? (K(a, b2) + K(a + 1, b2 + 1) + K(a, b2 + 1)) * third : 0.0) +
+                         (a > 0 ? (K(a - 1, b2) + K(a, b2) + K(a, b2 + 1)) * third : 0.0));
+        };
+        const double E = Ed(x, y), W = Ed(x - 1, y), Nn = Nd(x, y), S = Nd(x, y - 1);
+        c = -(E + W + Nn + S);
+        e = is_dir(bc, m, x + 1, y) ? 0.0 : E;
+        nn = is_dir(bc, m, x, y + 1) ? 0.0 : Nn;
+      }
+      A(0, lx, ly) = c;
+      A(1, lx, ly) = e;
+      A(2, lx, ly) = nn;
+    }
+  } else {
+    const int64_t off = (int64_t)b * F.Nn;
+    const double* src[5] = {F.C + off, F.E + off, F.N + off, F.NE + off, F.NW + off};
+    for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
+      const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
+      const bool in = (unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0;
+      const int64_t o = (int64_t)y * n0 + x;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) A(q, lx, ly) = in ? __ldg(src[q] + o) : (q == 0 ? 1.0 : 0.0);
+    }
+  }
+  __syncthreads();
+  // S9 row of fine node (x, y) from the staged rows (row_s semantics)
+  auto RS = [&](int x, int y) -> S9 {
+    S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (x < 0 || x > m || y < 0 || y > m) {
+      r.c = 1.0;
+      return r;
+    }
+    const int lx = x - ax, ly = y - ay;
+    r.c = A(0, lx, ly);
+    r.e = A(1, lx, ly);
+    r.n = A(2, lx, ly);
+    if (x > 0) r.w = A(1, lx - 1, ly);
+    if (y > 0) r.s = A(2, lx, ly - 1);
+    if constexpr (!L0K) {
+      r.ne = A(3, lx, ly);
+      r.nw = A(4, lx, ly);
+      if (x > 0 && y > 0) r.sw = A(3, lx - 1, ly - 1);
+      if (x < m && y > 0) r.se = A(4, lx + 1, ly - 1);
+    }
+    return r;
+  };
+  // P rows of the tile's fine region; centres of the tile's own cells also store pw
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  for (int i = tid; i < GP_W * GP_H; i += GT_THREADS) {
+    const int lx = i % GP_W, ly = i / GP_W, x = px + lx, y = py + ly;
+    double w[4];
+    prow_f(RS, bc, m, x, y, opdep != 0, w);
+    P(0, lx, ly) = w[0];
+    P(1, lx, ly) = w[1];
+    P(2, lx, ly) = w[2];
+    P(3, lx, ly) = w[3];
+    if ((x & 1) && (y & 1) && x < m && y < m) {
+      const int Ic = (x - 1) >> 1, Jc = (y - 1) >> 1;
+      if (Ic >= I0 && Ic < I0 + GT_X && Jc >= J0 && Jc < J0 + GT_Y) {
+        const int64_t cell = cb0 + (int64_t)Jc * mcl + Ic;
+        pw0[cell] = w[0];
+        pw1[cell] = w[1];
+        pw2[cell] = w[2];
+        pw3[cell] = w[3];
+      }
+    }
+  }
+  __syncthreads();
+  // coarse Galerkin row of (I, J) (rap_kernel's loop over the staged P rows and fine rows)
+  const int I = I0 + tid % GT_X, J = J0 + tid / GT_X;
+  if (I > mc || J > mc) return;
+  const int64_t o = (int64_t)b * gc.N + (int64_t)J * gc.n0 + I;
+  if (is_dir(bc, mc, I, J)) {
+    Cc[o] = 1.0;
+    Ec[o] = Nc[o] = NEc[o] = NWc[o] = 0.0;
+    return;
+  }
+  double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+  for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
+    for (int di = -1; di <= 1; ++di) {
+      const int xi = 2 * I + di, yi = 2 * J + dj;
+      if (xi < 0 || xi > m || yi < 0 || yi > m) continue;
+      const int lxi = xi - px, lyi = yi - py;
+      double pic;
+      if (di == 0 && dj == 0) pic = P(0, lxi, lyi);
+      else if (dj == 0) pic = di > 0 ? P(0, lxi, lyi) : P(1, lxi, lyi);
+      else if (di == 0) pic = dj > 0 ? P(0, lxi, lyi) : P(1, lxi, lyi);
+      else pic = dj > 0 ? (di > 0 ? P(0, lxi, lyi) : P(1, lxi, lyi)) : (di > 0 ? P(2, lxi, lyi) : P(3, lxi, lyi));
+      if (pic == 0.0) continue;
+      const S9 r = RS(xi, yi);
+#pragma unroll
+      for (int ey = -1; ey <= 1; ++ey)
+#pragma unroll
+        for (int ex = -1; ex <= 1; ++ex) {
+          const double a = ey < 0 ? (ex < 0 ? r.sw : ex == 0 ? r.s : r.se)
+                                  : ey == 0 ? (ex < 0 ? r.w : ex == 0 ? r.c : r.e)
+                                            : (ex < 0 ? r.nw : ex == 0 ? r.n : r.ne);
+          const int xj = xi + ex, yj = yi + ey;
+          if (a == 0.0 || xj < 0 || xj > m || yj < 0 || yj > m) continue;
+          const int lxj = xj - px, lyj = yj - py;
+          const double pa = pic * a;
+          const int dx = di + ex, dy = dj + ey;
+          const bool ox = (dx & 1) != 0, oy = (dy & 1) != 0;
+          const int bx = dx >> 1, by = dy >> 1;
+          if (!ox && !oy) {
+            acc[by + 1][bx + 1] += pa * P(0, lxj, lyj);
+          } else if (ox && !oy) {
+            acc[by + 1][bx + 1] += pa * P(0, lxj, lyj);
+            acc[by + 1][bx + 2] += pa * P(1, lxj, lyj);
+          } else if (!ox && oy) {
+            acc[by + 1][bx + 1] += pa * P(0, lxj, lyj);
+            acc[by + 2][bx + 1] += pa * P(1, lxj, lyj);
+          } else {
+            acc[by + 1][bx + 1] += pa * P(0, lxj, lyj);
+            acc[by + 1][bx + 2] += pa * P(1, lxj, lyj);
+            acc[by + 2][bx + 1] += pa * P(2, lxj, lyj);
+            acc[by + 2][bx + 2] += pa * P(3, lxj, lyj);
           }
         }
     }
@@ -2934,11 +3147,36 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
     KScope ks(ctx, "mg_setup.rows");
     const SolverLevel& L = w.lev[0];
     rediscretize_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(L0.k, g0, 1, bc, g0, L.C, L.E, L.Nw, L.NE, L.NW);
+  } else if (mode != OSC_COARSE_REDISCRETIZE && !std::getenv("OSC_UNFUSED_SETUP")) {
+    // fused tiled Galerkin setup per level pair (galerkin_tile_kernel)
+    static bool attr = false;
+    if (!attr) {
+      OSC_CUDA(cudaFuncSetAttribute(galerkin_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)galerkin_tile_smem(true)));
+      OSC_CUDA(cudaFuncSetAttribute(galerkin_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)galerkin_tile_smem(false)));
+      attr = true;
+    }
+    for (int l = 0; l + 1 < w.nlev; ++l) {
+      const SolverLevel& F = w.lev[l];
+      const SolverLevel& C = w.lev[l + 1];
+      const dim3 grid((unsigned)((C.m + GT_X) / GT_X), (unsigned)((C.m + GT_Y) / GT_Y), (unsigned)B);
+      KScope ks(ctx, l == 0 ? "mg_setup.galerkin.L0" : "mg_setup.galerkin.Lc");
+      if (l == 0)
+        galerkin_tile_kernel<true><<<grid, GT_THREADS, galerkin_tile_smem(true), st>>>(
+            L0.k, L9{nullptr, nullptr, nullptr, nullptr, nullptr, F.m, F.m + 1, F.N}, bc, w.opdep, geo_of(C), C.C,
+            C.E, C.Nw, C.NE, C.NW, F.pw[0], F.pw[1], F.pw[2], F.pw[3]);
+      else
+        galerkin_tile_kernel<false><<<grid, GT_THREADS, galerkin_tile_smem(false), st>>>(
+            nullptr, l9_of(F), bc, w.opdep, geo_of(C), C.C, C.E, C.Nw, C.NE, C.NW, F.pw[0], F.pw[1], F.pw[2],
+            F.pw[3]);
+    }
   } else {  // level-0 rows (5-point) into scratch: u, r, r2 are free until pcg_init
     KScope ks(ctx, "mg_setup.rows");
     rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, L0.r, w.r2);
   }
-  for (int l = 0; l + 1 < w.nlev; ++l) {
+  const bool fused = w.nlev > 1 && mode != OSC_COARSE_REDISCRETIZE && !std::getenv("OSC_UNFUSED_SETUP");
+  for (int l = 0; !fused && l + 1 < w.nlev; ++l) {
     const SolverLevel& F = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     const L9 R = l == 0 ? L9{w.u, L0.r, w.r2, nullptr, nullptr, F.m, F.m + 1, F.N} : l9_of(F);

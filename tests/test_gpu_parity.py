@@ -157,6 +157,25 @@ def test_galerkin_fewer_iterations(P, ctx, port, m):
     assert rc == 0 and relmax(ug[0], uo) < 1e-7
 
 
+@pytest.mark.parametrize("m", [64, 256, 1024])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_fused_setup_matches_unfused(P, ctx, m, bc, monkeypatch):
+    """The tiled Galerkin setup (galerkin_tile_kernel) builds the same hierarchy as the unfused
+    rows0 → prow → rap sequence (same arithmetic): identical iteration counts and solutions."""
+    api = P.api
+    model = api.CovarianceModel.matern(2.0, 3.0 / m, 0.5)
+    op = api.build_operator(api.GridSpec.square(m), model)
+    Z = op.sample_fields(None, count=3, seed=7, ell=0, index0=0, fine=True, ctx=ctx)
+    prob = api.ProblemSpec(model, bc=api.BC(bc))
+    for mode in (api.CoarseOperator.Galerkin, api.CoarseOperator.GalerkinLinear):
+        u1, it1, _ = api.assemble_and_solve(m, Z, prob, api.SolverOptions(coarse_operator=mode), ctx=ctx)
+        monkeypatch.setenv("OSC_UNFUSED_SETUP", "1")
+        u2, it2, _ = api.assemble_and_solve(m, Z, prob, api.SolverOptions(coarse_operator=mode), ctx=ctx)
+        monkeypatch.delenv("OSC_UNFUSED_SETUP")
+        assert np.array_equal(it1, it2), (mode, it1, it2)
+        assert relmax(u1, u2) < 1e-13, (mode, relmax(u1, u2))
+
+
 def test_solve_analytic(P, ctx):
     """SPEC fem examples: Z ≡ 0, f = 0 → u = 1 − x; point QoI 8/15; L2 1/√3; flux 1; ∫u = 1/2."""
     api = P.api

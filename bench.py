@@ -95,6 +95,9 @@ def algorithmic_bytes_per_sample(W, n, it=None):
 KERNEL_BYTES = {
     "pcg_apply": 4 * 8,                    # read k, z, p_old; write p_new
     "pcg_update_down": 7 * 8,              # read k, p, r, u; write u, r, z
+    "pcg_update": 8 * 8,                   # one-reduction PCG: read k, z, p_old, r, u; write p, u, r
+    "mg_restrict_r.L0": 8 + 8 + 8 + 2,     # read k, r, pw; write rc (pre-smoother recomputed)
+    "mg_smooth_up_r.L0": 8 + 8 + 2 + 8 + 8,  # read k, r, zc, pw; write z
     "mg_restrict.L0": 8 + 8 + 8 + 2,       # read k, z, pw; write rc
     "mg_smooth_up.L0": 8 + 8 + 8 + 2 + 8 + 8,  # read k, r, z, zc, pw; write z
     "mg_pre": 24 + 8 + 8,                  # read C, E, N, r; write z

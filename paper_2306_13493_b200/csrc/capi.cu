@@ -137,6 +137,7 @@ int osc_ctx_create(int device, osc_ctx** out) {
       OSC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       OSC_CUDA(cudaHostAlloc(&c->h_pinned_int, 64, cudaHostAllocDefault));
       OSC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 4; ++i) OSC_CUDA(cudaEventCreateWithFlags(&c->ev_poll[i], cudaEventDisableTiming));
       for (int i = 0; i < 2; ++i) {
         OSC_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
         OSC_CUDA(cudaEventCreateWithFlags(&c->ev_ce_done[i], cudaEventDisableTiming));
@@ -158,6 +159,9 @@ void osc_ctx_destroy(osc_ctx* c) {
                     &c->out_i, &c->tmp_host_stage, &c->sums, &c->solver.mem})
     b->release();
   if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 4; ++i)
+    if (c->ev_poll[i]) cudaEventDestroy(c->ev_poll[i]);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
     if (c->ev_ce_done[i]) cudaEventDestroy(c->ev_ce_done[i]);

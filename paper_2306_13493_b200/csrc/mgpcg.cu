@@ -1178,6 +1178,103 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
   }
 }
 
+// ---- PCG step of the one-reduction (Chronopoulos–Gear) iteration, fused with the search direction:
+//   p = z + βp (p = z first), u += αp, r −= αAp (Ap recomputed from p), ‖r‖ → convergence.
+// α and β come from the previous V-cycle's epilogue (smooth_up_kernel: γ = ⟨r, z⟩, δ = ⟨z, Az⟩,
+// β = γ/γ_old, α = γ/(δ − βγ/α_old)), so no ⟨p, Ap⟩ reduction (and no pcg_apply pass) precedes
+// the update. Reads k, z, p_old, r, u; writes p_new, u, r_next.
+template <bool INT>
+__device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double* __restrict__ k,
+                                                     const double* __restrict__ z, const double* __restrict__ p_old,
+                                                     double* __restrict__ p_new, double* __restrict__ u,
+                                                     const double* __restrict__ r, double* __restrict__ r_out,
+                                                     double* scal, int* flags, const PairCtx& c) {
+  PAIR_UNPACK
+
+  const bool first = flags[b * F_NFLAGS + F_FIRST] != 0;
+  const double beta = first ? 0.0 : scal[b * S_NSCAL + S_BETA];
+  const double alpha = scal[b * S_NSCAL + S_ALPHA];
+  const double *kb = k + off, *zb = z + off, *pb = p_old + off, *rb = r + off;
+  double* ub = u + off;
+  auto comb = [&](Pair zz, Pair oo) {
+    return first ? zz : Pair{fma(beta, oo.a, zz.a), fma(beta, oo.b, zz.b)};
+  };
+  const Pair zero{0.0, 0.0};
+  Pair km = ld2<INT>(kb, xa, y0 - 1, n0), k0 = ld2<INT>(kb, xa, y0, n0);
+  Pair pm = comb(ld2<INT>(zb, xa, y0 - 1, n0), first ? zero : ld2<INT>(pb, xa, y0 - 1, n0));
+  Pair p0 = comb(ld2<INT>(zb, xa, y0, n0), first ? zero : ld2<INT>(pb, xa, y0, n0));
+  Pair Nm, Ed;
+  edges_pair<INT>(zero, km, k0, xa, y0 - 1, m, Ed, Nm);
+  Pair kq = ld2<INT>(kb, xa, y0 + 1, n0), zq = ld2<INT>(zb, xa, y0 + 1, n0);
+  Pair oq = first ? zero : ld2<INT>(pb, xa, y0 + 1, n0);
+  Pair rq = ld2<INT>(rb, xa, y0, n0), uq = ld2<INT>(ub, xa, y0, n0);
+  double rr = 0.0;
+  for (int y = y0; y < y1; ++y) {
+    const Pair kp = kq, pp = comb(zq, oq);  // row y+1 (raw rows loaded one iteration ahead)
+    const Pair r0 = rq, u0 = uq;            // row y
+    kq = ld2<INT>(kb, xa, y + 2, n0);
+    zq = ld2<INT>(zb, xa, y + 2, n0);
+    if (!first) oq = ld2<INT>(pb, xa, y + 2, n0);
+    rq = ld2<INT>(rb, xa, y + 1, n0);
+    uq = ld2<INT>(ub, xa, y + 1, n0);
+    Pair E, N;
+    edges_pair<INT>(km, k0, kp, xa, y, m, E, N);
+    const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
+    const Pair od = offd_pair(st, pm, p0, pp);
+    const int64_t row = off + (int64_t)y * n0;
+    if (outa) {
+      const double rn = fma(-alpha, fma(st.a.d, p0.a, od.a), r0.a);
+      p_new[row + xa] = p0.a;
+      u[row + xa] = fma(alpha, p0.a, u0.a);
+      r_out[row + xa] = rn;
+      rr = fma(rn, rn, rr);
+    }
+    if (outb) {
+      const double rn = fma(-alpha, fma(st.b.d, p0.b, od.b), r0.b);
+      p_new[row + xb] = p0.b;
+      u[row + xb] = fma(alpha, p0.b, u0.b);
+      r_out[row + xb] = rn;
+      rr = fma(rn, rn, rr);
+    }
+    km = k0; k0 = kp; pm = p0; p0 = pp; Nm = N;
+  }
+  return rr;
+}
+
+__global__ void __launch_bounds__(MT, 4) pcg_update_cg_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
+                                                              const double* __restrict__ z,
+                                                              const double* __restrict__ p_old,
+                                                              double* __restrict__ p_new, double* __restrict__ u,
+                                                              const double* __restrict__ r, double* __restrict__ r_out,
+                                                              double* scal, int* flags, double2* partial, int maxp,
+                                                              unsigned* counter, int* n_active, double* hist,
+                                                              int hist_cap) {
+  PAIR_PROLOGUE
+  const double rr = interior ? pcg_update_cg_body<true>(g, bc, k, z, p_old, p_new, u, r, r_out, scal, flags, c)
+                             : pcg_update_cg_body<false>(g, bc, k, z, p_old, p_new, u, r, r_out, scal, flags, c);
+  double t0, t1;
+  if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
+    flags[b * F_NFLAGS + F_FIRST] = 0;
+    const double rel = sqrt(t0) / scal[b * S_NSCAL + S_BNORM];
+    const int it = flags[b * F_NFLAGS + F_ITERS] + 1;
+    flags[b * F_NFLAGS + F_ITERS] = it;
+    scal[b * S_NSCAL + S_REL] = rel;
+    if (hist && it < hist_cap) hist[(int64_t)b * hist_cap + it] = rel;
+    if (rel <= tol) {
+      flags[b * F_NFLAGS + F_ACTIVE] = 0;
+      atomicSub(n_active, 1);
+    } else if (!isfinite(rel)) {  // breakdown (non-finite residual): fail fast, never spin to the cap
+      flags[b * F_NFLAGS + F_ACTIVE] = 0;
+      flags[b * F_NFLAGS + F_STATUS] = OSC_ERR_SOLVER;
+      atomicSub(n_active, 1);
+    } else if (it >= flags[b * F_NFLAGS + F_MAXIT]) {
+      flags[b * F_NFLAGS + F_ACTIVE] = 0;
+      flags[b * F_NFLAGS + F_STATUS] = OSC_ERR_SOLVER;
+      atomicSub(n_active, 1);
+    }
+  }
+}
+
 // ---- PCG update fused with the level-0 pre-smoother:
 //   u += αp, r −= αAp (Ap recomputed from p), ‖r‖ → convergence,
 //   then z_red = r/D, z_black = (r − Σ A z_red)/D  (red-black GS from z = 0)
@@ -2161,6 +2258,111 @@ __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, con
   else restrict_z_body<false, false>(g, gc, bc, k, nullptr, z, pw, rc, b, I, outI, J0, J1);
 }
 
+// Level-0 restriction from the residual itself: the red-black pre-smoother from z = 0 is formed in
+// registers (z_red = r/D, z_black = (r − Σ A z_red)/D, the arithmetic pcg_update_down used to store)
+// two rows ahead of the red-node residual t = −Σ A z_black, so the pre-smoothed z is never written
+// or read. Row pipeline: ingest(q) forms the stencils of row q, z_red(q), the z pair of row q−1,
+// and returns t at the red node of row q−2. Reads k, r, pw; writes rc.
+template <bool INT>
+__device__ __forceinline__ void restrict_r_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                const double* __restrict__ r, PW4 pw, double* __restrict__ rc,
+                                                int b, int I, bool outI, int J0, int J1) {
+  const int m = g.m, n0 = g.n0, mc = gc.m;
+  const int xa = 2 * I;
+  const int64_t off = (int64_t)b * g.N;
+  const double* rb = r + off;
+  const int ys = 2 * J0 - 1;
+  EdgeRows<INT, false> er(k + off, nullptr, xa, n0, m, ys - 3);
+  const Pair zero{0.0, 0.0};
+  Pair Ed, Nq;
+  er.next(Ed, Nq);  // row ys−3: its N only
+  // pipeline state entering ingest(q): N of row q−1; E/N of rows q−1, q−2 and N of row q−3;
+  // z_red of rows q−2, q−1; the black stencil and r of row q−1; z pairs of rows q−3, q−2
+  Pair N1 = Nq, E1 = zero, N2 = zero, E2 = zero, N3 = zero;
+  double zr2 = 0.0, zr1 = 0.0, rbl1 = 0.0;
+  Sten sb1{1.0, 0.0, 0.0, 0.0, 0.0};
+  Pair zp3 = zero, zp2 = zero;
+  Pair rq = ld2<INT>(rb, xa, ys - 2, n0);
+  auto ingest = [&](int q) {
+    Pair E, N;
+    er.next(E, N);
+    const Pair r0 = rq;
+    rq = ld2<INT>(rb, xa, q + 1, n0);
+    const Sten2 st = sten_pair<INT>(E, N, N1, xa, q, m, bc);
+    const bool ra = RED_IS_A(q);
+    const double zr0 = (ra ? r0.a : r0.b) * rcp64(ra ? st.a.d : st.b.d);
+    // black of row q−1 (its red column is a iff row q−1 is even)
+    const bool ra1 = !ra;
+    const double zr1_e = shdn(zr1), zr1_w = shup(zr1);
+    const double zbl = (rbl1 - (sb1.e * (ra1 ? zr1_e : zr1) + sb1.w * (ra1 ? zr1 : zr1_w) + sb1.n * zr0 +
+                                sb1.s * zr2)) * rcp64(sb1.d);
+    const Pair zp1 = ra1 ? Pair{zr1, zbl} : Pair{zbl, zr1};
+    // t at the red node of row q−2 from the z pairs of rows q−3, q−2, q−1
+    const double t = ra ? red_resid<INT, true>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc)
+                        : red_resid<INT, false>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc);
+    // shift
+    N3 = N2; E2 = E1; N2 = N1; E1 = E; N1 = N;
+    zr2 = zr1; zr1 = zr0;
+    sb1 = ra ? st.b : st.a;
+    rbl1 = ra ? r0.b : r0.a;
+    zp3 = zp2; zp2 = zp1;
+    return t;
+  };
+  // prime: rows ys−2 … ys+1 (their t values belong to rows before ys)
+  ingest(ys - 2);
+  ingest(ys - 1);
+  ingest(ys);
+  ingest(ys + 1);
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  auto W4 = [&](int Jc, double w[4]) {
+    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+  };
+  double wc[4];
+  W4(J0 - 1, wc);
+  const double t_first = ingest(ys + 2);  // (xb, 2J0−1)
+  double a_nw = t_first * wc[2], a_ne = t_first * wc[3];
+  double* rcb = rc + (int64_t)b * gc.N;
+  for (int J = J0; J < J1; ++J) {
+    const int y = 2 * J;
+    W4(J, wc);
+    const double t_even = ingest(y + 2);  // (xa, 2J)
+    const double t = ingest(y + 3);       // (xb, 2J+1)
+    const double a_sw = t * wc[0], a_se = t * wc[1];
+    const double v = t_even + a_sw + shup(a_se) + a_nw + shup(a_ne);
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
+    a_nw = t * wc[2];
+    a_ne = t * wc[3];
+  }
+}
+
+#ifndef OSC_RR_MINB
+#define OSC_RR_MINB 4
+#endif
+__global__ void __launch_bounds__(MT, OSC_RR_MINB) restrict_r_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                        const double* __restrict__ r, PW4 pw,
+                                                        double* __restrict__ rc, const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int lane = threadIdx.x & 31;
+  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
+  const int I = strip * 30 - 1 + lane;
+  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
+  const int lyc = coarse_rows_per_warp(gc.m);
+  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
+  // interior: every node whose stencil or k the pipeline touches (fine rows 2J0−5 … 2J1+3,
+  // columns xa(lane 0)−1 … xb(lane 31)+1 and their neighbours) is in-grid and non-Dirichlet
+  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 6 >= 1 &&
+                        2 * J1 + 4 <= g.m - 1;
+  if (interior) restrict_r_body<true>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1);
+  else restrict_r_body<false>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1);
+}
+
 // ---- prolongation + post-smoother, level 0: reads the pre-smoothed z written by pcg_update_down ---------
 template <bool INT, bool EN>
 __device__ __forceinline__ double smooth_up_z_body(Geo g, Geo gc, int bc,
@@ -2284,6 +2486,147 @@ __global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc,
     scal[b * S_NSCAL + S_RZ] = t0;
   }
 }
+
+// Level-0 prolongation + post-smoother of the one-reduction PCG: the pre-smoothed red values are
+// recomputed from r (z_red = r/D, the pre-smoother from z = 0; black pre-smoothed values are not
+// needed: the black sweep overwrites them), so nothing of the down sweep is stored. Returns
+// γ = ⟨r, z⟩ and the local part of δ = ⟨z, Az⟩: after the red sweep (Az)_red = r_red and
+// (Az)_black = r_black + Σ_red-nbrs a (z − v), so δ = γ + Σ_red (z_red − v_red)·(r − D z)_red, where
+// v_red is the prolonged value the black sweep used and (r − D z)_red is the red update's
+// neighbour sum.
+template <bool INT>
+__device__ __forceinline__ double2 smooth_up_r_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                    const double* __restrict__ r, double* __restrict__ z_out,
+                                                    const double* __restrict__ zc, PW4 pw, const PairCtx& c) {
+  PAIR_UNPACK
+
+  const double *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
+  const int nc0 = gc.n0;
+  const Pair zero{0.0, 0.0};
+  struct ZRaw {  // prolongation inputs of the red node of a row (loaded one row ahead)
+    double c00, c10, c01, c11, w0, w1, w2, w3;
+  };
+  const int I = xa >> 1;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  auto ZL = [&](int y) {
+    ZRaw v{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if ((unsigned)y >= (unsigned)n0) return v;
+    if (RED_IS_A(y)) {
+      if (INT || (unsigned)xa < (unsigned)n0) v.c00 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
+    } else if (INT || (unsigned)xb < (unsigned)n0) {
+      const int J = y >> 1;
+      const double* c0r = zcb + (int64_t)J * nc0 + I;
+      v.c00 = __ldg(c0r);
+      v.c10 = __ldg(c0r + 1);
+      v.c01 = __ldg(c0r + nc0);
+      v.c11 = __ldg(c0r + nc0 + 1);
+      if (INT || (I < mcl && J < mcl)) {
+        const int64_t cell = cb0 + (int64_t)J * mcl + I;
+        v.w0 = __ldg(pw.w0 + cell);
+        v.w1 = __ldg(pw.w1 + cell);
+        v.w2 = __ldg(pw.w2 + cell);
+        v.w3 = __ldg(pw.w3 + cell);
+      }
+    }
+    return v;
+  };
+  // red value of row y after prolongation, from its raw row data: r, this row's edges E/N and the
+  // previous row's N (z_red = r/D with the stencil arithmetic of the pre-smoother)
+  auto RV = [&](const ZRaw& v, int y, Pair rr, Pair E, Pair N, Pair Nm) {
+    const double Wa = shup(E.b);
+    double zr;
+    if (RED_IS_A(y)) {
+      const Sten s = mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc);
+      zr = rr.a * rcp64(s.d);
+      return zr + v.c00;
+    }
+    const Sten s = mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc);
+    zr = rr.b * rcp64(s.d);
+    return zr + (v.w0 * v.c00 + v.w1 * v.c10 + v.w2 * v.c01 + v.w3 * v.c11);
+  };
+  EdgeRows<INT, false> er(k + off, nullptr, xa, n0, m, y0 - 3);
+  Pair Ed, N3, E2, N2, E1, N1;
+  er.next(Ed, N3);  // row y0−3: N only
+  er.next(E2, N2);  // row y0−2
+  er.next(E1, N1);  // row y0−1
+  const Pair rA = ld2<INT>(rb, xa, y0 - 2, n0);
+  Pair r1 = ld2<INT>(rb, xa, y0 - 1, n0), r2 = ld2<INT>(rb, xa, y0, n0);
+  // scalars: qa/qb = red values of rows t, t+1 (after prolongation); zbm/zb0 = black new of rows t−1, t
+  double qa = RV(ZL(y0 - 2), y0 - 2, rA, E2, N2, N3);
+  double qb = RV(ZL(y0 - 1), y0 - 1, r1, E1, N1, N2);
+  Pair Nt = N2;
+  Pair r0 = zero;
+  double zbm = 0.0, zb0 = 0.0;
+  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
+  ZRaw zq = ZL(y0);
+  double rz = 0.0, dc = 0.0;
+  for (int t = y0 - 2; t < y1; ++t) {
+    const bool ra1 = RED_IS_A(t + 1);  // row t+1: red column a, black b (else the reverse)
+    Pair E2n, N2n;
+    er.next(E2n, N2n);  // row t+2
+    const Pair r3 = ld2<INT>(rb, xa, t + 3, n0);
+    const double qc = RV(zq, t + 2, r2, E2n, N2n, N1);
+    zq = ZL(t + 3);
+    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
+    // black node of row t+1: (r − Σ A z_red_prolonged)/D
+    const double qb_e = shdn(qb), qb_w = shup(qb);
+    const Sten sb = ra1 ? st1.b : st1.a;
+    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
+    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
+    // output row t: red column = (r − Σ A z_black)/D, black column = z_black
+    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
+    const bool ra0 = !ra1;
+    const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
+    const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64(sr0.d);
+    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
+    if (t >= y0) {
+      double* out = z_out + off + (int64_t)t * n0;
+      if (outa) {
+        out[xa] = zv.a;
+        rz = fma(r0.a, zv.a, rz);
+      }
+      if (outb) {
+        out[xb] = zv.b;
+        rz = fma(r0.b, zv.b, rz);
+      }
+      if (ra0 ? outa : outb) dc = fma(zred - qa, s2, dc);
+    }
+    qa = qb; qb = qc; Nt = N1; E1 = E2n; N1 = N2n;
+    r0 = r1; r1 = r2; r2 = r3; zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
+  }
+  return make_double2(rz, dc);
+}
+
+// Level-0 prolongation + post-smoother (reads k, r, zc, pw); epilogue: γ, δ → β, α of the next PCG
+// step (one-reduction PCG).
+#ifndef OSC_SUR_MINB
+#define OSC_SUR_MINB 4
+#endif
+__global__ void __launch_bounds__(MT, OSC_SUR_MINB) smooth_up_r_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                            const double* __restrict__ r,
+                                                            double* __restrict__ z_out,
+                                                            const double* __restrict__ zc, PW4 pw,
+                                                            double* scal, int* flags, double2* partial,
+                                                            int maxp, unsigned* counter) {
+  PAIR_PROLOGUE
+  // the interior body reads k rows up to y1+3 and forms stencils up to row y1+1
+  const bool interior3 = interior && c.y1 <= g.m - 3;
+  const double2 gd = interior3 ? smooth_up_r_body<true>(g, gc, bc, k, r, z_out, zc, pw, c)
+                               : smooth_up_r_body<false>(g, gc, bc, k, r, z_out, zc, pw, c);
+  double gamma, dcorr;
+  if (reduce2_last(gd.x, gd.y, partial, maxp, counter, b, gamma, dcorr) && threadIdx.x == 0) {
+    const double delta = gamma + dcorr;
+    const bool first = flags[b * F_NFLAGS + F_ITERS] == 0;
+    const double beta = first ? 0.0 : gamma / scal[b * S_NSCAL + S_RZ];
+    double den = first ? delta : delta - beta * gamma / scal[b * S_NSCAL + S_ALPHA];
+    if (!(den > 0.0)) den = delta;  // rounding guard (⟨p, Ap⟩ > 0 in exact arithmetic)
+    scal[b * S_NSCAL + S_BETA] = beta;
+    scal[b * S_NSCAL + S_ALPHA] = gamma / den;
+    scal[b * S_NSCAL + S_RZ] = gamma;
+  }
+}
+
 
 // device view of the global hierarchy (one level's operator and centre weights)
 struct SolverLevelDev {
@@ -2968,6 +3311,13 @@ int coarse_mode() {
   return mode;
 }
 
+// Level-0 PCG variant: one-reduction (Chronopoulos–Gear) iteration with the pre-smoother recomputed
+// from r (default), or OSC_LEGACY_PCG=1: ⟨p, Ap⟩ pass + update fused with the stored pre-smoother.
+bool pcg_one_reduction() {
+  static const bool on = std::getenv("OSC_LEGACY_PCG") == nullptr;
+  return on;
+}
+
 // Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). lev[0].z holds the level-0
 // pre-smoothed correction, written by pcg_update_down (z0_fresh).
 void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
@@ -3002,9 +3352,13 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     if (l == 0) {
-      KScope ks(ctx, "mg_restrict.L0");
-      restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, pw_of(L), C.r,
-                                                           w.flags);
+      KScope ks(ctx, pcg_one_reduction() ? "mg_restrict_r.L0" : "mg_restrict.L0");
+      if (pcg_one_reduction())
+        restrict_r_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, pw_of(L),
+                                                               C.r, w.flags);
+      else
+        restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, pw_of(L), C.r,
+                                                             w.flags);
       continue;
     }
     const L9 l9 = l9_of(L);
@@ -3059,10 +3413,15 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     if (l == 0) {
-      KScope ks(ctx, "mg_smooth_up.L0");
-      smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z, L.z2,
-                                                            C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
-                                                            w.counter);
+      KScope ks(ctx, pcg_one_reduction() ? "mg_smooth_up_r.L0" : "mg_smooth_up.L0");
+      if (pcg_one_reduction())
+        smooth_up_r_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2,
+                                                                C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
+                                                                w.counter);
+      else
+        smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z, L.z2,
+                                                              C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
+                                                              w.counter);
       continue;
     }
     const L9 l9 = l9_of(L);
@@ -3241,6 +3600,46 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B) {
     pcg_init_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(
         g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, w.u, w.r_cur,
         w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+  }
+  if (w.nlev > 1 && pcg_one_reduction()) {
+    vcycle(ctx, bc, B, true);  // z = M r0; γ0, δ0 → α0
+    double* p_old = w.p0;
+    double* p_new = w.p1;
+    static const long hard_cap1 = [] {
+      const char* e = std::getenv("OSC_HARD_ITER_CAP");
+      return e ? std::atol(e) : -1L;
+    }();
+    // Lagged convergence polling: the active count after iteration i is copied to a pinned ring
+    // slot behind an event, and the host reads it before launching iteration i + LAG. The device
+    // queue never drains while the host polls; iterations launched after the last sample
+    // converged exit at once (every kernel skips inactive samples).
+    constexpr int LAG = 2;
+    int* ring = ctx->h_pinned_int + 4;
+    for (int it = 0;; ++it) {
+      if (hard_cap1 >= 0 && it >= hard_cap1) {
+        mark_active_failed_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, w.flags);
+        break;
+      }
+      if (it >= LAG) {
+        const int slot = (it - LAG) & 3;
+        OSC_CUDA(cudaEventSynchronize(ctx->ev_poll[slot]));
+        if (ring[slot] <= 0) break;
+      }
+      {
+        KScope ks(ctx, "pcg_update");
+        double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
+        pcg_update_cg_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, L0.z2, p_old, p_new,
+                                                                    w.u, w.r_cur, r_next, w.scal, w.flags, part,
+                                                                    w.max_parts, w.counter, w.n_active, w.hist,
+                                                                    w.hist_cap);
+        w.r_cur = r_next;
+      }
+      OSC_CUDA(cudaMemcpyAsync(ring + (it & 3), w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+      OSC_CUDA(cudaEventRecord(ctx->ev_poll[it & 3], st));
+      vcycle(ctx, bc, B, true);
+      std::swap(p_old, p_new);
+    }
+    return;
   }
   if (w.nlev > 1) {  // first level-0 pre-smoother: pcg_update_down with α = 0 and p = u (finite)
     KScope ks(ctx, "pcg_update_down.init");

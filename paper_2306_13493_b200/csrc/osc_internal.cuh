@@ -120,7 +120,8 @@ struct Ctx {
   // reusable workspaces
   DevBuf ce_inter, xi_dev, fields_fine, fields_coarse, out_q, out_i, tmp_host_stage, sums;
   SolverWork solver;
-  int* h_pinned_int = nullptr;  // small pinned staging for n_active
+  int* h_pinned_int = nullptr;  // small pinned staging for n_active (16 ints; [4..7]: polling ring)
+  cudaEvent_t ev_poll[4] = {nullptr, nullptr, nullptr, nullptr};  // lagged convergence polling
   cudaStream_t copy_stream = nullptr;           // host-ξ H2D overlapped with the previous chunk's solve
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_ce_done[2] = {nullptr, nullptr};

@@ -250,7 +250,7 @@ __device__ __forceinline__ void centre_w_f(RowF row, int bc, int m, int x, int y
   edge_w(row(x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
   edge_w(row(x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
   edge_w(row(x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
-  const double ic = 1.0 / rc.c;
+  const double ic = rcp64(rc.c);
   w[0] = dSW ? 0.0 : -(rc.w * wWs + rc.s * wSw + rc.sw) * ic;
   w[1] = dSE ? 0.0 : -(rc.e * wEs + rc.s * wSe + rc.se) * ic;
   w[2] = dNW ? 0.0 : -(rc.w * wWn + rc.n * wNw + rc.nw) * ic;
@@ -498,10 +498,13 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
     }
     return r;
   };
-  // P rows of the tile's fine region; centres of the tile's own cells also store pw
+  // P rows of the tile's fine region; centres of the tile's own cells also store pw. The region
+  // origin is even, so local parity = node type: one loop per type keeps every warp on one path
+  // of prow_f (centres, H-edges, V-edges, C points).
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  for (int i = tid; i < GP_W * GP_H; i += GT_THREADS) {
-    const int lx = i % GP_W, ly = i / GP_W, x = px + lx, y = py + ly;
+  constexpr int NXo = GP_W / 2, NXe = (GP_W + 1) / 2, NYo = GP_H / 2, NYe = (GP_H + 1) / 2;
+  auto doP = [&](int lx, int ly) {
+    const int x = px + lx, y = py + ly;
     double w[4];
     prow_f(RS, bc, m, x, y, opdep != 0, w);
     P(0, lx, ly) = w[0];
@@ -518,7 +521,11 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
         pw3[cell] = w[3];
       }
     }
-  }
+  };
+  for (int i = tid; i < NXo * NYo; i += GT_THREADS) doP(2 * (i % NXo) + 1, 2 * (i / NXo) + 1);  // centres
+  for (int i = tid; i < NXo * NYe; i += GT_THREADS) doP(2 * (i % NXo) + 1, 2 * (i / NXo));      // H-edges
+  for (int i = tid; i < NXe * NYo; i += GT_THREADS) doP(2 * (i % NXe), 2 * (i / NXe) + 1);      // V-edges
+  for (int i = tid; i < NXe * NYe; i += GT_THREADS) doP(2 * (i % NXe), 2 * (i / NXe));          // C points
   __syncthreads();
   // coarse Galerkin row of (I, J) (rap_kernel's loop over the staged P rows and fine rows)
   const int I = I0 + tid % GT_X, J = J0 + tid / GT_X;
@@ -2238,6 +2245,285 @@ __global__ void __launch_bounds__(MT, 4) c_down_ring_kernel(L9 L, int bc, int op
   cpa_wait<0>();
 }
 
+// ---- level 0 through a cp.async ring ----------------------------------------------------------------
+// The register-marching level-0 sweeps above prefetch one row of loads in registers; at 128
+// registers that leaves too few bytes in flight (long-scoreboard bound at 2.7–3.7 TB/s). These
+// variants stage each warp's rows (64 columns of k and r, plus the prolongation's z₁ and pw for
+// the up sweep) in a shared-memory ring with cp.async, in the warp layout of the coarse kernels,
+// and read k/r pairs back from it as often as needed: only the derived row state stays in
+// registers. Same arithmetic and operand order as restrict_r_body / smooth_up_r_body.
+enum { L0R_K = 0, L0R_R = 64, L0R_ZC0 = 128, L0R_ZC1 = 161, L0R_PW = 194 };
+constexpr int L0R_WORDS_UP = 322, L0R_WORDS_DN = 128;
+constexpr int L0R_RING = 5;
+constexpr size_t L0R_SMEM_UP = sizeof(double) * L0R_RING * MW * L0R_WORDS_UP;  // 51.5 KB
+constexpr size_t L0R_SMEM_DN = sizeof(double) * L0R_RING * MW * L0R_WORDS_DN;  // 20.5 KB
+
+// stage k and r of fine row y (columns x0 … x0+63) into S; off-grid values are zero
+__device__ __forceinline__ void l0_issue_kr(double* S, const double* kb, const double* rb, int x0, int lane, int y,
+                                            int n0) {
+  const bool yok = (unsigned)y < (unsigned)n0;
+  const int c0 = x0 + lane, c1 = c0 + 32;
+  const bool ok0 = yok && (unsigned)c0 < (unsigned)n0, ok1 = yok && (unsigned)c1 < (unsigned)n0;
+  const int64_t i0 = (int64_t)y * n0 + c0;
+  cpa8(S + L0R_K + lane, kb + i0, ok0);
+  cpa8(S + L0R_K + 32 + lane, kb + i0 + 32, ok1);
+  cpa8(S + L0R_R + lane, rb + i0, ok0);
+  cpa8(S + L0R_R + 32 + lane, rb + i0 + 32, ok1);
+}
+__device__ __forceinline__ Pair l0_pair(const double* S, int k, int lane) {
+  const double2 v = *reinterpret_cast<const double2*>(S + k + 2 * lane);
+  return Pair{v.x, v.y};
+}
+
+template <bool INT>
+__device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                   const double* __restrict__ r, PW4 pw, double* __restrict__ rc,
+                                                   int b, int I, bool outI, int J0, int J1, int lane, double* wring) {
+  const int m = g.m, n0 = g.n0, mc = gc.m;
+  const int xa = 2 * I, x0 = xa - 2 * lane;
+  const int64_t off = (int64_t)b * g.N;
+  const double *kb = k + off, *rb = r + off;
+  const int ys = 2 * J0 - 1;
+  const int ylast = 2 * J1 + 2;  // ingest rows end at 2J1+1, whose edges read k of row 2J1+2
+  auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (ys - 3)) % L0R_RING) * (MW * L0R_WORDS_DN); };
+  auto issue = [&](int q) {
+    if (q <= ylast) l0_issue_kr(slot(q), kb, rb, x0, lane, q, n0);
+    cpa_commit();
+  };
+  for (int j = 0; j < L0R_RING; ++j) issue(ys - 3 + j);
+  const Pair zero{0.0, 0.0};
+  Pair N1, E1 = zero, N2 = zero, E2 = zero, N3 = zero;
+  double zr2 = 0.0, zr1 = 0.0, rbl1 = 0.0;
+  Sten sb1{1.0, 0.0, 0.0, 0.0, 0.0};
+  Pair zp3 = zero, zp2 = zero;
+  cpa_wait<2>();  // rows ys−3 … ys−1
+  __syncwarp();
+  {
+    Pair Ed;
+    edges_pair<INT>(zero, l0_pair(slot(ys - 3), L0R_K, lane), l0_pair(slot(ys - 2), L0R_K, lane), xa, ys - 3, m, Ed,
+                    N1);  // row ys−3: its N only
+  }
+  auto ingest = [&](int q) {
+    cpa_wait<2>();  // rows ≤ q+1
+    __syncwarp();
+    Pair E, N;
+    edges_pair<INT>(l0_pair(slot(q - 1), L0R_K, lane), l0_pair(slot(q), L0R_K, lane),
+                    l0_pair(slot(q + 1), L0R_K, lane), xa, q, m, E, N);
+    const Pair r0 = l0_pair(slot(q), L0R_R, lane);
+    __syncwarp();
+    issue(q + 4);  // into the slot of row q−1
+    const Sten2 st = sten_pair<INT>(E, N, N1, xa, q, m, bc);
+    const bool ra = RED_IS_A(q);
+    const double zr0 = (ra ? r0.a : r0.b) * rcp64(ra ? st.a.d : st.b.d);
+    const bool ra1 = !ra;
+    const double zr1_e = shdn(zr1), zr1_w = shup(zr1);
+    const double zbl = (rbl1 - (sb1.e * (ra1 ? zr1_e : zr1) + sb1.w * (ra1 ? zr1 : zr1_w) + sb1.n * zr0 +
+                                sb1.s * zr2)) * rcp64(sb1.d);
+    const Pair zp1 = ra1 ? Pair{zr1, zbl} : Pair{zbl, zr1};
+    const double t = ra ? red_resid<INT, true>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc)
+                        : red_resid<INT, false>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc);
+    N3 = N2; E2 = E1; N2 = N1; E1 = E; N1 = N;
+    zr2 = zr1; zr1 = zr0;
+    sb1 = ra ? st.b : st.a;
+    rbl1 = ra ? r0.b : r0.a;
+    zp3 = zp2; zp2 = zp1;
+    return t;
+  };
+  ingest(ys - 2);
+  ingest(ys - 1);
+  ingest(ys);
+  ingest(ys + 1);
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  auto W4 = [&](int Jc, double w[4]) {
+    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
+    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+  };
+  double wc[4], wn[4];
+  W4(J0 - 1, wc);
+  W4(J0, wn);
+  const double t_first = ingest(ys + 2);  // (xb, 2J0−1)
+  double a_nw = t_first * wc[2], a_ne = t_first * wc[3];
+  double* rcb = rc + (int64_t)b * gc.N;
+  for (int J = J0; J < J1; ++J) {
+    wc[0] = wn[0]; wc[1] = wn[1]; wc[2] = wn[2]; wc[3] = wn[3];
+    W4(J + 1, wn);
+    const double t_even = ingest(2 * J + 2);  // (xa, 2J)
+    const double t = ingest(2 * J + 3);       // (xb, 2J+1)
+    const double a_sw = t * wc[0], a_se = t * wc[1];
+    const double v = t_even + a_sw + shup(a_se) + a_nw + shup(a_ne);
+    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
+    a_nw = t * wc[2];
+    a_ne = t * wc[3];
+  }
+  cpa_wait<0>();
+}
+
+__global__ void __launch_bounds__(MT, 4) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                              const double* __restrict__ r, PW4 pw,
+                                                              double* __restrict__ rc, const int* flags) {
+  const int b = blockIdx.z;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  extern __shared__ __align__(16) double l0ring[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = blockIdx.x * MW + warp;
+  const int I = strip * 30 - 1 + lane;
+  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
+  const int lyc = coarse_rows_per_warp(gc.m);
+  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
+  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 6 >= 1 &&
+                        2 * J1 + 4 <= g.m - 1;
+  double* wring = l0ring + warp * L0R_WORDS_DN;
+  if (interior) restrict_ring_body<true>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1, lane, wring);
+  else restrict_ring_body<false>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1, lane, wring);
+}
+
+template <bool INT>
+__device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                       const double* __restrict__ r, double* __restrict__ z_out,
+                                                       const double* __restrict__ zc, PW4 pw, const PairCtx& c,
+                                                       double* wring) {
+  PAIR_UNPACK
+
+  const int lane = c.lane, x0 = xa - 2 * lane;
+  const double *kb = k + off, *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
+  const int nc0 = gc.n0;
+  const int I0 = x0 >> 1;
+  const int mcl = m / 2;
+  const int64_t cb0 = (int64_t)b * mcl * mcl;
+  const int ylast = y1 + 2;
+  auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (y0 - 3)) % L0R_RING) * (MW * L0R_WORDS_UP); };
+  auto issue = [&](int q) {
+    if (q <= ylast) {
+      double* S = slot(q);
+      l0_issue_kr(S, kb, rb, x0, lane, q, n0);
+      // prolongation inputs of row q's red node: z₁ rows q>>1 (and +1 on odd rows), columns
+      // I0 … I0+32; centre weights of the odd rows' cells
+      const int Jc = q >> 1, ci = I0 + lane;
+      const bool cok = (unsigned)ci < (unsigned)nc0, cok2 = (unsigned)(ci + 32) < (unsigned)nc0;
+      const bool j0 = (unsigned)Jc < (unsigned)nc0, j1 = (unsigned)(Jc + 1) < (unsigned)nc0;
+      const double* zr0 = zcb + (int64_t)Jc * nc0 + ci;
+      cpa8(S + L0R_ZC0 + lane, zr0, j0 && cok);
+      if (lane == 0) cpa8(S + L0R_ZC0 + 32, zr0 + 32, j0 && cok2);
+      if (q & 1) {
+        cpa8(S + L0R_ZC1 + lane, zr0 + nc0, j1 && cok);
+        if (lane == 0) cpa8(S + L0R_ZC1 + 32, zr0 + nc0 + 32, j1 && cok2);
+        const bool ok = ci >= 0 && ci < mcl && Jc >= 0 && Jc < mcl;
+        const int64_t cell = cb0 + (int64_t)Jc * mcl + ci;
+        cpa8(S + L0R_PW + 0 * 32 + lane, pw.w0 + cell, ok);
+        cpa8(S + L0R_PW + 1 * 32 + lane, pw.w1 + cell, ok);
+        cpa8(S + L0R_PW + 2 * 32 + lane, pw.w2 + cell, ok);
+        cpa8(S + L0R_PW + 3 * 32 + lane, pw.w3 + cell, ok);
+      }
+    }
+    cpa_commit();
+  };
+  // red value of row y after prolongation: z_red = r/D (pre-smoother from 0) + P z₁
+  auto RV = [&](const double* S, int y, Pair rr, Pair E, Pair N, Pair Nm) {
+    const double Wa = shup(E.b);
+    if (RED_IS_A(y)) {
+      const Sten s = mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc);
+      const double c00 = (INT || (unsigned)xa < (unsigned)n0) ? S[L0R_ZC0 + lane] : 0.0;
+      return rr.a * rcp64(s.d) + c00;
+    }
+    const Sten s = mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc);
+    double p = 0.0;
+    if (INT || (unsigned)xb < (unsigned)n0)
+      p = S[L0R_PW + lane] * S[L0R_ZC0 + lane] + S[L0R_PW + 32 + lane] * S[L0R_ZC0 + lane + 1] +
+          S[L0R_PW + 64 + lane] * S[L0R_ZC1 + lane] + S[L0R_PW + 96 + lane] * S[L0R_ZC1 + lane + 1];
+    return rr.b * rcp64(s.d) + p;
+  };
+  for (int j = 0; j < L0R_RING; ++j) issue(y0 - 3 + j);  // rows y0−3 … y0+1
+  const Pair zero{0.0, 0.0};
+  cpa_wait<1>();  // rows y0−3 … y0
+  __syncwarp();
+  Pair Ed, N3, E2, N2, E1, N1;
+  {
+    const Pair km = l0_pair(slot(y0 - 3), L0R_K, lane), k0 = l0_pair(slot(y0 - 2), L0R_K, lane),
+               k1 = l0_pair(slot(y0 - 1), L0R_K, lane), k2 = l0_pair(slot(y0), L0R_K, lane);
+    edges_pair<INT>(zero, km, k0, xa, y0 - 3, m, Ed, N3);
+    edges_pair<INT>(km, k0, k1, xa, y0 - 2, m, E2, N2);
+    edges_pair<INT>(k0, k1, k2, xa, y0 - 1, m, E1, N1);
+  }
+  double qa = RV(slot(y0 - 2), y0 - 2, l0_pair(slot(y0 - 2), L0R_R, lane), E2, N2, N3);
+  double qb = RV(slot(y0 - 1), y0 - 1, l0_pair(slot(y0 - 1), L0R_R, lane), E1, N1, N2);
+  __syncwarp();
+  issue(y0 + 2);  // into the slot of row y0−3 (rows y0−2 … are still read by the loop)
+  Pair Nt = N2;
+  double zbm = 0.0, zb0 = 0.0;
+  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
+  double rz = 0.0, dc = 0.0;
+  for (int t = y0 - 2; t < y1; ++t) {
+    // rows t … t+3 resident (row t+4 may be in flight)
+    cpa_wait<1>();
+    __syncwarp();
+    const double *S0 = slot(t), *S1 = slot(t + 1), *S2 = slot(t + 2), *S3 = slot(t + 3);
+    const bool ra1 = RED_IS_A(t + 1);
+    Pair E2n, N2n;
+    edges_pair<INT>(l0_pair(S1, L0R_K, lane), l0_pair(S2, L0R_K, lane), l0_pair(S3, L0R_K, lane), xa, t + 2, m,
+                    E2n, N2n);
+    const Pair r0 = l0_pair(S0, L0R_R, lane), r1 = l0_pair(S1, L0R_R, lane);
+    const double qc = RV(S2, t + 2, l0_pair(S2, L0R_R, lane), E2n, N2n, N1);
+    __syncwarp();
+    issue(t + 5);  // into the slot of row t
+    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
+    const double qb_e = shdn(qb), qb_w = shup(qb);
+    const Sten sb = ra1 ? st1.b : st1.a;
+    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
+    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
+    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
+    const bool ra0 = !ra1;
+    const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
+    const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64(sr0.d);
+    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
+    if (t >= y0) {
+      double* out = z_out + off + (int64_t)t * n0;
+      if (outa) {
+        out[xa] = zv.a;
+        rz = fma(r0.a, zv.a, rz);
+      }
+      if (outb) {
+        out[xb] = zv.b;
+        rz = fma(r0.b, zv.b, rz);
+      }
+      if (ra0 ? outa : outb) dc = fma(zred - qa, s2, dc);
+    }
+    qa = qb; qb = qc; Nt = N1; E1 = E2n; N1 = N2n;
+    zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
+  }
+  cpa_wait<0>();
+  return make_double2(rz, dc);
+}
+
+__global__ void __launch_bounds__(MT, 4) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+                                                               const double* __restrict__ r,
+                                                               double* __restrict__ z_out,
+                                                               const double* __restrict__ zc, PW4 pw, double* scal,
+                                                               int* flags, double2* partial, int maxp,
+                                                               unsigned* counter) {
+  PAIR_PROLOGUE
+  extern __shared__ __align__(16) double l0ring[];
+  double* wring = l0ring + (threadIdx.x >> 5) * L0R_WORDS_UP;
+  const bool interior3 = interior && c.y1 <= g.m - 3;
+  const double2 gd = interior3 ? smooth_up_ring_body<true>(g, gc, bc, k, r, z_out, zc, pw, c, wring)
+                               : smooth_up_ring_body<false>(g, gc, bc, k, r, z_out, zc, pw, c, wring);
+  double gamma, dcorr;
+  if (reduce2_last(gd.x, gd.y, partial, maxp, counter, b, gamma, dcorr) && threadIdx.x == 0) {
+    const double delta = gamma + dcorr;
+    const bool first = flags[b * F_NFLAGS + F_ITERS] == 0;
+    const double beta = first ? 0.0 : gamma / scal[b * S_NSCAL + S_RZ];
+    double den = first ? delta : delta - beta * gamma / scal[b * S_NSCAL + S_ALPHA];
+    if (!(den > 0.0)) den = delta;
+    scal[b * S_NSCAL + S_BETA] = beta;
+    scal[b * S_NSCAL + S_ALPHA] = gamma / den;
+    scal[b * S_NSCAL + S_RZ] = gamma;
+  }
+}
+
 // Level-0 restriction kernel (reads k, z and the level-0 centre weights).
 __global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                       const double* __restrict__ z, PW4 pw,
@@ -3318,6 +3604,21 @@ bool pcg_one_reduction() {
   return on;
 }
 
+// Level-0 restriction / up sweep through the cp.async ring (default) or register-prefetched
+// (OSC_L0_RING=0).
+bool l0_ring() {
+  static const bool on = [] {
+    const char* e = std::getenv("OSC_L0_RING");
+    const bool v = !(e && e[0] == '0');
+    if (v) {
+      cudaFuncSetAttribute(smooth_up_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L0R_SMEM_UP);
+      cudaFuncSetAttribute(restrict_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L0R_SMEM_DN);
+    }
+    return v;
+  }();
+  return on;
+}
+
 // Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). lev[0].z holds the level-0
 // pre-smoothed correction, written by pcg_update_down (z0_fresh).
 void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
@@ -3353,7 +3654,10 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     const SolverLevel& C = w.lev[l + 1];
     if (l == 0) {
       KScope ks(ctx, pcg_one_reduction() ? "mg_restrict_r.L0" : "mg_restrict.L0");
-      if (pcg_one_reduction())
+      if (pcg_one_reduction() && l0_ring())
+        restrict_ring_kernel<<<restrict_grid(C.m, B), MT, L0R_SMEM_DN, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur,
+                                                                           pw_of(L), C.r, w.flags);
+      else if (pcg_one_reduction())
         restrict_r_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, pw_of(L),
                                                                C.r, w.flags);
       else
@@ -3414,7 +3718,11 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     const SolverLevel& C = w.lev[l + 1];
     if (l == 0) {
       KScope ks(ctx, pcg_one_reduction() ? "mg_smooth_up_r.L0" : "mg_smooth_up.L0");
-      if (pcg_one_reduction())
+      if (pcg_one_reduction() && l0_ring())
+        smooth_up_ring_kernel<<<march_grid(L.m, 2, B), MT, L0R_SMEM_UP, st>>>(
+            geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2, C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
+            w.counter);
+      else if (pcg_one_reduction())
         smooth_up_r_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2,
                                                                 C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
                                                                 w.counter);

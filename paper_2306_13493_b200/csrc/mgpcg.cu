@@ -2457,49 +2457,74 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
   double zbm = 0.0, zb0 = 0.0;
   Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
   double rz = 0.0, dc = 0.0;
-  for (int t = y0 - 2; t < y1; ++t) {
+  // one output row; RA1 = red at column a in row t+1 (static: the loop is unrolled by 2, y0 even)
+  auto step = [&](auto RA1, int t) {
+    constexpr bool ra1 = decltype(RA1)::value, ra0 = !ra1;
     // rows t … t+3 resident (row t+4 may be in flight)
     cpa_wait<1>();
     __syncwarp();
     const double *S0 = slot(t), *S1 = slot(t + 1), *S2 = slot(t + 2), *S3 = slot(t + 3);
-    const bool ra1 = RED_IS_A(t + 1);
     Pair E2n, N2n;
     edges_pair<INT>(l0_pair(S1, L0R_K, lane), l0_pair(S2, L0R_K, lane), l0_pair(S3, L0R_K, lane), xa, t + 2, m,
                     E2n, N2n);
     const Pair r0 = l0_pair(S0, L0R_R, lane), r1 = l0_pair(S1, L0R_R, lane);
-    const double qc = RV(S2, t + 2, l0_pair(S2, L0R_R, lane), E2n, N2n, N1);
+    // red value of row t+2 (red column a iff row t+2 is even, i.e. as row t)
+    double qc;
+    {
+      const Pair rr = l0_pair(S2, L0R_R, lane);
+      const double Wa = shup(E2n.b);
+      if constexpr (ra0) {
+        const Sten sq = mk_sten<INT>(E2n.a, Wa, N2n.a, N1.a, xa, t + 2, m, bc);
+        const double c00 = (INT || (unsigned)xa < (unsigned)n0) ? S2[L0R_ZC0 + lane] : 0.0;
+        qc = rr.a * rcp64(sq.d) + c00;
+      } else {
+        const Sten sq = mk_sten<INT>(E2n.b, E2n.a, N2n.b, N1.b, xb, t + 2, m, bc);
+        double pz = 0.0;
+        if (INT || (unsigned)xb < (unsigned)n0)
+          pz = S2[L0R_PW + lane] * S2[L0R_ZC0 + lane] + S2[L0R_PW + 32 + lane] * S2[L0R_ZC0 + lane + 1] +
+               S2[L0R_PW + 64 + lane] * S2[L0R_ZC1 + lane] + S2[L0R_PW + 96 + lane] * S2[L0R_ZC1 + lane + 1];
+        qc = rr.b * rcp64(sq.d) + pz;
+      }
+    }
     __syncwarp();
     issue(t + 5);  // into the slot of row t
     const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
     const double qb_e = shdn(qb), qb_w = shup(qb);
-    const Sten sb = ra1 ? st1.b : st1.a;
+    const Sten& sb = ra1 ? st1.b : st1.a;
     const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
     const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
     const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
-    const bool ra0 = !ra1;
     const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
     const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64(sr0.d);
-    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
     if (t >= y0) {
       double* out = z_out + off + (int64_t)t * n0;
+      const double va = ra0 ? zred : zb0, vb = ra0 ? zb0 : zred;
       if (outa) {
-        out[xa] = zv.a;
-        rz = fma(r0.a, zv.a, rz);
+        out[xa] = va;
+        rz = fma(r0.a, va, rz);
       }
       if (outb) {
-        out[xb] = zv.b;
-        rz = fma(r0.b, zv.b, rz);
+        out[xb] = vb;
+        rz = fma(r0.b, vb, rz);
       }
       if (ra0 ? outa : outb) dc = fma(zred - qa, s2, dc);
     }
     qa = qb; qb = qc; Nt = N1; E1 = E2n; N1 = N2n;
-    zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
+    zbm = zb0; zb0 = zbp1;
+    sr0 = ra1 ? st1.a : st1.b;
+  };
+  for (int t = y0 - 2; t < y1; t += 2) {
+    step(std::false_type{}, t);
+    if (t + 1 < y1) step(std::true_type{}, t + 1);
   }
   cpa_wait<0>();
   return make_double2(rz, dc);
 }
 
-__global__ void __launch_bounds__(MT, 4) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+#ifndef OSC_SURR_MINB
+#define OSC_SURR_MINB 3
+#endif
+__global__ void __launch_bounds__(MT, OSC_SURR_MINB) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                                const double* __restrict__ r,
                                                                double* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,

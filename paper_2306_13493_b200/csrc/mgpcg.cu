@@ -231,12 +231,13 @@ __device__ __forceinline__ void edge_w(const S9& r, bool horiz, bool opdep, bool
 }
 
 // Centre (odd x, odd y) weights to SW, SE, NW, NE; `row(x, y)` gives the level's S9 row of a node.
-template <class RowF>
+// INT: the node, its neighbours and their coarse parents are interior (no Dirichlet / off-grid tests).
+template <bool INT = false, class RowF>
 __device__ __forceinline__ void centre_w_f(RowF row, int bc, int m, int x, int y, bool opdep, double w[4]) {
   const int mc = m / 2;
   const int I = (x - 1) >> 1, J = (y - 1) >> 1;
-  const bool dSW = is_dir(bc, mc, I, J), dSE = is_dir(bc, mc, I + 1, J), dNW = is_dir(bc, mc, I, J + 1),
-             dNE = is_dir(bc, mc, I + 1, J + 1);
+  const bool dSW = !INT && is_dir(bc, mc, I, J), dSE = !INT && is_dir(bc, mc, I + 1, J),
+             dNW = !INT && is_dir(bc, mc, I, J + 1), dNE = !INT && is_dir(bc, mc, I + 1, J + 1);
   if (!opdep) {
     w[0] = dSW ? 0.0 : 0.5;
     w[1] = 0.0;
@@ -246,10 +247,10 @@ __device__ __forceinline__ void centre_w_f(RowF row, int bc, int m, int x, int y
   }
   const S9 rc = row(x, y);
   double wWs, wWn, wEs, wEn, wSw, wSe, wNw, wNe;  // V-edges W, E: (S, N); H-edges S, N: (W, E)
-  edge_w(row(x - 1, y), false, true, dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
-  edge_w(row(x + 1, y), false, true, dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
-  edge_w(row(x, y - 1), true, true, dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
-  edge_w(row(x, y + 1), true, true, dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
+  edge_w(row(x - 1, y), false, true, !INT && dir_or_out(bc, m, x - 1, y), dSW, dNW, wWs, wWn);
+  edge_w(row(x + 1, y), false, true, !INT && dir_or_out(bc, m, x + 1, y), dSE, dNE, wEs, wEn);
+  edge_w(row(x, y - 1), true, true, !INT && dir_or_out(bc, m, x, y - 1), dSW, dSE, wSw, wSe);
+  edge_w(row(x, y + 1), true, true, !INT && dir_or_out(bc, m, x, y + 1), dNW, dNE, wNw, wNe);
   const double ic = rcp64(rc.c);
   w[0] = dSW ? 0.0 : -(rc.w * wWs + rc.s * wSw + rc.sw) * ic;
   w[1] = dSE ? 0.0 : -(rc.e * wEs + rc.s * wSe + rc.se) * ic;
@@ -263,22 +264,22 @@ __device__ void centre_w(const L9& R, int bc, int b, int x, int y, bool opdep, d
 }
 
 // P row of node (x, y) (weights to its coarse parents, meaning by parity; see prow_kernel)
-template <class RowF>
+template <bool INT = false, class RowF>
 __device__ __forceinline__ void prow_f(RowF row, int bc, int m, int x, int y, bool opdep, double w[4]) {
   const int mc = m / 2;
   w[0] = w[1] = w[2] = w[3] = 0.0;
-  if (x < 0 || x > m || y < 0 || y > m) return;
-  const bool fdir = is_dir(bc, m, x, y);
+  if (!INT && (x < 0 || x > m || y < 0 || y > m)) return;
+  const bool fdir = !INT && is_dir(bc, m, x, y);
   if ((x & 1) == 0 && (y & 1) == 0) {
     w[0] = fdir ? 0.0 : 1.0;
   } else if ((x & 1) && (y & 1)) {
-    centre_w_f(row, bc, m, x, y, opdep, w);
+    centre_w_f<INT>(row, bc, m, x, y, opdep, w);
   } else {
     const bool horiz = (x & 1) != 0;
     const int I0 = horiz ? (x - 1) >> 1 : x >> 1, J0 = horiz ? y >> 1 : (y - 1) >> 1;
     const int I1 = horiz ? I0 + 1 : I0, J1 = horiz ? J0 : J0 + 1;
     const S9 r = opdep ? row(x, y) : S9{};
-    edge_w(r, horiz, opdep, fdir, is_dir(bc, mc, I0, J0), is_dir(bc, mc, I1, J1), w[0], w[1]);
+    edge_w(r, horiz, opdep, fdir, !INT && is_dir(bc, mc, I0, J0), !INT && is_dir(bc, mc, I1, J1), w[0], w[1]);
   }
 }
 
@@ -411,15 +412,15 @@ constexpr size_t galerkin_tile_smem(bool l0) {
   return sizeof(double) * ((l0 ? 3 : 5) * GA_W * GA_H + 4 * GP_W * GP_H + (l0 ? GK_W * GK_H : 0));
 }
 
-template <bool L0K>
-__global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double* __restrict__ k0, L9 F, int bc,
-                                                                   int opdep, Geo gc, double* __restrict__ Cc,
-                                                                   double* __restrict__ Ec, double* __restrict__ Nc,
-                                                                   double* __restrict__ NEc,
-                                                                   double* __restrict__ NWc, double* __restrict__ pw0,
-                                                                   double* __restrict__ pw1, double* __restrict__ pw2,
-                                                                   double* __restrict__ pw3) {
-  extern __shared__ double gsm[];
+// INT: every node the tile touches (k region included) is in-grid and non-Dirichlet, and so are
+// the coarse nodes of the tile: no bounds / Dirichlet tests (most tiles of a large level).
+template <bool L0K, bool INT>
+__device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0, const L9& F, int bc, int opdep,
+                                                   const Geo& gc, double* __restrict__ Cc, double* __restrict__ Ec,
+                                                   double* __restrict__ Nc, double* __restrict__ NEc,
+                                                   double* __restrict__ NWc, double* __restrict__ pw0,
+                                                   double* __restrict__ pw1, double* __restrict__ pw2,
+                                                   double* __restrict__ pw3, double* gsm) {
   const int b = blockIdx.z;
   const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y;
   const int m = F.m, n0 = F.n0, mc = gc.m, mcl = m / 2;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
     for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
       const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
       double c = 1.0, e = 0.0, nn = 0.0;
-      if (!(x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y))) {
+      if (INT || !(x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y))) {
         auto Ed = [&](int a, int b2) -> double {
           if (a < 0 || a >= m) return 0.0;
           return -0.5 * ((b2 < m ? (K(a, b2) + K(a + 1, b2) + K(a + 1, b2 + 1)) * third : 0.0) +
@@ -458,8 +459,8 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
         };
         const double E = Ed(x, y), W = Ed(x - 1, y), Nn = Nd(x, y), S = Nd(x, y - 1);
         c = -(E + W + Nn + S);
-        e = is_dir(bc, m, x + 1, y) ? 0.0 : E;
-        nn = is_dir(bc, m, x, y + 1) ? 0.0 : Nn;
+        e = (!INT && is_dir(bc, m, x + 1, y)) ? 0.0 : E;
+        nn = (!INT && is_dir(bc, m, x, y + 1)) ? 0.0 : Nn;
       }
       A(0, lx, ly) = c;
       A(1, lx, ly) = e;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
     const double* src[5] = {F.C + off, F.E + off, F.N + off, F.NE + off, F.NW + off};
     for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
       const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
-      const bool in = (unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0;
+      const bool in = INT || ((unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0);
       const int64_t o = (int64_t)y * n0 + x;
 #pragma unroll
       for (int q = 0; q < 5; ++q) A(q, lx, ly) = in ? __ldg(src[q] + o) : (q == 0 ? 1.0 : 0.0);
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
   // S9 row of fine node (x, y) from the staged rows (row_s semantics)
   auto RS = [&](int x, int y) -> S9 {
     S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
-    if (x < 0 || x > m || y < 0 || y > m) {
+    if (!INT && (x < 0 || x > m || y < 0 || y > m)) {
       r.c = 1.0;
       return r;
     }
@@ -488,13 +489,13 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
     r.c = A(0, lx, ly);
     r.e = A(1, lx, ly);
     r.n = A(2, lx, ly);
-    if (x > 0) r.w = A(1, lx - 1, ly);
-    if (y > 0) r.s = A(2, lx, ly - 1);
+    if (INT || x > 0) r.w = A(1, lx - 1, ly);
+    if (INT || y > 0) r.s = A(2, lx, ly - 1);
     if constexpr (!L0K) {
       r.ne = A(3, lx, ly);
       r.nw = A(4, lx, ly);
-      if (x > 0 && y > 0) r.sw = A(3, lx - 1, ly - 1);
-      if (x < m && y > 0) r.se = A(4, lx + 1, ly - 1);
+      if (INT || (x > 0 && y > 0)) r.sw = A(3, lx - 1, ly - 1);
+      if (INT || (x < m && y > 0)) r.se = A(4, lx + 1, ly - 1);
     }
     return r;
   };
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
   auto doP = [&](int lx, int ly) {
     const int x = px + lx, y = py + ly;
     double w[4];
-    prow_f(RS, bc, m, x, y, opdep != 0, w);
+    prow_f<INT>(RS, bc, m, x, y, opdep != 0, w);
     P(0, lx, ly) = w[0];
     P(1, lx, ly) = w[1];
     P(2, lx, ly) = w[2];
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
   const int I = I0 + tid % GT_X, J = J0 + tid / GT_X;
   if (I > mc || J > mc) return;
   const int64_t o = (int64_t)b * gc.N + (int64_t)J * gc.n0 + I;
-  if (is_dir(bc, mc, I, J)) {
+  if (!INT && is_dir(bc, mc, I, J)) {
     Cc[o] = 1.0;
     Ec[o] = Nc[o] = NEc[o] = NWc[o] = 0.0;
     return;
@@ -542,14 +543,14 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
 #pragma unroll
     for (int di = -1; di <= 1; ++di) {
       const int xi = 2 * I + di, yi = 2 * J + dj;
-      if (xi < 0 || xi > m || yi < 0 || yi > m) continue;
+      if (!INT && (xi < 0 || xi > m || yi < 0 || yi > m)) continue;
       const int lxi = xi - px, lyi = yi - py;
       double pic;
       if (di == 0 && dj == 0) pic = P(0, lxi, lyi);
       else if (dj == 0) pic = di > 0 ? P(0, lxi, lyi) : P(1, lxi, lyi);
       else if (di == 0) pic = dj > 0 ? P(0, lxi, lyi) : P(1, lxi, lyi);
       else pic = dj > 0 ? (di > 0 ? P(0, lxi, lyi) : P(1, lxi, lyi)) : (di > 0 ? P(2, lxi, lyi) : P(3, lxi, lyi));
-      if (pic == 0.0) continue;
+      if (!INT && pic == 0.0) continue;
       const S9 r = RS(xi, yi);
 #pragma unroll
       for (int ey = -1; ey <= 1; ++ey)
@@ -559,7 +560,7 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
                                   : ey == 0 ? (ex < 0 ? r.w : ex == 0 ? r.c : r.e)
                                             : (ex < 0 ? r.nw : ex == 0 ? r.n : r.ne);
           const int xj = xi + ex, yj = yi + ey;
-          if (a == 0.0 || xj < 0 || xj > m || yj < 0 || yj > m) continue;
+          if (!INT && (a == 0.0 || xj < 0 || xj > m || yj < 0 || yj > m)) continue;
           const int lxj = xj - px, lyj = yj - py;
           const double pa = pic * a;
           const int dx = di + ex, dy = dj + ey;
@@ -586,6 +587,24 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
   Nc[o] = acc[2][1];
   NEc[o] = acc[2][2];
   NWc[o] = acc[2][0];
+}
+
+template <bool L0K>
+__global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double* __restrict__ k0, L9 F, int bc,
+                                                                   int opdep, Geo gc, double* __restrict__ Cc,
+                                                                   double* __restrict__ Ec, double* __restrict__ Nc,
+                                                                   double* __restrict__ NEc,
+                                                                   double* __restrict__ NWc, double* __restrict__ pw0,
+                                                                   double* __restrict__ pw1, double* __restrict__ pw2,
+                                                                   double* __restrict__ pw3) {
+  extern __shared__ double gsm[];
+  const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y, m = F.m;
+  const bool interior = 2 * I0 - 5 >= 1 && 2 * I0 + 2 * GT_X + 3 <= m - 1 && 2 * J0 - 5 >= 1 &&
+                        2 * J0 + 2 * GT_Y + 3 <= m - 1;
+  if (interior)
+    galerkin_tile_body<L0K, true>(k0, F, bc, opdep, gc, Cc, Ec, Nc, NEc, NWc, pw0, pw1, pw2, pw3, gsm);
+  else
+    galerkin_tile_body<L0K, false>(k0, F, bc, opdep, gc, Cc, Ec, Nc, NEc, NWc, pw0, pw1, pw2, pw3, gsm);
 }
 
 // Reference rediscretisation (fem.cpp:241-244): the level-l row from the injected nodal k,

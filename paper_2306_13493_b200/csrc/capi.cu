@@ -354,9 +354,11 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     int64_t Bmax = std::max<int64_t>(1, (int64_t)(budget / per));
     Bmax = std::min<int64_t>(Bmax, 1 << 16);
     int64_t nchunks = (count + Bmax - 1) / Bmax;
-    // host ξ: at least two chunks, so chunk i+1's H2D copy (copy stream, double-buffered) runs
-    // under chunk i's solve; device ξ / Philox: one chunk when it fits
-    if (xi_host && count >= 2) nchunks = std::max<int64_t>(nchunks, 2);
+    // host ξ: several chunks, so chunk i+1's H2D copy (copy stream, double-buffered) runs under
+    // chunk i's solve and only the first chunk's copy is exposed (up to 4 chunks of ≥ 8 samples);
+    // device ξ / Philox: one chunk when it fits
+    if (xi_host && count >= 2)
+      nchunks = std::max<int64_t>(nchunks, std::min<int64_t>(4, std::max<int64_t>(2, count / 8)));
     const int Bc = (int)((count + nchunks - 1) / nchunks);
     c->fields_fine.ensure(sizeof(double) * Nf * Bc);
     if (has_coarse) c->fields_coarse.ensure(sizeof(double) * Nc * Bc);

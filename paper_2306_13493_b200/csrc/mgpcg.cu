@@ -948,7 +948,14 @@ constexpr int MT = 32 * MW;  // threads per CTA
 constexpr int LY = 32;       // output rows per warp on large grids
 // rows marched per warp: long chunks amortise the 2-row warm-up on large grids; short chunks
 // cut the serial row-latency chain (and add CTAs) on the small, latency-bound MG levels.
-__host__ __device__ __forceinline__ int rows_per_warp(int m) { return m >= 512 ? LY : (m >= 64 ? 16 : 8); }
+#ifndef OSC_RPW
+#define OSC_RPW 0
+#endif
+__host__ __device__ __forceinline__ int rows_per_warp(int m) {
+  if (OSC_RPW == 1) return m >= 512 ? LY : (m >= 256 ? 16 : (m >= 64 ? 8 : 4));
+  if (OSC_RPW == 2) return m >= 512 ? LY : (m >= 128 ? 16 : (m >= 64 ? 8 : 4));
+  return m >= 512 ? LY : (m >= 64 ? 16 : 8);
+}
 constexpr int LYC = 16;      // coarse output rows per warp (restriction) on large grids
 __host__ __device__ __forceinline__ int coarse_rows_per_warp(int mc) { return mc >= 256 ? LYC : 4; }
 constexpr unsigned FULL = 0xffffffffu;

@@ -161,7 +161,10 @@ def test_galerkin_fewer_iterations(P, ctx, port, m):
 @pytest.mark.parametrize("bc", [0, 1])
 def test_fused_setup_matches_unfused(P, ctx, m, bc, monkeypatch):
     """The tiled Galerkin setup (galerkin_tile_kernel) builds the same hierarchy as the unfused
-    rows0 → prow → rap sequence (same arithmetic): identical iteration counts and solutions."""
+    rows0 → prow → rap sequence: identical iteration counts, and solutions equal to rounding
+    (the interior-tile fast path adds the exact-zero products the boundary path skips, so the
+    compiler's FMA grouping may differ in the last bits; 1e-11 is far below the 1e-10 solve
+    tolerance)."""
     api = P.api
     model = api.CovarianceModel.matern(2.0, 3.0 / m, 0.5)
     op = api.build_operator(api.GridSpec.square(m), model)
@@ -173,7 +176,7 @@ def test_fused_setup_matches_unfused(P, ctx, m, bc, monkeypatch):
         u2, it2, _ = api.assemble_and_solve(m, Z, prob, api.SolverOptions(coarse_operator=mode), ctx=ctx)
         monkeypatch.delenv("OSC_UNFUSED_SETUP")
         assert np.array_equal(it1, it2), (mode, it1, it2)
-        assert relmax(u1, u2) < 1e-13, (mode, relmax(u1, u2))
+        assert relmax(u1, u2) < 1e-11, (mode, relmax(u1, u2))
 
 
 def test_solve_analytic(P, ctx):
@@ -332,6 +335,42 @@ print("ok")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
 
+
+
+@pytest.mark.parametrize("env", ["OSC_LEGACY_PCG=1", "OSC_L0_RING=0", "OSC_COARSE_MODE=0", "OSC_COARSE_MODE=1",
+                                 "OSC_UNFUSED_SETUP=1"])
+def test_solver_variants_vs_oracle(P, ctx, env):
+    """The A/B code paths kept beside the defaults (two-reduction PCG with a stored pre-smoother,
+    register-prefetched level-0 sweeps, register-marching / partly ring-staged coarse kernels, the
+    unfused setup) solve the same systems: QoIs match the oracle port to 1e-7 (in a subprocess,
+    since the switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2306_13493_b200 as P
+from oracle import oracle as O
+api = P.api
+port = O.Port()
+for m, bc in [(128, 1), (256, 0), (512, 1)]:
+    model = api.CovarianceModel.matern(2.0, 3.0 / m, 0.5)
+    op = api.build_operator(api.GridSpec.square(m), model)
+    Z = op.sample_fields(None, count=2, seed=11, ell=0, index0=0, fine=True)
+    prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.L2Norm), bc=api.BC(bc))
+    u, it, _ = api.assemble_and_solve(m, Z, prob)
+    q = api.evaluate_qoi(m, u, prob, Z=Z)
+    for b in range(2):
+        uo, ito, rc, _ = port.solve(m, Z[b], bc=bc)
+        qo = port.qoi(m, uo, bc=bc, qoi=1, Z=Z[b])
+        assert rc == 0 and abs(q[b] - qo) <= 1e-7 * abs(qo), (m, bc, b, q[b], qo)
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    k, v = env.split("=")
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{k: v}), capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
 
 
 def test_smoothing_error_estimate_vs_reference(P, ctx, ref):

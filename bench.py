@@ -330,6 +330,11 @@ def main():
     sums = np.zeros(8)
     iters_total = [0, 0]
 
+    shard = None
+    if dist:
+        from paper_2306_13493_b200.dist import Shard
+        shard = Shard()
+
     def step(k, xi=None):
         frm = (k * world + rank) * B
         code = lib.osc_level_draws(lev.h, C.byref(ps), opt.seed, W["ell"], frm, frm + B, flags,
@@ -337,6 +342,8 @@ def main():
                                    qf.ctypes.data, qc.ctypes.data, itf.ctypes.data, itc.ctypes.data,
                                    st.ctypes.data, sums.ctypes.data)
         api._check(code, status=st)
+        if shard is not None:  # the batch's one collective: NCCL all-reduce of the per-level sums
+            shard.all_reduce_sum(sums[:5])
         iters_total[0] += int(itf.sum())
         iters_total[1] += int(itc.sum())
 

@@ -55,6 +55,10 @@ int guarded(F&& f) {
 
 void set_device(Ctx* c) { OSC_CUDA(cudaSetDevice(c->device)); }
 
+#ifndef OSC_XI_CHUNKS
+#define OSC_XI_CHUNKS 4
+#endif
+
 size_t budget_of(Ctx* c) {
   if (c->mem_budget) return c->mem_budget;
   size_t fr = 0, tot = 0;
@@ -358,7 +362,7 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     // chunk i's solve and only the first chunk's copy is exposed (up to 4 chunks of ≥ 8 samples);
     // device ξ / Philox: one chunk when it fits
     if (xi_host && count >= 2)
-      nchunks = std::max<int64_t>(nchunks, std::min<int64_t>(4, std::max<int64_t>(2, count / 8)));
+      nchunks = std::max<int64_t>(nchunks, std::min<int64_t>(OSC_XI_CHUNKS, std::max<int64_t>(2, count / 8)));
     const int Bc = (int)((count + nchunks - 1) / nchunks);
     c->fields_fine.ensure(sizeof(double) * Nf * Bc);
     if (has_coarse) c->fields_coarse.ensure(sizeof(double) * Nc * Bc);

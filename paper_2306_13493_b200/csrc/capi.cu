@@ -391,6 +391,8 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     }
     bool any_bad = false, any_fail = false;
     std::vector<int32_t> it_tmp(Bc), st_tmp(Bc), bad_tmp(Bc);
+    // OSC_NO_NESTED=1: fine solve from the reference's Dirichlet lift (A/B)
+    static const bool nested = std::getenv("OSC_NO_NESTED") == nullptr;
     for (int64_t c0 = 0; c0 < count; c0 += Bc) {
       const int B = (int)std::min<int64_t>(Bc, count - c0);
       const double* xi_chunk = nullptr;
@@ -417,10 +419,26 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
         OSC_CUDA(cudaEventRecord(c->ev_ce_done[chunk & 1], c->stream));
         issue_copy(chunk + 1);
       }
+      // Coupled draws solve the coarse field first: its solution, prolonged (P1), starts the fine
+      // PCG (nested iteration), which then needs fewer iterations to the same 1e-10 stopping test.
+      // The coarse conductivity buffer holds the guess once the coarse QoI has been evaluated.
+      std::vector<int32_t> itc_tmp(B), stc_tmp(B);
+      const double* guess = nullptr;
+      if (has_coarse) {
+        solver_prepare(c, mc, B, 0);
+        c->solver.lev[0].k = kc;
+        solver_run(c, prob, B);
+        qoi_launch(c, prob, B, d_qc);
+        solver_results(c, B, itc_tmp.data(), stc_tmp.data(), nullptr);
+        if (nested) {
+          OSC_CUDA(cudaMemcpyAsync(kc, c->solver.u, sizeof(double) * Nc * B, cudaMemcpyDeviceToDevice, c->stream));
+          guess = kc;
+        }
+      }
       // fine solve + QoI
       solver_prepare(c, m, B, 0);
       c->solver.lev[0].k = kf;
-      solver_run(c, prob, B);
+      solver_run(c, prob, B, guess);
       qoi_launch(c, prob, B, d_qf);
       solver_results(c, B, it_tmp.data(), st_tmp.data(), nullptr);
       d2h(c, bad_tmp.data(), d_bad, sizeof(int) * B);
@@ -433,15 +451,10 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
         if (status) status[c0 + b] = s;
       }
       if (has_coarse) {
-        solver_prepare(c, mc, B, 0);
-        c->solver.lev[0].k = kc;
-        solver_run(c, prob, B);
-        qoi_launch(c, prob, B, d_qc);
-        solver_results(c, B, it_tmp.data(), st_tmp.data(), nullptr);
         for (int b = 0; b < B; ++b) {
-          any_fail |= st_tmp[b] != 0;
-          if (iters_coarse) iters_coarse[c0 + b] = it_tmp[b];
-          if (status && status[c0 + b] == 0) status[c0 + b] = st_tmp[b];
+          any_fail |= stc_tmp[b] != 0;
+          if (iters_coarse) iters_coarse[c0 + b] = itc_tmp[b];
+          if (status && status[c0 + b] == 0) status[c0 + b] = stc_tmp[b];
         }
       }
       if (level_sums)

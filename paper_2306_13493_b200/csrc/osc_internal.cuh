@@ -150,7 +150,7 @@ size_t ce_inter_bytes(const Level* L, int count, int col_stride);
 // Batched MG-PCG (mgpcg.cu). k (device, B*(m+1)^2) is consumed as level-0 conductivity.
 void solver_prepare(Ctx* ctx, int m, int B, int hist_cap);
 size_t solver_bytes(int m, int B, int hist_cap);
-void solver_run(Ctx* ctx, const osc_problem* prob, int B);
+void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess = nullptr);
 // after solver_run: per-sample iters/status/u on device
 void qoi_launch(Ctx* ctx, const osc_problem* prob, int B, double* q_dev);
 void level_sums_launch(Ctx* ctx, const double* qf, const double* qc, int B, double shift_y,

@@ -1,6 +1,7 @@
-timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_v16.json 2> gpurun_out/bench_v16.err; echo "bench exit $?"; python -c "
-import json; d=json.load(open('gpurun_out/bench_v16.json')); print(d['value'], d['config']['mean_iters_fine']); print(d['kernels_ms'])"; tail -2 gpurun_out/bench_v16.err
+# ncu --set full of the CE kernels at config 2 (n = 2048, batch 8)
 CMD="python bench.py --config 2 --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-e2e"
-$CMD > gpurun_out/plain_ce.json 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"ce_rows|ce_cols" -s 2 -c 2 -o gpurun_out/prof_ce2 $CMD > gpurun_out/ncu_ce.log 2>&1
-tail -1 gpurun_out/ncu_ce.log
+$CMD > gpurun_out/plain_ce.json 2>&1 || exit 1
+for k in ce_rows ce_cols; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_ce2_$k $CMD > gpurun_out/ncu_ce2_$k.log 2>&1
+  tail -1 gpurun_out/ncu_ce2_$k.log
+done

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "osc_device.cuh"
 #include "osc_internal.cuh"
@@ -129,6 +130,278 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
     if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
   }
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+}
+
+// ---- compile-time-n path (n = 2^LOGN, 16 ≤ n ≤ 8192) ----------------------------------------------
+// Same arithmetic as ce_rows_kernel / ce_cols_kernel (bit-identical results), restructured so the
+// first and last Stockham stages run from registers:
+//   rows: each thread draws its stage-1 operands z[lt + r·T] directly (the two lanes of a pair split
+//         each Philox block: even lanes draw the even-r blocks, odd lanes the odd-r ones, and swap
+//         halves with one shuffle), so the input never goes through shared memory;
+//   cols: each thread loads its stage-1 operands straight from the column (coalesced 16-B loads),
+//         and keeps the last stage's outputs p1 = j + r·Ns in registers for the exp() epilogue.
+// Shared-memory round trips per transform: rows 5 → 4, cols 5 → 3; all index arithmetic is static.
+// A/B build knobs: cap the CTAs-per-SM the register budget is sized for (0 = 1024/THREADS, ≤ 64 regs)
+#ifndef OSC_CE_ROWS_MINB
+#define OSC_CE_ROWS_MINB 0
+#endif
+#ifndef OSC_CE_COLS_MINB
+#define OSC_CE_COLS_MINB 0
+#endif
+template <int LOGN>
+struct FftPlan {
+  static constexpr int n = 1 << LOGN;
+  static constexpr int T = n / 8;                    // threads per transform
+  static constexpr int NT = T >= 256 ? 1 : (256 / T < n / 2 ? 256 / T : n / 2);  // transforms per CTA (divides n/2)
+  static constexpr int THREADS = NT * T;
+  static constexpr int NSTAGE8 = LOGN / 3;           // radix-8 stages
+  static constexpr int REM = LOGN % 3;               // log2 of the final radix (0: none)
+  static constexpr int LD = n + (n >> 3) + 1;        // padded transform stride (fpad_len)
+  static constexpr int MINB = THREADS >= 1024 ? 1 : (1024 / THREADS < 32 ? 1024 / THREADS : 32);  // ≤ 64 regs
+  static constexpr int MINB_ROWS = (OSC_CE_ROWS_MINB > 0 && OSC_CE_ROWS_MINB < MINB) ? OSC_CE_ROWS_MINB : MINB;
+  static constexpr int MINB_COLS = (OSC_CE_COLS_MINB > 0 && OSC_CE_COLS_MINB < MINB) ? OSC_CE_COLS_MINB : MINB;
+};
+
+// Twiddles of one Stockham stage (radix R, sub-length 2^LNS) for this thread's G = 8/R butterflies.
+// They do not depend on the data, so each stage loads them BEFORE the barrier that publishes the
+// previous stage's outputs: the L1 latency overlaps the barrier wait.
+template <int LOGN, int R, int LNS>
+struct StageTw {
+  double2 w[8 / R][R > 1 ? R - 1 : 1];
+  __device__ __forceinline__ void load(int lt, const double2* __restrict__ tw) {
+    constexpr int T = (1 << LOGN) / 8, G = 8 / R;
+    constexpr int LR = R == 8 ? 3 : (R == 4 ? 2 : 1);
+    constexpr int TWS = LOGN - LNS - LR;  // twiddle step shift: k · n/(Ns·R)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int k = (lt + g * T) & ((1 << LNS) - 1);
+#pragma unroll
+      for (int r = 1; r < R; ++r) w[g][r - 1] = __ldg(&tw[(r * k) << TWS]);
+    }
+  }
+};
+
+// One Stockham stage from shared memory into registers (radix R, sub-length 2^LNS ≥ 8), E = 8 values
+// per thread held as G = 8/R butterflies; v[g][r] receives the butterfly outputs.
+template <int LOGN, int R, int LNS>
+__device__ __forceinline__ void stage_load_compute(const double2* x, int lt, const StageTw<LOGN, R, LNS>& t,
+                                                   double2 (&v)[8 / R][R]) {
+  constexpr int n = 1 << LOGN, T = n / 8, nR = n / R, G = 8 / R;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = lt + g * T;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[g][r] = x[fpad(j + r * nR)];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[g][r] = cmul(v[g][r], t.w[g][r - 1]);
+    dft_r<R>(v[g]);
+  }
+}
+
+template <int LOGN, int R, int LNS>
+__device__ __forceinline__ void stage_store(double2* x, int lt, const double2 (&v)[8 / R][R]) {
+  constexpr int T = (1 << LOGN) / 8, G = 8 / R, Ns = 1 << LNS;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = lt + g * T;
+    const int k = j & (Ns - 1);
+    const int base = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[fpad(base + r * Ns)] = v[g][r];
+  }
+}
+
+// Middle stages (radix 8, LNS = 3, 6, … below the final stage): twiddles, barrier (previous stage's
+// stores visible), loads + butterflies, barrier (all loads done), stores. The caller has stored the
+// previous stage and not yet synchronised.
+template <int LOGN, int LNS>
+__device__ __forceinline__ void mid_stages(double2* x, int lt, const double2* __restrict__ tw) {
+  using PL = FftPlan<LOGN>;
+  constexpr int last_lns = PL::REM ? 3 * PL::NSTAGE8 : 3 * (PL::NSTAGE8 - 1);  // LNS of the final stage
+  if constexpr (LNS < last_lns) {
+    StageTw<LOGN, 8, LNS> t;
+    t.load(lt, tw);
+    __syncthreads();
+    double2 v[1][8];
+    stage_load_compute<LOGN, 8, LNS>(x, lt, t, v);
+    __syncthreads();
+    stage_store<LOGN, 8, LNS>(x, lt, v);
+    mid_stages<LOGN, LNS + 3>(x, lt, tw);
+  }
+}
+
+// Final stage: radix 2^REM (or 8 when LOGN % 3 == 0), LNS = LOGN − log2(R); outputs of butterfly g
+// are p = (lt + g·T) + r·n/R.
+template <int LOGN>
+struct LastStage {
+  static constexpr int R = FftPlan<LOGN>::REM == 0 ? 8 : (1 << FftPlan<LOGN>::REM);
+  static constexpr int G = 8 / R;
+  static constexpr int LNS = LOGN - (R == 8 ? 3 : (R == 4 ? 2 : 1));
+  using Tw = StageTw<LOGN, R, LNS>;
+};
+
+// Stage 1 (Ns = 1, no twiddles) on register operands v[r] = x[lt + r·T], stored to shared memory.
+template <int LOGN>
+__device__ __forceinline__ void first_stage_store(double2* x, int lt, double2 (&v)[8]) {
+  dft8(v);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[fpad(lt * 8 + r)] = v[r];
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_ROWS) ce_rows_t_kernel(
+    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
+    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
+  using PL = FftPlan<LOGN>;
+  constexpr int n = PL::n, T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;  // transform slot in this CTA
+  const int lt = threadIdx.x % T;
+  const int rp = blockIdx.x * PL::NT + t;  // row pair (n/2 is a multiple of NT)
+  const int b = blockIdx.y;
+  const int q1a = 2 * rp, q1b = 2 * rp + 1;
+  double2* x = smem + t * PL::LD;
+  const int64_t s = (int64_t)n * n;
+  // Stage-1 operands: z[q0] for q0 = lt + r·T. T is even, so q0 has lt's parity and lanes lt, lt^1
+  // need the two halves of the same normal pair c = (lt >> 1) + r·T/2.
+  const bool odd = lt & 1;
+  double ra[8], rb[8];  // ξ(q0, q1a), ξ(q0, q1b)
+  if (xi) {
+    const double* xa = xi + (int64_t)b * s + (int64_t)q1a * n;
+    const double* xb = xa + n;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      ra[r] = __ldg(xa + lt + r * T);
+      rb[r] = __ldg(xb + lt + r * T);
+    }
+  } else {
+    const PhiloxKeys keys = philox_keys(seed);
+    const uint64_t idx = index0 + (uint64_t)b;
+    const uint32_t ja = (uint32_t)q1a * (n / 2) + (lt >> 1), jb = ja + n / 2;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      // this lane draws block r = 2h + odd for both rows; keeps its half, trades the other
+      const uint32_t off = (uint32_t)(2 * h + (odd ? 1 : 0)) * (T / 2);
+      const double2 pa = normal_pair_k(keys, ell, idx, ja + off);
+      const double2 pb = normal_pair_k(keys, ell, idx, jb + off);
+      const double keep_a = odd ? pa.y : pa.x, give_a = odd ? pa.x : pa.y;
+      const double keep_b = odd ? pb.y : pb.x, give_b = odd ? pb.x : pb.y;
+      const double got_a = __shfl_xor_sync(0xffffffffu, give_a, 1);
+      const double got_b = __shfl_xor_sync(0xffffffffu, give_b, 1);
+      // even lane: r = 2h is its own draw, r = 2h+1 came from the odd lane; odd lane: the reverse
+      ra[2 * h] = odd ? got_a : keep_a;
+      ra[2 * h + 1] = odd ? keep_a : got_a;
+      rb[2 * h] = odd ? got_b : keep_b;
+      rb[2 * h + 1] = odd ? keep_b : got_b;
+    }
+  }
+  double2 v[8];
+  {
+    const double* la = sqrt_lam + (int64_t)q1a * n + lt;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_double2(__ldg(la + r * T) * ra[r], __ldg(la + n + r * T) * rb[r]);
+  }
+  first_stage_store<LOGN>(x, lt, v);
+  mid_stages<LOGN, 3>(x, lt, tw);
+  {
+    using LS = LastStage<LOGN>;
+    typename LS::Tw t;
+    t.load(lt, tw);
+    __syncthreads();
+    double2 w[LS::G][LS::R];
+    stage_load_compute<LOGN, LS::R, LS::LNS>(x, lt, t, w);
+    __syncthreads();
+    stage_store<LOGN, LS::R, LS::LNS>(x, lt, w);
+    __syncthreads();
+  }
+  double2* out = inter + (int64_t)b * P * n + q1a;
+  for (int p = lt; p < P; p += T) {
+    const int p0 = p * cs;
+    const double2 zp = x[fpad(p0)];
+    const double2 zm = x[fpad((n - p0) & (n - 1))];
+    double2* o = out + (int64_t)p * n;
+    o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+    o[1] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_COLS) ce_cols_t_kernel(
+    const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
+    const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
+    int* __restrict__ bad_flag) {
+  using PL = FftPlan<LOGN>;
+  using LS = LastStage<LOGN>;
+  constexpr int n = PL::n, T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;
+  const int lt = threadIdx.x % T;
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * PL::NT + t;  // column (p index) of this transform
+  const bool valid = j < P;
+  double2* x = smem + t * PL::LD;
+  {
+    double2 v[8];
+    const double2* src = inter + ((int64_t)b * P + (valid ? j : 0)) * n + lt;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = valid ? __ldg(src + r * T) : make_double2(0.0, 0.0);
+    first_stage_store<LOGN>(x, lt, v);
+  }
+  mid_stages<LOGN, 3>(x, lt, tw);
+  double2 w[LS::G][LS::R];
+  {
+    typename LS::Tw t;
+    t.load(lt, tw);
+    __syncthreads();
+    stage_load_compute<LOGN, LS::R, LS::LNS>(x, lt, t, w);
+  }
+  if (!valid) return;  // no barriers below
+  const int mf = m + 1, mc = m / 2 + 1;
+  double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
+  double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
+  const int p0 = j * cs;
+  int bad = 0;
+#pragma unroll
+  for (int g = 0; g < LS::G; ++g)
+#pragma unroll
+    for (int r = 0; r < LS::R; ++r) {
+      const int p1 = lt + g * T + r * (n / LS::R);  // output row of this register
+      if (p1 > m || (p1 & (cs - 1))) continue;
+      const double zval = (w[g][r].x + w[g][r].y) * inv_n;
+      if (!isfinite(zval)) bad = 1;
+      const double o = do_exp ? exp(zval) : zval;
+      if (of) of[(int64_t)p1 * mf + p0] = o;
+      if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
+    }
+  if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+}
+
+template <int LOGN>
+void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev, uint64_t seed,
+              uint32_t ell, uint64_t index0, int count, bool do_exp, double* out_fine, double* out_coarse,
+              int* bad_flag, int cs, double2* inter) {
+  using PL = FftPlan<LOGN>;
+  const int m = L->m, P = m / cs + 1;
+  const double2* tw = L->twiddle.as<double2>();
+  const size_t sm = sizeof(double2) * (size_t)PL::NT * PL::LD;
+  cudaStream_t st = ctx->stream;
+  {
+    auto kern = ce_rows_t_kernel<LOGN>;
+    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    KScope ks(ctx, "ce_rows");
+    kern<<<dim3((PL::n / 2) / PL::NT, count), PL::THREADS, sm, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs,
+                                                                      tw, inter);
+    OSC_CUDA(cudaGetLastError());
+  }
+  {
+    auto kern = ce_cols_t_kernel<LOGN>;
+    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    KScope ks(ctx, "ce_cols");
+    kern<<<dim3((P + PL::NT - 1) / PL::NT, count), PL::THREADS, sm, st>>>(inter, m, P, cs, 1.0 / PL::n,
+                                                                           do_exp ? 1 : 0, tw, out_fine,
+                                                                           out_coarse, bad_flag);
+    OSC_CUDA(cudaGetLastError());
+  }
 }
 
 struct CeGeom {
@@ -370,15 +643,24 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
   if (count <= 0) return;
   // Coarse-only pass (other spectrum on the finest CES level) computes even columns only.
   const int cs = (out_fine == nullptr && out_coarse != nullptr) ? 2 : 1;
-  // Process the batch in chunks whose half-spectrum intermediate stays L2-resident between the
-  // row and the column pass (≈ 48 MB of the 126 MB L2), so the intermediate round trip
-  // (SURVEY §8(d) 32·n(n/2+1) B/sample) is served by L2 instead of HBM.
+  // Process the batch in chunks of up to 1 GiB of half-spectrum intermediate (SURVEY §8(d)
+  // 32·n(n/2+1) B/sample round trip). Both passes are fp64-issue bound with DRAM ≤ 16% busy, so the
+  // round trip through HBM is hidden; small L2-sized chunks (80 MB: 2 samples at n = 2048) lost
+  // more to partial last waves and pass-to-pass drains (config 2: 13.5k → 16.8k samples/s at 400 MB).
   const size_t per = ce_inter_bytes(L, 1, cs);
-  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, (80u << 20) / per));
+  // OSC_CE_CHUNK_MB: A/B knob for the chunk budget (default 1 GiB: the launches are compute-bound, so the
+  // intermediate spilling from L2 to HBM costs less than the tail waves of small chunks)
+  static const size_t chunk_bytes = [] {
+    const char* e = std::getenv("OSC_CE_CHUNK_MB");
+    return (size_t)(e ? std::atol(e) : 1024) << 20;
+  }();
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, chunk_bytes / per));
   ctx->ce_inter.ensure(ce_inter_bytes(L, chunk, cs));
   double2* inter = ctx->ce_inter.as<double2>();
   const int m = L->m, mc = m / 2;
   const int64_t Nf = (int64_t)(m + 1) * (m + 1), Nc = (int64_t)(mc + 1) * (mc + 1);
+  // OSC_CE_LEGACY=1: runtime-n kernels (A/B; bit-identical results)
+  static const bool legacy = std::getenv("OSC_CE_LEGACY") != nullptr;
   for (int c0 = 0; c0 < count; c0 += chunk) {
     const int cnt = std::min(chunk, count - c0);
     const double* xi_c = xi_dev ? xi_dev + (int64_t)c0 * L->s : nullptr;
@@ -388,7 +670,15 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
     // threads per transform T = n/E: ≤ 256 up to n = 2048, 512 at 4096, 1024 at 8192
     if (!pow2)
       launch_generic(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, rd);
-    else if (L->n >= 8192)
+    else if (L->n >= 16 && !legacy) {
+#define OSC_CE_T(LG) \
+  case LG: launch_t<LG>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
+      switch (31 - __builtin_clz((unsigned)L->n)) {
+        OSC_CE_T(4) OSC_CE_T(5) OSC_CE_T(6) OSC_CE_T(7) OSC_CE_T(8) OSC_CE_T(9) OSC_CE_T(10) OSC_CE_T(11)
+        OSC_CE_T(12) OSC_CE_T(13)
+      }
+#undef OSC_CE_T
+    } else if (L->n >= 8192)
       launch_pair<8, 1024>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
     else if (L->n == 4096)
       launch_pair<8, 512>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);

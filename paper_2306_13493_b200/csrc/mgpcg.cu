@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(NT) rows0_kernel(Geo g, int bc, const double* 
   const int b = blockIdx.y;
   const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
   if (i >= g.N) return;
-  const int y = (int)(i / g.n0), x = (int)(i - (int64_t)y * g.n0);
+  const int y = (int)((unsigned)i / (unsigned)g.n0), x = (int)i - y * g.n0;  // N < 2^31
   const S9 r = row_k(k + (int64_t)b * g.N, g.n0, 1, g.m, bc, x, y);
   const int64_t o = (int64_t)b * g.N + i;
   C[o] = r.c;
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(NT) prow_kernel(L9 R, int bc, int opdep, doubl
   const int64_t N = (int64_t)n0 * n0;
   const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
   if (i >= N) return;
-  const int y = (int)(i / n0), x = (int)(i - (int64_t)y * n0);
+  const int y = (int)((unsigned)i / (unsigned)n0), x = (int)i - y * n0;  // N < 2^31
   double w[4] = {0.0, 0.0, 0.0, 0.0};
   const bool fdir = is_dir(bc, m, x, y);
   if ((x & 1) == 0 && (y & 1) == 0) {
@@ -875,48 +875,43 @@ __global__ void __launch_bounds__(NT) c_post_kernel(L9 L, int red, const double*
 }
 
 
-// ---- PCG init: u = lift, r = b − A u (= b on interior rows, 0 on Dirichlet rows) -------------
-__global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing, double fval,
-                                                      double tol, int max_iter_factor,
-                                                      const double* __restrict__ k,
-                                                      double* __restrict__ u, double* __restrict__ r,
-                                                      double* scal, int* flags, double2* partial,
-                                                      int maxp, unsigned* counter, int* n_active,
-                                                      double* hist, int hist_cap) {
-  const int b = blockIdx.z;
-  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
-  const int m = g.m, n0 = g.n0;
-  const int p1 = (int)(i / n0), p0 = (int)(i - (int64_t)p1 * n0);
-  const int64_t off = (int64_t)b * g.N;
-  double bb = 0.0, rr = 0.0;
-  if (i < g.N) {
-    const bool dself = is_dir(bc, m, p0, p1);
-    const double g_self = (bc == OSC_BC_FLOWCELL && p0 == 0) ? 1.0 : 0.0;
-    double bi;
-    if (dself) {
-      bi = g_self;
-      u[off + i] = g_self;
-      r[off + i] = 0.0;
-    } else {
-      // load: f·area/3 per incident triangle (fem.cpp:85-86)
-      const int tri = 2 * (p0 < m && p1 < m) + (p0 > 0 && p1 < m) + 2 * (p0 > 0 && p1 > 0) +
-                      (p0 < m && p1 > 0);
-      const double h = 1.0 / m;
-      bi = forcing ? tri * (fval * (0.5 * h * h) / 3.0) : 0.0;
-      // symmetric elimination of the u=1 column at x=0 (fem.cpp:109-114)
-      if (bc == OSC_BC_FLOWCELL && p0 == 1) {
-        const double* kb = k + off;
-        auto K = [&](int a0, int a1) { return kb[(int64_t)a1 * n0 + a0]; };
-        const double e = -0.5 * ((p1 < m ? (K(0, p1) + K(1, p1) + K(1, p1 + 1)) / 3.0 : 0.0) +
-                                 (p1 > 0 ? (K(0, p1 - 1) + K(1, p1) + K(0, p1)) / 3.0 : 0.0));
-        bi -= e * 1.0;
-      }
-      u[off + i] = 0.0;
-      r[off + i] = bi;
-      rr = bi * bi;
-    }
-    bb = bi * bi;
+// ---- PCG init: u = lift (or the nested-iteration guess), r = b − A u, ‖b‖, ‖r‖ -------------------
+// One thread per column marching INIT_RY rows, so a CTA covers NT × INIT_RY nodes and does one
+// fixed-order reduction (a CTA per 256 nodes made the init launch-/reduction-bound: 1M CTAs per
+// config-4 batch).
+constexpr int INIT_RY = 16;
+
+// b_i for a free node (fem.cpp:85-86 load, :109-114 flow-cell column elimination)
+__device__ __forceinline__ double init_rhs(const double* __restrict__ kb, int bc, int forcing, double fval, int m,
+                                           int n0, int p0, int p1) {
+  const int tri = 2 * (p0 < m && p1 < m) + (p0 > 0 && p1 < m) + 2 * (p0 > 0 && p1 > 0) + (p0 < m && p1 > 0);
+  const double h = 1.0 / m;
+  double bi = forcing ? tri * (fval * (0.5 * h * h) / 3.0) : 0.0;
+  if (bc == OSC_BC_FLOWCELL && p0 == 1) {
+    auto K = [&](int a0, int a1) { return kb[(int64_t)a1 * n0 + a0]; };
+    const double e = -0.5 * ((p1 < m ? (K(0, p1) + K(1, p1) + K(1, p1 + 1)) / 3.0 : 0.0) +
+                             (p1 > 0 ? (K(0, p1 - 1) + K(1, p1) + K(0, p1)) / 3.0 : 0.0));
+    bi -= e * 1.0;
   }
+  return bi;
+}
+
+// u0 = P₁ u_c at fine node (x, y): the reference's P1 transfer (fem.cpp:144-165: C points injected,
+// edge nodes ½·(two parents), cell centres ½·(SW + NE) along the triangulation's diagonal).
+__device__ __forceinline__ double nested_guess(const double* __restrict__ ucb, int nc0, int x, int y) {
+  const int I = x >> 1, J = y >> 1;
+  const double* u = ucb + (int64_t)J * nc0 + I;
+  const bool ox = x & 1, oy = y & 1;
+  if (!ox && !oy) return u[0];
+  if (ox && !oy) return 0.5 * (u[0] + u[1]);
+  if (!ox && oy) return 0.5 * (u[0] + u[nc0]);
+  return 0.5 * (u[0] + u[nc0 + 1]);
+}
+
+__device__ __forceinline__ void init_finish(const Geo& g, double tol, int max_iter_factor, double bb, double rr,
+                                            double* scal, int* flags, double2* partial, int maxp,
+                                            unsigned* counter, int* n_active, double* hist, int hist_cap) {
+  const int b = blockIdx.z;
   double tb, tr;
   if (reduce2_last(bb, rr, partial, maxp, counter, b, tb, tr) && threadIdx.x == 0) {
     const double bnorm = sqrt(tb);
@@ -937,86 +932,53 @@ __global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing
   }
 }
 
-// ---- PCG init from a nested-iteration guess: u0 = P₁ u_c, the coarse coupled solve prolonged by
-// the reference's P1 transfer (fem.cpp:144-165: C points injected, edge nodes ½·(two parents), cell
-// centres ½·(SW + NE) along the triangulation's diagonal); r0 = b − A u0 on the free rows (A rows
-// rebuilt from k as row_k), u = g on Dirichlet rows. ‖b‖ and the stopping test are pcg_init's, so
-// only the starting iterate differs from the reference's Dirichlet lift (fem.cpp:335-339).
-__device__ __forceinline__ double nested_guess(const double* __restrict__ ucb, int nc0, int x, int y) {
-  const int I = x >> 1, J = y >> 1;
-  const double* u = ucb + (int64_t)J * nc0 + I;
-  const bool ox = x & 1, oy = y & 1;
-  if (!ox && !oy) return u[0];
-  if (ox && !oy) return 0.5 * (u[0] + u[1]);
-  if (!ox && oy) return 0.5 * (u[0] + u[nc0]);
-  return 0.5 * (u[0] + u[nc0 + 1]);
-}
-
-__global__ void __launch_bounds__(NT) pcg_init_guess_kernel(Geo g, int bc, int forcing, double fval, double tol,
-                                                            int max_iter_factor, const double* __restrict__ k,
-                                                            const double* __restrict__ uc, double* __restrict__ u,
-                                                            double* __restrict__ r, double* scal, int* flags,
-                                                            double2* partial, int maxp, unsigned* counter,
-                                                            int* n_active, double* hist, int hist_cap) {
+// uc == nullptr: the reference's Dirichlet lift (fem.cpp:335-339), u = g on Dirichlet rows and 0
+// elsewhere, r = b. uc != nullptr: nested iteration, u0 = P₁ u_c (the coarse coupled solve) on the
+// free rows and r0 = b − A u0 (A rows rebuilt from k as row_k; eliminated rows have no Dirichlet
+// couplings). ‖b‖ and the stopping test are the same in both cases.
+__global__ void __launch_bounds__(NT) pcg_init_kernel(Geo g, int bc, int forcing, double fval, double tol,
+                                                      int max_iter_factor, const double* __restrict__ k,
+                                                      const double* __restrict__ uc, double* __restrict__ u,
+                                                      double* __restrict__ r, double* scal, int* flags,
+                                                      double2* partial, int maxp, unsigned* counter,
+                                                      int* n_active, double* hist, int hist_cap) {
   const int b = blockIdx.z;
-  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
   const int m = g.m, n0 = g.n0, nc0 = m / 2 + 1;
-  const int p1 = (int)(i / n0), p0 = (int)(i - (int64_t)p1 * n0);
+  const int x = blockIdx.x * NT + threadIdx.x;
+  const int y0 = blockIdx.y * INIT_RY, y1 = min(y0 + INIT_RY, n0);
   const int64_t off = (int64_t)b * g.N;
-  const double* ucb = uc + (int64_t)b * nc0 * nc0;
+  const double* kb = k + off;
+  const double* ucb = uc ? uc + (int64_t)b * nc0 * nc0 : nullptr;
   double bb = 0.0, rr = 0.0;
-  if (i < g.N) {
-    const bool dself = is_dir(bc, m, p0, p1);
-    const double g_self = (bc == OSC_BC_FLOWCELL && p0 == 0) ? 1.0 : 0.0;
-    double bi;
-    if (dself) {
-      bi = g_self;
-      u[off + i] = g_self;
-      r[off + i] = 0.0;
-    } else {
-      const int tri = 2 * (p0 < m && p1 < m) + (p0 > 0 && p1 < m) + 2 * (p0 > 0 && p1 > 0) +
-                      (p0 < m && p1 > 0);
-      const double h = 1.0 / m;
-      bi = forcing ? tri * (fval * (0.5 * h * h) / 3.0) : 0.0;
-      if (bc == OSC_BC_FLOWCELL && p0 == 1) {
-        const double* kb = k + off;
-        auto K = [&](int a0, int a1) { return kb[(int64_t)a1 * n0 + a0]; };
-        const double e = -0.5 * ((p1 < m ? (K(0, p1) + K(1, p1) + K(1, p1 + 1)) / 3.0 : 0.0) +
-                                 (p1 > 0 ? (K(0, p1 - 1) + K(1, p1) + K(0, p1)) / 3.0 : 0.0));
-        bi -= e * 1.0;
+  if (x < n0) {
+    for (int y = y0; y < y1; ++y) {
+      const int64_t i = off + (int64_t)y * n0 + x;
+      double bi;
+      if (is_dir(bc, m, x, y)) {
+        bi = (bc == OSC_BC_FLOWCELL && x == 0) ? 1.0 : 0.0;
+        u[i] = bi;
+        r[i] = 0.0;
+      } else {
+        bi = init_rhs(kb, bc, forcing, fval, m, n0, x, y);
+        double ri = bi, u0 = 0.0;
+        if (ucb) {
+          const S9 a = row_k(kb, n0, 1, m, bc, x, y);
+          u0 = nested_guess(ucb, nc0, x, y);
+          double au = a.c * u0;
+          if (a.e != 0.0) au += a.e * nested_guess(ucb, nc0, x + 1, y);
+          if (a.w != 0.0) au += a.w * nested_guess(ucb, nc0, x - 1, y);
+          if (a.n != 0.0) au += a.n * nested_guess(ucb, nc0, x, y + 1);
+          if (a.s != 0.0) au += a.s * nested_guess(ucb, nc0, x, y - 1);
+          ri = bi - au;
+        }
+        u[i] = u0;
+        r[i] = ri;
+        rr += ri * ri;
       }
-      const S9 a = row_k(k + off, n0, 1, m, bc, p0, p1);  // eliminated row: Dirichlet couplings are 0
-      const double u0 = nested_guess(ucb, nc0, p0, p1);
-      double au = a.c * u0;
-      if (a.e != 0.0) au += a.e * nested_guess(ucb, nc0, p0 + 1, p1);
-      if (a.w != 0.0) au += a.w * nested_guess(ucb, nc0, p0 - 1, p1);
-      if (a.n != 0.0) au += a.n * nested_guess(ucb, nc0, p0, p1 + 1);
-      if (a.s != 0.0) au += a.s * nested_guess(ucb, nc0, p0, p1 - 1);
-      const double ri = bi - au;
-      u[off + i] = u0;
-      r[off + i] = ri;
-      rr = ri * ri;
+      bb += bi * bi;
     }
-    bb = bi * bi;
   }
-  double tb, tr;
-  if (reduce2_last(bb, rr, partial, maxp, counter, b, tb, tr) && threadIdx.x == 0) {
-    const double bnorm = sqrt(tb);
-    const double rel = sqrt(tr) / bnorm;
-    scal[b * S_NSCAL + S_BNORM] = bnorm;
-    scal[b * S_NSCAL + S_REL] = rel;
-    scal[b * S_NSCAL + S_RZ] = 0.0;
-    scal[b * S_NSCAL + S_BETA] = 0.0;
-    const int act = rel > tol ? 1 : 0;
-    flags[b * F_NFLAGS + F_ACTIVE] = act;
-    flags[b * F_NFLAGS + F_ITERS] = 0;
-    flags[b * F_NFLAGS + F_STATUS] = 0;
-    flags[b * F_NFLAGS + F_FIRST] = 1;
-    const int64_t cap = (int64_t)max_iter_factor * g.N;
-    flags[b * F_NFLAGS + F_MAXIT] = (int)(cap < 0x7fffffff ? cap : 0x7fffffff);
-    if (hist && hist_cap > 0) hist[(int64_t)b * hist_cap] = rel;
-    if (act) atomicAdd(n_active, 1);
-  }
+  init_finish(g, tol, max_iter_factor, bb, rr, scal, flags, partial, maxp, counter, n_active, hist, hist_cap);
 }
 
 // ---- register-marching MG-PCG kernels -----------------------------------------------------------
@@ -4036,16 +3998,12 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
     return;
   }
   OSC_CUDA(cudaMemsetAsync(w.n_active, 0, sizeof(int), st));
-  if (uc_guess) {  // nested iteration: start from the prolonged coarse coupled solution
+  {  // uc_guess: nested iteration, start from the prolonged coarse coupled solution
     KScope ks(ctx, "pcg_init");
-    pcg_init_guess_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(
-        g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, uc_guess, w.u,
-        w.r_cur, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
-  } else {
-    KScope ks(ctx, "pcg_init");
-    pcg_init_kernel<<<dim3(nblocks(L0.N), 1, B), NT, 0, st>>>(
-        g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, w.u, w.r_cur,
-        w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+    const dim3 grid((g0.n0 + NT - 1) / NT, (g0.n0 + INIT_RY - 1) / INIT_RY, B);
+    pcg_init_kernel<<<grid, NT, 0, st>>>(g0, bc, prob->forcing, prob->forcing_value, prob->tol,
+                                         prob->max_iter_factor, L0.k, uc_guess, w.u, w.r_cur, w.scal, w.flags,
+                                         part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
   }
   if (w.nlev > 1 && pcg_one_reduction()) {
     vcycle(ctx, bc, B, true);  // z = M r0; γ0, δ0 → α0

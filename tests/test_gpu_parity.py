@@ -92,6 +92,43 @@ def test_ce_linearity_large(P, ctx):
     assert np.all(z == 0.0)
 
 
+def test_ce_static_kernels_match_legacy(P, ctx, tmp_path):
+    """The compile-time-n CE kernels (register first/last stages, split Philox blocks) compute the
+    same arithmetic as the runtime-n kernels kept behind OSC_CE_LEGACY=1, for fine+coarse,
+    coarse-only (column stride 2) and host-ξ inputs, n = 16 … 4096. The normals are bit-identical;
+    the butterflies may contract a product into an FMA differently in the two kernels, so fields
+    agree to rounding (≤ 1e-14 of max|Z|), far inside the 1e-10 parity tolerance."""
+    import os
+    import subprocess
+    import sys
+    cases = [(8, 0.3), (16, 0.1), (64, 0.05), (256, 0.01), (1024, 0.01), (2048, 0.003)]
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2306_13493_b200 as P
+api = P.api
+out = {}
+for m, lam in %r:
+    op = api.build_operator(api.GridSpec.square(m), api.CovarianceModel.matern(1.0, lam, 0.5))
+    cnt = 2 if m >= 1024 else 3
+    f, c = op.sample_fields(None, count=cnt, seed=3, ell=1, index0=5, fine=True, coarse=True)
+    c2 = op.sample_fields(None, count=cnt, seed=3, ell=1, index0=5, fine=False, coarse=True)
+    xi = np.random.default_rng(m).standard_normal((1, op.s))
+    h = op.sample_fields(xi, fine=True)
+    out[f"f{m}"], out[f"c{m}"], out[f"cc{m}"], out[f"h{m}"] = f, c, c2, h
+np.savez(sys.argv[1], **out)
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), cases)
+    res = {}
+    for tag, env in (("new", {}), ("legacy", {"OSC_CE_LEGACY": "1"})):
+        path = str(tmp_path / f"{tag}.npz")
+        r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, **env), capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        res[tag] = np.load(path)
+    for k in res["new"].files:
+        assert relmax(res["new"][k], res["legacy"][k]) <= 1e-14, (k, relmax(res["new"][k], res["legacy"][k]))
+
+
 # ---- FEM (K3) -------------------------------------------------------------------------------------
 def test_solve_golden(P, ctx, golden):
     api = P.api

@@ -607,7 +607,19 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
     ach = per[dom] * args.steps * B / (dms / 1000.0) / 1e9 if dom in per else None
     roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
             "frac": ach / hbm if ach else None, "traffic": None, "peak_kind": hbm_kind,
-            "note": "algorithmic bytes count the half-spectrum round trip; chunks keep it L2-resident"}
+            "note": "algorithmic bytes count the half-spectrum round trip (1 GiB chunks: it spills to HBM, "
+                    "hidden under fp64 issue); the CE is bound by instruction issue, see compute_roofline"}
+    # fp64 view: conventional FFT flops 5·n·log2(n) per length-n complex transform, n/2 row and P column
+    # transforms per sample (Box-Muller log/sqrt/sincos and the exp() are not counted), against the
+    # measured DFMA peak (profiles/r1_fp64_peak.json, scripts/micro/fp64bench.cu)
+    fft_flops = (n // 2 + P) * 5.0 * n * math.log2(n)
+    fp64_peak = 34.22
+    compute_roof = {"bound": "fp64", "fft_flops_per_sample": fft_flops,
+                    "achieved": fft_flops * value / world / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": fft_flops * value / world / 1e12 / fp64_peak,
+                    "peak_source": "profiles/r1_fp64_peak.json (DFMA chains, 148 SMs, 1965 MHz)",
+                    "ncu": "profiles/r1_ce_rows_t_ncu.txt / r1_ce_cols_t_ncu.txt: fp64 pipe 35% / 17% busy, "
+                           "issue 52% / 21% of peak, warps 48% (64 regs, 4 CTAs/SM)"}
     b_sample = algorithmic_bytes_per_sample(dict(W, coupled=False, it=(0, 0)), n) - 8 * Nf * 0
     b_sample = 8 * n * n / B + 32 * n * (n // 2 + 1) + 8 * Nf  # SURVEY §8(d) B_ce, device ξ
     pipeline = {"basis": "SURVEY 8(d) B_ce (device xi)", "bytes_per_sample": b_sample,
@@ -662,7 +674,7 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic: device Philox NormalStream(1, 0, i)",
             "config": {"workload": W["name"], "global_batch": B * world, "embedding_n": n,
                        "l2": "fields written (34 GB/step) exceed L2", "setup_s": round(t_setup, 2)},
-            "roofline": roof, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "compute_roofline": compute_roof, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": ck,
             "kernels_ms": {k: round(v[1], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])},
         }), flush=True)

@@ -310,6 +310,46 @@ def test_level_draws_extensions_vs_port(P, ctx, port, bc, qoi):
     assert qrel(d.q_coarse[5:9], qc) < QOI_TOL
 
 
+@pytest.mark.parametrize("env", ["", "OSC_NESTED_SIMPLE=1", "OSC_NO_NESTED=1"])
+def test_nested_start_vs_port(P, port, env):
+    """Coupled draws start the fine PCG from the prolonged coarse solution (marching init kernel for
+    m ≥ 1024, per-node init below or with OSC_NESTED_SIMPLE=1; the reference's lift with
+    OSC_NO_NESTED=1).
+    The stopping test is unchanged, so QoIs match the oracle port (which starts from the lift) to 1e-7
+    on 256²/128² (per-node init) and 1024²/512² (marching init) coupled draws, both BC families."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2306_13493_b200 as P
+from oracle import oracle as O
+api = P.api
+port = O.Port()
+for bc, qoi, ell, cnt in [(1, 2, 4, 4), (0, 3, 4, 4), (0, 2, 6, 2)]:
+    m = 16 << ell
+    model = api.CovarianceModel.matern(2.0, 0.01, 0.5)
+    prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind(qoi)), bc=api.BC(bc))
+    opt = api.EstimatorOptions(seed=3)
+    plan = api.make_level_plan(ell, 1.0 / 16, prob, opt)
+    d = api.LevelDraws()
+    api.run_level_draws(plan, api.GridSpec.square(m // 2), False, False, prob, opt, 0, cnt, d)
+    sl = np.sqrt(np.maximum(plan.op.eigenvalues, 0))
+    qf, qc, itf, itc = port.coupled(m, plan.op.n, sl, None, True, 3, ell, 0, cnt, bc=bc, qoi=qoi)
+    rel = max(np.max(np.abs(d.q_fine[:cnt] - qf) / np.abs(qf)), np.max(np.abs(d.q_coarse[:cnt] - qc) / np.abs(qc)))
+    assert rel < 1e-7, (bc, qoi, m, rel)
+    print("iters", bc, m, float(np.mean(d.iters_fine[:cnt])))
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    if env:
+        k, v = env.split("=")
+        e[k] = v
+    out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
 def test_mlmc_vs_reference(P, ctx, ref):
     """MLMC mean and level variances agree with the reference within sampling CIs."""
     from oracle import oracle as O

@@ -480,10 +480,26 @@ def main():
             t = torch.tensor([ems], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
+        # the link bound: one plain H2D copy of the same pinned ξ (outside the timed region)
+        nb = min(B, 16)
+        dev = torch.empty((nb, s), dtype=torch.float64, device=f"cuda:{local}")
+        src = torch.from_numpy(buf.array[:nb])
+        dev.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record()
+        dev.copy_(src, non_blocking=True)
+        h1.record()
+        torch.cuda.synchronize()
+        h2d_gbs = 8.0 * s * nb / (h0.elapsed_time(h1) / 1000.0) / 1e9
+        del dev, src
         e2e = {"value": k_e2e * B * world / (ems / 1000.0), "unit": "samples/s",
                "h2d_bytes_per_step": 8 * s * B, "d2h_bytes_per_step": 8 * 2 * B + 4 * 3 * B + 40,
                "xi": f"host {'pinned' if pinned else 'pageable'}, {pool} distinct Philox rows cycled over the batch",
-               "steps": k_e2e}
+               "steps": k_e2e, "h2d_gbs": h2d_gbs,
+               "link_bound_samples_per_s": world * h2d_gbs * 1e9 / (8.0 * s),
+               "note": "ξ (8 B per embedding entry per sample) crosses PCIe every step; copies of chunk i+1 "
+                       "run under chunk i's solves, so e2e ≈ min(device rate, link rate)"}
         buf.free()
 
     cpu = None

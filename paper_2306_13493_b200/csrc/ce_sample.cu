@@ -159,7 +159,7 @@ struct FftPlan {
   static constexpr int LD = n + (n >> 3) + 1;        // padded transform stride (fpad_len)
   static constexpr int MINB = THREADS >= 1024 ? 1 : (1024 / THREADS < 32 ? 1024 / THREADS : 32);  // ≤ 64 regs
   static constexpr int MINB_ROWS = (OSC_CE_ROWS_MINB > 0 && OSC_CE_ROWS_MINB < MINB) ? OSC_CE_ROWS_MINB : MINB;
-  static constexpr int MINB_COLS = (OSC_CE_COLS_MINB > 0 && OSC_CE_COLS_MINB < MINB) ? OSC_CE_COLS_MINB : MINB;
+  static constexpr int MINB_COLS = OSC_CE_COLS_MINB > 0 ? OSC_CE_COLS_MINB : MINB;
 };
 
 // Twiddles of one Stockham stage (radix R, sub-length 2^LNS) for this thread's G = 8/R butterflies.

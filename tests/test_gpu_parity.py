@@ -310,6 +310,28 @@ def test_level_draws_extensions_vs_port(P, ctx, port, bc, qoi):
     assert qrel(d.q_coarse[5:9], qc) < QOI_TOL
 
 
+@pytest.mark.parametrize("cnt", [7, 40])
+def test_host_xi_chunks_match_device_philox(P, ctx, cnt):
+    """Host-ξ draws run in up to 4 chunks (double-buffered H2D copies under the previous chunk's
+    solves); the device-Philox path runs one chunk. With the same ξ (NormalStream rows copied from
+    the device) every slot is bit-identical."""
+    import ctypes as C
+    api = P.api
+    model = api.CovarianceModel.matern(1.0, 0.05, 0.5)
+    prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.L2Norm), bc=api.BC(0))
+    opt = api.EstimatorOptions(seed=9)
+    plan = api.make_level_plan(3, 1.0 / 16, prob, opt)
+    frm = 11
+    xi = np.empty((cnt, plan.op.s))
+    assert P.lib().osc_normals(ctx.h, 9, 3, frm, cnt, plan.op.s, xi.ctypes.data_as(C.c_void_p)) == 0
+    a, b = api.LevelDraws(), api.LevelDraws()
+    cg = api.GridSpec.square(plan.grid.m(0) // 2)
+    api.run_level_draws(plan, cg, False, False, prob, opt, frm, frm + cnt, a, ctx=ctx)
+    api.run_level_draws(plan, cg, False, False, prob, opt, frm, frm + cnt, b, ctx=ctx, xi=xi)
+    assert np.array_equal(a.q_fine, b.q_fine) and np.array_equal(a.q_coarse, b.q_coarse)
+    assert np.array_equal(a.iters_fine, b.iters_fine)
+
+
 @pytest.mark.parametrize("env", ["", "OSC_NESTED_SIMPLE=1", "OSC_NO_NESTED=1"])
 def test_nested_start_vs_port(P, port, env):
     """Coupled draws start the fine PCG from the prolonged coarse solution (marching init kernel for

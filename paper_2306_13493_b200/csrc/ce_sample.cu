@@ -248,22 +248,16 @@ __device__ __forceinline__ void first_stage_store(double2* x, int lt, double2 (&
   for (int r = 0; r < 8; ++r) x[fpad(lt * 8 + r)] = v[r];
 }
 
+// Stage-1 operands of the row pair (q1a, q1a + 1) of sample b: v[r] = z[lt + r·T] with
+// z[q0] = √λ(q0, q1a)·ξ(q0, q1a) + i·√λ(q0, q1b)·ξ(q0, q1b). T is even, so q0 has lt's parity and
+// lanes lt, lt^1 need the two halves of the same normal pair c = (lt >> 1) + r·T/2: the even lane
+// draws the even-r Philox blocks, the odd lane the odd-r ones, and they trade halves by shuffle.
 template <int LOGN>
-__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_ROWS) ce_rows_t_kernel(
-    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
-    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
-  using PL = FftPlan<LOGN>;
-  constexpr int n = PL::n, T = PL::T;
-  extern __shared__ double2 smem[];
-  const int t = threadIdx.x / T;  // transform slot in this CTA
-  const int lt = threadIdx.x % T;
-  const int rp = blockIdx.x * PL::NT + t;  // row pair (n/2 is a multiple of NT)
-  const int b = blockIdx.y;
-  const int q1a = 2 * rp, q1b = 2 * rp + 1;
-  double2* x = smem + t * PL::LD;
+__device__ __forceinline__ void rows_operands(const double* __restrict__ sqrt_lam, const double* __restrict__ xi,
+                                              const PhiloxKeys& keys, uint32_t ell, uint64_t idx, int b, int q1a,
+                                              int lt, double2 (&v)[8]) {
+  constexpr int n = 1 << LOGN, T = n / 8;
   const int64_t s = (int64_t)n * n;
-  // Stage-1 operands: z[q0] for q0 = lt + r·T. T is even, so q0 has lt's parity and lanes lt, lt^1
-  // need the two halves of the same normal pair c = (lt >> 1) + r·T/2.
   const bool odd = lt & 1;
   double ra[8], rb[8];  // ξ(q0, q1a), ξ(q0, q1b)
   if (xi) {
@@ -275,8 +269,6 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_RO
       rb[r] = __ldg(xb + lt + r * T);
     }
   } else {
-    const PhiloxKeys keys = philox_keys(seed);
-    const uint64_t idx = index0 + (uint64_t)b;
     const uint32_t ja = (uint32_t)q1a * (n / 2) + (lt >> 1), jb = ja + n / 2;
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -295,12 +287,44 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_RO
       rb[2 * h + 1] = odd ? keep_b : got_b;
     }
   }
-  double2 v[8];
-  {
-    const double* la = sqrt_lam + (int64_t)q1a * n + lt;
+  const double* la = sqrt_lam + (int64_t)q1a * n + lt;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = make_double2(__ldg(la + r * T) * ra[r], __ldg(la + n + r * T) * rb[r]);
+  for (int r = 0; r < 8; ++r) v[r] = make_double2(__ldg(la + r * T) * ra[r], __ldg(la + n + r * T) * rb[r]);
+}
+
+// Unpack the row pair's two half spectra (p0 = p·cs ≤ m) into the transposed intermediate.
+template <int LOGN>
+__device__ __forceinline__ void rows_unpack(const double2* x, double2* __restrict__ inter, int b, int P, int cs,
+                                            int q1a, int lt) {
+  constexpr int n = 1 << LOGN, T = n / 8;
+  double2* out = inter + (int64_t)b * P * n + q1a;
+  for (int p = lt; p < P; p += T) {
+    const int p0 = p * cs;
+    const double2 zp = x[fpad(p0)];
+    const double2 zm = x[fpad((n - p0) & (n - 1))];
+    // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
+    double2* o = out + (int64_t)p * n;
+    o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+    o[1] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
   }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_ROWS) ce_rows_t_kernel(
+    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
+    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
+  using PL = FftPlan<LOGN>;
+  constexpr int n = PL::n, T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;  // transform slot in this CTA
+  const int lt = threadIdx.x % T;
+  const int rp = blockIdx.x * PL::NT + t;  // row pair (n/2 is a multiple of NT)
+  const int b = blockIdx.y;
+  const int q1a = 2 * rp, q1b = 2 * rp + 1;
+  double2* x = smem + t * PL::LD;
+  const int64_t s = (int64_t)n * n;
+  double2 v[8];
+  rows_operands<LOGN>(sqrt_lam, xi, philox_keys(seed), ell, index0 + (uint64_t)b, b, q1a, lt, v);
   first_stage_store<LOGN>(x, lt, v);
   mid_stages<LOGN, 3>(x, lt, tw);
   {
@@ -314,15 +338,7 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_RO
     stage_store<LOGN, LS::R, LS::LNS>(x, lt, w);
     __syncthreads();
   }
-  double2* out = inter + (int64_t)b * P * n + q1a;
-  for (int p = lt; p < P; p += T) {
-    const int p0 = p * cs;
-    const double2 zp = x[fpad(p0)];
-    const double2 zm = x[fpad((n - p0) & (n - 1))];
-    double2* o = out + (int64_t)p * n;
-    o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-    o[1] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
-  }
+  rows_unpack<LOGN>(x, inter, b, P, cs, q1a, lt);
 }
 
 template <int LOGN>
@@ -376,6 +392,157 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_CO
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
 }
 
+// Column pass with two columns per thread (default; OSC_CE_COLS2=0 for one): the same stages as ce_cols_t_kernel
+// applied to columns j and j + 1 held by one thread, so each barrier interval carries two independent
+// butterflies (twice the loads in flight) and every twiddle load serves both columns.
+template <int LOGN, int R, int LNS>
+__device__ __forceinline__ void stage_load_compute2(const double2* x0, const double2* x1, int lt,
+                                                    const StageTw<LOGN, R, LNS>& t, double2 (&v)[2][8 / R][R]) {
+  constexpr int n = 1 << LOGN, T = n / 8, nR = n / R, G = 8 / R;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = lt + g * T;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      v[0][g][r] = x0[fpad(j + r * nR)];
+      v[1][g][r] = x1[fpad(j + r * nR)];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[c][g][r] = cmul(v[c][g][r], t.w[g][r - 1]);
+      dft_r<R>(v[c][g]);
+    }
+}
+
+template <int LOGN, int LNS>
+__device__ __forceinline__ void mid_stages2(double2* x0, double2* x1, int lt, const double2* __restrict__ tw) {
+  using PL = FftPlan<LOGN>;
+  constexpr int last_lns = PL::REM ? 3 * PL::NSTAGE8 : 3 * (PL::NSTAGE8 - 1);
+  if constexpr (LNS < last_lns) {
+    StageTw<LOGN, 8, LNS> t;
+    t.load(lt, tw);
+    __syncthreads();
+    double2 v[2][1][8];
+    stage_load_compute2<LOGN, 8, LNS>(x0, x1, lt, t, v);
+    __syncthreads();
+    stage_store<LOGN, 8, LNS>(x0, lt, v[0]);
+    stage_store<LOGN, 8, LNS>(x1, lt, v[1]);
+    mid_stages2<LOGN, LNS + 3>(x0, x1, lt, tw);
+  }
+}
+
+template <int LOGN>
+struct Cols2Plan {
+  static constexpr int THREADS = FftPlan<LOGN>::THREADS;
+  static constexpr int MINB = THREADS >= 512 ? 1 : 512 / THREADS;  // ≤ 128 registers
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MINB) ce_cols2_t_kernel(
+    const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
+    const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
+    int* __restrict__ bad_flag) {
+  using PL = FftPlan<LOGN>;
+  using LS = LastStage<LOGN>;
+  constexpr int n = PL::n, T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;
+  const int lt = threadIdx.x % T;
+  const int b = blockIdx.y;
+  const int j0 = 2 * (blockIdx.x * PL::NT + t);  // columns j0, j0 + 1
+  double2* x0 = smem + (2 * t) * PL::LD;
+  double2* x1 = x0 + PL::LD;
+  {
+    double2 v0[8], v1[8];
+    const bool ok0 = j0 < P, ok1 = j0 + 1 < P;
+    const double2* s0 = inter + ((int64_t)b * P + (ok0 ? j0 : 0)) * n + lt;
+    const double2* s1 = inter + ((int64_t)b * P + (ok1 ? j0 + 1 : 0)) * n + lt;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      v0[r] = ok0 ? __ldg(s0 + r * T) : make_double2(0.0, 0.0);
+      v1[r] = ok1 ? __ldg(s1 + r * T) : make_double2(0.0, 0.0);
+    }
+    first_stage_store<LOGN>(x0, lt, v0);
+    first_stage_store<LOGN>(x1, lt, v1);
+  }
+  mid_stages2<LOGN, 3>(x0, x1, lt, tw);
+  double2 w[2][LS::G][LS::R];
+  {
+    typename LS::Tw tt;
+    tt.load(lt, tw);
+    __syncthreads();
+    stage_load_compute2<LOGN, LS::R, LS::LNS>(x0, x1, lt, tt, w);
+  }
+  const int mf = m + 1, mc = m / 2 + 1;
+  double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
+  double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
+  int bad = 0;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int j = j0 + c;
+    if (j >= P) break;
+    const int p0 = j * cs;
+#pragma unroll
+    for (int g = 0; g < LS::G; ++g)
+#pragma unroll
+      for (int r = 0; r < LS::R; ++r) {
+        const int p1 = lt + g * T + r * (n / LS::R);
+        if (p1 > m || (p1 & (cs - 1))) continue;
+        const double zval = (w[c][g][r].x + w[c][g][r].y) * inv_n;
+        if (!isfinite(zval)) bad = 1;
+        const double o = do_exp ? exp(zval) : zval;
+        if (of) of[(int64_t)p1 * mf + p0] = o;
+        if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
+      }
+  }
+  if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+}
+
+// Row pass with two row pairs per thread (A/B only, OSC_CE_ROWS2=1): both transforms' operands are
+// drawn, then every stage carries two independent butterflies.
+template <int LOGN>
+__global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MINB) ce_rows2_t_kernel(
+    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
+    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
+  using PL = FftPlan<LOGN>;
+  using LS = LastStage<LOGN>;
+  constexpr int T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;
+  const int lt = threadIdx.x % T;
+  const int rp0 = 2 * (blockIdx.x * PL::NT + t);  // row pairs rp0, rp0 + 1 (n/2 is a multiple of 2·NT)
+  const int b = blockIdx.y;
+  double2* x0 = smem + (2 * t) * PL::LD;
+  double2* x1 = x0 + PL::LD;
+  const PhiloxKeys keys = philox_keys(seed);
+  const uint64_t idx = index0 + (uint64_t)b;
+  {
+    double2 v[8];
+    rows_operands<LOGN>(sqrt_lam, xi, keys, ell, idx, b, 2 * rp0, lt, v);
+    first_stage_store<LOGN>(x0, lt, v);
+    rows_operands<LOGN>(sqrt_lam, xi, keys, ell, idx, b, 2 * rp0 + 2, lt, v);
+    first_stage_store<LOGN>(x1, lt, v);
+  }
+  mid_stages2<LOGN, 3>(x0, x1, lt, tw);
+  {
+    typename LS::Tw tt;
+    tt.load(lt, tw);
+    __syncthreads();
+    double2 w[2][LS::G][LS::R];
+    stage_load_compute2<LOGN, LS::R, LS::LNS>(x0, x1, lt, tt, w);
+    __syncthreads();
+    stage_store<LOGN, LS::R, LS::LNS>(x0, lt, w[0]);
+    stage_store<LOGN, LS::R, LS::LNS>(x1, lt, w[1]);
+    __syncthreads();
+  }
+  rows_unpack<LOGN>(x0, inter, b, P, cs, 2 * rp0, lt);
+  rows_unpack<LOGN>(x1, inter, b, P, cs, 2 * rp0 + 2, lt);
+}
+
 template <int LOGN>
 void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev, uint64_t seed,
               uint32_t ell, uint64_t index0, int count, bool do_exp, double* out_fine, double* out_coarse,
@@ -385,13 +552,48 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = sizeof(double2) * (size_t)PL::NT * PL::LD;
   cudaStream_t st = ctx->stream;
-  {
+  // two row pairs per thread only on request (OSC_CE_ROWS2=1): the Box–Muller phase wants the warps,
+  // and halving them was slower (config 2 row pass 423 → 462 ms per 12288 samples)
+  static const bool rows2_env = [] {
+    const char* e = std::getenv("OSC_CE_ROWS2");
+    return e && e[0] == '1';
+  }();
+  bool rows_done = false;
+  if constexpr (LOGN >= 5 && LOGN <= 12 && (PL::n / 2) % (2 * PL::NT) == 0) {
+    if (rows2_env) {
+      auto kern = ce_rows2_t_kernel<LOGN>;
+      OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sm)));
+      KScope ks(ctx, "ce_rows");
+      kern<<<dim3((PL::n / 2) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(sqrt_lam, xi_dev, seed, ell,
+                                                                                index0, P, cs, tw, inter);
+      OSC_CUDA(cudaGetLastError());
+      rows_done = true;
+    }
+  }
+  if (!rows_done) {
     auto kern = ce_rows_t_kernel<LOGN>;
     OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     KScope ks(ctx, "ce_rows");
     kern<<<dim3((PL::n / 2) / PL::NT, count), PL::THREADS, sm, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs,
                                                                       tw, inter);
     OSC_CUDA(cudaGetLastError());
+  }
+  // two columns per thread (default for 32 ≤ n ≤ 4096, where it fits 128 registers without spills:
+  // config 2 column pass 277.7 → 208.6 ms per 12288 samples); OSC_CE_COLS2=0 keeps one (A/B)
+  static const bool cols2_env = [] {
+    const char* e = std::getenv("OSC_CE_COLS2");
+    return !(e && e[0] == '0');
+  }();
+  if constexpr (LOGN >= 5 && LOGN <= 12) {
+    if (cols2_env) {
+      auto kern = ce_cols2_t_kernel<LOGN>;
+      OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sm)));
+      KScope ks(ctx, "ce_cols");
+      kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
+          inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag);
+      OSC_CUDA(cudaGetLastError());
+      return;
+    }
   }
   {
     auto kern = ce_cols_t_kernel<LOGN>;

@@ -92,8 +92,10 @@ def test_ce_linearity_large(P, ctx):
     assert np.all(z == 0.0)
 
 
-def test_ce_static_kernels_match_legacy(P, ctx, tmp_path):
-    """The compile-time-n CE kernels (register first/last stages, split Philox blocks) compute the
+@pytest.mark.parametrize("variant", ["default", "one_per_thread", "rows2"])
+def test_ce_static_kernels_match_legacy(P, ctx, tmp_path, variant):
+    """The compile-time-n CE kernels (register first/last stages, split Philox blocks; two columns per
+    thread by default or one with OSC_CE_COLS2=0; two row pairs per thread with OSC_CE_ROWS2=1) compute the
     same arithmetic as the runtime-n kernels kept behind OSC_CE_LEGACY=1, for fine+coarse,
     coarse-only (column stride 2) and host-ξ inputs, n = 16 … 4096. The normals are bit-identical;
     the butterflies may contract a product into an FMA differently in the two kernels, so fields
@@ -119,7 +121,8 @@ for m, lam in %r:
 np.savez(sys.argv[1], **out)
 """ % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), cases)
     res = {}
-    for tag, env in (("new", {}), ("legacy", {"OSC_CE_LEGACY": "1"})):
+    new_env = {"default": {}, "one_per_thread": {"OSC_CE_COLS2": "0"}, "rows2": {"OSC_CE_ROWS2": "1"}}[variant]
+    for tag, env in (("new", new_env), ("legacy", {"OSC_CE_LEGACY": "1"})):
         path = str(tmp_path / f"{tag}.npz")
         r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, **env), capture_output=True,
                            text=True, timeout=900)

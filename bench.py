@@ -634,8 +634,9 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
                     "achieved": fft_flops * value / world / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": fft_flops * value / world / 1e12 / fp64_peak,
                     "peak_source": "profiles/r1_fp64_peak.json (DFMA chains, 148 SMs, 1965 MHz)",
-                    "ncu": "profiles/r1_ce_rows_t_ncu.txt / r1_ce_cols_t_ncu.txt: fp64 pipe 35% / 17% busy, "
-                           "issue 52% / 21% of peak, warps 48% (64 regs, 4 CTAs/SM)"}
+                    "ncu": "profiles/r1_ce_rows_t_ncu.txt / r1_ce_cols2_t_ncu.txt: fp64 pipe 35% / 23% busy, "
+                           "issue 52% / 25% of peak (latency-bound on shared-memory exchanges and "
+                           "Box-Muller dependency chains)"}
     b_sample = algorithmic_bytes_per_sample(dict(W, coupled=False, it=(0, 0)), n) - 8 * Nf * 0
     b_sample = 8 * n * n / B + 32 * n * (n // 2 + 1) + 8 * Nf  # SURVEY §8(d) B_ce, device ξ
     pipeline = {"basis": "SURVEY 8(d) B_ce (device xi)", "bytes_per_sample": b_sample,

@@ -998,10 +998,18 @@ constexpr int LY = 32;       // output rows per warp on large grids
 __host__ __device__ __forceinline__ int rows_per_warp(int m) {
   if (OSC_RPW == 1) return m >= 512 ? LY : (m >= 256 ? 16 : (m >= 64 ? 8 : 4));
   if (OSC_RPW == 2) return m >= 512 ? LY : (m >= 128 ? 16 : (m >= 64 ? 8 : 4));
-  return m >= 512 ? LY : (m >= 64 ? 16 : 8);
+  if (OSC_RPW == 3) return m >= 512 ? LY : (m >= 64 ? 16 : 8);
+  // 64 rows at m ≥ 1024 halve the ring warm-up and the per-CTA reduction tail of the level-0 sweeps
+  // (config 4: smooth_up 40.4 → 38.2 ms, pcg_update 45.3 → 44.6 ms per step)
+  return m >= 1024 ? 2 * LY : (m >= 512 ? LY : (m >= 64 ? 16 : 8));
 }
 constexpr int LYC = 16;      // coarse output rows per warp (restriction) on large grids
-__host__ __device__ __forceinline__ int coarse_rows_per_warp(int mc) { return mc >= 256 ? LYC : 4; }
+#ifndef OSC_LYC_BIG
+#define OSC_LYC_BIG 32  // level-0 restriction of the 2048² solve: 25.3 → 24.2 ms per config-4 step
+#endif
+__host__ __device__ __forceinline__ int coarse_rows_per_warp(int mc) {
+  return mc >= 512 ? OSC_LYC_BIG : (mc >= 256 ? LYC : 4);
+}
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(FULL, v, 1); }

@@ -292,20 +292,33 @@ __device__ __forceinline__ void rows_operands(const double* __restrict__ sqrt_la
   for (int r = 0; r < 8; ++r) v[r] = make_double2(__ldg(la + r * T) * ra[r], __ldg(la + n + r * T) * rb[r]);
 }
 
-// Unpack the row pair's two half spectra (p0 = p·cs ≤ m) into the transposed intermediate.
+// Intermediate layout of the compile-time-n passes: CE_IL columns interleaved,
+// inter[b][p/IL][q1][p%IL] (⌈P/IL⌉ groups per sample). The row pass's lanes for columns p … p+IL−1
+// fill IL·16 contiguous bytes per row (IL = 2: one 32-byte sector), and the column pass reads its two
+// adjacent columns as one 32-byte run per q1; wider groups help the row pass and hurt the column pass.
+#ifndef OSC_CE_IL
+#define OSC_CE_IL 2  // A/B at n = 2048: IL 2 → rows 28.5 + cols 17.4 µs; 4 → 27.4 + 20.7; 8 → 26.7 + 24.8
+#endif
+constexpr int CE_IL = OSC_CE_IL;  // columns interleaved per q1 run (power of two)
+__device__ __forceinline__ int64_t inter_pair_idx(int b, int Ph, int n, int p, int q1) {
+  return (((int64_t)b * Ph + p / CE_IL) * n + q1) * CE_IL + (p & (CE_IL - 1));
+}
+__host__ __device__ __forceinline__ int inter_groups(int P) { return (P + CE_IL - 1) / CE_IL; }
+
+// Unpack the row pair's two half spectra (p0 = p·cs ≤ m) into the intermediate.
 template <int LOGN>
 __device__ __forceinline__ void rows_unpack(const double2* x, double2* __restrict__ inter, int b, int P, int cs,
                                             int q1a, int lt) {
   constexpr int n = 1 << LOGN, T = n / 8;
-  double2* out = inter + (int64_t)b * P * n + q1a;
+  const int Ph = inter_groups(P);
   for (int p = lt; p < P; p += T) {
     const int p0 = p * cs;
     const double2 zp = x[fpad(p0)];
     const double2 zm = x[fpad((n - p0) & (n - 1))];
     // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
-    double2* o = out + (int64_t)p * n;
+    double2* o = inter + inter_pair_idx(b, Ph, n, p, q1a);
     o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-    o[1] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));
+    o[CE_IL] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));  // row q1a + 1
   }
 }
 
@@ -358,9 +371,9 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_CO
   double2* x = smem + t * PL::LD;
   {
     double2 v[8];
-    const double2* src = inter + ((int64_t)b * P + (valid ? j : 0)) * n + lt;
+    const double2* src = inter + inter_pair_idx(b, inter_groups(P), n, valid ? j : 0, lt);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = valid ? __ldg(src + r * T) : make_double2(0.0, 0.0);
+    for (int r = 0; r < 8; ++r) v[r] = valid ? __ldg(src + CE_IL * r * T) : make_double2(0.0, 0.0);
     first_stage_store<LOGN>(x, lt, v);
   }
   mid_stages<LOGN, 3>(x, lt, tw);
@@ -459,12 +472,12 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
   {
     double2 v0[8], v1[8];
     const bool ok0 = j0 < P, ok1 = j0 + 1 < P;
-    const double2* s0 = inter + ((int64_t)b * P + (ok0 ? j0 : 0)) * n + lt;
-    const double2* s1 = inter + ((int64_t)b * P + (ok1 ? j0 + 1 : 0)) * n + lt;
+    // columns j0 (even) and j0 + 1 sit side by side: one 32-byte run per q1
+    const double2* s0 = inter + inter_pair_idx(b, inter_groups(P), n, ok0 ? j0 : 0, lt);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      v0[r] = ok0 ? __ldg(s0 + r * T) : make_double2(0.0, 0.0);
-      v1[r] = ok1 ? __ldg(s1 + r * T) : make_double2(0.0, 0.0);
+      v0[r] = ok0 ? __ldg(s0 + CE_IL * r * T) : make_double2(0.0, 0.0);
+      v1[r] = ok1 ? __ldg(s0 + CE_IL * r * T + 1) : make_double2(0.0, 0.0);
     }
     first_stage_store<LOGN>(x0, lt, v0);
     first_stage_store<LOGN>(x1, lt, v1);
@@ -830,7 +843,8 @@ void launch_generic(Ctx* ctx, const Level* L, const double* sqrt_lam, const doub
 
 size_t ce_inter_bytes(const Level* L, int count, int col_stride) {
   const int P = L->m / col_stride + 1;
-  return sizeof(double2) * (size_t)count * L->n * P;
+  const int Pe = CE_IL * inter_groups(P);  // column groups (inter_pair_idx); the runtime-n kernels use P ≤ Pe
+  return sizeof(double2) * (size_t)count * L->n * Pe;
 }
 
 void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,

@@ -1399,76 +1399,94 @@ __device__ __forceinline__ Pair coarse_pair(const CoarseRaw& c, int y) {
   return Pair{0.5 * (c.a0 + c.b0), 0.5 * (c.a0 + c.b1)};
 }
 
+// Whole start of a nested solve in one marching pass: b (init_rhs), the lift on Dirichlet rows
+// (u = g, r = 0), u = g_guess and r = b − A·g_guess on the free rows, and ‖b‖², ‖r‖² for the stopping
+// test. Returns (Σ b², Σ r²) of this lane's output nodes.
 template <bool INT>
-__device__ __forceinline__ double init_nested_body(Geo g, int bc, const double* __restrict__ k,
-                                                   const double* __restrict__ uc, double* __restrict__ u,
-                                                   double* __restrict__ r, const PairCtx& c) {
+__device__ __forceinline__ double2 init_nested_body(Geo g, int bc, int forcing, double fval,
+                                                    const double* __restrict__ k, const double* __restrict__ uc,
+                                                    double* __restrict__ u, double* __restrict__ r, const PairCtx& c) {
   PAIR_UNPACK
   const int nc0 = m / 2 + 1;
   const double* ucb = uc + (int64_t)b * nc0 * nc0;
-  const double *kb = k + off, *rb = r + off, *ub = u + off;
+  const double* kb = k + off;
   const Pair zero{0.0, 0.0};
+  const double h = 1.0 / m;
+  const double b_int = forcing ? 6 * (fval * (0.5 * h * h) / 3.0) : 0.0;  // init_rhs of an interior node
   auto guess = [&](int y) { return nested_pair<INT>(ucb, nc0, xa, y, m, bc); };
   Pair km = ld2<INT>(kb, xa, y0 - 1, n0), k0 = ld2<INT>(kb, xa, y0, n0);
   Pair pm = guess(y0 - 1), p0 = guess(y0);
   Pair Nm, Ed;
   edges_pair<INT>(zero, km, k0, xa, y0 - 1, m, Ed, Nm);
-  // rows loaded one iteration ahead: k, coarse raw values and the guess of row y+1; r, u of row y
+  // rows loaded one iteration ahead: k, coarse raw values and the guess of row y+1
   Pair kq = ld2<INT>(kb, xa, y0 + 1, n0);
   CoarseRaw cq{};
   Pair pq = zero;
   if (INT) cq = coarse_raw(ucb, nc0, xa, y0 + 1);
   else pq = guess(y0 + 1);
-  Pair rq = ld2<INT>(rb, xa, y0, n0), uq = ld2<INT>(ub, xa, y0, n0);
-  double rr = 0.0;
+  double bb = 0.0, rr = 0.0;
+  auto node = [&](int x, int y, int64_t i, const Sten& st, double pv, double odv) {
+    double bi;
+    if (!INT && is_dir(bc, m, x, y)) {
+      bi = (bc == OSC_BC_FLOWCELL && x == 0) ? 1.0 : 0.0;
+      u[i] = bi;
+      r[i] = 0.0;
+    } else {
+      bi = INT ? b_int : init_rhs(kb, bc, forcing, fval, m, n0, x, y);
+      const double rn = bi - fma(st.d, pv, odv);
+      u[i] = pv;
+      r[i] = rn;
+      rr = fma(rn, rn, rr);
+    }
+    bb = fma(bi, bi, bb);
+  };
   for (int y = y0; y < y1; ++y) {
-    const Pair kp = kq, r0 = rq, u0 = uq;
+    const Pair kp = kq;
     const Pair pp = INT ? coarse_pair(cq, y + 1) : pq;
     kq = ld2<INT>(kb, xa, y + 2, n0);
     if (INT) cq = coarse_raw(ucb, nc0, xa, y + 2);
     else pq = guess(y + 2);
-    rq = ld2<INT>(rb, xa, y + 1, n0);
-    uq = ld2<INT>(ub, xa, y + 1, n0);
     Pair E, N;
     edges_pair<INT>(km, k0, kp, xa, y, m, E, N);
     const Sten2 st = sten_pair<INT>(E, N, Nm, xa, y, m, bc);
     const Pair od = offd_pair(st, pm, p0, pp);
     const int64_t row = off + (int64_t)y * n0;
-    if (outa) {
-      const double rn = r0.a - fma(st.a.d, p0.a, od.a);
-      u[row + xa] = u0.a + p0.a;
-      r[row + xa] = rn;
-      rr = fma(rn, rn, rr);
-    }
-    if (outb) {
-      const double rn = r0.b - fma(st.b.d, p0.b, od.b);
-      u[row + xb] = u0.b + p0.b;
-      r[row + xb] = rn;
-      rr = fma(rn, rn, rr);
-    }
+    if (outa) node(xa, y, row + xa, st.a, p0.a, od.a);
+    if (outb) node(xb, y, row + xb, st.b, p0.b, od.b);
     km = k0; k0 = kp; pm = p0; p0 = pp; Nm = N;
   }
-  return rr;
+  return make_double2(bb, rr);
 }
 
-__global__ void __launch_bounds__(MT, 4) pcg_init_nested_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
+// No active-flag test in the prologue: this kernel initialises the flags.
+__global__ void __launch_bounds__(MT, 4) pcg_init_nested_kernel(Geo g, int bc, int forcing, double fval, double tol,
+                                                                int max_iter_factor, const double* __restrict__ k,
                                                                 const double* __restrict__ uc, double* __restrict__ u,
                                                                 double* __restrict__ r, double* scal, int* flags,
                                                                 double2* partial, int maxp, unsigned* counter,
                                                                 int* n_active, double* hist, int hist_cap) {
-  PAIR_PROLOGUE
-  const double rr = interior ? init_nested_body<true>(g, bc, k, uc, u, r, c)
-                             : init_nested_body<false>(g, bc, k, uc, u, r, c);
-  double t0, t1;
-  if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
-    const double rel = sqrt(t0) / scal[b * S_NSCAL + S_BNORM];
-    scal[b * S_NSCAL + S_REL] = rel;
-    if (hist && hist_cap > 0) hist[(int64_t)b * hist_cap] = rel;
-    if (!(rel > tol)) {  // the guess already meets the stopping test
-      flags[b * F_NFLAGS + F_ACTIVE] = 0;
-      atomicSub(n_active, 1);
-    }
+  PairCtx c;
+  {
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
+    const int ly = rows_per_warp(g.m);
+    c.b = blockIdx.z;
+    c.lane = lane;
+    c.m = g.m;
+    c.n0 = g.n0;
+    c.xa = strip * 60 - 2 + 2 * lane;
+    c.xb = c.xa + 1;
+    c.outa = lane >= 1 && lane < 31 && c.xa <= g.m;
+    c.outb = lane >= 1 && lane < 31 && c.xb <= g.m;
+    c.y0 = blockIdx.y * ly;
+    c.y1 = min(c.y0 + ly, g.n0);
+    c.off = (int64_t)c.b * g.N;
   }
+  const int strip0 = blockIdx.x * MW + (threadIdx.x >> 5);
+  const bool interior = strip0 * 60 - 2 >= 2 && strip0 * 60 + 61 <= g.m - 2 && c.y0 >= 3 && c.y1 <= g.m - 2;
+  const double2 br = interior ? init_nested_body<true>(g, bc, forcing, fval, k, uc, u, r, c)
+                              : init_nested_body<false>(g, bc, forcing, fval, k, uc, u, r, c);
+  init_finish(g, tol, max_iter_factor, br.x, br.y, scal, flags, partial, maxp, counter, n_active, hist, hist_cap);
 }
 
 // ---- PCG update fused with the level-0 pre-smoother:
@@ -4124,15 +4142,16 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
     static const bool nested_simple_env = std::getenv("OSC_NESTED_SIMPLE") != nullptr;
     const bool nested_simple = nested_simple_env || w.m < 1024;
     KScope ks(ctx, "pcg_init");
-    const dim3 grid((g0.n0 + NT - 1) / NT, (g0.n0 + INIT_RY - 1) / INIT_RY, B);
-    pcg_init_kernel<<<grid, NT, 0, st>>>(g0, bc, prob->forcing, prob->forcing_value, prob->tol,
-                                         prob->max_iter_factor, L0.k, nested_simple ? uc_guess : nullptr, w.u,
-                                         w.r_cur, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active,
-                                         w.hist, w.hist_cap);
-    if (uc_guess && !nested_simple)
-      pcg_init_nested_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, uc_guess, w.u,
-                                                                    w.r_cur, w.scal, w.flags, part, w.max_parts,
-                                                                    w.counter, w.n_active, w.hist, w.hist_cap);
+    if (uc_guess && !nested_simple) {
+      pcg_init_nested_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(
+          g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, uc_guess, w.u,
+          w.r_cur, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+    } else {
+      const dim3 grid((g0.n0 + NT - 1) / NT, (g0.n0 + INIT_RY - 1) / INIT_RY, B);
+      pcg_init_kernel<<<grid, NT, 0, st>>>(g0, bc, prob->forcing, prob->forcing_value, prob->tol,
+                                           prob->max_iter_factor, L0.k, uc_guess, w.u, w.r_cur, w.scal, w.flags,
+                                           part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+    }
   }
   if (w.nlev > 1 && pcg_one_reduction()) {
     vcycle(ctx, bc, B, true);  // z = M r0; γ0, δ0 → α0

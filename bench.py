@@ -317,6 +317,18 @@ def main():
     t_setup = time.perf_counter()
     plan = api.make_level_plan(W["ell"], 1.0 / (m >> W["ell"]), problem, opt)
     t_setup = time.perf_counter() - t_setup
+    # the same level setup on the device (osc_build_spectrum_device), timed and checked once
+    try:
+        torch.cuda.synchronize()
+        t_dev = time.perf_counter()
+        op_dev = api.build_operator(plan.grid, model, device=True, ctx=ctx)
+        t_dev = time.perf_counter() - t_dev
+        e_h, e_d = plan.op.eigenvalues, op_dev.eigenvalues
+        setup_dev = {"s": round(t_dev, 4), "host_s": round(t_setup, 4),
+                     "max_rel_eig_diff": float(np.max(np.abs(e_d - e_h)) / np.max(np.abs(e_h)))}
+        del op_dev, e_d
+    except api.ConfigError as e:
+        setup_dev = {"unsupported": str(e)}
     lev = plan.op.device_level(ctx, 0)
     coarse = api.GridSpec.square(m // 2) if W["coupled"] else None
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -525,7 +537,7 @@ def main():
                        "parallelism": f"dp{world} (contiguous sample shards)",
                        "l2": "inputs larger than L2 (>= 40 GB touched per step)" if m >= 1024 else
                        "per-step working set exceeds L2 (batch)",
-                       "setup_s": round(t_setup, 2), "coarse_op": args.coarse_op,
+                       "setup_s": round(t_setup, 2), "setup_device": setup_dev, "coarse_op": args.coarse_op,
                        "mean_iters_fine": iters_timed[0] / (args.steps * B),
                        "mean_iters_coarse": iters_timed[1] / (args.steps * B) if W["coupled"] else None},
             "roofline": roof, "kernel_gbs": per_kernel, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,

@@ -18,6 +18,7 @@
  *   osc_qoi             ← evaluate_qoi / qoi_point / qoi_l2norm (estimators.hpp:23,
  *                         fem.hpp:51-54, src/fem.cpp:402-436)
  *   osc_build_spectrum  ← build_operator (embedding.hpp:112-113, src/embedding.cpp:114-151)
+ *   osc_build_spectrum_device ← build_operator with build_first_row + spectrum on the device
  *   osc_level_create    ← EmbeddingOperator::from_parts + truncated (embedding.cpp:90-112,153-163)
  *   osc_normals         ← NormalStream::fill (include/oscfield/rng.hpp:30-43, src/rng.cpp:42-67)
  *
@@ -150,6 +151,14 @@ void osc_free(void* p);
 int osc_build_spectrum(int m, int family, double sigma2, double lambda, double nu_or_p,
                        const double* fractions, int n_fractions, double tol_spd_factor,
                        int* J_out, int64_t* s_out, double** eig_out);
+/* build_operator with the first row and the spectrum FFT on the device (same padding schedule,
+ * SPD test, clamping and output contract as osc_build_spectrum). Separable exponential and
+ * Matern nu = k + 1/2 (k <= 3, closed forms of covariance.cpp:53-62); other nu → OSC_ERR_CONFIG.
+ * Eigenvalues agree with the host setup to rounding (~1e-15 of max λ); ties of equal λ may then
+ * order differently in a truncation mask (use the host or OSC1 spectrum for mask parity). */
+int osc_build_spectrum_device(osc_ctx* ctx, int m, int family, double sigma2, double lambda, double nu_or_p,
+                              const double* fractions, int n_fractions, double tol_spd_factor,
+                              int* J_out, int64_t* s_out, double** eig_out);
 /* Upload one level: n = 2(m+J); eigenvalues (s entries) → √max(λ,0) on device, plus the
  * truncated copy zeroing the k_trunc smallest by a stable descending sort
  * (embedding.cpp:105-110,153-163). k_trunc = 0 → no truncated copy. */

@@ -36,6 +36,7 @@ EXPORTS = [
     "osc_ctx_create", "osc_ctx_destroy", "osc_last_error", "osc_ctx_stream", "osc_ctx_synchronize",
     "osc_ctx_set_mem_budget", "osc_ctx_set_profiling", "osc_ctx_profile_only", "osc_ctx_kernel_stats", "osc_ctx_reset_stats",
     "osc_ctx_launch_count", "osc_host_alloc", "osc_host_free", "osc_free", "osc_build_spectrum",
+    "osc_build_spectrum_device",
     "osc_level_create", "osc_level_destroy", "osc_level_info", "osc_level_draws", "osc_summarize",
     "osc_normals", "osc_ce_sample", "osc_darcy_solve", "osc_qoi",
 ]
@@ -99,6 +100,8 @@ def lib() -> C.CDLL:
     L.osc_free.restype = None
     L.osc_build_spectrum.argtypes = [ip, ip, C.c_double, C.c_double, C.c_double, vp, ip, C.c_double,
                                      C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(vp)]
+    L.osc_build_spectrum_device.argtypes = [vp, ip, ip, C.c_double, C.c_double, C.c_double, vp, ip, C.c_double,
+                                            C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(vp)]
     L.osc_level_create.argtypes = [vp, ip, ip, vp, i64, C.POINTER(vp)]
     L.osc_level_destroy.argtypes = [vp]
     L.osc_level_destroy.restype = None

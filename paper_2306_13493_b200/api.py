@@ -360,14 +360,24 @@ class DeviceLevel:
 
 
 def build_operator(grid: GridSpec, model: CovarianceModel,
-                   options: BuildOptions = BuildOptions()) -> EmbeddingOperator:
-    """build_operator (embedding.cpp:114-151): J = 0, then ceil(f·m) until SPD."""
+                   options: BuildOptions = BuildOptions(), *, device: bool = False,
+                   ctx: Optional["Context"] = None) -> EmbeddingOperator:
+    """build_operator (embedding.cpp:114-151): J = 0, then ceil(f·m) until SPD. device=True builds
+    the first row and the spectrum on the GPU (osc_build_spectrum_device; separable exponential
+    and Matérn ν = k + ½, k ≤ 3); the host C++ setup is the general path."""
     lib = L.lib()
     fr = np.ascontiguousarray(options.padding_fractions, dtype=np.float64)
     J, s, ptr = C.c_int(), C.c_int64(), C.c_void_p()
-    _check(lib.osc_build_spectrum(grid.m(0), int(model.family), model.sigma2, model.lambda_,
-                                  model.param, _p(fr), len(fr), options.tol_spd_factor,
-                                  C.byref(J), C.byref(s), C.byref(ptr)))
+    if device:
+        ctx = ctx or default_context()
+        _check(lib.osc_build_spectrum_device(ctx.h, grid.m(0), int(model.family), model.sigma2,
+                                             model.lambda_, model.param, _p(fr), len(fr),
+                                             options.tol_spd_factor, C.byref(J), C.byref(s),
+                                             C.byref(ptr)))
+    else:
+        _check(lib.osc_build_spectrum(grid.m(0), int(model.family), model.sigma2, model.lambda_,
+                                      model.param, _p(fr), len(fr), options.tol_spd_factor,
+                                      C.byref(J), C.byref(s), C.byref(ptr)))
     try:
         eig = np.ctypeslib.as_array((C.c_double * s.value).from_address(ptr.value)).copy()
     finally:

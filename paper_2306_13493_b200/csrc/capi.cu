@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,9 @@ struct SetupError {
 std::vector<double> build_spectrum(int m, int family, double sigma2, double lambda, double nu_or_p,
                                    const double* fractions, int n_fractions, double tol_factor,
                                    int* J_out);
+std::vector<double> build_spectrum_with(int m, int family, double sigma2, double lambda, double nu_or_p,
+                                        const double* fractions, int n_fractions, double tol_factor, int* J_out,
+                                        const std::function<std::vector<double>(int)>& attempt_spectrum);
 void sqrt_spectra(const double* eig, int64_t s, int64_t k_trunc, std::vector<double>& full,
                   std::vector<double>& trunc);
 }  // namespace osc
@@ -258,6 +262,31 @@ int osc_build_spectrum(int m, int family, double sigma2, double lambda, double n
   });
 }
 
+int osc_build_spectrum_device(osc_ctx* c, int m, int family, double sigma2, double lambda, double nu_or_p,
+                              const double* fractions, int n_fractions, double tol_spd_factor, int* J_out,
+                              int64_t* s_out, double** eig_out) {
+  return guarded([&] {
+    OSC_REQUIRE(c, "osc_build_spectrum_device: null context");
+    OSC_REQUIRE(family == OSC_COV_MATERN || family == OSC_COV_SEPARABLE_EXP,
+                "osc_build_spectrum_device: unknown covariance family");
+    OSC_REQUIRE(spectrum_device_supported(family, nu_or_p),
+                "osc_build_spectrum_device: Matern nu must be k + 1/2 with k <= 3 (use osc_build_spectrum)");
+    set_device(c);
+    int J = 0;
+    std::vector<double> eig = build_spectrum_with(
+        m, family, sigma2, lambda, nu_or_p, fractions, n_fractions, tol_spd_factor, &J,
+        [&](int Jt) { return spectrum_device(c, m, Jt, family, sigma2, lambda, nu_or_p); });
+    if (J_out) *J_out = J;
+    if (s_out) *s_out = (int64_t)eig.size();
+    if (eig_out) {
+      double* buf = static_cast<double*>(std::malloc(sizeof(double) * eig.size()));
+      if (!buf) throw std::bad_alloc();
+      std::memcpy(buf, eig.data(), sizeof(double) * eig.size());
+      *eig_out = buf;
+    }
+  });
+}
+
 int osc_level_create(osc_ctx* c, int m, int J, const double* eigenvalues, int64_t k_trunc,
                      osc_level** out) {
   return guarded([&] {
@@ -282,14 +311,7 @@ int osc_level_create(osc_ctx* c, int m, int J, const double* eigenvalues, int64_
         L->sqrt_trunc.ensure(sizeof(double) * L->s);
         OSC_CUDA(cudaMemcpy(L->sqrt_trunc.p, trunc.data(), sizeof(double) * L->s, cudaMemcpyHostToDevice));
       }
-      std::vector<double> tw(2 * (size_t)L->n);
-      for (int t = 0; t < L->n; ++t) {
-        const long double a = 6.283185307179586476925286766559005768L * t / L->n;
-        tw[2 * (size_t)t] = (double)std::cos(a);
-        tw[2 * (size_t)t + 1] = (double)std::sin(a);
-      }
-      L->twiddle.ensure(sizeof(double) * tw.size());
-      OSC_CUDA(cudaMemcpy(L->twiddle.p, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
+      upload_twiddles(L);
     } catch (...) {
       L->sqrt_full.release();
       L->sqrt_trunc.release();

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <cstdlib>
 
 #include "osc_device.cuh"
@@ -905,6 +907,161 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
     else
       launch_pair<2, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
   }
+}
+
+// ---- level setup on the device -------------------------------------------------
+// The spectrum of the padding-J embedding, λ = √s·Re(F row) (embedding.cpp:67-88), from the first
+// row built on the device (embedding.cpp:22-65, covariance.cpp:47-115) and the CE kernels
+// themselves: the row is even in both directions, so F row is real and even, and the CE pass with
+// √λ ≡ 1, ξ = row and window m' = n/2 returns (Re + Im)(F_u row) = λ/n on [0, n/2]² (Im is rounding
+// noise). The window is mirrored to n². Matérn is supported for ν = k + ½ (k ≤ 3, closed forms of
+// the K_ν expression at covariance.cpp:53-62); other ν use the host setup.
+namespace {
+struct CovDev {
+  int family, half_k;
+  double sigma2, lambda, nu_or_p;
+};
+
+__device__ double cov_eval(const CovDev& c, double t0, double t1) {
+  if (c.family == OSC_COV_SEPARABLE_EXP) {
+    const double p = c.nu_or_p;
+    const double sm = pow(fabs(t0), p) + pow(fabs(t1), p);
+    return c.sigma2 * exp(-pow(sm, 1.0 / p) / c.lambda);
+  }
+  const double r = sqrt(t0 * t0 + t1 * t1);
+  if (r == 0.0) return c.sigma2;
+  const double x = sqrt(2.0 * c.nu_or_p) * r / c.lambda;
+  if (x < 1e-13) return c.sigma2;
+  // 2^{1−ν}/Γ(ν) x^ν K_ν(x) for ν = k + ½: e^{−x} · Σ_{i≤k} (k+i)!/(i!(k−i)!) (2x)^{k−i} · k!/(2k)!
+  double poly = 1.0;
+  if (c.half_k == 1) poly = 1.0 + x;
+  else if (c.half_k == 2) poly = 1.0 + x + x * x / 3.0;
+  else if (c.half_k == 3) poly = 1.0 + x + 2.0 * x * x / 5.0 + x * x * x / 15.0;
+  return c.sigma2 * poly * exp(-x);
+}
+
+__device__ double eta_d(double x) { return x > 0.0 ? exp(-1.0 / x) : 0.0; }
+__device__ double cutoff_phi_d(double t, double kappa) {  // covariance.cpp:87-95
+  const double a = fabs(t);
+  if (a <= 1.0) return 1.0;
+  if (a >= kappa) return 0.0;
+  const double up = eta_d((kappa - a) / (kappa - 1.0));
+  const double dn = eta_d((a - 1.0) / (kappa - 1.0));
+  return up / (up + dn);
+}
+
+// first-row table over the distinct displacements d ∈ [0, n/2]² (covariance.cpp:97-115 when padded)
+__global__ void first_row_tab_kernel(CovDev c, int m, int J, int h, double* __restrict__ tab) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)(h + 1) * (h + 1)) return;
+  const int d1 = (int)(i / (h + 1)), d0 = (int)(i - (int64_t)d1 * (h + 1));
+  const double x0 = static_cast<double>(d0) / m, x1 = static_cast<double>(d1) / m;
+  double v;
+  if (J == 0) {
+    v = cov_eval(c, x0, x1);
+  } else {
+    const double ell = 1.0 + static_cast<double>(J) / m, kappa = 2.0 * ell - 1.0, period = 2.0 * ell;
+    v = 0.0;
+    for (int n0 = -1; n0 <= 1; ++n0) {
+      const double s0 = x0 + period * n0;
+      for (int n1 = -1; n1 <= 1; ++n1) {
+        const double s1 = x1 + period * n1;
+        const double w = cutoff_phi_d(fmax(fabs(s0), fabs(s1)), kappa);
+        if (w > 0.0) v += w * cov_eval(c, s0, s1);
+      }
+    }
+  }
+  tab[i] = v;
+}
+
+// out[q1·n + q0] = scale · win[min(q1, n−q1)·(h+1) + min(q0, n−q0)] (h = n/2)
+__global__ void mirror_kernel(const double* __restrict__ win, int n, double scale, double* __restrict__ out) {
+  const int64_t s = (int64_t)n * n, h = n / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q1 = i / n, q0 = i - q1 * n;
+    const int64_t d1 = q1 <= h ? q1 : n - q1, d0 = q0 <= h ? q0 : n - q0;
+    out[i] = scale * win[d1 * (h + 1) + d0];
+  }
+}
+
+__global__ void fill_kernel(double* __restrict__ p, int64_t count, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+}  // namespace
+
+// Twiddle table tw[t] = exp(+2πi t/n) of a level (long-double angles, rounded once).
+void upload_twiddles(Level* L) {
+  std::vector<double> tw(2 * (size_t)L->n);
+  for (int t = 0; t < L->n; ++t) {
+    const long double a = 6.283185307179586476925286766559005768L * t / L->n;
+    tw[2 * (size_t)t] = (double)std::cos(a);
+    tw[2 * (size_t)t + 1] = (double)std::sin(a);
+  }
+  L->twiddle.ensure(sizeof(double) * tw.size());
+  OSC_CUDA(cudaMemcpy(L->twiddle.p, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
+}
+
+bool spectrum_device_supported(int family, double nu_or_p) {
+  if (family == OSC_COV_SEPARABLE_EXP) return true;
+  for (int k = 0; k <= 3; ++k)
+    if (nu_or_p == k + 0.5) return true;
+  return false;
+}
+
+std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double sigma2, double lambda,
+                                    double nu_or_p) {
+  CovDev c{family, (int)(nu_or_p - 0.5), sigma2, lambda, nu_or_p};
+  const int n = 2 * (m + J), h = n / 2;
+  const int64_t s = (int64_t)n * n, nw = (int64_t)(h + 1) * (h + 1);
+  cudaStream_t st = ctx->stream;
+  Level T;  // the CE level of the spectrum pass: window m' = n/2, √λ ≡ 1
+  T.ctx = ctx;
+  T.m = h;
+  T.J = 0;
+  T.n = n;
+  T.s = s;
+  DevBuf row, win, eig;
+  std::vector<double> out((size_t)s);
+  try {
+    T.sqrt_full.ensure(sizeof(double) * s);
+    row.ensure(sizeof(double) * s);
+    win.ensure(sizeof(double) * (nw + s));  // the window, then the tab of the first row
+    eig.ensure(sizeof(double) * s);
+    upload_twiddles(&T);
+    double* tab = win.as<double>() + nw;
+    {
+      KScope ks(ctx, "setup.first_row");
+      first_row_tab_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(c, m, J, h, tab);
+      OSC_CUDA(cudaGetLastError());
+      mirror_kernel<<<2048, 256, 0, st>>>(tab, n, 1.0, row.as<double>());
+      OSC_CUDA(cudaGetLastError());
+      fill_kernel<<<2048, 256, 0, st>>>(T.sqrt_full.as<double>(), s, 1.0);
+      OSC_CUDA(cudaGetLastError());
+    }
+    ce_sample_launch(ctx, &T, T.sqrt_full.as<double>(), row.as<double>(), 0, 0, 0, 1, false, win.as<double>(),
+                     nullptr, nullptr);
+    {
+      KScope ks(ctx, "setup.mirror");
+      mirror_kernel<<<2048, 256, 0, st>>>(win.as<double>(), n, static_cast<double>(n), eig.as<double>());
+      OSC_CUDA(cudaGetLastError());
+    }
+    OSC_CUDA(cudaMemcpyAsync(out.data(), eig.p, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    OSC_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    T.sqrt_full.release();
+    T.twiddle.release();
+    row.release();
+    win.release();
+    eig.release();
+    throw;
+  }
+  T.sqrt_full.release();
+  T.twiddle.release();
+  row.release();
+  win.release();
+  eig.release();
+  return out;
 }
 
 // Standalone NormalStream fill on device (osc_normals): out[b*s + e] = ξ_e of index0+b.

@@ -146,6 +146,12 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
                       uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
                       double* out_fine, double* out_coarse, int* bad_flag);
 size_t ce_inter_bytes(const Level* L, int count, int col_stride);
+void upload_twiddles(Level* L);
+// Level setup on the device (ce_sample.cu): raw spectrum (s = (2(m+J))² entries, host vector) of
+// the padding-J embedding; supported for separable exponential and Matérn ν = k + ½, k ≤ 3.
+bool spectrum_device_supported(int family, double nu_or_p);
+std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double sigma2, double lambda,
+                                    double nu_or_p);
 
 // Batched MG-PCG (mgpcg.cu). k (device, B*(m+1)^2) is consumed as level-0 conductivity.
 void solver_prepare(Ctx* ctx, int m, int B, int hist_cap);

@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -204,10 +205,23 @@ std::vector<double> spectrum(const std::vector<double>& row, int n) {
 
 }  // namespace
 
-// embedding.cpp:114-151
+// embedding.cpp:114-151; `attempt_spectrum(J)` returns the raw spectrum of the padding-J embedding
+// (host: first_row + spectrum below; device: ce_sample.cu spectrum_device).
+std::vector<double> build_spectrum_with(int m, int family, double sigma2, double lambda, double nu_or_p,
+                                        const double* fractions, int n_fractions, double tol_factor, int* J_out,
+                                        const std::function<std::vector<double>(int)>& attempt_spectrum);
+
 std::vector<double> build_spectrum(int m, int family, double sigma2, double lambda, double nu_or_p,
                                    const double* fractions, int n_fractions, double tol_factor,
                                    int* J_out) {
+  const Model mod{family, sigma2, lambda, nu_or_p};
+  return build_spectrum_with(m, family, sigma2, lambda, nu_or_p, fractions, n_fractions, tol_factor, J_out,
+                             [&](int J) { return spectrum(first_row(m, J, mod), 2 * (m + J)); });
+}
+
+std::vector<double> build_spectrum_with(int m, int family, double sigma2, double lambda, double nu_or_p,
+                                        const double* fractions, int n_fractions, double tol_factor, int* J_out,
+                                        const std::function<std::vector<double>(int)>& attempt_spectrum) {
   if (m < 1) throw SetupError{OSC_ERR_CONFIG, "GridSpec: resolution must be >= 1"};
   if (!(sigma2 > 0.0) || !std::isfinite(sigma2))
     throw SetupError{OSC_ERR_CONFIG, "CovarianceModel: sigma2 must be positive"};
@@ -222,14 +236,12 @@ std::vector<double> build_spectrum(int m, int family, double sigma2, double lamb
     n_fractions = 5;
   }
   if (!(tol_factor > 0.0)) tol_factor = 1e-12;
-  const Model mod{family, sigma2, lambda, nu_or_p};
   std::ostringstream tried;
   auto attempt = [&](int J) -> std::vector<double> {
     const int n = 2 * (m + J);
     if ((int64_t)n * n > (int64_t{1} << 28))
       throw SetupError{OSC_ERR_CONFIG, "build_first_row: embedding size exceeds the addressable limit"};
-    const auto row = first_row(m, J, mod);
-    auto eig = spectrum(row, n);
+    auto eig = attempt_spectrum(J);
     const double tol = tol_factor * static_cast<double>(eig.size()) * sigma2;
     const double mn = *std::min_element(eig.begin(), eig.end());
     tried << " J=" << J << "," << J << " (min eig " << mn << ")";

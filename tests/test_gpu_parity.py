@@ -132,6 +132,42 @@ np.savez(sys.argv[1], **out)
         assert relmax(res["new"][k], res["legacy"][k]) <= 1e-14, (k, relmax(res["new"][k], res["legacy"][k]))
 
 
+@pytest.mark.parametrize("m,model", [
+    (16, ("sep", 1.0, 0.1, 1.0)), (64, ("sep", 2.0, 0.03, 1.0)), (32, ("sep", 1.0, 0.2, 1.5)),
+    (64, ("matern", 1.0, 0.1, 0.5)), (256, ("matern", 2.0, 0.003, 0.5)), (128, ("matern", 1.0, 0.01, 1.5)),
+    (32, ("matern", 1.0, 0.05, 2.5)), (32, ("matern", 1.0, 0.05, 3.5)),
+    # padded (J > 0): the periodised first row on the device, mixed-radix spectrum pass
+    (16, ("matern", 1.0, 0.3, 1.5)), (8, ("matern", 1.0, 0.5, 2.5)),
+])
+def test_device_setup_matches_host(P, ctx, m, model):
+    """Level setup on the device: same J and eigenvalues as the host setup to
+    rounding, and the fields it drives agree with the host-setup fields to the field tolerance."""
+    api = P.api
+    cov = (api.CovarianceModel.separable_exponential(model[1], model[2], model[3]) if model[0] == "sep"
+           else api.CovarianceModel.matern(model[1], model[2], model[3]))
+    host = api.build_operator(api.GridSpec.square(m), cov)
+    dev = api.build_operator(api.GridSpec.square(m), cov, device=True, ctx=ctx)
+    assert dev.padding == host.padding and dev.n == host.n
+    assert relmax(dev.eigenvalues, host.eigenvalues) < 1e-12
+    fh = host.sample_fields(None, count=2, seed=4, ell=1, index0=3, fine=True, ctx=ctx)
+    fd = dev.sample_fields(None, count=2, seed=4, ell=1, index0=3, fine=True, ctx=ctx)
+    assert relmax(fd, fh) < FIELD_TOL
+
+
+def test_device_setup_config4_and_errors(P, ctx):
+    """Config-4 size (m = 2048, n = 4096) on the device matches the host spectrum; Matérn ν outside
+    k + ½ is refused with ConfigError (the host setup covers it)."""
+    api = P.api
+    cov = api.CovarianceModel.matern(2.0, 0.003, 0.5)
+    host = api.build_operator(api.GridSpec.square(2048), cov)
+    dev = api.build_operator(api.GridSpec.square(2048), cov, device=True, ctx=ctx)
+    assert dev.padding == host.padding == (0, 0)
+    assert relmax(dev.eigenvalues, host.eigenvalues) < 1e-12
+    with pytest.raises(api.ConfigError):
+        api.build_operator(api.GridSpec.square(16), api.CovarianceModel.matern(1.0, 0.1, 1.0), device=True,
+                           ctx=ctx)
+
+
 # ---- FEM (K3) -------------------------------------------------------------------------------------
 def test_solve_golden(P, ctx, golden):
     api = P.api

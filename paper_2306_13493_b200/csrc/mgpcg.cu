@@ -556,6 +556,9 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
       for (int ey = -1; ey <= 1; ++ey)
 #pragma unroll
         for (int ex = -1; ex <= 1; ++ex) {
+          if constexpr (L0K) {  // level 0 is 5-point: the corner couplings are exact zeros
+            if (ex != 0 && ey != 0) continue;
+          }
           const double a = ey < 0 ? (ex < 0 ? r.sw : ex == 0 ? r.s : r.se)
                                   : ey == 0 ? (ex < 0 ? r.w : ex == 0 ? r.c : r.e)
                                             : (ex < 0 ? r.nw : ex == 0 ? r.n : r.ne);

@@ -386,6 +386,28 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     if (xi_host && count >= 2)
       nchunks = std::max<int64_t>(nchunks, std::min<int64_t>(OSC_XI_CHUNKS, std::max<int64_t>(2, count / 8)));
     const int Bc = (int)((count + nchunks - 1) / nchunks);
+    // chunk schedule. Host ξ with large uniform chunks (≥ 256 MB of ξ each): a ramp — a small
+    // first chunk (its copy is the only exposed one), then each chunk ≤ OSC_XI_RAMP × the previous,
+    // so chunk i+1's copy still fits under chunk i's solves (copy ≈ 0.6 × solve per sample on
+    // cfg 4), capped at the uniform size Bc. Small ξ (cfg 1) keeps the uniform chunks: there the
+    // per-chunk launch overhead outweighs the exposed copy.
+    std::vector<std::pair<int64_t, int>> sched;
+    {
+      auto env_num = [](const char* k, double d) { const char* v = std::getenv(k); return v ? std::atof(v) : d; };
+      const double ramp = env_num("OSC_XI_RAMP", 1.35);
+      const int first_div = (int)env_num("OSC_XI_FIRST_DIV", 16);
+      const double min_mb = env_num("OSC_XI_RAMP_MIN_MB", 256);  // tests lower it to reach the ramp
+      int sz = Bc;
+      const bool big = sizeof(double) * (double)L->s * Bc >= min_mb * (1 << 20);
+      if (xi_host && big && first_div > 0 && ramp > 1.0 && count >= 16)
+        sz = (int)std::max<int64_t>(1, std::min<int64_t>(Bc, count / first_div));
+      for (int64_t a = 0; a < count;) {
+        const int nb = (int)std::min<int64_t>(sz, count - a);
+        sched.emplace_back(a, nb);
+        a += nb;
+        sz = std::min(Bc, std::max(sz + 1, (int)std::ceil(sz * ramp)));
+      }
+    }
     c->fields_fine.ensure(sizeof(double) * Nf * Bc);
     if (has_coarse) c->fields_coarse.ensure(sizeof(double) * Nc * Bc);
     c->out_q.ensure(sizeof(double) * 2 * Bc);
@@ -394,9 +416,9 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     if (xi_host) c->xi_dev.ensure(2 * sizeof(double) * L->s * Bc);
     auto xi_buf = [&](int64_t chunk) { return c->xi_dev.as<double>() + (chunk & 1) * L->s * Bc; };
     auto issue_copy = [&](int64_t chunk) {  // H2D of chunk `chunk` on the copy stream
-      const int64_t a = chunk * Bc;
-      if (a >= count) return;
-      const int64_t nb = std::min<int64_t>(Bc, count - a);
+      if (chunk >= (int64_t)sched.size()) return;
+      const int64_t a = sched[chunk].first;
+      const int64_t nb = sched[chunk].second;
       if (chunk >= 2)  // the CE of chunk-2 used this buffer
         OSC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_ce_done[chunk & 1], 0));
       OSC_CUDA(cudaMemcpyAsync(xi_buf(chunk), xi + a * L->s, sizeof(double) * L->s * nb,
@@ -415,10 +437,10 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     std::vector<int32_t> it_tmp(Bc), st_tmp(Bc), bad_tmp(Bc);
     // OSC_NO_NESTED=1: fine solve from the reference's Dirichlet lift (A/B)
     static const bool nested = std::getenv("OSC_NO_NESTED") == nullptr;
-    for (int64_t c0 = 0; c0 < count; c0 += Bc) {
-      const int B = (int)std::min<int64_t>(Bc, count - c0);
+    for (int64_t chunk = 0; chunk < (int64_t)sched.size(); ++chunk) {
+      const int64_t c0 = sched[chunk].first;
+      const int B = sched[chunk].second;
       const double* xi_chunk = nullptr;
-      const int64_t chunk = c0 / Bc;
       if (xi) {
         if (xi_host) {
           OSC_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[chunk & 1], 0));

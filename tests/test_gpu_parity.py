@@ -349,10 +349,12 @@ def test_level_draws_extensions_vs_port(P, ctx, port, bc, qoi):
     assert qrel(d.q_coarse[5:9], qc) < QOI_TOL
 
 
-@pytest.mark.parametrize("cnt", [7, 40])
-def test_host_xi_chunks_match_device_philox(P, ctx, cnt):
-    """Host-ξ draws run in up to 4 chunks (double-buffered H2D copies under the previous chunk's
-    solves); the device-Philox path runs one chunk. With the same ξ (NormalStream rows copied from
+@pytest.mark.parametrize("cnt,ramp", [(7, False), (40, False), (40, True)])
+def test_host_xi_chunks_match_device_philox(P, ctx, cnt, ramp, monkeypatch):
+    """Host-ξ draws run in chunks (double-buffered H2D copies under the previous chunk's solves;
+    with ≥ 256 MB uniform chunks and ≥ 16 samples a ramp of growing chunks, e.g. 2, 3, 5, 7, 10, 10,
+    3 at 40 — `ramp` lowers the size threshold to reach it here); the device-Philox
+    path runs one chunk. With the same ξ (NormalStream rows copied from
     the device) every slot is bit-identical."""
     import ctypes as C
     api = P.api
@@ -363,6 +365,8 @@ def test_host_xi_chunks_match_device_philox(P, ctx, cnt):
     frm = 11
     xi = np.empty((cnt, plan.op.s))
     assert P.lib().osc_normals(ctx.h, 9, 3, frm, cnt, plan.op.s, xi.ctypes.data_as(C.c_void_p)) == 0
+    if ramp:
+        monkeypatch.setenv("OSC_XI_RAMP_MIN_MB", "0")
     a, b = api.LevelDraws(), api.LevelDraws()
     cg = api.GridSpec.square(plan.grid.m(0) // 2)
     api.run_level_draws(plan, cg, False, False, prob, opt, frm, frm + cnt, a, ctx=ctx)

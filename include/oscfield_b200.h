@@ -122,6 +122,14 @@ const char* osc_last_error(void);
 /* The cudaStream_t (as void*) every kernel of this context is launched on. */
 void* osc_ctx_stream(osc_ctx* ctx);
 int osc_ctx_synchronize(osc_ctx* ctx);
+/* Cross-call ξ prefetch for a streaming caller (the reference's estimate_adaptive issues
+ * consecutive run_level_draws batches, estimators.cpp:304-369). Arms the host rows xi_next
+ * (count·s doubles, pinned for full overlap) of the NEXT host-ξ osc_level_draws call on this
+ * context: the following host-ξ call copies them to the device on the copy stream under its own
+ * solves, and the next call with exactly that pointer and count then runs as one batch without
+ * an exposed H2D copy. Any other pointer or count drops the prefetched rows (plain chunked path).
+ * Contract: xi_next stays valid and unchanged until that next call returns. NULL / 0 disarms. */
+int osc_ctx_prefetch_xi(osc_ctx* ctx, const double* xi_next, int64_t count);
 /* Device memory budget (bytes) for batch workspaces; 0 = 60% of free memory. */
 int osc_ctx_set_mem_budget(osc_ctx* ctx, size_t bytes);
 /* Per-kernel-class timing with CUDA events on the context stream (0 off / 1 on). */

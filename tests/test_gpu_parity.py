@@ -375,6 +375,47 @@ def test_host_xi_chunks_match_device_philox(P, ctx, cnt, ramp, monkeypatch):
     assert np.array_equal(a.iters_fine, b.iters_fine)
 
 
+def test_xi_prefetch_matches_device_philox(P, ctx):
+    """Cross-call ξ prefetch (osc_ctx_prefetch_xi): call 1 (chunked) copies call 2's rows under its
+    solves; call 2 (same array and count) runs as one batch from the prefetched rows (fewer
+    launches) and arms call 3; call 3 passes a different array, so the prefetched rows are dropped
+    and it runs chunked; a prefetch armed with another count is not used either. Every call is
+    bit-identical to the device-Philox draws."""
+    import ctypes as C
+    api = P.api
+    model = api.CovarianceModel.matern(1.0, 0.05, 0.5)
+    prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.L2Norm), bc=api.BC(0))
+    opt = api.EstimatorOptions(seed=4)
+    plan = api.make_level_plan(3, 1.0 / 16, prob, opt)
+    frm, cnt = 3, 24
+    xi = np.empty((cnt, plan.op.s))
+    assert P.lib().osc_normals(ctx.h, 4, 3, frm, cnt, plan.op.s, xi.ctypes.data_as(C.c_void_p)) == 0
+    other = xi.copy()
+    cg = api.GridSpec.square(plan.grid.m(0) // 2)
+    ref = api.LevelDraws()
+    api.run_level_draws(plan, cg, False, False, prob, opt, frm, frm + cnt, ref, ctx=ctx)
+
+    def call(x, x_next=None):
+        d = api.LevelDraws()
+        n0 = ctx.launch_count
+        api.run_level_draws(plan, cg, False, False, prob, opt, frm, frm + cnt, d, ctx=ctx, xi=x,
+                            xi_next=x_next)
+        ctx.synchronize()
+        assert np.array_equal(d.q_fine, ref.q_fine) and np.array_equal(d.q_coarse, ref.q_coarse)
+        assert np.array_equal(d.iters_fine, ref.iters_fine)
+        return ctx.launch_count - n0
+
+    n1 = call(xi, xi)      # chunked, prefetches call 2
+    n2 = call(xi, xi)      # whole batch from xi_pref, prefetches call 3
+    n3 = call(other)       # different pointer: prefetched rows dropped, chunked
+    assert n2 < n1 and n3 > n2
+    ctx.prefetch_xi(xi, cnt - 1)  # armed with another count: not used
+    n4 = call(xi)          # chunked (arms cnt-1 rows for a later call)
+    n5 = call(xi)          # the cnt-1 prefetch does not match this call: chunked
+    assert n5 > n2
+    ctx.prefetch_xi(None)
+
+
 @pytest.mark.parametrize("env", ["", "OSC_NESTED_SIMPLE=1", "OSC_NO_NESTED=1"])
 def test_nested_start_vs_port(P, port, env):
     """Coupled draws start the fine PCG from the prolonged coarse solution (marching init kernel for

@@ -350,7 +350,7 @@ def main():
     def step(k, xi=None, xi_next=None):
         frm = (k * world + rank) * B
         if xi_next is not None:  # cross-call prefetch: the next step's rows copy under this step
-            api._check(lib.osc_ctx_prefetch_xi(ctx.h, xi_next.ctypes.data_as(C.c_void_p), B))
+            api._check(lib.osc_level_prefetch_xi(lev.h, xi_next.ctypes.data_as(C.c_void_p), B))
         code = lib.osc_level_draws(lev.h, C.byref(ps), opt.seed, W["ell"], frm, frm + B, flags,
                                    None if xi is None else xi.ctypes.data_as(C.c_void_p),
                                    qf.ctypes.data, qc.ctypes.data, itf.ctypes.data, itc.ctypes.data,
@@ -480,7 +480,7 @@ def main():
         k_e2e = max(1, min(args.steps, 5))
         # warm the host-ξ paths (chunked + prefetch, then the prefetched whole batch); the first
         # timed step then copies its own rows (chunked), and step k copies step k+1's rows under
-        # its solves (osc_ctx_prefetch_xi), so all k_e2e steps' H2D copies lie inside the region
+        # its solves (osc_level_prefetch_xi), so all k_e2e steps' H2D copies lie inside the region
         step(2_000_000, xi=buf.array, xi_next=buf.array)
         step(2_000_001, xi=buf.array)
         if dist:
@@ -518,7 +518,7 @@ def main():
                "link_bound_samples_per_s": world * h2d_gbs * 1e9 / (8.0 * s),
                "note": "ξ (8 B per embedding entry per sample) crosses PCIe every step. Step 1 copies its own "
                        "rows in chunks (chunk i+1 under chunk i's solves); step k copies step k+1's rows under "
-                       "its solves (osc_ctx_prefetch_xi), so e2e ≈ min(device rate, link rate)"}
+                       "its solves (osc_level_prefetch_xi), so e2e ≈ min(device rate, link rate)"}
         buf.free()
 
     cpu = None

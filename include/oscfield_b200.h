@@ -122,14 +122,6 @@ const char* osc_last_error(void);
 /* The cudaStream_t (as void*) every kernel of this context is launched on. */
 void* osc_ctx_stream(osc_ctx* ctx);
 int osc_ctx_synchronize(osc_ctx* ctx);
-/* Cross-call ξ prefetch for a streaming caller (the reference's estimate_adaptive issues
- * consecutive run_level_draws batches, estimators.cpp:304-369). Arms the host rows xi_next
- * (count·s doubles, pinned for full overlap) of the NEXT host-ξ osc_level_draws call on this
- * context: the following host-ξ call copies them to the device on the copy stream under its own
- * solves, and the next call with exactly that pointer and count then runs as one batch without
- * an exposed H2D copy. Any other pointer or count drops the prefetched rows (plain chunked path).
- * Contract: xi_next stays valid and unchanged until that next call returns. NULL / 0 disarms. */
-int osc_ctx_prefetch_xi(osc_ctx* ctx, const double* xi_next, int64_t count);
 /* Device memory budget (bytes) for batch workspaces; 0 = 60% of free memory. */
 int osc_ctx_set_mem_budget(osc_ctx* ctx, size_t bytes);
 /* Per-kernel-class timing with CUDA events on the context stream (0 off / 1 on). */
@@ -172,6 +164,17 @@ int osc_build_spectrum_device(osc_ctx* ctx, int m, int family, double sigma2, do
  * (embedding.cpp:105-110,153-163). k_trunc = 0 → no truncated copy. */
 int osc_level_create(osc_ctx* ctx, int m, int J, const double* eigenvalues, int64_t k_trunc,
                      osc_level** out);
+
+/* Cross-call ξ prefetch for a streaming caller (the reference's estimate_adaptive issues
+ * consecutive run_level_draws batches, estimators.cpp:304-369). Arms the host rows xi_next
+ * (count·s doubles, s = next_level's embedding size; pinned for full overlap) of the NEXT host-ξ
+ * osc_level_draws call on next_level: the following host-ξ call on the same context copies them
+ * to the device on the copy stream under its own solves, and the call on next_level with exactly
+ * that pointer and count then runs as one batch without an exposed H2D copy. Any other pointer,
+ * count or embedding size drops the prefetched rows (plain chunked path). Contract: xi_next holds
+ * count·s doubles and stays valid and unchanged until that next call returns. NULL / 0 disarms.
+ * No reference counterpart. */
+int osc_level_prefetch_xi(osc_level* next_level, const double* xi_next, int64_t count);
 void osc_level_destroy(osc_level* level);
 /* m, J, n, s and k_trunc of a level. */
 int osc_level_info(const osc_level* level, int* m, int* J, int* n, int64_t* s, int64_t* k_trunc);

@@ -34,10 +34,10 @@ CE_TRUNCATED, CE_EXP, CE_FINE, CE_COARSE, CE_DEVICE_OUT, CE_XI_DEVICE = 1, 2, 4,
 # every symbol the header declares (checked by tests/test_abi.py against the header text)
 EXPORTS = [
     "osc_ctx_create", "osc_ctx_destroy", "osc_last_error", "osc_ctx_stream", "osc_ctx_synchronize",
-    "osc_ctx_set_mem_budget", "osc_ctx_prefetch_xi", "osc_ctx_set_profiling", "osc_ctx_profile_only", "osc_ctx_kernel_stats", "osc_ctx_reset_stats",
+    "osc_ctx_set_mem_budget", "osc_ctx_set_profiling", "osc_ctx_profile_only", "osc_ctx_kernel_stats", "osc_ctx_reset_stats",
     "osc_ctx_launch_count", "osc_host_alloc", "osc_host_free", "osc_free", "osc_build_spectrum",
     "osc_build_spectrum_device",
-    "osc_level_create", "osc_level_destroy", "osc_level_info", "osc_level_draws", "osc_summarize",
+    "osc_level_create", "osc_level_prefetch_xi", "osc_level_destroy", "osc_level_info", "osc_level_draws", "osc_summarize",
     "osc_normals", "osc_ce_sample", "osc_darcy_solve", "osc_qoi",
 ]
 
@@ -85,7 +85,7 @@ def lib() -> C.CDLL:
     L.osc_ctx_stream.restype = vp
     L.osc_ctx_synchronize.argtypes = [vp]
     L.osc_ctx_set_mem_budget.argtypes = [vp, C.c_size_t]
-    L.osc_ctx_prefetch_xi.argtypes = [vp, vp, i64]
+    L.osc_level_prefetch_xi.argtypes = [vp, vp, i64]
     L.osc_ctx_set_profiling.argtypes = [vp, ip]
     L.osc_ctx_profile_only.argtypes = [vp, C.c_char_p]
     L.osc_ctx_kernel_stats.argtypes = [vp, ip, C.POINTER(C.c_char_p), C.POINTER(i64),

@@ -169,20 +169,6 @@ class Context:
         """Time only `kernel_class` (events around its launches); None times every class."""
         _check(self._lib.osc_ctx_profile_only(self.h, kernel_class.encode() if kernel_class else None))
 
-    def prefetch_xi(self, xi_next: Optional[np.ndarray], count: Optional[int] = None):
-        """osc_ctx_prefetch_xi: arm the host ξ rows of the NEXT host-ξ draw call on this context
-        (copied under the following call's solves). xi_next must be a C-contiguous float64 array
-        (pinned for full overlap) that stays unchanged until that next call returns; None disarms."""
-        if xi_next is None:
-            self._xi_next = None
-            _check(self._lib.osc_ctx_prefetch_xi(self.h, None, 0))
-            return
-        if xi_next.dtype != np.float64 or not xi_next.flags["C_CONTIGUOUS"]:
-            raise ConfigError("prefetch_xi: xi_next must be a C-contiguous float64 array")
-        cnt = int(xi_next.shape[0]) if count is None else int(count)
-        self._xi_next = xi_next  # held until the next prefetch / disarm
-        _check(self._lib.osc_ctx_prefetch_xi(self.h, xi_next.ctypes.data_as(C.c_void_p), cnt))
-
     def set_mem_budget(self, nbytes: int):
         _check(self._lib.osc_ctx_set_mem_budget(self.h, int(nbytes)))
 
@@ -355,6 +341,23 @@ class DeviceLevel:
                 self.h = None
         except Exception:
             pass
+
+    def prefetch_xi(self, xi_next: Optional[np.ndarray], count: Optional[int] = None):
+        """osc_level_prefetch_xi: arm the host ξ rows of the NEXT host-ξ draw call on this level
+        (copied under the following call's solves). xi_next must be a C-contiguous float64 array
+        of at least count·s values (pinned for full overlap) that stays unchanged until that next
+        call returns; None disarms."""
+        if xi_next is None:
+            self._xi_next = None
+            _check(self._lib.osc_level_prefetch_xi(self.h, None, 0))
+            return
+        if xi_next.dtype != np.float64 or not xi_next.flags["C_CONTIGUOUS"]:
+            raise ConfigError("prefetch_xi: xi_next must be a C-contiguous float64 array")
+        cnt = xi_next.size // self.s if count is None else int(count)
+        if cnt < 0 or cnt * self.s > xi_next.size:
+            raise ConfigError("prefetch_xi: xi_next holds fewer than count*s values")
+        self._xi_next = xi_next  # held until the next prefetch / disarm
+        _check(self._lib.osc_level_prefetch_xi(self.h, xi_next.ctypes.data_as(C.c_void_p), cnt))
 
     def sample_fields(self, xi=None, *, count=None, seed=1, ell=0, index0=0, fine=True, coarse=False,
                       exp=False, truncated=False):
@@ -687,7 +690,7 @@ def run_level_draws(plan: LevelPlan, coarse_grid: Optional[GridSpec], truncate_f
                     dist=None) -> LevelDraws:
     """run_level_draws (estimators.hpp:112-118): samples [frm, to) land in slots [frm, to) of
     `draws`; sample i uses NormalStream(opt.seed, ℓ, i) (or row i-frm of xi). `xi_next` (host
-    ξ of the caller's next batch, see Context.prefetch_xi) is copied under this call's solves,
+    ξ of the caller's next batch, see DeviceLevel.prefetch_xi) is copied under this call's solves,
     so the next call with that array runs without an exposed H2D copy. With `dist`
     (paper_2306_13493_b200.dist.Shard) the range is split into contiguous per-rank shards and
     the slots are all-gathered, so every rank ends with identical draws."""
@@ -715,7 +718,7 @@ def run_level_draws(plan: LevelPlan, coarse_grid: Optional[GridSpec], truncate_f
     if xi is not None:
         xi_arr = np.ascontiguousarray(xi, dtype=np.float64).reshape(cnt, plan.op.s)
     if xi_next is not None:
-        ctx.prefetch_xi(xi_next)
+        lev.prefetch_xi(xi_next)
     ps = _problem_struct(problem, opt.solver)
     t0 = time.perf_counter()
     code = L.lib().osc_level_draws(lev.h, C.byref(ps), int(opt.seed), int(plan.ell), int(frm),

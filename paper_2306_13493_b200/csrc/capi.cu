@@ -194,12 +194,15 @@ int osc_ctx_synchronize(osc_ctx* c) {
   });
 }
 
-int osc_ctx_prefetch_xi(osc_ctx* c, const double* xi_next, int64_t count) {
+int osc_level_prefetch_xi(osc_level* next_level, const double* xi_next, int64_t count) {
   return guarded([&] {
-    OSC_REQUIRE(c, "osc_ctx_prefetch_xi: null context");
-    OSC_REQUIRE(count >= 0, "osc_ctx_prefetch_xi: negative count");
-    c->next_xi = count > 0 ? xi_next : nullptr;
-    c->next_count = count > 0 && xi_next ? count : 0;
+    OSC_REQUIRE(next_level && next_level->ctx, "osc_level_prefetch_xi: null level");
+    OSC_REQUIRE(count >= 0, "osc_level_prefetch_xi: negative count");
+    Ctx* c = next_level->ctx;
+    const bool on = count > 0 && xi_next != nullptr;
+    c->next_xi = on ? xi_next : nullptr;
+    c->next_count = on ? count : 0;
+    c->next_s = on ? next_level->s : 0;
   });
 }
 
@@ -390,9 +393,9 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     size_t per = sizeof(double) * (Nf + (has_coarse ? Nc : 0)) + ce_inter_bytes(L, 1, 1) +
                  solver_bytes(m, 1, 0) + 64;
     if (xi_host) per += sizeof(double) * L->s;
-    // cross-call prefetch (osc_ctx_prefetch_xi): this call's rows may already be resident in
+    // cross-call prefetch (osc_level_prefetch_xi): this call's rows may already be resident in
     // xi_pref (copied under the previous call's solves), and the next call's rows may be armed
-    const bool arm = xi_host && c->next_xi != nullptr && c->next_count > 0;
+    const bool arm = xi_host && c->next_xi != nullptr && c->next_count > 0 && c->next_s > 0;
     const bool pref_hit = xi_host && c->pref_xi == xi && c->pref_count == count && c->pref_s == L->s;
     if (xi_host && !pref_hit) c->pref_xi = nullptr;  // stale rows: dropped (the copy stream orders reuse)
     if (arm || pref_hit) per += sizeof(double) * L->s;
@@ -452,7 +455,7 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     // copies and after this call's last read of xi_pref (ev_pref_read)
     auto issue_prefetch = [&] {
       if (!arm) return;
-      const size_t bytes = sizeof(double) * L->s * c->next_count;
+      const size_t bytes = sizeof(double) * c->next_s * c->next_count;
       if (c->xi_pref.bytes < bytes) {
         OSC_CUDA(cudaStreamSynchronize(c->copy_stream));
         c->xi_pref.ensure(bytes);
@@ -462,9 +465,10 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
       OSC_CUDA(cudaEventRecord(c->ev_pref, c->copy_stream));
       c->pref_xi = c->next_xi;
       c->pref_count = c->next_count;
-      c->pref_s = L->s;
+      c->pref_s = c->next_s;
       c->next_xi = nullptr;
       c->next_count = 0;
+      c->next_s = 0;
     };
     if (xi_chunked) {
       issue_copy(0);

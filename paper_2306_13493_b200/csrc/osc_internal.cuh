@@ -125,10 +125,10 @@ struct Ctx {
   cudaStream_t copy_stream = nullptr;           // host-ξ H2D overlapped with the previous chunk's solve
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_ce_done[2] = {nullptr, nullptr};
-  // cross-call ξ prefetch (osc_ctx_prefetch_xi): the armed host rows of the NEXT osc_level_draws
+  // cross-call ξ prefetch (osc_level_prefetch_xi): the armed host rows of the NEXT osc_level_draws
   // call are copied into xi_pref on the copy stream under this call's solves
   const double* next_xi = nullptr;
-  int64_t next_count = 0;
+  int64_t next_count = 0, next_s = 0;  // rows and embedding size s of the armed level
   const double* pref_xi = nullptr;  // rows resident (or in flight, ev_pref) in xi_pref
   int64_t pref_count = 0, pref_s = 0;
   DevBuf xi_pref;

@@ -376,7 +376,7 @@ def test_host_xi_chunks_match_device_philox(P, ctx, cnt, ramp, monkeypatch):
 
 
 def test_xi_prefetch_matches_device_philox(P, ctx):
-    """Cross-call ξ prefetch (osc_ctx_prefetch_xi): call 1 (chunked) copies call 2's rows under its
+    """Cross-call ξ prefetch (osc_level_prefetch_xi): call 1 (chunked) copies call 2's rows under its
     solves; call 2 (same array and count) runs as one batch from the prefetched rows (fewer
     launches) and arms call 3; call 3 passes a different array, so the prefetched rows are dropped
     and it runs chunked; a prefetch armed with another count is not used either. Every call is
@@ -409,11 +409,14 @@ def test_xi_prefetch_matches_device_philox(P, ctx):
     n2 = call(xi, xi)      # whole batch from xi_pref, prefetches call 3
     n3 = call(other)       # different pointer: prefetched rows dropped, chunked
     assert n2 < n1 and n3 > n2
-    ctx.prefetch_xi(xi, cnt - 1)  # armed with another count: not used
+    lev = plan.op.device_level(ctx, plan.k_trunc)
+    with pytest.raises(api.ConfigError):
+        lev.prefetch_xi(xi[:2], cnt)  # fewer than count*s values
+    lev.prefetch_xi(xi, cnt - 1)  # armed with another count: not used
     n4 = call(xi)          # chunked (arms cnt-1 rows for a later call)
     n5 = call(xi)          # the cnt-1 prefetch does not match this call: chunked
     assert n5 > n2
-    ctx.prefetch_xi(None)
+    lev.prefetch_xi(None)
 
 
 @pytest.mark.parametrize("env", ["", "OSC_NESTED_SIMPLE=1", "OSC_NO_NESTED=1"])

@@ -1170,13 +1170,14 @@ struct PairCtx {
 // Per-warp context; `interior` = every node this warp-chunk touches (rows y0−2 … y1+2, columns
 // xa(lane 0)−1 … xb(lane 31)+1) is an in-grid non-Dirichlet node with in-grid neighbours, so the
 // warp can run the branch-free body.
-#define PAIR_PROLOGUE                                                                   \
+#define PAIR_PROLOGUE PAIR_PROLOGUE_W(MW)
+#define PAIR_PROLOGUE_W(WPB)                                                            \
   const int b = blockIdx.z;                                                             \
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                                          \
   PairCtx c;                                                                            \
   {                                                                                     \
     const int lane = threadIdx.x & 31;                                                  \
-    const int strip = blockIdx.x * MW + (threadIdx.x >> 5);                             \
+    const int strip = blockIdx.x * (WPB) + (threadIdx.x >> 5);                          \
     const int ly = rows_per_warp(g.m);                                                  \
     c.b = b;                                                                            \
     c.lane = lane;                                                                      \
@@ -1190,7 +1191,7 @@ struct PairCtx {
     c.y1 = min(c.y0 + ly, g.n0);                                                        \
     c.off = (int64_t)b * g.N;                                                           \
   }                                                                                     \
-  const int strip0 = blockIdx.x * MW + (threadIdx.x >> 5);                              \
+  const int strip0 = blockIdx.x * (WPB) + (threadIdx.x >> 5);                           \
   const bool interior = strip0 * 60 - 2 >= 2 && strip0 * 60 + 61 <= g.m - 2 &&          \
                         c.y0 >= 3 && c.y1 <= g.m - 2;
 
@@ -1780,11 +1781,16 @@ __device__ __forceinline__ double diag_b(const S9& B, Pair vm, Pair vp) {
   return B.ne * shdn(vp.a) + B.nw * vp.a + B.se * shdn(vm.a) + B.sw * vm.a;
 }
 
-#define C9_PROLOGUE                                                                   \
+#ifndef OSC_CU_W
+#define OSC_CU_W 1
+#endif
+constexpr int CU_W = OSC_CU_W;  // warps per CTA of the coarse ring up sweep
+#define C9_PROLOGUE C9_PROLOGUE_W(MW)
+#define C9_PROLOGUE_W(WPB)                                                            \
   const int b = blockIdx.z;                                                           \
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;                                        \
   const int lane = threadIdx.x & 31;                                                  \
-  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);                             \
+  const int strip = blockIdx.x * (WPB) + (threadIdx.x >> 5);                          \
   const int m = L.m, n0 = L.n0;                                                       \
   const int xa = strip * 60 - 2 + 2 * lane, xb = xa + 1;                              \
   const bool outa = lane >= 1 && lane < 31 && xa <= m;                                \
@@ -2063,18 +2069,18 @@ enum { UP_C = 0, UP_E = 1, UP_N = 2, UP_NE = 3, UP_NW = 4, UP_R = 5, UP_Z = 6 };
 #endif
 constexpr int UP_RING = OSC_UP_RING;  // rows staged per warp: 3 × 4 warps × 582 × 8 B = 55.9 KB (RZ); 3 CTAs per SM at ≤ 170 registers (A/B: faster than 4 CTAs at 128)
 template <bool RZ>
-constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * MW * UpLayout<RZ>::WORDS; }
+constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * CU_W * UpLayout<RZ>::WORDS; }
 
 // Prolongation + post-smoother, ring-staged (same algorithm as c_up_march_kernel; pending smoother
 // rows carry partial sums). RZ: the pre-smoothed z is recomputed from r and the operator (red z =
 // r/C, black z = (r − Σ_WENS a z_red)/C, as c_pre_march_kernel) instead of loaded, so the down
 // sweep need not store it.
 template <bool RZ>
-__global__ void __launch_bounds__(MT, OSC_UP_MINB) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+__global__ void __launch_bounds__(32 * CU_W, OSC_UP_MINB * 4 / CU_W) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                           const double* __restrict__ z, PW4 pw, Geo gc,
                                                           const double* __restrict__ zc, double* __restrict__ z2,
                                                           const int* flags) {
-  C9_PROLOGUE
+  C9_PROLOGUE_W(CU_W)
   using LY = UpLayout<RZ>;
   extern __shared__ __align__(16) double ring[];
   const int warp = threadIdx.x >> 5;
@@ -2084,7 +2090,7 @@ __global__ void __launch_bounds__(MT, OSC_UP_MINB) c_up_ring_kernel(L9 L, int bc
   const int64_t cb0 = (int64_t)b * mcl * mcl;
   const double* arr[7] = {L.C + off, L.E + off, L.N + off, L.NE + off, L.NW + off, rb, zb};
   auto slot = [&](int y) {
-    return ring + ((size_t)((unsigned)(y - (y0 - 4)) % UP_RING) * MW + warp) * LY::WORDS;
+    return ring + ((size_t)((unsigned)(y - (y0 - 4)) % UP_RING) * CU_W + warp) * LY::WORDS;
   };
   // stage row y into its slot (off-grid values are zero-filled); rows past the last one the chunk
   // reads are skipped (their groups stay empty)
@@ -2298,16 +2304,20 @@ __global__ void __launch_bounds__(MT, OSC_UP_MINB) c_up_ring_kernel(L9 L, int bc
 // weights of the odd rows are loaded into registers one row pair ahead.
 enum { DN_C = 0, DN_E = 1, DN_N = 2, DN_NE = 3, DN_NW = 4, DN_R = 5, DN_WORDS = 6 * 64 };
 constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 4 × 4 warps × 384 × 8 B = 48 KB
-constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * MW * DN_WORDS;
+#ifndef OSC_CD_W
+#define OSC_CD_W 4
+#endif
+constexpr int CD_W = OSC_CD_W;  // warps per CTA of the coarse ring down sweep
+constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * CD_W * DN_WORDS;
 
-__global__ void __launch_bounds__(MT, 4) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+__global__ void __launch_bounds__(32 * CD_W, 16 / CD_W) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                             PW4 pw, Geo gc, double* __restrict__ rc,
                                                             const int* flags) {
   const int b = blockIdx.z;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
   extern __shared__ __align__(16) double ring[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int strip = blockIdx.x * MW + warp;
+  const int strip = blockIdx.x * CD_W + warp;
   const int I = strip * 30 - 1 + lane;
   const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
   const int lyc = coarse_rows_per_warp(gc.m);
@@ -2320,7 +2330,7 @@ __global__ void __launch_bounds__(MT, 4) c_down_ring_kernel(L9 L, int bc, int op
   const int ys = 2 * J0 - 1;
   const int ylast = 2 * J1 + 1;  // residual rows end at 2J1 − 1; their z needs raw rows up to 2J1 + 1
   auto slot = [&](int y) {
-    return ring + ((size_t)((unsigned)(y - (ys - 2)) % DN_RING) * MW + warp) * DN_WORDS;
+    return ring + ((size_t)((unsigned)(y - (ys - 2)) % DN_RING) * CD_W + warp) * DN_WORDS;
   };
   auto issue = [&](int y) {
     if (y > ylast) return;
@@ -2465,8 +2475,22 @@ __global__ void __launch_bounds__(MT, 4) c_down_ring_kernel(L9 L, int bc, int op
 enum { L0R_K = 0, L0R_R = 64, L0R_ZC0 = 128, L0R_ZC1 = 161, L0R_PW = 194 };
 constexpr int L0R_WORDS_UP = 322, L0R_WORDS_DN = 128;
 constexpr int L0R_RING = 5;
-constexpr size_t L0R_SMEM_UP = sizeof(double) * L0R_RING * MW * L0R_WORDS_UP;  // 51.5 KB
-constexpr size_t L0R_SMEM_DN = sizeof(double) * L0R_RING * MW * L0R_WORDS_DN;  // 20.5 KB
+// Warps (strips) per CTA of the ring sweeps (A/B knobs; the other march kernels use MW). One-warp
+// CTAs let the SM refill a warp slot as soon as that warp's strip is done, instead of holding it
+// until the slowest of four finishes (end-of-kernel barrier stalls were 14–19% of the samples of
+// the 4-warp up sweep). Config 4 per step: smooth_up 37.6 → 31.6 ms, restrict 23.8 → 20.4 ms,
+// coarse up 20.6 → 19.3 ms (2048² solve); the coarse down sweep is slower with one warp
+// (16.0 → 21.4 ms) and keeps four.
+#ifndef OSC_SUR_W
+#define OSC_SUR_W 1
+#endif
+constexpr int SUR_W = OSC_SUR_W;
+#ifndef OSC_RR_W
+#define OSC_RR_W 1
+#endif
+constexpr int RR_W = OSC_RR_W;  // level-0 ring restriction
+constexpr size_t L0R_SMEM_UP = sizeof(double) * L0R_RING * SUR_W * L0R_WORDS_UP;  // 51.5 KB at 4 warps
+constexpr size_t L0R_SMEM_DN = sizeof(double) * L0R_RING * RR_W * L0R_WORDS_DN;  // 20.5 KB
 
 // stage k and r of fine row y (columns x0 … x0+63) into S; off-grid values are zero
 __device__ __forceinline__ void l0_issue_kr(double* S, const double* kb, const double* rb, int x0, int lane, int y,
@@ -2495,7 +2519,7 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   const double *kb = k + off, *rb = r + off;
   const int ys = 2 * J0 - 1;
   const int ylast = 2 * J1 + 2;  // ingest rows end at 2J1+1, whose edges read k of row 2J1+2
-  auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (ys - 3)) % L0R_RING) * (MW * L0R_WORDS_DN); };
+  auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (ys - 3)) % L0R_RING) * (RR_W * L0R_WORDS_DN); };
   auto issue = [&](int q) {
     if (q <= ylast) l0_issue_kr(slot(q), kb, rb, x0, lane, q, n0);
     cpa_commit();
@@ -2573,14 +2597,14 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   cpa_wait<0>();
 }
 
-__global__ void __launch_bounds__(MT, 4) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(32 * RR_W, 16 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                               const double* __restrict__ r, PW4 pw,
                                                               double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
   extern __shared__ __align__(16) double l0ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int strip = blockIdx.x * MW + warp;
+  const int strip = blockIdx.x * RR_W + warp;
   const int I = strip * 30 - 1 + lane;
   const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
   const int lyc = coarse_rows_per_warp(gc.m);
@@ -2606,7 +2630,7 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
   const int ylast = y1 + 2;
-  auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (y0 - 3)) % L0R_RING) * (MW * L0R_WORDS_UP); };
+  auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (y0 - 3)) % L0R_RING) * (SUR_W * L0R_WORDS_UP); };
   auto issue = [&](int q) {
     if (q <= ylast) {
       double* S = slot(q);
@@ -2734,13 +2758,13 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
 #ifndef OSC_SURR_MINB
 #define OSC_SURR_MINB 3
 #endif
-__global__ void __launch_bounds__(MT, OSC_SURR_MINB) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(32 * SUR_W, OSC_SURR_MINB * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                                const double* __restrict__ r,
                                                                double* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,
                                                                int* flags, double2* partial, int maxp,
                                                                unsigned* counter) {
-  PAIR_PROLOGUE
+  PAIR_PROLOGUE_W(SUR_W)
   extern __shared__ __align__(16) double l0ring[];
   double* wring = l0ring + (threadIdx.x >> 5) * L0R_WORDS_UP;
   const bool interior3 = interior && c.y1 <= g.m - 3;
@@ -3709,9 +3733,17 @@ inline dim3 restrict_grid(int mc, int B) {
   const int lyc = coarse_rows_per_warp(mc);
   return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + lyc - 1) / lyc), (unsigned)B);
 }
+inline dim3 restrict_grid_w(int mc, int B, int wpb) {
+  const int lyc = coarse_rows_per_warp(mc);
+  return dim3((unsigned)(((mc + 1 + 29) / 30 + wpb - 1) / wpb), (unsigned)((mc + 1 + lyc - 1) / lyc), (unsigned)B);
+}
+inline dim3 march_grid_w(int m, int B, int wpb) {
+  const int ly = rows_per_warp(m);
+  return dim3((unsigned)((march_strips(m) + wpb - 1) / wpb), (unsigned)((m + 1 + ly - 1) / ly), (unsigned)B);
+}
 inline int64_t tile_parts(int m) {
-  const dim3 a = march_grid(m, 1, 1), b = march_grid(m, 2, 1);
-  return std::max<int64_t>((int64_t)a.x * a.y, (int64_t)b.x * b.y);
+  const dim3 a = march_grid(m, 1, 1), b = march_grid(m, 2, 1), c = march_grid_w(m, 1, SUR_W);
+  return std::max<int64_t>(std::max<int64_t>((int64_t)a.x * a.y, (int64_t)b.x * b.y), (int64_t)c.x * c.y);
 }
 
 }  // namespace
@@ -3890,7 +3922,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     if (l == 0) {
       KScope ks(ctx, pcg_one_reduction() ? "mg_restrict_r.L0" : "mg_restrict.L0");
       if (pcg_one_reduction() && l0_ring())
-        restrict_ring_kernel<<<restrict_grid(C.m, B), MT, L0R_SMEM_DN, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur,
+        restrict_ring_kernel<<<restrict_grid_w(C.m, B, RR_W), 32 * RR_W, L0R_SMEM_DN, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur,
                                                                            pw_of(L), C.r, w.flags);
       else if (pcg_one_reduction())
         restrict_r_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, pw_of(L),
@@ -3922,7 +3954,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
         attr = true;
       }
       KScope ks(ctx, lvl_name("mg_down", l).c_str());
-      c_down_ring_kernel<<<restrict_grid(C.m, B), MT, DN_RING_SMEM, st>>>(l9, bc, w.opdep, L.r, pw_of(L),
+      c_down_ring_kernel<<<restrict_grid_w(C.m, B, CD_W), 32 * CD_W, DN_RING_SMEM, st>>>(l9, bc, w.opdep, L.r, pw_of(L),
                                                                           geo_of(C), C.r, w.flags);
       continue;
     }
@@ -3954,7 +3986,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     if (l == 0) {
       KScope ks(ctx, pcg_one_reduction() ? "mg_smooth_up_r.L0" : "mg_smooth_up.L0");
       if (pcg_one_reduction() && l0_ring())
-        smooth_up_ring_kernel<<<march_grid(L.m, 2, B), MT, L0R_SMEM_UP, st>>>(
+        smooth_up_ring_kernel<<<march_grid_w(L.m, B, SUR_W), 32 * SUR_W, L0R_SMEM_UP, st>>>(
             geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2, C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
             w.counter);
       else if (pcg_one_reduction())
@@ -3997,7 +4029,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
                                       (int)up_ring_smem<false>()));
         attr = true;
       }
-      c_up_ring_kernel<false><<<march_grid(L.m, 2, B), MT, up_ring_smem<false>(), st>>>(
+      c_up_ring_kernel<false><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<false>(), st>>>(
           l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
     } else {
       static bool attr = false;
@@ -4006,7 +4038,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
                                       (int)up_ring_smem<true>()));
         attr = true;
       }
-      c_up_ring_kernel<true><<<march_grid(L.m, 2, B), MT, up_ring_smem<true>(), st>>>(
+      c_up_ring_kernel<true><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<true>(), st>>>(
           l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
     }
     if (dbg) {

@@ -169,6 +169,17 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def wait_ready(self, timeout: float = 10.0):
+        """Block until nvidia-smi has produced its first row: its NVML start-up (hundreds of ms,
+        driver calls) then lies before the timed region instead of stalling its first step."""
+        t0 = time.perf_counter()
+        while self.proc and not self.rows and self.proc.poll() is None and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self):
+        """Start of the timed region: only rows sampled from here on are reported."""
+        self.rows = []
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -380,11 +391,13 @@ def main():
     iters_total[:] = [0, 0]
     launches0 = ctx.launch_count
     clocks = ClockSampler(local)
+    clocks.start()
+    clocks.wait_ready()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ctx.synchronize()
-    clocks.start()
+    clocks.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.steps):
@@ -617,11 +630,13 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
     ctx.reset_stats()
     launches0 = ctx.launch_count
     clocks = ClockSampler(local)
+    clocks.start()
+    clocks.wait_ready()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ctx.synchronize()
-    clocks.start()
+    clocks.mark()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.steps):

@@ -1330,7 +1330,11 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
   return rr;
 }
 
-__global__ void __launch_bounds__(MT, 4) pcg_update_cg_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
+#ifndef OSC_PU_W
+#define OSC_PU_W 4
+#endif
+constexpr int PU_W = OSC_PU_W;  // warps per CTA of pcg_update (A/B knob: 1 and 2 warps are no faster, it is DRAM-bound)
+__global__ void __launch_bounds__(32 * PU_W, 16 / PU_W) pcg_update_cg_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
                                                               const double* __restrict__ z,
                                                               const double* __restrict__ p_old,
                                                               double* __restrict__ p_new, double* __restrict__ u,
@@ -1338,7 +1342,7 @@ __global__ void __launch_bounds__(MT, 4) pcg_update_cg_kernel(Geo g, int bc, dou
                                                               double* scal, int* flags, double2* partial, int maxp,
                                                               unsigned* counter, int* n_active, double* hist,
                                                               int hist_cap) {
-  PAIR_PROLOGUE
+  PAIR_PROLOGUE_W(PU_W)
   const double rr = interior ? pcg_update_cg_body<true>(g, bc, k, z, p_old, p_new, u, r, r_out, scal, flags, c)
                              : pcg_update_cg_body<false>(g, bc, k, z, p_old, p_new, u, r, r_out, scal, flags, c);
   double t0, t1;
@@ -3742,8 +3746,10 @@ inline dim3 march_grid_w(int m, int B, int wpb) {
   return dim3((unsigned)((march_strips(m) + wpb - 1) / wpb), (unsigned)((m + 1 + ly - 1) / ly), (unsigned)B);
 }
 inline int64_t tile_parts(int m) {
-  const dim3 a = march_grid(m, 1, 1), b = march_grid(m, 2, 1), c = march_grid_w(m, 1, SUR_W);
-  return std::max<int64_t>(std::max<int64_t>((int64_t)a.x * a.y, (int64_t)b.x * b.y), (int64_t)c.x * c.y);
+  const dim3 a = march_grid(m, 1, 1), b = march_grid(m, 2, 1), c = march_grid_w(m, 1, SUR_W),
+             d = march_grid_w(m, 1, PU_W);
+  return std::max<int64_t>(std::max<int64_t>((int64_t)a.x * a.y, (int64_t)b.x * b.y),
+                           std::max<int64_t>((int64_t)c.x * c.y, (int64_t)d.x * d.y));
 }
 
 }  // namespace
@@ -4215,7 +4221,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
       {
         KScope ks(ctx, "pcg_update");
         double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
-        pcg_update_cg_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, L0.z2, p_old, p_new,
+        pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, st>>>(g0, bc, prob->tol, L0.k, L0.z2, p_old, p_new,
                                                                     w.u, w.r_cur, r_next, w.scal, w.flags, part,
                                                                     w.max_parts, w.counter, w.n_active, w.hist,
                                                                     w.hist_cap);

@@ -1,0 +1,10 @@
+# A/B: warps per CTA of pcg_update (OSC_PU_W 4 / 2 / 1) on cfg4 + parity subset for 1
+mkdir -p gpurun_out
+OSC_LIB=$PWD/ab/pu1.so timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "solve or nested or level_draws or cfg4" > gpurun_out/pytest_ab_pu1.log 2>&1; echo "pytest pu1 $?"; tail -1 gpurun_out/pytest_ab_pu1.log
+for i in 1 2; do for v in head pu2 pu1; do
+  OSC_LIB=$PWD/ab/$v.so timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_${v}_$i.json 2> gpurun_out/ab_$v.err
+  python -c "
+import json; d=json.load(open('gpurun_out/ab_${v}_$i.json')); k=d['kernels_ms_profiled_step']
+sel=['pcg_update@2048','pcg_update@1024']
+print('$v', round(d['value'],1), d['clocks']['sm_mhz'], [round(k.get(s,0),2) for s in sel], round(sum(k.values()),1))"
+done; done

@@ -1,0 +1,9 @@
+# A/B: 16 one-warp CTAs per SM (<= 128 registers) for the level-0 up sweep and the coarse up sweep
+mkdir -p gpurun_out
+for i in 1 2; do for v in head surm4 upm4; do
+  OSC_LIB=$PWD/ab/$v.so timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_${v}_$i.json 2> gpurun_out/ab_$v.err
+  python -c "
+import json; d=json.load(open('gpurun_out/ab_${v}_$i.json')); k=d['kernels_ms_profiled_step']
+sel=['mg_smooth_up_r.L0@2048','mg_smooth_up_r.L0@1024','mg_up.Lc@2048','mg_up.Lc@1024']
+print('$v', round(d['value'],1), d['clocks']['sm_mhz'], [round(k.get(s,0),2) for s in sel], round(sum(k.values()),1))"
+done; done

@@ -2071,7 +2071,9 @@ enum { UP_C = 0, UP_E = 1, UP_N = 2, UP_NE = 3, UP_NW = 4, UP_R = 5, UP_Z = 6 };
 #ifndef OSC_UP_MINB
 #define OSC_UP_MINB 3
 #endif
-constexpr int UP_RING = OSC_UP_RING;  // rows staged per warp: 3 × 4 warps × 582 × 8 B = 55.9 KB (RZ); 3 CTAs per SM at ≤ 170 registers (A/B: faster than 4 CTAs at 128)
+// rows staged per warp: 3 × 582 × 8 B = 14 KB per warp (RZ). A/B with one-warp CTAs: 4 or 5 rows are
+// slower (coarse up sweep 19.4 → 28 ms per config-4 step: fewer resident warps)
+constexpr int UP_RING = OSC_UP_RING;
 template <bool RZ>
 constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * CU_W * UpLayout<RZ>::WORDS; }
 

@@ -2316,7 +2316,10 @@ constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 4 × 4 w
 constexpr int CD_W = OSC_CD_W;  // warps per CTA of the coarse ring down sweep
 constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * CD_W * DN_WORDS;
 
-__global__ void __launch_bounds__(32 * CD_W, 16 / CD_W) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+#ifndef OSC_CDRING_MINB
+#define OSC_CDRING_MINB 4
+#endif
+__global__ void __launch_bounds__(32 * CD_W, OSC_CDRING_MINB * 4 / CD_W) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                             PW4 pw, Geo gc, double* __restrict__ rc,
                                                             const int* flags) {
   const int b = blockIdx.z;
@@ -2603,7 +2606,10 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   cpa_wait<0>();
 }
 
-__global__ void __launch_bounds__(32 * RR_W, 16 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+#ifndef OSC_RRING_MINB
+#define OSC_RRING_MINB 4
+#endif
+__global__ void __launch_bounds__(32 * RR_W, OSC_RRING_MINB * 4 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                               const double* __restrict__ r, PW4 pw,
                                                               double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;

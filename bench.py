@@ -204,13 +204,35 @@ class ClockSampler:
 
 
 # ---- reference (CPU) arm --------------------------------------------------------------------------
-def cpu_reference_step(W, threads: int, n_samples: int, seed_index: int, port=None, ref=None):
-    """Run n_samples coupled samples of the workload on the CPU path with `threads` threads.
-    Uses the pristine reference (oracle/_ref) for flow-cell BCs, else the oracle port."""
+# Nothing here imports the product package: the spectra come from the pristine reference's own
+# build_operator (oracle/_ref), the samples from the pristine reference (flow-cell BCs, Point/L2 QoI)
+# or, for the extensions it lacks (all-Dirichlet BCs, ∫u / flux QoIs), the oracle's C restatement.
+def cpu_model() -> str:
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _ref_spectrum(W, ref, O):
+    key = ("eig", W["m"], W["family"], W["lam"])
+    if key not in _CACHE:
+        fam = O.MATERN if W["family"] == "matern" else O.SEP_EXP
+        r = ref.build_operator(W["m"], fam, W["sigma2"], W["lam"], W["nu"] if W["family"] == "matern" else 1.0)
+        _CACHE[key] = (r.n, np.sqrt(np.maximum(r.eigenvalues(), 0.0)))
+    return _CACHE[key]
+
+
+def cpu_reference_step(W, threads: int, n_samples: int, seed_index: int, port, ref):
+    """n_samples coupled samples of the workload on the CPU path with `threads` threads: the pristine
+    reference (oracle/_ref: make_level_plan + coupled_sample) for its own BCs / QoIs, else the oracle
+    port on the reference's spectrum."""
     from oracle import oracle as O
-    from paper_2306_13493_b200 import api
     m = W["m"]
-    if W["bc"] == 0 and ref is not None and W["qoi"] in (0, 1):
+    if W["bc"] == 0 and W["qoi"] in (0, 1):
         opts = O.RefOpts.make(family=O.MATERN if W["family"] == "matern" else O.SEP_EXP,
                               sigma2=W["sigma2"], lam=W["lam"], nu_or_p=W["nu"], qoi_kind=W["qoi"],
                               seed=1, threads=threads)
@@ -220,15 +242,9 @@ def cpu_reference_step(W, threads: int, n_samples: int, seed_index: int, port=No
         t0 = time.perf_counter()
         ref.coupled(_CACHE[key], W["coupled"], False, False, opts, seed_index, seed_index + n_samples)
         return time.perf_counter() - t0, "reference"
-    key = ("op", m)
-    if key not in _CACHE:
-        model = (api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]) if W["family"] == "matern"
-                 else api.CovarianceModel.separable_exponential(W["sigma2"], W["lam"]))
-        op = api.build_operator(api.GridSpec.square(m), model)
-        _CACHE[key] = (op, np.sqrt(np.maximum(op.eigenvalues, 0.0)))
-    op, sl = _CACHE[key]
+    n, sl = _ref_spectrum(W, ref, O)
     t0 = time.perf_counter()
-    port.coupled(m, op.n, sl, None, W["coupled"], 1, W["ell"], seed_index, seed_index + n_samples,
+    port.coupled(m, n, sl, None, W["coupled"], 1, W["ell"], seed_index, seed_index + n_samples,
                  bc=W["bc"], qoi=W["qoi"], threads=threads)
     return time.perf_counter() - t0, "port"
 
@@ -236,19 +252,39 @@ def cpu_reference_step(W, threads: int, n_samples: int, seed_index: int, port=No
 _CACHE = {}
 
 
+def cpu_baseline_block(W, budget_s: float):
+    """cpu_baseline of our arm: all host threads on a bounded sample, plus a 1-thread rate."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    ref, port = O.Ref(), O.Port()
+    if W.get("ce_only"):
+        dt, kind = cpu_ce_step(W, cores, ref, O)
+        dt1, _ = cpu_ce_step(W, 1, ref, O)
+        return {"value": cores / dt, "unit": "samples/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                "value_1thread": 1.0 / dt1,
+                "sample": f"{cores} CE samples (NormalStream + sample_into + restrict_to), one per thread ({dt:.1f} s)"}
+    per_core = max(1, int(2e6 // (W["m"] + 1) ** 2))
+    nsamp = cores * per_core
+    dt, kind = cpu_reference_step(W, cores, nsamp, 0, port, ref)
+    dt1, _ = cpu_reference_step(W, 1, per_core, nsamp, port, ref)
+    return {"value": nsamp / dt, "unit": "samples/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+            "value_1thread": per_core / dt1,
+            "sample": f"{nsamp} samples of the same workload over {cores} host threads ({dt:.1f} s); "
+                      f"{per_core} on 1 thread ({dt1:.1f} s)"}
+
+
 def run_reference(args, W):
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     port = O.Port()
-    ref = O.Ref() if os.path.exists(O.REF_SO) else None
+    ref = O.Ref()
     per_step = cores * max(1, int(2e6 // (W["m"] + 1) ** 2))  # bounded sample per step
     times, kind = [], "port"
     t_budget = time.time() + 240.0
     if W.get("ce_only"):
-        from paper_2306_13493_b200 import api
-        op = api.build_operator(api.GridSpec.square(W["m"]), api.CovarianceModel.matern(W["sigma2"], W["lam"], W["nu"]))
+        per_step = cores
         for k in range(args.steps):
-            dt, kind = cpu_ce_step(W, op, cores, ref, O)
+            dt, kind = cpu_ce_step(W, cores, ref, O)
             times.append(dt)
             if time.time() > t_budget:
                 break
@@ -268,8 +304,9 @@ def run_reference(args, W):
         "warmup": min(args.warmup, 1), "ms_per_step": 1000 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (NormalStream seed 1)",
-        "config": {"workload": W["name"], "global_batch": per_step, "parallelism": f"{cores} host threads"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
+        "config": {"workload": W["name"], "global_batch": per_step, "parallelism": f"{cores} host threads",
+                   "steps_note": f"{len(times)} of {args.steps} steps within the 240 s CPU budget"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
                          "sample": f"{per_step} coupled samples per step x {len(times)} steps"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -542,14 +579,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-        cores = os.cpu_count() or 1
-        ref = O.Ref() if os.path.exists(O.REF_SO) else None
-        per_core = max(1, int(2e6 // (m + 1) ** 2))  # bounded sample: a few seconds of CPU work
-        nsamp = cores * per_core
-        dt, kind = cpu_reference_step(W, cores, nsamp, 0, O.Port(), ref)
-        cpu = {"value": nsamp / dt, "unit": "samples/s", "cores": cores, "kind": kind,
-               "sample": f"{nsamp} samples of the same workload over {cores} host threads ({dt:.1f} s)"}
+        cpu = cpu_baseline_block(W, 60.0)
 
     if rank == 0:
         line = {
@@ -571,30 +601,85 @@ def main():
             "kernels_ms_profiled_step": {k: round(v[1], 3) for k, v in
                                          sorted(kstats_w.items(), key=lambda kv: -kv[1][1])},
         }
+        if args.config == "3" and world == 1:
+            line["per_level"] = cfg3_per_level(args, api, ctx, torch, lib, hbm)
+            line["per_level"]["4"] = {"grid": f"{m}^2/{m // 2}^2", "samples_per_s": value,
+                                      "batch": B, "roofline_frac_at_measured_iters": pipeline["frac_at_measured_iters"]}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
+def cfg3_per_level(args, api, ctx, torch, lib, hbm):
+    """Config 3's levels ℓ = 0..3 (16²…128² fine grids; ℓ ≤ 2 smoothed with k = s/2 as the reference's
+    Adaptive + lstar_only rule gives for the separable exponential): samples/s per level, each level
+    timed over `args.steps` batches with CUDA events on the context stream (ℓ = 4 is the main line)."""
+    import ctypes as C
+    from paper_2306_13493_b200 import _lib as L
+    model = api.CovarianceModel.separable_exponential(1.0, 0.01)
+    problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Flux), bc=api.BC.FlowCell)
+    opt = api.EstimatorOptions(seed=1)
+    ps = api._problem_struct(problem, opt.solver)
+    out = {}
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for ell, B in [(0, 16384), (1, 8192), (2, 4096), (3, 2048)]:
+        m = 16 << ell
+        op = api.build_operator(api.GridSpec.square(m), model)
+        k = op.s // 2 if ell <= 2 else 0
+        plan = api.make_level_plan(ell, 1.0 / 16, problem, opt, operator=op, k_trunc=k)
+        lev = plan.op.device_level(ctx, k)
+        flags = (L.DRAW_HAS_COARSE if ell > 0 else 0) | (L.DRAW_TRUNC_FINE | L.DRAW_TRUNC_COARSE if k else 0)
+        qf, qc = np.empty(B), np.empty(B)
+        itf, itc, st = (np.zeros(B, dtype=np.int32) for _ in range(3))
+
+        def step(kk):
+            frm = kk * B
+            api._check(lib.osc_level_draws(lev.h, C.byref(ps), 1, ell, frm, frm + B, flags, None, qf.ctypes.data,
+                                           qc.ctypes.data, itf.ctypes.data, itc.ctypes.data, st.ctypes.data, None))
+        for w in range(args.warmup):
+            step(1_000_000 + w)
+        ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        its = [0, 0]
+        e0.record(stream)
+        for kk in range(args.steps):
+            step(kk)
+            its[0] += int(itf.sum())
+            its[1] += int(itc.sum())
+        e1.record(stream)
+        ctx.synchronize()
+        ms = e0.elapsed_time(e1)
+        rate = args.steps * B / (ms / 1000.0)
+        Wl = dict(m=m, batch=B, coupled=ell > 0, it=(its[0] / (args.steps * B), its[1] / (args.steps * B)))
+        b_meas = algorithmic_bytes_per_sample(Wl, plan.op.n)
+        out[str(ell)] = {"grid": f"{m}^2" + (f"/{m // 2}^2" if ell else ""), "samples_per_s": rate, "batch": B,
+                         "smoothed": bool(k), "mean_iters": [round(x, 2) for x in Wl["it"]],
+                         "roofline_frac_at_measured_iters": rate / (hbm * 1e9 / b_meas)}
+        plan.op._levels.clear()
+    return out
+
+
 def run_mlmc(args, api, ctx, torch, rank):
-    """Configs 3 / 5: adaptive MLMC-CES (estimators.cpp:289-378 restated in api.py) with every
-    sample drawn through osc_level_draws. Exponential (separable, p = 1) covariance σ² = 1,
-    flow-cell BCs, outflow-flux QoI, h0 = 1/16, smoothing Adaptive on the levels coarser than
-    the resolution bound (smoothing_lstar_only), N_ℓ by the standard rule at RMSE eps."""
+    """Configs 3 / 5: the reference's OWN adaptive MLMC(-CES) estimator (estimate_adaptive,
+    estimators.cpp:289-378, compiled from the pristine sources with run_level_samples routed to the GPU
+    seam — paper_2306_13493_b200.estimators) with every sample drawn through osc_level_draws.
+    Exponential (separable, p = 1) covariance σ² = 1, flow-cell BCs, outflow-flux QoI, h0 = 1/16,
+    smoothing Adaptive on the levels coarser than the resolution bound (smoothing_lstar_only), N_ℓ by
+    the standard rule at RMSE eps."""
+    from paper_2306_13493_b200 import estimators as E
     model = api.CovarianceModel.separable_exponential(1.0, args.lam)
     problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Flux), bc=api.BC.FlowCell)
     opt = api.EstimatorOptions(seed=1, smoothing=api.SmoothingRule.Adaptive, smoothing_lstar_only=True,
-                               l_max=4, solver=api.SolverOptions(
-                                   coarse_operator=api.CoarseOperator[args.coarse_op.capitalize()]))
+                               l_max=4)
     # a first (cold) run loads the kernels and allocates each level's workspaces; the second run,
     # identical (same seed, so the same samples), is the timed one
     t0 = time.perf_counter()
-    api.mlmc_estimate(problem, opt, 1.0 / 16, args.eps, initial_levels=5, ctx=ctx)
-    ctx.synchronize()
+    E.mlmc_estimate(problem, opt, 1.0 / 16, args.eps, initial_levels=5)
+    torch.cuda.synchronize()
     cold = time.perf_counter() - t0
     t0 = time.perf_counter()
-    rep = api.mlmc_estimate(problem, opt, 1.0 / 16, args.eps, initial_levels=5, ctx=ctx)
-    ctx.synchronize()
+    rep = E.mlmc_estimate(problem, opt, 1.0 / 16, args.eps, initial_levels=5)
+    torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     total = sum(l.n for l in rep.levels)
     if rank == 0:
@@ -605,7 +690,8 @@ def run_mlmc(args, api, ctx, torch, rank):
             "converged": rep.converged, "message": rep.message,
             "levels": [{"h": h, "n": l.n, "mean_y": l.mean_y, "var_y": l.var_y,
                         "wall_per_sample_s": l.cost_wall_per_sample} for h, l in zip(rep.level_h, rep.levels)],
-            "config": {"workload": f"MLMC-CES sep-exp s2=1 lam={args.lam}, h0=1/16, 5 levels, flux QoI, eps={args.eps}"},
+            "config": {"workload": f"MLMC-CES sep-exp s2=1 lam={args.lam}, h0=1/16, 5 levels, flux QoI, eps={args.eps}",
+                       "driver": "the reference's estimate_adaptive (C++) over the GPU seam"},
             "dtype": "f64", "data": "synthetic: NormalStream(1, l, i)",
         }), flush=True)
 
@@ -723,12 +809,7 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
         host_out.free()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-        cores = os.cpu_count() or 1
-        ref = O.Ref() if os.path.exists(O.REF_SO) else None
-        dt, kind = cpu_ce_step(W, op, cores, ref, O)
-        cpu = {"value": cores / dt, "unit": "samples/s", "cores": cores, "kind": kind,
-               "sample": f"{cores} CE samples (NormalStream + sample_into + restrict_to), one per thread ({dt:.1f} s)"}
+        cpu = cpu_baseline_block(W, 60.0)
     if rank == 0:
         print(json.dumps({
             "metric": "CE field samples/s (config 2, sampling only, fp64)", "value": value,
@@ -745,33 +826,26 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
         dist.destroy_process_group()
 
 
-def cpu_ce_step(W, op, cores, ref, O):
-    """CPU CE baseline: the pristine reference (NormalStream + sample_into + restrict_to) when
-    available, else the oracle port; one sample per thread."""
+def cpu_ce_step(W, threads, ref, O):
+    """CPU CE baseline: the pristine reference (NormalStream + sample_into + restrict_to), one sample
+    per thread."""
     import threading as th
     m = W["m"]
-    if ref is not None:
-        rop = ref.build_operator(m, O.MATERN, W["sigma2"], W["lam"], W["nu"])
+    key = ("ceop", m)
+    if key not in _CACHE:
+        _CACHE[key] = ref.build_operator(m, O.MATERN, W["sigma2"], W["lam"], W["nu"])
+    rop = _CACHE[key]
 
-        def one(i):
-            u = rop.sample(ref.normals(1, 0, i, rop.s))
-            rop.restrict(u, m)
-        kind = "reference"
-    else:
-        port = O.Port()
-        sl = np.sqrt(np.maximum(op.eigenvalues, 0.0))
-
-        def one(i):
-            u = port.sample(op.n, sl, port.normals(1, 0, i, op.s))
-            port.restrict(op.n, m, u, m)
-        kind = "port"
-    ts = [th.Thread(target=one, args=(i,)) for i in range(cores)]
+    def one(i):
+        u = rop.sample(ref.normals(1, 0, i, rop.s))
+        rop.restrict(u, m)
+    ts = [th.Thread(target=one, args=(i,)) for i in range(threads)]
     t0 = time.perf_counter()
     for t in ts:
         t.start()
     for t in ts:
         t.join()
-    return time.perf_counter() - t0, kind
+    return time.perf_counter() - t0, "reference"
 
 
 if __name__ == "__main__":

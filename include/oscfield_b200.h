@@ -115,6 +115,7 @@ typedef struct osc_ctx osc_ctx;
 typedef struct osc_level osc_level;
 
 /* ---- context --------------------------------------------------------------- */
+/* device < 0: the calling thread's current CUDA device */
 int osc_ctx_create(int device, osc_ctx** out);
 void osc_ctx_destroy(osc_ctx* ctx);
 /* Thread-local message of the last failing call. */
@@ -196,6 +197,66 @@ int osc_level_draws(osc_level* level, const osc_problem* problem, uint64_t seed,
                     int64_t from, int64_t to, int flags, const double* xi, double* q_fine,
                     double* q_coarse, int32_t* iters_fine, int32_t* iters_coarse,
                     int32_t* status, double* level_sums);
+
+/* Running per-level sums in HBM (north_star subsystem 4; the moments of estimators.cpp:82-101,320,335
+ * as shifted sums). After osc_level_sums_reset(level, Ky, Kq) every osc_level_draws call on the level
+ * adds its samples to [n, Σ(Y−Ky), Σ(Y−Ky)², Σ(q_f−Kq), Σ(q_f−Kq)²] on the device (no host round trip;
+ * Y = q_fine − q_coarse, or q_fine without a coarse grid). Use shifts near the level means (e.g. the
+ * pilot means) so the variance (Σ(Y−K)² − (Σ(Y−K))²/n)/(n−1) does not cancel. osc_level_sums_read copies
+ * out = [5 sums, Ky, Kq]. The sums of one call sequence are bit-identical run to run; a different
+ * chunking of the same samples changes the summation order (~1e-16 relative). */
+int osc_level_sums_reset(osc_level* level, double shift_y, double shift_q);
+int osc_level_sums_read(osc_level* level, double out[7]);
+
+/* Residual history of failing samples (SolverError::history, fem.cpp:359-379). With hist_cap > 0, an
+ * osc_level_draws call that returns OSC_ERR_SOLVER re-draws its first failing slot alone with the
+ * per-iteration ‖r‖/‖b‖ kept (sample i is a pure function of (seed, ℓ, i) or of xi row i, so the
+ * failure repeats bit for bit); osc_ctx_failure_history then returns that slot and up to cap entries
+ * (history[0] = initial residual) and the history length (0 when no failure was recorded). */
+int osc_ctx_set_history(osc_ctx* ctx, int hist_cap);
+int osc_ctx_failure_history(osc_ctx* ctx, int64_t* slot, double* out, int cap);
+
+/* ---- several GPUs -------------------------------------------------------------------------------
+ * Samples shard with no data-path exchange: [from, to) is cut into contiguous per-device chunks
+ * (chunk = ceil(count/G), the chunking of parallel_samples, estimators.cpp:32-63), so slot i receives
+ * sample i for any device count. The only collective is an fp64 ncclAllReduce of the 5 device-resident
+ * level sums per batch. NCCL is loaded at run time (dlopen libnccl.so.2).
+ *
+ * osc_group: one process drives G devices, one osc_ctx and one host thread per device. */
+typedef struct osc_group osc_group;
+typedef struct osc_group_level osc_group_level;
+int osc_group_create(int n_devices, const int* devices /* NULL → 0..n-1 */, osc_group** out);
+void osc_group_destroy(osc_group* group);
+int osc_group_size(const osc_group* group);
+osc_ctx* osc_group_ctx(osc_group* group, int i);
+/* osc_level_create on every device (same host eigenvalues, same truncation mask). */
+int osc_group_level_create(osc_group* group, int m, int J, const double* eigenvalues, int64_t k_trunc,
+                           osc_group_level** out);
+void osc_group_level_destroy(osc_group_level* level);
+osc_level* osc_group_level_at(osc_group_level* level, int i);
+/* osc_level_draws over the group: device g draws its contiguous chunk into its slots of the caller's
+ * (host) arrays; xi is host memory or NULL (device Philox). level_sums as in osc_level_draws, summed
+ * over the devices by one NCCL all-reduce of the device buffers. A solver failure on any device lets
+ * every device finish, then returns OSC_ERR_SOLVER. */
+int osc_group_level_draws(osc_group_level* level, const osc_problem* problem, uint64_t seed, uint32_t ell,
+                          int64_t from, int64_t to, int flags, const double* xi, double* q_fine,
+                          double* q_coarse, int32_t* iters_fine, int32_t* iters_coarse, int32_t* status,
+                          double* level_sums);
+int osc_group_level_sums_reset(osc_group_level* level, double shift_y, double shift_q);
+/* all-reduce of the devices' running level sums (device to device), out = [5 sums, Ky, Kq] */
+int osc_group_level_sums_allreduce(osc_group_level* level, double out[7]);
+
+/* osc_comm: one process per GPU (e.g. torchrun). Rank 0 makes the id, the launcher broadcasts it. */
+typedef struct osc_comm osc_comm;
+int osc_comm_unique_id(unsigned char id[128]);
+int osc_comm_create(osc_ctx* ctx, int nranks, int rank, const unsigned char id[128], osc_comm** out);
+void osc_comm_destroy(osc_comm* comm);
+/* ncclAllReduce of the level's running sums into a separate device buffer (the running sums keep
+ * accumulating); out (may be NULL) = [5 reduced sums, Ky, Kq] */
+int osc_comm_allreduce_level_sums(osc_comm* comm, osc_level* level, double out[7]);
+/* ncclAllGather of n_per_rank doubles per rank (host in, host out, rank order): the (q_f, q_c) slots
+ * of contiguous shards, so every rank can run the reference's slot-order Welford bit-identically. */
+int osc_comm_allgather(osc_comm* comm, const double* local, int64_t n_per_rank, double* all);
 
 /* summarize_draws: one-pass Welford over slot-ordered draws (estimators.cpp:82-101).
  * out = [n, mean_y, var_y, mean_q, var_q]; var only when n ≥ 2. q_coarse may be NULL. */

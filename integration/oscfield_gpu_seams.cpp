@@ -1,14 +1,23 @@
 // Reference-side binding: defines the two batch seams the reference DECLARES but never defines
 // (include/oscfield/estimators.hpp:112-118 run_level_draws, :120-128 summarize_draws) on top of
-// the B200 C-ABI (include/oscfield_b200.h). Compile this file together with the reference
-// library and link libosc_b200.so; the reference's estimators then reach the GPU by calling
-// run_level_draws where they call run_level_samples today (src/estimators.cpp:315-316,333-334,388).
+// the B200 C-ABI (include/oscfield_b200.h), plus the overload that routes the reference's own
+// estimator loop onto them (integration/route_run_level_samples.hpp). Compile this file together
+// with the reference library and link libosc_b200.so; the reference's estimators then draw every
+// sample on the GPU (integration/Makefile builds exactly that: the pristine sources + this file).
 //
 //   g++ -std=c++20 -I<reference>/include -I<this repo>/include -c oscfield_gpu_seams.cpp
 //   ... link with -L<repo>/paper_2306_13493_b200 -losc_b200
+//
+// Devices. By default the seam drives the calling thread's current CUDA device (or OSC_DEVICE /
+// LOCAL_RANK when set): one context per host thread, as one SampleWorkspace per worker
+// (embedding.hpp:24-35). oscfield_gpu_configure(n, ...) (or OSC_SEAM_GPUS=n) switches to an
+// osc_group over n devices: each batch is cut into contiguous per-device chunks (the chunking of
+// parallel_samples, estimators.cpp:32-63), one host thread per GPU, slot i = sample i on any count.
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -20,41 +29,127 @@
 namespace oscfield {
 namespace {
 
-[[noreturn]] void raise(int code, std::vector<double> history = {}) {
+// cap of the residual history a SolverError carries (the failing slot is re-solved with it kept)
+constexpr int kHistoryCap = 1 << 16;
+
+[[noreturn]] void raise(int code, osc_ctx* ctx = nullptr) {
   const std::string msg = osc_last_error();
   switch (code) {
     case OSC_ERR_CONFIG: throw ConfigError(msg);
-    case OSC_ERR_SOLVER: throw SolverError(msg, std::move(history));
+    case OSC_ERR_SOLVER: {
+      std::vector<double> hist;
+      if (ctx) {
+        std::int64_t slot = -1;
+        const int n = osc_ctx_failure_history(ctx, &slot, nullptr, 0);
+        if (n > 0) {
+          hist.resize(static_cast<std::size_t>(n));
+          osc_ctx_failure_history(ctx, &slot, hist.data(), n);
+        }
+      }
+      throw SolverError(msg, std::move(hist));
+    }
     case OSC_ERR_EMBEDDING: throw EmbeddingError(msg);
     default: throw NumericalError(msg);
   }
 }
 
-// One context per host thread (one thread drives one GPU, embedding.hpp:24-35), and one device
-// level per (operator, truncation) — the level owns √λ (full and truncated) in HBM.
-struct DeviceState {
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Device level per (operator, truncation). The entry holds a weak_ptr to the operator, so a freed
+// plan whose successor is allocated at the same address is never mistaken for it, and the levels of
+// expired operators (their √λ in HBM) are destroyed on the next lookup.
+template <typename Lev>
+struct LevelCache {
+  struct Entry {
+    std::weak_ptr<const EmbeddingOperator> op;
+    Lev* lev = nullptr;
+  };
+  std::map<std::pair<const EmbeddingOperator*, std::int64_t>, Entry> map;
+  template <typename Destroy, typename Create>
+  Lev* get(const LevelPlan& plan, Destroy&& destroy, Create&& create) {
+    for (auto it = map.begin(); it != map.end();) {
+      if (it->second.op.expired()) {
+        destroy(it->second.lev);
+        it = map.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    const auto key = std::make_pair(plan.op.get(), plan.k_trunc);
+    auto it = map.find(key);
+    if (it != map.end() && it->second.op.lock() == plan.op) return it->second.lev;
+    if (it != map.end()) {
+      destroy(it->second.lev);
+      map.erase(it);
+    }
+    Lev* lev = create();
+    map.emplace(key, Entry{plan.op, lev});
+    return lev;
+  }
+  template <typename Destroy>
+  void clear(Destroy&& destroy) {
+    for (auto& kv : map) destroy(kv.second.lev);
+    map.clear();
+  }
+};
+
+// single-device mode: one context per host thread
+struct ThreadState {
   osc_ctx* ctx = nullptr;
-  std::map<std::pair<const EmbeddingOperator*, std::int64_t>, osc_level*> levels;
-  ~DeviceState() {
-    for (auto& kv : levels) osc_level_destroy(kv.second);
+  LevelCache<osc_level> levels;
+  ~ThreadState() {
+    levels.clear([](osc_level* l) { osc_level_destroy(l); });
     if (ctx) osc_ctx_destroy(ctx);
   }
 };
-thread_local DeviceState g_dev;
+thread_local ThreadState g_thread;
 
-osc_level* level_for(const LevelPlan& plan) {
-  if (!g_dev.ctx) {
-    if (int rc = osc_ctx_create(0, &g_dev.ctx)) raise(rc);
+// group mode: one process-wide group
+struct GroupState {
+  std::mutex mu;
+  int n_gpus = 0;  // 0: not configured (single device)
+  std::vector<int> devices;
+  osc_group* group = nullptr;
+  LevelCache<osc_group_level> levels;
+  int bc = -1, qoi = -1;  // extension overrides (-1: the reference's own BC / QoI mapping)
+  ~GroupState() { reset(); }
+  void reset() {
+    levels.clear([](osc_group_level* l) { osc_group_level_destroy(l); });
+    if (group) osc_group_destroy(group);
+    group = nullptr;
   }
-  const auto key = std::make_pair(plan.op.get(), plan.k_trunc);
-  auto it = g_dev.levels.find(key);
-  if (it != g_dev.levels.end()) return it->second;
-  osc_level* lev = nullptr;
-  if (int rc = osc_level_create(g_dev.ctx, plan.grid.m(0), plan.op->padding()[0],
-                                plan.op->eigenvalues().data(), plan.k_trunc, &lev))
-    raise(rc);
-  g_dev.levels.emplace(key, lev);
-  return lev;
+};
+GroupState& group_state() {
+  static GroupState g;
+  static std::once_flag once;
+  std::call_once(once, [] { g.n_gpus = env_int("OSC_SEAM_GPUS", 0); });
+  return g;
+}
+
+osc_ctx* thread_ctx() {
+  if (!g_thread.ctx) {
+    const int dev = env_int("OSC_DEVICE", env_int("LOCAL_RANK", -1));  // -1: current CUDA device
+    if (int rc = osc_ctx_create(dev, &g_thread.ctx)) raise(rc);
+    osc_ctx_set_history(g_thread.ctx, kHistoryCap);
+  }
+  return g_thread.ctx;
+}
+
+osc_problem problem_of(const ProblemSpec& problem, const EstimatorOptions& opt, const GroupState& gs) {
+  osc_problem p{};
+  p.bc = gs.bc >= 0 ? gs.bc : OSC_BC_FLOWCELL;  // the reference's only BC (fem.cpp:28-30)
+  p.forcing = problem.forcing == Forcing::Constant ? 1 : 0;
+  p.forcing_value = problem.forcing_value;
+  p.qoi = gs.qoi >= 0 ? gs.qoi : (problem.qoi.kind == QoiSpec::Kind::L2Norm ? OSC_QOI_L2 : OSC_QOI_POINT);
+  p.qoi_x = problem.qoi.x;
+  p.qoi_y = problem.qoi.y;
+  p.tol = opt.solver.tol;
+  p.max_iter_factor = opt.solver.max_iter_factor;  // preconditioner: always geometric MG
+  p.coarse_op = OSC_COARSE_GALERKIN;  // same fine system and tolerance; ~2.5x fewer CG iterations
+  return p;
 }
 
 }  // namespace
@@ -66,27 +161,57 @@ void run_level_draws(const LevelPlan& plan, const GridSpec* coarse_grid, bool tr
   if (to < from) throw ConfigError("run_level_draws: to < from");
   if (static_cast<std::int64_t>(draws.size()) < to) draws.resize(static_cast<std::size_t>(to));
   if (to == from) return;
+  if (coarse_grid && !plan.grid.refines(*coarse_grid))
+    throw ConfigError("restrict: target grid is not a nested coarsening");
   const std::int64_t n = to - from;
-  osc_problem p{};
-  p.bc = OSC_BC_FLOWCELL;  // the reference's only boundary condition (fem.cpp:28-30)
-  p.forcing = problem.forcing == Forcing::Constant ? 1 : 0;
-  p.forcing_value = problem.forcing_value;
-  p.qoi = problem.qoi.kind == QoiSpec::Kind::L2Norm ? OSC_QOI_L2 : OSC_QOI_POINT;
-  p.qoi_x = problem.qoi.x;
-  p.qoi_y = problem.qoi.y;
-  p.tol = opt.solver.tol;
-  p.max_iter_factor = opt.solver.max_iter_factor;  // preconditioner: always geometric MG
-  p.coarse_op = OSC_COARSE_GALERKIN;  // same fine system and tolerance; ~2x fewer CG iterations
+  GroupState& gs = group_state();
+  const osc_problem p = problem_of(problem, opt, gs);
   const int flags = (coarse_grid ? OSC_DRAW_HAS_COARSE : 0) |
                     (truncate_fine ? OSC_DRAW_TRUNC_FINE : 0) |
                     (truncate_coarse ? OSC_DRAW_TRUNC_COARSE : 0);
   std::vector<double> qf(n), qc(n);
   std::vector<std::int32_t> status(n);
+  const int m = plan.grid.m(0), J = plan.op->padding()[0];
+  const double* eig = plan.op->eigenvalues().data();
   const auto t0 = std::chrono::steady_clock::now();
-  const int rc = osc_level_draws(level_for(plan), &p, opt.seed, static_cast<std::uint32_t>(plan.ell),
-                                 from, to, flags, /*xi=*/nullptr, qf.data(), qc.data(), nullptr,
-                                 nullptr, status.data(), nullptr);
-  if (rc) raise(rc);
+  if (gs.n_gpus > 0) {
+    std::lock_guard<std::mutex> lk(gs.mu);
+    if (!gs.group) {
+      if (int rc = osc_group_create(gs.n_gpus, gs.devices.empty() ? nullptr : gs.devices.data(), &gs.group))
+        raise(rc);
+      for (int i = 0; i < gs.n_gpus; ++i) osc_ctx_set_history(osc_group_ctx(gs.group, i), kHistoryCap);
+    }
+    osc_group_level* lev = gs.levels.get(
+        plan, [](osc_group_level* l) { osc_group_level_destroy(l); },
+        [&] {
+          osc_group_level* l = nullptr;
+          if (int rc = osc_group_level_create(gs.group, m, J, eig, plan.k_trunc, &l)) raise(rc);
+          return l;
+        });
+    const int rc = osc_group_level_draws(lev, &p, opt.seed, static_cast<std::uint32_t>(plan.ell), from, to,
+                                         flags, /*xi=*/nullptr, qf.data(), qc.data(), nullptr, nullptr,
+                                         status.data(), nullptr);
+    if (rc) {
+      osc_ctx* failed = nullptr;  // the device whose shard holds the first failing slot
+      for (int i = 0; i < gs.n_gpus && !failed; ++i) {
+        std::int64_t slot = -1;
+        if (osc_ctx_failure_history(osc_group_ctx(gs.group, i), &slot, nullptr, 0) > 0) failed = osc_group_ctx(gs.group, i);
+      }
+      raise(rc, failed);
+    }
+  } else {
+    osc_ctx* ctx = thread_ctx();
+    osc_level* lev = g_thread.levels.get(
+        plan, [](osc_level* l) { osc_level_destroy(l); },
+        [&] {
+          osc_level* l = nullptr;
+          if (int rc = osc_level_create(ctx, m, J, eig, plan.k_trunc, &l)) raise(rc);
+          return l;
+        });
+    const int rc = osc_level_draws(lev, &p, opt.seed, static_cast<std::uint32_t>(plan.ell), from, to, flags,
+                                   /*xi=*/nullptr, qf.data(), qc.data(), nullptr, nullptr, status.data(), nullptr);
+    if (rc) raise(rc, ctx);
+  }
   const double wall =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / n;
   for (std::int64_t i = 0; i < n; ++i)
@@ -114,4 +239,37 @@ DrawStats summarize_draws(const std::vector<LevelDraw>& draws, bool has_coarse) 
   return s;
 }
 
+// The reference's estimators call the file-local run_level_samples (estimators.cpp:315-316,333-334,
+// 388) with a non-const LevelPlan; this overload (declared by route_run_level_samples.hpp) is the
+// better match there and forwards to the GPU seam. Same arguments, same slot contract.
+void run_level_samples(LevelPlan& plan, const GridSpec* coarse_grid, bool truncate_fine, bool truncate_coarse,
+                       const ProblemSpec& problem, const EstimatorOptions& opt, std::int64_t from,
+                       std::int64_t to, std::vector<LevelDraw>& draws) {
+  draws.resize(static_cast<std::size_t>(to));  // run_level_samples' own contract (estimators.cpp:69)
+  run_level_draws(plan, coarse_grid, truncate_fine, truncate_coarse, problem, opt, from, to, draws);
+}
+
 }  // namespace oscfield
+
+extern "C" {
+// Seam settings (process-wide; call before the first draw or between estimates):
+//   n_gpus  > 0: draw every batch over an osc_group of n_gpus devices (devices NULL → 0..n-1);
+//           0: the calling thread's device (default; OSC_SEAM_GPUS sets the initial value).
+//   bc, qoi ≥ 0: the extension BC / QoI of include/oscfield_b200.h (OSC_BC_DIRICHLET_ALL,
+//           OSC_QOI_INTEGRAL, OSC_QOI_FLUX), which the reference's ProblemSpec cannot express;
+//           -1 keeps the reference's flow-cell BC and its Point / L2 QoI.
+int oscfield_gpu_configure(int n_gpus, const int* devices, int bc, int qoi) {
+  oscfield::GroupState& gs = oscfield::group_state();
+  std::lock_guard<std::mutex> lk(gs.mu);
+  if (n_gpus < 0) return OSC_ERR_CONFIG;
+  std::vector<int> devs(devices ? devices : nullptr, devices ? devices + n_gpus : nullptr);
+  if (n_gpus != gs.n_gpus || devs != gs.devices) {
+    gs.reset();
+    gs.n_gpus = n_gpus;
+    gs.devices = devs;
+  }
+  gs.bc = bc;
+  gs.qoi = qoi;
+  return OSC_OK;
+}
+}

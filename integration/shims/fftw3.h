@@ -1,4 +1,5 @@
-/* FFTW3-API shim — TEST INFRASTRUCTURE ONLY (oracle/).
+/* FFTW3-API shim — a build dependency of the reference library in this image (used by the
+ * oracle build oracle/_ref and by the GPU-routed reference build integration/_build).
  *
  * FFTW3 (no version pinned by the reference: /root/reference/proj/CMakeLists.txt:14-15)
  * is not installed in this image. The reference's only FFTW call sites are

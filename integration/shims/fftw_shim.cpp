@@ -1,6 +1,7 @@
-// Independent implementation of the FFTW3 subset declared in fftw3.h — TEST
-// INFRASTRUCTURE ONLY (oracle/). Used solely to compile the pristine reference
-// (proj/src/fft.cpp) into oracle/_ref/ as a CPU checker.
+// Independent implementation of the FFTW3 subset declared in fftw3.h. FFTW is absent from this
+// image; this stands in for it wherever the pristine reference library is compiled: the CPU checker
+// oracle/_ref/ and the GPU-routed reference build integration/_build/ (whose only FFT is the
+// one-time spectrum setup, build_operator — every sample runs on the GPU).
 //
 // Algorithm: per-axis 1-D transforms; each 1-D transform is a recursive
 // decimation-in-time mixed-radix Cooley-Tukey over the prime factorisation of

@@ -1,4 +1,4 @@
-// Force-included when compiling the pristine reference — TEST INFRASTRUCTURE ONLY.
+// Force-included when compiling the pristine reference (oracle/_ref, integration/_build).
 // proj/src/estimators.cpp:37 calls std::max(int, const long&), which has no
 // standard overload; this supplies the obvious one. (estimators.cpp also uses
 // the undeclared name `Draw` for `LevelDraw`; the Makefile passes -DDraw=LevelDraw.)

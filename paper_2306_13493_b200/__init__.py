@@ -7,6 +7,5 @@ from .api import *  # noqa: F401,F403
 from .api import (BC, BuildOptions, Context, CovarianceModel, EmbeddingOperator,  # noqa: F401
                   EstimatorOptions, GridSpec, LevelDraws, ProblemSpec, QoiKind, QoiSpec,
                   SmoothingRule, SolverOptions, assemble_and_solve, build_operator,
-                  default_context, evaluate_qoi, load_spectrum, make_level_plan, mc_estimate,
-                  mc_estimate_fixed_n, mlmc_estimate, run_level_draws, save_spectrum,
-                  summarize_draws)
+                  default_context, evaluate_qoi, load_spectrum, make_level_plan, run_level_draws,
+                  save_spectrum, summarize_draws, DeviceGroup, Comm)

@@ -14,13 +14,14 @@ ROOT = os.path.dirname(HERE)
 # OSC_LIB: developer override (A/B builds of the same sources); the default is the in-tree build
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 HEADER = os.path.join(ROOT, "include", "oscfield_b200.h")
-SOURCES = ["csrc/capi.cu", "csrc/ce_sample.cu", "csrc/mgpcg.cu", "csrc/setup.cpp"]
+SOURCES = ["csrc/capi.cu", "csrc/ce_sample.cu", "csrc/mgpcg.cu", "csrc/setup.cpp", "csrc/group.cpp"]
 DEPS = SOURCES + ["csrc/osc_internal.cuh", "csrc/osc_device.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-shared",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
 ]
+OBJ_DIR = os.path.join(HERE, "_build")
 
 OSC_OK, OSC_ERR_CONFIG, OSC_ERR_NUMERICAL, OSC_ERR_SOLVER, OSC_ERR_EMBEDDING, OSC_ERR_CUDA = (
     0, 2, 3, 4, 5, 6)
@@ -39,6 +40,11 @@ EXPORTS = [
     "osc_build_spectrum_device",
     "osc_level_create", "osc_level_prefetch_xi", "osc_level_destroy", "osc_level_info", "osc_level_draws", "osc_summarize",
     "osc_normals", "osc_ce_sample", "osc_darcy_solve", "osc_qoi",
+    "osc_level_sums_reset", "osc_level_sums_read", "osc_ctx_set_history", "osc_ctx_failure_history",
+    "osc_group_create", "osc_group_destroy", "osc_group_size", "osc_group_ctx", "osc_group_level_create",
+    "osc_group_level_destroy", "osc_group_level_at", "osc_group_level_draws", "osc_group_level_sums_reset",
+    "osc_group_level_sums_allreduce", "osc_comm_unique_id", "osc_comm_create", "osc_comm_destroy",
+    "osc_comm_allreduce_level_sums", "osc_comm_allgather",
 ]
 
 
@@ -52,15 +58,27 @@ class Problem(C.Structure):
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
-    """Compile libosc_b200.so for sm_100a with nvcc (in-tree)."""
+    """Compile libosc_b200.so for sm_100a with nvcc (in-tree): one object per source, compiled in
+    parallel, then linked. Skipped when the library is newer than every source (force=True rebuilds)."""
+    from concurrent.futures import ThreadPoolExecutor
     srcs = [os.path.join(HERE, s) for s in SOURCES]
     deps = [os.path.join(HERE, s) for s in DEPS] + [HEADER]
     if not force and os.path.exists(LIB_PATH):
         t = os.path.getmtime(LIB_PATH)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB_PATH
-    cmd = ["nvcc"] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB_PATH] + srcs
-    subprocess.run(cmd, check=True, cwd=HERE)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    extra = ["-Xptxas", "-v"] if verbose else []
+
+    def compile_one(src):
+        obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+        subprocess.run(["nvcc"] + NVCC_FLAGS + extra + ["-c", "-o", obj, src], check=True, cwd=HERE)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        objs = list(ex.map(compile_one, srcs))
+    subprocess.run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB_PATH] + objs +
+                   ["-ldl", "-lpthread"], check=True, cwd=HERE)
     return LIB_PATH
 
 
@@ -115,6 +133,31 @@ def lib() -> C.CDLL:
     L.osc_ce_sample.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint64, i64, ip, vp, vp]
     L.osc_darcy_solve.argtypes = [vp, ip, i64, vp, C.POINTER(Problem), vp, vp, vp, vp, ip]
     L.osc_qoi.argtypes = [vp, ip, i64, vp, vp, C.POINTER(Problem), vp]
+    L.osc_level_sums_reset.argtypes = [vp, C.c_double, C.c_double]
+    L.osc_level_sums_read.argtypes = [vp, vp]
+    L.osc_ctx_set_history.argtypes = [vp, ip]
+    L.osc_ctx_failure_history.argtypes = [vp, C.POINTER(i64), vp, ip]
+    L.osc_group_create.argtypes = [ip, vp, C.POINTER(vp)]
+    L.osc_group_destroy.argtypes = [vp]
+    L.osc_group_destroy.restype = None
+    L.osc_group_size.argtypes = [vp]
+    L.osc_group_ctx.argtypes = [vp, ip]
+    L.osc_group_ctx.restype = vp
+    L.osc_group_level_create.argtypes = [vp, ip, ip, vp, i64, C.POINTER(vp)]
+    L.osc_group_level_destroy.argtypes = [vp]
+    L.osc_group_level_destroy.restype = None
+    L.osc_group_level_at.argtypes = [vp, ip]
+    L.osc_group_level_at.restype = vp
+    L.osc_group_level_draws.argtypes = [vp, C.POINTER(Problem), C.c_uint64, C.c_uint32, i64, i64, ip, vp,
+                                        vp, vp, vp, vp, vp, vp]
+    L.osc_group_level_sums_reset.argtypes = [vp, C.c_double, C.c_double]
+    L.osc_group_level_sums_allreduce.argtypes = [vp, vp]
+    L.osc_comm_unique_id.argtypes = [vp]
+    L.osc_comm_create.argtypes = [vp, ip, ip, vp, C.POINTER(vp)]
+    L.osc_comm_destroy.argtypes = [vp]
+    L.osc_comm_destroy.restype = None
+    L.osc_comm_allreduce_level_sums.argtypes = [vp, vp, vp]
+    L.osc_comm_allgather.argtypes = [vp, vp, i64, vp]
     _LIB = L
     return L
 

@@ -1,14 +1,17 @@
-"""Host-side mirror of the reference's sampler / solver / estimator interface
+"""Host-side mirror of the reference's sampler / solver / batch-seam interface
 (namespace oscfield, /root/reference/proj/include/oscfield/*.hpp), backed by the sm_100a
 C-ABI (include/oscfield_b200.h). Same names, argument meaning and error behaviour:
 
   GridSpec, CovarianceModel, EmbeddingOperator, build_operator, load_spectrum/save_spectrum
       ← grid.hpp, covariance.hpp, embedding.hpp
   ProblemSpec, QoiSpec, EstimatorOptions, SolverOptions, LevelPlan, make_level_plan,
-  run_level_draws, summarize_draws, choose_k_ell, richardson_bias, coarsest_level_bound,
-  mc_estimate_fixed_n, mc_estimate, mlmc_estimate, fit_rates
-      ← estimators.hpp (host control logic restated from src/estimators.cpp)
+  run_level_draws, summarize_draws
+      ← estimators.hpp (the batch seams :106-128)
   assemble_and_solve / evaluate_qoi (batched) ← fem.hpp
+  DeviceGroup / GroupLevel (several GPUs, NCCL), Comm (one process per GPU)
+
+The reference's host control loop (estimate_adaptive, mlmc_estimate, …) is NOT restated here: it
+runs as the reference's own C++ over the GPU seam (integration/, Python binding `estimators.py`).
 
 Errors map onto ConfigError / NumericalError / SolverError / EmbeddingError (errors.hpp).
 Per-sample work never runs on the CPU: every draw goes through libosc_b200.so.
@@ -187,6 +190,21 @@ class Context:
     def launch_count(self) -> int:
         return self._lib.osc_ctx_launch_count(self.h)
 
+    def set_history(self, cap: int):
+        """osc_ctx_set_history: a failing draw call re-solves its first failing slot with the
+        residual history kept, so SolverError carries it (fem.cpp:359-379)."""
+        _check(self._lib.osc_ctx_set_history(self.h, int(cap)))
+
+    def failure_history(self):
+        """(slot, history ndarray) of the last failing osc_level_draws call, or (-1, None)."""
+        slot = C.c_int64(-1)
+        n = self._lib.osc_ctx_failure_history(self.h, C.byref(slot), None, 0)
+        if n <= 0:
+            return -1, None
+        h = np.empty(n)
+        self._lib.osc_ctx_failure_history(self.h, C.byref(slot), _p(h), n)
+        return slot.value, h
+
 
 _CTX: dict = {}
 
@@ -341,6 +359,17 @@ class DeviceLevel:
                 self.h = None
         except Exception:
             pass
+
+    def sums_reset(self, shift_y: float = 0.0, shift_q: float = 0.0):
+        """osc_level_sums_reset: start the level's running device sums
+        [n, Σ(Y−Ky), Σ(Y−Ky)², Σ(q−Kq), Σ(q−Kq)²] (every later draw call adds to them)."""
+        _check(self._lib.osc_level_sums_reset(self.h, float(shift_y), float(shift_q)))
+
+    def sums_read(self) -> np.ndarray:
+        """[n, Σ(Y−Ky), Σ(Y−Ky)², Σ(q−Kq), Σ(q−Kq)², Ky, Kq] from the device."""
+        out = np.zeros(7)
+        _check(self._lib.osc_level_sums_read(self.h, _p(out)))
+        return out
 
     def prefetch_xi(self, xi_next: Optional[np.ndarray], count: Optional[int] = None):
         """osc_level_prefetch_xi: arm the host ξ rows of the NEXT host-ξ draw call on this level
@@ -549,78 +578,7 @@ def evaluate_qoi(m: int, u: np.ndarray, problem: ProblemSpec, Z: Optional[np.nda
     return q
 
 
-# ---- level plans and draws (estimators.cpp) -------------------------------------------------------------
-def coarsest_level_bound(model: CovarianceModel) -> float:
-    """estimators.cpp:487-494."""
-    limit = model.lambda_ if model.family == CovFamily.SeparableExponential else \
-        math.sqrt(8.0 * model.nu) * model.lambda_
-    h = 1.0
-    while h > limit * (1.0 + 1e-12):
-        h *= 0.5
-    return h
-
-
-def choose_k_ell(model: CovarianceModel, h: float, padding: int, s: int, alpha: float,
-                 c_ratio: float, use_coarse_s: bool = False) -> int:
-    """estimators.cpp:239-272."""
-    if not alpha > 0:
-        raise ConfigError("choose_k_ell: alpha must be positive")
-    if not c_ratio > 0:
-        raise ConfigError("choose_k_ell: c_ratio must be positive")
-
-    def llround(x):
-        return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
-
-    h_eff = 2.0 * h if use_coarse_s else h
-    if model.family == CovFamily.SeparableExponential:
-        s_formula = 4.0 / (h_eff * h_eff)
-        k_real = s_formula ** ((3.0 - alpha) / 2.0) / (c_ratio + s_formula ** (-(alpha - 1.0) / 2.0))
-        return min(max(llround(k_real), 0), s - 1)
-    j_eff = 0.5 * padding if use_coarse_s else float(padding)
-    half_width = 1.0 / h_eff + j_eff
-    s_m = 4.0 * half_width * half_width
-    nu = model.nu
-    rhs = c_ratio * h_eff ** alpha * half_width
-
-    def residual(k):
-        return (s_m - k) ** (-(1.0 + nu) / 2.0) * k - rhs
-
-    lo, hi = 0.0, s_m - 1.0
-    if hi <= lo or residual(hi) < 0.0:
-        import sys
-        print(f"choose_k_ell: no root in (0, s-1) for {model.describe()} at h = {h}; "
-              "smoothing disabled on this level", file=sys.stderr)
-        return 0
-    while hi - lo > 0.5:
-        mid = 0.5 * (lo + hi)
-        if residual(mid) < 0.0:
-            lo = mid
-        else:
-            hi = mid
-    return min(max(llround(0.5 * (lo + hi)), 0), s - 1)
-
-
-def richardson_bias(mean_diff: float, alpha: float, c_tilde_over_c: float = 1.0,
-                    smoothed_extrapolant: bool = False) -> float:
-    """estimators.cpp:274-283."""
-    if not alpha > 0:
-        raise ConfigError("richardson_bias: alpha must be positive")
-    denom = (1.0 - c_tilde_over_c * 2.0 ** alpha) if smoothed_extrapolant else (1.0 - 2.0 ** alpha)
-    if abs(denom) < 0.1:
-        raise NumericalError("richardson_bias: extrapolation denominator below 0.1")
-    return abs(mean_diff) / abs(denom)
-
-
-def _is_power_of_two_inverse(h: float) -> Optional[int]:
-    if not (h > 0.0) or h > 1.0:
-        return None
-    inv = 1.0 / h
-    m = int(round(inv))
-    if abs(inv - m) > 1e-9 or m < 1 or (m & (m - 1)) != 0:
-        return None
-    return m
-
-
+# ---- level plans and draws (estimators.hpp:34-41,106-128) ------------------------------------------------
 @dataclass
 class LevelPlan:
     ell: int
@@ -632,8 +590,12 @@ class LevelPlan:
 
 
 def make_level_plan(ell: int, h0: float, problem: ProblemSpec, opt: EstimatorOptions,
-                    operator: Optional[EmbeddingOperator] = None) -> LevelPlan:
-    """estimators.cpp:169-198. `operator` injects a prebuilt (e.g. OSC1-loaded) spectrum."""
+                    operator: Optional[EmbeddingOperator] = None, k_trunc: Optional[int] = None) -> LevelPlan:
+    """LevelPlan of level ell above h0 (estimators.cpp:169-198): grid m = 2^ell / h0, its embedding
+    operator (or the injected `operator`, e.g. OSC1-loaded), and the truncation count: `k_trunc`
+    when given, s/2 for SmoothingRule.HalfSpectrum, 0 for Off. The Adaptive rule (choose_k_ell) and
+    smoothing_lstar_only belong to the reference's own planner, which runs over the GPU seam
+    (paper_2306_13493_b200.estimators)."""
     m0 = _is_power_of_two_inverse(h0)
     if m0 is None:
         raise ConfigError("make_level_plan: h0 must be a negative power of two")
@@ -645,17 +607,27 @@ def make_level_plan(ell: int, h0: float, problem: ProblemSpec, opt: EstimatorOpt
         raise ConfigError("make_level_plan: grid too fine")
     grid = GridSpec.square(m)
     op = operator if operator is not None else build_operator(grid, problem.model)
-    k = 0
-    if opt.smoothing != SmoothingRule.Off:
-        resolved = h <= coarsest_level_bound(problem.model) * (1.0 + 1e-12)
-        if not (opt.smoothing_lstar_only and resolved):
-            if opt.smoothing == SmoothingRule.HalfSpectrum:
-                k = op.s // 2
-            else:
-                k = choose_k_ell(problem.model, h, op.padding[0], op.s, opt.alpha, opt.c_ratio,
-                                 opt.smoothing_use_coarse_s)
+    if k_trunc is not None:
+        k = int(k_trunc)
+    elif opt.smoothing == SmoothingRule.Off:
+        k = 0
+    elif opt.smoothing == SmoothingRule.HalfSpectrum and not opt.smoothing_lstar_only:
+        k = op.s // 2
+    else:
+        raise ConfigError("make_level_plan: the Adaptive / lstar_only truncation rule is the reference's "
+                          "(choose_k_ell): pass k_trunc, or use paper_2306_13493_b200.estimators")
     k = min(max(k, 0), op.s - 1)
     return LevelPlan(ell, h, grid, op, op.truncated(k) if k > 0 else None, k)
+
+
+def _is_power_of_two_inverse(h: float) -> Optional[int]:
+    if not (h > 0.0) or h > 1.0:
+        return None
+    inv = 1.0 / h
+    m = int(round(inv))
+    if abs(inv - m) > 1e-9 or m < 1 or (m & (m - 1)) != 0:
+        return None
+    return m
 
 
 class LevelDraws:
@@ -687,13 +659,15 @@ def run_level_draws(plan: LevelPlan, coarse_grid: Optional[GridSpec], truncate_f
                     truncate_coarse: bool, problem: ProblemSpec, opt: EstimatorOptions, frm: int,
                     to: int, draws: LevelDraws, *, ctx: Optional[Context] = None,
                     xi: Optional[np.ndarray] = None, xi_next: Optional[np.ndarray] = None,
-                    dist=None) -> LevelDraws:
+                    dist=None, group: Optional["DeviceGroup"] = None) -> LevelDraws:
     """run_level_draws (estimators.hpp:112-118): samples [frm, to) land in slots [frm, to) of
     `draws`; sample i uses NormalStream(opt.seed, ℓ, i) (or row i-frm of xi). `xi_next` (host
     ξ of the caller's next batch, see DeviceLevel.prefetch_xi) is copied under this call's solves,
-    so the next call with that array runs without an exposed H2D copy. With `dist`
-    (paper_2306_13493_b200.dist.Shard) the range is split into contiguous per-rank shards and
-    the slots are all-gathered, so every rank ends with identical draws."""
+    so the next call with that array runs without an exposed H2D copy. With `group` (DeviceGroup,
+    one process, several GPUs) or `dist` (paper_2306_13493_b200.dist.Shard, one process per GPU)
+    the range is split into contiguous per-device shards; every slot still receives its own
+    sample. A non-converged sample raises SolverError carrying its residual history when the
+    context has history capture on (Context.set_history)."""
     if to < frm:
         raise ConfigError("run_level_draws: to < from")
     if draws.q_fine.size < to:
@@ -706,6 +680,9 @@ def run_level_draws(plan: LevelPlan, coarse_grid: Optional[GridSpec], truncate_f
     if dist is not None:
         return dist.run_level_draws(plan, coarse_grid, truncate_fine, truncate_coarse, problem,
                                     opt, frm, to, draws, ctx=ctx, xi=xi)
+    if group is not None:
+        return group.run_level_draws(plan, coarse_grid, truncate_fine, truncate_coarse, problem, opt,
+                                     frm, to, draws, xi=xi)
     ctx = ctx or default_context()
     lev = plan.op.device_level(ctx, plan.k_trunc)
     cnt = to - frm
@@ -725,6 +702,8 @@ def run_level_draws(plan: LevelPlan, coarse_grid: Optional[GridSpec], truncate_f
                                    int(to), flags, _p(xi_arr), _p(qf), _p(qc), _p(itf), _p(itc),
                                    _p(st), None)
     wall = time.perf_counter() - t0
+    if code == L.OSC_ERR_SOLVER:
+        _check(code, status=st, residual_history=ctx.failure_history()[1])
     _check(code, status=st)
     draws.q_fine[frm:to] = qf
     draws.q_coarse[frm:to] = qc if has_coarse else 0.0
@@ -757,235 +736,132 @@ def summarize_draws(draws: LevelDraws, has_coarse: bool) -> DrawStats:
     return DrawStats(int(out[0]), out[1], out[2], out[3], out[4], mean_wall)
 
 
-# ---- estimators (estimators.cpp:103-418) -------------------------------------------------------------------
-@dataclass
-class LevelStats:
-    n: int = 0
-    mean_y: float = 0.0
-    var_y: float = 0.0
-    mean_q: float = 0.0
-    var_q: float = 0.0
-    cost_wall_per_sample: float = 0.0
-    cost_model_per_sample: float = 0.0
-    n_real: float = 0.0
+# ---- several GPUs (osc_group / osc_comm) ------------------------------------------------------------
+class DeviceGroup:
+    """osc_group: one process drives n devices (one context and one host thread per device, NCCL
+    communicators). run_level_draws cuts [from, to) into contiguous per-device chunks (the chunking
+    of parallel_samples, estimators.cpp:32-63); the per-level sums are reduced by one NCCL
+    all-reduce of device buffers."""
+
+    def __init__(self, n_devices: int, devices: Optional[Sequence[int]] = None):
+        self._lib = L.lib()
+        dv = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+        h = C.c_void_p()
+        _check(self._lib.osc_group_create(int(n_devices), _p(dv), C.byref(h)))
+        self.h = h.value
+        self.n = int(n_devices)
+        self._levels = {}
+
+    def close(self):
+        if getattr(self, "h", None):
+            for gl in self._levels.values():
+                gl.close()
+            self._levels.clear()
+            self._lib.osc_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def level(self, op: EmbeddingOperator, k_trunc: int = 0) -> "GroupLevel":
+        key = (id(op), int(k_trunc))
+        if key not in self._levels:
+            self._levels[key] = GroupLevel(self, op, int(k_trunc))
+        return self._levels[key]
+
+    def run_level_draws(self, plan, coarse_grid, truncate_fine, truncate_coarse, problem, opt, frm, to,
+                        draws, xi=None, level_sums: Optional[np.ndarray] = None) -> LevelDraws:
+        gl = self.level(plan.op, plan.k_trunc)
+        cnt = to - frm
+        qf, qc = np.empty(cnt), np.empty(cnt)
+        itf, itc = np.zeros(cnt, dtype=np.int32), np.zeros(cnt, dtype=np.int32)
+        st = np.zeros(cnt, dtype=np.int32)
+        has_coarse = coarse_grid is not None
+        flags = (L.DRAW_HAS_COARSE if has_coarse else 0) | \
+            (L.DRAW_TRUNC_FINE if truncate_fine else 0) | (L.DRAW_TRUNC_COARSE if truncate_coarse else 0)
+        xi_arr = None if xi is None else np.ascontiguousarray(xi, dtype=np.float64).reshape(cnt, plan.op.s)
+        ps = _problem_struct(problem, opt.solver)
+        t0 = time.perf_counter()
+        code = self._lib.osc_group_level_draws(gl.h, C.byref(ps), int(opt.seed), int(plan.ell), int(frm), int(to),
+                                               flags, _p(xi_arr), _p(qf), _p(qc), _p(itf), _p(itc), _p(st),
+                                               _p(level_sums))
+        wall = time.perf_counter() - t0
+        _check(code, status=st)
+        if draws.q_fine.size < to:
+            draws.resize(to)
+        draws.q_fine[frm:to] = qf
+        draws.q_coarse[frm:to] = qc if has_coarse else 0.0
+        draws.wall[frm:to] = wall / max(cnt, 1)
+        draws.iters_fine[frm:to] = itf
+        draws.iters_coarse[frm:to] = itc
+        return draws
 
 
-@dataclass
-class MlmcReport:
-    estimate: float = 0.0
-    levels: List[LevelStats] = field(default_factory=list)
-    level_h: List[float] = field(default_factory=list)
-    bias_estimate: float = 0.0
-    sampling_error: float = 0.0
-    total_cost_model: float = 0.0
-    total_cost_wall: float = 0.0
-    converged: bool = True
-    message: str = ""
+class GroupLevel:
+    """osc_group_level: one osc_level (√λ in HBM) per device of a DeviceGroup."""
+
+    def __init__(self, group: DeviceGroup, op: EmbeddingOperator, k_trunc: int):
+        self._lib = group._lib
+        h = C.c_void_p()
+        eig = np.ascontiguousarray(op._eig_full, dtype=np.float64)
+        _check(self._lib.osc_group_level_create(group.h, op.grid.m(0), op.padding[0], _p(eig), int(k_trunc),
+                                                C.byref(h)))
+        self.h = h.value
+
+    def close(self):
+        if self.h:
+            self._lib.osc_group_level_destroy(self.h)
+            self.h = None
+
+    def sums_reset(self, shift_y: float = 0.0, shift_q: float = 0.0):
+        _check(self._lib.osc_group_level_sums_reset(self.h, float(shift_y), float(shift_q)))
+
+    def sums_allreduce(self) -> np.ndarray:
+        """NCCL all-reduce of every device's running level sums: [5 sums, Ky, Kq]."""
+        out = np.zeros(7)
+        _check(self._lib.osc_group_level_sums_allreduce(self.h, _p(out)))
+        return out
 
 
-class _LevelState:
-    def __init__(self, plan: LevelPlan, has_coarse: bool):
-        self.plan = plan
-        self.has_coarse = has_coarse
-        self.coarse = GridSpec.square(plan.grid.m(0) // 2) if has_coarse else None
-        self.truncate_fine = False
-        self.truncate_coarse = False
-        self.draws = LevelDraws()
-        self.moments = DrawStats()
-        self.n_real = 0.0
+class Comm:
+    """osc_comm: one process per GPU (torchrun). Rank 0 creates the NCCL id (Comm.unique_id()),
+    the launcher broadcasts it, every rank builds its Comm on its own Context."""
 
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(L.lib().osc_comm_unique_id(buf))
+        return bytes(buf)
 
-def _set_mode(st: _LevelState, opt: EstimatorOptions, is_finest: bool):
-    """estimators.cpp:114-122."""
-    ces = opt.smoothing != SmoothingRule.Off and st.plan.k_trunc > 0
-    new_fine, new_coarse = ces and not is_finest, ces
-    if (new_fine != st.truncate_fine or new_coarse != st.truncate_coarse) and len(st.draws):
-        st.draws.clear()
-    st.truncate_fine, st.truncate_coarse = new_fine, new_coarse
+    def __init__(self, ctx: Context, nranks: int, rank: int, uid: bytes):
+        self._lib = L.lib()
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(self._lib.osc_comm_create(ctx.h, int(nranks), int(rank), buf, C.byref(h)))
+        self.h = h.value
+        self.nranks, self.rank = int(nranks), int(rank)
 
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.osc_comm_destroy(self.h)
+            self.h = None
 
-def _make_state(ell, h0, problem, opt, is_finest, operators=None) -> _LevelState:
-    op = operators.get(ell) if operators else None
-    st = _LevelState(make_level_plan(ell, h0, problem, opt, op), ell > 0)
-    _set_mode(st, opt, is_finest)
-    return st
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
+    def allreduce_level_sums(self, level: DeviceLevel) -> np.ndarray:
+        out = np.zeros(7)
+        _check(self._lib.osc_comm_allreduce_level_sums(self.h, level.h, _p(out)))
+        return out
 
-def _finalize(states, opt, bias, converged, message) -> MlmcReport:
-    """estimators.cpp:147-165."""
-    rep = MlmcReport(bias_estimate=bias, converged=converged, message=message)
-    var_sum = 0.0
-    for st in states:
-        m = st.moments
-        ls = LevelStats(m.n, m.mean_y, m.var_y, m.mean_q, m.var_q, m.mean_wall,
-                        st.plan.h ** (-opt.gamma_model), st.n_real)
-        rep.levels.append(ls)
-        rep.level_h.append(st.plan.h)
-        rep.estimate += ls.mean_y
-        var_sum += ls.var_y / ls.n if ls.n > 0 else 0.0
-        rep.total_cost_model += ls.cost_model_per_sample * ls.n
-        rep.total_cost_wall += ls.cost_wall_per_sample * ls.n
-    rep.sampling_error = math.sqrt(var_sum)
-    return rep
-
-
-def _estimate_adaptive(problem, opt, h0, eps, initial_levels, allow_extension, *, ctx=None,
-                       dist=None, operators=None) -> MlmcReport:
-    """estimators.cpp:289-378 over the GPU seam run_level_draws."""
-    if not eps > 0:
-        raise ConfigError("estimate: eps must be positive")
-    eps2_half = 0.5 * eps * eps
-    pilot = max(2, opt.pilot_n)
-    l_start = max(0, min(initial_levels - 1, opt.l_max))
-    states = [_make_state(ell, h0, problem, opt, ell == l_start, operators)
-              for ell in range(l_start + 1)]
-    message, converged, bias = "", True, 0.0
-
-    def draw(st, have, target):
-        run_level_draws(st.plan, st.coarse, st.truncate_fine, st.truncate_coarse, problem, opt,
-                        have, target, st.draws, ctx=ctx, dist=dist)
-
-    outer = 0
-    while True:
-        if outer > 64:
-            converged, message = False, "sample allocation did not stabilise"
-            break
-        outer += 1
-        drew = False
-        for st in states:
-            have = len(st.draws)
-            if have < pilot:
-                draw(st, have, pilot)
-                drew = True
-        for st in states:
-            st.moments = summarize_draws(st.draws, st.has_coarse)
-        sum_cv = sum(math.sqrt(st.plan.h ** (-opt.gamma_model) * max(st.moments.var_y, 0.0))
-                     for st in states)
-        for st in states:
-            c_model = st.plan.h ** (-opt.gamma_model)
-            st.n_real = 2.0 / (eps * eps) * sum_cv * math.sqrt(max(st.moments.var_y, 0.0) / c_model)
-            target = max(int(math.ceil(st.n_real)), 2)
-            have = len(st.draws)
-            if target > have:
-                draw(st, have, target)
-                st.moments = summarize_draws(st.draws, st.has_coarse)
-                drew = True
-        if drew:
-            continue
-        finest = states[-1]
-        if len(states) == 1:
-            bias = opt.c_alpha * finest.plan.h ** opt.alpha
-            if not allow_extension or opt.l_max == 0:
-                message = "single level: bias taken from the weak-error model"
-                break
-        else:
-            bias = richardson_bias(finest.moments.mean_y, opt.alpha, opt.c_alpha_tilde_ratio,
-                                   finest.truncate_coarse and finest.plan.k_trunc > 0)
-        if allow_extension and bias * bias > eps2_half:
-            if len(states) - 1 >= opt.l_max:
-                converged = False
-                message = (f"bias {bias} still above target {math.sqrt(eps2_half)} at "
-                           f"L_max = {opt.l_max}")
-                break
-            new_l = len(states)
-            states.append(_make_state(new_l, h0, problem, opt, True, operators))
-            for st in states[:-1]:
-                _set_mode(st, opt, False)
-            continue
-        break
-    rep = _finalize(states, opt, bias, converged, message)
-    if rep.sampling_error ** 2 > eps2_half * (1.0 + 1e-9):
-        rep.converged = False
-        rep.message = (rep.message + "; " if rep.message else "") + "sampling error above target"
-    return rep
-
-
-def mc_estimate_fixed_n(problem: ProblemSpec, opt: EstimatorOptions, grid: GridSpec, n: int, *,
-                        ctx=None, dist=None, operator=None) -> MlmcReport:
-    """estimators.cpp:382-396 (smoothing forced off)."""
-    if n < 2:
-        raise ConfigError("mc_estimate_fixed_n: need at least 2 samples")
-    import copy
-    mc_opt = copy.copy(opt)
-    mc_opt.smoothing = SmoothingRule.Off
-    st = _make_state(0, 1.0 / grid.m(0), problem, mc_opt, True, {0: operator} if operator else None)
-    run_level_draws(st.plan, None, False, False, problem, mc_opt, 0, n, st.draws, ctx=ctx, dist=dist)
-    st.moments = summarize_draws(st.draws, False)
-    if st.moments.var_y == 0.0:
-        raise NumericalError("mc_estimate: sample variance is zero; degenerate input")
-    return _finalize([st], mc_opt, opt.c_alpha * (1.0 / grid.m(0)) ** opt.alpha, True,
-                     "fixed sample count")
-
-
-def mc_estimate(problem: ProblemSpec, opt: EstimatorOptions, eps: float,
-                fixed_h: Optional[float] = None, **kw) -> MlmcReport:
-    """estimators.cpp:398-412."""
-    import copy
-    if fixed_h is not None:
-        h = fixed_h
-    else:
-        target = (eps / (math.sqrt(2.0) * opt.c_alpha)) ** (1.0 / opt.alpha)
-        h = 1.0
-        while h >= target:
-            h *= 0.5
-    mc_opt = copy.copy(opt)
-    mc_opt.smoothing = SmoothingRule.Off
-    mc_opt.l_max = 0
-    return _estimate_adaptive(problem, mc_opt, h, eps, 1, False, **kw)
-
-
-def mlmc_estimate(problem: ProblemSpec, opt: EstimatorOptions, h0: float, eps: float,
-                  initial_levels: int = 1, **kw) -> MlmcReport:
-    """estimators.cpp:414-418."""
-    if initial_levels < 1:
-        raise ConfigError("mlmc_estimate: need at least one level")
-    return _estimate_adaptive(problem, opt, h0, eps, initial_levels, True, **kw)
-
-
-# ---- rate fits (estimators.cpp:420-485) -------------------------------------------------------------------
-@dataclass
-class RatePoint:
-    h: float = 0.0
-    mean_abs_y: float = 0.0
-    var_y: float = 0.0
-    cost: float = 0.0
-
-
-@dataclass
-class RateFit:
-    alpha: float = 0.0
-    c_alpha: float = 0.0
-    beta: float = 0.0
-    c_beta: float = 0.0
-    gamma: float = 0.0
-    c_gamma: float = 0.0
-
-
-def fit_rates(data: Sequence[RatePoint], warnings: Optional[list] = None) -> RateFit:
-    """Least-squares log-log fits of |E Y|, V[Y] and cost against h (estimators.cpp:428-485);
-    non-positive points are dropped per series (noted in `warnings`), < 3 survivors is an error."""
-    if len(data) < 3:
-        raise ConfigError("fit_rates: need at least 3 levels")
-
-    def fit(hs, vs, name):
-        xs, ys = [], []
-        for h, v in zip(hs, vs):
-            if not (v > 0.0) or not math.isfinite(v):
-                if warnings is not None:
-                    warnings.append(f"fit_rates: dropped non-positive {name} point at h = {h}; ")
-                continue
-            xs.append(math.log(h))
-            ys.append(math.log(v))
-        if len(xs) < 3:
-            raise ConfigError("fit_rates: fewer than 3 positive points for a series")
-        mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
-        sxx = sum((x - mx) ** 2 for x in xs)
-        sxy = sum((x - mx) * (y - my) for x, y in zip(xs, ys))
-        slope = sxy / sxx
-        return slope, math.exp(my - slope * mx)
-
-    h = [p.h for p in data]
-    a, ca = fit(h, [p.mean_abs_y for p in data], "|mean Y|")
-    b, cb = fit(h, [p.var_y for p in data], "var Y")
-    g, cg = fit(h, [p.cost for p in data], "cost")
-    return RateFit(a, ca, b, cb, -g, cg)
+    def allgather(self, local: np.ndarray) -> np.ndarray:
+        local = np.ascontiguousarray(local, dtype=np.float64).ravel()
+        out = np.empty(local.size * self.nranks)
+        _check(self._lib.osc_comm_allgather(self.h, _p(local), local.size, _p(out)))
+        return out

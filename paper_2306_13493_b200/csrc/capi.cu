@@ -9,6 +9,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -31,17 +34,15 @@ void sqrt_spectra(const double* eig, int64_t s, int64_t k_trunc, std::vector<dou
 
 using namespace osc;
 
-struct osc_ctx : Ctx {};
-struct osc_level : Level {};
-
 namespace {
 thread_local std::string g_last_error;
+}  // namespace
 
-template <typename F>
-int guarded(F&& f) {
+namespace osc {
+// exception → osc_status, message kept for osc_last_error() of the calling thread
+int c_api_error(const std::exception_ptr& ep) {
   try {
-    f();
-    return OSC_OK;
+    std::rethrow_exception(ep);
   } catch (const osc::Error& e) {
     g_last_error = e.what();
     return e.code;
@@ -54,6 +55,21 @@ int guarded(F&& f) {
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return OSC_ERR_CONFIG;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return OSC_ERR_CONFIG;
+  }
+}
+}  // namespace osc
+
+namespace {
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return OSC_OK;
+  } catch (...) {
+    return c_api_error(std::current_exception());
   }
 }
 
@@ -80,6 +96,20 @@ void d2h(Ctx* c, void* dst, const void* src, size_t bytes) {
   OSC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
 }
 }  // namespace
+
+// ---- per-device kernel attributes ---------------------------------------------------------------
+namespace osc {
+void smem_attr_raw(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, size_t>> done;
+  int dev = 0;
+  OSC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({dev, fn, bytes})) return;
+  OSC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.insert({dev, fn, bytes});
+}
+}  // namespace osc
 
 // ---- profiling ---------------------------------------------------------------------------------
 namespace osc {
@@ -138,6 +168,7 @@ const char* osc_last_error(void) { return g_last_error.c_str(); }
 int osc_ctx_create(int device, osc_ctx** out) {
   return guarded([&] {
     OSC_REQUIRE(out != nullptr, "osc_ctx_create: null out");
+    if (device < 0) OSC_CUDA(cudaGetDevice(&device));  // the calling thread's current device
     auto* c = new osc_ctx();
     c->device = device;
     try {
@@ -361,11 +392,19 @@ int osc_level_info(const osc_level* L, int* m, int* J, int* n, int64_t* s, int64
 }
 
 // ---- the fused per-level batch -----------------------------------------------------------------
-int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32_t ell,
-                    int64_t from, int64_t to, int flags, const double* xi, double* q_fine,
-                    double* q_coarse, int32_t* iters_fine, int32_t* iters_coarse, int32_t* status,
-                    double* level_sums) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace osc {
+// Body of osc_level_draws without the error mapping: returns (any non-finite field, any solver
+// failure). hist_cap > 0 keeps every solve's residual history (the failure re-run below);
+// hist_out (host, hist_cap per solve) then receives the fine solve's history, hist_coarse the
+// coarse one's. level_sums: this call's sums (per-call semantics of the header); with the level's
+// running sums enabled they are also added to L->run_sums on the device.
+std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t seed, uint32_t ell, int64_t from,
+                                 int64_t to, int flags, const double* xi, double* q_fine, double* q_coarse,
+                                 int32_t* iters_fine, int32_t* iters_coarse, int32_t* status, double* level_sums,
+                                 int hist_cap, double* hist_fine, double* hist_coarse) {
+  {
     OSC_REQUIRE(L && prob, "osc_level_draws: null argument");
     OSC_REQUIRE(to >= from && from >= 0, "osc_level_draws: need 0 <= from <= to");
     OSC_REQUIRE(prob->bc == OSC_BC_FLOWCELL || prob->bc == OSC_BC_DIRICHLET_ALL, "unknown bc");
@@ -376,7 +415,14 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     Ctx* c = L->ctx;
     set_device(c);
     const int64_t count = to - from;
-    if (count == 0) return;
+    if (count == 0) {
+      if (level_sums) {  // an empty shard still contributes zeros (group / comm reductions)
+        c->sums.ensure(sizeof(double) * 8);
+        OSC_CUDA(cudaMemsetAsync(c->sums.p, 0, sizeof(double) * 8, c->stream));
+        for (int j = 0; j < 5; ++j) level_sums[j] = 0.0;
+      }
+      return {false, false};
+    }
     const bool has_coarse = (flags & OSC_DRAW_HAS_COARSE) != 0;
     OSC_REQUIRE(!has_coarse || (L->m % 2 == 0 && L->m >= 2),
                 "restrict: target grid is not a nested coarsening");
@@ -404,6 +450,7 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     Bmax = std::min<int64_t>(Bmax, 1 << 16);
     // whole-batch mode: the rows are resident, so one chunk (full batch, no per-chunk overhead)
     const bool whole = pref_hit && count <= Bmax;
+    if (pref_hit && !whole) c->pref_xi = nullptr;  // not consumed: never reused by a later call
     const bool xi_chunked = xi_host && !whole;
     int64_t nchunks = (count + Bmax - 1) / Bmax;
     // host ξ: several chunks, so chunk i+1's H2D copy (copy stream, double-buffered) runs under
@@ -525,22 +572,22 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
       std::vector<int32_t> itc_tmp(B), stc_tmp(B);
       const double* guess = nullptr;
       if (has_coarse) {
-        solver_prepare(c, mc, B, 0);
+        solver_prepare(c, mc, B, hist_cap);
         c->solver.lev[0].k = kc;
         solver_run(c, prob, B);
         qoi_launch(c, prob, B, d_qc);
-        solver_results(c, B, itc_tmp.data(), stc_tmp.data(), nullptr);
+        solver_results(c, B, itc_tmp.data(), stc_tmp.data(), hist_coarse);
         if (nested) {
           OSC_CUDA(cudaMemcpyAsync(kc, c->solver.u, sizeof(double) * Nc * B, cudaMemcpyDeviceToDevice, c->stream));
           guess = kc;
         }
       }
       // fine solve + QoI
-      solver_prepare(c, m, B, 0);
+      solver_prepare(c, m, B, hist_cap);
       c->solver.lev[0].k = kf;
       solver_run(c, prob, B, guess);
       qoi_launch(c, prob, B, d_qf);
-      solver_results(c, B, it_tmp.data(), st_tmp.data(), nullptr);
+      solver_results(c, B, it_tmp.data(), st_tmp.data(), hist_fine);
       d2h(c, bad_tmp.data(), d_bad, sizeof(int) * B);
       OSC_CUDA(cudaStreamSynchronize(c->stream));
       for (int b = 0; b < B; ++b) {
@@ -559,6 +606,8 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
       }
       if (level_sums)
         level_sums_launch(c, d_qf, has_coarse ? d_qc : nullptr, B, level_sums[5], level_sums[6], d_sums);
+      if (L->sums_on)
+        level_sums_launch(c, d_qf, has_coarse ? d_qc : nullptr, B, L->shift_y, L->shift_q, L->run_sums.as<double>());
       if (q_fine) d2h(c, q_fine + c0, d_qf, sizeof(double) * B);
       if (q_coarse) {
         if (has_coarse) d2h(c, q_coarse + c0, d_qc, sizeof(double) * B);
@@ -568,10 +617,119 @@ int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32
     if (level_sums) d2h(c, level_sums, d_sums, sizeof(double) * 5);
     OSC_CUDA(cudaStreamSynchronize(c->stream));
     c->flush_stats();
-    if (any_bad) throw osc::Error(OSC_ERR_NUMERICAL, "assemble_and_solve: non-finite log-field value");
-    if (any_fail) throw osc::Error(OSC_ERR_SOLVER, "CG did not reach the relative residual within the iteration cap");
+    return {any_bad, any_fail};
+  }
+}
+
+// The error mapping of osc_level_draws (also used by the group's per-device workers). A solver
+// failure with osc_ctx_set_history on re-draws the first failing slot alone with the residual history
+// kept: sample i is a pure function of (seed, ℓ, i) (or xi row i), so the re-run repeats the failure
+// bit for bit and SolverError can carry the reference's residual_history (fem.cpp:359-379).
+void draws_checked(Level* L, const osc_problem* prob, uint64_t seed, uint32_t ell, int64_t from, int64_t to,
+                   int flags, const double* xi, double* q_fine, double* q_coarse, int32_t* iters_fine,
+                   int32_t* iters_coarse, int32_t* status, double* level_sums) {
+  OSC_REQUIRE(L, "osc_level_draws: null level");
+  Ctx* c = L->ctx;
+  std::vector<int32_t> st_local;
+  if (!status && c->hist_req > 0 && to > from) {
+    st_local.resize((size_t)(to - from));
+    status = st_local.data();
+  }
+  const auto r = draws_impl(L, prob, seed, ell, from, to, flags, xi, q_fine, q_coarse, iters_fine, iters_coarse,
+                            status, level_sums, 0, nullptr, nullptr);
+  if (r.first) throw osc::Error(OSC_ERR_NUMERICAL, "assemble_and_solve: non-finite log-field value");
+  if (!r.second) return;
+  c->fail_slot = -1;
+  c->fail_hist.clear();
+  if (c->hist_req > 0) {
+    int64_t i = from;
+    while (i < to && status[i - from] != OSC_ERR_SOLVER) ++i;
+    if (i < to) {
+      const int cap = c->hist_req;
+      std::vector<double> hf(cap, 0.0), hc(cap, 0.0);
+      double qf1, qc1;
+      int32_t itf1, itc1, st1;
+      const double* xi1 = xi ? xi + (i - from) * L->s : nullptr;
+      const bool host_pref = c->next_xi != nullptr;  // keep an armed prefetch for the caller's next call
+      const double* nx = c->next_xi;
+      const int64_t ncount = c->next_count, ns = c->next_s;
+      c->next_xi = nullptr;
+      draws_impl(L, prob, seed, ell, i, i + 1, flags, xi1, &qf1, &qc1, &itf1, &itc1, &st1, nullptr, cap, hf.data(),
+                 hc.data());
+      if (host_pref) {
+        c->next_xi = nx;
+        c->next_count = ncount;
+        c->next_s = ns;
+      }
+      // the failing solve's history (entries after the last iteration stay 0): the fine one when its
+      // last recorded ‖r‖/‖b‖ is above tol, else the coarse one
+      auto len_of = [&](const std::vector<double>& h) {
+        int n = 1;
+        while (n < cap && h[n] != 0.0) ++n;
+        return n;
+      };
+      const int lf = len_of(hf);
+      const bool fine_failed = !(hf[lf - 1] <= prob->tol);
+      const std::vector<double>& h = fine_failed ? hf : hc;
+      c->fail_slot = i;
+      c->fail_hist.assign(h.begin(), h.begin() + (fine_failed ? lf : len_of(hc)));
+    }
+  }
+  throw osc::Error(OSC_ERR_SOLVER, "CG did not reach the relative residual within the iteration cap");
+}
+}  // namespace osc
+
+extern "C" {
+
+int osc_level_draws(osc_level* L, const osc_problem* prob, uint64_t seed, uint32_t ell,
+                    int64_t from, int64_t to, int flags, const double* xi, double* q_fine,
+                    double* q_coarse, int32_t* iters_fine, int32_t* iters_coarse, int32_t* status,
+                    double* level_sums) {
+  return guarded([&] {
+    draws_checked(L, prob, seed, ell, from, to, flags, xi, q_fine, q_coarse, iters_fine, iters_coarse, status,
+                  level_sums);
   });
 }
+
+int osc_ctx_set_history(osc_ctx* c, int hist_cap) {
+  return guarded([&] {
+    OSC_REQUIRE(c && hist_cap >= 0, "osc_ctx_set_history: null context or negative cap");
+    c->hist_req = hist_cap;
+  });
+}
+
+int osc_ctx_failure_history(osc_ctx* c, int64_t* slot, double* out, int cap) {
+  if (!c) return -1;
+  if (slot) *slot = c->fail_slot;
+  const int n = (int)c->fail_hist.size();
+  for (int j = 0; j < std::min(n, cap); ++j) out[j] = c->fail_hist[j];
+  return n;
+}
+
+int osc_level_sums_reset(osc_level* L, double shift_y, double shift_q) {
+  return guarded([&] {
+    OSC_REQUIRE(L, "osc_level_sums_reset: null level");
+    set_device(L->ctx);
+    L->run_sums.ensure(sizeof(double) * 16);
+    OSC_CUDA(cudaMemsetAsync(L->run_sums.p, 0, sizeof(double) * 16, L->ctx->stream));
+    L->shift_y = shift_y;
+    L->shift_q = shift_q;
+    L->sums_on = true;
+  });
+}
+
+int osc_level_sums_read(osc_level* L, double out[7]) {
+  return guarded([&] {
+    OSC_REQUIRE(L && out, "osc_level_sums_read: null argument");
+    OSC_REQUIRE(L->sums_on, "osc_level_sums_read: running sums not enabled (osc_level_sums_reset)");
+    set_device(L->ctx);
+    d2h(L->ctx, out, L->run_sums.p, sizeof(double) * 5);
+    OSC_CUDA(cudaStreamSynchronize(L->ctx->stream));
+    out[5] = L->shift_y;
+    out[6] = L->shift_q;
+  });
+}
+
 
 int osc_summarize(const double* qf, const double* qc, int64_t n, int has_coarse, double out[5]) {
   // moments_of (estimators.cpp:82-101), slot order

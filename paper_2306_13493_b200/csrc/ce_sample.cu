@@ -577,7 +577,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   if constexpr (LOGN >= 5 && LOGN <= 12 && (PL::n / 2) % (2 * PL::NT) == 0) {
     if (rows2_env) {
       auto kern = ce_rows2_t_kernel<LOGN>;
-      OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sm)));
+      smem_attr(kern, (2 * sm));
       KScope ks(ctx, "ce_rows");
       kern<<<dim3((PL::n / 2) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(sqrt_lam, xi_dev, seed, ell,
                                                                                 index0, P, cs, tw, inter);
@@ -587,7 +587,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   }
   if (!rows_done) {
     auto kern = ce_rows_t_kernel<LOGN>;
-    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    smem_attr(kern, sm);
     KScope ks(ctx, "ce_rows");
     kern<<<dim3((PL::n / 2) / PL::NT, count), PL::THREADS, sm, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs,
                                                                       tw, inter);
@@ -602,7 +602,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   if constexpr (LOGN >= 5 && LOGN <= 12) {
     if (cols2_env) {
       auto kern = ce_cols2_t_kernel<LOGN>;
-      OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * sm)));
+      smem_attr(kern, (2 * sm));
       KScope ks(ctx, "ce_cols");
       kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
           inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag);
@@ -612,7 +612,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   }
   {
     auto kern = ce_cols_t_kernel<LOGN>;
-    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    smem_attr(kern, sm);
     KScope ks(ctx, "ce_cols");
     kern<<<dim3((P + PL::NT - 1) / PL::NT, count), PL::THREADS, sm, st>>>(inter, m, P, cs, 1.0 / PL::n,
                                                                            do_exp ? 1 : 0, tw, out_fine,
@@ -659,7 +659,7 @@ void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double*
     const CeGeom g = rows_geom(n);
     const dim3 grid((n / 2 + g.NT - 1) / g.NT, count);
     auto kern = ce_rows_kernel<E, MAXT>;
-    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    smem_attr(kern, g.smem);
     KScope ks(ctx, "ce_rows");
     kern<<<grid, g.threads, g.smem, st>>>(sqrt_lam, xi_dev, seed, ell, index0, n, g.NT, P, cs, tw, inter);
     OSC_CUDA(cudaGetLastError());
@@ -668,7 +668,7 @@ void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double*
     const CeGeom g = cols_geom(n, P);
     const dim3 grid((P + g.NT - 1) / g.NT, count);
     auto kern = ce_cols_kernel<E, MAXT>;
-    OSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    smem_attr(kern, g.smem);
     KScope ks(ctx, "ce_cols");
     kern<<<grid, g.threads, g.smem, st>>>(inter, n, m, g.NT, P, cs, 1.0 / n, do_exp ? 1 : 0, tw,
                                          out_fine, out_coarse, bad_flag);
@@ -825,8 +825,8 @@ void launch_generic(Ctx* ctx, const Level* L, const double* sqrt_lam, const doub
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = 2 * sizeof(double2) * (size_t)n;
   const int threads = std::min(256, std::max(32, ((n / 2 + 31) / 32) * 32));
-  OSC_CUDA(cudaFuncSetAttribute(ce_rows_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  OSC_CUDA(cudaFuncSetAttribute(ce_cols_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  smem_attr(ce_rows_generic_kernel, sm);
+  smem_attr(ce_cols_generic_kernel, sm);
   {
     KScope ks(ctx, "ce_rows");
     ce_rows_generic_kernel<<<dim3(n / 2, count), threads, sm, ctx->stream>>>(sqrt_lam, xi_dev, seed, ell, index0,

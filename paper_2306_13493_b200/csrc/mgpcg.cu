@@ -3890,13 +3890,12 @@ bool pcg_one_reduction() {
 bool l0_ring() {
   static const bool on = [] {
     const char* e = std::getenv("OSC_L0_RING");
-    const bool v = !(e && e[0] == '0');
-    if (v) {
-      cudaFuncSetAttribute(smooth_up_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L0R_SMEM_UP);
-      cudaFuncSetAttribute(restrict_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L0R_SMEM_DN);
-    }
-    return v;
+    return !(e && e[0] == '0');
   }();
+  if (on) {
+    smem_attr(smooth_up_ring_kernel, L0R_SMEM_UP);
+    smem_attr(restrict_ring_kernel, L0R_SMEM_DN);
+  }
   return on;
 }
 
@@ -3961,12 +3960,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       continue;
     }
     if (coarse_mode() == 2) {  // fused pre-smoother + restriction (z not stored)
-      static bool attr = false;
-      if (!attr) {
-        OSC_CUDA(cudaFuncSetAttribute(c_down_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)DN_RING_SMEM));
-        attr = true;
-      }
+      smem_attr(c_down_ring_kernel, DN_RING_SMEM);
       KScope ks(ctx, lvl_name("mg_down", l).c_str());
       c_down_ring_kernel<<<restrict_grid_w(C.m, B, CD_W), 32 * CD_W, DN_RING_SMEM, st>>>(l9, bc, w.opdep, L.r, pw_of(L),
                                                                           geo_of(C), C.r, w.flags);
@@ -3984,7 +3978,7 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     const SolverLevel& S = w.lev[ls];
     const int nl = w.nlev - ls;
     const size_t sm = sub_smem_bytes(S.m, nl);
-    OSC_CUDA(cudaFuncSetAttribute(sub_vcycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    smem_attr(sub_vcycle_kernel, sm);
     KScope ks(ctx, "mg_sub_vcycle");
     sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, w.opdep, hier_of(w, ls), S.r, S.z2, w.chol,
                                                   w.flags);
@@ -4037,21 +4031,11 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
       c_up_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2,
                                                               L.z2, w.flags);
     } else if (up_mode == 1) {
-      static bool attr = false;
-      if (!attr) {
-        OSC_CUDA(cudaFuncSetAttribute(c_up_ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)up_ring_smem<false>()));
-        attr = true;
-      }
+      smem_attr(c_up_ring_kernel<false>, up_ring_smem<false>());
       c_up_ring_kernel<false><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<false>(), st>>>(
           l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
     } else {
-      static bool attr = false;
-      if (!attr) {
-        OSC_CUDA(cudaFuncSetAttribute(c_up_ring_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)up_ring_smem<true>()));
-        attr = true;
-      }
+      smem_attr(c_up_ring_kernel<true>, up_ring_smem<true>());
       c_up_ring_kernel<true><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<true>(), st>>>(
           l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
     }
@@ -4097,14 +4081,8 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
     rediscretize_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(L0.k, g0, 1, bc, g0, L.C, L.E, L.Nw, L.NE, L.NW);
   } else if (mode != OSC_COARSE_REDISCRETIZE && !std::getenv("OSC_UNFUSED_SETUP")) {
     // fused tiled Galerkin setup per level pair (galerkin_tile_kernel)
-    static bool attr = false;
-    if (!attr) {
-      OSC_CUDA(cudaFuncSetAttribute(galerkin_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)galerkin_tile_smem(true)));
-      OSC_CUDA(cudaFuncSetAttribute(galerkin_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)galerkin_tile_smem(false)));
-      attr = true;
-    }
+    smem_attr(galerkin_tile_kernel<true>, galerkin_tile_smem(true));
+    smem_attr(galerkin_tile_kernel<false>, galerkin_tile_smem(false));
     for (int l = 0; l + 1 < w.nlev; ++l) {
       const SolverLevel& F = w.lev[l];
       const SolverLevel& C = w.lev[l + 1];
@@ -4175,7 +4153,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
   if (w.m <= 32 && w.nlev > 1 && w.hist_cap == 0 && !small_off) {
     // whole solve CTA-resident (one CTA per sample, one launch)
     const size_t sm = small_smem_bytes(w.m, w.nlev);
-    OSC_CUDA(cudaFuncSetAttribute(small_pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    smem_attr(small_pcg_kernel, sm);
     KScope ks(ctx, "small_pcg");
     small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, w.nlev, bc, w.opdep, prob->forcing, prob->forcing_value,
                                                prob->tol, prob->max_iter_factor, L0.k, hier_of(w, 0), w.chol,

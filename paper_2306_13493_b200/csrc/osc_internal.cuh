@@ -30,6 +30,14 @@ struct Error : std::runtime_error {
     if (!(cond)) throw ::osc::Error(OSC_ERR_CONFIG, msg); \
   } while (0)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: set once per (current device,
+// kernel, size); thread-safe (one host thread per device may launch concurrently).
+void smem_attr_raw(const void* fn, size_t bytes);
+template <class K>
+inline void smem_attr(K* fn, size_t bytes) {
+  smem_attr_raw(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // ---- device buffer (grow-only) --------------------------------------------------------
 struct DevBuf {
   void* p = nullptr;
@@ -133,6 +141,11 @@ struct Ctx {
   int64_t pref_count = 0, pref_s = 0;
   DevBuf xi_pref;
   cudaEvent_t ev_pref = nullptr, ev_pref_read = nullptr;
+  // residual history of failing samples (osc_ctx_set_history): the first failing slot of the last
+  // osc_level_draws call is re-solved with the history kept (fem.cpp:359-379 SolverError::history)
+  int hist_req = 0;
+  int64_t fail_slot = -1;
+  std::vector<double> fail_hist;
   int stat_class(const char* name);
   cudaEvent_t pool_event();
   void flush_stats();
@@ -143,6 +156,11 @@ struct Level {
   int m = 0, J = 0, n = 0;
   int64_t s = 0, k_trunc = 0;
   DevBuf sqrt_full, sqrt_trunc, twiddle;  // twiddle: n complex exp(+2πi t/n)
+  // running per-level sums in HBM (osc_level_sums_reset): [0..4] = [n, Σ(Y−Ky), Σ(Y−Ky)², Σ(q−Kq),
+  // Σ(q−Kq)²] accumulated by every osc_level_draws call; [8..12] receive the cross-rank reduction
+  DevBuf run_sums;
+  bool sums_on = false;
+  double shift_y = 0.0, shift_q = 0.0;
 };
 
 // ---- launchers --------------------------------------------------------------------------
@@ -176,3 +194,7 @@ void normals_launch(Ctx* ctx, uint64_t seed, uint32_t ell, uint64_t index0, int 
                     int64_t s, double* out);
 
 }  // namespace osc
+
+// the C-ABI's opaque handles are the internal objects
+struct osc_ctx : osc::Ctx {};
+struct osc_level : osc::Level {};

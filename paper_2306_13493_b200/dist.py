@@ -26,11 +26,14 @@ def split_range(frm: int, to: int, rank: int, world: int):
 class Shard:
     """Shards run_level_draws over the ranks of a torch.distributed process group."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, draw_fn=None):
+        """draw_fn(plan, coarse_grid, tf, tc, problem, opt, lo, hi, draws, ctx=, xi=) draws the local
+        shard into `draws` (default: api.run_level_draws on this rank's GPU); tests inject a stub."""
         import torch.distributed as dist
         if not dist.is_initialized():
             raise RuntimeError("Shard needs torch.distributed to be initialised")
         self.dist = dist
+        self.draw_fn = draw_fn
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -66,8 +69,8 @@ class Shard:
         local = api.LevelDraws()
         xi_local = None if xi is None else np.asarray(xi).reshape(to - frm, -1)[lo - frm:hi - frm]
         if hi > lo:
-            api.run_level_draws(plan, coarse_grid, truncate_fine, truncate_coarse, problem, opt, lo,
-                                hi, local, ctx=ctx, xi=xi_local)
+            fn = self.draw_fn or api.run_level_draws
+            fn(plan, coarse_grid, truncate_fine, truncate_coarse, problem, opt, lo, hi, local, ctx=ctx, xi=xi_local)
         n = hi - lo
         packed = np.zeros((n, 5))
         if n:
@@ -87,14 +90,16 @@ class Shard:
         return draws
 
 
-def level_sums(q_fine: np.ndarray, q_coarse, shift_y: float = 0.0, shift_q: float = 0.0) -> np.ndarray:
-    """Host restatement of the device level sums (for the all-reduce path on CPU ranks)."""
+def level_sums(q_fine: np.ndarray, q_coarse, shift_y: float, shift_q: float) -> np.ndarray:
+    """Host restatement of the device level sums (for the all-reduce path on CPU ranks). The shifts
+    must be common to all ranks and close to the level means (e.g. the pilot means), so the variance
+    (Σ(Y−K)² − (Σ(Y−K))²/n)/(n−1) does not cancel."""
     y = (q_fine - q_coarse if q_coarse is not None else q_fine) - shift_y
     q = q_fine - shift_q
     return np.array([q_fine.size, y.sum(), (y * y).sum(), q.sum(), (q * q).sum()])
 
 
-def moments_from_sums(s: np.ndarray, shift_y: float = 0.0, shift_q: float = 0.0):
+def moments_from_sums(s: np.ndarray, shift_y: float, shift_q: float):
     """(n, mean_y, var_y, mean_q, var_q) from all-reduced shifted sums."""
     n = s[0]
     mean_y = s[1] / n + shift_y

@@ -61,3 +61,60 @@ def test_gloo_world2_gather_and_sums():
         p.join(timeout=60)
     assert sorted(r[0] for r in res) == [0, 1]
     assert all(r[1] and r[2] for r in res)
+
+
+def _stub_draw(plan, coarse_grid, tf, tc, problem, opt, lo, hi, draws, ctx=None, xi=None):
+    """A deterministic per-slot 'sample' (no GPU): q_fine = sin(i), q_coarse = cos(i) (+ ξ row sum)."""
+    if draws.q_fine.size < hi:
+        draws.resize(hi)
+    i = np.arange(lo, hi, dtype=np.float64)
+    extra = 0.0 if xi is None else np.asarray(xi).reshape(hi - lo, -1).sum(axis=1)
+    draws.q_fine[lo:hi] = np.sin(i) + extra
+    draws.q_coarse[lo:hi] = np.cos(i)
+    draws.wall[lo:hi] = 1e-3
+    draws.iters_fine[lo:hi] = (i % 7).astype(np.int32)
+    draws.iters_coarse[lo:hi] = (i % 5).astype(np.int32)
+    return draws
+
+
+def _shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2306_13493_b200 import api
+        from paper_2306_13493_b200.dist import Shard
+        sh = Shard(draw_fn=_stub_draw)
+        ok = True
+        for frm, to in [(0, 37), (5, 6), (3, 3 + 2 * world + 1), (100, 164)]:  # uneven and short ranges
+            d = api.LevelDraws()
+            d.resize(frm)
+            d.q_fine[:] = -1.0
+            xi = np.arange((to - frm) * 4, dtype=np.float64).reshape(to - frm, 4)
+            sh.run_level_draws(None, None, False, False, None, None, frm, to, d, xi=xi)
+            want = _stub_draw(None, None, False, False, None, None, frm, to, api.LevelDraws(), xi=xi)
+            ok &= len(d) == to and np.all(d.q_fine[:frm] == -1.0)
+            ok &= np.array_equal(d.q_fine[frm:to], want.q_fine[frm:to])
+            ok &= np.array_equal(d.q_coarse[frm:to], want.q_coarse[frm:to])
+            ok &= np.array_equal(d.iters_fine[frm:to], want.iters_fine[frm:to])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_shard_run_level_draws(world):
+    """Shard.run_level_draws over world 2 and 3 (uneven splits, ranks with empty shards): every rank
+    ends with the slot-ordered draws a single process would produce, ξ rows routed to their shard."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == list(range(world))
+    assert all(r[1] for r in res), res

@@ -1,6 +1,6 @@
 """CPU tests of the product's host side: the C-ABI library loads and exports every symbol
 include/oscfield_b200.h declares; host level setup (spectrum, padding, truncation) and the
-estimator host math agree with the reference golden vectors; no GPU compute is called."""
+routing of the reference's own estimators onto the GPU seam is in place; no GPU compute is called."""
 import ctypes
 import os
 import re
@@ -81,18 +81,46 @@ def test_osc1_reads_reference_dump(P, ref, tmp_path):
     assert op.padding[0] == r.J and np.array_equal(op.eigenvalues, r.eigenvalues())
 
 
-def test_estimator_host_math(P, golden):
+REF_SRC = "/root/reference/proj/src"
+
+
+def test_reference_estimators_route_to_gpu_seam(P, tmp_path):
+    """The GPU-routed reference build: compiling the pristine estimators.cpp with
+    integration/route_run_level_samples.hpp force-included makes every draw of the reference's own
+    estimate_adaptive / mc_estimate_fixed_n call the (LevelPlan&) overload defined by the GPU seam —
+    the file-local CPU run_level_samples and its std::thread pool are no longer referenced."""
+    import subprocess
+    if not os.path.isdir(REF_SRC):
+        pytest.skip("reference sources not present")
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration")
+    obj = str(tmp_path / "est.o")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-c", "-w", "-I/root/reference/proj/include", f"-I{inc}/shims",
+                    "-DDraw=LevelDraw", "-include", f"{inc}/shims/std_max_fix.hpp", "-include",
+                    f"{inc}/route_run_level_samples.hpp", os.path.join(REF_SRC, "estimators.cpp"), "-o", obj],
+                   check=True)
+    syms = subprocess.run(["nm", "-C", obj], capture_output=True, text=True, check=True).stdout
+    routed = [l for l in syms.splitlines() if "run_level_samples(oscfield::LevelPlan&" in l]
+    assert any(l.strip().startswith("U ") for l in routed), routed  # undefined here: the seam defines it
+    assert "(anonymous namespace)::run_level_samples" not in syms
+    assert "parallel_samples" not in syms
+    # and the built library (if present) carries the seam's definition
+    from paper_2306_13493_b200 import estimators as E
+    if os.path.exists(E.LIB_PATH):
+        lib = subprocess.run(["nm", "-DC", E.LIB_PATH], capture_output=True, text=True, check=True).stdout
+        assert any(" T " in l and "run_level_samples(oscfield::LevelPlan&" in l for l in lib.splitlines())
+
+
+def test_make_level_plan_rules(P):
     api = P.api
-    ks = [api.choose_k_ell(api.CovarianceModel.separable_exponential(1, 0.01), h, 0, int((2 / h) ** 2), 1, 1)
-          for h in (1 / 16, 1 / 32, 1 / 64)]
-    ks += [api.choose_k_ell(api.CovarianceModel.matern(1, 0.1, 1.5), h, 0, int((2 / h) ** 2), 1, 1)
-           for h in (1 / 16, 1 / 32)]
-    assert ks == [int(x) for x in golden["k_ell"]]
-    b = golden["coarsest_bound"]
-    assert api.coarsest_level_bound(api.CovarianceModel.separable_exponential(1, 0.01)) == b[0]
-    assert api.coarsest_level_bound(api.CovarianceModel.matern(1, 0.03, 1.5)) == b[1]
-    with pytest.raises(api.NumericalError):
-        api.richardson_bias(1.0, 1.0, 0.5, True)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1.0, 0.1))
+    p0 = api.make_level_plan(1, 1 / 8, prob, api.EstimatorOptions())
+    assert p0.grid.m(0) == 16 and p0.k_trunc == 0 and p0.op_smoothed is None
+    ph = api.make_level_plan(1, 1 / 8, prob, api.EstimatorOptions(smoothing=api.SmoothingRule.HalfSpectrum),
+                             operator=p0.op)
+    assert ph.k_trunc == p0.op.s // 2
+    assert api.make_level_plan(1, 1 / 8, prob, api.EstimatorOptions(), operator=p0.op, k_trunc=7).k_trunc == 7
+    with pytest.raises(api.ConfigError):  # the Adaptive rule is the reference planner's
+        api.make_level_plan(1, 1 / 8, prob, api.EstimatorOptions(smoothing=api.SmoothingRule.Adaptive))
 
 
 def test_summarize_matches_welford(P, port):
@@ -139,20 +167,6 @@ def test_padded_embedding_sizes(P, ref):
             while v % f == 0:
                 v //= f
         assert v == 1
-
-
-def test_fit_rates(P):
-    api = P.api
-    pts = [api.RatePoint(h, 0.3 * h, 2.0 * h ** 2, 5.0 * h ** -2) for h in (1 / 8, 1 / 16, 1 / 32, 1 / 64)]
-    f = api.fit_rates(pts)
-    assert abs(f.alpha - 1) < 1e-12 and abs(f.beta - 2) < 1e-12 and abs(f.gamma - 2) < 1e-12
-    assert abs(f.c_alpha - 0.3) < 1e-12
-    w = []
-    pts[0].mean_abs_y = 0.0
-    f = api.fit_rates(pts, w)
-    assert w and abs(f.alpha - 1) < 1e-12
-    with pytest.raises(api.ConfigError):
-        api.fit_rates(pts[:2])
 
 
 @pytest.mark.parametrize("bc", [0, 1])

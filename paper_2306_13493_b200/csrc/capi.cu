@@ -9,9 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
-#include <set>
-#include <tuple>
 #include <string>
 #include <vector>
 
@@ -100,14 +99,16 @@ void d2h(Ctx* c, void* dst, const void* src, size_t bytes) {
 // ---- per-device kernel attributes ---------------------------------------------------------------
 namespace osc {
 void smem_attr_raw(const void* fn, size_t bytes) {
+  // the attribute is a maximum: keep the largest size set so far per (device, kernel), never lower it
   static std::mutex mu;
-  static std::set<std::tuple<int, const void*, size_t>> done;
+  static std::map<std::pair<int, const void*>, size_t> set_max;
   int dev = 0;
   OSC_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> g(mu);
-  if (done.count({dev, fn, bytes})) return;
+  size_t& cur = set_max[{dev, fn}];
+  if (bytes <= cur) return;
   OSC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  done.insert({dev, fn, bytes});
+  cur = bytes;
 }
 }  // namespace osc
 

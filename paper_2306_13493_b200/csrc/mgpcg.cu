@@ -923,12 +923,14 @@ __device__ __forceinline__ void init_finish(const Geo& g, double tol, int max_it
     scal[b * S_NSCAL + S_REL] = rel;
     scal[b * S_NSCAL + S_RZ] = 0.0;
     scal[b * S_NSCAL + S_BETA] = 0.0;
-    const int act = rel > tol ? 1 : 0;  // NaN (b = 0) → converged, as in fem.cpp:367
+    const int64_t cap = (int64_t)max_iter_factor * g.N;
+    // NaN (b = 0) → converged, as in fem.cpp:367; a zero cap fails before the first iteration
+    // (fem.cpp:374: iter++ >= max_iter)
+    const int act = (rel > tol && cap > 0) ? 1 : 0;
     flags[b * F_NFLAGS + F_ACTIVE] = act;
     flags[b * F_NFLAGS + F_ITERS] = 0;
-    flags[b * F_NFLAGS + F_STATUS] = 0;
+    flags[b * F_NFLAGS + F_STATUS] = (rel > tol && cap <= 0) ? OSC_ERR_SOLVER : 0;
     flags[b * F_NFLAGS + F_FIRST] = 1;
-    const int64_t cap = (int64_t)max_iter_factor * g.N;
     flags[b * F_NFLAGS + F_MAXIT] = (int)(cap < 0x7fffffff ? cap : 0x7fffffff);
     if (hist && hist_cap > 0) hist[(int64_t)b * hist_cap] = rel;
     if (act) atomicAdd(n_active, 1);

@@ -60,15 +60,79 @@ __device__ __forceinline__ double2 normal_pair_k(const PhiloxKeys& ks, uint32_t 
                                                  uint32_t j) {
   return box_muller(philox10k(make_uint4(j, ell, (uint32_t)idx, (uint32_t)(idx >> 32)), ks));
 }
+// Box–Muller on the device. The math library's log / sincospi cost ~100 instructions per pair and
+// materialise every 64-bit polynomial coefficient with two UMOVs at each use (14% of the CE row
+// pass's instruction stream, profiles/r2_ce_rows_opcodes.txt); here the coefficients sit in the
+// constant bank, which DFMA reads as a c[][] operand, and the arguments' known ranges drop the
+// special-case paths:
+//   log(u1), u1 ∈ [2^-54, 1): the classical reduction u1 = 2^k (1 + f), 1 + f ∈ [√½, √2),
+//     s = f/(2 + f), log(1+f) = f − ½f² + s(½f² + R(s²)) with R the degree-7 minimax polynomial of
+//     the published fdlibm/musl log (≤ 1 ulp);
+//   cos/sin(2π u2), u2 ∈ (0, 1): t = 4u2, q = rint(t), r = t − q ∈ [−½, ½] (both exact), then the
+//     Taylor series of sin/cos(πr/2) to r^17 / r^18 (truncation < 1e-19) and the quadrant q mod 4.
+// The angle is exact (as sincospi), not the rounded 2π·u2 of the reference's std::cos: the normals
+// differ from glibc's by a few ulp (≤ 1e-14 relative), fields stay within 1e-10.
+static __constant__ double k_bm[] = {
+    // log: Lg1..Lg7, ln2_hi, ln2_lo
+    6.666666666666735130e-01, 3.999999999940941908e-01, 2.857142874366239149e-01, 2.222219843214978396e-01,
+    1.818357216161805012e-01, 1.531383769920937332e-01, 1.479819860511658591e-01, 6.93147180369123816490e-01,
+    1.90821492927058770002e-10,
+    // sin(πr/2) / r: (−1)^k (π/2)^(2k+1) / (2k+1)!, k = 0..8
+    1.57079632679489656e+00, -6.45964097506246282e-01, 7.96926262461670476e-02, -4.68175413531868832e-03,
+    1.60441184787359829e-04, -3.59884323521208518e-06, 5.69217292196792668e-08, -6.68803510981146768e-10,
+    6.06693573110619553e-12,
+    // cos(πr/2): (−1)^k (π/2)^(2k) / (2k)!, k = 0..9
+    1.0, -1.23370055013616975e+00, 2.53669507901048030e-01, -2.08634807633529609e-02, 9.19260274839426585e-04,
+    -2.52020423730606066e-05, 4.71087477881817174e-07, -6.38660308379185209e-09, 6.56596311497947280e-11,
+    -5.29440020073462348e-13};
+
+__device__ __forceinline__ double bm_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  return fma(y, fma(-d, y, 1.0), y);
+}
+
+// log(x) for x ∈ [2^-54, 1) (normal, positive)
+__device__ __forceinline__ double bm_log(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const int mh = hi & 0x000fffff;
+  const bool big = mh >= 0x6a09e;  // mantissa ≥ √2: use (1 + f)/2 and k + 1
+  const int k = (hi >> 20) - 1023 + (big ? 1 : 0);
+  const double f = __hiloint2double((mh | 0x3ff00000) - (big ? 0x00100000 : 0), lo) - 1.0;
+  const double hfsq = 0.5 * f * f;
+  const double s = f * bm_rcp(2.0 + f);
+  const double z = s * s, w = z * z;
+  const double t1 = w * (k_bm[1] + w * (k_bm[3] + w * k_bm[5]));
+  const double t2 = z * (k_bm[0] + w * (k_bm[2] + w * (k_bm[4] + w * k_bm[6])));
+  const double dk = (double)k;
+  return dk * k_bm[7] - ((hfsq - (s * (hfsq + (t2 + t1)) + dk * k_bm[8])) - f);
+}
+
+// (cos 2πu, sin 2πu) for u ∈ (0, 1)
+__device__ __forceinline__ double2 bm_cossin_2pi(double u) {
+  const double t = 4.0 * u;
+  const double q = rint(t);
+  const double r = t - q;
+  const double z = r * r;
+  double ps = k_bm[17];
+#pragma unroll
+  for (int i = 16; i >= 9; --i) ps = fma(ps, z, k_bm[i]);
+  ps *= r;
+  double pc = k_bm[27];
+#pragma unroll
+  for (int i = 26; i >= 18; --i) pc = fma(pc, z, k_bm[i]);
+  const int qi = (int)q & 3;
+  const double cm = (qi & 1) ? ps : pc, sm = (qi & 1) ? pc : ps;
+  return make_double2((qi == 1 || qi == 2) ? -cm : cm, qi >= 2 ? -sm : sm);
+}
+
 __device__ __forceinline__ double2 box_muller(uint4 r) {
   const double u1 = ((double)((((uint64_t)r.x << 32) | r.y) >> 11) + 0.5) * 0x1p-53;
   const double u2 = ((double)((((uint64_t)r.z << 32) | r.w) >> 11) + 0.5) * 0x1p-53;
-  const double mag = sqrt(-2.0 * log(u1));
-  // cos/sin(2π u2) via sincospi(2 u2): the same angle without sincos's Payne–Hanek slow path
-  // (differs from glibc's sin(2π·u2) by ≲ 2 ulp; fields stay within 1e-10 of the reference)
-  double s, c;
-  sincospi(2.0 * u2, &s, &c);
-  return make_double2(mag * c, mag * s);
+  const double mag = sqrt(-2.0 * bm_log(u1));
+  const double2 cs = bm_cossin_2pi(u2);
+  return make_double2(mag * cs.x, mag * cs.y);
 }
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }

@@ -112,8 +112,8 @@ def test_solver_error_carries_history_through_reference(P, E):
     its residual history (fem.cpp:359-379), through the reference's own estimator and the seam."""
     api = P.api
     prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1.0, 0.1))
-    opt = api.EstimatorOptions(seed=1, solver=api.SolverOptions(tol=1e-30, max_iter_factor=1))
+    opt = api.EstimatorOptions(seed=1, solver=api.SolverOptions(max_iter_factor=0))
     with pytest.raises(api.SolverError) as ei:
         E.mc_estimate_fixed_n(prob, opt, 8, 4)
     h = ei.value.residual_history
-    assert h is not None and len(h) >= 2 and np.all(np.isfinite(h)) and h[0] > 0
+    assert h is not None and len(h) >= 1 and np.all(np.isfinite(h)) and h[0] > 1e-10

@@ -86,7 +86,7 @@ def test_failure_history_through_level_draws(P, ctx):
     failing slot's residual history, re-solved alone — the reference's SolverError::history."""
     api = P.api
     prob = api.ProblemSpec(api.CovarianceModel.matern(1.0, 0.1, 0.5))
-    opt = api.EstimatorOptions(seed=1, solver=api.SolverOptions(tol=1e-30, max_iter_factor=1))
+    opt = api.EstimatorOptions(seed=1, solver=api.SolverOptions(max_iter_factor=0))
     plan = api.make_level_plan(1, 1.0 / 32, prob, opt)  # 64² fine / 32² coarse: the streaming solver
     d = api.LevelDraws()
     ctx.set_history(4096)
@@ -99,7 +99,7 @@ def test_failure_history_through_level_draws(P, ctx):
         assert slot == 3
         h2 = ei.value.residual_history
         assert h2 is not None and np.array_equal(h, h2)
-        assert len(h) >= 2 and np.all(np.isfinite(h)) and np.all(h > 0)
+        assert len(h) == 1 and np.isfinite(h[0]) and h[0] > 1e-10  # a zero cap fails before iterating (fem.cpp:374)
     finally:
         ctx.set_history(0)
     # history off: the error still carries the per-slot status, no re-run

@@ -74,9 +74,7 @@ int guarded(F&& f) {
 
 void set_device(Ctx* c) { OSC_CUDA(cudaSetDevice(c->device)); }
 
-#ifndef OSC_XI_CHUNKS
-#define OSC_XI_CHUNKS 4
-#endif
+constexpr int kXiChunks = 4;  // host-ξ batches: up to 4 chunks, so only the first chunk's H2D is exposed
 
 size_t budget_of(Ctx* c) {
   if (c->mem_budget) return c->mem_budget;
@@ -458,7 +456,7 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
     // chunk i's solve and only the first chunk's copy is exposed (up to 4 chunks of ≥ 8 samples);
     // device ξ / Philox: one chunk when it fits
     if (xi_chunked && count >= 2)
-      nchunks = std::max<int64_t>(nchunks, std::min<int64_t>(OSC_XI_CHUNKS, std::max<int64_t>(2, count / 8)));
+      nchunks = std::max<int64_t>(nchunks, std::min<int64_t>(kXiChunks, std::max<int64_t>(2, count / 8)));
     const int Bc = (int)((count + nchunks - 1) / nchunks);
     // chunk schedule. Host ξ with large uniform chunks (≥ 256 MB of ξ each): a ramp — a small
     // first chunk (its copy is the only exposed one), then each chunk ≤ OSC_XI_RAMP × the previous,
@@ -468,8 +466,8 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
     std::vector<std::pair<int64_t, int>> sched;
     {
       auto env_num = [](const char* k, double d) { const char* v = std::getenv(k); return v ? std::atof(v) : d; };
-      const double ramp = env_num("OSC_XI_RAMP", 1.35);
-      const int first_div = (int)env_num("OSC_XI_FIRST_DIV", 16);
+      const double ramp = 1.35;
+      const int first_div = 16;
       const double min_mb = env_num("OSC_XI_RAMP_MIN_MB", 256);  // tests lower it to reach the ramp
       int sz = Bc;
       const bool big = sizeof(double) * (double)L->s * Bc >= min_mb * (1 << 20);
@@ -531,8 +529,7 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
     }
     bool any_bad = false, any_fail = false;
     std::vector<int32_t> it_tmp(Bc), st_tmp(Bc), bad_tmp(Bc);
-    // OSC_NO_NESTED=1: fine solve from the reference's Dirichlet lift (A/B)
-    static const bool nested = std::getenv("OSC_NO_NESTED") == nullptr;
+    constexpr bool nested = true;  // the fine solve starts from the prolonged coarse solution
     for (int64_t chunk = 0; chunk < (int64_t)sched.size(); ++chunk) {
       const int64_t c0 = sched[chunk].first;
       const int B = sched[chunk].second;

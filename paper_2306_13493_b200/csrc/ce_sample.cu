@@ -144,12 +144,6 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
 //         and keeps the last stage's outputs p1 = j + r·Ns in registers for the exp() epilogue.
 // Shared-memory round trips per transform: rows 5 → 4, cols 5 → 3; all index arithmetic is static.
 // A/B build knobs: cap the CTAs-per-SM the register budget is sized for (0 = 1024/THREADS, ≤ 64 regs)
-#ifndef OSC_CE_ROWS_MINB
-#define OSC_CE_ROWS_MINB 0
-#endif
-#ifndef OSC_CE_COLS_MINB
-#define OSC_CE_COLS_MINB 0
-#endif
 template <int LOGN>
 struct FftPlan {
   static constexpr int n = 1 << LOGN;
@@ -160,8 +154,6 @@ struct FftPlan {
   static constexpr int REM = LOGN % 3;               // log2 of the final radix (0: none)
   static constexpr int LD = n + (n >> 3) + 1;        // padded transform stride (fpad_len)
   static constexpr int MINB = THREADS >= 1024 ? 1 : (1024 / THREADS < 32 ? 1024 / THREADS : 32);  // ≤ 64 regs
-  static constexpr int MINB_ROWS = (OSC_CE_ROWS_MINB > 0 && OSC_CE_ROWS_MINB < MINB) ? OSC_CE_ROWS_MINB : MINB;
-  static constexpr int MINB_COLS = OSC_CE_COLS_MINB > 0 ? OSC_CE_COLS_MINB : MINB;
 };
 
 // Twiddles of one Stockham stage (radix R, sub-length 2^LNS) for this thread's G = 8/R butterflies.
@@ -298,10 +290,9 @@ __device__ __forceinline__ void rows_operands(const double* __restrict__ sqrt_la
 // inter[b][p/IL][q1][p%IL] (⌈P/IL⌉ groups per sample). The row pass's lanes for columns p … p+IL−1
 // fill IL·16 contiguous bytes per row (IL = 2: one 32-byte sector), and the column pass reads its two
 // adjacent columns as one 32-byte run per q1; wider groups help the row pass and hurt the column pass.
-#ifndef OSC_CE_IL
-#define OSC_CE_IL 2  // A/B at n = 2048: IL 2 → rows 28.5 + cols 17.4 µs; 4 → 27.4 + 20.7; 8 → 26.7 + 24.8
-#endif
-constexpr int CE_IL = OSC_CE_IL;  // columns interleaved per q1 run (power of two)
+// columns interleaved per q1 run (power of two). Measured at n = 2048: IL 2 → rows 28.5 + cols 17.4 µs;
+// 4 → 27.4 + 20.7; 8 → 26.7 + 24.8
+constexpr int CE_IL = 2;
 __device__ __forceinline__ int64_t inter_pair_idx(int b, int Ph, int n, int p, int q1) {
   return (((int64_t)b * Ph + p / CE_IL) * n + q1) * CE_IL + (p & (CE_IL - 1));
 }
@@ -325,7 +316,7 @@ __device__ __forceinline__ void rows_unpack(const double2* x, double2* __restric
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_ROWS) ce_rows_t_kernel(
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) ce_rows_t_kernel(
     const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
     uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
   using PL = FftPlan<LOGN>;
@@ -357,7 +348,7 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_RO
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_COLS) ce_cols_t_kernel(
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) ce_cols_t_kernel(
     const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
     const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
     int* __restrict__ bad_flag) {
@@ -407,7 +398,7 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB_CO
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
 }
 
-// Column pass with two columns per thread (default; OSC_CE_COLS2=0 for one): the same stages as ce_cols_t_kernel
+// Column pass with two columns per thread (32 ≤ n ≤ 4096; ce_cols_t_kernel below and above): the same stages as ce_cols_t_kernel
 // applied to columns j and j + 1 held by one thread, so each barrier interval carries two independent
 // butterflies (twice the loads in flight) and every twiddle load serves both columns.
 template <int LOGN, int R, int LNS>
@@ -517,47 +508,6 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
 }
 
-// Row pass with two row pairs per thread (A/B only, OSC_CE_ROWS2=1): both transforms' operands are
-// drawn, then every stage carries two independent butterflies.
-template <int LOGN>
-__global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MINB) ce_rows2_t_kernel(
-    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
-    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
-  using PL = FftPlan<LOGN>;
-  using LS = LastStage<LOGN>;
-  constexpr int T = PL::T;
-  extern __shared__ double2 smem[];
-  const int t = threadIdx.x / T;
-  const int lt = threadIdx.x % T;
-  const int rp0 = 2 * (blockIdx.x * PL::NT + t);  // row pairs rp0, rp0 + 1 (n/2 is a multiple of 2·NT)
-  const int b = blockIdx.y;
-  double2* x0 = smem + (2 * t) * PL::LD;
-  double2* x1 = x0 + PL::LD;
-  const PhiloxKeys keys = philox_keys(seed);
-  const uint64_t idx = index0 + (uint64_t)b;
-  {
-    double2 v[8];
-    rows_operands<LOGN>(sqrt_lam, xi, keys, ell, idx, b, 2 * rp0, lt, v);
-    first_stage_store<LOGN>(x0, lt, v);
-    rows_operands<LOGN>(sqrt_lam, xi, keys, ell, idx, b, 2 * rp0 + 2, lt, v);
-    first_stage_store<LOGN>(x1, lt, v);
-  }
-  mid_stages2<LOGN, 3>(x0, x1, lt, tw);
-  {
-    typename LS::Tw tt;
-    tt.load(lt, tw);
-    __syncthreads();
-    double2 w[2][LS::G][LS::R];
-    stage_load_compute2<LOGN, LS::R, LS::LNS>(x0, x1, lt, tt, w);
-    __syncthreads();
-    stage_store<LOGN, LS::R, LS::LNS>(x0, lt, w[0]);
-    stage_store<LOGN, LS::R, LS::LNS>(x1, lt, w[1]);
-    __syncthreads();
-  }
-  rows_unpack<LOGN>(x0, inter, b, P, cs, 2 * rp0, lt);
-  rows_unpack<LOGN>(x1, inter, b, P, cs, 2 * rp0 + 2, lt);
-}
-
 template <int LOGN>
 void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev, uint64_t seed,
               uint32_t ell, uint64_t index0, int count, bool do_exp, double* out_fine, double* out_coarse,
@@ -567,25 +517,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = sizeof(double2) * (size_t)PL::NT * PL::LD;
   cudaStream_t st = ctx->stream;
-  // two row pairs per thread only on request (OSC_CE_ROWS2=1): the Box–Muller phase wants the warps,
-  // and halving them was slower (config 2 row pass 423 → 462 ms per 12288 samples)
-  static const bool rows2_env = [] {
-    const char* e = std::getenv("OSC_CE_ROWS2");
-    return e && e[0] == '1';
-  }();
-  bool rows_done = false;
-  if constexpr (LOGN >= 5 && LOGN <= 12 && (PL::n / 2) % (2 * PL::NT) == 0) {
-    if (rows2_env) {
-      auto kern = ce_rows2_t_kernel<LOGN>;
-      smem_attr(kern, (2 * sm));
-      KScope ks(ctx, "ce_rows");
-      kern<<<dim3((PL::n / 2) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(sqrt_lam, xi_dev, seed, ell,
-                                                                                index0, P, cs, tw, inter);
-      OSC_CUDA(cudaGetLastError());
-      rows_done = true;
-    }
-  }
-  if (!rows_done) {
+  {
     auto kern = ce_rows_t_kernel<LOGN>;
     smem_attr(kern, sm);
     KScope ks(ctx, "ce_rows");
@@ -593,22 +525,16 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
                                                                       tw, inter);
     OSC_CUDA(cudaGetLastError());
   }
-  // two columns per thread (default for 32 ≤ n ≤ 4096, where it fits 128 registers without spills:
-  // config 2 column pass 277.7 → 208.6 ms per 12288 samples); OSC_CE_COLS2=0 keeps one (A/B)
-  static const bool cols2_env = [] {
-    const char* e = std::getenv("OSC_CE_COLS2");
-    return !(e && e[0] == '0');
-  }();
+  // two columns per thread for 32 ≤ n ≤ 4096, where it fits 128 registers without spills (config 2
+  // column pass 277.7 → 208.6 ms per 12288 samples against one column per thread)
   if constexpr (LOGN >= 5 && LOGN <= 12) {
-    if (cols2_env) {
-      auto kern = ce_cols2_t_kernel<LOGN>;
-      smem_attr(kern, (2 * sm));
-      KScope ks(ctx, "ce_cols");
-      kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
-          inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag);
-      OSC_CUDA(cudaGetLastError());
-      return;
-    }
+    auto kern = ce_cols2_t_kernel<LOGN>;
+    smem_attr(kern, (2 * sm));
+    KScope ks(ctx, "ce_cols");
+    kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
+        inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag);
+    OSC_CUDA(cudaGetLastError());
+    return;
   }
   {
     auto kern = ce_cols_t_kernel<LOGN>;
@@ -866,19 +792,12 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
   // round trip through HBM is hidden; small L2-sized chunks (80 MB: 2 samples at n = 2048) lost
   // more to partial last waves and pass-to-pass drains (config 2: 13.5k → 16.8k samples/s at 400 MB).
   const size_t per = ce_inter_bytes(L, 1, cs);
-  // OSC_CE_CHUNK_MB: A/B knob for the chunk budget (default 1 GiB: the launches are compute-bound, so the
-  // intermediate spilling from L2 to HBM costs less than the tail waves of small chunks)
-  static const size_t chunk_bytes = [] {
-    const char* e = std::getenv("OSC_CE_CHUNK_MB");
-    return (size_t)(e ? std::atol(e) : 1024) << 20;
-  }();
+  constexpr size_t chunk_bytes = size_t(1024) << 20;
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, chunk_bytes / per));
   ctx->ce_inter.ensure(ce_inter_bytes(L, chunk, cs));
   double2* inter = ctx->ce_inter.as<double2>();
   const int m = L->m, mc = m / 2;
   const int64_t Nf = (int64_t)(m + 1) * (m + 1), Nc = (int64_t)(mc + 1) * (mc + 1);
-  // OSC_CE_LEGACY=1: runtime-n kernels (A/B; bit-identical results)
-  static const bool legacy = std::getenv("OSC_CE_LEGACY") != nullptr;
   for (int c0 = 0; c0 < count; c0 += chunk) {
     const int cnt = std::min(chunk, count - c0);
     const double* xi_c = xi_dev ? xi_dev + (int64_t)c0 * L->s : nullptr;
@@ -888,7 +807,7 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
     // threads per transform T = n/E: ≤ 256 up to n = 2048, 512 at 4096, 1024 at 8192
     if (!pow2)
       launch_generic(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, rd);
-    else if (L->n >= 16 && !legacy) {
+    else if (L->n >= 16) {
 #define OSC_CE_T(LG) \
   case LG: launch_t<LG>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
       switch (31 - __builtin_clz((unsigned)L->n)) {

@@ -321,79 +321,6 @@ __global__ void __launch_bounds__(NT) prow_kernel(L9 R, int bc, int opdep, doubl
   P3[o] = w[3];
 }
 
-// Galerkin row of coarse node (I, J): A_c(c, c') = Σ_i P(i,c) Σ_j A(i,j) P(j,c') over the fine
-// nodes i of c's 3×3 support and their 9-point neighbours j (P rows from prow_kernel). Fully
-// unrolled: every fine offset, node type and parent offset is a compile-time constant, so the
-// 3×3 accumulator stays in registers. Stores C, E, N, NE, NW of the symmetric result; Dirichlet
-// coarse rows are identity.
-__global__ void __launch_bounds__(NT) rap_kernel(L9 F, int bc, const double* __restrict__ P0,
-                                                 const double* __restrict__ P1, const double* __restrict__ P2,
-                                                 const double* __restrict__ P3, Geo gc, double* __restrict__ Cc,
-                                                 double* __restrict__ Ec, double* __restrict__ Nc,
-                                                 double* __restrict__ NEc, double* __restrict__ NWc) {
-  const int b = blockIdx.y;
-  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (ic >= gc.N) return;
-  const int mc = gc.m, J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
-  const int m = F.m, n0 = F.n0;
-  const int64_t off = (int64_t)b * F.Nn, o = (int64_t)b * gc.N + ic;
-  if (is_dir(bc, mc, I, J)) {
-    Cc[o] = 1.0;
-    Ec[o] = Nc[o] = NEc[o] = NWc[o] = 0.0;
-    return;
-  }
-  double acc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-#pragma unroll
-  for (int dj = -1; dj <= 1; ++dj)
-#pragma unroll
-    for (int di = -1; di <= 1; ++di) {
-      const int xi = 2 * I + di, yi = 2 * J + dj;
-      if (xi < 0 || xi > m || yi < 0 || yi > m) continue;
-      const int64_t ii = off + (int64_t)yi * n0 + xi;
-      double pic;  // P(i, c) by i's type and position relative to c
-      if (di == 0 && dj == 0) pic = P0[ii];
-      else if (dj == 0) pic = di > 0 ? P0[ii] : P1[ii];  // H-edge: c is its W (di = +1) or E parent
-      else if (di == 0) pic = dj > 0 ? P0[ii] : P1[ii];  // V-edge: c is its S or N parent
-      else pic = dj > 0 ? (di > 0 ? P0[ii] : P1[ii]) : (di > 0 ? P2[ii] : P3[ii]);  // centre: SW SE NW NE
-      if (pic == 0.0) continue;
-      const S9 r = row_s(F, off, xi, yi);
-#pragma unroll
-      for (int ey = -1; ey <= 1; ++ey)
-#pragma unroll
-        for (int ex = -1; ex <= 1; ++ex) {
-          const double a = ey < 0 ? (ex < 0 ? r.sw : ex == 0 ? r.s : r.se)
-                                  : ey == 0 ? (ex < 0 ? r.w : ex == 0 ? r.c : r.e)
-                                            : (ex < 0 ? r.nw : ex == 0 ? r.n : r.ne);
-          const int xj = xi + ex, yj = yi + ey;
-          if (a == 0.0 || xj < 0 || xj > m || yj < 0 || yj > m) continue;
-          const int64_t jj = off + (int64_t)yj * n0 + xj;
-          const double pa = pic * a;
-          const int dx = di + ex, dy = dj + ey;  // j relative to (2I, 2J), in [−2, 2]
-          const bool ox = (dx & 1) != 0, oy = (dy & 1) != 0;
-          const int bx = dx >> 1, by = dy >> 1;  // floor(dx/2): j's W/S parent offset from c
-          if (!ox && !oy) {
-            acc[by + 1][bx + 1] += pa * P0[jj];
-          } else if (ox && !oy) {
-            acc[by + 1][bx + 1] += pa * P0[jj];
-            acc[by + 1][bx + 2] += pa * P1[jj];
-          } else if (!ox && oy) {
-            acc[by + 1][bx + 1] += pa * P0[jj];
-            acc[by + 2][bx + 1] += pa * P1[jj];
-          } else {
-            acc[by + 1][bx + 1] += pa * P0[jj];
-            acc[by + 1][bx + 2] += pa * P1[jj];
-            acc[by + 2][bx + 1] += pa * P2[jj];
-            acc[by + 2][bx + 2] += pa * P3[jj];
-          }
-        }
-    }
-  Cc[o] = acc[1][1];
-  Ec[o] = acc[1][2];
-  Nc[o] = acc[2][1];
-  NEc[o] = acc[2][2];
-  NWc[o] = acc[2][0];
-}
-
 // Fused Galerkin setup of one level pair, tiled in shared memory: the fine rows (level 0: rebuilt
 // from nodal k; levels ≥ 1: the stored 9-point rows) of a halo'd tile are staged once, the P rows of
 // the tile's fine nodes are formed in shared memory (prow_f, the arithmetic of prow_kernel), and each
@@ -723,161 +650,6 @@ __global__ void coarse_factor_kernel(L9 Lv, int B, double* __restrict__ chol) {
 // terms vanish: red z = r/C, black z = (r − Σ_WENS a z_red)/C.
 __device__ __forceinline__ bool is_red(int x, int y) { return ((x + y) & 1) == 0; }
 
-__device__ __forceinline__ double row_dot(const S9& a, const double* __restrict__ v, int64_t i, int n0, int x,
-                                          int y, int m) {
-  // Σ over the 8 neighbours a_j v_j (off-grid couplings are 0)
-  double s = 0.0;
-  if (x > 0) s += a.w * v[i - 1];
-  if (x < m) s += a.e * v[i + 1];
-  if (y > 0) {
-    s += a.s * v[i - n0];
-    if (x > 0) s += a.sw * v[i - n0 - 1];
-    if (x < m) s += a.se * v[i - n0 + 1];
-  }
-  if (y < m) {
-    s += a.n * v[i + n0];
-    if (x > 0) s += a.nw * v[i + n0 - 1];
-    if (x < m) s += a.ne * v[i + n0 + 1];
-  }
-  return s;
-}
-
-#define C_PROLOGUE                                          \
-  const int b = blockIdx.z;                                 \
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;              \
-  const int64_t li = blockIdx.x * (int64_t)NT + threadIdx.x; \
-  if (li >= L.Nn) return;                                   \
-  const int y = (int)(li / L.n0), x = (int)(li - (int64_t)y * L.n0); \
-  const int64_t off = (int64_t)b * L.Nn, i = off + li;
-
-// pre-smoother from z = 0, red then black (two launches: the black pass reads the new red values)
-__global__ void __launch_bounds__(NT) c_pre_kernel(L9 L, int black, const double* __restrict__ r,
-                                                  double* __restrict__ z, const int* flags) {
-  C_PROLOGUE
-  if (!black) {
-    z[i] = is_red(x, y) ? r[i] / L.C[i] : 0.0;
-  } else if (!is_red(x, y)) {
-    const S9 a = row_s(L, off, x, y);
-    double s = 0.0;  // W, E, N, S are red; the black diagonal neighbours are still 0
-    if (x > 0) s += a.w * z[i - 1];
-    if (x < L.m) s += a.e * z[i + 1];
-    if (y > 0) s += a.s * z[i - L.n0];
-    if (y < L.m) s += a.n * z[i + L.n0];
-    z[i] = (r[i] - s) / a.c;
-  }
-}
-
-// residual t = r − A z (written over t, the level's z2 scratch)
-__global__ void __launch_bounds__(NT) c_resid_kernel(L9 L, const double* __restrict__ r,
-                                                    const double* __restrict__ z, double* __restrict__ t,
-                                                    const int* flags) {
-  C_PROLOGUE
-  const S9 a = row_s(L, off, x, y);
-  t[i] = r[i] - (a.c * z[i] + row_dot(a, z, i, L.n0, x, y, L.m));
-}
-
-// restriction rc = Pᵀ t (coarse node per thread): C point 1, edge weights from the edge rows
-// (opdep) or ½, centre weights from pw (this level's cells); coarse Dirichlet rows 0
-__global__ void __launch_bounds__(NT) c_restrict_kernel(L9 L, int bc, int opdep, const double* __restrict__ t,
-                                                       const double* __restrict__ pw0, const double* __restrict__ pw1,
-                                                       const double* __restrict__ pw2, const double* __restrict__ pw3,
-                                                       Geo gc, double* __restrict__ rc, const int* flags) {
-  const int b = blockIdx.z;
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
-  if (ic >= gc.N) return;
-  const int mc = gc.m, J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
-  double* out = rc + (int64_t)b * gc.N + ic;
-  if (is_dir(bc, mc, I, J)) {
-    *out = 0.0;
-    return;
-  }
-  const int m = L.m, n0 = L.n0;
-  const int64_t off = (int64_t)b * L.Nn;
-  const int x = 2 * I, y = 2 * J;
-  auto T = [&](int xx, int yy) { return t[off + (int64_t)yy * n0 + xx]; };
-  double acc = T(x, y);
-  // H-edges (x±1, y) and V-edges (x, y±1): weight toward (I, J)
-  for (int s = -1; s <= 1; s += 2) {
-    if (x + s >= 0 && x + s <= m) {
-      double w0, w1;
-      edge_w(row_s(L, off, x + s, y), true, opdep != 0, is_dir(bc, m, x + s, y), false, false, w0, w1);
-      acc += (s > 0 ? w0 : w1) * T(x + s, y);
-    }
-    if (y + s >= 0 && y + s <= m) {
-      double w0, w1;
-      edge_w(row_s(L, off, x, y + s), false, opdep != 0, is_dir(bc, m, x, y + s), false, false, w0, w1);
-      acc += (s > 0 ? w0 : w1) * T(x, y + s);
-    }
-  }
-  // centres: (x+1, y+1) → its SW; (x−1, y+1) → SE; (x+1, y−1) → NW; (x−1, y−1) → NE
-  const int mcl = m / 2;
-  const int64_t cb = (int64_t)b * mcl * mcl;
-  if (I < mcl && J < mcl) acc += pw0[cb + (int64_t)J * mcl + I] * T(x + 1, y + 1);
-  if (I > 0 && J < mcl) acc += pw1[cb + (int64_t)J * mcl + I - 1] * T(x - 1, y + 1);
-  if (I < mcl && J > 0) acc += pw2[cb + (int64_t)(J - 1) * mcl + I] * T(x + 1, y - 1);
-  if (I > 0 && J > 0) acc += pw3[cb + (int64_t)(J - 1) * mcl + I - 1] * T(x - 1, y - 1);
-  *out = acc;
-}
-
-// prolongation z += P zc at every node (in place)
-__global__ void __launch_bounds__(NT) c_prolong_kernel(L9 L, int bc, int opdep, const double* __restrict__ pw0,
-                                                      const double* __restrict__ pw1, const double* __restrict__ pw2,
-                                                      const double* __restrict__ pw3, Geo gc,
-                                                      const double* __restrict__ zc, double* __restrict__ z,
-                                                      const int* flags) {
-  C_PROLOGUE
-  const int m = L.m;
-  const double* zcb = zc + (int64_t)b * gc.N;
-  auto ZC = [&](int I, int J) { return zcb[(int64_t)J * gc.n0 + I]; };
-  const int ox = x & 1, oy = y & 1;
-  double v;
-  if (!ox && !oy) {
-    v = ZC(x >> 1, y >> 1);
-  } else if (ox && oy) {
-    const int mcl = m / 2, I = x >> 1, J = y >> 1;
-    const int64_t cell = (int64_t)b * mcl * mcl + (int64_t)J * mcl + I;
-    v = pw0[cell] * ZC(I, J) + pw1[cell] * ZC(I + 1, J) + pw2[cell] * ZC(I, J + 1) + pw3[cell] * ZC(I + 1, J + 1);
-  } else {
-    double w0, w1;
-    const bool horiz = ox != 0;
-    edge_w(row_s(L, off, x, y), horiz, opdep != 0, is_dir(bc, m, x, y), false, false, w0, w1);
-    v = horiz ? w0 * ZC(x >> 1, y >> 1) + w1 * ZC((x >> 1) + 1, y >> 1)
-              : w0 * ZC(x >> 1, y >> 1) + w1 * ZC(x >> 1, (y >> 1) + 1);
-  }
-  z[i] += v;
-}
-
-// post-smoother: black from (z) into z2, then red from (z2 black, z red) into z2
-__global__ void __launch_bounds__(NT) c_post_kernel(L9 L, int red, const double* __restrict__ r,
-                                                   const double* __restrict__ z, double* __restrict__ z2,
-                                                   const int* flags) {
-  C_PROLOGUE
-  if (is_red(x, y) != (red != 0)) return;
-  const S9 a = row_s(L, off, x, y);
-  const int n0 = L.n0, m = L.m;
-  double s;
-  if (!red) {
-    s = row_dot(a, z, i, n0, x, y, m);
-  } else {  // W, E, N, S are black (new, z2); the diagonals are red (prolonged, z)
-    s = 0.0;
-    if (x > 0) s += a.w * z2[i - 1];
-    if (x < m) s += a.e * z2[i + 1];
-    if (y > 0) {
-      s += a.s * z2[i - n0];
-      if (x > 0) s += a.sw * z[i - n0 - 1];
-      if (x < m) s += a.se * z[i - n0 + 1];
-    }
-    if (y < m) {
-      s += a.n * z2[i + n0];
-      if (x > 0) s += a.nw * z[i + n0 - 1];
-      if (x < m) s += a.ne * z[i + n0 + 1];
-    }
-  }
-  z2[i] = (r[i] - s) / a.c;
-}
-
-
 // ---- PCG init: u = lift (or the nested-iteration guess), r = b − A u, ‖b‖, ‖r‖ -------------------
 // One thread per column marching INIT_RY rows, so a CTA covers NT × INIT_RY nodes and does one
 // fixed-order reduction (a CTA per 256 nodes made the init launch-/reduction-bound: 1M CTAs per
@@ -997,23 +769,14 @@ constexpr int MT = 32 * MW;  // threads per CTA
 constexpr int LY = 32;       // output rows per warp on large grids
 // rows marched per warp: long chunks amortise the 2-row warm-up on large grids; short chunks
 // cut the serial row-latency chain (and add CTAs) on the small, latency-bound MG levels.
-#ifndef OSC_RPW
-#define OSC_RPW 0
-#endif
 __host__ __device__ __forceinline__ int rows_per_warp(int m) {
-  if (OSC_RPW == 1) return m >= 512 ? LY : (m >= 256 ? 16 : (m >= 64 ? 8 : 4));
-  if (OSC_RPW == 2) return m >= 512 ? LY : (m >= 128 ? 16 : (m >= 64 ? 8 : 4));
-  if (OSC_RPW == 3) return m >= 512 ? LY : (m >= 64 ? 16 : 8);
   // 64 rows at m ≥ 1024 halve the ring warm-up and the per-CTA reduction tail of the level-0 sweeps
   // (config 4: smooth_up 40.4 → 38.2 ms, pcg_update 45.3 → 44.6 ms per step)
   return m >= 1024 ? 2 * LY : (m >= 512 ? LY : (m >= 64 ? 16 : 8));
 }
 constexpr int LYC = 16;      // coarse output rows per warp (restriction) on large grids
-#ifndef OSC_LYC_BIG
-#define OSC_LYC_BIG 32  // level-0 restriction of the 2048² solve: 25.3 → 24.2 ms per config-4 step
-#endif
 __host__ __device__ __forceinline__ int coarse_rows_per_warp(int mc) {
-  return mc >= 512 ? OSC_LYC_BIG : (mc >= 256 ? LYC : 4);
+  return mc >= 512 ? 32 : (mc >= 256 ? LYC : 4);
 }
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -1332,10 +1095,7 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
   return rr;
 }
 
-#ifndef OSC_PU_W
-#define OSC_PU_W 4
-#endif
-constexpr int PU_W = OSC_PU_W;  // warps per CTA of pcg_update (A/B knob: 1 and 2 warps are no faster, it is DRAM-bound)
+constexpr int PU_W = 4;  // warps per CTA of pcg_update (A/B knob: 1 and 2 warps are no faster, it is DRAM-bound)
 __global__ void __launch_bounds__(32 * PU_W, 16 / PU_W) pcg_update_cg_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
                                                               const double* __restrict__ z,
                                                               const double* __restrict__ p_old,
@@ -1524,47 +1284,6 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
   Pair kq = ld2<INT>(kb, xa, y0, n0), pq = ld2<INT>(pb, xa, y0, n0), rq = ld2<INT>(rb, xa, y0 - 1, n0);
   Pair uq = ld2<INT>(u + off, xa, y0 - 2, n0);
   double rr = 0.0;
-#ifdef OSC_UD_UNROLL2
-  // rows alternate parity: run them in (even, odd) pairs so the red/black roles are static
-  auto step = [&](int t, auto ra) {
-    constexpr bool ra0 = decltype(ra)::value, ra1 = !ra0;  // red column of row t is a
-    const Pair kc = kq, pc = pq, r1 = rq, u0 = uq;  // rows t+2 / t+1 / t, loaded one iteration ahead
-    kq = ld2<INT>(kb, xa, t + 3, n0);
-    pq = ld2<INT>(pb, xa, t + 3, n0);
-    rq = ld2<INT>(rb, xa, t + 2, n0);
-    uq = ld2<INT>(u + off, xa, t + 1, n0);
-    Pair E1, N1;
-    edges_pair<INT>(ka, kb1, kc, xa, t + 1, m, E1, N1);
-    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
-    const Pair od1 = offd_pair(st1, pa, pb1, pc);
-    const Pair rn1{fma(-alpha, fma(st1.a.d, pb1.a, od1.a), r1.a), fma(-alpha, fma(st1.b.d, pb1.b, od1.b), r1.b)};
-    const double zrp = ra1 ? rn1.a * rcp64(st1.a.d) : rn1.b * rcp64(st1.b.d);
-    const double zbl = ra0 ? (rn0.b - (sb0.e * shdn(zr0) + sb0.w * zr0 + sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d)
-                           : (rn0.a - (sb0.e * zr0 + sb0.w * shup(zr0) + sb0.n * zrp + sb0.s * zrm)) * rcp64(sb0.d);
-    const Pair zv = ra0 ? Pair{zr0, zbl} : Pair{zbl, zr0};
-    if (t >= y0) {
-      const int64_t row = off + (int64_t)t * n0;
-      if (outa) {
-        u[row + xa] = fma(alpha, pa.a, u0.a);
-        r_out[row + xa] = rn0.a;
-        z[row + xa] = zv.a;
-        rr = fma(rn0.a, rn0.a, rr);
-      }
-      if (outb) {
-        u[row + xb] = fma(alpha, pa.b, u0.b);
-        r_out[row + xb] = rn0.b;
-        z[row + xb] = zv.b;
-        rr = fma(rn0.b, rn0.b, rr);
-      }
-    }
-    ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
-    rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
-  };
-  for (int t = y0 - 2; t < y1; t += 2) {  // y0 is even
-    step(t, std::true_type{});
-    if (t + 1 < y1) step(t + 1, std::false_type{});
-  }
-#else
   for (int t = y0 - 2; t < y1; ++t) {
     const Pair kc = kq, pc = pq, r1 = rq, u0 = uq;  // rows t+2 / t+1 / t, loaded one iteration ahead
     kq = ld2<INT>(kb, xa, t + 3, n0);
@@ -1603,27 +1322,18 @@ __device__ __forceinline__ double pcg_update_down_kernel_body(
     ka = kb1; kb1 = kc; pa = pb1; pb1 = pc; Nt = N1;
     rn0 = rn1; zrm = zr0; zr0 = zrp; sb0 = ra1 ? st1.b : st1.a;
   }
-#endif
   return rr;
 }
 
-#ifndef OSC_UD_MINB
-#define OSC_UD_MINB 4
-#endif
-__global__ void __launch_bounds__(MT, OSC_UD_MINB) pcg_update_down_kernel(
+__global__ void __launch_bounds__(MT, 4) pcg_update_down_kernel(
     Geo g, int bc, double tol, const double* __restrict__ k, const double* __restrict__ p,
     double* __restrict__ u, const double* __restrict__ r, double* __restrict__ r_out,
     double* __restrict__ z, double* scal, int* flags, double2* partial, int maxp, unsigned* counter,
     int* n_active, double* hist, int hist_cap, int init) {
   PAIR_PROLOGUE
-#ifdef OSC_UD_INTERIOR
-  const double rr = interior ? pcg_update_down_kernel_body<true>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, init, c)
-                             : pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, init, c);
-#else
   // generic body only: the interior specialisation pushes this kernel past 128 registers (spills)
   (void)interior;
   const double rr = pcg_update_down_kernel_body<false>(g, bc, tol, k, p, u, r, r_out, z, scal, flags, partial, maxp, counter, n_active, hist, hist_cap, init, c);
-#endif
   if (init) return;  // the first V-cycle's pre-smoother pass (α = 0): no PCG bookkeeping
   double t0, t1;
   if (reduce2_last(rr, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
@@ -1677,66 +1387,6 @@ struct PW4 {
   const double *w0, *w1, *w2, *w3;  // centre weights to SW, SE, NW, NE per cell (m/2 × m/2 per sample)
 };
 
-template <bool INT, bool EN>
-__device__ __forceinline__ void restrict_z_body(Geo g, Geo gc, int bc, const double* __restrict__ ca,
-                                              const double* __restrict__ cb, const double* __restrict__ z,
-                                              PW4 pw, double* __restrict__ rc, int b, int I, bool outI, int J0,
-                                              int J1) {
-  const int m = g.m, n0 = g.n0, mc = gc.m;
-  const int xa = 2 * I;
-  const int64_t off = (int64_t)b * g.N;
-  const double* zb = z + off;
-  // fine rows y = 2J0−1 (odd: t at (xb, 2J0−1)), then pairs (2J, 2J+1) for J = J0 … J1−1;
-  // state: z rows y−1, y (+ y+1 in flight), N of row y−1
-  const int ys = 2 * J0 - 1;
-  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, ys - 1);
-  Pair E, N, Nm;
-  er.next(E, Nm);
-  Pair zm = ld2<INT>(zb, xa, ys - 1, n0), z0 = ld2<INT>(zb, xa, ys, n0);
-  Pair zq = ld2<INT>(zb, xa, ys + 1, n0);
-  double* rcb = rc + (int64_t)b * gc.N;
-  auto advance = [&](int y, Pair& zp) {  // row y's edges and z row y+1; prefetch z row y+2
-    zp = zq;
-    zq = ld2<INT>(zb, xa, y + 2, n0);
-    er.next(E, N);
-  };
-  // centre cell (I, Jc) weights (0 outside the grid of cells)
-  const int mcl = m / 2;
-  const int64_t cb0 = (int64_t)b * mcl * mcl;
-  auto W4 = [&](int Jc, double w[4]) {
-    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
-    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
-    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
-    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
-    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
-  };
-  Pair zp;
-  advance(ys, zp);
-  double wc[4];
-  W4(J0 - 1, wc);
-  const double t_first = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, ys, m, bc);  // (xb, 2J0−1)
-  // contributions of the previous odd row's centre to the coarse row J: NW (own), NE (lane I−1)
-  double a_nw = t_first * wc[2], a_ne = t_first * wc[3];
-  zm = z0; z0 = zp; Nm = N;
-  for (int J = J0; J < J1; ++J) {
-    const int y = 2 * J;
-    W4(J, wc);
-    advance(y, zp);
-    const double t_even = red_resid<INT, true>(E, N, Nm, zm, z0, zp, xa, y, m, bc);  // (xa, 2J)
-    zm = z0; z0 = zp; Nm = N;
-    advance(y + 1, zp);
-    const double t = red_resid<INT, false>(E, N, Nm, zm, z0, zp, xa, y + 1, m, bc);  // (xb, 2J+1)
-    zm = z0; z0 = zp; Nm = N;
-    // centre (2I+1, 2J+1): SW → (I, J) own; SE → (I+1, J) (next lane reads it with shup)
-    const double a_sw = t * wc[0], a_se = t * wc[1];
-    const double v = t_even + a_sw + shup(a_se) + a_nw + shup(a_ne);
-    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
-    a_nw = t * wc[2];
-    a_ne = t * wc[3];
-  }
-}
-
 // ---- coarse levels (9-point): row-marching kernels ----------------------------------------------------
 // The same column-pair layout as level 0: lane l owns the even column xa and xb = xa + 1 of its
 // 64-column strip, so each row gives every lane one red and one black node. The stored operator
@@ -1745,22 +1395,6 @@ __device__ __forceinline__ void restrict_z_body(Geo g, Geo gc, int bc, const dou
 struct R9 {
   Pair C, E, N, NE, NW;
 };
-
-template <bool INT>
-__device__ __forceinline__ R9 ld9(const L9& L, int64_t off, int xa, int y) {
-  R9 q;
-  q.C = ld2<INT>(L.C + off, xa, y, L.n0);
-  q.E = ld2<INT>(L.E + off, xa, y, L.n0);
-  q.N = ld2<INT>(L.N + off, xa, y, L.n0);
-  q.NE = ld2<INT>(L.NE + off, xa, y, L.n0);
-  q.NW = ld2<INT>(L.NW + off, xa, y, L.n0);
-  if (!INT) {  // off-grid nodes: identity rows (their r and couplings are 0)
-    const bool yok = (unsigned)y < (unsigned)L.n0;
-    if (!(yok && (unsigned)xa < (unsigned)L.n0)) q.C.a = 1.0;
-    if (!(yok && (unsigned)(xa + 1) < (unsigned)L.n0)) q.C.b = 1.0;
-  }
-  return q;
-}
 
 // 9-point rows of both columns of row y from its loads and row y−1's N, NE, NW.
 __device__ __forceinline__ void st9_pair(const R9& q, Pair Nm, Pair NEm, Pair NWm, S9& A, S9& Bc) {
@@ -1787,10 +1421,7 @@ __device__ __forceinline__ double diag_b(const S9& B, Pair vm, Pair vp) {
   return B.ne * shdn(vp.a) + B.nw * vp.a + B.se * shdn(vm.a) + B.sw * vm.a;
 }
 
-#ifndef OSC_CU_W
-#define OSC_CU_W 1
-#endif
-constexpr int CU_W = OSC_CU_W;  // warps per CTA of the coarse ring up sweep
+constexpr int CU_W = 1;  // warps per CTA of the coarse ring up sweep
 #define C9_PROLOGUE C9_PROLOGUE_W(MW)
 #define C9_PROLOGUE_W(WPB)                                                            \
   const int b = blockIdx.z;                                                           \
@@ -1805,234 +1436,6 @@ constexpr int CU_W = OSC_CU_W;  // warps per CTA of the coarse ring up sweep
   const int y0 = blockIdx.y * ly, y1 = min(y0 + ly, n0);                              \
   const int64_t off = (int64_t)b * L.Nn;                                              \
   (void)outa; (void)outb;
-
-// Pre-smoother from z = 0 (red then black; the black sweep's diagonal neighbours are still 0):
-//   z_red = r/C,  z_black = (r − Σ_WENS a z_red)/C.  Reads C, E, N, r; writes z. Ingesting row t+1
-// gives z_red(t+1) and z_black(t).
-__global__ void __launch_bounds__(MT) c_pre_march_kernel(L9 L, const double* __restrict__ r,
-                                                         double* __restrict__ z, const int* flags) {
-  C9_PROLOGUE
-  const double *Cb = L.C + off, *Eb = L.E + off, *Nb = L.N + off, *rb = r + off;
-  auto ldC = [&](int y) {
-    Pair c = ld2<false>(Cb, xa, y, n0);
-    const bool yok = (unsigned)y < (unsigned)n0;
-    if (!(yok && (unsigned)xa < (unsigned)n0)) c.a = 1.0;
-    if (!(yok && (unsigned)xb < (unsigned)n0)) c.b = 1.0;
-    return c;
-  };
-  // state: row t: C, E, N, r; row t−1: N; red z of rows t−1, t
-  Pair Nm = ld2<false>(Nb, xa, y0 - 2, n0);
-  Pair C0 = ldC(y0 - 1), E0 = ld2<false>(Eb, xa, y0 - 1, n0), N0 = ld2<false>(Nb, xa, y0 - 1, n0);
-  Pair r0 = ld2<false>(rb, xa, y0 - 1, n0);
-  double zrm = 0.0;
-  double zr0 = (RED_IS_A(y0 - 1) ? r0.a / C0.a : r0.b / C0.b);
-  for (int t = y0 - 1; t < y1; ++t) {
-    const Pair C1 = ldC(t + 1), E1 = ld2<false>(Eb, xa, t + 1, n0), N1 = ld2<false>(Nb, xa, t + 1, n0);
-    const Pair r1 = ld2<false>(rb, xa, t + 1, n0);
-    const bool ra0 = RED_IS_A(t), ra1 = !ra0;
-    const double zrp = ra1 ? r1.a / C1.a : r1.b / C1.b;  // red of row t+1
-    // black of row t: at b (ra0: red at a) or at a
-    const double zr0_e = shdn(zr0), zr0_w = shup(zr0), Ew = shup(E0.b);
-    double zbl;
-    if (ra0)  // black at xb: E = E0.b toward the next lane's xa, W = E0.a toward own xa
-      zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) / C0.b;
-    else      // black at xa: E toward own xb, W = E(xa−1) toward the previous lane's xb
-      zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) / C0.a;
-    if (t >= y0) {
-      double* out = z + off + (int64_t)t * n0;
-      if (outa) out[xa] = ra0 ? zr0 : zbl;
-      if (outb) out[xb] = ra0 ? zbl : zr0;
-    }
-    Nm = N0; C0 = C1; E0 = E1; N0 = N1; r0 = r1;
-    zrm = zr0; zr0 = zrp;
-  }
-}
-
-// Residual after the pre-smoother and its restriction rc = Pᵀ t (coarse-row layout: lane l owns
-// coarse column I, fine columns 2I and 2I+1). With C·z_red = r and the black update absorbing its
-// WENS red terms:
-//   t_red = −Σ_8 a z,  t_black = −Σ_diag a z_black.
-// Row roles:
-//   even row 2J: a = C point (red), b = H-edge (black; weights to (I,J), (I+1,J));
-//   odd row 2J±1: a = V-edge (black), b = centre (red, weights pw of cell (I, J)).
-// Edge weights are rebuilt from the edge node's 9-point row (opdep) or ½.
-__global__ void __launch_bounds__(MT) c_restrict_march_kernel(L9 L, int bc, int opdep, const double* __restrict__ z,
-                                                              PW4 pw, Geo gc, double* __restrict__ rc,
-                                                              const int* flags) {
-  const int b = blockIdx.z;
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
-  const int I = strip * 30 - 1 + lane;
-  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
-  const int lyc = coarse_rows_per_warp(gc.m);
-  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
-  const int m = L.m, n0 = L.n0, mc = gc.m, xa = 2 * I;
-  const int64_t off = (int64_t)b * L.Nn;
-  const double* zb = z + off;
-  const int mcl = m / 2;
-  const int64_t cb0 = (int64_t)b * mcl * mcl;
-  auto W4 = [&](int Jc, double w[4]) {
-    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
-    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
-    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
-    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
-    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
-  };
-  // state for row y: its loads q, row y−1's N/NE/NW, z rows y−1, y (+ y+1 in flight)
-  const int ys = 2 * J0 - 1;
-  R9 q = ld9<false>(L, off, xa, ys);
-  Pair Nm = ld2<false>(L.N + off, xa, ys - 1, n0), NEm = ld2<false>(L.NE + off, xa, ys - 1, n0),
-       NWm = ld2<false>(L.NW + off, xa, ys - 1, n0);
-  Pair zm = ld2<false>(zb, xa, ys - 1, n0), z0 = ld2<false>(zb, xa, ys, n0), zq = ld2<false>(zb, xa, ys + 1, n0);
-  R9 qn = ld9<false>(L, off, xa, ys + 1);
-  // residuals of row y (both columns) and the row's stencils; advances the state to row y+1
-  auto row = [&](int y, double& ta, double& tb, S9& A, S9& Bc) {
-    const Pair zp = zq;
-    zq = ld2<false>(zb, xa, y + 2, n0);
-    st9_pair(q, Nm, NEm, NWm, A, Bc);
-    const bool red_a = RED_IS_A(y);
-    ta = red_a ? -dot8_a(A, zm, z0, zp) : -diag_a(A, zm, zp);
-    tb = red_a ? -diag_b(Bc, zm, zp) : -dot8_b(Bc, zm, z0, zp);
-    // off-grid or Dirichlet nodes carry no residual
-    if (is_dir(bc, m, xa, y) || (unsigned)xa > (unsigned)m || (unsigned)y > (unsigned)m) ta = 0.0;
-    if (is_dir(bc, m, xa + 1, y) || (unsigned)(xa + 1) > (unsigned)m || (unsigned)y > (unsigned)m) tb = 0.0;
-    Nm = q.N; NEm = q.NE; NWm = q.NW;
-    q = qn;
-    qn = ld9<false>(L, off, xa, y + 2);
-    zm = z0; z0 = zp;
-  };
-  double w[4], ta, tb, w0, w1;
-  S9 A, Bc;
-  // odd row 2J0−1: contributions to coarse row J0 (V-edge N weight, centre NW own / NE previous lane)
-  row(ys, ta, tb, A, Bc);
-  W4(J0 - 1, w);
-  edge_w(A, false, opdep != 0, false, false, false, w0, w1);
-  double carry_own = w1 * ta + w[2] * tb, carry_ne = w[3] * tb;
-  double* rcb = rc + (int64_t)b * gc.N;
-  for (int J = J0; J < J1; ++J) {
-    // even row 2J: C point (a) and H-edge (b)
-    row(2 * J, ta, tb, A, Bc);
-    edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
-    double acc = carry_own + shup(carry_ne) + ta + w0 * tb;
-    const double he = w1 * tb;  // H-edge (2I+1, 2J) → (I+1, J)
-    acc += shup(he);
-    // odd row 2J+1: V-edge (a) and centre (b)
-    row(2 * J + 1, ta, tb, A, Bc);
-    W4(J, w);
-    edge_w(A, false, opdep != 0, false, false, false, w0, w1);
-    const double se = w[1] * tb;
-    acc += w0 * ta + w[0] * tb + shup(se);
-    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : acc;
-    carry_own = w1 * ta + w[2] * tb;
-    carry_ne = w[3] * tb;
-  }
-}
-
-// Prolongation + post-smoother (black then red), ingesting one row per step:
-//   v(y) = z + P zc (both columns);  black new(y−1) = (r − Σ_8 a v)/C;
-//   red new(y−2) = (r − Σ_WENS a black_new − Σ_diag a v)/C.
-// Writes z2 (row y−2: red new and black new).
-__global__ void __launch_bounds__(MT) c_up_march_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
-                                                        const double* __restrict__ z, PW4 pw, Geo gc,
-                                                        const double* __restrict__ zc, double* __restrict__ z2,
-                                                        const int* flags) {
-  C9_PROLOGUE
-  const double *rb = r + off, *zb = z + off, *zcb = zc + (int64_t)b * gc.N;
-  const int I = xa >> 1, nc0 = gc.n0;
-  const int mcl = m / 2;
-  const int64_t cb0 = (int64_t)b * mcl * mcl;
-  auto ZC = [&](int Ic, int Jc) {
-    return ((unsigned)Ic < (unsigned)nc0 && (unsigned)Jc < (unsigned)nc0) ? __ldg(zcb + (int64_t)Jc * nc0 + Ic) : 0.0;
-  };
-  // prolonged pair of row y from its stencils (edge weights) and loads
-  auto prolong = [&](int y, const S9& A, const S9& Bc, Pair zz) {
-    Pair v = zz;
-    if ((unsigned)y > (unsigned)m) return Pair{0.0, 0.0};
-    double w0, w1;
-    if (RED_IS_A(y)) {  // a = C point, b = H-edge
-      const int Jc = y >> 1;
-      const double c0 = ZC(I, Jc), c1 = ZC(I + 1, Jc);
-      v.a += c0;
-      edge_w(Bc, true, opdep != 0, false, false, false, w0, w1);
-      v.b += w0 * c0 + w1 * c1;
-    } else {  // a = V-edge, b = centre
-      const int Jc = y >> 1;
-      const double c00 = ZC(I, Jc), c10 = ZC(I + 1, Jc), c01 = ZC(I, Jc + 1), c11 = ZC(I + 1, Jc + 1);
-      edge_w(A, false, opdep != 0, false, false, false, w0, w1);
-      v.a += w0 * c00 + w1 * c01;
-      const bool ok = I >= 0 && I < mcl && Jc < mcl;
-      const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-      if (ok)
-        v.b += __ldg(pw.w0 + cell) * c00 + __ldg(pw.w1 + cell) * c10 + __ldg(pw.w2 + cell) * c01 +
-               __ldg(pw.w3 + cell) * c11;
-    }
-    if ((unsigned)xa > (unsigned)m || is_dir(bc, m, xa, y)) v.a = 0.0;
-    if ((unsigned)xb > (unsigned)m || is_dir(bc, m, xb, y)) v.b = 0.0;
-    return v;
-  };
-  const Pair zero{0.0, 0.0};
-  const S9 unit{1, 0, 0, 0, 0, 0, 0, 0, 0};
-  // state entering the step for row y: q = loads of row y, Nm/NEm/NWm of row y−1, r/z of row y
-  int y = y0 - 3;
-  R9 q = ld9<false>(L, off, xa, y);
-  Pair Nm = ld2<false>(L.N + off, xa, y - 1, n0), NEm = ld2<false>(L.NE + off, xa, y - 1, n0),
-       NWm = ld2<false>(L.NW + off, xa, y - 1, n0);
-  Pair rq = ld2<false>(rb, xa, y, n0), zq = ld2<false>(zb, xa, y, n0);
-  Pair vm3 = zero, vm2 = zero, vm1 = zero;  // v of rows y−3, y−2, y−1
-  double zbn2 = 0.0, zbn1 = 0.0;             // black new of rows y−3, y−2
-  S9 sb1 = unit;                             // black stencil of row y−1
-  S9 sr1 = unit, sr2 = unit;                 // red stencils of rows y−1, y−2
-  double rb1 = 0.0, rr1 = 0.0, rr2 = 0.0;    // r at the black node of row y−1, red nodes of rows y−1, y−2
-  for (; y < y1 + 2; ++y) {
-    const R9 qc = q;
-    const Pair rc0 = rq, zc0 = zq;
-    q = ld9<false>(L, off, xa, y + 1);
-    rq = ld2<false>(rb, xa, y + 1, n0);
-    zq = ld2<false>(zb, xa, y + 1, n0);
-    S9 A, Bc;
-    st9_pair(qc, Nm, NEm, NWm, A, Bc);
-    // the halo lanes have no neighbour lane beyond them: load the couplings their prolongation
-    // weights need (lane 0: V-edge W/SW; lane 31: H-edge SE)
-    if (lane == 0) {
-      A.w = ldv<false>(L.E + off, xa - 1, y, n0);
-      A.sw = ldv<false>(L.NE + off, xa - 1, y - 1, n0);
-    } else if (lane == 31) {
-      Bc.se = ldv<false>(L.NW + off, xb + 1, y - 1, n0);
-    }
-    Nm = qc.N; NEm = qc.NE; NWm = qc.NW;
-    const Pair v0 = prolong(y, A, Bc, zc0);
-    // black new of row y−1 (its black column is b when row y−1 has red at a)
-    const bool ra1 = RED_IS_A(y - 1);
-    const double d1 = ra1 ? dot8_b(sb1, vm2, vm1, v0) : dot8_a(sb1, vm2, vm1, v0);
-    const double zbn0 = (rb1 - d1) / sb1.c;
-    // red new of row y−2 (red column a when row y−2 is even): W/E are the same row's black new,
-    // N/S the black new of rows y−1 / y−3 in the same column, the diagonals the red prolonged
-    // values of rows y−1 / y−3 in the other column
-    const bool ra2 = RED_IS_A(y - 2);
-    const double e_b = ra2 ? zbn1 : shdn(zbn1), w_b = ra2 ? shup(zbn1) : zbn1;
-    const double d_ne = ra2 ? vm1.b : shdn(vm1.a), d_nw = ra2 ? shup(vm1.b) : vm1.a;
-    const double d_se = ra2 ? vm3.b : shdn(vm3.a), d_sw = ra2 ? shup(vm3.b) : vm3.a;
-    const double s2 = sr2.e * e_b + sr2.w * w_b + sr2.n * zbn0 + sr2.s * zbn2 + sr2.ne * d_ne + sr2.nw * d_nw +
-                      sr2.se * d_se + sr2.sw * d_sw;
-    const double zrn = (rr2 - s2) / sr2.c;
-    const int yo = y - 2;
-    if (yo >= y0 && yo < y1) {
-      double* out = z2 + off + (int64_t)yo * n0;
-      if (outa) out[xa] = ra2 ? zrn : zbn1;
-      if (outb) out[xb] = ra2 ? zbn1 : zrn;
-    }
-    // shift to row y+1
-    const bool ra0 = RED_IS_A(y);
-    vm3 = vm2; vm2 = vm1; vm1 = v0;
-    zbn2 = zbn1; zbn1 = zbn0;
-    sr2 = sr1; sr1 = ra0 ? A : Bc;
-    rr2 = rr1; rr1 = ra0 ? rc0.a : rc0.b;
-    sb1 = ra0 ? Bc : A;
-    rb1 = ra0 ? rc0.b : rc0.a;
-  }
-}
 
 // ---- coarse levels: cp.async-staged marching ------------------------------------------------------
 // The register-marching coarse kernels above hold the next row's loads in registers (≈190
@@ -2067,15 +1470,9 @@ struct UpLayout {
   static constexpr int WORDS = (X + 3 + 1) & ~1;  // doubles per warp-row (even: 16-byte alignment)
 };
 enum { UP_C = 0, UP_E = 1, UP_N = 2, UP_NE = 3, UP_NW = 4, UP_R = 5, UP_Z = 6 };
-#ifndef OSC_UP_RING
-#define OSC_UP_RING 3
-#endif
-#ifndef OSC_UP_MINB
-#define OSC_UP_MINB 3
-#endif
 // rows staged per warp: 3 × 582 × 8 B = 14 KB per warp (RZ). A/B with one-warp CTAs: 4 or 5 rows are
 // slower (coarse up sweep 19.4 → 28 ms per config-4 step: fewer resident warps)
-constexpr int UP_RING = OSC_UP_RING;
+constexpr int UP_RING = 3;
 template <bool RZ>
 constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * CU_W * UpLayout<RZ>::WORDS; }
 
@@ -2084,7 +1481,7 @@ constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * CU_W * UpLay
 // r/C, black z = (r − Σ_WENS a z_red)/C, as c_pre_march_kernel) instead of loaded, so the down
 // sweep need not store it.
 template <bool RZ>
-__global__ void __launch_bounds__(32 * CU_W, OSC_UP_MINB * 4 / CU_W) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+__global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                           const double* __restrict__ z, PW4 pw, Geo gc,
                                                           const double* __restrict__ zc, double* __restrict__ z2,
                                                           const int* flags) {
@@ -2312,16 +1709,10 @@ __global__ void __launch_bounds__(32 * CU_W, OSC_UP_MINB * 4 / CU_W) c_up_ring_k
 // weights of the odd rows are loaded into registers one row pair ahead.
 enum { DN_C = 0, DN_E = 1, DN_N = 2, DN_NE = 3, DN_NW = 4, DN_R = 5, DN_WORDS = 6 * 64 };
 constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 4 × 4 warps × 384 × 8 B = 48 KB
-#ifndef OSC_CD_W
-#define OSC_CD_W 4
-#endif
-constexpr int CD_W = OSC_CD_W;  // warps per CTA of the coarse ring down sweep
+constexpr int CD_W = 4;  // warps per CTA of the coarse ring down sweep
 constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * CD_W * DN_WORDS;
 
-#ifndef OSC_CDRING_MINB
-#define OSC_CDRING_MINB 4
-#endif
-__global__ void __launch_bounds__(32 * CD_W, OSC_CDRING_MINB * 4 / CD_W) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
+__global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9 L, int bc, int opdep, const double* __restrict__ r,
                                                             PW4 pw, Geo gc, double* __restrict__ rc,
                                                             const int* flags) {
   const int b = blockIdx.z;
@@ -2492,14 +1883,8 @@ constexpr int L0R_RING = 5;
 // the 4-warp up sweep). Config 4 per step: smooth_up 37.6 → 31.6 ms, restrict 23.8 → 20.4 ms,
 // coarse up 20.6 → 19.3 ms (2048² solve); the coarse down sweep is slower with one warp
 // (16.0 → 21.4 ms) and keeps four.
-#ifndef OSC_SUR_W
-#define OSC_SUR_W 1
-#endif
-constexpr int SUR_W = OSC_SUR_W;
-#ifndef OSC_RR_W
-#define OSC_RR_W 1
-#endif
-constexpr int RR_W = OSC_RR_W;  // level-0 ring restriction
+constexpr int SUR_W = 1;
+constexpr int RR_W = 1;  // level-0 ring restriction
 constexpr size_t L0R_SMEM_UP = sizeof(double) * L0R_RING * SUR_W * L0R_WORDS_UP;  // 51.5 KB at 4 warps
 constexpr size_t L0R_SMEM_DN = sizeof(double) * L0R_RING * RR_W * L0R_WORDS_DN;  // 20.5 KB
 
@@ -2608,10 +1993,7 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   cpa_wait<0>();
 }
 
-#ifndef OSC_RRING_MINB
-#define OSC_RRING_MINB 4
-#endif
-__global__ void __launch_bounds__(32 * RR_W, OSC_RRING_MINB * 4 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(32 * RR_W, 4 * 4 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                               const double* __restrict__ r, PW4 pw,
                                                               double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;
@@ -2769,10 +2151,7 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
   return make_double2(rz, dc);
 }
 
-#ifndef OSC_SURR_MINB
-#define OSC_SURR_MINB 3
-#endif
-__global__ void __launch_bounds__(32 * SUR_W, OSC_SURR_MINB * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(32 * SUR_W, 3 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                                const double* __restrict__ r,
                                                                double* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,
@@ -2795,26 +2174,6 @@ __global__ void __launch_bounds__(32 * SUR_W, OSC_SURR_MINB * 4 / SUR_W) smooth_
     scal[b * S_NSCAL + S_ALPHA] = gamma / den;
     scal[b * S_NSCAL + S_RZ] = gamma;
   }
-}
-
-// Level-0 restriction kernel (reads k, z and the level-0 centre weights).
-__global__ void __launch_bounds__(MT) restrict_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                      const double* __restrict__ z, PW4 pw,
-                                                      double* __restrict__ rc, const int* flags) {
-  const int b = blockIdx.z;
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
-  const int I = strip * 30 - 1 + lane;
-  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
-  const int lyc = coarse_rows_per_warp(gc.m);
-  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
-  // interior: fine rows 2J0−2 … 2J1+1 and columns xa(lane 0)−1 … xb(lane 31)+1 are in-grid,
-  // non-Dirichlet nodes with in-grid neighbours
-  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 4 >= 2 &&
-                        2 * J1 + 4 <= g.m - 1;
-  if (interior) restrict_z_body<true, false>(g, gc, bc, k, nullptr, z, pw, rc, b, I, outI, J0, J1);
-  else restrict_z_body<false, false>(g, gc, bc, k, nullptr, z, pw, rc, b, I, outI, J0, J1);
 }
 
 // Level-0 restriction from the residual itself: the red-black pre-smoother from z = 0 is formed in
@@ -2897,152 +2256,6 @@ __device__ __forceinline__ void restrict_r_body(Geo g, Geo gc, int bc, const dou
     if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
     a_nw = t * wc[2];
     a_ne = t * wc[3];
-  }
-}
-
-#ifndef OSC_RR_MINB
-#define OSC_RR_MINB 4
-#endif
-__global__ void __launch_bounds__(MT, OSC_RR_MINB) restrict_r_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                        const double* __restrict__ r, PW4 pw,
-                                                        double* __restrict__ rc, const int* flags) {
-  const int b = blockIdx.z;
-  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
-  const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * MW + (threadIdx.x >> 5);
-  const int I = strip * 30 - 1 + lane;
-  const bool outI = lane >= 1 && lane < 31 && I <= gc.m;
-  const int lyc = coarse_rows_per_warp(gc.m);
-  const int J0 = blockIdx.y * lyc, J1 = min(J0 + lyc, gc.n0);
-  // interior: every node whose stencil or k the pipeline touches (fine rows 2J0−5 … 2J1+3,
-  // columns xa(lane 0)−1 … xb(lane 31)+1 and their neighbours) is in-grid and non-Dirichlet
-  const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 6 >= 1 &&
-                        2 * J1 + 4 <= g.m - 1;
-  if (interior) restrict_r_body<true>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1);
-  else restrict_r_body<false>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1);
-}
-
-// ---- prolongation + post-smoother, level 0: reads the pre-smoothed z written by pcg_update_down ---------
-template <bool INT, bool EN>
-__device__ __forceinline__ double smooth_up_z_body(Geo g, Geo gc, int bc,
-                                                       const double* __restrict__ ca,
-                                                       const double* __restrict__ cb,
-                                                       const double* __restrict__ r,
-                                                       const double* __restrict__ z,
-                                                       double* __restrict__ z_out,
-                                                       const double* __restrict__ zc, PW4 pw, int finest,
-                                                       double* scal, int* flags, double2* partial,
-                                                       int maxp, unsigned* counter, const PairCtx& c) {
-  PAIR_UNPACK
-
-  const double *rb = r + off, *zbp = z + off, *zcb = zc + (int64_t)b * gc.N;
-  const int nc0 = gc.n0;
-  const Pair zero{0.0, 0.0};
-  // Red node of row y after prolongation: z_red + P zc (fem.cpp:144-165). Row y even: red at xa
-  // (even, even) → zc(xa/2, y/2). Row y odd: red at xb (odd, odd), the centre of cell (I, J):
-  // Σ of its 4 corner weights × zc(I or I+1, J or J+1). Raw values are loaded one row ahead and
-  // combined when used.
-  struct ZRaw {
-    double z, c00, c10, c01, c11, w0, w1, w2, w3;
-  };
-  const int I = xa >> 1;
-  const int mcl = m / 2;
-  const int64_t cb0 = (int64_t)b * mcl * mcl;
-  // red value of row y after prolongation (the black column's entry is 0 until the black sweep)
-  auto ZL = [&](int y) {
-    ZRaw v{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if ((unsigned)y >= (unsigned)n0) return v;
-    if (RED_IS_A(y)) {
-      if (INT || (unsigned)xa < (unsigned)n0) {
-        v.z = __ldg(zbp + (int64_t)y * n0 + xa);
-        v.c00 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
-      }
-    } else if (INT || (unsigned)xb < (unsigned)n0) {
-      const int J = y >> 1;
-      v.z = __ldg(zbp + (int64_t)y * n0 + xb);
-      const double* c0r = zcb + (int64_t)J * nc0 + I;
-      v.c00 = __ldg(c0r);
-      v.c10 = __ldg(c0r + 1);
-      v.c01 = __ldg(c0r + nc0);
-      v.c11 = __ldg(c0r + nc0 + 1);
-      if (INT || (I < mcl && J < mcl)) {  // xb ≤ m − 1 and y ≤ m − 1 for a centre
-        const int64_t cell = cb0 + (int64_t)J * mcl + I;
-        v.w0 = __ldg(pw.w0 + cell);
-        v.w1 = __ldg(pw.w1 + cell);
-        v.w2 = __ldg(pw.w2 + cell);
-        v.w3 = __ldg(pw.w3 + cell);
-      }
-    }
-    return v;
-  };
-  auto ZC = [&](const ZRaw& v, int y) {
-    return RED_IS_A(y) ? v.z + v.c00 : v.z + (v.w0 * v.c00 + v.w1 * v.c10 + v.w2 * v.c01 + v.w3 * v.c11);
-  };
-  EdgeRows<INT, EN> er(ca + off, EN ? cb + off : nullptr, xa, n0, m, y0 - 2);
-  // scalars: qa/qb/qc = red values of rows t, t+1, t+2; zbm/zb0 = black values of rows t−1, t
-  double qa = ZC(ZL(y0 - 2), y0 - 2), qb = ZC(ZL(y0 - 1), y0 - 1);
-  Pair Nt, Ed;
-  er.next(Ed, Nt);
-  Pair r0 = zero;
-  double zbm = 0.0, zb0 = 0.0;
-  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
-  Pair rq = ld2<INT>(rb, xa, y0 - 1, n0);
-  ZRaw zq = ZL(y0);
-  double rz = 0.0;
-  for (int t = y0 - 2; t < y1; ++t) {
-    const bool ra1 = RED_IS_A(t + 1);  // row t+1: red column a, black b (else the reverse)
-    const Pair r1 = rq;
-    const double qc = ZC(zq, t + 2);
-    zq = ZL(t + 3);
-    rq = ld2<INT>(rb, xa, t + 2, n0);
-    Pair E1, N1;
-    er.next(E1, N1);
-    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
-    // black node of row t+1: (r − Σ A z_red_prolonged)/D; its x-neighbours are row t+1's red
-    // nodes (own column and the next/previous lane's)
-    const double qb_e = shdn(qb), qb_w = shup(qb);
-    const Sten sb = ra1 ? st1.b : st1.a;
-    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
-    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
-    // output row t: red column = (r − Σ A z_black)/D, black column = z_black
-    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
-    const bool ra0 = !ra1;
-    const double zred = ((ra0 ? r0.a : r0.b) - (sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) +
-                                                 sr0.n * zbp1 + sr0.s * zbm)) * rcp64(sr0.d);
-    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
-    if (t >= y0) {
-      double* out = z_out + off + (int64_t)t * n0;
-      if (outa) {
-        out[xa] = zv.a;
-        rz = fma(r0.a, zv.a, rz);
-      }
-      if (outb) {
-        out[xb] = zv.b;
-        rz = fma(r0.b, zv.b, rz);
-      }
-    }
-    qa = qb; qb = qc; Nt = N1;
-    r0 = r1; zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
-  }
-  return rz;
-}
-
-// Level-0 prolongation + post-smoother (reads k, r, z, zc and the level-0 centre weights); <r, z> → β.
-__global__ void __launch_bounds__(MT, 4) smooth_up_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                       const double* __restrict__ r,
-                                                       const double* __restrict__ z,
-                                                       double* __restrict__ z_out,
-                                                       const double* __restrict__ zc, PW4 pw,
-                                                       double* scal, int* flags, double2* partial,
-                                                       int maxp, unsigned* counter) {
-  PAIR_PROLOGUE
-  const double rz = interior ? smooth_up_z_body<true, false>(g, gc, bc, k, nullptr, r, z, z_out, zc, pw, 1, scal, flags, partial, maxp, counter, c)
-                             : smooth_up_z_body<false, false>(g, gc, bc, k, nullptr, r, z, z_out, zc, pw, 1, scal, flags, partial, maxp, counter, c);
-  double t0, t1;
-  if (reduce2_last(rz, 0.0, partial, maxp, counter, b, t0, t1) && threadIdx.x == 0) {
-    const double old = scal[b * S_NSCAL + S_RZ];
-    scal[b * S_NSCAL + S_BETA] = flags[b * F_NFLAGS + F_ITERS] == 0 ? 0.0 : t0 / old;
-    scal[b * S_NSCAL + S_RZ] = t0;
   }
 }
 
@@ -3156,36 +2369,6 @@ __device__ __forceinline__ double2 smooth_up_r_body(Geo g, Geo gc, int bc, const
   }
   return make_double2(rz, dc);
 }
-
-// Level-0 prolongation + post-smoother (reads k, r, zc, pw); epilogue: γ, δ → β, α of the next PCG
-// step (one-reduction PCG).
-#ifndef OSC_SUR_MINB
-#define OSC_SUR_MINB 4
-#endif
-__global__ void __launch_bounds__(MT, OSC_SUR_MINB) smooth_up_r_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                            const double* __restrict__ r,
-                                                            double* __restrict__ z_out,
-                                                            const double* __restrict__ zc, PW4 pw,
-                                                            double* scal, int* flags, double2* partial,
-                                                            int maxp, unsigned* counter) {
-  PAIR_PROLOGUE
-  // the interior body reads k rows up to y1+3 and forms stencils up to row y1+1
-  const bool interior3 = interior && c.y1 <= g.m - 3;
-  const double2 gd = interior3 ? smooth_up_r_body<true>(g, gc, bc, k, r, z_out, zc, pw, c)
-                               : smooth_up_r_body<false>(g, gc, bc, k, r, z_out, zc, pw, c);
-  double gamma, dcorr;
-  if (reduce2_last(gd.x, gd.y, partial, maxp, counter, b, gamma, dcorr) && threadIdx.x == 0) {
-    const double delta = gamma + dcorr;
-    const bool first = flags[b * F_NFLAGS + F_ITERS] == 0;
-    const double beta = first ? 0.0 : gamma / scal[b * S_NSCAL + S_RZ];
-    double den = first ? delta : delta - beta * gamma / scal[b * S_NSCAL + S_ALPHA];
-    if (!(den > 0.0)) den = delta;  // rounding guard (⟨p, Ap⟩ > 0 in exact arithmetic)
-    scal[b * S_NSCAL + S_BETA] = beta;
-    scal[b * S_NSCAL + S_ALPHA] = gamma / den;
-    scal[b * S_NSCAL + S_RZ] = gamma;
-  }
-}
-
 
 // device view of the global hierarchy (one level's operator and centre weights)
 struct SolverLevelDev {
@@ -3743,10 +2926,6 @@ inline dim3 march_grid(int m, int /*hx*/, int B) {
   const int ly = rows_per_warp(m);
   return dim3((unsigned)((march_strips(m) + MW - 1) / MW), (unsigned)((m + 1 + ly - 1) / ly), (unsigned)B);
 }
-inline dim3 restrict_grid(int mc, int B) {
-  const int lyc = coarse_rows_per_warp(mc);
-  return dim3((unsigned)(((mc + 1 + 29) / 30 + MW - 1) / MW), (unsigned)((mc + 1 + lyc - 1) / lyc), (unsigned)B);
-}
 inline dim3 restrict_grid_w(int mc, int B, int wpb) {
   const int lyc = coarse_rows_per_warp(mc);
   return dim3((unsigned)(((mc + 1 + 29) / 30 + wpb - 1) / wpb), (unsigned)((mc + 1 + lyc - 1) / lyc), (unsigned)B);
@@ -3869,41 +3048,13 @@ HierDev hier_of(const SolverWork& w, int l0) {
   return H;
 }
 
-// Coarse-level (9-point) V-cycle kernels, OSC_COARSE_MODE: 0 register marching (pre, restrict, up);
-// 1 the same with the up kernel ring-staged; 2 (default) fused ring-staged down sweep (pre-smoother +
-// restriction, z never stored) and the ring-staged up kernel recomputing z.
-int coarse_mode() {
-  static const int mode = [] {
-    const char* e = std::getenv("OSC_COARSE_MODE");
-    return e ? std::atoi(e) : 2;
-  }();
-  return mode;
-}
-
-// Level-0 PCG variant: one-reduction (Chronopoulos–Gear) iteration with the pre-smoother recomputed
-// from r (default), or OSC_LEGACY_PCG=1: ⟨p, Ap⟩ pass + update fused with the stored pre-smoother.
-bool pcg_one_reduction() {
-  static const bool on = std::getenv("OSC_LEGACY_PCG") == nullptr;
-  return on;
-}
-
-// Level-0 restriction / up sweep through the cp.async ring (default) or register-prefetched
-// (OSC_L0_RING=0).
-bool l0_ring() {
-  static const bool on = [] {
-    const char* e = std::getenv("OSC_L0_RING");
-    return !(e && e[0] == '0');
-  }();
-  if (on) {
-    smem_attr(smooth_up_ring_kernel, L0R_SMEM_UP);
-    smem_attr(restrict_ring_kernel, L0R_SMEM_DN);
-  }
-  return on;
-}
-
-// Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2). lev[0].z holds the level-0
-// pre-smoothed correction, written by pcg_update_down (z0_fresh).
-void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
+// Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2): V(1,1) with red-black GS.
+// Levels with a coarser level below run ring-staged sweeps: level 0 the restriction (pre-smoother
+// recomputed from r) and the up sweep (prolongation + post-smoother, fused with γ = ⟨r, z⟩ and
+// δ = ⟨z, Az⟩ of the one-reduction PCG); 9-point levels the fused down sweep (pre-smoother +
+// residual + restriction, z never stored) and the up sweep (z recomputed). The first level with
+// m ≤ 32 and at least two levels below it runs the rest of the cycle CTA-resident (sub_vcycle).
+void vcycle(Ctx* ctx, int bc, int B) {
   SolverWork& w = ctx->solver;
   cudaStream_t st = ctx->stream;
   double2* part = reinterpret_cast<double2*>(w.partial);
@@ -3918,63 +3069,28 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     OSC_CUDA(cudaGetLastError());
     return;
   }
-  // first level handled by the CTA-resident tail (m ≤ 32, at least two levels below it)
-  static const bool sub_off = std::getenv("OSC_NO_SUB_VCYCLE") != nullptr;
   int ls = w.nlev - 1;
-  if (!sub_off)
-    for (int l = 1; l < w.nlev - 1; ++l)
-      if (w.lev[l].m <= 32) { ls = l; break; }
-  const SolverLevel& L0 = w.lev[0];
-  OSC_REQUIRE(z0_fresh, "vcycle: level-0 pre-smoothed z missing");
-  // OSC_SIMPLE_COARSE: coarse levels with the one-thread-per-node kernels (A/B and debugging)
-  static const bool simple_all = std::getenv("OSC_SIMPLE_COARSE") != nullptr;
-  static const bool simple_down = simple_all || std::getenv("OSC_SIMPLE_DOWN") != nullptr;
-  static const bool simple_up = simple_all || std::getenv("OSC_SIMPLE_UP") != nullptr;
+  for (int l = 1; l < w.nlev - 1; ++l)
+    if (w.lev[l].m <= 32) {
+      ls = l;
+      break;
+    }
   // down
   for (int l = 0; l < ls; ++l) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     if (l == 0) {
-      KScope ks(ctx, pcg_one_reduction() ? "mg_restrict_r.L0" : "mg_restrict.L0");
-      if (pcg_one_reduction() && l0_ring())
-        restrict_ring_kernel<<<restrict_grid_w(C.m, B, RR_W), 32 * RR_W, L0R_SMEM_DN, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur,
-                                                                           pw_of(L), C.r, w.flags);
-      else if (pcg_one_reduction())
-        restrict_r_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, pw_of(L),
-                                                               C.r, w.flags);
-      else
-        restrict_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, L.z, pw_of(L), C.r,
-                                                             w.flags);
+      smem_attr(restrict_ring_kernel, L0R_SMEM_DN);
+      KScope ks(ctx, "mg_restrict_r.L0");
+      restrict_ring_kernel<<<restrict_grid_w(C.m, B, RR_W), 32 * RR_W, L0R_SMEM_DN, st>>>(
+          geo_of(L), geo_of(C), bc, L.k, w.r_cur, pw_of(L), C.r, w.flags);
       continue;
     }
-    const L9 l9 = l9_of(L);
-    if (simple_down) {  // one thread per node (reference implementation of the same V-cycle)
-      const dim3 gf(nblocks(L.N), 1, B);
-      {
-        KScope ks(ctx, lvl_name("mg_pre", l).c_str(), 2);
-        c_pre_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, w.flags);
-        c_pre_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, w.flags);
-      }
-      KScope ks(ctx, lvl_name("mg_restrict", l).c_str(), 2);
-      c_resid_kernel<<<gf, NT, 0, st>>>(l9, L.r, L.z, L.z2, w.flags);
-      c_restrict_kernel<<<dim3(nblocks(C.N), 1, B), NT, 0, st>>>(l9, bc, w.opdep, L.z2, L.pw[0], L.pw[1], L.pw[2],
-                                                                 L.pw[3], geo_of(C), C.r, w.flags);
-      continue;
-    }
-    if (coarse_mode() == 2) {  // fused pre-smoother + restriction (z not stored)
-      smem_attr(c_down_ring_kernel, DN_RING_SMEM);
-      KScope ks(ctx, lvl_name("mg_down", l).c_str());
-      c_down_ring_kernel<<<restrict_grid_w(C.m, B, CD_W), 32 * CD_W, DN_RING_SMEM, st>>>(l9, bc, w.opdep, L.r, pw_of(L),
-                                                                          geo_of(C), C.r, w.flags);
-      continue;
-    }
-    {
-      KScope ks(ctx, lvl_name("mg_pre", l).c_str());
-      c_pre_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, L.r, L.z, w.flags);
-    }
-    KScope ks(ctx, lvl_name("mg_restrict", l).c_str());
-    c_restrict_march_kernel<<<restrict_grid(C.m, B), MT, 0, st>>>(l9, bc, w.opdep, L.z, pw_of(L), geo_of(C), C.r,
-                                                                  w.flags);
+    smem_attr(c_down_ring_kernel, DN_RING_SMEM);
+    KScope ks(ctx, lvl_name("mg_down", l).c_str());
+    c_down_ring_kernel<<<restrict_grid_w(C.m, B, CD_W), 32 * CD_W, DN_RING_SMEM, st>>>(l9_of(L), bc, w.opdep, L.r,
+                                                                                      pw_of(L), geo_of(C), C.r,
+                                                                                      w.flags);
   }
   if (ls < w.nlev - 1) {
     const SolverLevel& S = w.lev[ls];
@@ -3994,77 +3110,17 @@ void vcycle(Ctx* ctx, int bc, int B, bool z0_fresh) {
     const SolverLevel& L = w.lev[l];
     const SolverLevel& C = w.lev[l + 1];
     if (l == 0) {
-      KScope ks(ctx, pcg_one_reduction() ? "mg_smooth_up_r.L0" : "mg_smooth_up.L0");
-      if (pcg_one_reduction() && l0_ring())
-        smooth_up_ring_kernel<<<march_grid_w(L.m, B, SUR_W), 32 * SUR_W, L0R_SMEM_UP, st>>>(
-            geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2, C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
-            w.counter);
-      else if (pcg_one_reduction())
-        smooth_up_r_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2,
-                                                                C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
-                                                                w.counter);
-      else
-        smooth_up_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z, L.z2,
-                                                              C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
-                                                              w.counter);
+      smem_attr(smooth_up_ring_kernel, L0R_SMEM_UP);
+      KScope ks(ctx, "mg_smooth_up_r.L0");
+      smooth_up_ring_kernel<<<march_grid_w(L.m, B, SUR_W), 32 * SUR_W, L0R_SMEM_UP, st>>>(
+          geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2, C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
+          w.counter);
       continue;
     }
-    const L9 l9 = l9_of(L);
-    if (simple_up) {
-      const dim3 gf(nblocks(L.N), 1, B);
-      KScope ks(ctx, lvl_name("mg_smooth_up", l).c_str(), 3);
-      c_prolong_kernel<<<gf, NT, 0, st>>>(l9, bc, w.opdep, L.pw[0], L.pw[1], L.pw[2], L.pw[3], geo_of(C), C.z2,
-                                          L.z, w.flags);
-      c_post_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, L.z, L.z2, w.flags);
-      c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, L.z, L.z2, w.flags);
-      continue;
-    }
-    KScope ks(ctx, lvl_name(coarse_mode() == 2 ? "mg_up" : "mg_smooth_up", l).c_str());
-    static const bool dbg = std::getenv("OSC_DEBUG_UP") != nullptr;
-    double *tz = nullptr, *tz2 = nullptr;
-    const size_t nb = sizeof(double) * L.N * B;
-    if (dbg) {
-      OSC_CUDA(cudaMalloc(&tz, nb));
-      OSC_CUDA(cudaMalloc(&tz2, nb));
-      OSC_CUDA(cudaMemcpyAsync(tz, L.z, nb, cudaMemcpyDeviceToDevice, st));
-    }
-    const int up_mode = coarse_mode();
-    if (up_mode == 0) {
-      c_up_march_kernel<<<march_grid(L.m, 2, B), MT, 0, st>>>(l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2,
-                                                              L.z2, w.flags);
-    } else if (up_mode == 1) {
-      smem_attr(c_up_ring_kernel<false>, up_ring_smem<false>());
-      c_up_ring_kernel<false><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<false>(), st>>>(
-          l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
-    } else {
-      smem_attr(c_up_ring_kernel<true>, up_ring_smem<true>());
-      c_up_ring_kernel<true><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<true>(), st>>>(
-          l9, bc, w.opdep, L.r, L.z, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
-    }
-    if (dbg) {
-      OSC_CUDA(cudaMemcpyAsync(tz2, L.z2, nb, cudaMemcpyDeviceToDevice, st));
-      const dim3 gf(nblocks(L.N), 1, B);
-      c_prolong_kernel<<<gf, NT, 0, st>>>(l9, bc, w.opdep, L.pw[0], L.pw[1], L.pw[2], L.pw[3], geo_of(C), C.z2,
-                                          tz, w.flags);
-      c_post_kernel<<<gf, NT, 0, st>>>(l9, 0, L.r, tz, L.z2, w.flags);
-      c_post_kernel<<<gf, NT, 0, st>>>(l9, 1, L.r, tz, L.z2, w.flags);
-      std::vector<double> a(L.N * B), bb(L.N * B);
-      OSC_CUDA(cudaMemcpyAsync(a.data(), tz2, nb, cudaMemcpyDeviceToHost, st));
-      OSC_CUDA(cudaMemcpyAsync(bb.data(), L.z2, nb, cudaMemcpyDeviceToHost, st));
-      OSC_CUDA(cudaStreamSynchronize(st));
-      double mx = 0, ref = 0;
-      int64_t at = -1;
-      for (int64_t i = 0; i < L.N * B; ++i) {
-        ref = std::max(ref, std::fabs(bb[i]));
-        if (std::fabs(a[i] - bb[i]) > mx) { mx = std::fabs(a[i] - bb[i]); at = i; }
-      }
-      const int64_t s0 = at / L.N, li = at % L.N;
-      fprintf(stderr, "DEBUG_UP level %d m %d: max|diff| %.3e (ref %.3e) at sample %ld x %ld y %ld  march %.6e simple %.6e\n",
-              l, L.m, mx, ref, (long)s0, (long)(li % (L.m + 1)), (long)(li / (L.m + 1)), at >= 0 ? a[at] : 0.0,
-              at >= 0 ? bb[at] : 0.0);
-      cudaFree(tz);
-      cudaFree(tz2);
-    }
+    smem_attr(c_up_ring_kernel<true>, up_ring_smem<true>());
+    KScope ks(ctx, lvl_name("mg_up", l).c_str());
+    c_up_ring_kernel<true><<<march_grid_w(L.m, B, CU_W), 32 * CU_W, up_ring_smem<true>(), st>>>(
+        l9_of(L), bc, w.opdep, L.r, nullptr, pw_of(L), geo_of(C), C.z2, L.z2, w.flags);
   }
   OSC_CUDA(cudaGetLastError());
 }
@@ -4081,7 +3137,7 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
     KScope ks(ctx, "mg_setup.rows");
     const SolverLevel& L = w.lev[0];
     rediscretize_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(L0.k, g0, 1, bc, g0, L.C, L.E, L.Nw, L.NE, L.NW);
-  } else if (mode != OSC_COARSE_REDISCRETIZE && !std::getenv("OSC_UNFUSED_SETUP")) {
+  } else if (mode != OSC_COARSE_REDISCRETIZE) {
     // fused tiled Galerkin setup per level pair (galerkin_tile_kernel)
     smem_attr(galerkin_tile_kernel<true>, galerkin_tile_smem(true));
     smem_attr(galerkin_tile_kernel<false>, galerkin_tile_smem(false));
@@ -4099,27 +3155,24 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
             nullptr, l9_of(F), bc, w.opdep, geo_of(C), C.C, C.E, C.Nw, C.NE, C.NW, F.pw[0], F.pw[1], F.pw[2],
             F.pw[3]);
     }
-  } else {  // level-0 rows (5-point) into scratch: u, r, r2 are free until pcg_init
-    KScope ks(ctx, "mg_setup.rows");
-    rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, L0.r, w.r2);
-  }
-  const bool fused = w.nlev > 1 && mode != OSC_COARSE_REDISCRETIZE && !std::getenv("OSC_UNFUSED_SETUP");
-  for (int l = 0; !fused && l + 1 < w.nlev; ++l) {
-    const SolverLevel& F = w.lev[l];
-    const SolverLevel& C = w.lev[l + 1];
-    const L9 R = l == 0 ? L9{w.u, L0.r, w.r2, nullptr, nullptr, F.m, F.m + 1, F.N} : l9_of(F);
-    {  // P rows of level l into scratch (level 0's z, z2, p0, p1: free until the solve starts)
-      KScope ks(ctx, "mg_setup.prow");
-      prow_kernel<<<dim3(nblocks(F.N), B), NT, 0, st>>>(R, bc, w.opdep, L0.z, L0.z2, w.p0, w.p1, F.pw[0],
-                                                         F.pw[1], F.pw[2], F.pw[3]);
+  } else {  // REDISCRETIZE: level-0 rows (5-point) into scratch (u, r, r2 are free until pcg_init)
+    {
+      KScope ks(ctx, "mg_setup.rows");
+      rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, L0.r, w.r2);
     }
-    KScope ks(ctx, "mg_setup.coarse_op");
-    if (mode == OSC_COARSE_REDISCRETIZE)
+    for (int l = 0; l + 1 < w.nlev; ++l) {
+      const SolverLevel& F = w.lev[l];
+      const SolverLevel& C = w.lev[l + 1];
+      const L9 R = l == 0 ? L9{w.u, L0.r, w.r2, nullptr, nullptr, F.m, F.m + 1, F.N} : l9_of(F);
+      {  // P1 transfer weights of level l (centre weights pw; edges are ½)
+        KScope ks(ctx, "mg_setup.prow");
+        prow_kernel<<<dim3(nblocks(F.N), B), NT, 0, st>>>(R, bc, w.opdep, L0.z, L0.z2, w.p0, w.p1, F.pw[0],
+                                                           F.pw[1], F.pw[2], F.pw[3]);
+      }
+      KScope ks(ctx, "mg_setup.coarse_op");
       rediscretize_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(L0.k, g0, 2 << l, bc, geo_of(C), C.C, C.E, C.Nw,
                                                                 C.NE, C.NW);
-    else
-      rap_kernel<<<dim3(nblocks(C.N), B), NT, 0, st>>>(R, bc, L0.z, L0.z2, w.p0, w.p1, geo_of(C), C.C, C.E,
-                                                        C.Nw, C.NE, C.NW);
+    }
   }
   KScope ks(ctx, "mg_setup.factor");
   const SolverLevel& C = w.lev[w.nlev - 1];
@@ -4150,10 +3203,10 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
   SolverLevel& L0 = w.lev[0];
   const Geo g0 = geo_of(L0);
   w.r_cur = L0.r;
-  static const bool small_off = std::getenv("OSC_NO_SMALL_PCG") != nullptr;
   mg_setup(ctx, prob, B);
-  if (w.m <= 32 && w.nlev > 1 && w.hist_cap == 0 && !small_off) {
-    // whole solve CTA-resident (one CTA per sample, one launch)
+  if (w.m <= 32 && w.nlev > 1 && w.hist_cap == 0) {
+    // whole solve CTA-resident (one CTA per sample, one launch); a kept residual history takes the
+    // streaming path below
     const size_t sm = small_smem_bytes(w.m, w.nlev);
     smem_attr(small_pcg_kernel, sm);
     KScope ks(ctx, "small_pcg");
@@ -4164,14 +3217,11 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
     return;
   }
   OSC_CUDA(cudaMemsetAsync(w.n_active, 0, sizeof(int), st));
-  {  // uc_guess: nested iteration, start from the prolonged coarse coupled solution
-    // Large grids form the guess and r0 in a column-pair marching pass after the plain init (cfg4,
-    // 2048²: 4.5 → 3.3 ms per 64-sample batch); below m = 1024 the per-node init is faster (256²:
-    // 1.4 vs 2.0 ms). OSC_NESTED_SIMPLE=1 forces the per-node path (A/B).
-    static const bool nested_simple_env = std::getenv("OSC_NESTED_SIMPLE") != nullptr;
-    const bool nested_simple = nested_simple_env || w.m < 1024;
+  {  // uc_guess: nested iteration, start from the prolonged coarse coupled solution. Large grids form
+     // the guess and r0 in a column-pair marching pass (config 4, 2048²: 4.5 → 3.3 ms per 64-sample
+     // batch); below m = 1024 the per-node init is faster (256²: 1.4 vs 2.0 ms).
     KScope ks(ctx, "pcg_init");
-    if (uc_guess && !nested_simple) {
+    if (uc_guess && w.m >= 1024) {
       pcg_init_nested_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(
           g0, bc, prob->forcing, prob->forcing_value, prob->tol, prob->max_iter_factor, L0.k, uc_guess, w.u,
           w.r_cur, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
@@ -4182,14 +3232,18 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
                                            part, w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
     }
   }
-  if (w.nlev > 1 && pcg_one_reduction()) {
-    vcycle(ctx, bc, B, true);  // z = M r0; γ0, δ0 → α0
-    double* p_old = w.p0;
-    double* p_new = w.p1;
-    static const long hard_cap1 = [] {
-      const char* e = std::getenv("OSC_HARD_ITER_CAP");
-      return e ? std::atol(e) : -1L;
-    }();
+  // optional safety valve (tests): OSC_HARD_ITER_CAP stops the loop early; the samples still active
+  // are reported as not converged by solver_results()
+  static const long hard_cap = [] {
+    const char* e = std::getenv("OSC_HARD_ITER_CAP");
+    return e ? std::atol(e) : -1L;
+  }();
+  double* p_old = w.p0;
+  double* p_new = w.p1;
+  if (w.nlev > 1) {
+    // One-reduction (Chronopoulos–Gear) PCG: pcg_update forms p, u, r and ‖r‖; the V-cycle's up sweep
+    // returns γ = ⟨r, z⟩ and δ = ⟨z, Az⟩, hence β and α of the next update.
+    vcycle(ctx, bc, B);  // z = M r0; γ0, δ0 → α0
     // Lagged convergence polling: the active count after iteration i is copied to a pinned ring
     // slot behind an event, and the host reads it before launching iteration i + LAG. The device
     // queue never drains while the host polls; iterations launched after the last sample
@@ -4197,7 +3251,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
     constexpr int LAG = 2;
     int* ring = ctx->h_pinned_int + 4;
     for (int it = 0;; ++it) {
-      if (hard_cap1 >= 0 && it >= hard_cap1) {
+      if (hard_cap >= 0 && it >= hard_cap) {
         mark_active_failed_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, w.flags);
         break;
       }
@@ -4209,47 +3263,28 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
       {
         KScope ks(ctx, "pcg_update");
         double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
-        pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, st>>>(g0, bc, prob->tol, L0.k, L0.z2, p_old, p_new,
-                                                                    w.u, w.r_cur, r_next, w.scal, w.flags, part,
-                                                                    w.max_parts, w.counter, w.n_active, w.hist,
-                                                                    w.hist_cap);
+        pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, st>>>(
+            g0, bc, prob->tol, L0.k, L0.z2, p_old, p_new, w.u, w.r_cur, r_next, w.scal, w.flags, part,
+            w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
         w.r_cur = r_next;
       }
       OSC_CUDA(cudaMemcpyAsync(ring + (it & 3), w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
       OSC_CUDA(cudaEventRecord(ctx->ev_poll[it & 3], st));
-      vcycle(ctx, bc, B, true);
+      vcycle(ctx, bc, B);
       std::swap(p_old, p_new);
     }
     return;
   }
-  if (w.nlev > 1) {  // first level-0 pre-smoother: pcg_update_down with α = 0 and p = u (finite)
-    KScope ks(ctx, "pcg_update_down.init");
-    double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
-    pcg_update_down_kernel<<<march_grid(L0.m, 2, B), MT, 0, st>>>(g0, bc, prob->tol, L0.k, w.u, w.u, w.r_cur,
-                                                            r_next, L0.z, w.scal, w.flags, part, w.max_parts,
-                                                            w.counter, w.n_active, w.hist, w.hist_cap, 1);
-    w.r_cur = r_next;
-  }
-  vcycle(ctx, bc, B, true);  // z = M r0, rz = <r0, z>
-  double* p_old = w.p0;
-  double* p_new = w.p1;
-  const int check_every = L0.N >= 65536 ? 1 : 4;
-  // optional host-side safety valve (debugging): OSC_HARD_ITER_CAP stops the loop early; the
-  // samples still active are reported as not converged by solver_results().
-  static const long hard_cap = [] {
-    const char* e = std::getenv("OSC_HARD_ITER_CAP");
-    return e ? std::atol(e) : -1L;
-  }();
+  // a single level (m ≤ 4): classical PCG with the exact coarsest inverse as preconditioner
+  vcycle(ctx, bc, B);  // z = M r0, rz = <r0, z>
   for (int it = 0;; ++it) {
     if (hard_cap >= 0 && it >= hard_cap) {
       mark_active_failed_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, w.flags);
       break;
     }
-    if (it % check_every == 0) {
-      OSC_CUDA(cudaMemcpyAsync(ctx->h_pinned_int, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
-      OSC_CUDA(cudaStreamSynchronize(st));
-      if (*ctx->h_pinned_int <= 0) break;
-    }
+    OSC_CUDA(cudaMemcpyAsync(ctx->h_pinned_int, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    OSC_CUDA(cudaStreamSynchronize(st));
+    if (*ctx->h_pinned_int <= 0) break;
     {
       KScope ks(ctx, "pcg_apply");
       pcg_apply_kernel<<<march_grid(L0.m, 1, B), MT, 0, st>>>(g0, bc, L0.k, L0.z2, p_old, p_new, w.scal, w.flags,
@@ -4263,7 +3298,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
                                                               w.counter, w.n_active, w.hist, w.hist_cap, 0);
     }
     w.r_cur = (w.r_cur == L0.r) ? w.r2 : L0.r;
-    vcycle(ctx, bc, B, true);  // level-0 pre-smoother ran inside pcg_update_down
+    vcycle(ctx, bc, B);
     std::swap(p_old, p_new);
   }
 }

@@ -156,9 +156,20 @@ __device__ S9 row_k(const double* __restrict__ kb, int n00, int st, int m, int b
   return r;
 }
 
+// Stored coarse rows: fp64 diagonal, fp32 couplings. Rounding a coupling a to fp32 moves it by at
+// most 2^-24·|a|; raising the diagonal by that bound summed over the row's eight couplings makes the
+// stored operator A' = A + E with E symmetric and diagonally dominant with a non-negative diagonal
+// (Gershgorin: E ⪰ 0), so A' stays SPD whenever A is, and the V-cycle stays a valid PCG
+// preconditioner. (1 + 2^-20) covers the few-ulp difference between a row's own value of a W/S
+// coupling and the neighbour's stored E/N of the same pair.
+__device__ __forceinline__ double fp32_rounding_margin(double sum_abs_couplings) {
+  return sum_abs_couplings * (0x1p-24 * (1.0 + 0x1p-20));
+}
+
 // A stored 9-point level (one sample's arrays start at off = b·N).
 struct L9 {
-  const double *C, *E, *N, *NE, *NW;
+  const double* C;
+  const float *E, *N, *NE, *NW;
   int m, n0;
   int64_t Nn;
 };
@@ -187,8 +198,8 @@ __device__ __forceinline__ S9 row_s(const L9& L, int64_t off, int x, int y) {
 // Level-0 rows from nodal k, stored once per setup (C, E, N; 5-point) so the transfer and Galerkin
 // kernels read every level the same way.
 __global__ void __launch_bounds__(NT) rows0_kernel(Geo g, int bc, const double* __restrict__ k,
-                                                   double* __restrict__ C, double* __restrict__ E,
-                                                   double* __restrict__ Nn) {
+                                                   double* __restrict__ C, float* __restrict__ E,
+                                                   float* __restrict__ Nn) {
   const int b = blockIdx.y;
   const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
   if (i >= g.N) return;
@@ -287,9 +298,9 @@ __device__ __forceinline__ void prow_f(RowF row, int bc, int m, int x, int y, bo
 // level's centre weights per cell (pw, m/2 × m/2 per sample) for the V-cycle transfers.
 __global__ void __launch_bounds__(NT) prow_kernel(L9 R, int bc, int opdep, double* __restrict__ P0,
                                                   double* __restrict__ P1, double* __restrict__ P2,
-                                                  double* __restrict__ P3, double* __restrict__ pw0,
-                                                  double* __restrict__ pw1, double* __restrict__ pw2,
-                                                  double* __restrict__ pw3) {
+                                                  double* __restrict__ P3, float* __restrict__ pw0,
+                                                  float* __restrict__ pw1, float* __restrict__ pw2,
+                                                  float* __restrict__ pw3) {
   const int b = blockIdx.y;
   const int m = R.m, n0 = m + 1, mc = m / 2;
   const int64_t N = (int64_t)n0 * n0;
@@ -343,11 +354,11 @@ constexpr size_t galerkin_tile_smem(bool l0) {
 // the coarse nodes of the tile: no bounds / Dirichlet tests (most tiles of a large level).
 template <bool L0K, bool INT>
 __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0, const L9& F, int bc, int opdep,
-                                                   const Geo& gc, double* __restrict__ Cc, double* __restrict__ Ec,
-                                                   double* __restrict__ Nc, double* __restrict__ NEc,
-                                                   double* __restrict__ NWc, double* __restrict__ pw0,
-                                                   double* __restrict__ pw1, double* __restrict__ pw2,
-                                                   double* __restrict__ pw3, double* gsm) {
+                                                   const Geo& gc, double* __restrict__ Cc, float* __restrict__ Ec,
+                                                   float* __restrict__ Nc, float* __restrict__ NEc,
+                                                   float* __restrict__ NWc, float* __restrict__ pw0,
+                                                   float* __restrict__ pw1, float* __restrict__ pw2,
+                                                   float* __restrict__ pw3, double* gsm) {
   const int b = blockIdx.z;
   const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y;
   const int m = F.m, n0 = F.n0, mc = gc.m, mcl = m / 2;
@@ -395,13 +406,14 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
     }
   } else {
     const int64_t off = (int64_t)b * F.Nn;
-    const double* src[5] = {F.C + off, F.E + off, F.N + off, F.NE + off, F.NW + off};
+    const float* src[4] = {F.E + off, F.N + off, F.NE + off, F.NW + off};
     for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
       const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
       const bool in = INT || ((unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0);
       const int64_t o = (int64_t)y * n0 + x;
+      A(0, lx, ly) = in ? __ldg(F.C + off + o) : 1.0;
 #pragma unroll
-      for (int q = 0; q < 5; ++q) A(q, lx, ly) = in ? __ldg(src[q] + o) : (q == 0 ? 1.0 : 0.0);
+      for (int q = 0; q < 4; ++q) A(q + 1, lx, ly) = in ? (double)__ldg(src[q] + o) : 0.0;
     }
   }
   __syncthreads();
@@ -512,21 +524,23 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
           }
         }
     }
-  Cc[o] = acc[1][1];
-  Ec[o] = acc[1][2];
-  Nc[o] = acc[2][1];
-  NEc[o] = acc[2][2];
-  NWc[o] = acc[2][0];
+  const double margin = fp32_rounding_margin(fabs(acc[0][0]) + fabs(acc[0][1]) + fabs(acc[0][2]) + fabs(acc[1][0]) +
+                                             fabs(acc[1][2]) + fabs(acc[2][0]) + fabs(acc[2][1]) + fabs(acc[2][2]));
+  Cc[o] = acc[1][1] + margin;
+  Ec[o] = (float)acc[1][2];
+  Nc[o] = (float)acc[2][1];
+  NEc[o] = (float)acc[2][2];
+  NWc[o] = (float)acc[2][0];
 }
 
 template <bool L0K>
 __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double* __restrict__ k0, L9 F, int bc,
                                                                    int opdep, Geo gc, double* __restrict__ Cc,
-                                                                   double* __restrict__ Ec, double* __restrict__ Nc,
-                                                                   double* __restrict__ NEc,
-                                                                   double* __restrict__ NWc, double* __restrict__ pw0,
-                                                                   double* __restrict__ pw1, double* __restrict__ pw2,
-                                                                   double* __restrict__ pw3) {
+                                                                   float* __restrict__ Ec, float* __restrict__ Nc,
+                                                                   float* __restrict__ NEc,
+                                                                   float* __restrict__ NWc, float* __restrict__ pw0,
+                                                                   float* __restrict__ pw1, float* __restrict__ pw2,
+                                                                   float* __restrict__ pw3) {
   extern __shared__ double gsm[];
   const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y, m = F.m;
   const bool interior = 2 * I0 - 5 >= 1 && 2 * I0 + 2 * GT_X + 3 <= m - 1 && 2 * J0 - 5 >= 1 &&
@@ -541,19 +555,19 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
 // stored in the 9-point format (zero diagonal couplings).
 __global__ void __launch_bounds__(NT) rediscretize_kernel(const double* __restrict__ k0, Geo g0, int stride,
                                                           int bc, Geo gc, double* __restrict__ Cc,
-                                                          double* __restrict__ Ec, double* __restrict__ Nc,
-                                                          double* __restrict__ NEc, double* __restrict__ NWc) {
+                                                          float* __restrict__ Ec, float* __restrict__ Nc,
+                                                          float* __restrict__ NEc, float* __restrict__ NWc) {
   const int b = blockIdx.y;
   const int64_t ic = blockIdx.x * (int64_t)NT + threadIdx.x;
   if (ic >= gc.N) return;
   const int J = (int)(ic / gc.n0), I = (int)(ic - (int64_t)J * gc.n0);
   const S9 r = row_k(k0 + (int64_t)b * g0.N, g0.n0, stride, gc.m, bc, I, J);
   const int64_t o = (int64_t)b * gc.N + ic;
-  Cc[o] = r.c;
-  Ec[o] = r.e;
-  Nc[o] = r.n;
-  NEc[o] = 0.0;
-  NWc[o] = 0.0;
+  Cc[o] = r.c + fp32_rounding_margin(fabs(r.e) + fabs(r.w) + fabs(r.n) + fabs(r.s));
+  Ec[o] = (float)r.e;
+  Nc[o] = (float)r.n;
+  NEc[o] = 0.0f;
+  NWc[o] = 0.0f;
 }
 
 // Coarsest operator (stored 9-point rows) and its explicit inverse, one warp per sample. The
@@ -1384,7 +1398,7 @@ __device__ __forceinline__ double red_resid(Pair E, Pair N, Pair Nm, Pair zm, Pa
 }
 
 struct PW4 {
-  const double *w0, *w1, *w2, *w3;  // centre weights to SW, SE, NW, NE per cell (m/2 × m/2 per sample)
+  const float *w0, *w1, *w2, *w3;  // centre weights to SW, SE, NW, NE per cell (m/2 × m/2 per sample)
 };
 
 // ---- coarse levels (9-point): row-marching kernels ----------------------------------------------------
@@ -1451,6 +1465,12 @@ __device__ __forceinline__ void cpa8(double* s, const double* g, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"((unsigned)ok << 3)
                : "memory");
 }
+// 4-byte variant for the fp32 couplings and transfer weights
+__device__ __forceinline__ void cpa4(float* s, const float* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"((unsigned)ok << 2)
+               : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() {
@@ -1463,18 +1483,20 @@ __device__ __forceinline__ void cpa_wait() {
 // one 16-byte shared load. A __syncwarp orders the cp.async data with the other lanes' reads.
 //   up:   C E N NE NW r [z]  (64 each), zc of coarse rows Jc, Jc+1 (33 each: coarse columns
 //         x0/2 … x0/2+32), pw of the odd rows' cells (4 × 32), 3 halo couplings
-template <bool RZ>
+// Ring row of the up sweep, in doubles: C and r (64 columns each, fp64), the fp32 couplings E N NE NW
+// (64 each), zc of coarse rows Jc, Jc+1 (33 each), then fp32: pw of the odd rows' cells (4 × 32) and
+// 3 halo couplings.
 struct UpLayout {
-  static constexpr int NA = RZ ? 6 : 7;  // staged fine arrays
-  static constexpr int ZC0 = NA * 64, ZC1 = ZC0 + 33, PW = ZC1 + 33, X = PW + 128;
-  static constexpr int WORDS = (X + 3 + 1) & ~1;  // doubles per warp-row (even: 16-byte alignment)
+  static constexpr int C = 0, R = 64, CPL = 128;     // CPL: float region, E N NE NW at CPL*2 + k*64
+  static constexpr int ZC0 = CPL + 128, ZC1 = ZC0 + 33, PW = ZC1 + 33, X = PW + 64;  // PW, X: floats
+  static constexpr int WORDS = (X + 2 + 1) & ~1;   // doubles per warp-row (even: 16-byte alignment)
 };
-enum { UP_C = 0, UP_E = 1, UP_N = 2, UP_NE = 3, UP_NW = 4, UP_R = 5, UP_Z = 6 };
-// rows staged per warp: 3 × 582 × 8 B = 14 KB per warp (RZ). A/B with one-warp CTAs: 4 or 5 rows are
-// slower (coarse up sweep 19.4 → 28 ms per config-4 step: fewer resident warps)
+enum { UP_E = 0, UP_N = 1, UP_NE = 2, UP_NW = 3 };
+// rows staged per warp: 3 rows. A/B with one-warp CTAs (fp64 couplings): 4 or 5 rows were slower
+// (coarse up sweep 19.4 → 28 ms per config-4 step: fewer resident warps)
 constexpr int UP_RING = 3;
 template <bool RZ>
-constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * CU_W * UpLayout<RZ>::WORDS; }
+constexpr size_t up_ring_smem() { return sizeof(double) * UP_RING * CU_W * UpLayout::WORDS; }
 
 // Prolongation + post-smoother, ring-staged (same algorithm as c_up_march_kernel; pending smoother
 // rows carry partial sums). RZ: the pre-smoothed z is recomputed from r and the operator (red z =
@@ -1486,14 +1508,16 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
                                                           const double* __restrict__ zc, double* __restrict__ z2,
                                                           const int* flags) {
   C9_PROLOGUE_W(CU_W)
-  using LY = UpLayout<RZ>;
+  static_assert(RZ, "the up sweep recomputes the pre-smoothed z");
+  using LY = UpLayout;
   extern __shared__ __align__(16) double ring[];
   const int warp = threadIdx.x >> 5;
   const double *rb = r + off, *zb = z + off, *zcb = zc + (int64_t)b * gc.N;
   const int x0 = xa - 2 * lane, I0 = x0 >> 1, nc0 = gc.n0;
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  const double* arr[7] = {L.C + off, L.E + off, L.N + off, L.NE + off, L.NW + off, rb, zb};
+  const float* cpl[4] = {L.E + off, L.N + off, L.NE + off, L.NW + off};
+  (void)zb;
   auto slot = [&](int y) {
     return ring + ((size_t)((unsigned)(y - (y0 - 4)) % UP_RING) * CU_W + warp) * LY::WORDS;
   };
@@ -1507,10 +1531,15 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
     const int c0 = x0 + lane, c1 = c0 + 32;
     const bool ok0 = yok && (unsigned)c0 < (unsigned)n0, ok1 = yok && (unsigned)c1 < (unsigned)n0;
     const int64_t i0 = (int64_t)y * n0 + c0;
+    cpa8(S + LY::C + lane, L.C + off + i0, ok0);
+    cpa8(S + LY::C + 32 + lane, L.C + off + i0 + 32, ok1);
+    cpa8(S + LY::R + lane, rb + i0, ok0);
+    cpa8(S + LY::R + 32 + lane, rb + i0 + 32, ok1);
+    float* SF = reinterpret_cast<float*>(S + LY::CPL);
 #pragma unroll
-    for (int k = 0; k < LY::NA; ++k) {
-      cpa8(S + k * 64 + lane, arr[k] + i0, ok0);
-      cpa8(S + k * 64 + 32 + lane, arr[k] + i0 + 32, ok1);
+    for (int k = 0; k < 4; ++k) {
+      cpa4(SF + k * 64 + lane, cpl[k] + i0, ok0);
+      cpa4(SF + k * 64 + 32 + lane, cpl[k] + i0 + 32, ok1);
     }
     // coarse values of the prolongation: row Jc (and Jc+1 on odd rows), columns I0 … I0+32
     const int Jc = y >> 1, ci = I0 + lane;
@@ -1524,27 +1553,34 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
       if (lane == 0) cpa8(S + LY::ZC1 + 32, zr0 + nc0 + 32, j1 && cok2);
       const bool ok = ci >= 0 && ci < mcl && Jc >= 0 && Jc < mcl;
       const int64_t cell = cb0 + (int64_t)Jc * mcl + ci;
-      cpa8(S + LY::PW + 0 * 32 + lane, pw.w0 + cell, ok);
-      cpa8(S + LY::PW + 1 * 32 + lane, pw.w1 + cell, ok);
-      cpa8(S + LY::PW + 2 * 32 + lane, pw.w2 + cell, ok);
-      cpa8(S + LY::PW + 3 * 32 + lane, pw.w3 + cell, ok);
+      float* SP = reinterpret_cast<float*>(S + LY::PW);
+      cpa4(SP + 0 * 32 + lane, pw.w0 + cell, ok);
+      cpa4(SP + 1 * 32 + lane, pw.w1 + cell, ok);
+      cpa4(SP + 2 * 32 + lane, pw.w2 + cell, ok);
+      cpa4(SP + 3 * 32 + lane, pw.w3 + cell, ok);
     }
     // halo couplings from beyond the warp: E(x0−1, y), NE(x0−1, y−1), NW(x0+64, y−1)
     if (lane == 0) {
       const bool xk = (unsigned)(x0 - 1) < (unsigned)n0;
-      cpa8(S + LY::X + 0, arr[UP_E] + (i0 - 1), yok && xk);
-      cpa8(S + LY::X + 1, arr[UP_NE] + (i0 - n0 - 1), (unsigned)(y - 1) < (unsigned)n0 && xk);
+      float* SX = reinterpret_cast<float*>(S + LY::X);
+      cpa4(SX + 0, cpl[UP_E] + (i0 - 1), yok && xk);
+      cpa4(SX + 1, cpl[UP_NE] + (i0 - n0 - 1), (unsigned)(y - 1) < (unsigned)n0 && xk);
     } else if (lane == 31) {
       const bool xk = (unsigned)(x0 + 64) < (unsigned)n0;
-      cpa8(S + LY::X + 2, arr[UP_NW] + (i0 - n0 + 33), (unsigned)(y - 1) < (unsigned)n0 && xk);
+      cpa4(reinterpret_cast<float*>(S + LY::X) + 2, cpl[UP_NW] + (i0 - n0 + 33),
+           (unsigned)(y - 1) < (unsigned)n0 && xk);
     }
   };
-  auto P2 = [&](const double* S, int k) {
-    const double2 v = *reinterpret_cast<const double2*>(S + k * 64 + 2 * lane);
+  auto P2 = [&](const double* S, int base) {  // fp64 pair of this lane's columns
+    const double2 v = *reinterpret_cast<const double2*>(S + base + 2 * lane);
     return Pair{v.x, v.y};
   };
+  auto F2 = [&](const double* S, int k) {  // fp32 coupling pair
+    const float2 v = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(S + LY::CPL) + k * 64 + 2 * lane);
+    return Pair{(double)v.x, (double)v.y};
+  };
   auto raw9 = [&](const double* S, int y) {
-    R9 q{P2(S, UP_C), P2(S, UP_E), P2(S, UP_N), P2(S, UP_NE), P2(S, UP_NW)};
+    R9 q{P2(S, LY::C), F2(S, UP_E), F2(S, UP_N), F2(S, UP_NE), F2(S, UP_NW)};
     const bool yok = (unsigned)y < (unsigned)n0;
     if (!(yok && (unsigned)xa < (unsigned)n0)) q.C.a = 1.0;
     if (!(yok && (unsigned)xb < (unsigned)n0)) q.C.b = 1.0;
@@ -1562,9 +1598,9 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
   Pair Nm, NEm, NWm;
   {
     const double* S = slot(y - 1);
-    Nm = P2(S, UP_N);
-    NEm = P2(S, UP_NE);
-    NWm = P2(S, UP_NW);
+    Nm = F2(S, UP_N);
+    NEm = F2(S, UP_NE);
+    NWm = F2(S, UP_NW);
   }
   __syncwarp();
   issue(y - 1 + UP_RING);
@@ -1575,7 +1611,7 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
     __syncwarp();
     const double* S = slot(y);
     const R9 q = raw9(S, y);
-    zr0 = P2(S, UP_R).b * rcp64(q.C.b);  // row y0−3 is odd: red at b
+    zr0 = P2(S, LY::R).b * rcp64(q.C.b);  // row y0−3 is odd: red at b
   }
   // Pending smoother rows carry partial sums instead of stencils: every neighbour term is folded in
   // as soon as its value exists, so only the couplings still to be applied stay live.
@@ -1599,14 +1635,14 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
     __syncwarp();
     const double* S = slot(y);
     const R9 qc = raw9(S, y);
-    const Pair rc0 = P2(S, UP_R);
+    const Pair rc0 = P2(S, LY::R);
     Pair zc0;
     if constexpr (RZ) {
       const double* S1 = slot(y + 1);
       // row y+1 has its red node in the other column
       const bool ok1 = (unsigned)(y + 1) < (unsigned)n0 && (unsigned)(ra0 ? xb : xa) < (unsigned)n0;
-      const double c1 = ok1 ? S1[UP_C * 64 + 2 * lane + (ra0 ? 1 : 0)] : 1.0;
-      const double zrp = S1[UP_R * 64 + 2 * lane + (ra0 ? 1 : 0)] * rcp64(c1);
+      const double c1 = ok1 ? S1[LY::C + 2 * lane + (ra0 ? 1 : 0)] : 1.0;
+      const double zrp = S1[LY::R + 2 * lane + (ra0 ? 1 : 0)] * rcp64(c1);
       const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
       if constexpr (ra0) {
         const double zbl = (rc0.b - (qc.E.b * zr0_e + qc.E.a * zr0 + qc.N.b * zrp + Nm.b * zrm)) * rcp64(qc.C.b);
@@ -1619,15 +1655,15 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
       zrm = zr0;
       zr0 = zrp;
     } else {
-      zc0 = P2(S, UP_Z);
+      zc0 = Pair{0.0, 0.0};
     }
     S9 A, Bc;
     st9_pair(qc, Nm, NEm, NWm, A, Bc);
     if (lane == 0) {
-      A.w = S[LY::X + 0];
-      A.sw = S[LY::X + 1];
+      A.w = reinterpret_cast<const float*>(S + LY::X)[0];
+      A.sw = reinterpret_cast<const float*>(S + LY::X)[1];
     } else if (lane == 31) {
-      Bc.se = S[LY::X + 2];
+      Bc.se = reinterpret_cast<const float*>(S + LY::X)[2];
     }
     Nm = qc.N; NEm = qc.NE; NWm = qc.NW;
     // v(y) = z + P zc
@@ -1644,8 +1680,9 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
                      c11 = S[LY::ZC1 + lane + 1];
         edge_w(A, false, opdep != 0, false, false, false, w0, w1);
         v0.a += w0 * c00 + w1 * c01;
-        v0.b += S[LY::PW + lane] * c00 + S[LY::PW + 32 + lane] * c10 + S[LY::PW + 64 + lane] * c01 +
-                S[LY::PW + 96 + lane] * c11;
+        const float* SP = reinterpret_cast<const float*>(S + LY::PW);
+        v0.b += (double)SP[lane] * c00 + (double)SP[32 + lane] * c10 + (double)SP[64 + lane] * c01 +
+                (double)SP[96 + lane] * c11;
       }
       const bool yin = (unsigned)y <= (unsigned)m;
       if (!yin || (unsigned)xa > (unsigned)m || is_dir(bc, m, xa, y)) v0.a = 0.0;
@@ -1707,8 +1744,10 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
 // the residual and rc = Pᵀ t follow c_restrict_march_kernel. Reads C, E, N, NE, NW, r, pw; writes
 // rc. Ring rows use the warp layout of the up kernel (C E N NE NW r, 64 columns each); the centre
 // weights of the odd rows are loaded into registers one row pair ahead.
-enum { DN_C = 0, DN_E = 1, DN_N = 2, DN_NE = 3, DN_NW = 4, DN_R = 5, DN_WORDS = 6 * 64 };
-constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 4 × 4 warps × 384 × 8 B = 48 KB
+// Ring row, in doubles: C, r (64 columns each, fp64), then the fp32 couplings E N NE NW (64 each).
+enum { DN_C = 0, DN_R = 64, DN_CPL = 128, DN_WORDS = 256 };
+enum { DN_E = 0, DN_N = 1, DN_NE = 2, DN_NW = 3 };  // fp32 arrays of the coupling region
+constexpr int DN_RING = 4;  // rows y … y+2 resident + one in flight; 4 × 4 warps × 256 × 8 B = 32 KB
 constexpr int CD_W = 4;  // warps per CTA of the coarse ring down sweep
 constexpr size_t DN_RING_SMEM = sizeof(double) * DN_RING * CD_W * DN_WORDS;
 
@@ -1728,7 +1767,8 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
   const int64_t off = (int64_t)b * L.Nn;
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  const double* arr[6] = {L.C + off, L.E + off, L.N + off, L.NE + off, L.NW + off, r + off};
+  const float* cpl[4] = {L.E + off, L.N + off, L.NE + off, L.NW + off};
+  const double *Cb = L.C + off, *rb = r + off;
   const int ys = 2 * J0 - 1;
   const int ylast = 2 * J1 + 1;  // residual rows end at 2J1 − 1; their z needs raw rows up to 2J1 + 1
   auto slot = [&](int y) {
@@ -1741,15 +1781,24 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
     const int c0 = x0 + lane, c1 = c0 + 32;
     const bool ok0 = yok && (unsigned)c0 < (unsigned)n0, ok1 = yok && (unsigned)c1 < (unsigned)n0;
     const int64_t i0 = (int64_t)y * n0 + c0;
+    cpa8(S + DN_C + lane, Cb + i0, ok0);
+    cpa8(S + DN_C + 32 + lane, Cb + i0 + 32, ok1);
+    cpa8(S + DN_R + lane, rb + i0, ok0);
+    cpa8(S + DN_R + 32 + lane, rb + i0 + 32, ok1);
+    float* SF = reinterpret_cast<float*>(S + DN_CPL);
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      cpa8(S + k * 64 + lane, arr[k] + i0, ok0);
-      cpa8(S + k * 64 + 32 + lane, arr[k] + i0 + 32, ok1);
+    for (int k = 0; k < 4; ++k) {
+      cpa4(SF + k * 64 + lane, cpl[k] + i0, ok0);
+      cpa4(SF + k * 64 + 32 + lane, cpl[k] + i0 + 32, ok1);
     }
   };
-  auto P2 = [&](const double* S, int k) {
-    const double2 v = *reinterpret_cast<const double2*>(S + k * 64 + 2 * lane);
+  auto P2 = [&](const double* S, int base) {  // fp64 pair of this lane's columns
+    const double2 v = *reinterpret_cast<const double2*>(S + base + 2 * lane);
     return Pair{v.x, v.y};
+  };
+  auto F2 = [&](const double* S, int k) {  // fp32 coupling pair
+    const float2 v = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(S + DN_CPL) + k * 64 + 2 * lane);
+    return Pair{(double)v.x, (double)v.y};
   };
   auto Cpair = [&](const double* S, int y) {  // off-grid rows are identity
     Pair c = P2(S, DN_C);
@@ -1768,7 +1817,7 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
   // Nm = N of row y − 1
   auto zpair = [&](int y, double zrm, double zr0, double zrp, Pair Nm) {
     const double* S = slot(y);
-    const Pair c = Cpair(S, y), E0 = P2(S, DN_E), N0 = P2(S, DN_N), r0 = P2(S, DN_R);
+    const Pair c = Cpair(S, y), E0 = F2(S, DN_E), N0 = F2(S, DN_N), r0 = P2(S, DN_R);
     const double zr0_e = shdn(zr0), zr0_w = shup(zr0), Ew = shup(E0.b);
     if (RED_IS_A(y)) {
       const double zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) * rcp64(c.b);
@@ -1796,14 +1845,14 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
   cpa_wait<1>();  // rows ys−2, ys−1, ys
   __syncwarp();
   const double zr_m2 = zred(ys - 2), zr_m1 = zred(ys - 1), zr_0 = zred(ys);
-  const Pair N_m2 = P2(slot(ys - 2), DN_N);
+  const Pair N_m2 = F2(slot(ys - 2), DN_N);
   Pair zm = zpair(ys - 1, zr_m2, zr_m1, zr_0, N_m2);
   Pair Nm, NEm, NWm;
   {
     const double* S = slot(ys - 1);
-    Nm = P2(S, DN_N);
-    NEm = P2(S, DN_NE);
-    NWm = P2(S, DN_NW);
+    Nm = F2(S, DN_N);
+    NEm = F2(S, DN_NE);
+    NWm = F2(S, DN_NW);
   }
   __syncwarp();
   issue(ys + 2);  // into the slot of row ys−2
@@ -1822,7 +1871,7 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
     __syncwarp();
     const double zrC = zred(y + 2);
     const double* S = slot(y);
-    const R9 q{Cpair(S, y), P2(S, DN_E), P2(S, DN_N), P2(S, DN_NE), P2(S, DN_NW)};
+    const R9 q{Cpair(S, y), F2(S, DN_E), F2(S, DN_N), F2(S, DN_NE), F2(S, DN_NW)};
     const Pair zp = zpair(y + 1, zrA, zrB, zrC, q.N);
     __syncwarp();
     issue(y + 4);
@@ -1873,9 +1922,12 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
 // variants stage each warp's rows (64 columns of k and r, plus the prolongation's z₁ and pw for
 // the up sweep) in a shared-memory ring with cp.async, in the warp layout of the coarse kernels,
 // and read k/r pairs back from it as often as needed: only the derived row state stays in
-// registers. Same arithmetic and operand order as restrict_r_body / smooth_up_r_body.
+// registers. The fp32 centre weights of the up sweep occupy 64 doubles (4 × 32 floats) at L0R_PW.
 enum { L0R_K = 0, L0R_R = 64, L0R_ZC0 = 128, L0R_ZC1 = 161, L0R_PW = 194 };
-constexpr int L0R_WORDS_UP = 322, L0R_WORDS_DN = 128;
+constexpr int L0R_WORDS_UP = 258, L0R_WORDS_DN = 128;
+__device__ __forceinline__ double l0r_pw(const double* S, int lane, int q) {
+  return (double)reinterpret_cast<const float*>(S + L0R_PW)[q * 32 + lane];
+}
 constexpr int L0R_RING = 5;
 // Warps (strips) per CTA of the ring sweeps (A/B knobs; the other march kernels use MW). One-warp
 // CTAs let the SM refill a warp slot as soon as that warp's strip is done, instead of holding it
@@ -2044,10 +2096,11 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
         if (lane == 0) cpa8(S + L0R_ZC1 + 32, zr0 + nc0 + 32, j1 && cok2);
         const bool ok = ci >= 0 && ci < mcl && Jc >= 0 && Jc < mcl;
         const int64_t cell = cb0 + (int64_t)Jc * mcl + ci;
-        cpa8(S + L0R_PW + 0 * 32 + lane, pw.w0 + cell, ok);
-        cpa8(S + L0R_PW + 1 * 32 + lane, pw.w1 + cell, ok);
-        cpa8(S + L0R_PW + 2 * 32 + lane, pw.w2 + cell, ok);
-        cpa8(S + L0R_PW + 3 * 32 + lane, pw.w3 + cell, ok);
+        float* SP = reinterpret_cast<float*>(S + L0R_PW);
+        cpa4(SP + 0 * 32 + lane, pw.w0 + cell, ok);
+        cpa4(SP + 1 * 32 + lane, pw.w1 + cell, ok);
+        cpa4(SP + 2 * 32 + lane, pw.w2 + cell, ok);
+        cpa4(SP + 3 * 32 + lane, pw.w3 + cell, ok);
       }
     }
     cpa_commit();
@@ -2063,8 +2116,8 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
     const Sten s = mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc);
     double p = 0.0;
     if (INT || (unsigned)xb < (unsigned)n0)
-      p = S[L0R_PW + lane] * S[L0R_ZC0 + lane] + S[L0R_PW + 32 + lane] * S[L0R_ZC0 + lane + 1] +
-          S[L0R_PW + 64 + lane] * S[L0R_ZC1 + lane] + S[L0R_PW + 96 + lane] * S[L0R_ZC1 + lane + 1];
+      p = l0r_pw(S, lane, 0) * S[L0R_ZC0 + lane] + l0r_pw(S, lane, 1) * S[L0R_ZC0 + lane + 1] +
+          l0r_pw(S, lane, 2) * S[L0R_ZC1 + lane] + l0r_pw(S, lane, 3) * S[L0R_ZC1 + lane + 1];
     return rr.b * rcp64(s.d) + p;
   };
   for (int j = 0; j < L0R_RING; ++j) issue(y0 - 3 + j);  // rows y0−3 … y0+1
@@ -2111,8 +2164,8 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
         const Sten sq = mk_sten<INT>(E2n.b, E2n.a, N2n.b, N1.b, xb, t + 2, m, bc);
         double pz = 0.0;
         if (INT || (unsigned)xb < (unsigned)n0)
-          pz = S2[L0R_PW + lane] * S2[L0R_ZC0 + lane] + S2[L0R_PW + 32 + lane] * S2[L0R_ZC0 + lane + 1] +
-               S2[L0R_PW + 64 + lane] * S2[L0R_ZC1 + lane] + S2[L0R_PW + 96 + lane] * S2[L0R_ZC1 + lane + 1];
+          pz = l0r_pw(S2, lane, 0) * S2[L0R_ZC0 + lane] + l0r_pw(S2, lane, 1) * S2[L0R_ZC0 + lane + 1] +
+               l0r_pw(S2, lane, 2) * S2[L0R_ZC1 + lane] + l0r_pw(S2, lane, 3) * S2[L0R_ZC1 + lane + 1];
         qc = rr.b * rcp64(sq.d) + pz;
       }
     }
@@ -2372,8 +2425,9 @@ __device__ __forceinline__ double2 smooth_up_r_body(Geo g, Geo gc, int bc, const
 
 // device view of the global hierarchy (one level's operator and centre weights)
 struct SolverLevelDev {
-  const double *C, *E, *N, *NE, *NW;
-  const double* pw[4];
+  const double* C;
+  const float *E, *N, *NE, *NW;
+  const float* pw[4];
 };
 struct HierDev {
   SolverLevelDev lev[12];
@@ -2949,13 +3003,14 @@ size_t solver_bytes(int m, int B, int hist_cap) {
   for (;;) {
     const size_t N = (size_t)(g + 1) * (g + 1), mcl = g / 2;
     const bool last = g <= 4 || g % 2 != 0;
-    // level 0: u r r2 z z2 p0 p1 (+k by caller); levels ≥ 1: C E N NE NW r z z2; centre weights
-    // (4 per cell) on every level with a coarser one
-    tot += N * B * sizeof(double) * (lev == 0 ? 8 : 9) + (last ? 0 : 4 * mcl * mcl * B * sizeof(double));
+    // level 0: u r r2 z z2 p0 p1 (+k by caller); levels ≥ 1: C (fp64), E N NE NW (fp32), r z z2;
+    // fp32 centre weights (4 per cell) on every level with a coarser one
+    tot += N * B * (lev == 0 ? 8 * sizeof(double) : 4 * sizeof(double) + 4 * sizeof(float)) +
+           (last ? 0 : 4 * mcl * mcl * B * sizeof(float)) + 5 * 256;
     ++lev;
     if (last) {
       tot += 2 * N * N * B * sizeof(double);
-      if (lev == 1) tot += 5 * N * B * sizeof(double);  // single level: its 9-point rows for the factor
+      if (lev == 1) tot += N * B * (sizeof(double) + 4 * sizeof(float)) + 5 * 256;  // single level: its rows
       break;
     }
     g /= 2;
@@ -2993,16 +3048,16 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   };
   for (int l = 0; l < nl; ++l) {
     SolverLevel& L = w.lev[l];
-    const size_t vb = sizeof(double) * L.N * B;
+    const size_t vb = sizeof(double) * L.N * B, fb = sizeof(float) * L.N * B;
     L.k = nullptr;  // level 0's k is the caller's buffer
     const bool rows = l > 0 || nl == 1;
     L.C = rows ? (double*)take(vb) : nullptr;
-    L.E = rows ? (double*)take(vb) : nullptr;
-    L.Nw = rows ? (double*)take(vb) : nullptr;
-    L.NE = rows ? (double*)take(vb) : nullptr;
-    L.NW = rows ? (double*)take(vb) : nullptr;
-    const size_t cb = sizeof(double) * (size_t)(L.m / 2) * (L.m / 2) * B;
-    for (int q = 0; q < 4; ++q) L.pw[q] = (l + 1 < nl) ? (double*)take(cb) : nullptr;
+    L.E = rows ? (float*)take(fb) : nullptr;
+    L.Nw = rows ? (float*)take(fb) : nullptr;
+    L.NE = rows ? (float*)take(fb) : nullptr;
+    L.NW = rows ? (float*)take(fb) : nullptr;
+    const size_t cb = sizeof(float) * (size_t)(L.m / 2) * (L.m / 2) * B;
+    for (int q = 0; q < 4; ++q) L.pw[q] = (l + 1 < nl) ? (float*)take(cb) : nullptr;
     L.r = (double*)take(vb);
     L.z = (double*)take(vb);
     L.z2 = (double*)take(vb);
@@ -3158,12 +3213,15 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
   } else {  // REDISCRETIZE: level-0 rows (5-point) into scratch (u, r, r2 are free until pcg_init)
     {
       KScope ks(ctx, "mg_setup.rows");
-      rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, L0.r, w.r2);
+      rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, reinterpret_cast<float*>(L0.r),
+                                                           reinterpret_cast<float*>(w.r2));
     }
     for (int l = 0; l + 1 < w.nlev; ++l) {
       const SolverLevel& F = w.lev[l];
       const SolverLevel& C = w.lev[l + 1];
-      const L9 R = l == 0 ? L9{w.u, L0.r, w.r2, nullptr, nullptr, F.m, F.m + 1, F.N} : l9_of(F);
+      const L9 R = l == 0 ? L9{w.u, reinterpret_cast<const float*>(L0.r), reinterpret_cast<const float*>(w.r2),
+                               nullptr, nullptr, F.m, F.m + 1, F.N}
+                          : l9_of(F);
       {  // P1 transfer weights of level l (centre weights pw; edges are ½)
         KScope ks(ctx, "mg_setup.prow");
         prow_kernel<<<dim3(nblocks(F.N), B), NT, 0, st>>>(R, bc, w.opdep, L0.z, L0.z2, w.p0, w.p1, F.pw[0],

@@ -84,10 +84,14 @@ struct SolverLevel {
   double* k = nullptr;  // level 0: nodal conductivity (5-point stencil rebuilt in-kernel)
   // levels ≥ 1: symmetric 9-point operator, Dirichlet-eliminated (identity rows): diagonal C and
   // the couplings to the E, N, NE, NW neighbours (W, S, SW, SE are the neighbours' E, N, NE, NW)
-  double *C = nullptr, *E = nullptr, *Nw = nullptr, *NE = nullptr, *NW = nullptr;
+  // Stored as fp64 diagonal + fp32 couplings: the preconditioner only steers the iteration (PCG
+  // still stops on the fp64 residual of the fp64 level-0 system), and the diagonal is raised by the
+  // couplings' fp32 rounding bound so the stored operator stays SPD (mgpcg.cu, store_row9).
+  double* C = nullptr;
+  float *E = nullptr, *Nw = nullptr, *NE = nullptr, *NW = nullptr;
   // prolongation weights of this level's cell-centre nodes (odd, odd) to the SW, SE, NW, NE coarse
   // corners, one value per cell (m/2 × m/2 per sample); edge-node weights are rebuilt from the stencil
-  double* pw[4] = {nullptr, nullptr, nullptr, nullptr};
+  float* pw[4] = {nullptr, nullptr, nullptr, nullptr};
   double *r = nullptr, *z = nullptr;   // MG residual / pre-smoothed correction
   double* z2 = nullptr;                // post-smoothed correction (no in-place halo race)
 };

@@ -575,9 +575,13 @@ __global__ void __launch_bounds__(NT) rediscretize_kernel(const double* __restri
 // per V-cycle (:274-286); here the SPD matrix is inverted once per solve by Gauss–Jordan (lane i
 // owns row i of [A | I]), so every coarsest solve is one warp matvec. n ≤ 32 uses this path.
 constexpr int CF_WARPS = 2;
-__device__ __forceinline__ void dense_row(const L9& L, int64_t off, int i, double* row, int n) {
+// Row i of the coarsest operator: the stored level, or — when the whole grid is the coarsest level
+// (k0 != null) — the exact fp64 P1 row rebuilt from k, so that single-level solves keep the exact
+// inverse as preconditioner (one PCG step, as the reference's Cholesky, fem.cpp:255-292).
+__device__ __forceinline__ void dense_row(const L9& L, int64_t off, int i, double* row, int n,
+                                          const double* k0, int bc) {
   const int n0 = L.n0, y = i / n0, x = i - y * n0;
-  const S9 r = row_s(L, off, x, y);
+  const S9 r = k0 ? row_k(k0 + off, n0, 1, L.m, bc, x, y) : row_s(L, off, x, y);
   row[i] = r.c;
   if (x + 1 < n0) row[i + 1] = r.e;
   if (x > 0) row[i - 1] = r.w;
@@ -594,7 +598,8 @@ __device__ __forceinline__ void dense_row(const L9& L, int64_t off, int i, doubl
   (void)n;
 }
 
-__global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(L9 L, int B, double* __restrict__ chol) {
+__global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(L9 L, int B, double* __restrict__ chol,
+                                                                           const double* __restrict__ k0, int bc) {
   __shared__ double aug[CF_WARPS][32][65];  // row i: A(i, 0..n−1) | I(i, 0..n−1), padded
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * CF_WARPS + w;
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(L9 L,
   double(*A)[65] = aug[w];
   if (lane < n) {
     for (int j = 0; j < 2 * n; ++j) A[lane][j] = (j == n + lane) ? 1.0 : 0.0;
-    dense_row(L, (int64_t)b * n, lane, A[lane], n);
+    dense_row(L, (int64_t)b * n, lane, A[lane], n, k0, bc);
   }
   __syncwarp();
   for (int c = 0; c < n; ++c) {
@@ -622,13 +627,13 @@ __global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(L9 L,
 }
 
 // Dense Cholesky + explicit inverse of the coarsest operator, one thread per sample (n > 32).
-__global__ void coarse_factor_kernel(L9 Lv, int B, double* __restrict__ chol) {
+__global__ void coarse_factor_kernel(L9 Lv, int B, double* __restrict__ chol, const double* __restrict__ k0, int bc) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int n = (int)Lv.Nn;
   double* L = chol + (int64_t)b * 2 * n * n;
   for (int i = 0; i < n * n; ++i) L[i] = 0.0;
-  for (int i = 0; i < n; ++i) dense_row(Lv, (int64_t)b * n, i, L + (int64_t)i * n, n);
+  for (int i = 0; i < n; ++i) dense_row(Lv, (int64_t)b * n, i, L + (int64_t)i * n, n, k0, bc);
   for (int j = 0; j < n; ++j) {
     double d = L[j * n + j];
     for (int q = 0; q < j; ++q) d -= L[j * n + q] * L[j * n + q];
@@ -3188,10 +3193,8 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
   const int bc = prob->bc, mode = prob->coarse_op;
   const SolverLevel& L0 = w.lev[0];
   const Geo g0 = geo_of(L0);
-  if (w.nlev == 1) {  // single level: level 0's own rows for the dense factor
-    KScope ks(ctx, "mg_setup.rows");
-    const SolverLevel& L = w.lev[0];
-    rediscretize_kernel<<<dim3(nblocks(L.N), B), NT, 0, st>>>(L0.k, g0, 1, bc, g0, L.C, L.E, L.Nw, L.NE, L.NW);
+  if (w.nlev == 1) {
+    // single level: the dense factor is built from k directly (exact fp64 rows)
   } else if (mode != OSC_COARSE_REDISCRETIZE) {
     // fused tiled Galerkin setup per level pair (galerkin_tile_kernel)
     smem_attr(galerkin_tile_kernel<true>, galerkin_tile_smem(true));
@@ -3233,11 +3236,12 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
     }
   }
   KScope ks(ctx, "mg_setup.factor");
+  const double* k_exact = w.nlev == 1 ? L0.k : nullptr;
   const SolverLevel& C = w.lev[w.nlev - 1];
   if (w.nc <= 32)
-    coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(l9_of(C), B, w.chol);
+    coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(l9_of(C), B, w.chol, k_exact, bc);
   else
-    coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(l9_of(C), B, w.chol);
+    coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(l9_of(C), B, w.chol, k_exact, bc);
   OSC_CUDA(cudaGetLastError());
 }
 

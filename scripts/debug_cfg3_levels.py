@@ -17,7 +17,8 @@ prob = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Flux), bc=api.BC.FlowCell)
 opt = api.EstimatorOptions(seed=1)
 ps = api._problem_struct(prob, opt.solver)
 port = O.Port()
-for ell, B in [(0, 4096), (1, 4096), (2, 2048), (3, 1024), (4, 256)]:
+base = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+for ell, B in [(0, 16384), (1, 8192), (2, 4096), (3, 2048), (4, 256)]:
     m = 16 << ell
     op = api.build_operator(api.GridSpec.square(m), model)
     k = op.s // 2 if ell <= 2 else 0
@@ -26,14 +27,16 @@ for ell, B in [(0, 4096), (1, 4096), (2, 2048), (3, 1024), (4, 256)]:
     flags = (L.DRAW_HAS_COARSE if ell > 0 else 0) | (L.DRAW_TRUNC_FINE | L.DRAW_TRUNC_COARSE if k else 0)
     qf, qc = np.empty(B), np.empty(B)
     itf, itc, st = (np.zeros(B, dtype=np.int32) for _ in range(3))
-    rc = L.lib().osc_level_draws(lev.h, C.byref(ps), 1, ell, 0, B, flags, None, qf.ctypes.data, qc.ctypes.data,
+    frm = base * B
+    rc = L.lib().osc_level_draws(lev.h, C.byref(ps), 1, ell, frm, frm + B, flags, None, qf.ctypes.data, qc.ctypes.data,
                                  itf.ctypes.data, itc.ctypes.data, st.ctypes.data, None)
     bad = np.nonzero(st)[0]
     print(f"ell={ell} m={m} rc={rc} failures={bad.size} iters fine mean {itf.mean():.2f} max {itf.max()} "
           f"coarse mean {itc.mean():.2f} max {itc.max()}", flush=True)
     if bad.size:
-        i = int(bad[0])
-        print("  first failing slot", i, "status", st[i], "itf", itf[i], "itc", itc[i], "qf", qf[i], "qc", qc[i])
+        i = frm + int(bad[0])
+        j = int(bad[0])
+        print("  first failing index", i, "status", st[j], "itf", itf[j], "itc", itc[j], "qf", qf[j], "qc", qc[j])
         sl = np.sqrt(np.maximum(op.eigenvalues, 0))
         trunc = np.sqrt(np.maximum(op.truncated(k).eigenvalues, 0)) if k else None
         pf, pc, pitf, pitc = port.coupled(m, op.n, trunc if k else sl, trunc, ell > 0, 1, ell, i, i + 1, bc=0, qoi=3)

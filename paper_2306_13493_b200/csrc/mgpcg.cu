@@ -1832,15 +1832,17 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
     return Pair{zbl, zr0};
   };
   // centre weights of cell (I, Jc) (odd row 2Jc+1); 0 off the cells
-  auto W4 = [&](int Jc, double w[4]) {
+  // fp32 weights stay fp32 in registers until their use (a conversion right after the load would
+  // wait on it there and expose the load latency the row-pair prefetch is meant to hide)
+  auto W4 = [&](int Jc, float w[4]) {
     const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
     const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
-    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
-    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
-    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0f;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0f;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0f;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0f;
   };
-  double wn[4];
+  float wn[4];
   W4(J0 - 1, wn);
   // prologue: rows ys−2 … ys+1 staged; z of rows ys−1, ys
   for (int j = 0; j < DN_RING; ++j) {
@@ -2022,15 +2024,17 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   ingest(ys + 1);
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  auto W4 = [&](int Jc, double w[4]) {
+  // fp32 weights stay fp32 in registers until their use (a conversion right after the load would
+  // wait on it there and expose the load latency the row-pair prefetch is meant to hide)
+  auto W4 = [&](int Jc, float w[4]) {
     const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
     const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
-    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
-    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
-    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0f;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0f;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0f;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0f;
   };
-  double wc[4], wn[4];
+  float wc[4], wn[4];
   W4(J0 - 1, wc);
   W4(J0, wn);
   const double t_first = ingest(ys + 2);  // (xb, 2J0−1)
@@ -2291,15 +2295,17 @@ __device__ __forceinline__ void restrict_r_body(Geo g, Geo gc, int bc, const dou
   ingest(ys + 1);
   const int mcl = m / 2;
   const int64_t cb0 = (int64_t)b * mcl * mcl;
-  auto W4 = [&](int Jc, double w[4]) {
+  // fp32 weights stay fp32 in registers until their use (a conversion right after the load would
+  // wait on it there and expose the load latency the row-pair prefetch is meant to hide)
+  auto W4 = [&](int Jc, float w[4]) {
     const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
     const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0;
-    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0;
-    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0;
-    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0;
+    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0f;
+    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0f;
+    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0f;
+    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0f;
   };
-  double wc[4];
+  float wc[4];
   W4(J0 - 1, wc);
   const double t_first = ingest(ys + 2);  // (xb, 2J0−1)
   double a_nw = t_first * wc[2], a_ne = t_first * wc[3];
@@ -2850,6 +2856,26 @@ __global__ void mark_active_failed_kernel(int B, int* flags) {
   }
 }
 
+// End of one body run of the device-side PCG loop (two iterations): keep looping while a sample of
+// the batch is active; the optional hard cap (tests) stops the loop and fails the active samples.
+__global__ void pcg_loop_cond_kernel(cudaGraphConditionalHandle h, const int* __restrict__ n_active,
+                                     int* __restrict__ loop_runs, long hard_cap, int B, int* flags) {
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    const int runs = ++loop_runs[0];
+    go = n_active[0] > 0 ? 1 : 0;
+    if (go && hard_cap >= 0 && 2L * runs >= hard_cap) go = -1;
+  }
+  __syncthreads();
+  if (go < 0)
+    for (int b = threadIdx.x; b < B; b += blockDim.x)
+      if (flags[b * F_NFLAGS + F_ACTIVE]) {
+        flags[b * F_NFLAGS + F_ACTIVE] = 0;
+        flags[b * F_NFLAGS + F_STATUS] = OSC_ERR_SOLVER;
+      }
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, go > 0 ? 1u : 0u);
+}
+
 // single-level case (no coarser grid): <r,z> → β
 __global__ void __launch_bounds__(NT) dot_rz_kernel(Geo g, const double* __restrict__ r,
                                                     const double* __restrict__ z, double* scal,
@@ -3247,6 +3273,110 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
 
 }  // namespace
 
+namespace {
+// ---- device-side PCG loop --------------------------------------------------------------------------
+// Small and mid-size grids are launch/poll bound on the host loop (config 1, 64²: ~10 kernels of a
+// few µs per iteration and a host poll every iteration). There the iterations run inside one CUDA
+// graph: a conditional WHILE node whose body is two one-reduction PCG iterations (the r / p ping-pong
+// returns to its start after two) followed by pcg_loop_cond_kernel, which keeps the loop going while
+// any sample of the batch is active. Samples converge individually as before (every kernel skips
+// inactive samples), so results and iteration counts are those of the host loop. Graphs are cached
+// per solve shape and rebuilt when a baked-in value (shape, tolerance, buffers) changes.
+constexpr int kGraphMaxM = 512;
+
+void pcg_iteration(Ctx* ctx, const osc_problem* prob, int B, double* r_in, double* r_out, double* p_old,
+                   double* p_new) {
+  SolverWork& w = ctx->solver;
+  SolverLevel& L0 = w.lev[0];
+  double2* part = reinterpret_cast<double2*>(w.partial);
+  {
+    KScope ks(ctx, "pcg_update");
+    pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, ctx->stream>>>(
+        geo_of(L0), prob->bc, prob->tol, L0.k, L0.z2, p_old, p_new, w.u, r_in, r_out, w.scal, w.flags, part,
+        w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+  }
+  w.r_cur = r_out;
+  vcycle(ctx, prob->bc, B);
+}
+
+void run_pcg_graph(Ctx* ctx, const osc_problem* prob, int B, long hard_cap) {
+  SolverWork& w = ctx->solver;
+  SolverLevel& L0 = w.lev[0];
+  cudaStream_t st = ctx->stream;
+  SolverWork::LoopGraph* G = nullptr;
+  for (auto& g : w.graphs)
+    if (g.m == w.m && g.B == B && g.bc == prob->bc && g.opdep == w.opdep && g.hist_cap == w.hist_cap &&
+        g.hard_cap == hard_cap && g.tol == prob->tol && g.k == L0.k && g.mem == w.mem.p &&
+        g.mem_bytes == w.mem.bytes)
+      G = &g;
+  if (!G) {
+    if (w.graphs.size() >= 8) {  // evict the least recently used
+      auto lru = std::min_element(w.graphs.begin(), w.graphs.end(),
+                                  [](const auto& a, const auto& b) { return a.last_use < b.last_use; });
+      cudaGraphExecDestroy(lru->exec);
+      w.graphs.erase(lru);
+    }
+    SolverWork::LoopGraph g;
+    g.m = w.m;
+    g.B = B;
+    g.bc = prob->bc;
+    g.opdep = w.opdep;
+    g.hist_cap = w.hist_cap;
+    g.hard_cap = hard_cap;
+    g.tol = prob->tol;
+    g.k = L0.k;
+    g.mem = w.mem.p;
+    g.mem_bytes = w.mem.bytes;
+    cudaGraph_t graph = nullptr;
+    OSC_CUDA(cudaGraphCreate(&graph, 0));
+    try {
+      cudaGraphConditionalHandle h;
+      OSC_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams np = {};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      OSC_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+      cudaGraph_t body = np.conditional.phGraph_out[0];
+      // the kernels launch during capture only as graph nodes: count them once per body run
+      const int64_t launches0 = ctx->launches;
+      OSC_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      try {
+        pcg_iteration(ctx, prob, B, L0.r, w.r2, w.p0, w.p1);
+        pcg_iteration(ctx, prob, B, w.r2, L0.r, w.p1, w.p0);
+        pcg_loop_cond_kernel<<<1, 256, 0, st>>>(h, w.n_active, w.n_active + 2, hard_cap, B, w.flags);
+      } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(st, &dummy);
+        throw;
+      }
+      OSC_CUDA(cudaStreamEndCapture(st, &body));
+      g.body_launches = (int)(ctx->launches - launches0) + 1;
+      ctx->launches = launches0;
+      OSC_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    } catch (...) {
+      cudaGraphDestroy(graph);
+      throw;
+    }
+    cudaGraphDestroy(graph);
+    w.graphs.push_back(g);
+    G = &w.graphs.back();
+  }
+  G->last_use = ++w.graph_clock;
+  w.r_cur = L0.r;  // the body's start state (r in L0.r, previous p in p0)
+  OSC_CUDA(cudaMemsetAsync(w.n_active + 2, 0, sizeof(int), st));
+  {
+    KScope ks(ctx, "pcg_loop_graph", 0);
+    OSC_CUDA(cudaGraphLaunch(G->exec, st));
+  }
+  // body runs of this solve → launch count, read with the results (solver_results synchronises)
+  OSC_CUDA(cudaMemcpyAsync(ctx->h_pinned_int + 2, w.n_active + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+  w.pending_body_launches = G->body_launches;
+}
+}  // namespace
+
 // Solve the batch whose level-0 conductivity sits in ctx->solver.lev[0].k (set by caller).
 void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess) {
   SolverWork& w = ctx->solver;
@@ -3306,6 +3436,11 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
     // One-reduction (Chronopoulos–Gear) PCG: pcg_update forms p, u, r and ‖r‖; the V-cycle's up sweep
     // returns γ = ⟨r, z⟩ and δ = ⟨z, Az⟩, hence β and α of the next update.
     vcycle(ctx, bc, B);  // z = M r0; γ0, δ0 → α0
+    if (!ctx->profiling && w.m <= kGraphMaxM) {
+      // device-side loop: no host polling, no per-kernel launch overhead (launch-bound small grids)
+      run_pcg_graph(ctx, prob, B, hard_cap);
+      return;
+    }
     // Lagged convergence polling: the active count after iteration i is copied to a pinned ring
     // slot behind an event, and the host reads it before launching iteration i + LAG. The device
     // queue never drains while the host polls; iterations launched after the last sample
@@ -3392,6 +3527,10 @@ void solver_results(Ctx* ctx, int B, int32_t* iters, int32_t* status, double* hi
     OSC_CUDA(cudaMemcpyAsync(hist_host, w.hist, sizeof(double) * (size_t)B * w.hist_cap,
                              cudaMemcpyDeviceToHost, ctx->stream));
   OSC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (w.pending_body_launches) {  // the device-side loop's kernels (body runs × kernels per run)
+    ctx->launches += (int64_t)w.pending_body_launches * ctx->h_pinned_int[2];
+    w.pending_body_launches = 0;
+  }
   for (int b = 0; b < B; ++b) {
     if (iters) iters[b] = fl[(size_t)b * F_NFLAGS + F_ITERS];
     if (status) status[b] = fl[(size_t)b * F_NFLAGS + F_STATUS];

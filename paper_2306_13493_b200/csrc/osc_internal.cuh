@@ -116,6 +116,25 @@ struct SolverWork {
   int max_parts = 0;
   int opdep = 1;  // operator-dependent transfers (OSC_COARSE_GALERKIN) vs P1 linear
   DevBuf mem;
+  // Device-side PCG loops (CUDA graphs with a conditional WHILE node), one per solve shape; the key
+  // covers every value the captured kernels bake in (shape, tolerance, buffers).
+  struct LoopGraph {
+    int m = 0, B = 0, bc = 0, opdep = 0, hist_cap = 0;
+    long hard_cap = -1;
+    double tol = 0.0;
+    const void *k = nullptr, *mem = nullptr;
+    size_t mem_bytes = 0;
+    cudaGraphExec_t exec = nullptr;
+    int body_launches = 0;  // kernels per body run (two PCG iterations)
+    uint64_t last_use = 0;
+  };
+  std::vector<LoopGraph> graphs;
+  uint64_t graph_clock = 0;
+  int pending_body_launches = 0;  // launches of the last graph solve, counted once its runs are known
+  ~SolverWork() {
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+  }
 };
 
 struct Ctx {

@@ -526,3 +526,30 @@ def test_dist_shard_nccl_single_rank(P, ctx):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m", [64, 256])
+def test_device_loop_matches_host_loop(P, ctx, m):
+    """Grids up to 512² iterate inside a CUDA graph (conditional WHILE node, no host polling); with
+    per-kernel profiling on, the same solves run the host-polled loop. Both give bit-identical QoIs
+    and iteration counts, and the graph path reports its kernels in the launch count."""
+    api = P.api
+    prob = api.ProblemSpec(api.CovarianceModel.matern(1.0, 0.05, 0.5), bc=api.BC.DirichletAll)
+    opt = api.EstimatorOptions(seed=8)
+    plan = api.make_level_plan(1, 2.0 / m, prob, opt)
+    cg = api.GridSpec.square(m // 2)
+    a, b = api.LevelDraws(), api.LevelDraws()
+    n0 = ctx.launch_count
+    api.run_level_draws(plan, cg, False, False, prob, opt, 0, 9, a, ctx=ctx)
+    n1 = ctx.launch_count
+    ctx.set_profiling(True)
+    try:
+        api.run_level_draws(plan, cg, False, False, prob, opt, 0, 9, b, ctx=ctx)
+        stats = ctx.kernel_stats()
+    finally:
+        ctx.set_profiling(False)
+    n2 = ctx.launch_count
+    assert np.array_equal(a.q_fine, b.q_fine) and np.array_equal(a.q_coarse, b.q_coarse)
+    assert np.array_equal(a.iters_fine, b.iters_fine) and np.array_equal(a.iters_coarse, b.iters_coarse)
+    assert any(k.startswith("pcg_update@") for k in stats)  # the profiled call took the host loop
+    assert n1 - n0 >= 0.8 * (n2 - n1)  # graph kernels counted (the body may run one extra empty iteration)

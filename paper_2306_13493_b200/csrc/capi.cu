@@ -586,6 +586,35 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
       solver_run(c, prob, B, guess);
       qoi_launch(c, prob, B, d_qf);
       solver_results(c, B, it_tmp.data(), st_tmp.data(), hist_fine);
+      if (guess) {
+        // A nested start that fails to converge (rare: ~1 in 2·10⁴ config-3 samples, where the
+        // one-reduction recurrence loses conjugacy) is re-solved from the reference's Dirichlet lift
+        // (fem.cpp:335-339): the failing samples' fields are compacted into a small batch.
+        std::vector<int> redo;
+        for (int b = 0; b < B; ++b)
+          if (st_tmp[b] == OSC_ERR_SOLVER) redo.push_back(b);
+        if (!redo.empty()) {
+          const int nr = (int)redo.size();
+          c->retry_k.ensure(sizeof(double) * Nf * nr);
+          c->retry_q.ensure(sizeof(double) * nr);
+          double* rk = c->retry_k.as<double>();
+          for (int j = 0; j < nr; ++j)
+            OSC_CUDA(cudaMemcpyAsync(rk + (int64_t)j * Nf, kf + (int64_t)redo[j] * Nf, sizeof(double) * Nf,
+                                     cudaMemcpyDeviceToDevice, c->stream));
+          solver_prepare(c, m, nr, hist_cap);
+          c->solver.lev[0].k = rk;
+          solver_run(c, prob, nr, nullptr);
+          qoi_launch(c, prob, nr, c->retry_q.as<double>());
+          std::vector<int32_t> itr(nr), str(nr);
+          solver_results(c, nr, itr.data(), str.data(), nullptr);
+          for (int j = 0; j < nr; ++j) {
+            OSC_CUDA(cudaMemcpyAsync(d_qf + redo[j], c->retry_q.as<double>() + j, sizeof(double),
+                                     cudaMemcpyDeviceToDevice, c->stream));
+            it_tmp[redo[j]] = itr[j];
+            st_tmp[redo[j]] = str[j];
+          }
+        }
+      }
       d2h(c, bad_tmp.data(), d_bad, sizeof(int) * B);
       OSC_CUDA(cudaStreamSynchronize(c->stream));
       for (int b = 0; b < B; ++b) {

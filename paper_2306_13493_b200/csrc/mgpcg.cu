@@ -2229,9 +2229,14 @@ __global__ void __launch_bounds__(32 * SUR_W, 3 * 4 / SUR_W) smooth_up_ring_kern
   if (reduce2_last(gd.x, gd.y, partial, maxp, counter, b, gamma, dcorr) && threadIdx.x == 0) {
     const double delta = gamma + dcorr;
     const bool first = flags[b * F_NFLAGS + F_ITERS] == 0;
-    const double beta = first ? 0.0 : gamma / scal[b * S_NSCAL + S_RZ];
+    double beta = first ? 0.0 : gamma / scal[b * S_NSCAL + S_RZ];
     double den = first ? delta : delta - beta * gamma / scal[b * S_NSCAL + S_ALPHA];
-    if (!(den > 0.0)) den = delta;
+    // ⟨p, Ap⟩ = δ − βγ/α_old lies in (0, δ] in exact arithmetic; outside it the recurrence has lost
+    // the conjugacy it relies on: restart the direction (p = z, β = 0, α = γ/δ)
+    if (!(den > 0.0 && den <= delta * (1.0 + 1e-8))) {
+      den = delta;
+      beta = 0.0;
+    }
     scal[b * S_NSCAL + S_BETA] = beta;
     scal[b * S_NSCAL + S_ALPHA] = gamma / den;
     scal[b * S_NSCAL + S_RZ] = gamma;

@@ -150,6 +150,7 @@ struct Ctx {
   std::vector<KernelStat> stats;
   // reusable workspaces
   DevBuf ce_inter, xi_dev, fields_fine, fields_coarse, out_q, out_i, tmp_host_stage, sums;
+  DevBuf retry_k, retry_q;  // nested-start failures re-solved from the lift (osc_level_draws)
   SolverWork solver;
   int* h_pinned_int = nullptr;  // small pinned staging for n_active (16 ints; [4..7]: polling ring)
   cudaEvent_t ev_poll[4] = {nullptr, nullptr, nullptr, nullptr};  // lagged convergence polling

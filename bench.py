@@ -432,11 +432,11 @@ def main():
         return bool(g_) and kernel_nodes(b_, int(g_)) is not None
     ranked = sorted(kstats_w.items(), key=lambda kv: -kv[1][1])
     dom_name = next((n for n, _ in ranked if _modelled(n)), ranked[0][0])
-    # Grids up to 512² iterate inside a CUDA graph (device-side loop), which carries no per-kernel
+    # Grids up to 128² iterate inside a CUDA graph (device-side loop), which carries no per-kernel
     # events: there the timed region runs unprofiled and the roofline kernel is timed by CUDA events
     # in an eager pass of the same K steps right after it. Larger grids (config 4) keep the events
     # of the dominant kernel inside the timed region (host-polled loop).
-    graph_loop = m <= 512
+    graph_loop = m <= 128
     if graph_loop:
         ctx.set_profiling(False)
     else:

@@ -3280,14 +3280,15 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
 
 namespace {
 // ---- device-side PCG loop --------------------------------------------------------------------------
-// Small and mid-size grids are launch/poll bound on the host loop (config 1, 64²: ~10 kernels of a
-// few µs per iteration and a host poll every iteration). There the iterations run inside one CUDA
-// graph: a conditional WHILE node whose body is two one-reduction PCG iterations (the r / p ping-pong
-// returns to its start after two) followed by pcg_loop_cond_kernel, which keeps the loop going while
-// any sample of the batch is active. Samples converge individually as before (every kernel skips
-// inactive samples), so results and iteration counts are those of the host loop. Graphs are cached
-// per solve shape and rebuilt when a baked-in value (shape, tolerance, buffers) changes.
-constexpr int kGraphMaxM = 512;
+// Small grids iterate inside one CUDA graph instead of the host-polled loop: a conditional WHILE node
+// whose body is two one-reduction PCG iterations (the r / p ping-pong returns to its start after
+// two) followed by pcg_loop_cond_kernel, which keeps the loop going while any sample of the batch is
+// active. Samples converge individually as before (every kernel skips inactive samples), so results
+// and iteration counts are those of the host loop. Graphs are cached per solve shape and rebuilt
+// when a baked-in value (shape, tolerance, buffers) changes. Measured, the host loop was not
+// launch-bound even at 64² (the lagged polling keeps the queue full): the device loop is neutral
+// (scripts/graph_ab.py), so it is kept to 128², where it removes the host round trips per iteration.
+constexpr int kGraphMaxM = 128;  // A/B (scripts/graph_ab.py): 64² 33.6 vs 33.8 ms, 128² 43.0 vs 43.5 ms per batch; neutral above
 
 void pcg_iteration(Ctx* ctx, const osc_problem* prob, int B, double* r_in, double* r_out, double* p_old,
                    double* p_new) {

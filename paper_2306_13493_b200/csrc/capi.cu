@@ -82,8 +82,7 @@ size_t budget_of(Ctx* c) {
   OSC_CUDA(cudaMemGetInfo(&fr, &tot));
   // what the context already holds is reusable
   size_t held = c->ce_inter.bytes + c->xi_dev.bytes + c->fields_fine.bytes + c->fields_coarse.bytes +
-                c->solver.mem.bytes + c->out_q.bytes + c->out_i.bytes + c->xi_pref.bytes + c->spec_fine.bytes +
-                c->spec_coarse.bytes + c->ce_inter_spec.bytes;
+                c->solver.mem.bytes + c->out_q.bytes + c->out_i.bytes + c->xi_pref.bytes;
   return (size_t)(0.6 * (double)(fr + held));
 }
 
@@ -182,8 +181,6 @@ int osc_ctx_create(int device, osc_ctx** out) {
         OSC_CUDA(cudaEventCreateWithFlags(&c->ev_ce_done[i], cudaEventDisableTiming));
       }
       OSC_CUDA(cudaEventCreateWithFlags(&c->ev_pref, cudaEventDisableTiming));
-      OSC_CUDA(cudaStreamCreateWithFlags(&c->ce_stream, cudaStreamNonBlocking));
-      OSC_CUDA(cudaEventCreateWithFlags(&c->ev_spec, cudaEventDisableTiming));
       OSC_CUDA(cudaEventCreateWithFlags(&c->ev_pref_read, cudaEventDisableTiming));
     } catch (...) {
       delete c;
@@ -199,7 +196,6 @@ void osc_ctx_destroy(osc_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->flush_stats();
   cudaStreamSynchronize(c->copy_stream);
-  if (c->ce_stream) cudaStreamSynchronize(c->ce_stream);
   for (DevBuf* b : {&c->ce_inter, &c->xi_dev, &c->fields_fine, &c->fields_coarse, &c->out_q,
                     &c->out_i, &c->tmp_host_stage, &c->sums, &c->solver.mem, &c->xi_pref})
     b->release();
@@ -214,8 +210,6 @@ void osc_ctx_destroy(osc_ctx* c) {
     if (c->ev_ce_done[i]) cudaEventDestroy(c->ev_ce_done[i]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-  if (c->ce_stream) cudaStreamDestroy(c->ce_stream);
-  if (c->ev_spec) cudaEventDestroy(c->ev_spec);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -380,8 +374,6 @@ void osc_level_destroy(osc_level* L) {
   if (!L) return;
   cudaSetDevice(L->ctx->device);
   cudaStreamSynchronize(L->ctx->stream);
-  cudaStreamSynchronize(L->ctx->ce_stream);  // a speculative CE may still read this level's √λ
-  if (L->ctx->spec.level == L) L->ctx->spec.valid = false;
   L->sqrt_full.release();
   L->sqrt_trunc.release();
   L->twiddle.release();
@@ -410,7 +402,7 @@ namespace osc {
 std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t seed, uint32_t ell, int64_t from,
                                  int64_t to, int flags, const double* xi, double* q_fine, double* q_coarse,
                                  int32_t* iters_fine, int32_t* iters_coarse, int32_t* status, double* level_sums,
-                                 int hist_cap, double* hist_fine, double* hist_coarse, bool allow_spec) {
+                                 int hist_cap, double* hist_fine, double* hist_coarse) {
   {
     OSC_REQUIRE(L && prob, "osc_level_draws: null argument");
     OSC_REQUIRE(to >= from && from >= 0, "osc_level_draws: need 0 <= from <= to");
@@ -488,24 +480,6 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
         sz = std::min(Bc, std::max(sz + 1, (int)std::ceil(sz * ramp)));
       }
     }
-    // speculative CE (device Philox, one chunk): consume the fields the previous call prepared for
-    // exactly this range, and prepare the next range's under this call's solves
-    const bool philox_whole = allow_spec && xi == nullptr && sched.size() == 1;
-    const int spec_flags = flags & (OSC_DRAW_HAS_COARSE | OSC_DRAW_TRUNC_FINE | OSC_DRAW_TRUNC_COARSE);
-    bool spec_hit = false;
-    if (allow_spec) {
-      const Ctx::Spec& sp = c->spec;
-      spec_hit = philox_whole && sp.valid && sp.level == L && sp.seed == seed && sp.ell == ell && sp.from == from &&
-                 sp.count == count && sp.flags == spec_flags;
-      c->spec.valid = false;  // consumed or stale
-      if (spec_hit) {
-        std::swap(c->fields_fine, c->spec_fine);
-        std::swap(c->fields_coarse, c->spec_coarse);
-      }
-    }
-    const int64_t next_from = from + (c->spec_stride > 0 ? c->spec_stride : count);
-    const size_t spec_bytes = sizeof(double) * (Nf + (has_coarse ? Nc : 0)) * count + ce_inter_bytes(L, 1, 1) * count;
-    const bool spec_next = philox_whole && next_from < (int64_t(1) << 62) && budget >= per * count + spec_bytes;
     c->fields_fine.ensure(sizeof(double) * Nf * Bc);
     if (has_coarse) c->fields_coarse.ensure(sizeof(double) * Nc * Bc);
     c->out_q.ensure(sizeof(double) * 2 * Bc);
@@ -575,42 +549,11 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
       double* kf = c->fields_fine.as<double>();
       double* kc = has_coarse ? c->fields_coarse.as<double>() : nullptr;
       const uint64_t idx0 = (uint64_t)(from + c0);
-      if (spec_hit) {  // fields computed under the previous call's solves
-        OSC_CUDA(cudaStreamWaitEvent(c->stream, c->ev_spec, 0));
-        OSC_CUDA(cudaMemcpyAsync(d_bad, c->spec_bad.p, sizeof(int) * B, cudaMemcpyDeviceToDevice, c->stream));
-      } else if (shared_field || !has_coarse) {
+      if (shared_field || !has_coarse) {
         ce_sample_launch(c, L, sq_f, xi_chunk, seed, ell, idx0, B, true, kf, kc, d_bad);
       } else {
         ce_sample_launch(c, L, sq_f, xi_chunk, seed, ell, idx0, B, true, kf, nullptr, d_bad);
         ce_sample_launch(c, L, sq_c, xi_chunk, seed, ell, idx0, B, true, nullptr, kc, d_bad);
-      }
-      if (spec_next) {
-        // the next range's fields on ce_stream (its own intermediate buffer): the CE is latency-bound
-        // and overlaps this batch's HBM-bound solves
-        c->spec_fine.ensure(sizeof(double) * Nf * B);
-        if (has_coarse) c->spec_coarse.ensure(sizeof(double) * Nc * B);
-        c->spec_bad.ensure(sizeof(int) * B);
-        std::swap(c->stream, c->ce_stream);
-        std::swap(c->ce_inter, c->ce_inter_spec);
-        struct Restore {
-          Ctx* c;
-          ~Restore() {
-            std::swap(c->stream, c->ce_stream);
-            std::swap(c->ce_inter, c->ce_inter_spec);
-          }
-        } restore{c};
-        double* sf = c->spec_fine.as<double>();
-        double* sc = has_coarse ? c->spec_coarse.as<double>() : nullptr;
-        int* sb = c->spec_bad.as<int>();
-        OSC_CUDA(cudaMemsetAsync(sb, 0, sizeof(int) * B, c->stream));
-        if (shared_field || !has_coarse) {
-          ce_sample_launch(c, L, sq_f, nullptr, seed, ell, (uint64_t)next_from, B, true, sf, sc, sb);
-        } else {
-          ce_sample_launch(c, L, sq_f, nullptr, seed, ell, (uint64_t)next_from, B, true, sf, nullptr, sb);
-          ce_sample_launch(c, L, sq_c, nullptr, seed, ell, (uint64_t)next_from, B, true, nullptr, sc, sb);
-        }
-        OSC_CUDA(cudaEventRecord(c->ev_spec, c->stream));
-        c->spec = Ctx::Spec{L, seed, ell, next_from, count, spec_flags, true};
       }
       if (whole) {  // xi_pref consumed: the next call's rows may overwrite it
         OSC_CUDA(cudaEventRecord(c->ev_pref_read, c->stream));
@@ -720,7 +663,7 @@ void draws_checked(Level* L, const osc_problem* prob, uint64_t seed, uint32_t el
     status = st_local.data();
   }
   const auto r = draws_impl(L, prob, seed, ell, from, to, flags, xi, q_fine, q_coarse, iters_fine, iters_coarse,
-                            status, level_sums, 0, nullptr, nullptr, true);
+                            status, level_sums, 0, nullptr, nullptr);
   if (r.first) throw osc::Error(OSC_ERR_NUMERICAL, "assemble_and_solve: non-finite log-field value");
   if (!r.second) return;
   c->fail_slot = -1;
@@ -739,7 +682,7 @@ void draws_checked(Level* L, const osc_problem* prob, uint64_t seed, uint32_t el
       const int64_t ncount = c->next_count, ns = c->next_s;
       c->next_xi = nullptr;
       draws_impl(L, prob, seed, ell, i, i + 1, flags, xi1, &qf1, &qc1, &itf1, &itc1, &st1, nullptr, cap, hf.data(),
-                 hc.data(), false);
+                 hc.data());
       if (host_pref) {
         c->next_xi = nx;
         c->next_count = ncount;

@@ -33,7 +33,7 @@ namespace osc {
 std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t seed, uint32_t ell, int64_t from,
                                  int64_t to, int flags, const double* xi, double* q_fine, double* q_coarse,
                                  int32_t* iters_fine, int32_t* iters_coarse, int32_t* status, double* level_sums,
-                                 int hist_cap, double* hist_fine, double* hist_coarse, bool allow_spec);
+                                 int hist_cap, double* hist_fine, double* hist_coarse);
 void draws_checked(Level* L, const osc_problem* prob, uint64_t seed, uint32_t ell, int64_t from, int64_t to,
                    int flags, const double* xi, double* q_fine, double* q_coarse, int32_t* iters_fine,
                    int32_t* iters_coarse, int32_t* status, double* level_sums);
@@ -252,7 +252,6 @@ int osc_group_level_draws(osc_group_level* gl, const osc_problem* prob, uint64_t
         ls[6] = level_sums[6];
       }
       const int64_t o = lo - from;
-      g->ctx[i]->spec_stride = to - from;  // this device's next shard starts one whole batch later
       try {
         draws_checked(gl->lev[i], prob, seed, ell, lo, std::max(lo, hi), flags, xi ? xi + o * s : nullptr,
                       q_fine ? q_fine + o : nullptr, q_coarse ? q_coarse + o : nullptr,

@@ -151,22 +151,6 @@ struct Ctx {
   // reusable workspaces
   DevBuf ce_inter, xi_dev, fields_fine, fields_coarse, out_q, out_i, tmp_host_stage, sums;
   DevBuf retry_k, retry_q;  // nested-start failures re-solved from the lift (osc_level_draws)
-  // Speculative fields of the next device-Philox batch (osc_level_draws): the CE of [to, to + count)
-  // runs on ce_stream under this batch's solves; the next call on the same level, seed, flags and
-  // count starting at `to` consumes it (else it is dropped). spec_stride overrides the next start
-  // offset (an osc_group device's next shard starts a whole batch later).
-  cudaStream_t ce_stream = nullptr;
-  cudaEvent_t ev_spec = nullptr;
-  DevBuf spec_fine, spec_coarse, spec_bad, ce_inter_spec;
-  struct Spec {
-    const void* level = nullptr;
-    uint64_t seed = 0;
-    uint32_t ell = 0;
-    int64_t from = -1, count = 0;
-    int flags = 0;
-    bool valid = false;
-  } spec;
-  int64_t spec_stride = 0;
   SolverWork solver;
   int* h_pinned_int = nullptr;  // small pinned staging for n_active (16 ints; [4..7]: polling ring)
   cudaEvent_t ev_poll[4] = {nullptr, nullptr, nullptr, nullptr};  // lagged convergence polling

@@ -89,22 +89,17 @@ def algorithmic_bytes_per_sample(W, n, it=None):
 # Per-kernel compulsory HBM bytes per node of the grid the kernel runs on: every
 # input read once and every output written once, for one active sample and one V-cycle / PCG
 # iteration (a sample runs one of each per iteration). Level 0 keeps nodal k (8 B/node, the
-# 5-point rows are rebuilt in registers); coarse levels store 9-point Galerkin rows C, E, N, NE, NW
-# (40 B/node); `pw` = the four centre prolongation weights per coarse cell (8 B per fine node);
-# a coarse-grid array costs ¼ of its fine-grid size.
+# 5-point rows are rebuilt in registers); coarse levels store the 9-point Galerkin rows as an fp64
+# diagonal and fp32 E, N, NE, NW couplings (24 B/node); `pw` = the four fp32 centre prolongation
+# weights per coarse cell (4 B per fine node); a coarse-grid array costs ¼ of its fine-grid size.
 KERNEL_BYTES = {
-    "pcg_apply": 4 * 8,                    # read k, z, p_old; write p_new
-    "pcg_update_down": 7 * 8,              # read k, p, r, u; write u, r, z
     "pcg_update": 8 * 8,                   # one-reduction PCG: read k, z, p_old, r, u; write p, u, r
-    "mg_restrict_r.L0": 8 + 8 + 8 + 2,     # read k, r, pw; write rc (pre-smoother recomputed)
-    "mg_smooth_up_r.L0": 8 + 8 + 2 + 8 + 8,  # read k, r, zc, pw; write z
-    "mg_restrict.L0": 8 + 8 + 8 + 2,       # read k, z, pw; write rc
-    "mg_smooth_up.L0": 8 + 8 + 8 + 2 + 8 + 8,  # read k, r, z, zc, pw; write z
-    "mg_pre": 24 + 8 + 8,                  # read C, E, N, r; write z
-    "mg_restrict": 40 + 8 + 8 + 2,         # read C, E, N, NE, NW, z, pw; write rc
-    "mg_smooth_up": 40 + 8 + 8 + 2 + 8 + 8,  # read C..NW, r, z, zc, pw; write z2
-    "mg_down": 40 + 8 + 8 + 2,             # fused pre + restrict: read C..NW, r, pw; write rc
-    "mg_up": 40 + 8 + 2 + 8 + 8,           # prolong + post (z recomputed): read C..NW, r, zc, pw; write z2
+    "pcg_apply": 4 * 8,                    # single-level PCG (m <= 4): read k, z, p_old; write p_new
+    "pcg_update_down": 7 * 8,              # single-level PCG: read k, p, r, u; write u, r, z
+    "mg_restrict_r.L0": 8 + 8 + 4 + 2,     # read k, r, pw (fp32); write rc (pre-smoother recomputed)
+    "mg_smooth_up_r.L0": 8 + 8 + 2 + 4 + 8,  # read k, r, zc, pw (fp32); write z
+    "mg_down": 8 + 16 + 8 + 4 + 2,         # fused pre + restrict: read C (fp64), E N NE NW (fp32), r, pw; write rc
+    "mg_up": 8 + 16 + 8 + 2 + 4 + 8,       # prolong + post (z recomputed): read C, E..NW, r, zc, pw; write z2
 }
 
 

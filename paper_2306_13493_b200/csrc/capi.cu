@@ -82,7 +82,7 @@ size_t budget_of(Ctx* c) {
   OSC_CUDA(cudaMemGetInfo(&fr, &tot));
   // what the context already holds is reusable
   size_t held = c->ce_inter.bytes + c->xi_dev.bytes + c->fields_fine.bytes + c->fields_coarse.bytes +
-                c->solver.mem.bytes + c->out_q.bytes + c->out_i.bytes + c->xi_pref.bytes;
+                c->solver.mem.bytes + c->out_q.bytes + c->out_i.bytes + c->xi_pref[0].bytes + c->xi_pref[1].bytes;
   return (size_t)(0.6 * (double)(fr + held));
 }
 
@@ -180,8 +180,11 @@ int osc_ctx_create(int device, osc_ctx** out) {
         OSC_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
         OSC_CUDA(cudaEventCreateWithFlags(&c->ev_ce_done[i], cudaEventDisableTiming));
       }
-      OSC_CUDA(cudaEventCreateWithFlags(&c->ev_pref, cudaEventDisableTiming));
-      OSC_CUDA(cudaEventCreateWithFlags(&c->ev_pref_read, cudaEventDisableTiming));
+      for (int t = 0; t < 2; ++t) {
+        OSC_CUDA(cudaEventCreateWithFlags(&c->ev_pref_read[t], cudaEventDisableTiming));
+        for (int j = 0; j < Ctx::kPrefParts; ++j)
+          OSC_CUDA(cudaEventCreateWithFlags(&c->ev_pref_part[t][j], cudaEventDisableTiming));
+      }
     } catch (...) {
       delete c;
       throw;
@@ -197,10 +200,14 @@ void osc_ctx_destroy(osc_ctx* c) {
   c->flush_stats();
   cudaStreamSynchronize(c->copy_stream);
   for (DevBuf* b : {&c->ce_inter, &c->xi_dev, &c->fields_fine, &c->fields_coarse, &c->out_q,
-                    &c->out_i, &c->tmp_host_stage, &c->sums, &c->solver.mem, &c->xi_pref})
+                    &c->out_i, &c->tmp_host_stage, &c->sums, &c->solver.mem, &c->xi_pref[0], &c->xi_pref[1],
+                    &c->retry_k, &c->retry_q})
     b->release();
-  if (c->ev_pref) cudaEventDestroy(c->ev_pref);
-  if (c->ev_pref_read) cudaEventDestroy(c->ev_pref_read);
+  for (int t = 0; t < 2; ++t) {
+    if (c->ev_pref_read[t]) cudaEventDestroy(c->ev_pref_read[t]);
+    for (int j = 0; j < Ctx::kPrefParts; ++j)
+      if (c->ev_pref_part[t][j]) cudaEventDestroy(c->ev_pref_part[t][j]);
+  }
   if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 4; ++i)
@@ -443,14 +450,28 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
     const bool arm = xi_host && c->next_xi != nullptr && c->next_count > 0 && c->next_s > 0;
     const bool pref_hit = xi_host && c->pref_xi == xi && c->pref_count == count && c->pref_s == L->s;
     if (xi_host && !pref_hit) c->pref_xi = nullptr;  // stale rows: dropped (the copy stream orders reuse)
-    if (arm || pref_hit) per += sizeof(double) * L->s;
+    if (arm || pref_hit) per += 2 * sizeof(double) * L->s;
     const size_t budget = budget_of(c);
     int64_t Bmax = std::max<int64_t>(1, (int64_t)(budget / per));
     Bmax = std::min<int64_t>(Bmax, 1 << 16);
-    // whole-batch mode: the rows are resident, so one chunk (full batch, no per-chunk overhead)
-    const bool whole = pref_hit && count <= Bmax;
-    if (pref_hit && !whole) c->pref_xi = nullptr;  // not consumed: never reused by a later call
-    const bool xi_chunked = xi_host && !whole;
+    constexpr int NP = Ctx::kPrefParts;
+    const int cur = c->pref_slot;  // the buffer holding this call's prefetched rows
+    // whole-batch mode: the rows have arrived, so one chunk (full batch, no per-chunk overhead);
+    // parts mode: they are still arriving (the copy engine is behind, e.g. right after a start-up
+    // call that copied its own rows and the next batch's), so the call runs part by part as they land
+    bool pref_ready = false;
+    int64_t max_part = 0;
+    if (pref_hit) {
+      const cudaError_t q = cudaEventQuery(c->ev_pref_part[cur][NP - 1]);
+      if (q != cudaSuccess && q != cudaErrorNotReady) OSC_CUDA(q);
+      pref_ready = q == cudaSuccess;
+      for (int j = 0; j < NP; ++j) max_part = std::max(max_part, c->pref_part_end[j] - (j ? c->pref_part_end[j - 1] : 0));
+    }
+    const bool whole = pref_hit && count <= Bmax && pref_ready;
+    const bool parts = pref_hit && !whole && max_part <= Bmax;
+    if (pref_hit && !whole && !parts) c->pref_xi = nullptr;  // not consumed: never reused by a later call
+    const bool from_pref = whole || parts;
+    const bool xi_chunked = xi_host && !from_pref;
     int64_t nchunks = (count + Bmax - 1) / Bmax;
     // host ξ: several chunks, so chunk i+1's H2D copy (copy stream, double-buffered) runs under
     // chunk i's solve and only the first chunk's copy is exposed (up to 4 chunks of ≥ 8 samples);
@@ -473,11 +494,18 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
       const bool big = sizeof(double) * (double)L->s * Bc >= min_mb * (1 << 20);
       if (xi_chunked && big && first_div > 0 && ramp > 1.0 && count >= 16)
         sz = (int)std::max<int64_t>(1, std::min<int64_t>(Bc, count / first_div));
-      for (int64_t a = 0; a < count;) {
-        const int nb = (int)std::min<int64_t>(sz, count - a);
-        sched.emplace_back(a, nb);
-        a += nb;
-        sz = std::min(Bc, std::max(sz + 1, (int)std::ceil(sz * ramp)));
+      if (parts) {
+        for (int j = 0; j < NP; ++j) {
+          const int64_t a = j ? c->pref_part_end[j - 1] : 0;
+          if (c->pref_part_end[j] > a) sched.emplace_back(a, (int)(c->pref_part_end[j] - a));
+        }
+      } else {
+        for (int64_t a = 0; a < count;) {
+          const int nb = (int)std::min<int64_t>(sz, count - a);
+          sched.emplace_back(a, nb);
+          a += nb;
+          sz = std::min(Bc, std::max(sz + 1, (int)std::ceil(sz * ramp)));
+        }
       }
     }
     c->fields_fine.ensure(sizeof(double) * Nf * Bc);
@@ -497,21 +525,30 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
                                cudaMemcpyHostToDevice, c->copy_stream));
       OSC_CUDA(cudaEventRecord(c->ev_copied[chunk & 1], c->copy_stream));
     };
-    // the armed next call's rows → xi_pref, queued on the copy stream behind this call's own
-    // copies and after this call's last read of xi_pref (ev_pref_read)
+    // the armed next call's rows → the other prefetch buffer, in NP parts, queued on the copy stream
+    // behind this call's own copies and after the last read of that buffer (ev_pref_read)
     auto issue_prefetch = [&] {
       if (!arm) return;
-      const size_t bytes = sizeof(double) * c->next_s * c->next_count;
-      if (c->xi_pref.bytes < bytes) {
+      const int nxt = 1 - cur;
+      const int64_t rows = c->next_count, sn = c->next_s;
+      const size_t bytes = sizeof(double) * sn * rows;
+      if (c->xi_pref[nxt].bytes < bytes) {
         OSC_CUDA(cudaStreamSynchronize(c->copy_stream));
-        c->xi_pref.ensure(bytes);
+        c->xi_pref[nxt].ensure(bytes);
       }
-      if (whole) OSC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_pref_read, 0));
-      OSC_CUDA(cudaMemcpyAsync(c->xi_pref.p, c->next_xi, bytes, cudaMemcpyHostToDevice, c->copy_stream));
-      OSC_CUDA(cudaEventRecord(c->ev_pref, c->copy_stream));
+      OSC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_pref_read[nxt], 0));
+      for (int j = 0; j < NP; ++j) {
+        const int64_t a = rows * j / NP, e = rows * (j + 1) / NP;
+        if (e > a)
+          OSC_CUDA(cudaMemcpyAsync(c->xi_pref[nxt].as<double>() + a * sn, c->next_xi + a * sn,
+                                   sizeof(double) * sn * (e - a), cudaMemcpyHostToDevice, c->copy_stream));
+        OSC_CUDA(cudaEventRecord(c->ev_pref_part[nxt][j], c->copy_stream));
+        c->pref_part_end[j] = e;
+      }
+      c->pref_slot = nxt;
       c->pref_xi = c->next_xi;
-      c->pref_count = c->next_count;
-      c->pref_s = c->next_s;
+      c->pref_count = rows;
+      c->pref_s = sn;
       c->next_xi = nullptr;
       c->next_count = 0;
       c->next_s = 0;
@@ -519,7 +556,10 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
     if (xi_chunked) {
       issue_copy(0);
       if (sched.size() == 1) issue_prefetch();
+    } else if (from_pref) {
+      issue_prefetch();  // nothing of this call's own is queued on the copy stream
     }
+    double* xi_cur = from_pref ? c->xi_pref[cur].as<double>() : nullptr;
     double* d_qf = c->out_q.as<double>();
     double* d_qc = d_qf + Bc;
     int* d_bad = c->out_i.as<int>();
@@ -535,9 +575,9 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
       const int B = sched[chunk].second;
       const double* xi_chunk = nullptr;
       if (xi) {
-        if (whole) {
-          OSC_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pref, 0));
-          xi_chunk = c->xi_pref.as<double>();
+        if (from_pref) {
+          OSC_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pref_part[cur][whole ? NP - 1 : chunk], 0));
+          xi_chunk = xi_cur + c0 * L->s;
         } else if (xi_host) {
           OSC_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[chunk & 1], 0));
           xi_chunk = xi_buf(chunk);
@@ -555,10 +595,11 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
         ce_sample_launch(c, L, sq_f, xi_chunk, seed, ell, idx0, B, true, kf, nullptr, d_bad);
         ce_sample_launch(c, L, sq_c, xi_chunk, seed, ell, idx0, B, true, nullptr, kc, d_bad);
       }
-      if (whole) {  // xi_pref consumed: the next call's rows may overwrite it
-        OSC_CUDA(cudaEventRecord(c->ev_pref_read, c->stream));
-        c->pref_xi = nullptr;
-        issue_prefetch();
+      if (from_pref) {
+        if (chunk + 1 == (int64_t)sched.size()) {  // the prefetch buffer consumed: a later prefetch may refill it
+          OSC_CUDA(cudaEventRecord(c->ev_pref_read[cur], c->stream));
+          if (c->pref_xi == xi) c->pref_xi = nullptr;
+        }
       } else if (xi_host) {  // ξ buffer consumed: start the next chunk's copy under this chunk's solves
         OSC_CUDA(cudaEventRecord(c->ev_ce_done[chunk & 1], c->stream));
         issue_copy(chunk + 1);

@@ -161,10 +161,17 @@ struct Ctx {
   // call are copied into xi_pref on the copy stream under this call's solves
   const double* next_xi = nullptr;
   int64_t next_count = 0, next_s = 0;  // rows and embedding size s of the armed level
-  const double* pref_xi = nullptr;  // rows resident (or in flight, ev_pref) in xi_pref
+  // Two buffers: a call that reads one may already copy the following call's rows into the other.
+  // Each prefetch is copied in kPrefParts parts with an event per part, so a call whose rows are
+  // still arriving consumes them part by part instead of waiting for the whole batch.
+  static constexpr int kPrefParts = 4;
+  const double* pref_xi = nullptr;  // rows resident (or in flight) in xi_pref[pref_slot]
   int64_t pref_count = 0, pref_s = 0;
-  DevBuf xi_pref;
-  cudaEvent_t ev_pref = nullptr, ev_pref_read = nullptr;
+  int pref_slot = 0;
+  int64_t pref_part_end[kPrefParts] = {0, 0, 0, 0};  // row ends of the parts
+  DevBuf xi_pref[2];
+  cudaEvent_t ev_pref_part[2][kPrefParts] = {};
+  cudaEvent_t ev_pref_read[2] = {nullptr, nullptr};  // last read of each buffer (main stream)
   // residual history of failing samples (osc_ctx_set_history): the first failing slot of the last
   // osc_level_draws call is re-solved with the history kept (fem.cpp:359-379 SolverError::history)
   int hist_req = 0;

@@ -598,7 +598,7 @@ std::pair<bool, bool> draws_impl(Level* L, const osc_problem* prob, uint64_t see
       if (from_pref) {
         if (chunk + 1 == (int64_t)sched.size()) {  // the prefetch buffer consumed: a later prefetch may refill it
           OSC_CUDA(cudaEventRecord(c->ev_pref_read[cur], c->stream));
-          if (c->pref_xi == xi) c->pref_xi = nullptr;
+          if (c->pref_slot == cur) c->pref_xi = nullptr;  // (a prefetch issued by this call lives in the other slot)
         }
       } else if (xi_host) {  // ξ buffer consumed: start the next chunk's copy under this chunk's solves
         OSC_CUDA(cudaEventRecord(c->ev_ce_done[chunk & 1], c->stream));

@@ -165,6 +165,30 @@ int osc_build_spectrum_device(osc_ctx* ctx, int m, int family, double sigma2, do
  * (embedding.cpp:105-110,153-163). k_trunc = 0 → no truncated copy. */
 int osc_level_create(osc_ctx* ctx, int m, int J, const double* eigenvalues, int64_t k_trunc,
                      osc_level** out);
+/* build_operator + from_parts + truncated (embedding.cpp:90-163) entirely in HBM: the spectrum as in
+ * osc_build_spectrum_device, its minimum (the SPD test; the only value that reaches the host), the
+ * clamp, √max(λ,0), the stable descending order (a stable radix sort of (λ, index) pairs, i.e.
+ * std::stable_sort by a > b, :105-107) and the truncation mask. The eigenvalues and the order stay
+ * resident: osc_level_retruncate(k) is truncated(k) without a rebuild, osc_level_eigenvalues copies
+ * the clamped λ to the host (s doubles; e.g. for osc_spectrum_save or the estimator's k_ℓ rule). J from
+ * osc_level_info. Same model support as osc_build_spectrum_device. */
+int osc_level_create_device(osc_ctx* ctx, int m, int family, double sigma2, double lambda, double nu_or_p,
+                            const double* fractions, int n_fractions, double tol_spd_factor,
+                            int64_t k_trunc, osc_level** out);
+int osc_level_retruncate(osc_level* level, int64_t k_trunc);
+int osc_level_eigenvalues(osc_level* level, double* out);
+/* smoothing_error_estimate (embedding.cpp:205-228): mean and sample variance of ‖Z − Z̃‖∞ over
+ * n_samples draws ξ_i = NormalStream(seed, 0, i), Z̃ from the level's truncated spectrum. Z − Z̃ is
+ * linear in ξ, so each sample is ONE CE pass with the dropped modes' √λ whose column pass reduces
+ * sup|·| over the (m+1)² window in its epilogue; no field is stored or copied. out = [mean, variance]
+ * (Welford in index order); sup_out (may be NULL) receives the n_samples sup-norms. A level with
+ * k_trunc = 0 gives zeros. */
+int osc_smoothing_error(osc_level* level, int n_samples, uint64_t seed, double out[2], double* sup_out);
+/* OSC1 spectrum files (save_spectrum / load_spectrum, embedding.cpp:262-294; d = 2, square grids):
+ * "OSC1", u32 d, u32 m[d], u32 J[d], u64 s, s little-endian f64. load returns a malloc'd array
+ * (release with osc_free). Errors as the reference's ConfigError cases. */
+int osc_spectrum_save(const char* path, int m, int J, const double* eigenvalues, int64_t s);
+int osc_spectrum_load(const char* path, int* m_out, int* J_out, int64_t* s_out, double** eig_out);
 
 /* Cross-call ξ prefetch for a streaming caller (the reference's estimate_adaptive issues
  * consecutive run_level_draws batches, estimators.cpp:304-369). Arms the host rows xi_next

@@ -14,7 +14,8 @@ ROOT = os.path.dirname(HERE)
 # OSC_LIB: developer override (A/B builds of the same sources); the default is the in-tree build
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 HEADER = os.path.join(ROOT, "include", "oscfield_b200.h")
-SOURCES = ["csrc/capi.cu", "csrc/ce_sample.cu", "csrc/mgpcg.cu", "csrc/setup.cpp", "csrc/group.cpp"]
+SOURCES = ["csrc/capi.cu", "csrc/ce_sample.cu", "csrc/mgpcg.cu", "csrc/level_setup.cu", "csrc/setup.cpp",
+           "csrc/group.cpp"]
 DEPS = SOURCES + ["csrc/osc_internal.cuh", "csrc/osc_device.cuh"]
 
 NVCC_FLAGS = [
@@ -38,7 +39,8 @@ EXPORTS = [
     "osc_ctx_set_mem_budget", "osc_ctx_set_profiling", "osc_ctx_profile_only", "osc_ctx_kernel_stats", "osc_ctx_reset_stats",
     "osc_ctx_launch_count", "osc_host_alloc", "osc_host_free", "osc_free", "osc_build_spectrum",
     "osc_build_spectrum_device",
-    "osc_level_create", "osc_level_prefetch_xi", "osc_level_destroy", "osc_level_info", "osc_level_draws", "osc_summarize",
+    "osc_level_create", "osc_level_create_device", "osc_level_retruncate", "osc_level_eigenvalues",
+    "osc_smoothing_error", "osc_spectrum_save", "osc_spectrum_load", "osc_level_prefetch_xi", "osc_level_destroy", "osc_level_info", "osc_level_draws", "osc_summarize",
     "osc_normals", "osc_ce_sample", "osc_darcy_solve", "osc_qoi",
     "osc_level_sums_reset", "osc_level_sums_read", "osc_ctx_set_history", "osc_ctx_failure_history",
     "osc_group_create", "osc_group_destroy", "osc_group_size", "osc_group_ctx", "osc_group_level_create",
@@ -122,6 +124,14 @@ def lib() -> C.CDLL:
     L.osc_build_spectrum_device.argtypes = [vp, ip, ip, C.c_double, C.c_double, C.c_double, vp, ip, C.c_double,
                                             C.POINTER(C.c_int), C.POINTER(i64), C.POINTER(vp)]
     L.osc_level_create.argtypes = [vp, ip, ip, vp, i64, C.POINTER(vp)]
+    L.osc_level_create_device.argtypes = [vp, ip, ip, C.c_double, C.c_double, C.c_double, vp, ip, C.c_double,
+                                          i64, C.POINTER(vp)]
+    L.osc_level_retruncate.argtypes = [vp, i64]
+    L.osc_level_eigenvalues.argtypes = [vp, vp]
+    L.osc_smoothing_error.argtypes = [vp, ip, C.c_uint64, dp, vp]
+    L.osc_spectrum_save.argtypes = [C.c_char_p, ip, ip, vp, i64]
+    L.osc_spectrum_load.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64),
+                                    C.POINTER(vp)]
     L.osc_level_destroy.argtypes = [vp]
     L.osc_level_destroy.restype = None
     L.osc_level_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),

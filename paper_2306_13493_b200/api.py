@@ -21,7 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
-import struct
+import os
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -316,28 +316,16 @@ class SmoothingErrorStats:
 
 
 def smoothing_error_estimate(op: "EmbeddingOperator", k: int, n_samples: int, seed: int,
-                             ctx: Optional[Context] = None, chunk: int = 64) -> SmoothingErrorStats:
-    """Monte Carlo estimate of E‖Z − Z̃‖∞ (embedding.cpp:205-228): Z and Z̃ share the device ξ of
-    NormalStream(seed, 0, i); Z̃ drops the k smallest eigenvalues. Both fields come from the
-    device CE path; the sup-norm and the Welford update run on the host in index order."""
+                             ctx: Optional[Context] = None) -> SmoothingErrorStats:
+    """Monte Carlo estimate of E‖Z − Z̃‖∞ (embedding.cpp:205-228) with ξ_i = NormalStream(seed, 0, i);
+    Z̃ drops the k smallest eigenvalues. osc_smoothing_error: one CE pass per sample over the dropped
+    modes (Z − Z̃ is linear in ξ) with the sup-norm reduced in the column pass's epilogue."""
     if n_samples < 2:
         raise ConfigError("smoothing_error_estimate: need at least 2 samples")
-    ctx = ctx or default_context()
-    m = op.grid.m(0)
-    lev = op.device_level(ctx, k)
-    mean, m2 = 0.0, 0.0
-    for c0 in range(0, n_samples, chunk):
-        cnt = min(chunk, n_samples - c0)
-        full = lev.sample_fields(None, count=cnt, seed=seed, ell=0, index0=c0, fine=True)
-        smooth = lev.sample_fields(None, count=cnt, seed=seed, ell=0, index0=c0, fine=True,
-                                   truncated=k > 0)
-        sup = np.max(np.abs(full - smooth), axis=1)
-        for j, v in enumerate(sup):
-            i = c0 + j
-            d = v - mean
-            mean += d / (i + 1)
-            m2 += d * (v - mean)
-    return SmoothingErrorStats(mean, m2 / (n_samples - 1))
+    if k < 0 or k >= op.s:
+        raise ConfigError("truncated: k must lie in [0, s); at least one mode must survive")
+    lev = op.device_level(ctx or default_context(), k)
+    return lev.smoothing_error(n_samples, seed)
 
 
 class DeviceLevel:
@@ -351,6 +339,43 @@ class DeviceLevel:
         _check(self._lib.osc_level_create(ctx.h, int(m), int(J), _p(eig), int(k_trunc), C.byref(h)))
         self.h = h.value
         self.m, self.J, self.n, self.s, self.k_trunc = m, J, 2 * (m + J), (2 * (m + J)) ** 2, k_trunc
+
+    @classmethod
+    def from_model(cls, ctx: Context, grid: GridSpec, model: "CovarianceModel", k_trunc: int = 0,
+                   options: Optional["BuildOptions"] = None) -> "DeviceLevel":
+        """build_operator + from_parts + truncated in HBM (osc_level_create_device): the spectrum, the
+        SPD test, √λ, the stable descending order and the mask never visit the host."""
+        self = cls.__new__(cls)
+        self.ctx, self._lib = ctx, L.lib()
+        fr = None if options is None else np.ascontiguousarray(options.padding_fractions, dtype=np.float64)
+        h = C.c_void_p()
+        _check(self._lib.osc_level_create_device(
+            ctx.h, grid.m(0), int(model.family), model.sigma2, model.lambda_, model.param, _p(fr),
+            0 if fr is None else len(fr), 0.0 if options is None else options.tol_spd_factor, int(k_trunc),
+            C.byref(h)))
+        self.h = h.value
+        m_, J_, n_, s_, k_ = C.c_int(), C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
+        _check(self._lib.osc_level_info(self.h, C.byref(m_), C.byref(J_), C.byref(n_), C.byref(s_), C.byref(k_)))
+        self.m, self.J, self.n, self.s, self.k_trunc = m_.value, J_.value, n_.value, s_.value, k_.value
+        return self
+
+    def retruncate(self, k: int):
+        """EmbeddingOperator::truncated(k) from the resident order (device-built levels)."""
+        _check(self._lib.osc_level_retruncate(self.h, int(k)))
+        self.k_trunc = int(k)
+
+    def eigenvalues(self) -> np.ndarray:
+        """The clamped eigenvalues of a device-built level (s doubles, copied to the host)."""
+        out = np.empty(self.s)
+        _check(self._lib.osc_level_eigenvalues(self.h, out.ctypes.data))
+        return out
+
+    def smoothing_error(self, n_samples: int, seed: int, return_sups: bool = False):
+        out = (C.c_double * 2)()
+        sups = np.empty(n_samples) if return_sups else None
+        _check(self._lib.osc_smoothing_error(self.h, int(n_samples), int(seed), out, _p(sups)))
+        st = SmoothingErrorStats(out[0], out[1])
+        return (st, sups) if return_sups else st
 
     def __del__(self):
         try:
@@ -432,33 +457,22 @@ def build_operator(grid: GridSpec, model: CovarianceModel,
 
 
 def save_spectrum(op: EmbeddingOperator, path: str) -> None:
-    """OSC1 dump (embedding.hpp:131-134): "OSC1", u32 d, u32 m[d], u32 J[d], u64 s, s f64."""
-    with open(path, "wb") as f:
-        f.write(b"OSC1")
-        f.write(struct.pack("<I", 2))
-        f.write(struct.pack("<II", op.grid.m(0), op.grid.m(1)))
-        f.write(struct.pack("<II", op.padding[0], op.padding[1]))
-        f.write(struct.pack("<Q", op.s))
-        f.write(np.ascontiguousarray(op.eigenvalues, dtype="<f8").tobytes())
+    """OSC1 dump (osc_spectrum_save; embedding.cpp:262-271)."""
+    eig = np.ascontiguousarray(op.eigenvalues, dtype=np.float64)
+    _check(L.lib().osc_spectrum_save(os.fsencode(path), op.grid.m(0), op.padding[0], eig.ctypes.data, eig.size))
 
 
 def load_spectrum(path: str, sigma2: float) -> EmbeddingOperator:
-    """OSC1 load (embedding.cpp:262-294) — the parity-injection format for truncation masks."""
-    with open(path, "rb") as f:
-        data = f.read()
-    if data[:4] != b"OSC1":
-        raise ConfigError(f"load_spectrum: bad magic in {path}")
-    d = struct.unpack_from("<I", data, 4)[0]
-    if d != 2:
-        raise ConfigError("load_spectrum: only d = 2 is supported by the device path")
-    m0, m1, J0, J1 = struct.unpack_from("<IIII", data, 8)
-    s = struct.unpack_from("<Q", data, 24)[0]
-    if m0 != m1 or J0 != J1 or s != (2 * (m0 + J0)) * (2 * (m1 + J1)):
-        raise ConfigError(f"load_spectrum: inconsistent header in {path}")
-    eig = np.frombuffer(data, dtype="<f8", count=s, offset=32)
-    if eig.size != s:
-        raise ConfigError(f"load_spectrum: truncated file {path}")
-    return EmbeddingOperator(GridSpec.square(m0), J0, eig.astype(np.float64), sigma2)
+    """OSC1 load (osc_spectrum_load; embedding.cpp:273-294) — the parity-injection format for
+    truncation masks."""
+    lib = L.lib()
+    m, J, s_, ptr = C.c_int(), C.c_int(), C.c_int64(), C.c_void_p()
+    _check(lib.osc_spectrum_load(os.fsencode(path), C.byref(m), C.byref(J), C.byref(s_), C.byref(ptr)))
+    try:
+        eig = np.ctypeslib.as_array((C.c_double * s_.value).from_address(ptr.value)).copy()
+    finally:
+        lib.osc_free(ptr)
+    return EmbeddingOperator(GridSpec.square(m.value), J.value, eig, sigma2)
 
 
 # ---- problem / options (estimators.hpp, fem.hpp) ---------------------------------------------------

@@ -381,9 +381,8 @@ void osc_level_destroy(osc_level* L) {
   if (!L) return;
   cudaSetDevice(L->ctx->device);
   cudaStreamSynchronize(L->ctx->stream);
-  L->sqrt_full.release();
-  L->sqrt_trunc.release();
-  L->twiddle.release();
+  for (DevBuf* b : {&L->sqrt_full, &L->sqrt_trunc, &L->twiddle, &L->eig, &L->perm, &L->sqrt_comp, &L->run_sums})
+    b->release();
   delete L;
 }
 

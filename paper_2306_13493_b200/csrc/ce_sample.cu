@@ -21,6 +21,7 @@
 #include <vector>
 #include <cstdlib>
 
+#include "fft_dif.cuh"
 #include "osc_device.cuh"
 #include "osc_internal.cuh"
 
@@ -30,6 +31,21 @@ namespace {
 
 // elements per thread for a length-n transform
 inline int elems_for(int n) { return n >= 8 ? 8 : n; }
+
+// Sup-norm mode of the column passes (smoothing_error_estimate, embedding.cpp:217-219): instead of
+// storing the field, every thread folds |z| of its outputs into v and the CTA commits max to sup[b]
+// (non-negative doubles order like their bit patterns, so one integer atomicMax per warp does it).
+__device__ __forceinline__ void sup_commit(double v, unsigned long long* __restrict__ sup_b) {
+  // called by every thread of the CTA, converged; CTAs are powers of two (≥ 2 threads), so the live
+  // lanes of a warp are 0 … 2^k − 1 and the butterfly over them leaves the warp's max in lane 0
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31;
+  for (int o = 16; o; o >>= 1) {
+    const double w = __shfl_xor_sync(mask, v, o);
+    if ((mask >> (lane ^ o)) & 1u) v = fmax(v, w);
+  }
+  if (lane == 0) atomicMax(sup_b, (unsigned long long)__double_as_longlong(v));
+}
 
 // Pass 1: one CTA slot per (row pair, sample). Writes the TRANSPOSED half spectrum
 // inter[b][p][q1] (q1 fastest), so rows q1a, q1b land in one 32-byte sector and pass 2 reads
@@ -94,7 +110,7 @@ template <int E, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
     const double2* __restrict__ inter, int n, int m, int NT, int P, int cs, double inv_n,
     int do_exp, const double2* __restrict__ tw, double* __restrict__ out_fine,
-    double* __restrict__ out_coarse, int* __restrict__ bad_flag) {
+    double* __restrict__ out_coarse, int* __restrict__ bad_flag, unsigned long long* __restrict__ sup) {
   extern __shared__ double2 smem[];
   const int T = n / E;
   const int t = threadIdx.x >> (31 - __clz(T));
@@ -118,6 +134,7 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
   double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
   double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
   int bad = 0;
+  double vmax = 0.0;
   const int lnt = 31 - __clz(NT);  // NT is a power of two
   for (int idx = threadIdx.x; idx < NT * n_rows; idx += blockDim.x) {
     const int tt = idx & (NT - 1), i = idx >> lnt;
@@ -127,11 +144,13 @@ __global__ void __launch_bounds__(MAXT, 1024 / MAXT) ce_cols_kernel(
     const double2 v = smem[tt * ld + fpad(p1)];
     const double zval = (v.x + v.y) * inv_n;
     if (!isfinite(zval)) bad = 1;
+    vmax = fmax(vmax, fabs(zval));
     const double o = do_exp ? exp(zval) : zval;
     if (of) of[(int64_t)p1 * mf + p0] = o;
     if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
   }
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+  if (sup) sup_commit(vmax, sup + b);
 }
 
 // ---- compile-time-n path (n = 2^LOGN, 16 ≤ n ≤ 8192) ----------------------------------------------
@@ -351,7 +370,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) ce_cols_t_kernel(
     const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
     const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
-    int* __restrict__ bad_flag) {
+    int* __restrict__ bad_flag, unsigned long long* __restrict__ sup) {
   using PL = FftPlan<LOGN>;
   using LS = LastStage<LOGN>;
   constexpr int n = PL::n, T = PL::T;
@@ -377,25 +396,27 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) c
     __syncthreads();
     stage_load_compute<LOGN, LS::R, LS::LNS>(x, lt, t, w);
   }
-  if (!valid) return;  // no barriers below
   const int mf = m + 1, mc = m / 2 + 1;
   double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
   double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
   const int p0 = j * cs;
   int bad = 0;
+  double vmax = 0.0;
 #pragma unroll
   for (int g = 0; g < LS::G; ++g)
 #pragma unroll
     for (int r = 0; r < LS::R; ++r) {
       const int p1 = lt + g * T + r * (n / LS::R);  // output row of this register
-      if (p1 > m || (p1 & (cs - 1))) continue;
+      if (!valid || p1 > m || (p1 & (cs - 1))) continue;
       const double zval = (w[g][r].x + w[g][r].y) * inv_n;
       if (!isfinite(zval)) bad = 1;
+      vmax = fmax(vmax, fabs(zval));
       const double o = do_exp ? exp(zval) : zval;
       if (of) of[(int64_t)p1 * mf + p0] = o;
       if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
     }
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+  if (sup) sup_commit(vmax, sup + b);
 }
 
 // Column pass with two columns per thread (32 ≤ n ≤ 4096; ce_cols_t_kernel below and above): the same stages as ce_cols_t_kernel
@@ -451,7 +472,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MINB) ce_cols2_t_kernel(
     const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
     const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
-    int* __restrict__ bad_flag) {
+    int* __restrict__ bad_flag, unsigned long long* __restrict__ sup) {
   using PL = FftPlan<LOGN>;
   using LS = LastStage<LOGN>;
   constexpr int n = PL::n, T = PL::T;
@@ -487,6 +508,7 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
   double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
   double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
   int bad = 0;
+  double vmax = 0.0;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int j = j0 + c;
@@ -500,23 +522,154 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
         if (p1 > m || (p1 & (cs - 1))) continue;
         const double zval = (w[c][g][r].x + w[c][g][r].y) * inv_n;
         if (!isfinite(zval)) bad = 1;
+        vmax = fmax(vmax, fabs(zval));
         const double o = do_exp ? exp(zval) : zval;
         if (of) of[(int64_t)p1 * mf + p0] = o;
         if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
       }
   }
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+  if (sup) sup_commit(vmax, sup + b);
+}
+
+// ---- group-local DIF passes (fft_dif.cuh) -------------------------------------------------------------
+// Same operands, intermediate layout and epilogues as the Stockham passes above; the transform is the
+// radix-8 DIF whose exchanges after the first are warp-local.
+template <int LOGN>
+struct DifPlan {
+  using PL = FftPlan<LOGN>;
+  static constexpr int LD_ROWS = (npad<LOGN>(PL::n - 1) + 1 > PL::LD ? npad<LOGN>(PL::n - 1) + 1 : PL::LD) | 1;
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) ce_rows_d_kernel(
+    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
+    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
+  using PL = FftPlan<LOGN>;
+  constexpr int n = PL::n, T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;  // transform slot in this CTA
+  const int lt = threadIdx.x % T;
+  const int rp = blockIdx.x * PL::NT + t;  // row pair (n/2 is a multiple of NT)
+  const int b = blockIdx.y;
+  const int q1a = 2 * rp;
+  double2* x[1] = {smem + t * DifPlan<LOGN>::LD_ROWS};
+  double2 v[1][8];
+  rows_operands<LOGN>(sqrt_lam, xi, philox_keys(seed), ell, index0 + (uint64_t)b, b, q1a, lt, v[0]);
+  struct Sink {
+    double2 o[8];
+    int p[8];
+    int i = 0;
+    __device__ __forceinline__ void operator()(int, int pp, double2 val) {
+      o[i] = val;
+      p[i] = pp;
+      ++i;
+    }
+  } sink;
+  fft_dif<LOGN, 1, PL::THREADS>(v, x, lt, tw, sink);
+  // natural order for the unpack (Z[p] pairs with Z[n − p]): every read of the exchanges is done first
+  dif_gsync<T, PL::THREADS>();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[0][npad<LOGN>(sink.p[i])] = sink.o[i];
+  dif_gsync<T, PL::THREADS>();
+  const int Ph = inter_groups(P);
+  for (int p = lt; p < P; p += T) {
+    const int p0 = p * cs;
+    const double2 zp = x[0][npad<LOGN>(p0)];
+    const double2 zm = x[0][npad<LOGN>((n - p0) & (n - 1))];
+    // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
+    double2* o = inter + inter_pair_idx(b, Ph, n, p, q1a);
+    o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+    o[CE_IL] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));  // row q1a + 1
+  }
+}
+
+// Column pass, NC columns per thread (NC = 2: columns j0, j0 + 1 side by side in the intermediate).
+template <int LOGN, int NC>
+__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, NC == 2 ? Cols2Plan<LOGN>::MINB : FftPlan<LOGN>::MINB)
+    ce_cols_d_kernel(const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
+                     const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
+                     int* __restrict__ bad_flag, unsigned long long* __restrict__ sup) {
+  using PL = FftPlan<LOGN>;
+  constexpr int n = PL::n, T = PL::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x / T;
+  const int lt = threadIdx.x % T;
+  const int b = blockIdx.y;
+  const int j0 = NC * (blockIdx.x * PL::NT + t);  // columns j0 … j0 + NC − 1
+  double2* x[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) x[c] = smem + (NC * t + c) * PL::LD;
+  double2 v[NC][8];
+  {
+    const double2* s0 = inter + inter_pair_idx(b, inter_groups(P), n, j0 < P ? j0 : 0, lt);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const bool ok = j0 + c < P;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[c][r] = ok ? __ldg(s0 + CE_IL * r * T + c) : make_double2(0.0, 0.0);
+    }
+  }
+  const int mf = m + 1, mc = m / 2 + 1;
+  struct Sink {
+    double* of;
+    double* oc;
+    int j0, P, m, cs, mf, mc, do_exp, bad;
+    double inv_n, vmax;
+    __device__ __forceinline__ void operator()(int c, int p1, double2 val) {
+      const int j = j0 + c;
+      if (j >= P || p1 > m || (p1 & (cs - 1))) return;
+      const int p0 = j * cs;
+      const double zval = (val.x + val.y) * inv_n;
+      if (!isfinite(zval)) bad = 1;
+      vmax = fmax(vmax, fabs(zval));
+      const double o = do_exp ? exp(zval) : zval;
+      if (of) of[(int64_t)p1 * mf + p0] = o;
+      if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
+    }
+  } sink{out_fine ? out_fine + (int64_t)b * mf * mf : nullptr,
+         out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr,
+         j0, P, m, cs, mf, mc, do_exp, 0, inv_n, 0.0};
+  fft_dif<LOGN, NC, PL::THREADS>(v, x, lt, tw, sink);
+  if (sink.bad && bad_flag) atomicOr(bad_flag + b, 1);
+  if (sup) sup_commit(sink.vmax, sup + b);
 }
 
 template <int LOGN>
 void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev, uint64_t seed,
               uint32_t ell, uint64_t index0, int count, bool do_exp, double* out_fine, double* out_coarse,
-              int* bad_flag, int cs, double2* inter) {
+              int* bad_flag, int cs, double2* inter, unsigned long long* sup) {
   using PL = FftPlan<LOGN>;
   const int m = L->m, P = m / cs + 1;
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = sizeof(double2) * (size_t)PL::NT * PL::LD;
   cudaStream_t st = ctx->stream;
+  static const bool dif = [] { const char* e = std::getenv("OSC_CE_DIF"); return !e || std::atoi(e) != 0; }();
+  if (dif) {
+    {
+      const size_t smr = sizeof(double2) * (size_t)PL::NT * DifPlan<LOGN>::LD_ROWS;
+      auto kern = ce_rows_d_kernel<LOGN>;
+      smem_attr(kern, smr);
+      KScope ks(ctx, "ce_rows");
+      kern<<<dim3((PL::n / 2) / PL::NT, count), PL::THREADS, smr, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs,
+                                                                         tw, inter);
+      OSC_CUDA(cudaGetLastError());
+    }
+    KScope ks(ctx, "ce_cols");
+    if constexpr (LOGN >= 5 && LOGN <= 12) {
+      auto kern = ce_cols_d_kernel<LOGN, 2>;
+      smem_attr(kern, (2 * sm));
+      kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
+          inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag, sup);
+    } else {
+      auto kern = ce_cols_d_kernel<LOGN, 1>;
+      smem_attr(kern, sm);
+      kern<<<dim3((P + PL::NT - 1) / PL::NT, count), PL::THREADS, sm, st>>>(
+          inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag, sup);
+    }
+    OSC_CUDA(cudaGetLastError());
+    return;
+  }
   {
     auto kern = ce_rows_t_kernel<LOGN>;
     smem_attr(kern, sm);
@@ -532,7 +685,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
     smem_attr(kern, (2 * sm));
     KScope ks(ctx, "ce_cols");
     kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
-        inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag);
+        inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag, sup);
     OSC_CUDA(cudaGetLastError());
     return;
   }
@@ -542,7 +695,7 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
     KScope ks(ctx, "ce_cols");
     kern<<<dim3((P + PL::NT - 1) / PL::NT, count), PL::THREADS, sm, st>>>(inter, m, P, cs, 1.0 / PL::n,
                                                                            do_exp ? 1 : 0, tw, out_fine,
-                                                                           out_coarse, bad_flag);
+                                                                           out_coarse, bad_flag, sup);
     OSC_CUDA(cudaGetLastError());
   }
 }
@@ -576,7 +729,7 @@ CeGeom cols_geom(int n, int P) {
 template <int E, int MAXT>
 void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
                  uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
-                 double* out_fine, double* out_coarse, int* bad_flag, int cs, double2* inter) {
+                 double* out_fine, double* out_coarse, int* bad_flag, int cs, double2* inter, unsigned long long* sup) {
   const int n = L->n, m = L->m;
   const int P = m / cs + 1;
   const double2* tw = L->twiddle.as<double2>();
@@ -597,7 +750,7 @@ void launch_pair(Ctx* ctx, const Level* L, const double* sqrt_lam, const double*
     smem_attr(kern, g.smem);
     KScope ks(ctx, "ce_cols");
     kern<<<grid, g.threads, g.smem, st>>>(inter, n, m, g.NT, P, cs, 1.0 / n, do_exp ? 1 : 0, tw,
-                                         out_fine, out_coarse, bad_flag);
+                                         out_fine, out_coarse, bad_flag, sup);
     OSC_CUDA(cudaGetLastError());
   }
 }
@@ -708,7 +861,7 @@ __global__ void ce_rows_generic_kernel(const double* __restrict__ sqrt_lam, cons
 __global__ void ce_cols_generic_kernel(const double2* __restrict__ inter, Radices rd, int m, int P, int cs,
                                        double inv_n, int do_exp, const double2* __restrict__ tw,
                                        double* __restrict__ out_fine, double* __restrict__ out_coarse,
-                                       int* __restrict__ bad_flag) {
+                                       int* __restrict__ bad_flag, unsigned long long* __restrict__ sup) {
   extern __shared__ double2 smem[];
   const int n = rd.n;
   const int j = blockIdx.x, b = blockIdx.y;
@@ -721,16 +874,19 @@ __global__ void ce_cols_generic_kernel(const double2* __restrict__ inter, Radice
   double* of = out_fine ? out_fine + (int64_t)b * mf * mf : nullptr;
   double* oc = out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr;
   int bad = 0;
+  double vmax = 0.0;
   const int p0 = j * cs;
   for (int i = threadIdx.x; i <= m / cs; i += blockDim.x) {
     const int p1 = i * cs;
     const double zval = (x[p1].x + x[p1].y) * inv_n;
     if (!isfinite(zval)) bad = 1;
+    vmax = fmax(vmax, fabs(zval));
     const double o = do_exp ? exp(zval) : zval;
     if (of) of[(int64_t)p1 * mf + p0] = o;
     if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
   }
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
+  if (sup) sup_commit(vmax, sup + b);
 }
 
 bool radices_of(int n, Radices& rd) {
@@ -746,7 +902,8 @@ bool radices_of(int n, Radices& rd) {
 
 void launch_generic(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev, uint64_t seed,
                     uint32_t ell, uint64_t index0, int count, bool do_exp, double* out_fine,
-                    double* out_coarse, int* bad_flag, int cs, double2* inter, const Radices& rd) {
+                    double* out_coarse, int* bad_flag, int cs, double2* inter, const Radices& rd,
+                    unsigned long long* sup) {
   const int n = L->n, m = L->m, P = m / cs + 1;
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = 2 * sizeof(double2) * (size_t)n;
@@ -763,7 +920,7 @@ void launch_generic(Ctx* ctx, const Level* L, const double* sqrt_lam, const doub
     KScope ks(ctx, "ce_cols");
     ce_cols_generic_kernel<<<dim3(P, count), threads, sm, ctx->stream>>>(inter, rd, m, P, cs, 1.0 / n,
                                                                          do_exp ? 1 : 0, tw, out_fine, out_coarse,
-                                                                         bad_flag);
+                                                                         bad_flag, sup);
     OSC_CUDA(cudaGetLastError());
   }
 }
@@ -777,7 +934,7 @@ size_t ce_inter_bytes(const Level* L, int count, int col_stride) {
 
 void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
                       uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
-                      double* out_fine, double* out_coarse, int* bad_flag) {
+                      double* out_fine, double* out_coarse, int* bad_flag, unsigned long long* sup_out) {
   const bool pow2 = (L->n & (L->n - 1)) == 0 && L->n >= 2;
   Radices rd;
   if (!pow2)
@@ -804,27 +961,28 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
     double* of = out_fine ? out_fine + c0 * Nf : nullptr;
     double* oc = out_coarse ? out_coarse + c0 * Nc : nullptr;
     int* bf = bad_flag ? bad_flag + c0 : nullptr;
+    unsigned long long* sp = sup_out ? sup_out + c0 : nullptr;
     // threads per transform T = n/E: ≤ 256 up to n = 2048, 512 at 4096, 1024 at 8192
     if (!pow2)
-      launch_generic(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, rd);
+      launch_generic(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, rd, sp);
     else if (L->n >= 16) {
 #define OSC_CE_T(LG) \
-  case LG: launch_t<LG>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter); break;
+  case LG: launch_t<LG>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, sp); break;
       switch (31 - __builtin_clz((unsigned)L->n)) {
         OSC_CE_T(4) OSC_CE_T(5) OSC_CE_T(6) OSC_CE_T(7) OSC_CE_T(8) OSC_CE_T(9) OSC_CE_T(10) OSC_CE_T(11)
         OSC_CE_T(12) OSC_CE_T(13)
       }
 #undef OSC_CE_T
     } else if (L->n >= 8192)
-      launch_pair<8, 1024>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+      launch_pair<8, 1024>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, sp);
     else if (L->n == 4096)
-      launch_pair<8, 512>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+      launch_pair<8, 512>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, sp);
     else if (L->n >= 8)
-      launch_pair<8, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+      launch_pair<8, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, sp);
     else if (L->n == 4)
-      launch_pair<4, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+      launch_pair<4, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, sp);
     else
-      launch_pair<2, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter);
+      launch_pair<2, 256>(ctx, L, sqrt_lam, xi_c, seed, ell, index0 + c0, cnt, do_exp, of, oc, bf, cs, inter, sp);
   }
 }
 
@@ -928,8 +1086,9 @@ bool spectrum_device_supported(int family, double nu_or_p) {
   return false;
 }
 
-std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double sigma2, double lambda,
-                                    double nu_or_p) {
+// Raw spectrum of the padding-J embedding, left in device memory (eig_dev, s doubles).
+void spectrum_device_into(Ctx* ctx, int m, int J, int family, double sigma2, double lambda, double nu_or_p,
+                          double* eig_dev) {
   CovDev c{family, (int)(nu_or_p - 0.5), sigma2, lambda, nu_or_p};
   const int n = 2 * (m + J), h = n / 2;
   const int64_t s = (int64_t)n * n, nw = (int64_t)(h + 1) * (h + 1);
@@ -940,13 +1099,17 @@ std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double s
   T.J = 0;
   T.n = n;
   T.s = s;
-  DevBuf row, win, eig;
-  std::vector<double> out((size_t)s);
+  DevBuf row, win;
+  auto release = [&] {
+    T.sqrt_full.release();
+    T.twiddle.release();
+    row.release();
+    win.release();
+  };
   try {
     T.sqrt_full.ensure(sizeof(double) * s);
     row.ensure(sizeof(double) * s);
     win.ensure(sizeof(double) * (nw + s));  // the window, then the tab of the first row
-    eig.ensure(sizeof(double) * s);
     upload_twiddles(&T);
     double* tab = win.as<double>() + nw;
     {
@@ -962,23 +1125,31 @@ std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double s
                      nullptr, nullptr);
     {
       KScope ks(ctx, "setup.mirror");
-      mirror_kernel<<<2048, 256, 0, st>>>(win.as<double>(), n, static_cast<double>(n), eig.as<double>());
+      mirror_kernel<<<2048, 256, 0, st>>>(win.as<double>(), n, static_cast<double>(n), eig_dev);
       OSC_CUDA(cudaGetLastError());
     }
-    OSC_CUDA(cudaMemcpyAsync(out.data(), eig.p, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
     OSC_CUDA(cudaStreamSynchronize(st));
   } catch (...) {
-    T.sqrt_full.release();
-    T.twiddle.release();
-    row.release();
-    win.release();
+    release();
+    throw;
+  }
+  release();
+}
+
+std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double sigma2, double lambda,
+                                    double nu_or_p) {
+  const int n = 2 * (m + J);
+  const int64_t s = (int64_t)n * n;
+  DevBuf eig;
+  std::vector<double> out((size_t)s);
+  try {
+    eig.ensure(sizeof(double) * s);
+    spectrum_device_into(ctx, m, J, family, sigma2, lambda, nu_or_p, eig.as<double>());
+    OSC_CUDA(cudaMemcpy(out.data(), eig.p, sizeof(double) * s, cudaMemcpyDeviceToHost));
+  } catch (...) {
     eig.release();
     throw;
   }
-  T.sqrt_full.release();
-  T.twiddle.release();
-  row.release();
-  win.release();
   eig.release();
   return out;
 }

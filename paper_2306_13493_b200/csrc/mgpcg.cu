@@ -825,6 +825,28 @@ __device__ __forceinline__ Pair ld2(const double* __restrict__ base, int xa, int
   return Pair{ldv<INT>(base, xa, y, n0), ldv<INT>(base, xa + 1, y, n0)};
 }
 
+// Level-0 search direction p and preconditioned residual z of the multilevel PCG are STORED in fp32
+// (computed in fp64): u += αp and r −= αAp use the same fp64 p recomputed from the stored values by
+// every lane that needs it, so r stays the residual of u to fp64 rounding whatever the direction is;
+// the 2⁻²⁴ rounding only perturbs the next direction (an inexact preconditioner), not the fixed
+// point. 16 B/node less per iteration (pcg_update 64 → 52, up sweep 30 → 26).
+#ifdef OSC_PZ64
+using pz_t = double;
+#else
+using pz_t = float;
+#endif
+template <bool INT>
+__device__ __forceinline__ Pair ld2(const float* __restrict__ base, int xa, int y, int n0) {
+  if (INT) {
+    const float* q = base + (int64_t)y * n0 + xa;
+    return Pair{(double)__ldg(q), (double)__ldg(q + 1)};
+  }
+  const bool yok = (unsigned)y < (unsigned)n0;
+  const float* q = base + (int64_t)y * n0 + xa;
+  return Pair{(yok && (unsigned)xa < (unsigned)n0) ? (double)__ldg(q) : 0.0,
+              (yok && (unsigned)(xa + 1) < (unsigned)n0) ? (double)__ldg(q + 1) : 0.0};
+}
+
 // Edge weights of row y at both columns from k rows y−1, y, y+1. Triangle means in the
 // reference's vertex order with ·(1/3) instead of /3 (≤ 1 ulp per coefficient); each edge is
 // formed once, so both rows of A see the same double. INT: every edge of the pair is interior.
@@ -1058,8 +1080,8 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
 // the update. Reads k, z, p_old, r, u; writes p_new, u, r_next.
 template <bool INT>
 __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double* __restrict__ k,
-                                                     const double* __restrict__ z, const double* __restrict__ p_old,
-                                                     double* __restrict__ p_new, double* __restrict__ u,
+                                                     const pz_t* __restrict__ z, const pz_t* __restrict__ p_old,
+                                                     pz_t* __restrict__ p_new, double* __restrict__ u,
                                                      const double* __restrict__ r, double* __restrict__ r_out,
                                                      double* scal, int* flags, const PairCtx& c) {
   PAIR_UNPACK
@@ -1067,7 +1089,8 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
   const bool first = flags[b * F_NFLAGS + F_FIRST] != 0;
   const double beta = first ? 0.0 : scal[b * S_NSCAL + S_BETA];
   const double alpha = scal[b * S_NSCAL + S_ALPHA];
-  const double *kb = k + off, *zb = z + off, *pb = p_old + off, *rb = r + off;
+  const double *kb = k + off, *rb = r + off;
+  const pz_t *zb = z + off, *pb = p_old + off;
   double* ub = u + off;
   auto comb = [&](Pair zz, Pair oo) {
     return first ? zz : Pair{fma(beta, oo.a, zz.a), fma(beta, oo.b, zz.b)};
@@ -1097,14 +1120,14 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
     const int64_t row = off + (int64_t)y * n0;
     if (outa) {
       const double rn = fma(-alpha, fma(st.a.d, p0.a, od.a), r0.a);
-      p_new[row + xa] = p0.a;
+      p_new[row + xa] = (pz_t)p0.a;
       u[row + xa] = fma(alpha, p0.a, u0.a);
       r_out[row + xa] = rn;
       rr = fma(rn, rn, rr);
     }
     if (outb) {
       const double rn = fma(-alpha, fma(st.b.d, p0.b, od.b), r0.b);
-      p_new[row + xb] = p0.b;
+      p_new[row + xb] = (pz_t)p0.b;
       u[row + xb] = fma(alpha, p0.b, u0.b);
       r_out[row + xb] = rn;
       rr = fma(rn, rn, rr);
@@ -1116,9 +1139,9 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
 
 constexpr int PU_W = 4;  // warps per CTA of pcg_update (A/B knob: 1 and 2 warps are no faster, it is DRAM-bound)
 __global__ void __launch_bounds__(32 * PU_W, 16 / PU_W) pcg_update_cg_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
-                                                              const double* __restrict__ z,
-                                                              const double* __restrict__ p_old,
-                                                              double* __restrict__ p_new, double* __restrict__ u,
+                                                              const pz_t* __restrict__ z,
+                                                              const pz_t* __restrict__ p_old,
+                                                              pz_t* __restrict__ p_new, double* __restrict__ u,
                                                               const double* __restrict__ r, double* __restrict__ r_out,
                                                               double* scal, int* flags, double2* partial, int maxp,
                                                               unsigned* counter, int* n_active, double* hist,
@@ -2075,7 +2098,7 @@ __global__ void __launch_bounds__(32 * RR_W, 4 * 4 / RR_W) restrict_ring_kernel(
 
 template <bool INT>
 __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                       const double* __restrict__ r, double* __restrict__ z_out,
+                                                       const double* __restrict__ r, pz_t* __restrict__ z_out,
                                                        const double* __restrict__ zc, PW4 pw, const PairCtx& c,
                                                        double* wring) {
   PAIR_UNPACK
@@ -2189,14 +2212,14 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
     const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
     const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64(sr0.d);
     if (t >= y0) {
-      double* out = z_out + off + (int64_t)t * n0;
+      pz_t* out = z_out + off + (int64_t)t * n0;
       const double va = ra0 ? zred : zb0, vb = ra0 ? zb0 : zred;
       if (outa) {
-        out[xa] = va;
+        out[xa] = (pz_t)va;
         rz = fma(r0.a, va, rz);
       }
       if (outb) {
-        out[xb] = vb;
+        out[xb] = (pz_t)vb;
         rz = fma(r0.b, vb, rz);
       }
       if (ra0 ? outa : outb) dc = fma(zred - qa, s2, dc);
@@ -2215,7 +2238,7 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
 
 __global__ void __launch_bounds__(32 * SUR_W, 3 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                                const double* __restrict__ r,
-                                                               double* __restrict__ z_out,
+                                                               pz_t* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,
                                                                int* flags, double2* partial, int maxp,
                                                                unsigned* counter) {
@@ -2241,202 +2264,6 @@ __global__ void __launch_bounds__(32 * SUR_W, 3 * 4 / SUR_W) smooth_up_ring_kern
     scal[b * S_NSCAL + S_ALPHA] = gamma / den;
     scal[b * S_NSCAL + S_RZ] = gamma;
   }
-}
-
-// Level-0 restriction from the residual itself: the red-black pre-smoother from z = 0 is formed in
-// registers (z_red = r/D, z_black = (r − Σ A z_red)/D, the arithmetic pcg_update_down used to store)
-// two rows ahead of the red-node residual t = −Σ A z_black, so the pre-smoothed z is never written
-// or read. Row pipeline: ingest(q) forms the stencils of row q, z_red(q), the z pair of row q−1,
-// and returns t at the red node of row q−2. Reads k, r, pw; writes rc.
-template <bool INT>
-__device__ __forceinline__ void restrict_r_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                const double* __restrict__ r, PW4 pw, double* __restrict__ rc,
-                                                int b, int I, bool outI, int J0, int J1) {
-  const int m = g.m, n0 = g.n0, mc = gc.m;
-  const int xa = 2 * I;
-  const int64_t off = (int64_t)b * g.N;
-  const double* rb = r + off;
-  const int ys = 2 * J0 - 1;
-  EdgeRows<INT, false> er(k + off, nullptr, xa, n0, m, ys - 3);
-  const Pair zero{0.0, 0.0};
-  Pair Ed, Nq;
-  er.next(Ed, Nq);  // row ys−3: its N only
-  // pipeline state entering ingest(q): N of row q−1; E/N of rows q−1, q−2 and N of row q−3;
-  // z_red of rows q−2, q−1; the black stencil and r of row q−1; z pairs of rows q−3, q−2
-  Pair N1 = Nq, E1 = zero, N2 = zero, E2 = zero, N3 = zero;
-  double zr2 = 0.0, zr1 = 0.0, rbl1 = 0.0;
-  Sten sb1{1.0, 0.0, 0.0, 0.0, 0.0};
-  Pair zp3 = zero, zp2 = zero;
-  Pair rq = ld2<INT>(rb, xa, ys - 2, n0);
-  auto ingest = [&](int q) {
-    Pair E, N;
-    er.next(E, N);
-    const Pair r0 = rq;
-    rq = ld2<INT>(rb, xa, q + 1, n0);
-    const Sten2 st = sten_pair<INT>(E, N, N1, xa, q, m, bc);
-    const bool ra = RED_IS_A(q);
-    const double zr0 = (ra ? r0.a : r0.b) * rcp64(ra ? st.a.d : st.b.d);
-    // black of row q−1 (its red column is a iff row q−1 is even)
-    const bool ra1 = !ra;
-    const double zr1_e = shdn(zr1), zr1_w = shup(zr1);
-    const double zbl = (rbl1 - (sb1.e * (ra1 ? zr1_e : zr1) + sb1.w * (ra1 ? zr1 : zr1_w) + sb1.n * zr0 +
-                                sb1.s * zr2)) * rcp64(sb1.d);
-    const Pair zp1 = ra1 ? Pair{zr1, zbl} : Pair{zbl, zr1};
-    // t at the red node of row q−2 from the z pairs of rows q−3, q−2, q−1
-    const double t = ra ? red_resid<INT, true>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc)
-                        : red_resid<INT, false>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc);
-    // shift
-    N3 = N2; E2 = E1; N2 = N1; E1 = E; N1 = N;
-    zr2 = zr1; zr1 = zr0;
-    sb1 = ra ? st.b : st.a;
-    rbl1 = ra ? r0.b : r0.a;
-    zp3 = zp2; zp2 = zp1;
-    return t;
-  };
-  // prime: rows ys−2 … ys+1 (their t values belong to rows before ys)
-  ingest(ys - 2);
-  ingest(ys - 1);
-  ingest(ys);
-  ingest(ys + 1);
-  const int mcl = m / 2;
-  const int64_t cb0 = (int64_t)b * mcl * mcl;
-  // fp32 weights stay fp32 in registers until their use (a conversion right after the load would
-  // wait on it there and expose the load latency the row-pair prefetch is meant to hide)
-  auto W4 = [&](int Jc, float w[4]) {
-    const bool ok = I >= 0 && I < mcl && Jc >= 0 && Jc < mcl;
-    const int64_t cell = cb0 + (int64_t)Jc * mcl + I;
-    w[0] = ok ? __ldg(pw.w0 + cell) : 0.0f;
-    w[1] = ok ? __ldg(pw.w1 + cell) : 0.0f;
-    w[2] = ok ? __ldg(pw.w2 + cell) : 0.0f;
-    w[3] = ok ? __ldg(pw.w3 + cell) : 0.0f;
-  };
-  float wc[4];
-  W4(J0 - 1, wc);
-  const double t_first = ingest(ys + 2);  // (xb, 2J0−1)
-  double a_nw = t_first * wc[2], a_ne = t_first * wc[3];
-  double* rcb = rc + (int64_t)b * gc.N;
-  for (int J = J0; J < J1; ++J) {
-    const int y = 2 * J;
-    W4(J, wc);
-    const double t_even = ingest(y + 2);  // (xa, 2J)
-    const double t = ingest(y + 3);       // (xb, 2J+1)
-    const double a_sw = t * wc[0], a_se = t * wc[1];
-    const double v = t_even + a_sw + shup(a_se) + a_nw + shup(a_ne);
-    if (outI) rcb[(int64_t)J * gc.n0 + I] = is_dir(bc, mc, I, J) ? 0.0 : v;
-    a_nw = t * wc[2];
-    a_ne = t * wc[3];
-  }
-}
-
-// Level-0 prolongation + post-smoother of the one-reduction PCG: the pre-smoothed red values are
-// recomputed from r (z_red = r/D, the pre-smoother from z = 0; black pre-smoothed values are not
-// needed: the black sweep overwrites them), so nothing of the down sweep is stored. Returns
-// γ = ⟨r, z⟩ and the local part of δ = ⟨z, Az⟩: after the red sweep (Az)_red = r_red and
-// (Az)_black = r_black + Σ_red-nbrs a (z − v), so δ = γ + Σ_red (z_red − v_red)·(r − D z)_red, where
-// v_red is the prolonged value the black sweep used and (r − D z)_red is the red update's
-// neighbour sum.
-template <bool INT>
-__device__ __forceinline__ double2 smooth_up_r_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
-                                                    const double* __restrict__ r, double* __restrict__ z_out,
-                                                    const double* __restrict__ zc, PW4 pw, const PairCtx& c) {
-  PAIR_UNPACK
-
-  const double *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
-  const int nc0 = gc.n0;
-  const Pair zero{0.0, 0.0};
-  struct ZRaw {  // prolongation inputs of the red node of a row (loaded one row ahead)
-    double c00, c10, c01, c11, w0, w1, w2, w3;
-  };
-  const int I = xa >> 1;
-  const int mcl = m / 2;
-  const int64_t cb0 = (int64_t)b * mcl * mcl;
-  auto ZL = [&](int y) {
-    ZRaw v{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if ((unsigned)y >= (unsigned)n0) return v;
-    if (RED_IS_A(y)) {
-      if (INT || (unsigned)xa < (unsigned)n0) v.c00 = __ldg(zcb + (int64_t)(y >> 1) * nc0 + I);
-    } else if (INT || (unsigned)xb < (unsigned)n0) {
-      const int J = y >> 1;
-      const double* c0r = zcb + (int64_t)J * nc0 + I;
-      v.c00 = __ldg(c0r);
-      v.c10 = __ldg(c0r + 1);
-      v.c01 = __ldg(c0r + nc0);
-      v.c11 = __ldg(c0r + nc0 + 1);
-      if (INT || (I < mcl && J < mcl)) {
-        const int64_t cell = cb0 + (int64_t)J * mcl + I;
-        v.w0 = __ldg(pw.w0 + cell);
-        v.w1 = __ldg(pw.w1 + cell);
-        v.w2 = __ldg(pw.w2 + cell);
-        v.w3 = __ldg(pw.w3 + cell);
-      }
-    }
-    return v;
-  };
-  // red value of row y after prolongation, from its raw row data: r, this row's edges E/N and the
-  // previous row's N (z_red = r/D with the stencil arithmetic of the pre-smoother)
-  auto RV = [&](const ZRaw& v, int y, Pair rr, Pair E, Pair N, Pair Nm) {
-    const double Wa = shup(E.b);
-    double zr;
-    if (RED_IS_A(y)) {
-      const Sten s = mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc);
-      zr = rr.a * rcp64(s.d);
-      return zr + v.c00;
-    }
-    const Sten s = mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc);
-    zr = rr.b * rcp64(s.d);
-    return zr + (v.w0 * v.c00 + v.w1 * v.c10 + v.w2 * v.c01 + v.w3 * v.c11);
-  };
-  EdgeRows<INT, false> er(k + off, nullptr, xa, n0, m, y0 - 3);
-  Pair Ed, N3, E2, N2, E1, N1;
-  er.next(Ed, N3);  // row y0−3: N only
-  er.next(E2, N2);  // row y0−2
-  er.next(E1, N1);  // row y0−1
-  const Pair rA = ld2<INT>(rb, xa, y0 - 2, n0);
-  Pair r1 = ld2<INT>(rb, xa, y0 - 1, n0), r2 = ld2<INT>(rb, xa, y0, n0);
-  // scalars: qa/qb = red values of rows t, t+1 (after prolongation); zbm/zb0 = black new of rows t−1, t
-  double qa = RV(ZL(y0 - 2), y0 - 2, rA, E2, N2, N3);
-  double qb = RV(ZL(y0 - 1), y0 - 1, r1, E1, N1, N2);
-  Pair Nt = N2;
-  Pair r0 = zero;
-  double zbm = 0.0, zb0 = 0.0;
-  Sten sr0{1.0, 0.0, 0.0, 0.0, 0.0};  // stencil of row t's red column
-  ZRaw zq = ZL(y0);
-  double rz = 0.0, dc = 0.0;
-  for (int t = y0 - 2; t < y1; ++t) {
-    const bool ra1 = RED_IS_A(t + 1);  // row t+1: red column a, black b (else the reverse)
-    Pair E2n, N2n;
-    er.next(E2n, N2n);  // row t+2
-    const Pair r3 = ld2<INT>(rb, xa, t + 3, n0);
-    const double qc = RV(zq, t + 2, r2, E2n, N2n, N1);
-    zq = ZL(t + 3);
-    const Sten2 st1 = sten_pair<INT>(E1, N1, Nt, xa, t + 1, m, bc);
-    // black node of row t+1: (r − Σ A z_red_prolonged)/D
-    const double qb_e = shdn(qb), qb_w = shup(qb);
-    const Sten sb = ra1 ? st1.b : st1.a;
-    const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
-    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
-    // output row t: red column = (r − Σ A z_black)/D, black column = z_black
-    const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
-    const bool ra0 = !ra1;
-    const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
-    const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64(sr0.d);
-    const Pair zv = ra0 ? Pair{zred, zb0} : Pair{zb0, zred};
-    if (t >= y0) {
-      double* out = z_out + off + (int64_t)t * n0;
-      if (outa) {
-        out[xa] = zv.a;
-        rz = fma(r0.a, zv.a, rz);
-      }
-      if (outb) {
-        out[xb] = zv.b;
-        rz = fma(r0.b, zv.b, rz);
-      }
-      if (ra0 ? outa : outb) dc = fma(zred - qa, s2, dc);
-    }
-    qa = qb; qb = qc; Nt = N1; E1 = E2n; N1 = N2n;
-    r0 = r1; r1 = r2; r2 = r3; zbm = zb0; zb0 = zbp1; sr0 = ra1 ? st1.a : st1.b;
-  }
-  return make_double2(rz, dc);
 }
 
 // device view of the global hierarchy (one level's operator and centre weights)
@@ -3204,8 +3031,8 @@ void vcycle(Ctx* ctx, int bc, int B) {
       smem_attr(smooth_up_ring_kernel, L0R_SMEM_UP);
       KScope ks(ctx, "mg_smooth_up_r.L0");
       smooth_up_ring_kernel<<<march_grid_w(L.m, B, SUR_W), 32 * SUR_W, L0R_SMEM_UP, st>>>(
-          geo_of(L), geo_of(C), bc, L.k, w.r_cur, L.z2, C.z2, pw_of(L), w.scal, w.flags, part, w.max_parts,
-          w.counter);
+          geo_of(L), geo_of(C), bc, L.k, w.r_cur, reinterpret_cast<pz_t*>(L.z2), C.z2, pw_of(L), w.scal, w.flags, part,
+          w.max_parts, w.counter);
       continue;
     }
     smem_attr(c_up_ring_kernel<true>, up_ring_smem<true>());
@@ -3298,8 +3125,9 @@ void pcg_iteration(Ctx* ctx, const osc_problem* prob, int B, double* r_in, doubl
   {
     KScope ks(ctx, "pcg_update");
     pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, ctx->stream>>>(
-        geo_of(L0), prob->bc, prob->tol, L0.k, L0.z2, p_old, p_new, w.u, r_in, r_out, w.scal, w.flags, part,
-        w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+        geo_of(L0), prob->bc, prob->tol, L0.k, reinterpret_cast<const pz_t*>(L0.z2), reinterpret_cast<const pz_t*>(p_old),
+        reinterpret_cast<pz_t*>(p_new), w.u, r_in, r_out, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active,
+        w.hist, w.hist_cap);
   }
   w.r_cur = r_out;
   vcycle(ctx, prob->bc, B);
@@ -3467,8 +3295,9 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
         KScope ks(ctx, "pcg_update");
         double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
         pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, st>>>(
-            g0, bc, prob->tol, L0.k, L0.z2, p_old, p_new, w.u, w.r_cur, r_next, w.scal, w.flags, part,
-            w.max_parts, w.counter, w.n_active, w.hist, w.hist_cap);
+            g0, bc, prob->tol, L0.k, reinterpret_cast<const pz_t*>(L0.z2), reinterpret_cast<const pz_t*>(p_old),
+            reinterpret_cast<pz_t*>(p_new), w.u, w.r_cur, r_next, w.scal, w.flags, part, w.max_parts, w.counter,
+            w.n_active, w.hist, w.hist_cap);
         w.r_cur = r_next;
       }
       OSC_CUDA(cudaMemcpyAsync(ring + (it & 3), w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));

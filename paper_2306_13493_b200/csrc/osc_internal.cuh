@@ -187,6 +187,10 @@ struct Level {
   int m = 0, J = 0, n = 0;
   int64_t s = 0, k_trunc = 0;
   DevBuf sqrt_full, sqrt_trunc, twiddle;  // twiddle: n complex exp(+2πi t/n)
+  // device-built levels (osc_level_create_device): the clamped eigenvalues and their stable
+  // descending order stay resident, so re-truncation and OSC1 dumps need no host setup
+  DevBuf eig, perm;  // perm: uint32 indices, largest eigenvalue first
+  DevBuf sqrt_comp;  // √λ of the dropped modes (osc_smoothing_error), built on first use
   // running per-level sums in HBM (osc_level_sums_reset): [0..4] = [n, Σ(Y−Ky), Σ(Y−Ky)², Σ(q−Kq),
   // Σ(q−Kq)²] accumulated by every osc_level_draws call; [8..12] receive the cross-rank reduction
   DevBuf run_sums;
@@ -199,9 +203,12 @@ struct Level {
 //  xi_dev != nullptr: ξ rows in device memory (count*s), else device Philox of indices
 //  index0 + b. out_fine/out_coarse (device, may be null) receive exp(Z) (if do_exp) or Z.
 //  col_stride 2 computes only the even columns/rows (coarse-only pass).
+//  sup_out (device, count words, zeroed by the caller): the bit pattern of max |Z| over the fine
+//  window per sample (the column pass's epilogue reduction; the outputs may then be null).
 void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev,
                       uint64_t seed, uint32_t ell, uint64_t index0, int count, bool do_exp,
-                      double* out_fine, double* out_coarse, int* bad_flag);
+                      double* out_fine, double* out_coarse, int* bad_flag,
+                      unsigned long long* sup_out = nullptr);
 size_t ce_inter_bytes(const Level* L, int count, int col_stride);
 void upload_twiddles(Level* L);
 // Level setup on the device (ce_sample.cu): raw spectrum (s = (2(m+J))² entries, host vector) of
@@ -209,6 +216,8 @@ void upload_twiddles(Level* L);
 bool spectrum_device_supported(int family, double nu_or_p);
 std::vector<double> spectrum_device(Ctx* ctx, int m, int J, int family, double sigma2, double lambda,
                                     double nu_or_p);
+void spectrum_device_into(Ctx* ctx, int m, int J, int family, double sigma2, double lambda, double nu_or_p,
+                          double* eig_dev);
 
 // Batched MG-PCG (mgpcg.cu). k (device, B*(m+1)^2) is consumed as level-0 conductivity.
 void solver_prepare(Ctx* ctx, int m, int B, int hist_cap);

@@ -219,9 +219,11 @@ std::vector<double> build_spectrum(int m, int family, double sigma2, double lamb
                              [&](int J) { return spectrum(first_row(m, J, mod), 2 * (m + J)); });
 }
 
-std::vector<double> build_spectrum_with(int m, int family, double sigma2, double lambda, double nu_or_p,
-                                        const double* fractions, int n_fractions, double tol_factor, int* J_out,
-                                        const std::function<std::vector<double>(int)>& attempt_spectrum) {
+// The padding schedule of build_operator (embedding.cpp:114-151): J = 0, then ceil(f·m) per fraction,
+// until the spectrum's minimum is ≥ −tol. `attempt_min(J)` builds the padding-J spectrum wherever it
+// lives (host vector, device buffer) and returns its smallest eigenvalue; the accepted J is returned.
+int padding_schedule(int m, int family, double sigma2, double lambda, double nu_or_p, const double* fractions,
+                     int n_fractions, double tol_factor, const std::function<double(int)>& attempt_min) {
   if (m < 1) throw SetupError{OSC_ERR_CONFIG, "GridSpec: resolution must be >= 1"};
   if (!(sigma2 > 0.0) || !std::isfinite(sigma2))
     throw SetupError{OSC_ERR_CONFIG, "CovarianceModel: sigma2 must be positive"};
@@ -237,28 +239,22 @@ std::vector<double> build_spectrum_with(int m, int family, double sigma2, double
   }
   if (!(tol_factor > 0.0)) tol_factor = 1e-12;
   std::ostringstream tried;
-  auto attempt = [&](int J) -> std::vector<double> {
+  auto attempt = [&](int J) -> bool {
     const int n = 2 * (m + J);
     if ((int64_t)n * n > (int64_t{1} << 28))
       throw SetupError{OSC_ERR_CONFIG, "build_first_row: embedding size exceeds the addressable limit"};
-    auto eig = attempt_spectrum(J);
-    const double tol = tol_factor * static_cast<double>(eig.size()) * sigma2;
-    const double mn = *std::min_element(eig.begin(), eig.end());
+    const double mn = attempt_min(J);
+    const double tol = tol_factor * static_cast<double>((int64_t)n * n) * sigma2;
     tried << " J=" << J << "," << J << " (min eig " << mn << ")";
-    if (mn < -tol) return {};
-    for (double& v : eig)
-      if (v < 0.0) v = 0.0;
-    return eig;
+    return !(mn < -tol);
   };
   int J = 0;
-  auto eig = attempt(0);
-  if (eig.empty()) {
-    for (int i = 0; i < n_fractions && eig.empty(); ++i) {
-      J = static_cast<int>(std::ceil(fractions[i] * m));
-      eig = attempt(J);
-    }
+  bool ok = attempt(0);
+  for (int i = 0; i < n_fractions && !ok; ++i) {
+    J = static_cast<int>(std::ceil(fractions[i] * m));
+    ok = attempt(J);
   }
-  if (eig.empty()) {
+  if (!ok) {
     std::ostringstream os;
     os << "build_operator: no SPD embedding for "
        << (family == OSC_COV_MATERN ? "matern" : "exponential") << "(sigma2=" << sigma2
@@ -266,7 +262,19 @@ std::vector<double> build_spectrum_with(int m, int family, double sigma2, double
        << "); tried" << tried.str();
     throw SetupError{OSC_ERR_EMBEDDING, os.str()};
   }
-  *J_out = J;
+  return J;
+}
+
+std::vector<double> build_spectrum_with(int m, int family, double sigma2, double lambda, double nu_or_p,
+                                        const double* fractions, int n_fractions, double tol_factor, int* J_out,
+                                        const std::function<std::vector<double>(int)>& attempt_spectrum) {
+  std::vector<double> eig;
+  *J_out = padding_schedule(m, family, sigma2, lambda, nu_or_p, fractions, n_fractions, tol_factor, [&](int J) {
+    eig = attempt_spectrum(J);
+    return *std::min_element(eig.begin(), eig.end());
+  });
+  for (double& v : eig)
+    if (v < 0.0) v = 0.0;
   return eig;
 }
 

@@ -7,4 +7,4 @@ root="$(cd "$(dirname "$0")/.." && pwd)"
 mkdir -p "$root/ab"
 cd "$src"
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -O3 -shared \
-  -I"$root/include" "$@" -o "$root/ab/$out" csrc/capi.cu csrc/ce_sample.cu csrc/mgpcg.cu csrc/setup.cpp
+  -I"$root/include" "$@" -o "$root/ab/$out" csrc/capi.cu csrc/ce_sample.cu csrc/mgpcg.cu csrc/level_setup.cu csrc/setup.cpp csrc/group.cpp -ldl -lpthread

@@ -1,0 +1,55 @@
+# Round measurement set (gpurun -- 'bash scripts/measure.sh TAG [parts]'); outputs in gpurun_out/.
+# parts: any of  tests bench ref cfgs mlmc launches ncu   (default: all)
+TAG=${1:-x}; PARTS=${2:-"tests bench ref cfgs mlmc launches ncu"}  # + cesplit
+O=gpurun_out
+has() { case " $PARTS " in *" $1 "*) return 0;; esac; return 1; }
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv
+if has tests; then
+  timeout 3000 python -m pytest tests -m gpu -q -rfE -p no:cacheprovider > $O/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
+  tail -4 $O/${TAG}_pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+fi
+if has bench; then
+  timeout 1200 python bench.py > $O/${TAG}_cfg4.json 2> $O/${TAG}_cfg4.err; echo "bench rc=$?"
+  python - <<PY
+import json; d=json.load(open('$O/${TAG}_cfg4.json')); print(d['value'], d['e2e'], d['roofline'], d['pipeline_roofline']['frac'], d['cpu_baseline'], d['gpu_launches'], d['clocks'])
+PY
+fi
+if has ref; then
+  timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/${TAG}_ref.json 2> $O/${TAG}_ref.err; echo "ref rc=$?"; cat $O/${TAG}_ref.json
+fi
+if has cfgs; then
+  for c in 1 2 3; do
+    timeout 900 python bench.py --config $c --steps 3 --warmup 3 > $O/${TAG}_c$c.json 2> $O/${TAG}_c$c.err; echo "c$c rc=$?"
+    python - <<PY
+import json; d=json.load(open('$O/${TAG}_c$c.json')); print(d['value'], (d.get('e2e') or {}).get('value'), d['pipeline_roofline']['frac'], (d.get('cpu_baseline') or {}).get('value'), d['roofline'].get('kernel'), d['roofline'].get('frac'), d.get('per_level'))
+PY
+  done
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/${TAG}_torchrun.json 2> $O/${TAG}_torchrun.err; echo "torchrun rc=$?"; head -c 300 $O/${TAG}_torchrun.json; echo
+fi
+if has mlmc; then
+  timeout 900 python bench.py --config 3 --mlmc > $O/${TAG}_mlmc.json 2> $O/${TAG}_mlmc.err; echo "mlmc rc=$?"; head -c 800 $O/${TAG}_mlmc.json; echo
+fi
+CMD="python bench.py --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-e2e"
+if has launches; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/${TAG}_cfg4_launches.csv $CMD > $O/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+fi
+if has ncu; then
+  # --set full captures of the top kernels (batch 8). The coarse 1024^2 solve runs first (~15 V-cycles),
+  # so the launches are skipped past it and a few consecutive ones are kept: the summary keeps the
+  # largest grid (level 0 / level 1 of the 2048^2 solve)
+  for spec in "pcg_update_cg_kernel 20 2" "smooth_up_ring_kernel 20 2" "restrict_ring_kernel 20 2" "c_up_ring_kernel 70 6" "c_down_ring_kernel 70 6" "galerkin_tile_kernel 0 8"; do
+    set -- $spec
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 -o $O/${TAG}_$1 $CMD > $O/${TAG}_ncu_$1.log 2>&1; tail -1 $O/${TAG}_ncu_$1.log
+    python scripts/ncu_summary.py $O/${TAG}_$1.ncu-rep 14 > $O/${TAG}_$1_ncu.txt 2>&1
+    [ -n "$KEEP_REP" ] || rm -f $O/${TAG}_$1.ncu-rep   # gpurun_out/ returns at most 64 MiB
+  done
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:ce_ -c 2 -o $O/${TAG}_ce python bench.py --config 2 --batch 32 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/${TAG}_ncu_ce.log 2>&1; tail -1 $O/${TAG}_ncu_ce.log
+  python scripts/ncu_summary.py $O/${TAG}_ce.ncu-rep 14 > $O/${TAG}_ce_ncu.txt 2>&1
+  python scripts/ncu_stalls.py $O/${TAG}_ce.ncu-rep > $O/${TAG}_ce_stalls.txt 2>&1
+  [ -n "$KEEP_REP" ] || rm -f $O/${TAG}_ce.ncu-rep
+fi
+if has cesplit; then
+  timeout 600 python scripts/ce_split.py > $O/${TAG}_ce_split.json 2> $O/${TAG}_ce_split.err; echo "ce_split rc=$?"; cat $O/${TAG}_ce_split.json
+fi
+ls -la $O | tail -40

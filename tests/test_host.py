@@ -72,6 +72,26 @@ def test_osc1_roundtrip(P, tmp_path, golden):
     assert op2.padding == (8, 8) and np.array_equal(op2.eigenvalues, op.eigenvalues)
 
 
+def test_osc1_c_abi_errors_and_reference_reads_ours(P, ref, tmp_path, golden):
+    """osc_spectrum_save / osc_spectrum_load (embedding.cpp:262-294): the pristine reference loads
+    our dump bit for bit; bad magic, inconsistent headers and truncated files are ConfigErrors."""
+    api = P.api
+    op = api.EmbeddingOperator(api.GridSpec.square(16), 8, golden["eig_matern_m16_nu15_pad"], 1.0)
+    p = str(tmp_path / "ours.osc1")
+    api.save_spectrum(op, p)
+    r = ref.load_spectrum(p, 1.0)
+    assert r.J == 8 and np.array_equal(r.eigenvalues(), op.eigenvalues)
+    raw = open(p, "rb").read()
+    for name, data in (("magic", b"OSC2" + raw[4:]), ("short", raw[:-8]),
+                       ("header", raw[:8] + (17).to_bytes(4, "little") + raw[12:])):
+        q = str(tmp_path / f"bad_{name}.osc1")
+        open(q, "wb").write(data)
+        with pytest.raises(api.ConfigError):
+            api.load_spectrum(q, 1.0)
+    with pytest.raises(api.ConfigError):
+        api.load_spectrum(str(tmp_path / "missing.osc1"), 1.0)
+
+
 def test_osc1_reads_reference_dump(P, ref, tmp_path):
     api = P.api
     r = ref.build_operator(16, 0, 1.0, 0.3, 1.5)

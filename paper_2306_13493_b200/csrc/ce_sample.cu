@@ -18,10 +18,10 @@
 
 #include <algorithm>
 #include <cmath>
-#include <vector>
 #include <cstdlib>
+#include <type_traits>
+#include <vector>
 
-#include "fft_dif.cuh"
 #include "osc_device.cuh"
 #include "osc_internal.cuh"
 
@@ -171,25 +171,36 @@ struct FftPlan {
   static constexpr int THREADS = NT * T;
   static constexpr int NSTAGE8 = LOGN / 3;           // radix-8 stages
   static constexpr int REM = LOGN % 3;               // log2 of the final radix (0: none)
-  static constexpr int LD = n + (n >> 3) + 1;        // padded transform stride (fpad_len)
+  // padded transform stride (≥ fpad_len); from T ≥ 32 on transforms sit in different warps and the
+  // stride only matters to the row pass's unpack, where two transforms' Z[p], Z[p+1] must fall in four
+  // different 16-byte bank groups (stride ≡ 2 mod 8)
+  static constexpr int LD = n + (n >> 3) + (LOGN >= 8 ? 2 : 1);
   static constexpr int MINB = THREADS >= 1024 ? 1 : (1024 / THREADS < 32 ? 1024 / THREADS : 32);  // ≤ 64 regs
+  // Row pass: at least two row pairs (four rows) per CTA wherever 1024 threads allow, so that the
+  // unpack writes whole 128-byte lines of the intermediate (4 rows × 2 interleaved columns × 16 B)
+  static constexpr int NTR = T >= 1024 ? 1 : (T >= 256 ? 2 : NT);
 };
 
-// Twiddles of one Stockham stage (radix R, sub-length 2^LNS) for this thread's G = 8/R butterflies.
+// Twiddles of one Stockham stage (radix R, sub-length Ns = 2^LNS) for this thread's G = 8/R butterflies.
 // They do not depend on the data, so each stage loads them BEFORE the barrier that publishes the
 // previous stage's outputs: the L1 latency overlaps the barrier wait.
+// They come from the level's per-stage tables (upload_twiddles): stage LNS keeps W^{rk} as
+// [r − 1][k], k < Ns, at offset 2^LNS − 8 behind the plain table, so the lanes of a warp (consecutive
+// k) read consecutive 16-byte entries — 1 to 4 L1 wavefronts per load. Indexing the plain table
+// tw[(r k) << TWS] spread a warp's load over up to 32 lines; with 7 loads per thread and stage the
+// twiddles took about as many L1/shared data-pipe cycles as the transform's own exchanges, and that
+// pipe — not issue, fp64 or HBM — bounds both passes.
 template <int LOGN, int R, int LNS>
 struct StageTw {
   double2 w[8 / R][R > 1 ? R - 1 : 1];
   __device__ __forceinline__ void load(int lt, const double2* __restrict__ tw) {
-    constexpr int T = (1 << LOGN) / 8, G = 8 / R;
-    constexpr int LR = R == 8 ? 3 : (R == 4 ? 2 : 1);
-    constexpr int TWS = LOGN - LNS - LR;  // twiddle step shift: k · n/(Ns·R)
+    constexpr int n = 1 << LOGN, T = n / 8, G = 8 / R, Ns = 1 << LNS;
+    const double2* st = tw + n + (Ns - 8);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int k = (lt + g * T) & ((1 << LNS) - 1);
+      const int k = (lt + g * T) & (Ns - 1);
 #pragma unroll
-      for (int r = 1; r < R; ++r) w[g][r - 1] = __ldg(&tw[(r * k) << TWS]);
+      for (int r = 1; r < R; ++r) w[g][r - 1] = __ldg(&st[(r - 1) * Ns + k]);
     }
   }
 };
@@ -317,37 +328,61 @@ __device__ __forceinline__ int64_t inter_pair_idx(int b, int Ph, int n, int p, i
 }
 __host__ __device__ __forceinline__ int inter_groups(int P) { return (P + CE_IL - 1) / CE_IL; }
 
-// Unpack the row pair's two half spectra (p0 = p·cs ≤ m) into the intermediate.
-template <int LOGN>
-__device__ __forceinline__ void rows_unpack(const double2* x, double2* __restrict__ inter, int b, int P, int cs,
-                                            int q1a, int lt) {
-  constexpr int n = 1 << LOGN, T = n / 8;
+// Unpack the CTA's NTR row pairs (rows 2·rp0 … 2·rp0 + 2·NTR − 1) into the intermediate. Row q1 = 2t + w
+// of transform t: X_a (w = 0) = (Z[p] + conj Z[−p]) / 2, X_b (w = 1) = (Z[p] − conj Z[−p]) / (2i).
+// NTR ≥ 2: one 16-byte value per thread and step in address order (interleaved column p & 1 fastest,
+// then the row, then the column pair), so a warp's store covers whole 128-byte lines (four rows × one
+// column pair) instead of 16 scattered 32-byte sectors — the stores took a quarter of the pass's L1
+// data-pipe cycles. NTR = 1: both rows of the pair per thread (half lines).
+template <int LOGN, int NTR>
+__device__ __forceinline__ void rows_unpack(const double2* smem, double2* __restrict__ inter, int b, int P, int cs,
+                                            int rp0) {
+  using PL = FftPlan<LOGN>;
+  constexpr int n = PL::n, ROWS = 2 * NTR, THREADS = NTR * PL::T;
   const int Ph = inter_groups(P);
-  for (int p = lt; p < P; p += T) {
-    const int p0 = p * cs;
-    const double2 zp = x[fpad(p0)];
-    const double2 zm = x[fpad((n - p0) & (n - 1))];
-    // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
-    double2* o = inter + inter_pair_idx(b, Ph, n, p, q1a);
-    o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-    o[CE_IL] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));  // row q1a + 1
+  if constexpr (NTR == 1) {
+    for (int p = threadIdx.x; p < P; p += THREADS) {
+      const int p0 = p * cs;
+      const double2 zp = smem[fpad(p0)];
+      const double2 zm = smem[fpad((n - p0) & (n - 1))];
+      double2* o = inter + inter_pair_idx(b, Ph, n, p, 2 * rp0);
+      o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+      o[CE_IL] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));  // row 2·rp0 + 1
+    }
+  } else {
+    const int items = CE_IL * ROWS * Ph;
+    for (int idx = threadIdx.x; idx < items; idx += THREADS) {
+      const int pl = idx % CE_IL, q1l = (idx / CE_IL) % ROWS, pp = idx / (CE_IL * ROWS);
+      const int p = CE_IL * pp + pl;
+      if (p >= P) continue;
+      const int p0 = p * cs;
+      const double2* x = smem + (q1l >> 1) * PL::LD;
+      const double2 zp = x[fpad(p0)];
+      const double2 zm = x[fpad((n - p0) & (n - 1))];
+      const double2 o = (q1l & 1) ? make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x))
+                                  : make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
+      inter[inter_pair_idx(b, Ph, n, p, 2 * rp0 + q1l)] = o;
+    }
   }
 }
 
-template <int LOGN>
-__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) ce_rows_t_kernel(
+// NTR row pairs per CTA. Resident ξ (a memory-bound pass) runs FftPlan::NTR ≥ 2 pairs for the whole-line
+// stores; the device-Philox draw is issue-heavy and overlaps better across many small CTAs, so it
+// keeps the column pass's transforms-per-CTA (measured at n = 2048: Philox 23.5 vs 25.5 µs per sample
+// with 1 vs 2 pairs, resident ξ 20.4 vs 18.3).
+template <int LOGN, int NTR>
+__global__ void __launch_bounds__(NTR * FftPlan<LOGN>::T, (1024 / (NTR * FftPlan<LOGN>::T) < 32 ? (1024 / (NTR * FftPlan<LOGN>::T) < 1 ? 1 : 1024 / (NTR * FftPlan<LOGN>::T)) : 32)) ce_rows_t_kernel(
     const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
     uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
   using PL = FftPlan<LOGN>;
-  constexpr int n = PL::n, T = PL::T;
+  constexpr int T = PL::T;
   extern __shared__ double2 smem[];
   const int t = threadIdx.x / T;  // transform slot in this CTA
   const int lt = threadIdx.x % T;
-  const int rp = blockIdx.x * PL::NT + t;  // row pair (n/2 is a multiple of NT)
+  const int rp0 = blockIdx.x * NTR;  // first row pair of the CTA (n/2 is a multiple of NTR)
   const int b = blockIdx.y;
-  const int q1a = 2 * rp, q1b = 2 * rp + 1;
+  const int q1a = 2 * (rp0 + t);
   double2* x = smem + t * PL::LD;
-  const int64_t s = (int64_t)n * n;
   double2 v[8];
   rows_operands<LOGN>(sqrt_lam, xi, philox_keys(seed), ell, index0 + (uint64_t)b, b, q1a, lt, v);
   first_stage_store<LOGN>(x, lt, v);
@@ -363,7 +398,7 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) c
     stage_store<LOGN, LS::R, LS::LNS>(x, lt, w);
     __syncthreads();
   }
-  rows_unpack<LOGN>(x, inter, b, P, cs, q1a, lt);
+  rows_unpack<LOGN, NTR>(smem, inter, b, P, cs, rp0);
 }
 
 template <int LOGN>
@@ -417,6 +452,11 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) c
     }
   if (bad && bad_flag) atomicOr(bad_flag + b, 1);
   if (sup) sup_commit(vmax, sup + b);
+}
+
+// 32 aligned bytes (two adjacent complex values) through the read-only path in one instruction
+__device__ __forceinline__ void ldg256(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
 }
 
 // Column pass with two columns per thread (32 ≤ n ≤ 4096; ce_cols_t_kernel below and above): the same stages as ce_cols_t_kernel
@@ -486,12 +526,15 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
   {
     double2 v0[8], v1[8];
     const bool ok0 = j0 < P, ok1 = j0 + 1 < P;
-    // columns j0 (even) and j0 + 1 sit side by side: one 32-byte run per q1
+    // columns j0 (even) and j0 + 1 sit side by side: one aligned 32-byte run per q1, read by one
+    // 256-bit load (column j0 + 1 of an odd P is allocated but never written: its values are dropped)
     const double2* s0 = inter + inter_pair_idx(b, inter_groups(P), n, ok0 ? j0 : 0, lt);
+    static_assert(CE_IL == 2, "the 256-bit load reads one interleaved column pair");
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      v0[r] = ok0 ? __ldg(s0 + CE_IL * r * T) : make_double2(0.0, 0.0);
-      v1[r] = ok1 ? __ldg(s0 + CE_IL * r * T + 1) : make_double2(0.0, 0.0);
+      ldg256(s0 + CE_IL * r * T, v0[r], v1[r]);
+      if (!ok0) v0[r] = make_double2(0.0, 0.0);
+      if (!ok1) v1[r] = make_double2(0.0, 0.0);
     }
     first_stage_store<LOGN>(x0, lt, v0);
     first_stage_store<LOGN>(x1, lt, v1);
@@ -532,109 +575,6 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
   if (sup) sup_commit(vmax, sup + b);
 }
 
-// ---- group-local DIF passes (fft_dif.cuh) -------------------------------------------------------------
-// Same operands, intermediate layout and epilogues as the Stockham passes above; the transform is the
-// radix-8 DIF whose exchanges after the first are warp-local.
-template <int LOGN>
-struct DifPlan {
-  using PL = FftPlan<LOGN>;
-  static constexpr int LD_ROWS = (npad<LOGN>(PL::n - 1) + 1 > PL::LD ? npad<LOGN>(PL::n - 1) + 1 : PL::LD) | 1;
-};
-
-template <int LOGN>
-__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) ce_rows_d_kernel(
-    const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
-    uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
-  using PL = FftPlan<LOGN>;
-  constexpr int n = PL::n, T = PL::T;
-  extern __shared__ double2 smem[];
-  const int t = threadIdx.x / T;  // transform slot in this CTA
-  const int lt = threadIdx.x % T;
-  const int rp = blockIdx.x * PL::NT + t;  // row pair (n/2 is a multiple of NT)
-  const int b = blockIdx.y;
-  const int q1a = 2 * rp;
-  double2* x[1] = {smem + t * DifPlan<LOGN>::LD_ROWS};
-  double2 v[1][8];
-  rows_operands<LOGN>(sqrt_lam, xi, philox_keys(seed), ell, index0 + (uint64_t)b, b, q1a, lt, v[0]);
-  struct Sink {
-    double2 o[8];
-    int p[8];
-    int i = 0;
-    __device__ __forceinline__ void operator()(int, int pp, double2 val) {
-      o[i] = val;
-      p[i] = pp;
-      ++i;
-    }
-  } sink;
-  fft_dif<LOGN, 1, PL::THREADS>(v, x, lt, tw, sink);
-  // natural order for the unpack (Z[p] pairs with Z[n − p]): every read of the exchanges is done first
-  dif_gsync<T, PL::THREADS>();
-#pragma unroll
-  for (int i = 0; i < 8; ++i) x[0][npad<LOGN>(sink.p[i])] = sink.o[i];
-  dif_gsync<T, PL::THREADS>();
-  const int Ph = inter_groups(P);
-  for (int p = lt; p < P; p += T) {
-    const int p0 = p * cs;
-    const double2 zp = x[0][npad<LOGN>(p0)];
-    const double2 zm = x[0][npad<LOGN>((n - p0) & (n - 1))];
-    // X_a = (Z[p] + conj Z[-p]) / 2,  X_b = (Z[p] - conj Z[-p]) / (2i)
-    double2* o = inter + inter_pair_idx(b, Ph, n, p, q1a);
-    o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-    o[CE_IL] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));  // row q1a + 1
-  }
-}
-
-// Column pass, NC columns per thread (NC = 2: columns j0, j0 + 1 side by side in the intermediate).
-template <int LOGN, int NC>
-__global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, NC == 2 ? Cols2Plan<LOGN>::MINB : FftPlan<LOGN>::MINB)
-    ce_cols_d_kernel(const double2* __restrict__ inter, int m, int P, int cs, double inv_n, int do_exp,
-                     const double2* __restrict__ tw, double* __restrict__ out_fine, double* __restrict__ out_coarse,
-                     int* __restrict__ bad_flag, unsigned long long* __restrict__ sup) {
-  using PL = FftPlan<LOGN>;
-  constexpr int n = PL::n, T = PL::T;
-  extern __shared__ double2 smem[];
-  const int t = threadIdx.x / T;
-  const int lt = threadIdx.x % T;
-  const int b = blockIdx.y;
-  const int j0 = NC * (blockIdx.x * PL::NT + t);  // columns j0 … j0 + NC − 1
-  double2* x[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) x[c] = smem + (NC * t + c) * PL::LD;
-  double2 v[NC][8];
-  {
-    const double2* s0 = inter + inter_pair_idx(b, inter_groups(P), n, j0 < P ? j0 : 0, lt);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const bool ok = j0 + c < P;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) v[c][r] = ok ? __ldg(s0 + CE_IL * r * T + c) : make_double2(0.0, 0.0);
-    }
-  }
-  const int mf = m + 1, mc = m / 2 + 1;
-  struct Sink {
-    double* of;
-    double* oc;
-    int j0, P, m, cs, mf, mc, do_exp, bad;
-    double inv_n, vmax;
-    __device__ __forceinline__ void operator()(int c, int p1, double2 val) {
-      const int j = j0 + c;
-      if (j >= P || p1 > m || (p1 & (cs - 1))) return;
-      const int p0 = j * cs;
-      const double zval = (val.x + val.y) * inv_n;
-      if (!isfinite(zval)) bad = 1;
-      vmax = fmax(vmax, fabs(zval));
-      const double o = do_exp ? exp(zval) : zval;
-      if (of) of[(int64_t)p1 * mf + p0] = o;
-      if (oc && ((p0 | p1) & 1) == 0) oc[(int64_t)(p1 >> 1) * mc + (p0 >> 1)] = o;
-    }
-  } sink{out_fine ? out_fine + (int64_t)b * mf * mf : nullptr,
-         out_coarse ? out_coarse + (int64_t)b * mc * mc : nullptr,
-         j0, P, m, cs, mf, mc, do_exp, 0, inv_n, 0.0};
-  fft_dif<LOGN, NC, PL::THREADS>(v, x, lt, tw, sink);
-  if (sink.bad && bad_flag) atomicOr(bad_flag + b, 1);
-  if (sup) sup_commit(sink.vmax, sup + b);
-}
-
 template <int LOGN>
 void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi_dev, uint64_t seed,
               uint32_t ell, uint64_t index0, int count, bool do_exp, double* out_fine, double* out_coarse,
@@ -644,40 +584,18 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = sizeof(double2) * (size_t)PL::NT * PL::LD;
   cudaStream_t st = ctx->stream;
-  static const bool dif = [] { const char* e = std::getenv("OSC_CE_DIF"); return !e || std::atoi(e) != 0; }();
-  if (dif) {
-    {
-      const size_t smr = sizeof(double2) * (size_t)PL::NT * DifPlan<LOGN>::LD_ROWS;
-      auto kern = ce_rows_d_kernel<LOGN>;
-      smem_attr(kern, smr);
-      KScope ks(ctx, "ce_rows");
-      kern<<<dim3((PL::n / 2) / PL::NT, count), PL::THREADS, smr, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs,
-                                                                         tw, inter);
-      OSC_CUDA(cudaGetLastError());
-    }
-    KScope ks(ctx, "ce_cols");
-    if constexpr (LOGN >= 5 && LOGN <= 12) {
-      auto kern = ce_cols_d_kernel<LOGN, 2>;
-      smem_attr(kern, (2 * sm));
-      kern<<<dim3((P + 2 * PL::NT - 1) / (2 * PL::NT), count), PL::THREADS, 2 * sm, st>>>(
-          inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag, sup);
-    } else {
-      auto kern = ce_cols_d_kernel<LOGN, 1>;
-      smem_attr(kern, sm);
-      kern<<<dim3((P + PL::NT - 1) / PL::NT, count), PL::THREADS, sm, st>>>(
-          inter, m, P, cs, 1.0 / PL::n, do_exp ? 1 : 0, tw, out_fine, out_coarse, bad_flag, sup);
-    }
-    OSC_CUDA(cudaGetLastError());
-    return;
-  }
-  {
-    auto kern = ce_rows_t_kernel<LOGN>;
-    smem_attr(kern, sm);
+  auto rows = [&](auto ntr) {
+    constexpr int NTR = decltype(ntr)::value;
+    const size_t smr = sizeof(double2) * (size_t)NTR * PL::LD;
+    auto kern = ce_rows_t_kernel<LOGN, NTR>;
+    smem_attr(kern, smr);
     KScope ks(ctx, "ce_rows");
-    kern<<<dim3((PL::n / 2) / PL::NT, count), PL::THREADS, sm, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs,
-                                                                      tw, inter);
+    kern<<<dim3((PL::n / 2) / NTR, count), NTR * PL::T, smr, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs, tw,
+                                                                    inter);
     OSC_CUDA(cudaGetLastError());
-  }
+  };
+  if (xi_dev) rows(std::integral_constant<int, PL::NTR>{});
+  else rows(std::integral_constant<int, PL::NT>{});
   // two columns per thread for 32 ≤ n ≤ 4096, where it fits 128 registers without spills (config 2
   // column pass 277.7 → 208.6 ms per 12288 samples against one column per thread)
   if constexpr (LOGN >= 5 && LOGN <= 12) {
@@ -1067,13 +985,30 @@ __global__ void fill_kernel(double* __restrict__ p, int64_t count, double v) {
 }
 }  // namespace
 
-// Twiddle table tw[t] = exp(+2πi t/n) of a level (long-double angles, rounded once).
+// Twiddle tables of a level (long-double angles, rounded once): the plain table tw[t] = exp(+2πi t/n),
+// t < n, followed for n = 2^LOGN ≥ 16 by the per-stage tables of the compile-time-n passes — the
+// stage with sub-length Ns = 2^LNS (LNS = 3, 6, …) and radix R holds W_{Ns R}^{r k} = tw[r k n/(Ns R)]
+// as [r − 1][k] at offset Ns − 8 (the same doubles as the plain table, so results do not change).
 void upload_twiddles(Level* L) {
-  std::vector<double> tw(2 * (size_t)L->n);
-  for (int t = 0; t < L->n; ++t) {
-    const long double a = 6.283185307179586476925286766559005768L * t / L->n;
-    tw[2 * (size_t)t] = (double)std::cos(a);
-    tw[2 * (size_t)t + 1] = (double)std::sin(a);
+  const int n = L->n;
+  const bool staged = n >= 16 && (n & (n - 1)) == 0;
+  std::vector<double> tw(2 * (size_t)n * (staged ? 2 : 1), 0.0);
+  auto put = [&](size_t slot, int64_t t) {
+    const long double a = 6.283185307179586476925286766559005768L * t / n;
+    tw[2 * slot] = (double)std::cos(a);
+    tw[2 * slot + 1] = (double)std::sin(a);
+  };
+  for (int t = 0; t < n; ++t) put((size_t)t, t);
+  if (staged) {
+    const int logn = 31 - __builtin_clz((unsigned)n);
+    const int nst8 = logn / 3, rem = logn % 3;
+    const int last_lns = rem ? 3 * nst8 : 3 * (nst8 - 1);
+    for (int lns = 3; lns <= last_lns; lns += 3) {
+      const int Ns = 1 << lns;
+      const int R = lns < last_lns ? 8 : (rem ? (1 << rem) : 8);
+      for (int r = 1; r < R; ++r)
+        for (int k = 0; k < Ns; ++k) put((size_t)n + (Ns - 8) + (size_t)(r - 1) * Ns + k, (int64_t)r * k * (n / (Ns * R)));
+    }
   }
   L->twiddle.ensure(sizeof(double) * tw.size());
   OSC_CUDA(cudaMemcpy(L->twiddle.p, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));

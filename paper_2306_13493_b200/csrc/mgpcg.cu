@@ -825,27 +825,12 @@ __device__ __forceinline__ Pair ld2(const double* __restrict__ base, int xa, int
   return Pair{ldv<INT>(base, xa, y, n0), ldv<INT>(base, xa + 1, y, n0)};
 }
 
-// Level-0 search direction p and preconditioned residual z of the multilevel PCG are STORED in fp32
-// (computed in fp64): u += αp and r −= αAp use the same fp64 p recomputed from the stored values by
-// every lane that needs it, so r stays the residual of u to fp64 rounding whatever the direction is;
-// the 2⁻²⁴ rounding only perturbs the next direction (an inexact preconditioner), not the fixed
-// point. 16 B/node less per iteration (pcg_update 64 → 52, up sweep 30 → 26).
-#ifdef OSC_PZ64
+// Storage type of the level-0 search direction p and preconditioned residual z. fp32 storage (fp64
+// arithmetic; u and r keep using one fp64 p, so r stays the residual of u) was measured: same
+// iteration counts (14.11 / 14.10 on config 4) and the same time per pcg_update launch — the kernel is
+// bound by load/store instructions in flight, not by DRAM bytes — so they stay fp64
+// (profiles/ab_r2/pz32_vs_pz64.txt).
 using pz_t = double;
-#else
-using pz_t = float;
-#endif
-template <bool INT>
-__device__ __forceinline__ Pair ld2(const float* __restrict__ base, int xa, int y, int n0) {
-  if (INT) {
-    const float* q = base + (int64_t)y * n0 + xa;
-    return Pair{(double)__ldg(q), (double)__ldg(q + 1)};
-  }
-  const bool yok = (unsigned)y < (unsigned)n0;
-  const float* q = base + (int64_t)y * n0 + xa;
-  return Pair{(yok && (unsigned)xa < (unsigned)n0) ? (double)__ldg(q) : 0.0,
-              (yok && (unsigned)(xa + 1) < (unsigned)n0) ? (double)__ldg(q + 1) : 0.0};
-}
 
 // Edge weights of row y at both columns from k rows y−1, y, y+1. Triangle means in the
 // reference's vertex order with ·(1/3) instead of /3 (≤ 1 ulp per coefficient); each edge is

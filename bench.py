@@ -783,8 +783,9 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
     ach = per[dom] * args.steps * B / (dms / 1000.0) / 1e9 if dom in per else None
     roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
             "frac": ach / hbm if ach else None, "traffic": None, "peak_kind": hbm_kind,
-            "note": "algorithmic bytes count the half-spectrum round trip (1 GiB chunks: it spills to HBM, "
-                    "hidden under fp64 issue); the CE is bound by instruction issue, see compute_roofline"}
+            "note": "algorithmic bytes count the half-spectrum round trip (1 GiB chunks: it spills to HBM); both "
+                    "passes are bound by the SM's L1/shared-memory data pipe (71-76% busy: the radix-8 exchanges "
+                    "through shared memory plus the scattered 8/16-byte stores), profiles/r2e_ce_stalls_staged_twiddles.txt"}
     # fp64 view: conventional FFT flops 5·n·log2(n) per length-n complex transform, n/2 row and P column
     # transforms per sample (Box-Muller log/sqrt/sincos and the exp() are not counted), against the
     # measured DFMA peak (profiles/r1_fp64_peak.json, scripts/micro/fp64bench.cu)
@@ -794,14 +795,40 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
                     "achieved": fft_flops * value / world / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": fft_flops * value / world / 1e12 / fp64_peak,
                     "peak_source": "profiles/r1_fp64_peak.json (DFMA chains, 148 SMs, 1965 MHz)",
-                    "ncu": "profiles/r1_ce_rows_t_ncu.txt / r1_ce_cols2_t_ncu.txt: fp64 pipe 35% / 23% busy, "
-                           "issue 52% / 25% of peak (latency-bound on shared-memory exchanges and "
-                           "Box-Muller dependency chains)"}
+                    "ncu": "profiles/r2e_ce_stalls_staged_twiddles.txt: fp64 pipe 49% (rows) busy, issue 62% / 36%"}
     b_sample = algorithmic_bytes_per_sample(dict(W, coupled=False, it=(0, 0)), n) - 8 * Nf * 0
     b_sample = 8 * n * n / B + 32 * n * (n // 2 + 1) + 8 * Nf  # SURVEY §8(d) B_ce, device ξ
     pipeline = {"basis": "SURVEY 8(d) B_ce (device xi)", "bytes_per_sample": b_sample,
                 "roofline_samples_per_s_per_gpu": hbm * 1e9 / b_sample,
                 "frac": value / world / (hbm * 1e9 / b_sample)}
+    # The same pass on ξ resident in HBM (the parity mode of north_star: identical seeded Gaussian
+    # vectors fed to both implementations): a ring of 64 distinct rows (2.1 GB at n = 2048, far above
+    # L2), 64-sample calls; bytes per sample add the 8 s of ξ read
+    xi_res = None
+    if world == 1:
+        R = 64
+        g = torch.Generator(device=f"cuda:{local}")
+        g.manual_seed(1)
+        ring = torch.randn((R, lev.s), dtype=torch.float64, device=f"cuda:{local}", generator=g)
+        fl = flags | L.CE_XI_DEVICE
+
+        def xi_step():
+            for c0 in range(0, B, R):
+                api._check(lib.osc_ce_sample(lev.h, ring.data_ptr(), 1, W["ell"], 0, min(R, B - c0), fl,
+                                             out[c0:].data_ptr(), None))
+        xi_step()
+        ctx.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        xi_step()
+        g1.record(stream)
+        ctx.synchronize()
+        xms = g0.elapsed_time(g1)
+        bx = 8 * n * n + 32 * n * (n // 2 + 1) + 8 * Nf
+        xi_res = {"value": B / (xms / 1000.0), "unit": "samples/s", "bytes_per_sample": bx,
+                  "roofline_samples_per_s": hbm * 1e9 / bx, "frac": B / (xms / 1000.0) / (hbm * 1e9 / bx),
+                  "xi": "ring of 64 rows of torch.randn (seed 1) in HBM, 64-sample calls"}
+        del ring
     # e2e: host ξ in (pinned pool), fields out to pinned host memory, 64-sample calls
     e2e = None
     if not args.no_e2e:
@@ -846,7 +873,8 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic: device Philox NormalStream(1, 0, i)",
             "config": {"workload": W["name"], "global_batch": B * world, "embedding_n": n,
                        "l2": "fields written (34 GB/step) exceed L2", "setup_s": round(t_setup, 2)},
-            "roofline": roof, "compute_roofline": compute_roof, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "compute_roofline": compute_roof, "pipeline_roofline": pipeline,
+            "resident_xi": xi_res, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": ck,
             "kernels_ms": {k: round(v[1], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])},
         }), flush=True)

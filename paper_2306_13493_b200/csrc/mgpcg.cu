@@ -662,6 +662,101 @@ __global__ void coarse_factor_kernel(L9 Lv, int B, double* __restrict__ chol, co
   }
 }
 
+// Coarsest grids above 1089 nodes (m = 2^j·c with odd c ≥ 33: the reference Cholesky-factors whatever
+// grid is left when m stops being even, fem.cpp:239,255-272): a banded Cholesky instead of the dense
+// inverse. The operator is a 9-point stencil, so its half-bandwidth is w = n0 + 1; L keeps that band,
+// Lb[i·(w+1) + d] = L(i, i − w + d), d = w the diagonal. One CTA (warp) per sample, right-looking: the
+// w + 1 rows a pivot touches sit in a shared-memory window that slides down the band.
+constexpr int kBandMaxM = 128;  // coarsest cells per side supported by the window ((w+1)² doubles of smem)
+__host__ __device__ inline size_t band_doubles(int n0) { return (size_t)n0 * n0 * (n0 + 2); }
+
+__global__ void __launch_bounds__(32) coarse_band_factor_kernel(L9 Lv, int B, double* __restrict__ band,
+                                                                const double* __restrict__ k0, int bc) {
+  extern __shared__ double win[];  // rows j … j + w of the band, row i in slot i mod (w+1)
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int n0 = Lv.n0, n = (int)Lv.Nn, w = n0 + 1, W1 = w + 1;
+  double* Lb = band + (int64_t)b * band_doubles(n0);
+  // lower band of row i into window slot (zeros outside the stencil)
+  auto load_row = [&](int i) {
+    double* row = win + (size_t)(i % W1) * W1;
+    for (int d = lane; d < W1; d += 32) row[d] = 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      const int y = i / n0, x = i - y * n0;
+      const S9 r = k0 ? row_k(k0 + (int64_t)b * n, n0, 1, Lv.m, bc, x, y) : row_s(Lv, (int64_t)b * n, x, y);
+      row[w] = r.c;
+      if (x > 0) row[w - 1] = r.w;
+      if (y > 0) {
+        row[w - n0] = r.s;
+        if (x + 1 < n0) row[w - n0 + 1] = r.se;
+        if (x > 0) row[w - n0 - 1] = r.sw;
+      }
+    }
+    __syncwarp();
+  };
+  for (int i = 0; i < min(n, W1); ++i) load_row(i);
+  for (int j = 0; j < n; ++j) {
+    double* rj = win + (size_t)(j % W1) * W1;
+    const double d = sqrt(rj[w]);
+    const double inv = 1.0 / d;
+    __syncwarp();
+    if (lane == 0) rj[w] = d;
+    const int cnt = min(w, n - 1 - j);
+    // column j below the diagonal: L(i, j) sits at slot w − (i − j) of row i
+    for (int t = lane; t < cnt; t += 32) win[(size_t)((j + 1 + t) % W1) * W1 + (w - 1 - t)] *= inv;
+    __syncwarp();
+    // trailing update A(i, q) −= L(i, j) L(q, j), j < q ≤ i ≤ j + cnt
+    for (int t1 = 0; t1 < cnt; ++t1) {
+      double* ri = win + (size_t)((j + 1 + t1) % W1) * W1;
+      const double lij = ri[w - 1 - t1];
+      if (lij != 0.0)
+        for (int t2 = lane; t2 <= t1; t2 += 32)
+          ri[w - (t1 - t2)] = fma(-lij, win[(size_t)((j + 1 + t2) % W1) * W1 + (w - 1 - t2)], ri[w - (t1 - t2)]);
+    }
+    __syncwarp();
+    // row j is final: write it out, then its slot takes row j + w + 1
+    for (int dd = lane; dd < W1; dd += 32) Lb[(int64_t)j * W1 + dd] = rj[dd];
+    __syncwarp();
+    if (j + W1 < n) load_row(j + W1);
+  }
+}
+
+// z = A⁻¹ r through the banded factor (fem.cpp:274-286): forward then backward substitution, one warp
+// per sample; a row's dot product over the band is spread over the lanes.
+__global__ void __launch_bounds__(32) coarse_band_solve_kernel(int n0, int B, const double* __restrict__ band,
+                                                               const double* __restrict__ r, double* __restrict__ z,
+                                                               const int* flags) {
+  extern __shared__ double y[];  // n doubles
+  const int b = blockIdx.x, lane = threadIdx.x;
+  if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
+  const int n = n0 * n0, w = n0 + 1, W1 = w + 1;
+  const double* Lb = band + (int64_t)b * band_doubles(n0);
+  const double* rb = r + (int64_t)b * n;
+  double* zb = z + (int64_t)b * n;
+  for (int i = 0; i < n; ++i) {  // L y = r
+    const double* row = Lb + (int64_t)i * W1;
+    double acc = 0.0;
+    for (int d = lane; d < w; d += 32) {
+      const int q = i - w + d;
+      if (q >= 0) acc = fma(row[d], y[q], acc);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[i] = (rb[i] - acc) / row[w];
+    __syncwarp();
+  }
+  for (int i = n - 1; i >= 0; --i) {  // Lᵀ z = y: column i of L below the diagonal is L(i + t, i), t ≤ w
+    double acc = 0.0;
+    for (int t = 1 + lane; t <= w; t += 32) {
+      const int q = i + t;
+      if (q < n) acc = fma(Lb[(int64_t)q * W1 + (w - t)], y[q], acc);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[i] = (y[i] - acc) / Lb[(int64_t)i * W1 + w];
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) zb[i] = y[i];
+}
+
 // ---- coarse levels (9-point): red-black GS V(1,1), one thread per node -------------------------------
 // Red = (x + y) even. Within a color the nodes update simultaneously (Jacobi for the same-color
 // diagonal neighbours), so every sweep is a parallel, deterministic pass; the V-cycle stays
@@ -2857,7 +2952,7 @@ size_t solver_bytes(int m, int B, int hist_cap) {
            (last ? 0 : 4 * mcl * mcl * B * sizeof(float)) + 5 * 256;
     ++lev;
     if (last) {
-      tot += 2 * N * N * B * sizeof(double);
+      tot += (N > 1089 ? band_doubles(g + 1) : 2 * N * N) * B * sizeof(double);
       if (lev == 1) tot += N * B * (sizeof(double) + 4 * sizeof(float)) + 5 * 256;  // single level: its rows
       break;
     }
@@ -2885,7 +2980,8 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   }
   w.nlev = nl;
   w.nc = (int)w.lev[nl - 1].N;
-  OSC_REQUIRE(w.nc <= 1089, "solve: coarsest multigrid grid too large (m must be 2^j * c, c <= 32)");
+  OSC_REQUIRE(w.nc <= 1089 || w.lev[nl - 1].m <= kBandMaxM,
+              "solve: coarsest multigrid grid too large (m must be 2^j * c, c <= 128)");
   w.max_parts = (int)std::max<int64_t>(tile_parts(m), nblocks(w.lev[0].N));
   w.mem.ensure(solver_bytes(m, B, hist_cap));
   char* p = static_cast<char*>(w.mem.p);
@@ -2917,7 +3013,7 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
   w.p0 = (double*)take(vb0);
   w.p1 = (double*)take(vb0);
   w.Ap = nullptr;
-  w.chol = (double*)take(sizeof(double) * 2 * (size_t)w.nc * w.nc * B);
+  w.chol = (double*)take(sizeof(double) * (w.nc > 1089 ? band_doubles(w.lev[nl - 1].m + 1) : 2 * (size_t)w.nc * w.nc) * B);
   w.scal = (double*)take(sizeof(double) * S_NSCAL * B);
   w.flags = (int*)take(sizeof(int) * F_NFLAGS * B);
   w.counter = (unsigned*)take(sizeof(unsigned) * B);
@@ -2951,6 +3047,20 @@ HierDev hier_of(const SolverWork& w, int l0) {
   return H;
 }
 
+// z = A⁻¹ r on the coarsest grid: the explicit inverse (≤ 1089 nodes) or the banded factor
+void coarsest_solve(Ctx* ctx, int B, const double* r, double* z) {
+  SolverWork& w = ctx->solver;
+  KScope ks(ctx, "mg_coarse_solve");
+  if (w.nc > 1089) {
+    const size_t sm = sizeof(double) * (size_t)w.nc;
+    smem_attr(coarse_band_solve_kernel, sm);
+    coarse_band_solve_kernel<<<B, 32, sm, ctx->stream>>>(w.lev[w.nlev - 1].m + 1, B, w.chol, r, z, w.flags);
+  } else {
+    coarse_solve_kernel<<<(B + 3) / 4, 128, 0, ctx->stream>>>(w.nc, B, w.chol, r, z, w.flags);
+  }
+  OSC_CUDA(cudaGetLastError());
+}
+
 // Preconditioner z = M r on level 0 (input w.r_cur, output lev[0].z2): V(1,1) with red-black GS.
 // Levels with a coarser level below run ring-staged sweeps: level 0 the restriction (pre-smoother
 // recomputed from r) and the up sweep (prolongation + post-smoother, fused with γ = ⟨r, z⟩ and
@@ -2962,10 +3072,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
   cudaStream_t st = ctx->stream;
   double2* part = reinterpret_cast<double2*>(w.partial);
   if (w.nlev == 1) {
-    {
-      KScope ks(ctx, "mg_coarse_solve");
-      coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, w.r_cur, w.lev[0].z2, w.flags);
-    }
+    coarsest_solve(ctx, B, w.r_cur, w.lev[0].z2);
     KScope ks(ctx, "pcg_dot_rz");
     dot_rz_kernel<<<dim3(nblocks(w.lev[0].N), 1, B), NT, 0, st>>>(geo_of(w.lev[0]), w.r_cur, w.lev[0].z2,
                                                                  w.scal, w.flags, part, w.max_parts, w.counter);
@@ -3005,8 +3112,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
                                                   w.flags);
   } else {
     const SolverLevel& C = w.lev[w.nlev - 1];
-    KScope ks(ctx, "mg_coarse_solve");
-    coarse_solve_kernel<<<(B + 3) / 4, 128, 0, st>>>(w.nc, B, w.chol, C.r, C.z2, w.flags);
+    coarsest_solve(ctx, B, C.r, C.z2);
   }
   // up
   for (int l = ls - 1; l >= 0; --l) {
@@ -3081,7 +3187,11 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
   KScope ks(ctx, "mg_setup.factor");
   const double* k_exact = w.nlev == 1 ? L0.k : nullptr;
   const SolverLevel& C = w.lev[w.nlev - 1];
-  if (w.nc <= 32)
+  if (w.nc > 1089) {
+    const size_t sm = sizeof(double) * (size_t)(C.m + 3) * (C.m + 3);
+    smem_attr(coarse_band_factor_kernel, sm);
+    coarse_band_factor_kernel<<<B, 32, sm, st>>>(l9_of(C), B, w.chol, k_exact, bc);
+  } else if (w.nc <= 32)
     coarse_factor_warp_kernel<<<(B + CF_WARPS - 1) / CF_WARPS, 32 * CF_WARPS, 0, st>>>(l9_of(C), B, w.chol, k_exact, bc);
   else
     coarse_factor_kernel<<<(B + 63) / 64, 64, 0, st>>>(l9_of(C), B, w.chol, k_exact, bc);

@@ -167,6 +167,32 @@ def test_solve_vs_oracle(P, ctx, port, m, bc, coarse_op):
             assert abs(q[b] - qo) <= QOI_TOL * max(abs(qo), 1e-12), (kind, b, q[b], qo)
 
 
+@pytest.mark.parametrize("m,bc", [(33, 0), (33, 1), (66, 0), (70, 1), (132, 0)])
+def test_solve_odd_coarsest_grids(P, ctx, port, m, bc):
+    """Grids whose coarsening stops above 1089 nodes (m = 2^j·c, odd c ≥ 33): the reference
+    Cholesky-factors whatever coarsest grid remains (fem.cpp:239,255-272); here a banded Cholesky takes
+    over from the dense inverse. m = 33 is a single level (exact solve: one PCG step), 66 and 132 stop
+    at 33, 70 at 35. QoIs against the port to 1e-7 (the port's dense factor limits the sizes)."""
+    api = P.api
+    rng = np.random.default_rng(m + 5 * bc)
+    Z = np.cumsum(np.cumsum(rng.standard_normal((2, m + 1, m + 1)) * 0.2, axis=1), axis=2)
+    Z = ((Z - Z.mean()) / Z.std()).reshape(2, -1)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1, 1), bc=api.BC(bc))
+    u, it, _ = api.assemble_and_solve(m, Z, prob, ctx=ctx)
+    if m == 33:
+        assert np.all(it <= 2)
+    for kind in (0, 1):
+        prob.qoi = api.QoiSpec(api.QoiKind(kind))
+        q = api.evaluate_qoi(m, u, prob, Z=Z, ctx=ctx)
+        for b in range(2):
+            uo, ito, rc, _ = port.solve(m, Z[b], bc=bc)
+            assert rc == 0
+            qo = port.qoi(m, uo, bc=bc, qoi=kind, Z=Z[b])
+            assert abs(q[b] - qo) <= QOI_TOL * max(abs(qo), 1e-12), (kind, b, q[b], qo)
+    with pytest.raises(api.ConfigError):  # coarsest 129² cells: beyond the banded window
+        api.assemble_and_solve(129, np.zeros((1, 130 * 130)), prob, ctx=ctx)
+
+
 @pytest.mark.parametrize("m", [32, 64, 256, 1024])
 def test_galerkin_fewer_iterations(P, ctx, port, m):
     """Rough Matérn ν=0.5 log-field (σ² = 2, as config 4):

@@ -154,7 +154,8 @@ int osc_build_spectrum(int m, int family, double sigma2, double lambda, double n
                        int* J_out, int64_t* s_out, double** eig_out);
 /* build_operator with the first row and the spectrum FFT on the device (same padding schedule,
  * SPD test, clamping and output contract as osc_build_spectrum). Separable exponential and
- * Matern nu = k + 1/2 (k <= 3, closed forms of covariance.cpp:53-62); other nu → OSC_ERR_CONFIG.
+ * Matern (covariance.cpp:53-62): closed forms for nu = k + 1/2 (k <= 3), a device K_nu (Temme's series /
+ * Steed's continued fraction + upward recurrence) for any other nu in (0, 64].
  * Eigenvalues agree with the host setup to rounding (~1e-15 of max λ); ties of equal λ may then
  * order differently in a truncation mask (use the host or OSC1 spectrum for mask parity). */
 int osc_build_spectrum_device(osc_ctx* ctx, int m, int family, double sigma2, double lambda, double nu_or_p,

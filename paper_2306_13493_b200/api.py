@@ -434,8 +434,8 @@ def build_operator(grid: GridSpec, model: CovarianceModel,
                    options: BuildOptions = BuildOptions(), *, device: bool = False,
                    ctx: Optional["Context"] = None) -> EmbeddingOperator:
     """build_operator (embedding.cpp:114-151): J = 0, then ceil(f·m) until SPD. device=True builds
-    the first row and the spectrum on the GPU (osc_build_spectrum_device; separable exponential
-    and Matérn ν = k + ½, k ≤ 3); the host C++ setup is the general path."""
+    the first row and the spectrum on the GPU (osc_build_spectrum_device: every model of the host setup,
+    Matérn ν up to 64 through a device K_ν)."""
     lib = L.lib()
     fr = np.ascontiguousarray(options.padding_fractions, dtype=np.float64)
     J, s, ptr = C.c_int(), C.c_int64(), C.c_void_p()

@@ -324,7 +324,7 @@ int osc_build_spectrum_device(osc_ctx* c, int m, int family, double sigma2, doub
     OSC_REQUIRE(family == OSC_COV_MATERN || family == OSC_COV_SEPARABLE_EXP,
                 "osc_build_spectrum_device: unknown covariance family");
     OSC_REQUIRE(spectrum_device_supported(family, nu_or_p),
-                "osc_build_spectrum_device: Matern nu must be k + 1/2 with k <= 3 (use osc_build_spectrum)");
+                "osc_build_spectrum_device: Matern nu must lie in (0, 64] (use osc_build_spectrum)");
     set_device(c);
     int J = 0;
     std::vector<double> eig = build_spectrum_with(

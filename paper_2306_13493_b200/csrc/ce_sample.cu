@@ -32,6 +32,29 @@ namespace {
 // elements per thread for a length-n transform
 inline int elems_for(int n) { return n >= 8 ? 8 : n; }
 
+// L2 residency hints of the compile-time-n passes. √λ (n² doubles, read by every sample) is kept
+// (evict_last); ξ rows and the half-spectrum intermediate pass through once (evict_first) — without
+// the hints the streams evict √λ and the row pass re-reads most of it from DRAM for every sample
+// (resident ξ at n = 2048: 26 MB of the 60 MB read per sample).
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldg_hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_hint(double2* a, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // Sup-norm mode of the column passes (smoothing_error_estimate, embedding.cpp:217-219): instead of
 // storing the field, every thread folds |z| of its outputs into v and the CTA commits max to sup[b]
 // (non-negative doubles order like their bit patterns, so one integer atomicMax per warp does it).
@@ -276,7 +299,7 @@ __device__ __forceinline__ void first_stage_store(double2* x, int lt, double2 (&
 // z[q0] = √λ(q0, q1a)·ξ(q0, q1a) + i·√λ(q0, q1b)·ξ(q0, q1b). T is even, so q0 has lt's parity and
 // lanes lt, lt^1 need the two halves of the same normal pair c = (lt >> 1) + r·T/2: the even lane
 // draws the even-r Philox blocks, the odd lane the odd-r ones, and they trade halves by shuffle.
-template <int LOGN>
+template <int LOGN, bool XI>
 __device__ __forceinline__ void rows_operands(const double* __restrict__ sqrt_lam, const double* __restrict__ xi,
                                               const PhiloxKeys& keys, uint32_t ell, uint64_t idx, int b, int q1a,
                                               int lt, double2 (&v)[8]) {
@@ -284,13 +307,14 @@ __device__ __forceinline__ void rows_operands(const double* __restrict__ sqrt_la
   const int64_t s = (int64_t)n * n;
   const bool odd = lt & 1;
   double ra[8], rb[8];  // ξ(q0, q1a), ξ(q0, q1b)
-  if (xi) {
+  if constexpr (XI) {
     const double* xa = xi + (int64_t)b * s + (int64_t)q1a * n;
     const double* xb = xa + n;
+    const uint64_t once = l2_policy_stream();
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      ra[r] = __ldg(xa + lt + r * T);
-      rb[r] = __ldg(xb + lt + r * T);
+      ra[r] = ldg_hint(xa + lt + r * T, once);
+      rb[r] = ldg_hint(xb + lt + r * T, once);
     }
   } else {
     const uint32_t ja = (uint32_t)q1a * (n / 2) + (lt >> 1), jb = ja + n / 2;
@@ -312,8 +336,15 @@ __device__ __forceinline__ void rows_operands(const double* __restrict__ sqrt_la
     }
   }
   const double* la = sqrt_lam + (int64_t)q1a * n + lt;
+  if constexpr (XI) {
+    const uint64_t keep = l2_policy_keep();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) v[r] = make_double2(__ldg(la + r * T) * ra[r], __ldg(la + n + r * T) * rb[r]);
+    for (int r = 0; r < 8; ++r)
+      v[r] = make_double2(ldg_hint(la + r * T, keep) * ra[r], ldg_hint(la + n + r * T, keep) * rb[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_double2(__ldg(la + r * T) * ra[r], __ldg(la + n + r * T) * rb[r]);
+  }
 }
 
 // Intermediate layout of the compile-time-n passes: CE_IL columns interleaved,
@@ -334,20 +365,25 @@ __host__ __device__ __forceinline__ int inter_groups(int P) { return (P + CE_IL 
 // then the row, then the column pair), so a warp's store covers whole 128-byte lines (four rows × one
 // column pair) instead of 16 scattered 32-byte sectors — the stores took a quarter of the pass's L1
 // data-pipe cycles. NTR = 1: both rows of the pair per thread (half lines).
-template <int LOGN, int NTR>
+template <int LOGN, int NTR, bool HINT>
 __device__ __forceinline__ void rows_unpack(const double2* smem, double2* __restrict__ inter, int b, int P, int cs,
                                             int rp0) {
   using PL = FftPlan<LOGN>;
   constexpr int n = PL::n, ROWS = 2 * NTR, THREADS = NTR * PL::T;
   const int Ph = inter_groups(P);
+  const uint64_t once = HINT ? l2_policy_stream() : 0;
+  auto put = [&](double2* a, double2 v) {
+    if constexpr (HINT) stg_hint(a, v, once);
+    else *a = v;
+  };
   if constexpr (NTR == 1) {
     for (int p = threadIdx.x; p < P; p += THREADS) {
       const int p0 = p * cs;
       const double2 zp = smem[fpad(p0)];
       const double2 zm = smem[fpad((n - p0) & (n - 1))];
       double2* o = inter + inter_pair_idx(b, Ph, n, p, 2 * rp0);
-      o[0] = make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-      o[CE_IL] = make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x));  // row 2·rp0 + 1
+      put(o, make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y)));
+      put(o + CE_IL, make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x)));  // row 2·rp0 + 1
     }
   } else {
     const int items = CE_IL * ROWS * Ph;
@@ -361,7 +397,7 @@ __device__ __forceinline__ void rows_unpack(const double2* smem, double2* __rest
       const double2 zm = x[fpad((n - p0) & (n - 1))];
       const double2 o = (q1l & 1) ? make_double2(0.5 * (zp.y + zm.y), 0.5 * (zm.x - zp.x))
                                   : make_double2(0.5 * (zp.x + zm.x), 0.5 * (zp.y - zm.y));
-      inter[inter_pair_idx(b, Ph, n, p, 2 * rp0 + q1l)] = o;
+      put(inter + inter_pair_idx(b, Ph, n, p, 2 * rp0 + q1l), o);
     }
   }
 }
@@ -370,7 +406,7 @@ __device__ __forceinline__ void rows_unpack(const double2* smem, double2* __rest
 // stores; the device-Philox draw is issue-heavy and overlaps better across many small CTAs, so it
 // keeps the column pass's transforms-per-CTA (measured at n = 2048: Philox 23.5 vs 25.5 µs per sample
 // with 1 vs 2 pairs, resident ξ 20.4 vs 18.3).
-template <int LOGN, int NTR>
+template <int LOGN, int NTR, bool XI>
 __global__ void __launch_bounds__(NTR * FftPlan<LOGN>::T, (1024 / (NTR * FftPlan<LOGN>::T) < 32 ? (1024 / (NTR * FftPlan<LOGN>::T) < 1 ? 1 : 1024 / (NTR * FftPlan<LOGN>::T)) : 32)) ce_rows_t_kernel(
     const double* __restrict__ sqrt_lam, const double* __restrict__ xi, uint64_t seed, uint32_t ell,
     uint64_t index0, int P, int cs, const double2* __restrict__ tw, double2* __restrict__ inter) {
@@ -384,7 +420,7 @@ __global__ void __launch_bounds__(NTR * FftPlan<LOGN>::T, (1024 / (NTR * FftPlan
   const int q1a = 2 * (rp0 + t);
   double2* x = smem + t * PL::LD;
   double2 v[8];
-  rows_operands<LOGN>(sqrt_lam, xi, philox_keys(seed), ell, index0 + (uint64_t)b, b, q1a, lt, v);
+  rows_operands<LOGN, XI>(sqrt_lam, xi, philox_keys(seed), ell, index0 + (uint64_t)b, b, q1a, lt, v);
   first_stage_store<LOGN>(x, lt, v);
   mid_stages<LOGN, 3>(x, lt, tw);
   {
@@ -398,7 +434,7 @@ __global__ void __launch_bounds__(NTR * FftPlan<LOGN>::T, (1024 / (NTR * FftPlan
     stage_store<LOGN, LS::R, LS::LNS>(x, lt, w);
     __syncthreads();
   }
-  rows_unpack<LOGN, NTR>(smem, inter, b, P, cs, rp0);
+  rows_unpack<LOGN, NTR, XI>(smem, inter, b, P, cs, rp0);
 }
 
 template <int LOGN>
@@ -455,8 +491,10 @@ __global__ void __launch_bounds__(FftPlan<LOGN>::THREADS, FftPlan<LOGN>::MINB) c
 }
 
 // 32 aligned bytes (two adjacent complex values) through the read-only path in one instruction
-__device__ __forceinline__ void ldg256(const double2* p, double2& a, double2& b) {
-  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+__device__ __forceinline__ void ldg256(const double2* p, double2& a, double2& b, uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p), "l"(pol));
 }
 
 // Column pass with two columns per thread (32 ≤ n ≤ 4096; ce_cols_t_kernel below and above): the same stages as ce_cols_t_kernel
@@ -530,9 +568,10 @@ __global__ void __launch_bounds__(Cols2Plan<LOGN>::THREADS, Cols2Plan<LOGN>::MIN
     // 256-bit load (column j0 + 1 of an odd P is allocated but never written: its values are dropped)
     const double2* s0 = inter + inter_pair_idx(b, inter_groups(P), n, ok0 ? j0 : 0, lt);
     static_assert(CE_IL == 2, "the 256-bit load reads one interleaved column pair");
+    const uint64_t once = l2_policy_stream();
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      ldg256(s0 + CE_IL * r * T, v0[r], v1[r]);
+      ldg256(s0 + CE_IL * r * T, v0[r], v1[r], once);
       if (!ok0) v0[r] = make_double2(0.0, 0.0);
       if (!ok1) v1[r] = make_double2(0.0, 0.0);
     }
@@ -584,18 +623,18 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   const double2* tw = L->twiddle.as<double2>();
   const size_t sm = sizeof(double2) * (size_t)PL::NT * PL::LD;
   cudaStream_t st = ctx->stream;
-  auto rows = [&](auto ntr) {
+  auto rows = [&](auto ntr, auto with_xi) {
     constexpr int NTR = decltype(ntr)::value;
     const size_t smr = sizeof(double2) * (size_t)NTR * PL::LD;
-    auto kern = ce_rows_t_kernel<LOGN, NTR>;
+    auto kern = ce_rows_t_kernel<LOGN, NTR, decltype(with_xi)::value>;
     smem_attr(kern, smr);
     KScope ks(ctx, "ce_rows");
     kern<<<dim3((PL::n / 2) / NTR, count), NTR * PL::T, smr, st>>>(sqrt_lam, xi_dev, seed, ell, index0, P, cs, tw,
                                                                     inter);
     OSC_CUDA(cudaGetLastError());
   };
-  if (xi_dev) rows(std::integral_constant<int, PL::NTR>{});
-  else rows(std::integral_constant<int, PL::NT>{});
+  if (xi_dev) rows(std::integral_constant<int, PL::NTR>{}, std::true_type{});
+  else rows(std::integral_constant<int, PL::NT>{}, std::false_type{});
   // two columns per thread for 32 ≤ n ≤ 4096, where it fits 128 registers without spills (config 2
   // column pass 277.7 → 208.6 ms per 12288 samples against one column per thread)
   if constexpr (LOGN >= 5 && LOGN <= 12) {
@@ -913,9 +952,87 @@ void ce_sample_launch(Ctx* ctx, const Level* L, const double* sqrt_lam, const do
 // the K_ν expression at covariance.cpp:53-62); other ν use the host setup.
 namespace {
 struct CovDev {
-  int family, half_k;
+  int family, half_k;  // half_k ≥ 0: Matérn ν = half_k + ½ (closed form); −1: general ν (K_ν below)
   double sigma2, lambda, nu_or_p;
+  double pre;  // σ² 2^{1−ν} / Γ(ν) (general ν)
 };
+
+// Modified Bessel function K_ν(x), ν > 0, x > 0 (covariance.cpp:58 boost::math::cyl_bessel_k): Temme's
+// method. ν = n + μ, |μ| ≤ ½: K_μ, K_{μ+1} from Temme's series (x < 2) or Steed's continued fraction
+// CF2 (x ≥ 2), then the stable upward recurrence K_{μ+k+1} = K_{μ+k−1} + 2(μ+k)/x · K_{μ+k}. The
+// series' Γ terms come from the Taylor coefficients of 1/Γ(1+z) (Abramowitz–Stegun 6.1.34), whose
+// even and odd parts give (1/Γ(1−μ) ± 1/Γ(1+μ))/2 without cancellation. Relative error ≤ 1e-13
+// against the host's std::cyl_bessel_k over the Matérn range.
+__device__ double bessel_k_dev(double nu, double x) {
+  constexpr double kA[26] = {1.0, 0.5772156649015329, -0.6558780715202538, -0.0420026350340952, 0.1665386113822915,
+                             -0.0421977345555443, -0.0096219715278770, 0.0072189432466630, -0.0011651675918591,
+                             -0.0002152416741149, 0.0001280502823882, -0.0000201348547807, -0.0000012504934821,
+                             0.0000011330272320, -0.0000002056338417, 0.0000000061160950, 0.0000000050020075,
+                             -0.0000000011812746, 0.0000000001043427, 0.0000000000077823, -0.0000000000036968,
+                             0.0000000000005100, -0.0000000000000206, -0.0000000000000054, 0.0000000000000014,
+                             0.0000000000000001};
+  constexpr double pi = 3.14159265358979323846, eps = 1e-16;
+  const int nl = (int)(nu + 0.5);
+  const double mu = nu - nl, mu2 = mu * mu, xi = 1.0 / x, xi2 = 2.0 * xi;
+  double rkmu, rk1;
+  if (x < 2.0) {
+    double ev = 0.0, od = 0.0;  // even part Σ a_{2j} μ^{2j}, odd part / μ = Σ a_{2j+1} μ^{2j}
+    for (int j = 12; j >= 0; --j) {
+      ev = fma(ev, mu2, kA[2 * j]);
+      od = fma(od, mu2, kA[2 * j + 1]);
+    }
+    const double gam1 = -od, gam2 = ev, gampl = gam2 - mu * gam1, gammi = gam2 + mu * gam1;
+    const double x2 = 0.5 * x, pimu = pi * mu;
+    const double fact = fabs(pimu) < eps ? 1.0 : pimu / sin(pimu);
+    double d = -log(x2), e = mu * d;
+    const double fact2 = fabs(e) < eps ? 1.0 : sinh(e) / e;
+    double ff = fact * (gam1 * cosh(e) + gam2 * fact2 * d);
+    double sum = ff;
+    e = exp(e);
+    double p = 0.5 * e / gampl, q = 0.5 / (e * gammi), c = 1.0, sum1 = p;
+    d = x2 * x2;
+    for (int i = 1; i <= 500; ++i) {
+      ff = (i * ff + p + q) / (i * (double)i - mu2);
+      c *= d / i;
+      p /= i - mu;
+      q /= i + mu;
+      const double del = c * ff;
+      sum += del;
+      sum1 += c * (p - i * ff);
+      if (fabs(del) < fabs(sum) * eps) break;
+    }
+    rkmu = sum;
+    rk1 = sum1 * xi2;
+  } else {
+    double b = 2.0 * (1.0 + x), d = 1.0 / b, h = d, delh = d, q1 = 0.0, q2 = 1.0;
+    const double a1 = 0.25 - mu2;
+    double q = a1, c = a1, a = -a1, sv = 1.0 + q * delh;
+    for (int i = 2; i <= 2000; ++i) {
+      a -= 2 * (i - 1);
+      c = -a * c / i;
+      const double qnew = (q1 - b * q2) / a;
+      q1 = q2;
+      q2 = qnew;
+      q += c * qnew;
+      b += 2.0;
+      d = 1.0 / (b + a * d);
+      delh = (b * d - 1.0) * delh;
+      h += delh;
+      const double dels = q * delh;
+      sv += dels;
+      if (fabs(dels / sv) < eps) break;
+    }
+    h = a1 * h;
+    rkmu = sqrt(pi / (2.0 * x)) * exp(-x) / sv;
+    rk1 = rkmu * (mu + x + 0.5 - h) * xi;
+  }
+  for (int i = 1; i <= nl; ++i) {
+    const double t = (mu + i) * xi2 * rk1 + rkmu;
+    rkmu = rk1;
+    rk1 = t;
+  }
+  return rkmu;
+}
 
 __device__ double cov_eval(const CovDev& c, double t0, double t1) {
   if (c.family == OSC_COV_SEPARABLE_EXP) {
@@ -927,6 +1044,7 @@ __device__ double cov_eval(const CovDev& c, double t0, double t1) {
   if (r == 0.0) return c.sigma2;
   const double x = sqrt(2.0 * c.nu_or_p) * r / c.lambda;
   if (x < 1e-13) return c.sigma2;
+  if (c.half_k < 0) return c.pre * pow(x, c.nu_or_p) * bessel_k_dev(c.nu_or_p, x);
   // 2^{1−ν}/Γ(ν) x^ν K_ν(x) for ν = k + ½: e^{−x} · Σ_{i≤k} (k+i)!/(i!(k−i)!) (2x)^{k−i} · k!/(2k)!
   double poly = 1.0;
   if (c.half_k == 1) poly = 1.0 + x;
@@ -1014,17 +1132,19 @@ void upload_twiddles(Level* L) {
   OSC_CUDA(cudaMemcpy(L->twiddle.p, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
 }
 
+// every model of the host setup: separable exponential, Matérn ν = k + ½ (closed forms) and general ν
 bool spectrum_device_supported(int family, double nu_or_p) {
-  if (family == OSC_COV_SEPARABLE_EXP) return true;
-  for (int k = 0; k <= 3; ++k)
-    if (nu_or_p == k + 0.5) return true;
-  return false;
+  return family == OSC_COV_SEPARABLE_EXP || (family == OSC_COV_MATERN && nu_or_p > 0.0 && nu_or_p <= 64.0);
 }
 
 // Raw spectrum of the padding-J embedding, left in device memory (eig_dev, s doubles).
 void spectrum_device_into(Ctx* ctx, int m, int J, int family, double sigma2, double lambda, double nu_or_p,
                           double* eig_dev) {
-  CovDev c{family, (int)(nu_or_p - 0.5), sigma2, lambda, nu_or_p};
+  int half_k = -1;
+  for (int k = 0; k <= 3; ++k)
+    if (nu_or_p == k + 0.5) half_k = k;
+  CovDev c{family, half_k, sigma2, lambda, nu_or_p,
+           family == OSC_COV_MATERN ? sigma2 * std::pow(2.0, 1.0 - nu_or_p) / std::tgamma(nu_or_p) : 0.0};
   const int n = 2 * (m + J), h = n / 2;
   const int64_t s = (int64_t)n * n, nw = (int64_t)(h + 1) * (h + 1);
   cudaStream_t st = ctx->stream;

@@ -130,7 +130,7 @@ int osc_level_create_device(osc_ctx* c, int m, int family, double sigma2, double
     OSC_REQUIRE(family == OSC_COV_MATERN || family == OSC_COV_SEPARABLE_EXP,
                 "osc_level_create_device: unknown covariance family");
     OSC_REQUIRE(spectrum_device_supported(family, nu_or_p),
-                "osc_level_create_device: Matern nu must be k + 1/2 with k <= 3 (use osc_build_spectrum)");
+                "osc_level_create_device: Matern nu must lie in (0, 64] (use osc_build_spectrum)");
     OSC_CUDA(cudaSetDevice(c->device));
     auto* L = new osc_level();
     L->ctx = c;

@@ -115,16 +115,21 @@ def test_device_setup_matches_host(P, ctx, m, model):
 
 
 def test_device_setup_config4_and_errors(P, ctx):
-    """Config-4 size (m = 2048, n = 4096) on the device matches the host spectrum; Matérn ν outside
-    k + ½ is refused with ConfigError (the host setup covers it)."""
+    """Config-4 size (m = 2048, n = 4096) on the device matches the host spectrum; general Matérn ν
+    (device K_ν) matches the host's std::cyl_bessel_k; ν beyond the device range is a ConfigError."""
     api = P.api
     cov = api.CovarianceModel.matern(2.0, 0.003, 0.5)
     host = api.build_operator(api.GridSpec.square(2048), cov)
     dev = api.build_operator(api.GridSpec.square(2048), cov, device=True, ctx=ctx)
     assert dev.padding == host.padding == (0, 0)
     assert relmax(dev.eigenvalues, host.eigenvalues) < 1e-12
+    for nu in (1.0, 0.3, 2.2):
+        cov = api.CovarianceModel.matern(1.0, 0.1, nu)
+        host = api.build_operator(api.GridSpec.square(16), cov)
+        dev = api.build_operator(api.GridSpec.square(16), cov, device=True, ctx=ctx)
+        assert dev.padding == host.padding and relmax(dev.eigenvalues, host.eigenvalues) < 1e-12, nu
     with pytest.raises(api.ConfigError):
-        api.build_operator(api.GridSpec.square(16), api.CovarianceModel.matern(1.0, 0.1, 1.0), device=True,
+        api.build_operator(api.GridSpec.square(16), api.CovarianceModel.matern(1.0, 0.1, 70.0), device=True,
                            ctx=ctx)
 
 

@@ -18,6 +18,8 @@ def _cov(api, O, model):
     (64, ("matern", 1.0, 0.1, 0.5)),                      # config 1
     (1024, ("matern", 1.0, 0.01, 1.5)),                   # config 2
     (16, ("matern", 1.0, 0.3, 1.5)),                      # padded, J > 0 (mixed-radix CE)
+    (32, ("matern", 1.5, 0.2, 0.8)), (64, ("matern", 1.0, 0.05, 2.3)),  # general ν: the device K_ν
+    (16, ("matern", 1.0, 0.4, 1.0)),                      # integer ν, padded
 ])
 def test_level_create_device_vs_pristine_reference(P, ctx, ref, m, model):
     """build_operator + from_parts + truncated in HBM: same J and eigenvalues (1e-12 of max λ) as
@@ -59,8 +61,8 @@ def test_level_create_device_vs_pristine_reference(P, ctx, ref, m, model):
 def test_level_create_device_errors(P, ctx):
     api = P.api
     g = api.GridSpec.square(16)
-    with pytest.raises(api.ConfigError):  # general ν has no device K_ν
-        api.DeviceLevel.from_model(ctx, g, api.CovarianceModel.matern(1.0, 0.1, 0.8))
+    with pytest.raises(api.ConfigError):  # ν beyond the device K_ν's range
+        api.DeviceLevel.from_model(ctx, g, api.CovarianceModel.matern(1.0, 0.1, 80.0))
     with pytest.raises(api.EmbeddingError):  # no SPD padding in the schedule
         api.DeviceLevel.from_model(ctx, g, api.CovarianceModel.matern(1.0, 2.0, 3.5),
                                    options=api.BuildOptions(padding_fractions=(0.5,)))

@@ -16,6 +16,7 @@
 using namespace oscfield;
 
 extern "C" int oscfield_gpu_configure(int n_gpus, const int* devices, int bc, int qoi);
+extern "C" int oscfield_gpu_set_setup(int mode);
 
 namespace {
 thread_local std::string g_err;
@@ -85,6 +86,8 @@ int64_t oscgpu_last_history(double* out, int64_t cap) {
 int oscgpu_configure(int n_gpus, const int* devices, int bc, int qoi) {
   return oscfield_gpu_configure(n_gpus, devices, bc, qoi);
 }
+
+int oscgpu_set_setup(int mode) { return oscfield_gpu_set_setup(mode); }
 
 }  // extern "C"
 

@@ -27,6 +27,8 @@
 #include "oscfield_b200.h"
 
 namespace oscfield {
+EmbeddingOperator build_operator_routed(const GridSpec& grid, const CovarianceModel& model,
+                                        const BuildOptions& options);
 namespace {
 
 // cap of the residual history a SolverError carries (the failing slot is re-solved with it kept)
@@ -115,6 +117,7 @@ struct GroupState {
   osc_group* group = nullptr;
   LevelCache<osc_group_level> levels;
   int bc = -1, qoi = -1;  // extension overrides (-1: the reference's own BC / QoI mapping)
+  int setup_mode = -1;    // build_operator_routed: -1 = OSC_SEAM_SETUP, 0 reference, 1 host, 2 device
   ~GroupState() { reset(); }
   void reset() {
     levels.clear([](osc_group_level* l) { osc_group_level_destroy(l); });
@@ -239,6 +242,37 @@ DrawStats summarize_draws(const std::vector<LevelDraw>& draws, bool has_coarse) 
   return s;
 }
 
+// Level setup of the routed estimator. integration/Makefile compiles the pristine estimators.cpp
+// with -Dbuild_operator=build_operator_routed, so make_level_plan (estimators.cpp:181) lands here.
+// Mode 0 (default) is the reference's own build_operator (bit-identical spectrum, hence the same
+// truncation mask as the CPU reference: the parity tests). Modes 1 / 2 take the spectrum from this
+// repo's threaded host setup / from the GPU (osc_build_spectrum[_device]: same padding schedule, SPD
+// test and clamp, eigenvalues equal to rounding) and hand it to EmbeddingOperator::from_parts — at
+// n = 4096 the reference's single-threaded first row + FFT take ~10 s per estimate, these < 1 s.
+EmbeddingOperator build_operator_routed(const GridSpec& grid, const CovarianceModel& model,
+                                        const BuildOptions& options) {
+  static const int env_mode = env_int("OSC_SEAM_SETUP", 0);
+  const int mode = group_state().setup_mode >= 0 ? group_state().setup_mode : env_mode;
+  if (mode == 0 || grid.dim() != 2 || grid.m(0) != grid.m(1)) return build_operator(grid, model, options);
+  const int family = model.family() == CovFamily::Matern ? OSC_COV_MATERN : OSC_COV_SEPARABLE_EXP;
+  const double nu_or_p = family == OSC_COV_MATERN ? model.nu() : model.p_norm();
+  int J = 0;
+  std::int64_t s = 0;
+  double* eig = nullptr;
+  const int rc = mode == 2 ? osc_build_spectrum_device(thread_ctx(), grid.m(0), family, model.sigma2(), model.lambda(),
+                                                       nu_or_p, options.padding_fractions.data(),
+                                                       static_cast<int>(options.padding_fractions.size()),
+                                                       options.tol_spd_factor, &J, &s, &eig)
+                           : osc_build_spectrum(grid.m(0), family, model.sigma2(), model.lambda(), nu_or_p,
+                                                options.padding_fractions.data(),
+                                                static_cast<int>(options.padding_fractions.size()),
+                                                options.tol_spd_factor, &J, &s, &eig);
+  if (rc) raise(rc);
+  std::vector<double> ev(eig, eig + s);
+  osc_free(eig);
+  return EmbeddingOperator::from_parts(grid, {J, J}, std::move(ev), model.sigma2());
+}
+
 // The reference's estimators call the file-local run_level_samples (estimators.cpp:315-316,333-334,
 // 388) with a non-const LevelPlan; this overload (declared by route_run_level_samples.hpp) is the
 // better match there and forwards to the GPU seam. Same arguments, same slot contract.
@@ -270,6 +304,16 @@ int oscfield_gpu_configure(int n_gpus, const int* devices, int bc, int qoi) {
   }
   gs.bc = bc;
   gs.qoi = qoi;
+  return OSC_OK;
+}
+
+// Level setup of the routed estimator: 0 the reference's own build_operator (default), 1 this repo's
+// host setup, 2 the GPU setup (see build_operator_routed); -1 returns to OSC_SEAM_SETUP.
+int oscfield_gpu_set_setup(int mode) {
+  if (mode < -1 || mode > 2) return OSC_ERR_CONFIG;
+  oscfield::GroupState& gs = oscfield::group_state();
+  std::lock_guard<std::mutex> lk(gs.mu);
+  gs.setup_mode = mode;
   return OSC_OK;
 }
 }

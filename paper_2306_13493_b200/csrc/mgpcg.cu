@@ -3210,7 +3210,10 @@ namespace {
 // when a baked-in value (shape, tolerance, buffers) changes. Measured, the host loop was not
 // launch-bound even at 64² (the lagged polling keeps the queue full): the device loop is neutral
 // (scripts/graph_ab.py), so it is kept to 128², where it removes the host round trips per iteration.
-constexpr int kGraphMaxM = 128;  // A/B (scripts/graph_ab.py): 64² 33.6 vs 33.8 ms, 128² 43.0 vs 43.5 ms per batch; neutral above
+#ifndef OSC_GRAPH_MAX_M
+#define OSC_GRAPH_MAX_M 128
+#endif
+constexpr int kGraphMaxM = OSC_GRAPH_MAX_M;  // A/B (scripts/graph_ab.py): 64² 33.6 vs 33.8 ms, 128² 43.0 vs 43.5 ms per batch; neutral above
 
 void pcg_iteration(Ctx* ctx, const osc_problem* prob, int B, double* r_in, double* r_out, double* p_old,
                    double* p_new) {

@@ -12,8 +12,8 @@ from paper_2306_13493_b200 import _lib as L  # noqa: E402
 api = P.api
 lib = L.lib()
 ctx = api.default_context(0)
-m, B = 1024, 31
-op = api.build_operator(api.GridSpec.square(m), api.CovarianceModel.matern(1.0, 0.01, 1.5))
+m, B = (2048, 8) if "--n4096" in sys.argv else (1024, 31)
+op = api.build_operator(api.GridSpec.square(m), api.CovarianceModel.matern(1.0, 0.01, 1.5 if m == 1024 else 0.5))
 lev = op.device_level(ctx, 0)
 out = torch.empty((B, (m + 1) ** 2), dtype=torch.float64, device="cuda:0")
 xi = torch.randn((B, op.s), dtype=torch.float64, device="cuda:0")

@@ -4,8 +4,10 @@ Smoothed CE (MLMC-CES: h0 = 1/16, adaptive k_ℓ on the levels coarser than the 
 versus standard CE (no smoothing, coarsest mesh forced to resolve λ: h0 = coarsest_level_bound(λ)).
 
 Every run is the REFERENCE'S OWN estimate_adaptive (integration/_build/liboscfield_gpu.so) with its
-draws routed to the GPU seam. The finest grid is capped at 2048² (l_max); a row whose bias estimate
-is still above ε/√2 there reports converged = false, as the reference does.
+draws routed to the GPU seam and — in the sweep — its build_operator routed to the GPU level setup
+(estimators.set_setup: the reference's single-threaded setup takes ~10 s per estimate at n = 4096).
+The finest grid is capped at 2048² (l_max); a row whose bias estimate is still above ε/√2 there
+reports converged = false, as the reference does.
 
 "CPU beside it" (part 2): the pristine reference on the host cores (oracle/_ref, all threads) and the
 GPU-routed run with IDENTICAL options, on the rows the CPU finishes in minutes — finest grid capped
@@ -39,6 +41,8 @@ def options(variant, l_max):
     return api.EstimatorOptions(seed=1, l_max=l_max)
 
 
+setup = "--reference-setup" not in sys.argv
+E.set_setup(E.SETUP_DEVICE if setup else E.SETUP_REFERENCE)
 for lam in (0.03, 0.01):
     model = api.CovarianceModel.separable_exponential(1.0, lam)
     problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Flux), bc=api.BC.FlowCell)
@@ -52,12 +56,14 @@ for lam in (0.03, 0.01):
             ctx.synchronize()
             wall = time.perf_counter() - t0
             row = dict(lam=lam, eps=eps, variant=variant, h0=h0, wall_s=wall, estimate=rep.estimate,
+                       level_setup="device" if setup else "reference",
                        sampling_error=rep.sampling_error, bias=rep.bias_estimate, converged=rep.converged,
                        levels=len(rep.levels), n=[l.n for l in rep.levels], cost_model=rep.total_cost_model,
                        samples_per_s=sum(l.n for l in rep.levels) / wall, message=rep.message)
             rows.append(row)
             print(json.dumps(row), flush=True)
 
+E.set_setup(E.SETUP_REFERENCE)  # the CPU comparison uses the reference's own setup on both sides
 if with_cpu:
     from oracle import oracle as O
     if os.path.exists(O.REF_SO):

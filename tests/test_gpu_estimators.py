@@ -78,6 +78,30 @@ def test_mlmc_gpu_vs_cpu_reference(P, E, ref, case):
     _same_report(gpu, cpu)
 
 
+@pytest.mark.parametrize("mode", ["host", "device"])
+def test_mlmc_routed_level_setup(P, E, ref, mode):
+    """build_operator of the routed estimator taken from this repo's host / GPU setup
+    (build_operator_routed): with smoothing Off no truncation mask is involved, so the run must take
+    the CPU reference's decisions (identical N_ℓ) and agree in every level moment."""
+    import os
+    from oracle import oracle as O
+    api = P.api
+    lam, h0, eps, pilot, l_max = 0.1, 1.0 / 8, 2e-3, 50, 4
+    opts = O.RefOpts.make(family=O.SEP_EXP, sigma2=1.0, lam=lam, nu_or_p=1.0, seed=1, pilot_n=pilot,
+                          threads=os.cpu_count() or 1, l_max=l_max)
+    cpu = ref.mlmc(opts, h0, eps, 2)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1.0, lam))
+    opt = api.EstimatorOptions(seed=1, pilot_n=pilot, l_max=l_max)
+    E.set_setup(E.SETUP_HOST if mode == "host" else E.SETUP_DEVICE)
+    try:
+        gpu = E.mlmc_estimate(prob, opt, h0, eps, 2)
+    finally:
+        E.set_setup(E.SETUP_REFERENCE)
+    _same_report(gpu, cpu)
+    with pytest.raises(api.ConfigError):
+        E.set_setup(7)
+
+
 def test_mlmc_group_mode_matches_single_device(P, E):
     """The seam's osc_group path (n_gpus = 1 here; contiguous per-device chunks + NCCL all-reduce of
     the level sums) gives the bit-identical estimate of the single-context path."""

@@ -323,6 +323,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mlmc", action="store_true",
                     help="config 3/5: full adaptive MLMC(-CES) estimate over the GPU seam (wall time)")
+    ap.add_argument("--setup", default="device", choices=["reference", "host", "device"],
+                    help="--mlmc: who builds the levels' spectra (estimators.set_setup)")
     ap.add_argument("--eps", type=float, default=1e-3)
     ap.add_argument("--lam", type=float, default=0.01)
     args = ap.parse_args()
@@ -408,8 +410,15 @@ def main():
         iters_total[0] += int(itf.sum())
         iters_total[1] += int(itc.sum())
 
-    for w in range(args.warmup - 1):
+    # W warm-up steps, continued until at least 0.4 s have been spent warming up: an idle B200 sits at
+    # 120 MHz and the few-ms steps of the small configs would otherwise be timed on ramping clocks
+    # (config 1 measured 94k or 140k samples/s depending on it)
+    t_warm = time.perf_counter()
+    w = 0
+    while w < args.warmup - 1 or (time.perf_counter() - t_warm < 0.4 and w < 500):
         step(1_000_000 + w)
+        w += 1
+    warm_extra = max(0, w - (args.warmup - 1))
     # the last warm-up step is profiled (every kernel class, untimed): per-class times for the
     # kernel table and the choice of the dominant kernel; in the timed region only the dominant
     # kernel's launches carry CUDA events, so the step time is not perturbed by profiling
@@ -604,7 +613,8 @@ def main():
         line = {
             "metric": "MLMC samples/s per level (CE field + Darcy solve, fp64)",
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "warmup_extra_steps": warm_extra, "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: xi = NormalStream(seed 1, l, i) on device (Philox4x32-10 + Box-Muller)",
             "config": {"workload": W["name"], "global_batch": B * world, "per_gpu_batch": B,
@@ -663,8 +673,10 @@ def cfg3_per_level(args, api, ctx, torch, lib, hbm):
                 failed.extend(int(frm + i) for i in np.nonzero(st)[0][:8])
             elif code:
                 api._check(code, status=st)
-        for w in range(args.warmup):
+        t_warm, w = time.perf_counter(), 0
+        while w < args.warmup or (time.perf_counter() - t_warm < 0.2 and w < 500):
             step(1_000_000 + w)
+            w += 1
         ctx.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         its = [0, 0]
@@ -699,6 +711,9 @@ def run_mlmc(args, api, ctx, torch, rank):
     problem = api.ProblemSpec(model, api.QoiSpec(api.QoiKind.Flux), bc=api.BC.FlowCell)
     opt = api.EstimatorOptions(seed=1, smoothing=api.SmoothingRule.Adaptive, smoothing_lstar_only=True,
                                l_max=4)
+    # build_operator of the reference's make_level_plan routed to the GPU level setup (the reference's
+    # own single-threaded host setup otherwise takes a third of this run's wall time)
+    E.set_setup({"reference": E.SETUP_REFERENCE, "host": E.SETUP_HOST, "device": E.SETUP_DEVICE}[args.setup])
     # a first (cold) run loads the kernels and allocates each level's workspaces; the second run,
     # identical (same seed, so the same samples), is the timed one
     t0 = time.perf_counter()
@@ -719,7 +734,8 @@ def run_mlmc(args, api, ctx, torch, rank):
             "levels": [{"h": h, "n": l.n, "mean_y": l.mean_y, "var_y": l.var_y,
                         "wall_per_sample_s": l.cost_wall_per_sample} for h, l in zip(rep.level_h, rep.levels)],
             "config": {"workload": f"MLMC-CES sep-exp s2=1 lam={args.lam}, h0=1/16, 5 levels, flux QoI, eps={args.eps}",
-                       "driver": "the reference's estimate_adaptive (C++) over the GPU seam"},
+                       "driver": "the reference's estimate_adaptive (C++) over the GPU seam",
+                       "level_setup": args.setup},
             "dtype": "f64", "data": "synthetic: NormalStream(1, l, i)",
         }), flush=True)
 

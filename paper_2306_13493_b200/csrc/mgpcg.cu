@@ -1185,7 +1185,23 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
   Pair oq = first ? zero : ld2<INT>(pb, xa, y0 + 1, n0);
   Pair rq = ld2<INT>(rb, xa, y0, n0), uq = ld2<INT>(ub, xa, y0, n0);
   double rr = 0.0;
+  // L2 prefetch PU_PREFETCH rows ahead of the register pipeline (which holds one row of loads): the
+  // kernel is latency-bound on DRAM (70% of its stall samples are long-scoreboard waits at 16 warps per
+  // SM), and the prefetched rows turn those into L2 hits without spending registers. Every fourth
+  // lane's address covers the 64 bytes its four lanes will load. Measured at 2048² (A/B of the
+  // distance, profiles/ab_r2/pcg_update_prefetch.txt): none 5.37, 3 rows 5.68, 4 rows 5.71, 6 rows
+  // 5.66, 8 rows 5.45, 12 rows 4.66 TB/s.
+  constexpr int PU_PREFETCH = 4;
+  const bool pf_lane = (c.lane & 3) == 0;
   for (int y = y0; y < y1; ++y) {
+    if (INT && pf_lane && y + PU_PREFETCH < y1 + 2) {
+      const int64_t o = (int64_t)(y + PU_PREFETCH) * n0 + xa;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + o));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(zb + o));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + o));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + o));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ub + o));
+    }
     const Pair kp = kq, pp = comb(zq, oq);  // row y+1 (raw rows loaded one iteration ahead)
     const Pair r0 = rq, u0 = uq;            // row y
     kq = ld2<INT>(kb, xa, y + 2, n0);
@@ -2316,7 +2332,10 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
   return make_double2(rz, dc);
 }
 
-__global__ void __launch_bounds__(32 * SUR_W, 3 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+// 16 one-warp CTAs per SM (128 registers, no spills): the sweep is bound by dependent fp64 latency at
+// 60% issue with 12 warps per SM; 16 gave 3.68 → 3.98 TB/s at 2048² and 3.13 → 3.26 at 1024²
+// (profiles/ab_r2/ring_occupancy.txt; 20 CTAs for the restriction spill and lose)
+__global__ void __launch_bounds__(32 * SUR_W, 4 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
                                                                const double* __restrict__ r,
                                                                pz_t* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,

@@ -17,6 +17,14 @@ for r in rows[2:]:
     for h in ["smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
               "smsp__warps_eligible.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
               "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+              "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+              "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+              "l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed",
+              "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+              "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum",
+              "smsp__inst_executed_op_shared_ld.sum", "smsp__inst_executed_op_shared_st.sum",
+              "smsp__inst_executed_op_global_ld.sum", "smsp__inst_executed_op_global_st.sum",
+              "smsp__inst_executed_op_ldgsts.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
               "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
               "lts__t_sectors.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
               "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_barriers"]:

@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "osc_internal.cuh"
 
 namespace osc {
@@ -139,9 +141,17 @@ cudaEvent_t Ctx::pool_event() {
   return ev_pool[ev_next++];
 }
 
-// Without profiling a scope only counts launches (no string work on the launch path).
+// Without profiling a scope only counts launches (no string work on the launch path). With OSC_NVTX=1
+// (read at context creation) every scope is also an NVTX range named "<class>:<grid>" (SURVEY §5:
+// NVTX ranges per kernel; ':' because '@' separates the domain in ncu's filter syntax), so ncu / nsys
+// can select a kernel class at one grid size:
+//   OSC_NVTX=1 ncu --nvtx --nvtx-include "mg_up.Lc:2048/" ...
 KScope::KScope(Ctx* c, const char* name, int n_launches) : ctx(c), cls(-1) {
   c->launches += n_launches;
+  if (c->nvtx) {
+    const std::string full = c->tag.empty() ? std::string(name) : std::string(name) + ":" + c->tag;
+    nvtxRangePushA(full.c_str());
+  }
   if (!c->profiling) return;
   const std::string full = c->tag.empty() ? std::string(name) : std::string(name) + "@" + c->tag;
   cls = c->stat_class(full.c_str());
@@ -153,6 +163,7 @@ KScope::KScope(Ctx* c, const char* name, int n_launches) : ctx(c), cls(-1) {
 }
 
 KScope::~KScope() {
+  if (ctx->nvtx) nvtxRangePop();
   if (e0) {
     cudaEventRecord(e1, ctx->stream);
     ctx->stats[cls].pending.emplace_back(e0, e1);
@@ -170,6 +181,8 @@ int osc_ctx_create(int device, osc_ctx** out) {
     if (device < 0) OSC_CUDA(cudaGetDevice(&device));  // the calling thread's current device
     auto* c = new osc_ctx();
     c->device = device;
+    const char* nv = std::getenv("OSC_NVTX");
+    c->nvtx = nv && std::atoi(nv) != 0;
     try {
       OSC_CUDA(cudaSetDevice(device));
       OSC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

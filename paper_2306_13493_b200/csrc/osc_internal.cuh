@@ -142,6 +142,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   size_t mem_budget = 0;
   bool profiling = false;
+  bool nvtx = false;  // OSC_NVTX=1: every kernel-class scope is an NVTX range "<class>:<grid>"
   std::string profile_only;  // non-empty: events only around this kernel class's launches
   std::vector<cudaEvent_t> ev_pool;  // timing events, reused across profiled launches
   size_t ev_next = 0;

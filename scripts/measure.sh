@@ -35,14 +35,14 @@ if has launches; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/${TAG}_cfg4_launches.csv $CMD > $O/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 fi
 if has ncu; then
-  # --set full captures of the top kernels (batch 8). The coarse 1024^2 solve runs first (~15 V-cycles),
-  # so the launches are skipped past it and a few consecutive ones are kept: the summary keeps the
-  # largest grid (level 0 / level 1 of the 2048^2 solve)
-  for spec in "pcg_update_cg_kernel 20 2" "smooth_up_ring_kernel 20 2" "restrict_ring_kernel 20 2" "c_up_ring_kernel 70 6" "c_down_ring_kernel 70 6" "galerkin_tile_kernel 0 8"; do
-    set -- $spec
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c $3 -o $O/${TAG}_$1 $CMD > $O/${TAG}_ncu_$1.log 2>&1; tail -1 $O/${TAG}_ncu_$1.log
-    python scripts/ncu_summary.py $O/${TAG}_$1.ncu-rep 14 > $O/${TAG}_$1_ncu.txt 2>&1
-    [ -n "$KEEP_REP" ] || rm -f $O/${TAG}_$1.ncu-rep   # gpurun_out/ returns at most 64 MiB
+  # --set full captures of the top kernels at the 2048^2 solve (batch 8), selected by their NVTX range
+  # (OSC_NVTX=1: every kernel-class scope is a range "<class>:<grid>"; OSC_LEVEL_STATS=1 names levels)
+  for cls in "pcg_update:2048" "mg_smooth_up_r.L0:2048" "mg_restrict_r.L0:2048" "mg_up.L1:2048" "mg_down.L1:2048" "mg_setup.galerkin.L0:2048"; do
+    f=$(echo $cls | tr ':.' '__')
+    OSC_NVTX=1 OSC_LEVEL_STATS=1 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "$cls/" -s 2 -c 1 -o $O/${TAG}_$f $CMD > $O/${TAG}_ncu_$f.log 2>&1; tail -1 $O/${TAG}_ncu_$f.log
+    python scripts/ncu_summary.py $O/${TAG}_$f.ncu-rep 14 > $O/${TAG}_${f}_ncu.txt 2>&1
+    python scripts/ncu_stalls.py $O/${TAG}_$f.ncu-rep >> $O/${TAG}_${f}_ncu.txt 2>&1
+    [ -n "$KEEP_REP" ] || rm -f $O/${TAG}_$f.ncu-rep   # gpurun_out/ returns at most 64 MiB
   done
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:ce_ -c 2 -o $O/${TAG}_ce python bench.py --config 2 --batch 32 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/${TAG}_ncu_ce.log 2>&1; tail -1 $O/${TAG}_ncu_ce.log
   python scripts/ncu_summary.py $O/${TAG}_ce.ncu-rep 14 > $O/${TAG}_ce_ncu.txt 2>&1

@@ -98,6 +98,16 @@ __device__ __forceinline__ double rcp64(double d) {
   return y;
 }
 
+// Reciprocal of the smoothing sweeps: one Newton step on the 2^-23 hardware estimate (relative error
+// ≈ 2^-46). The sweeps divide by stencil diagonals inside the preconditioner, where 1e-14 is a
+// perturbation of the smoother far below the fp32 couplings'; setup (transfer weights, Galerkin
+// products) keeps rcp64.
+__device__ __forceinline__ double rcp64s(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  return fma(y, fma(-d, y, 1.0), y);
+}
+
 // ---- multigrid hierarchy: rows, transfers, coarse operators -----------------------------------------
 // Level 0 is the fine P1 system: a 5-point stencil rebuilt from nodal k in every kernel. Levels ≥ 1
 // keep a symmetric 9-point operator in HBM, stored with Dirichlet elimination already applied
@@ -209,6 +219,31 @@ __global__ void __launch_bounds__(NT) rows0_kernel(Geo g, int bc, const double* 
   C[o] = r.c;
   E[o] = r.e;
   Nn[o] = r.n;
+}
+
+// Raw (un-eliminated) level-0 edge weights E(x,y) = A((x,y),(x+1,y)), N(x,y) = A((x,y),(x,y+1)) in fp32
+// for the level-0 preconditioner sweeps (the Galerkin setup writes them as a by-product of its tile;
+// this kernel serves the rediscretised hierarchy). Same formulas as edges_pair.
+__global__ void __launch_bounds__(NT) edges0_kernel(Geo g, const double* __restrict__ k, float* __restrict__ E,
+                                                    float* __restrict__ Nn) {
+  const int b = blockIdx.y;
+  const int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x;
+  if (i >= g.N) return;
+  const int m = g.m, n0 = g.n0;
+  const int y = (int)((unsigned)i / (unsigned)n0), x = (int)i - y * n0;
+  const double* kb = k + (int64_t)b * g.N;
+  constexpr double third = 1.0 / 3.0;
+  auto K = [&](int a, int b2) { return __ldg(kb + (int64_t)b2 * n0 + a); };
+  double e = 0.0, nn = 0.0;
+  if (x < m)
+    e = -0.5 * ((y < m ? (K(x, y) + K(x + 1, y) + K(x + 1, y + 1)) * third : 0.0) +
+                (y > 0 ? (K(x, y - 1) + K(x + 1, y) + K(x, y)) * third : 0.0));
+  if (y < m)
+    nn = -0.5 * ((x < m ? (K(x, y) + K(x + 1, y + 1) + K(x, y + 1)) * third : 0.0) +
+                 (x > 0 ? (K(x - 1, y) + K(x, y) + K(x, y + 1)) * third : 0.0));
+  const int64_t o = (int64_t)b * g.N + i;
+  E[o] = (float)e;
+  Nn[o] = (float)nn;
 }
 
 __device__ __forceinline__ bool dir_or_out(int bc, int m, int x, int y) {
@@ -358,7 +393,9 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
                                                    float* __restrict__ Nc, float* __restrict__ NEc,
                                                    float* __restrict__ NWc, float* __restrict__ pw0,
                                                    float* __restrict__ pw1, float* __restrict__ pw2,
-                                                   float* __restrict__ pw3, double* gsm) {
+                                                   float* __restrict__ pw3, double* gsm,
+                                                   float* __restrict__ E0 = nullptr,
+                                                   float* __restrict__ N0 = nullptr) {
   const int b = blockIdx.z;
   const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y;
   const int m = F.m, n0 = F.n0, mc = gc.m, mcl = m / 2;
@@ -384,21 +421,33 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
     for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
       const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
       double c = 1.0, e = 0.0, nn = 0.0;
-      if (INT || !(x < 0 || x > m || y < 0 || y > m || is_dir(bc, m, x, y))) {
-        auto Ed = [&](int a, int b2) -> double {
-          if (a < 0 || a >= m) return 0.0;
-          return -0.5 * ((b2 < m ? (K(a, b2) + K(a + 1, b2) + K(a + 1, b2 + 1)) * third : 0.0) +
-                         (b2 > 0 ? (K(a, b2 - 1) + K(a + 1, b2) + K(a, b2)) * third : 0.0));
-        };
-        auto Nd = [&](int a, int b2) -> double {
-          if (b2 < 0 || b2 >= m) return 0.0;
-          return -0.5 * ((a < m ? (K(a, b2) + K(a + 1, b2 + 1) + K(a, b2 + 1)) * third : 0.0) +
-                         (a > 0 ? (K(a - 1, b2) + K(a, b2) + K(a, b2 + 1)) * third : 0.0));
-        };
-        const double E = Ed(x, y), W = Ed(x - 1, y), Nn = Nd(x, y), S = Nd(x, y - 1);
+      auto Ed = [&](int a, int b2) -> double {
+        if (a < 0 || a >= m) return 0.0;
+        return -0.5 * ((b2 < m ? (K(a, b2) + K(a + 1, b2) + K(a + 1, b2 + 1)) * third : 0.0) +
+                       (b2 > 0 ? (K(a, b2 - 1) + K(a + 1, b2) + K(a, b2)) * third : 0.0));
+      };
+      auto Nd = [&](int a, int b2) -> double {
+        if (b2 < 0 || b2 >= m) return 0.0;
+        return -0.5 * ((a < m ? (K(a, b2) + K(a + 1, b2 + 1) + K(a, b2 + 1)) * third : 0.0) +
+                       (a > 0 ? (K(a - 1, b2) + K(a, b2) + K(a, b2 + 1)) * third : 0.0));
+      };
+      const bool in_grid = INT || !(x < 0 || x > m || y < 0 || y > m);
+      double E = 0.0, Nn = 0.0;
+      if (in_grid) {
+        E = Ed(x, y);
+        Nn = Nd(x, y);
+      }
+      if (INT || (in_grid && !is_dir(bc, m, x, y))) {
+        const double W = Ed(x - 1, y), S = Nd(x, y - 1);
         c = -(E + W + Nn + S);
         e = (!INT && is_dir(bc, m, x + 1, y)) ? 0.0 : E;
         nn = (!INT && is_dir(bc, m, x, y + 1)) ? 0.0 : Nn;
+      }
+      // raw (un-eliminated) edge weights of the tile's own fine nodes for the level-0 sweeps, fp32
+      if (E0 && in_grid && x >= 2 * I0 && x < 2 * I0 + 2 * GT_X && y >= 2 * J0 && y < 2 * J0 + 2 * GT_Y) {
+        const int64_t o = (int64_t)b * F.Nn + (int64_t)y * n0 + x;
+        E0[o] = (float)E;
+        N0[o] = (float)Nn;
       }
       A(0, lx, ly) = c;
       A(1, lx, ly) = e;
@@ -540,15 +589,16 @@ __global__ void __launch_bounds__(GT_THREADS) galerkin_tile_kernel(const double*
                                                                    float* __restrict__ NEc,
                                                                    float* __restrict__ NWc, float* __restrict__ pw0,
                                                                    float* __restrict__ pw1, float* __restrict__ pw2,
-                                                                   float* __restrict__ pw3) {
+                                                                   float* __restrict__ pw3, float* __restrict__ E0,
+                                                                   float* __restrict__ N0) {
   extern __shared__ double gsm[];
   const int I0 = blockIdx.x * GT_X, J0 = blockIdx.y * GT_Y, m = F.m;
   const bool interior = 2 * I0 - 5 >= 1 && 2 * I0 + 2 * GT_X + 3 <= m - 1 && 2 * J0 - 5 >= 1 &&
                         2 * J0 + 2 * GT_Y + 3 <= m - 1;
   if (interior)
-    galerkin_tile_body<L0K, true>(k0, F, bc, opdep, gc, Cc, Ec, Nc, NEc, NWc, pw0, pw1, pw2, pw3, gsm);
+    galerkin_tile_body<L0K, true>(k0, F, bc, opdep, gc, Cc, Ec, Nc, NEc, NWc, pw0, pw1, pw2, pw3, gsm, E0, N0);
   else
-    galerkin_tile_body<L0K, false>(k0, F, bc, opdep, gc, Cc, Ec, Nc, NEc, NWc, pw0, pw1, pw2, pw3, gsm);
+    galerkin_tile_body<L0K, false>(k0, F, bc, opdep, gc, Cc, Ec, Nc, NEc, NWc, pw0, pw1, pw2, pw3, gsm, E0, N0);
 }
 
 // Reference rediscretisation (fem.cpp:241-244): the level-l row from the injected nodal k,
@@ -1735,7 +1785,7 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
     __syncwarp();
     const double* S = slot(y);
     const R9 q = raw9(S, y);
-    zr0 = P2(S, LY::R).b * rcp64(q.C.b);  // row y0−3 is odd: red at b
+    zr0 = P2(S, LY::R).b * rcp64s(q.C.b);  // row y0−3 is odd: red at b
   }
   // Pending smoother rows carry partial sums instead of stencils: every neighbour term is folded in
   // as soon as its value exists, so only the couplings still to be applied stay live.
@@ -1766,14 +1816,14 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
       // row y+1 has its red node in the other column
       const bool ok1 = (unsigned)(y + 1) < (unsigned)n0 && (unsigned)(ra0 ? xb : xa) < (unsigned)n0;
       const double c1 = ok1 ? S1[LY::C + 2 * lane + (ra0 ? 1 : 0)] : 1.0;
-      const double zrp = S1[LY::R + 2 * lane + (ra0 ? 1 : 0)] * rcp64(c1);
+      const double zrp = S1[LY::R + 2 * lane + (ra0 ? 1 : 0)] * rcp64s(c1);
       const double zr0_e = shdn(zr0), zr0_w = shup(zr0);
       if constexpr (ra0) {
-        const double zbl = (rc0.b - (qc.E.b * zr0_e + qc.E.a * zr0 + qc.N.b * zrp + Nm.b * zrm)) * rcp64(qc.C.b);
+        const double zbl = (rc0.b - (qc.E.b * zr0_e + qc.E.a * zr0 + qc.N.b * zrp + Nm.b * zrm)) * rcp64s(qc.C.b);
         zc0 = Pair{zr0, zbl};
       } else {
         const double Ew = shup(qc.E.b);
-        const double zbl = (rc0.a - (qc.E.a * zr0 + Ew * zr0_w + qc.N.a * zrp + Nm.a * zrm)) * rcp64(qc.C.a);
+        const double zbl = (rc0.a - (qc.E.a * zr0 + Ew * zr0_w + qc.N.a * zrp + Nm.a * zrm)) * rcp64s(qc.C.a);
         zc0 = Pair{zbl, zr0};
       }
       zrm = zr0;
@@ -1842,16 +1892,16 @@ __global__ void __launch_bounds__(32 * CU_W, 3 * 4 / CU_W) c_up_ring_kernel(L9 L
     const double vm1a_e = shdn(vm1.a), vm1b_w = shup(vm1.b);
     if constexpr (ra0) {  // red a, black b
       const S9& K = Bc;    // black at b: E = next lane's a, W = own a; S row: S = vm1.b, SE = next a, SW = vm1.a
-      pb = PendB{K.n, K.ne, K.nw, rcp64(K.c),
+      pb = PendB{K.n, K.ne, K.nw, rcp64s(K.c),
                  rc0.b - (K.e * v0a_e + K.w * v0.a + K.s * vm1.b + K.se * vm1a_e + K.sw * vm1.a)};
       const S9& R = A;     // red at a: S = black new of row y−1 at a (= zbn0), SE = vm1.b, SW = prev lane's b
-      pr1 = PendR1{R.e, R.w, R.ne, R.nw, R.n, rcp64(R.c), rc0.a - (R.s * zbn0 + R.se * vm1.b + R.sw * vm1b_w)};
+      pr1 = PendR1{R.e, R.w, R.ne, R.nw, R.n, rcp64s(R.c), rc0.a - (R.s * zbn0 + R.se * vm1.b + R.sw * vm1b_w)};
     } else {  // red b, black a
       const S9& K = A;     // black at a: E = own b, W = prev lane's b; SE = vm1.b, SW = prev lane's b
-      pb = PendB{K.n, K.ne, K.nw, rcp64(K.c),
+      pb = PendB{K.n, K.ne, K.nw, rcp64s(K.c),
                  rc0.a - (K.e * v0.b + K.w * v0b_w + K.s * vm1.a + K.se * vm1.b + K.sw * vm1b_w)};
       const S9& R = Bc;    // red at b: S = zbn0 (black new of row y−1 at b), SE = next lane's a, SW = vm1.a
-      pr1 = PendR1{R.e, R.w, R.ne, R.nw, R.n, rcp64(R.c), rc0.b - (R.s * zbn0 + R.se * vm1a_e + R.sw * vm1.a)};
+      pr1 = PendR1{R.e, R.w, R.ne, R.nw, R.n, rcp64s(R.c), rc0.b - (R.s * zbn0 + R.se * vm1a_e + R.sw * vm1.a)};
     }
     vm1 = v0;
     zbn1 = zbn0;
@@ -1935,7 +1985,7 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
   auto zred = [&](int y) {
     const double* S = slot(y);
     const Pair c = Cpair(S, y), rr = P2(S, DN_R);
-    return RED_IS_A(y) ? rr.a * rcp64(c.a) : rr.b * rcp64(c.b);
+    return RED_IS_A(y) ? rr.a * rcp64s(c.a) : rr.b * rcp64s(c.b);
   };
   // pre-smoothed pair of row y from its red value zr0 and the red values of rows y∓1 (zrm, zrp);
   // Nm = N of row y − 1
@@ -1944,10 +1994,10 @@ __global__ void __launch_bounds__(32 * CD_W, 4 * 4 / CD_W) c_down_ring_kernel(L9
     const Pair c = Cpair(S, y), E0 = F2(S, DN_E), N0 = F2(S, DN_N), r0 = P2(S, DN_R);
     const double zr0_e = shdn(zr0), zr0_w = shup(zr0), Ew = shup(E0.b);
     if (RED_IS_A(y)) {
-      const double zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) * rcp64(c.b);
+      const double zbl = (r0.b - (E0.b * zr0_e + E0.a * zr0 + N0.b * zrp + Nm.b * zrm)) * rcp64s(c.b);
       return Pair{zr0, zbl};
     }
-    const double zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) * rcp64(c.a);
+    const double zbl = (r0.a - (E0.a * zr0 + Ew * zr0_w + N0.a * zrp + Nm.a * zrm)) * rcp64s(c.a);
     return Pair{zbl, zr0};
   };
   // centre weights of cell (I, Jc) (odd row 2Jc+1); 0 off the cells
@@ -2066,15 +2116,19 @@ constexpr int RR_W = 1;  // level-0 ring restriction
 constexpr size_t L0R_SMEM_UP = sizeof(double) * L0R_RING * SUR_W * L0R_WORDS_UP;  // 51.5 KB at 4 warps
 constexpr size_t L0R_SMEM_DN = sizeof(double) * L0R_RING * RR_W * L0R_WORDS_DN;  // 20.5 KB
 
-// stage k and r of fine row y (columns x0 … x0+63) into S; off-grid values are zero
-__device__ __forceinline__ void l0_issue_kr(double* S, const double* kb, const double* rb, int x0, int lane, int y,
-                                            int n0) {
+// stage the raw edge weights (fp32 E then N, 64 + 64 floats in the 64 doubles at L0R_K) and r of fine
+// row y (columns x0 … x0+63) into S; off-grid values are zero
+__device__ __forceinline__ void l0_issue_kr(double* S, const float* eb, const float* nb, const double* rb, int x0,
+                                            int lane, int y, int n0) {
   const bool yok = (unsigned)y < (unsigned)n0;
   const int c0 = x0 + lane, c1 = c0 + 32;
   const bool ok0 = yok && (unsigned)c0 < (unsigned)n0, ok1 = yok && (unsigned)c1 < (unsigned)n0;
   const int64_t i0 = (int64_t)y * n0 + c0;
-  cpa8(S + L0R_K + lane, kb + i0, ok0);
-  cpa8(S + L0R_K + 32 + lane, kb + i0 + 32, ok1);
+  float* SF = reinterpret_cast<float*>(S + L0R_K);
+  cpa4(SF + lane, eb + i0, ok0);
+  cpa4(SF + 32 + lane, eb + i0 + 32, ok1);
+  cpa4(SF + 64 + lane, nb + i0, ok0);
+  cpa4(SF + 96 + lane, nb + i0 + 32, ok1);
   cpa8(S + L0R_R + lane, rb + i0, ok0);
   cpa8(S + L0R_R + 32 + lane, rb + i0 + 32, ok1);
 }
@@ -2082,20 +2136,30 @@ __device__ __forceinline__ Pair l0_pair(const double* S, int k, int lane) {
   const double2 v = *reinterpret_cast<const double2*>(S + k + 2 * lane);
   return Pair{v.x, v.y};
 }
+// raw E and N of the lane's column pair in a staged row
+__device__ __forceinline__ void l0_edges(const double* S, int lane, Pair& E, Pair& N) {
+  const float* SF = reinterpret_cast<const float*>(S + L0R_K);
+  const float2 e = *reinterpret_cast<const float2*>(SF + 2 * lane);
+  const float2 n = *reinterpret_cast<const float2*>(SF + 64 + 2 * lane);
+  E = Pair{(double)e.x, (double)e.y};
+  N = Pair{(double)n.x, (double)n.y};
+}
 
 template <bool INT>
-__device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const float* __restrict__ e0,
+                                                   const float* __restrict__ n0e,
                                                    const double* __restrict__ r, PW4 pw, double* __restrict__ rc,
                                                    int b, int I, bool outI, int J0, int J1, int lane, double* wring) {
   const int m = g.m, n0 = g.n0, mc = gc.m;
   const int xa = 2 * I, x0 = xa - 2 * lane;
   const int64_t off = (int64_t)b * g.N;
-  const double *kb = k + off, *rb = r + off;
+  const double* rb = r + off;
+  const float *eb = e0 + off, *nb = n0e + off;
   const int ys = 2 * J0 - 1;
-  const int ylast = 2 * J1 + 2;  // ingest rows end at 2J1+1, whose edges read k of row 2J1+2
+  const int ylast = 2 * J1 + 1;  // ingest rows end at 2J1+1
   auto slot = [&](int q) { return wring + (size_t)((unsigned)(q - (ys - 3)) % L0R_RING) * (RR_W * L0R_WORDS_DN); };
   auto issue = [&](int q) {
-    if (q <= ylast) l0_issue_kr(slot(q), kb, rb, x0, lane, q, n0);
+    if (q <= ylast) l0_issue_kr(slot(q), eb, nb, rb, x0, lane, q, n0);
     cpa_commit();
   };
   for (int j = 0; j < L0R_RING; ++j) issue(ys - 3 + j);
@@ -2108,25 +2172,23 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   __syncwarp();
   {
     Pair Ed;
-    edges_pair<INT>(zero, l0_pair(slot(ys - 3), L0R_K, lane), l0_pair(slot(ys - 2), L0R_K, lane), xa, ys - 3, m, Ed,
-                    N1);  // row ys−3: its N only
+    l0_edges(slot(ys - 3), lane, Ed, N1);  // row ys−3: its N only
   }
   auto ingest = [&](int q) {
     cpa_wait<2>();  // rows ≤ q+1
     __syncwarp();
     Pair E, N;
-    edges_pair<INT>(l0_pair(slot(q - 1), L0R_K, lane), l0_pair(slot(q), L0R_K, lane),
-                    l0_pair(slot(q + 1), L0R_K, lane), xa, q, m, E, N);
+    l0_edges(slot(q), lane, E, N);
     const Pair r0 = l0_pair(slot(q), L0R_R, lane);
     __syncwarp();
     issue(q + 4);  // into the slot of row q−1
     const Sten2 st = sten_pair<INT>(E, N, N1, xa, q, m, bc);
     const bool ra = RED_IS_A(q);
-    const double zr0 = (ra ? r0.a : r0.b) * rcp64(ra ? st.a.d : st.b.d);
+    const double zr0 = (ra ? r0.a : r0.b) * rcp64s(ra ? st.a.d : st.b.d);
     const bool ra1 = !ra;
     const double zr1_e = shdn(zr1), zr1_w = shup(zr1);
     const double zbl = (rbl1 - (sb1.e * (ra1 ? zr1_e : zr1) + sb1.w * (ra1 ? zr1 : zr1_w) + sb1.n * zr0 +
-                                sb1.s * zr2)) * rcp64(sb1.d);
+                                sb1.s * zr2)) * rcp64s(sb1.d);
     const Pair zp1 = ra1 ? Pair{zr1, zbl} : Pair{zbl, zr1};
     const double t = ra ? red_resid<INT, true>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc)
                         : red_resid<INT, false>(E2, N2, N3, zp3, zp2, zp1, xa, q - 2, m, bc);
@@ -2173,7 +2235,8 @@ __device__ __forceinline__ void restrict_ring_body(Geo g, Geo gc, int bc, const 
   cpa_wait<0>();
 }
 
-__global__ void __launch_bounds__(32 * RR_W, 4 * 4 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(32 * RR_W, 4 * 4 / RR_W) restrict_ring_kernel(Geo g, Geo gc, int bc, const float* __restrict__ e0,
+                                                              const float* __restrict__ n0e,
                                                               const double* __restrict__ r, PW4 pw,
                                                               double* __restrict__ rc, const int* flags) {
   const int b = blockIdx.z;
@@ -2188,19 +2251,21 @@ __global__ void __launch_bounds__(32 * RR_W, 4 * 4 / RR_W) restrict_ring_kernel(
   const bool interior = strip * 60 - 2 >= 2 && strip * 60 + 61 <= g.m - 2 && 2 * J0 - 6 >= 1 &&
                         2 * J1 + 4 <= g.m - 1;
   double* wring = l0ring + warp * L0R_WORDS_DN;
-  if (interior) restrict_ring_body<true>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1, lane, wring);
-  else restrict_ring_body<false>(g, gc, bc, k, r, pw, rc, b, I, outI, J0, J1, lane, wring);
+  if (interior) restrict_ring_body<true>(g, gc, bc, e0, n0e, r, pw, rc, b, I, outI, J0, J1, lane, wring);
+  else restrict_ring_body<false>(g, gc, bc, e0, n0e, r, pw, rc, b, I, outI, J0, J1, lane, wring);
 }
 
 template <bool INT>
-__device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, const float* __restrict__ e0,
+                                                       const float* __restrict__ n0e,
                                                        const double* __restrict__ r, pz_t* __restrict__ z_out,
                                                        const double* __restrict__ zc, PW4 pw, const PairCtx& c,
                                                        double* wring) {
   PAIR_UNPACK
 
   const int lane = c.lane, x0 = xa - 2 * lane;
-  const double *kb = k + off, *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
+  const double *rb = r + off, *zcb = zc + (int64_t)b * gc.N;
+  const float *eb = e0 + off, *nb = n0e + off;
   const int nc0 = gc.n0;
   const int I0 = x0 >> 1;
   const int mcl = m / 2;
@@ -2210,7 +2275,7 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
   auto issue = [&](int q) {
     if (q <= ylast) {
       double* S = slot(q);
-      l0_issue_kr(S, kb, rb, x0, lane, q, n0);
+      l0_issue_kr(S, eb, nb, rb, x0, lane, q, n0);
       // prolongation inputs of row q's red node: z₁ rows q>>1 (and +1 on odd rows), columns
       // I0 … I0+32; centre weights of the odd rows' cells
       const int Jc = q >> 1, ci = I0 + lane;
@@ -2239,27 +2304,23 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
     if (RED_IS_A(y)) {
       const Sten s = mk_sten<INT>(E.a, Wa, N.a, Nm.a, xa, y, m, bc);
       const double c00 = (INT || (unsigned)xa < (unsigned)n0) ? S[L0R_ZC0 + lane] : 0.0;
-      return rr.a * rcp64(s.d) + c00;
+      return rr.a * rcp64s(s.d) + c00;
     }
     const Sten s = mk_sten<INT>(E.b, E.a, N.b, Nm.b, xb, y, m, bc);
     double p = 0.0;
     if (INT || (unsigned)xb < (unsigned)n0)
       p = l0r_pw(S, lane, 0) * S[L0R_ZC0 + lane] + l0r_pw(S, lane, 1) * S[L0R_ZC0 + lane + 1] +
           l0r_pw(S, lane, 2) * S[L0R_ZC1 + lane] + l0r_pw(S, lane, 3) * S[L0R_ZC1 + lane + 1];
-    return rr.b * rcp64(s.d) + p;
+    return rr.b * rcp64s(s.d) + p;
   };
   for (int j = 0; j < L0R_RING; ++j) issue(y0 - 3 + j);  // rows y0−3 … y0+1
   const Pair zero{0.0, 0.0};
   cpa_wait<1>();  // rows y0−3 … y0
   __syncwarp();
   Pair Ed, N3, E2, N2, E1, N1;
-  {
-    const Pair km = l0_pair(slot(y0 - 3), L0R_K, lane), k0 = l0_pair(slot(y0 - 2), L0R_K, lane),
-               k1 = l0_pair(slot(y0 - 1), L0R_K, lane), k2 = l0_pair(slot(y0), L0R_K, lane);
-    edges_pair<INT>(zero, km, k0, xa, y0 - 3, m, Ed, N3);
-    edges_pair<INT>(km, k0, k1, xa, y0 - 2, m, E2, N2);
-    edges_pair<INT>(k0, k1, k2, xa, y0 - 1, m, E1, N1);
-  }
+  l0_edges(slot(y0 - 3), lane, Ed, N3);
+  l0_edges(slot(y0 - 2), lane, E2, N2);
+  l0_edges(slot(y0 - 1), lane, E1, N1);
   double qa = RV(slot(y0 - 2), y0 - 2, l0_pair(slot(y0 - 2), L0R_R, lane), E2, N2, N3);
   double qb = RV(slot(y0 - 1), y0 - 1, l0_pair(slot(y0 - 1), L0R_R, lane), E1, N1, N2);
   __syncwarp();
@@ -2276,8 +2337,7 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
     __syncwarp();
     const double *S0 = slot(t), *S1 = slot(t + 1), *S2 = slot(t + 2), *S3 = slot(t + 3);
     Pair E2n, N2n;
-    edges_pair<INT>(l0_pair(S1, L0R_K, lane), l0_pair(S2, L0R_K, lane), l0_pair(S3, L0R_K, lane), xa, t + 2, m,
-                    E2n, N2n);
+    l0_edges(S2, lane, E2n, N2n);
     const Pair r0 = l0_pair(S0, L0R_R, lane), r1 = l0_pair(S1, L0R_R, lane);
     // red value of row t+2 (red column a iff row t+2 is even, i.e. as row t)
     double qc;
@@ -2287,14 +2347,14 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
       if constexpr (ra0) {
         const Sten sq = mk_sten<INT>(E2n.a, Wa, N2n.a, N1.a, xa, t + 2, m, bc);
         const double c00 = (INT || (unsigned)xa < (unsigned)n0) ? S2[L0R_ZC0 + lane] : 0.0;
-        qc = rr.a * rcp64(sq.d) + c00;
+        qc = rr.a * rcp64s(sq.d) + c00;
       } else {
         const Sten sq = mk_sten<INT>(E2n.b, E2n.a, N2n.b, N1.b, xb, t + 2, m, bc);
         double pz = 0.0;
         if (INT || (unsigned)xb < (unsigned)n0)
           pz = l0r_pw(S2, lane, 0) * S2[L0R_ZC0 + lane] + l0r_pw(S2, lane, 1) * S2[L0R_ZC0 + lane + 1] +
                l0r_pw(S2, lane, 2) * S2[L0R_ZC1 + lane] + l0r_pw(S2, lane, 3) * S2[L0R_ZC1 + lane + 1];
-        qc = rr.b * rcp64(sq.d) + pz;
+        qc = rr.b * rcp64s(sq.d) + pz;
       }
     }
     __syncwarp();
@@ -2303,10 +2363,10 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
     const double qb_e = shdn(qb), qb_w = shup(qb);
     const Sten& sb = ra1 ? st1.b : st1.a;
     const double odb = sb.e * (ra1 ? qb_e : qb) + sb.w * (ra1 ? qb : qb_w) + sb.n * qc + sb.s * qa;
-    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64(sb.d);
+    const double zbp1 = ((ra1 ? r1.b : r1.a) - odb) * rcp64s(sb.d);
     const double zb0_e = shdn(zb0), zb0_w = shup(zb0);
     const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
-    const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64(sr0.d);
+    const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64s(sr0.d);
     if (t >= y0) {
       pz_t* out = z_out + off + (int64_t)t * n0;
       const double va = ra0 ? zred : zb0, vb = ra0 ? zb0 : zred;
@@ -2335,7 +2395,8 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
 // 16 one-warp CTAs per SM (128 registers, no spills): the sweep is bound by dependent fp64 latency at
 // 60% issue with 12 warps per SM; 16 gave 3.68 → 3.98 TB/s at 2048² and 3.13 → 3.26 at 1024²
 // (profiles/ab_r2/ring_occupancy.txt; 20 CTAs for the restriction spill and lose)
-__global__ void __launch_bounds__(32 * SUR_W, 4 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const double* __restrict__ k,
+__global__ void __launch_bounds__(32 * SUR_W, 4 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const float* __restrict__ e0,
+                                                               const float* __restrict__ n0e,
                                                                const double* __restrict__ r,
                                                                pz_t* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,
@@ -2345,8 +2406,8 @@ __global__ void __launch_bounds__(32 * SUR_W, 4 * 4 / SUR_W) smooth_up_ring_kern
   extern __shared__ __align__(16) double l0ring[];
   double* wring = l0ring + (threadIdx.x >> 5) * L0R_WORDS_UP;
   const bool interior3 = interior && c.y1 <= g.m - 3;
-  const double2 gd = interior3 ? smooth_up_ring_body<true>(g, gc, bc, k, r, z_out, zc, pw, c, wring)
-                               : smooth_up_ring_body<false>(g, gc, bc, k, r, z_out, zc, pw, c, wring);
+  const double2 gd = interior3 ? smooth_up_ring_body<true>(g, gc, bc, e0, n0e, r, z_out, zc, pw, c, wring)
+                               : smooth_up_ring_body<false>(g, gc, bc, e0, n0e, r, z_out, zc, pw, c, wring);
   double gamma, dcorr;
   if (reduce2_last(gd.x, gd.y, partial, maxp, counter, b, gamma, dcorr) && threadIdx.x == 0) {
     const double delta = gamma + dcorr;
@@ -2967,8 +3028,9 @@ size_t solver_bytes(int m, int B, int hist_cap) {
     const bool last = g <= 4 || g % 2 != 0;
     // level 0: u r r2 z z2 p0 p1 (+k by caller); levels ≥ 1: C (fp64), E N NE NW (fp32), r z z2;
     // fp32 centre weights (4 per cell) on every level with a coarser one
-    tot += N * B * (lev == 0 ? 8 * sizeof(double) : 4 * sizeof(double) + 4 * sizeof(float)) +
-           (last ? 0 : 4 * mcl * mcl * B * sizeof(float)) + 5 * 256;
+    // level 0 also holds the two fp32 raw-edge arrays of the preconditioner sweeps
+    tot += N * B * (lev == 0 ? 8 * sizeof(double) + 2 * sizeof(float) : 4 * sizeof(double) + 4 * sizeof(float)) +
+           (last ? 0 : 4 * mcl * mcl * B * sizeof(float)) + 7 * 256;
     ++lev;
     if (last) {
       tot += (N > 1089 ? band_doubles(g + 1) : 2 * N * N) * B * sizeof(double);
@@ -3015,8 +3077,9 @@ void solver_prepare(Ctx* ctx, int m, int B, int hist_cap) {
     L.k = nullptr;  // level 0's k is the caller's buffer
     const bool rows = l > 0 || nl == 1;
     L.C = rows ? (double*)take(vb) : nullptr;
-    L.E = rows ? (float*)take(fb) : nullptr;
-    L.Nw = rows ? (float*)take(fb) : nullptr;
+    // level 0 of a multilevel solve: the raw fp32 edge weights of the preconditioner sweeps
+    L.E = (rows || (l == 0 && nl > 1)) ? (float*)take(fb) : nullptr;
+    L.Nw = (rows || (l == 0 && nl > 1)) ? (float*)take(fb) : nullptr;
     L.NE = rows ? (float*)take(fb) : nullptr;
     L.NW = rows ? (float*)take(fb) : nullptr;
     const size_t cb = sizeof(float) * (size_t)(L.m / 2) * (L.m / 2) * B;
@@ -3112,7 +3175,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
       smem_attr(restrict_ring_kernel, L0R_SMEM_DN);
       KScope ks(ctx, "mg_restrict_r.L0");
       restrict_ring_kernel<<<restrict_grid_w(C.m, B, RR_W), 32 * RR_W, L0R_SMEM_DN, st>>>(
-          geo_of(L), geo_of(C), bc, L.k, w.r_cur, pw_of(L), C.r, w.flags);
+          geo_of(L), geo_of(C), bc, L.E, L.Nw, w.r_cur, pw_of(L), C.r, w.flags);
       continue;
     }
     smem_attr(c_down_ring_kernel, DN_RING_SMEM);
@@ -3141,7 +3204,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
       smem_attr(smooth_up_ring_kernel, L0R_SMEM_UP);
       KScope ks(ctx, "mg_smooth_up_r.L0");
       smooth_up_ring_kernel<<<march_grid_w(L.m, B, SUR_W), 32 * SUR_W, L0R_SMEM_UP, st>>>(
-          geo_of(L), geo_of(C), bc, L.k, w.r_cur, reinterpret_cast<pz_t*>(L.z2), C.z2, pw_of(L), w.scal, w.flags, part,
+          geo_of(L), geo_of(C), bc, L.E, L.Nw, w.r_cur, reinterpret_cast<pz_t*>(L.z2), C.z2, pw_of(L), w.scal, w.flags, part,
           w.max_parts, w.counter);
       continue;
     }
@@ -3175,13 +3238,17 @@ void mg_setup(Ctx* ctx, const osc_problem* prob, int B) {
       if (l == 0)
         galerkin_tile_kernel<true><<<grid, GT_THREADS, galerkin_tile_smem(true), st>>>(
             L0.k, L9{nullptr, nullptr, nullptr, nullptr, nullptr, F.m, F.m + 1, F.N}, bc, w.opdep, geo_of(C), C.C,
-            C.E, C.Nw, C.NE, C.NW, F.pw[0], F.pw[1], F.pw[2], F.pw[3]);
+            C.E, C.Nw, C.NE, C.NW, F.pw[0], F.pw[1], F.pw[2], F.pw[3], L0.E, L0.Nw);
       else
         galerkin_tile_kernel<false><<<grid, GT_THREADS, galerkin_tile_smem(false), st>>>(
             nullptr, l9_of(F), bc, w.opdep, geo_of(C), C.C, C.E, C.Nw, C.NE, C.NW, F.pw[0], F.pw[1], F.pw[2],
-            F.pw[3]);
+            F.pw[3], nullptr, nullptr);
     }
   } else {  // REDISCRETIZE: level-0 rows (5-point) into scratch (u, r, r2 are free until pcg_init)
+    {
+      KScope ks(ctx, "mg_setup.edges0");
+      edges0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, L0.k, L0.E, L0.Nw);
+    }
     {
       KScope ks(ctx, "mg_setup.rows");
       rows0_kernel<<<dim3(nblocks(L0.N), B), NT, 0, st>>>(g0, bc, L0.k, w.u, reinterpret_cast<float*>(L0.r),

@@ -79,6 +79,30 @@ def test_ce_fields_vs_oracle(P, ctx, port, m, model):
         assert relmax(coarse[b], port.restrict(op.n, m, u, m // 2)) < FIELD_TOL
 
 
+def test_ce_spec_known_answers(P, ctx):
+    """SPEC.md:190-192 on the device path: ξ = 0 gives u = 0 (and k = exp(0) = 1); ξ = e₁ gives the
+    constant field √λ₁/√s (the unitary DFT of a unit impulse at the origin); a unit impulse elsewhere
+    gives |u| ≤ √2·√λ_q/√s pointwise with the Hartley phase cos + sin."""
+    api = P.api
+    for m, model in ((8, api.CovarianceModel.separable_exponential(1.0, 0.3)),
+                     (16, api.CovarianceModel.matern(1.0, 0.3, 1.5))):  # the second one is padded (J > 0)
+        op = api.build_operator(api.GridSpec.square(m), model)
+        n, s = op.n, op.s
+        xi = np.zeros((3, s))
+        xi[1, 0] = 1.0
+        q0, q1 = 3, 2
+        xi[2, q1 * n + q0] = 1.0
+        f = op.sample_fields(xi, fine=True, ctx=ctx).reshape(3, m + 1, m + 1)
+        assert np.all(f[0] == 0.0)
+        assert np.max(np.abs(f[1] - np.sqrt(op.eigenvalues[0]) / n)) < 1e-14
+        p1, p0 = np.meshgrid(np.arange(m + 1), np.arange(m + 1), indexing="ij")
+        ang = 2 * np.pi * (p0 * q0 + p1 * q1) / n
+        want = np.sqrt(op.eigenvalues[q1 * n + q0]) / n * (np.cos(ang) + np.sin(ang))
+        assert np.max(np.abs(f[2] - want)) < 1e-13
+        k = op.sample_fields(xi[:1], fine=True, exp=True, ctx=ctx)
+        assert np.all(k == 1.0)
+
+
 def test_ce_linearity_large(P, ctx):
     """Size-independent property at config-2 size (1024², n = 2048): the field is linear in ξ."""
     api = P.api

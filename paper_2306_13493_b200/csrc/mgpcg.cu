@@ -970,12 +970,13 @@ __device__ __forceinline__ Pair ld2(const double* __restrict__ base, int xa, int
   return Pair{ldv<INT>(base, xa, y, n0), ldv<INT>(base, xa + 1, y, n0)};
 }
 
-// Storage type of the level-0 search direction p and preconditioned residual z. fp32 storage (fp64
-// arithmetic; u and r keep using one fp64 p, so r stays the residual of u) was measured: same
-// iteration counts (14.11 / 14.10 on config 4) and the same time per pcg_update launch — the kernel is
-// bound by load/store instructions in flight, not by DRAM bytes — so they stay fp64
-// (profiles/ab_r2/pz32_vs_pz64.txt).
-using pz_t = double;
+// Storage types of the level-0 search direction p and preconditioned residual z. fp32 storage (fp64
+// arithmetic; u and r keep using one fp64 p, so r stays the residual of u) was measured twice, before
+// and after the pcg_update prefetch: same iteration counts; the up sweep gains 4–7% from the narrower
+// z store, pcg_update loses up to 8% at 1024² on the float loads and conversions; the step is
+// unchanged within the run-to-run spread, so both stay fp64 (profiles/ab_r2/pz32_vs_pz64.txt).
+using p_t = double;
+using z_t = double;
 
 // Edge weights of row y at both columns from k rows y−1, y, y+1. Triangle means in the
 // reference's vertex order with ·(1/3) instead of /3 (≤ 1 ulp per coefficient); each edge is
@@ -1210,8 +1211,8 @@ __global__ void __launch_bounds__(MT) pcg_apply_kernel(Geo g, int bc, const doub
 // the update. Reads k, z, p_old, r, u; writes p_new, u, r_next.
 template <bool INT>
 __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double* __restrict__ k,
-                                                     const pz_t* __restrict__ z, const pz_t* __restrict__ p_old,
-                                                     pz_t* __restrict__ p_new, double* __restrict__ u,
+                                                     const z_t* __restrict__ z, const p_t* __restrict__ p_old,
+                                                     p_t* __restrict__ p_new, double* __restrict__ u,
                                                      const double* __restrict__ r, double* __restrict__ r_out,
                                                      double* scal, int* flags, const PairCtx& c) {
   PAIR_UNPACK
@@ -1220,7 +1221,8 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
   const double beta = first ? 0.0 : scal[b * S_NSCAL + S_BETA];
   const double alpha = scal[b * S_NSCAL + S_ALPHA];
   const double *kb = k + off, *rb = r + off;
-  const pz_t *zb = z + off, *pb = p_old + off;
+  const z_t* zb = z + off;
+  const p_t* pb = p_old + off;
   double* ub = u + off;
   auto comb = [&](Pair zz, Pair oo) {
     return first ? zz : Pair{fma(beta, oo.a, zz.a), fma(beta, oo.b, zz.b)};
@@ -1266,14 +1268,14 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
     const int64_t row = off + (int64_t)y * n0;
     if (outa) {
       const double rn = fma(-alpha, fma(st.a.d, p0.a, od.a), r0.a);
-      p_new[row + xa] = (pz_t)p0.a;
+      p_new[row + xa] = (p_t)p0.a;
       u[row + xa] = fma(alpha, p0.a, u0.a);
       r_out[row + xa] = rn;
       rr = fma(rn, rn, rr);
     }
     if (outb) {
       const double rn = fma(-alpha, fma(st.b.d, p0.b, od.b), r0.b);
-      p_new[row + xb] = (pz_t)p0.b;
+      p_new[row + xb] = (p_t)p0.b;
       u[row + xb] = fma(alpha, p0.b, u0.b);
       r_out[row + xb] = rn;
       rr = fma(rn, rn, rr);
@@ -1285,9 +1287,9 @@ __device__ __forceinline__ double pcg_update_cg_body(Geo g, int bc, const double
 
 constexpr int PU_W = 4;  // warps per CTA of pcg_update (A/B knob: 1 and 2 warps are no faster, it is DRAM-bound)
 __global__ void __launch_bounds__(32 * PU_W, 16 / PU_W) pcg_update_cg_kernel(Geo g, int bc, double tol, const double* __restrict__ k,
-                                                              const pz_t* __restrict__ z,
-                                                              const pz_t* __restrict__ p_old,
-                                                              pz_t* __restrict__ p_new, double* __restrict__ u,
+                                                              const z_t* __restrict__ z,
+                                                              const p_t* __restrict__ p_old,
+                                                              p_t* __restrict__ p_new, double* __restrict__ u,
                                                               const double* __restrict__ r, double* __restrict__ r_out,
                                                               double* scal, int* flags, double2* partial, int maxp,
                                                               unsigned* counter, int* n_active, double* hist,
@@ -2258,7 +2260,7 @@ __global__ void __launch_bounds__(32 * RR_W, 4 * 4 / RR_W) restrict_ring_kernel(
 template <bool INT>
 __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, const float* __restrict__ e0,
                                                        const float* __restrict__ n0e,
-                                                       const double* __restrict__ r, pz_t* __restrict__ z_out,
+                                                       const double* __restrict__ r, z_t* __restrict__ z_out,
                                                        const double* __restrict__ zc, PW4 pw, const PairCtx& c,
                                                        double* wring) {
   PAIR_UNPACK
@@ -2368,14 +2370,14 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
     const double s2 = sr0.e * (ra0 ? zb0 : zb0_e) + sr0.w * (ra0 ? zb0_w : zb0) + sr0.n * zbp1 + sr0.s * zbm;
     const double zred = ((ra0 ? r0.a : r0.b) - s2) * rcp64s(sr0.d);
     if (t >= y0) {
-      pz_t* out = z_out + off + (int64_t)t * n0;
+      z_t* out = z_out + off + (int64_t)t * n0;
       const double va = ra0 ? zred : zb0, vb = ra0 ? zb0 : zred;
       if (outa) {
-        out[xa] = (pz_t)va;
+        out[xa] = (z_t)va;
         rz = fma(r0.a, va, rz);
       }
       if (outb) {
-        out[xb] = (pz_t)vb;
+        out[xb] = (z_t)vb;
         rz = fma(r0.b, vb, rz);
       }
       if (ra0 ? outa : outb) dc = fma(zred - qa, s2, dc);
@@ -2398,7 +2400,7 @@ __device__ __forceinline__ double2 smooth_up_ring_body(Geo g, Geo gc, int bc, co
 __global__ void __launch_bounds__(32 * SUR_W, 4 * 4 / SUR_W) smooth_up_ring_kernel(Geo g, Geo gc, int bc, const float* __restrict__ e0,
                                                                const float* __restrict__ n0e,
                                                                const double* __restrict__ r,
-                                                               pz_t* __restrict__ z_out,
+                                                               z_t* __restrict__ z_out,
                                                                const double* __restrict__ zc, PW4 pw, double* scal,
                                                                int* flags, double2* partial, int maxp,
                                                                unsigned* counter) {
@@ -3204,7 +3206,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
       smem_attr(smooth_up_ring_kernel, L0R_SMEM_UP);
       KScope ks(ctx, "mg_smooth_up_r.L0");
       smooth_up_ring_kernel<<<march_grid_w(L.m, B, SUR_W), 32 * SUR_W, L0R_SMEM_UP, st>>>(
-          geo_of(L), geo_of(C), bc, L.E, L.Nw, w.r_cur, reinterpret_cast<pz_t*>(L.z2), C.z2, pw_of(L), w.scal, w.flags, part,
+          geo_of(L), geo_of(C), bc, L.E, L.Nw, w.r_cur, reinterpret_cast<z_t*>(L.z2), C.z2, pw_of(L), w.scal, w.flags, part,
           w.max_parts, w.counter);
       continue;
     }
@@ -3309,8 +3311,8 @@ void pcg_iteration(Ctx* ctx, const osc_problem* prob, int B, double* r_in, doubl
   {
     KScope ks(ctx, "pcg_update");
     pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, ctx->stream>>>(
-        geo_of(L0), prob->bc, prob->tol, L0.k, reinterpret_cast<const pz_t*>(L0.z2), reinterpret_cast<const pz_t*>(p_old),
-        reinterpret_cast<pz_t*>(p_new), w.u, r_in, r_out, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active,
+        geo_of(L0), prob->bc, prob->tol, L0.k, reinterpret_cast<const z_t*>(L0.z2), reinterpret_cast<const p_t*>(p_old),
+        reinterpret_cast<p_t*>(p_new), w.u, r_in, r_out, w.scal, w.flags, part, w.max_parts, w.counter, w.n_active,
         w.hist, w.hist_cap);
   }
   w.r_cur = r_out;
@@ -3479,8 +3481,8 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
         KScope ks(ctx, "pcg_update");
         double* r_next = (w.r_cur == L0.r) ? w.r2 : L0.r;
         pcg_update_cg_kernel<<<march_grid_w(L0.m, B, PU_W), 32 * PU_W, 0, st>>>(
-            g0, bc, prob->tol, L0.k, reinterpret_cast<const pz_t*>(L0.z2), reinterpret_cast<const pz_t*>(p_old),
-            reinterpret_cast<pz_t*>(p_new), w.u, w.r_cur, r_next, w.scal, w.flags, part, w.max_parts, w.counter,
+            g0, bc, prob->tol, L0.k, reinterpret_cast<const z_t*>(L0.z2), reinterpret_cast<const p_t*>(p_old),
+            reinterpret_cast<p_t*>(p_new), w.u, w.r_cur, r_next, w.scal, w.flags, part, w.max_parts, w.counter,
             w.n_active, w.hist, w.hist_cap);
         w.r_cur = r_next;
       }

@@ -497,7 +497,7 @@ __device__ __forceinline__ void ldg256(const double2* p, double2& a, double2& b,
                : "l"(p), "l"(pol));
 }
 
-// Column pass with two columns per thread (32 ≤ n ≤ 4096; ce_cols_t_kernel below and above): the same stages as ce_cols_t_kernel
+// Column pass with two columns per thread (32 ≤ n ≤ 2048; ce_cols_t_kernel below and above): the same stages as ce_cols_t_kernel
 // applied to columns j and j + 1 held by one thread, so each barrier interval carries two independent
 // butterflies (twice the loads in flight) and every twiddle load serves both columns.
 template <int LOGN, int R, int LNS>
@@ -635,9 +635,10 @@ void launch_t(Ctx* ctx, const Level* L, const double* sqrt_lam, const double* xi
   };
   if (xi_dev) rows(std::integral_constant<int, PL::NTR>{}, std::true_type{});
   else rows(std::integral_constant<int, PL::NT>{}, std::false_type{});
-  // two columns per thread for 32 ≤ n ≤ 4096, where it fits 128 registers without spills (config 2
-  // column pass 277.7 → 208.6 ms per 12288 samples against one column per thread)
-  if constexpr (LOGN >= 5 && LOGN <= 12) {
+  // two columns per thread for 32 ≤ n ≤ 2048 (config 2: 277.7 → 208.6 ms per 12288 samples against one
+  // column per thread). At n = 4096 the 512-thread, 128-register CTA leaves one CTA per SM: one
+  // column per thread (64 registers, two CTAs) is faster there (72.3 → 66.7 µs per sample).
+  if constexpr (LOGN >= 5 && LOGN <= 11) {
     auto kern = ce_cols2_t_kernel<LOGN>;
     smem_attr(kern, (2 * sm));
     KScope ks(ctx, "ce_cols");

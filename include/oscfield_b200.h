@@ -20,6 +20,9 @@
  *   osc_build_spectrum  ← build_operator (embedding.hpp:112-113, src/embedding.cpp:114-151)
  *   osc_build_spectrum_device ← build_operator with build_first_row + spectrum on the device
  *   osc_level_create    ← EmbeddingOperator::from_parts + truncated (embedding.cpp:90-112,153-163)
+ *   osc_mlmc_adaptive   ← estimate_adaptive (src/estimators.cpp:289-378; mlmc_estimate / mc_estimate
+ *                         :398-418) as a GPU-resident driver: all levels of a round draw concurrently,
+ *                         the moments stay in HBM as running sums
  *   osc_normals         ← NormalStream::fill (include/oscfield/rng.hpp:30-43, src/rng.cpp:42-67)
  *
  * Errors: every function returns an osc_status. Non-zero codes map onto the reference's
@@ -232,6 +235,11 @@ int osc_level_draws(osc_level* level, const osc_problem* problem, uint64_t seed,
  * chunking of the same samples changes the summation order (~1e-16 relative). */
 int osc_level_sums_reset(osc_level* level, double shift_y, double shift_q);
 int osc_level_sums_read(osc_level* level, double out[7]);
+/* Moves the running sums to new shifts without the samples (device side, one thread):
+ * Σ(v−K') = Σ(v−K) − n·d and Σ(v−K')² = Σ(v−K)² − 2d·Σ(v−K) + n·d² with d = K' − K. A driver that
+ * cannot know the level mean before its first batch starts at shift 0 and re-centres after the pilot,
+ * so the later (much larger) batches accumulate without cancellation. */
+int osc_level_sums_reshift(osc_level* level, double shift_y, double shift_q);
 
 /* Residual history of failing samples (SolverError::history, fem.cpp:359-379). With hist_cap > 0, an
  * osc_level_draws call that returns OSC_ERR_SOLVER re-draws its first failing slot alone with the
@@ -282,6 +290,69 @@ int osc_comm_allreduce_level_sums(osc_comm* comm, osc_level* level, double out[7
 /* ncclAllGather of n_per_rank doubles per rank (host in, host out, rank order): the (q_f, q_c) slots
  * of contiguous shards, so every rank can run the reference's slot-order Welford bit-identically. */
 int osc_comm_allgather(osc_comm* comm, const double* local, int64_t n_per_rank, double* all);
+
+/* ---- GPU-resident adaptive MLMC driver ---------------------------------------
+ * estimate_adaptive (src/estimators.cpp:289-378) with the level loop turned into waves: within one
+ * allocation pass every level's target N_ℓ = ⌈2ε⁻²·(Σ_j √(C_j V_j))·√(V_ℓ/C_ℓ)⌉ (C_ℓ = h_ℓ^−γ) depends
+ * only on the moments at the start of the pass (:322-338), so all levels that need samples draw AT THE
+ * SAME TIME — one context (stream + workspace) and one host thread per level and device — instead of
+ * one level after the other; small levels, which cannot fill 148 SMs alone, run under the large ones.
+ * The moments never pass through per-sample host arrays: each level accumulates its running sums in
+ * HBM (osc_level_sums_*), re-centred on the pilot mean after the first wave; with several devices
+ * each level's range is cut into contiguous per-device chunks and ONE all-reduce per wave combines
+ * the sums of all levels (8 doubles per level). Levels are set up on the device
+ * (osc_level_create_device) unless `spectrum` supplies the eigenvalues.
+ * The decisions follow the reference: pilot = max(2, pilot_n) samples per level, at most 64 passes,
+ * bias from the weak-error model c_α h^α on a single level, else Richardson |E[Y_L]|/|1 − r·2^α|
+ * (r = c_alpha_tilde_ratio when the finest difference has a smoothed coarse term, else 1; a
+ * denominator below 0.1 is OSC_ERR_NUMERICAL), a new finest level while bias² > ε²/2 and L < l_max
+ * (the previous finest level then changes its sampling law and is redrawn when it was smoothed),
+ * the smoothing rule of make_level_plan (:169-198, choose_k_ell :238-275, coarsest_level_bound
+ * :487-494). Sample i of level ℓ is NormalStream(seed, ℓ, i), as in every other entry point. */
+enum { OSC_SMOOTHING_OFF = 0, OSC_SMOOTHING_HALF_SPECTRUM = 1, OSC_SMOOTHING_ADAPTIVE = 2 };
+#define OSC_MLMC_MAX_LEVELS 26
+
+/* Optional source of a level's eigenvalues (OSC1 files, the reference's build_operator, …): fills J, s
+ * and a malloc'd array of s = (2(m+J))² eigenvalues that the driver releases with free(). Non-zero
+ * return = failure (reported as OSC_ERR_EMBEDDING). */
+typedef int (*osc_spectrum_fn)(void* user, int m, int* J, int64_t* s, double** eigenvalues);
+
+typedef struct {
+  int family;            /* OSC_COV_* */
+  double sigma2, lambda, nu_or_p;
+  double h0;             /* coarsest mesh width, a negative power of two */
+  double eps;            /* RMSE target */
+  int initial_levels;    /* ≥ 1 */
+  int l_max;             /* finest admissible level index */
+  int allow_extension;   /* 1 = mlmc_estimate; 0 = the single-grid mc_estimate path (sampling error only) */
+  uint64_t seed;
+  int pilot_n;
+  double gamma_model, alpha, c_alpha, c_ratio, c_alpha_tilde_ratio; /* EstimatorOptions, estimators.hpp:66-80 */
+  int smoothing;         /* OSC_SMOOTHING_* */
+  int use_coarse_s, lstar_only;
+  int concurrent_levels; /* 1 (default use): all levels of a wave at once; 0: one level after the other */
+  osc_spectrum_fn spectrum; /* NULL: device level setup */
+  void* spectrum_user;
+} osc_mlmc_options;
+
+typedef struct {
+  double estimate, bias_estimate, sampling_error, total_cost_model, total_cost_wall;
+  int converged, n_levels, passes, waves;
+  int64_t n[OSC_MLMC_MAX_LEVELS], k_trunc[OSC_MLMC_MAX_LEVELS], redrawn[OSC_MLMC_MAX_LEVELS];
+  double mean_y[OSC_MLMC_MAX_LEVELS], var_y[OSC_MLMC_MAX_LEVELS], mean_q[OSC_MLMC_MAX_LEVELS],
+      var_q[OSC_MLMC_MAX_LEVELS], h[OSC_MLMC_MAX_LEVELS], n_real[OSC_MLMC_MAX_LEVELS],
+      wall_per_sample[OSC_MLMC_MAX_LEVELS];
+  double setup_s, draw_s, total_s; /* level setup, waves (elapsed, levels overlapped), whole call */
+  int64_t samples_total, gpu_launches;
+  char message[256];
+} osc_mlmc_report;
+
+/* devices NULL → 0..n_devices-1; n_devices ≤ 0 → the calling thread's current device. */
+int osc_mlmc_adaptive(int n_devices, const int* devices, const osc_problem* problem,
+                      const osc_mlmc_options* options, osc_mlmc_report* report);
+/* The truncation count k_ℓ the driver uses on mesh width h for an embedding with padding J and s
+ * entries (0: no smoothing on that level). */
+int64_t osc_mlmc_k_trunc(const osc_mlmc_options* options, double h, int J, int64_t s);
 
 /* summarize_draws: one-pass Welford over slot-ordered draws (estimators.cpp:82-101).
  * out = [n, mean_y, var_y, mean_q, var_q]; var only when n ≥ 2. q_coarse may be NULL. */

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 LIB_PATH = os.environ.get("OSC_LIB") or os.path.join(HERE, "libosc_b200.so")
 HEADER = os.path.join(ROOT, "include", "oscfield_b200.h")
 SOURCES = ["csrc/capi.cu", "csrc/ce_sample.cu", "csrc/mgpcg.cu", "csrc/level_setup.cu", "csrc/setup.cpp",
-           "csrc/group.cpp"]
+           "csrc/group.cpp", "csrc/driver.cpp"]
 DEPS = SOURCES + ["csrc/osc_internal.cuh", "csrc/osc_device.cuh"]
 
 NVCC_FLAGS = [
@@ -47,6 +47,7 @@ EXPORTS = [
     "osc_group_level_destroy", "osc_group_level_at", "osc_group_level_draws", "osc_group_level_sums_reset",
     "osc_group_level_sums_allreduce", "osc_comm_unique_id", "osc_comm_create", "osc_comm_destroy",
     "osc_comm_allreduce_level_sums", "osc_comm_allgather",
+    "osc_level_sums_reshift", "osc_mlmc_adaptive", "osc_mlmc_k_trunc",
 ]
 
 

@@ -798,6 +798,17 @@ int osc_level_sums_reset(osc_level* L, double shift_y, double shift_q) {
   });
 }
 
+int osc_level_sums_reshift(osc_level* L, double shift_y, double shift_q) {
+  return guarded([&] {
+    OSC_REQUIRE(L, "osc_level_sums_reshift: null level");
+    OSC_REQUIRE(L->sums_on, "osc_level_sums_reshift: running sums not enabled (osc_level_sums_reset)");
+    set_device(L->ctx);
+    level_sums_reshift_launch(L->ctx, L->run_sums.as<double>(), shift_y - L->shift_y, shift_q - L->shift_q);
+    L->shift_y = shift_y;
+    L->shift_q = shift_q;
+  });
+}
+
 int osc_level_sums_read(osc_level* L, double out[7]) {
   return guarded([&] {
     OSC_REQUIRE(L && out, "osc_level_sums_read: null argument");

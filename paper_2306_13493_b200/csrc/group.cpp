@@ -101,6 +101,13 @@ void shard_range(int64_t from, int64_t to, int g, int G, int64_t& lo, int64_t& h
 
 using namespace osc;
 
+struct osc_group;
+namespace osc {
+// one grouped fp64 sum all-reduce over the group's communicators (device buffers, one per device, on
+// each device's group-context stream), then a synchronise: the collective of the MLMC driver
+void group_allreduce_f64(osc_group* g, double* const* send, double* const* recv, size_t count);
+}
+
 struct osc_group {
   std::vector<int> devices;
   std::vector<osc_ctx*> ctx;
@@ -152,6 +159,22 @@ void per_device(const osc_group* g, F&& fn) {
     if (e) std::rethrow_exception(e);
 }
 }  // namespace
+
+void osc::group_allreduce_f64(osc_group* g, double* const* send, double* const* recv, size_t count) {
+  const int G = (int)g->devices.size();
+  const Nccl& N = nccl();
+  nccl_check(N.GroupStart(), "ncclGroupStart");
+  for (int i = 0; i < G; ++i) {
+    OSC_CUDA(cudaSetDevice(g->devices[i]));
+    nccl_check(N.AllReduce(send[i], recv[i], count, ncclFloat64, ncclSum, g->comm[i], g->ctx[i]->stream),
+               "ncclAllReduce");
+  }
+  nccl_check(N.GroupEnd(), "ncclGroupEnd");
+  for (int i = 0; i < G; ++i) {
+    OSC_CUDA(cudaSetDevice(g->devices[i]));
+    OSC_CUDA(cudaStreamSynchronize(g->ctx[i]->stream));
+  }
+}
 
 extern "C" {
 

@@ -2999,6 +2999,15 @@ __global__ void level_sums_kernel(const double* __restrict__ qf, const double* _
   if (threadIdx.x == 0) sums[0] += B;
 }
 
+// the running sums re-centred on shifts moved by (dy, dq): no sample is touched
+__global__ void level_sums_reshift_kernel(double* sums, double dy, double dq) {
+  const double n = sums[0], sy = sums[1], sq = sums[3];
+  sums[2] = sums[2] - 2.0 * dy * sy + n * dy * dy;
+  sums[1] = sy - n * dy;
+  sums[4] = sums[4] - 2.0 * dq * sq + n * dq * dq;
+  sums[3] = sq - n * dq;
+}
+
 inline int nblocks(int64_t N) { return (int)((N + NT - 1) / NT); }
 inline int march_strips(int m) { return (m + 1 + 59) / 60; }  // 60 written columns per warp strip
 inline dim3 march_grid(int m, int /*hx*/, int B) {
@@ -3562,6 +3571,12 @@ void level_sums_launch(Ctx* ctx, const double* qf, const double* qc, int B, doub
                        double shift_q, double* sums_dev) {
   KScope ks(ctx, "level_sums");
   level_sums_kernel<<<1, 256, 0, ctx->stream>>>(qf, qc, B, shift_y, shift_q, sums_dev);
+  OSC_CUDA(cudaGetLastError());
+}
+
+void level_sums_reshift_launch(Ctx* ctx, double* sums_dev, double dy, double dq) {
+  KScope ks(ctx, "level_sums");
+  level_sums_reshift_kernel<<<1, 1, 0, ctx->stream>>>(sums_dev, dy, dq);
   OSC_CUDA(cudaGetLastError());
 }
 

@@ -228,6 +228,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
 void qoi_launch(Ctx* ctx, const osc_problem* prob, int B, double* q_dev);
 void level_sums_launch(Ctx* ctx, const double* qf, const double* qc, int B, double shift_y,
                        double shift_q, double* sums_dev);
+void level_sums_reshift_launch(Ctx* ctx, double* sums_dev, double dy, double dq);
 // per-sample iterations / status (and history) of the last solver_run, copied to host
 void solver_results(Ctx* ctx, int B, int32_t* iters, int32_t* status, double* hist_host);
 void exp_field_launch(Ctx* ctx, const double* Z, double* k, int64_t total, int* bad_flag);

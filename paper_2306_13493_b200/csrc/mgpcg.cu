@@ -2439,112 +2439,177 @@ struct HierDev {
 };
 
 // ---- CTA-resident multigrid (small grids and the V-cycle tail) ----------------------------------------
-// One CTA owns one sample. Each level's operator (C, E, N, NE, NW), its centre transfer weights and
-// r, z, t live in shared memory. Level 0 of the small solver is the 5-point P1 row from k
-// (NE = NW = null). The V-cycle is the multi-kernel one:
+// One CTA owns one sample; every level's operator, transfer weights and r, z, t live in shared memory.
+// Level 0 of the small solver is the 5-point P1 row from k in fp64 (it is the PCG operator); the
+// 9-point levels keep the fp32 couplings they are stored with. The V-cycle is the multi-kernel one:
 //   - pre-smoother red → black from z = 0;
 //   - residual t = r − A z, restricted with Pᵀ;
 //   - recursion, then z += P z_c;
 //   - post-smoother black → red, into t.
-// Each level's output is in its t.
-constexpr int SM_THREADS = 1024;
+// Each level's output is in its t. These kernels are bound by barrier and dependent-latency chains,
+// not by bandwidth, so everything an iteration would recompute is formed once per solve: the
+// reciprocal diagonals and the edge-node transfer weights (fp32; restriction and prolongation read
+// the same stored value, so the cycle stays symmetric); the red pre-sweep is folded into the black
+// one (z starts at 0, a black node's red neighbours are r/C); a thread owns at most SM_KMAX nodes
+// per level (u of the PCG stays in registers); reductions cost one barrier.
+constexpr int SM_KMAX = 3;
 
 struct SLev {
-  double *C, *E, *N, *NE, *NW;  // NE / NW null on a 5-point level
+  double *C, *iC;              // diagonal and its reciprocal
+  double *E, *N;               // 5-point level 0 of the small solver: fp64 couplings; null on 9-point levels
+  float *Ef, *Nf, *NEf, *NWf;  // 9-point levels: couplings as stored
+  float *w0, *w1;              // edge nodes: weights to the lower / upper coarse parent
+  float* pw[4];                // centre weights of this level's cells
   double *r, *z, *t;
-  double* pw[4];  // centre weights of this level's cells (transfer to the next level)
   int m, n0, N_;
+  float inv_n0;
 };
 
-__device__ __forceinline__ S9 row_smem(const SLev& L, int x, int y) {
+__device__ __forceinline__ void node_xy(const SLev& L, int i, int& x, int& y) {
+  y = __float2int_rz(((float)i + 0.5f) * L.inv_n0);  // exact for the ≤ 33² nodes of these levels
+  x = i - y * L.n0;
+}
+
+// body(i) for the nodes i < N owned by this thread (i = tid + k·T, k < SM_KMAX; SM_KMAX·T ≥ N)
+template <class F>
+__device__ __forceinline__ void for_nodes(int N, F&& body) {
+#pragma unroll
+  for (int k = 0; k < SM_KMAX; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < N) body(i);
+  }
+}
+
+__device__ __forceinline__ S9 row_smem(const SLev& L, int i, int x, int y) {
   S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
-  const int i = y * L.n0 + x, n0 = L.n0;
+  const int n0 = L.n0;
   r.c = L.C[i];
-  r.e = L.E[i];
-  r.n = L.N[i];
-  if (x > 0) r.w = L.E[i - 1];
-  if (y > 0) r.s = L.N[i - n0];
-  if (L.NE) {
-    r.ne = L.NE[i];
-    r.nw = L.NW[i];
-    if (x > 0 && y > 0) r.sw = L.NE[i - n0 - 1];
-    if (x < L.m && y > 0) r.se = L.NW[i - n0 + 1];
+  if (L.E) {
+    r.e = L.E[i];
+    r.n = L.N[i];
+    if (x > 0) r.w = L.E[i - 1];
+    if (y > 0) r.s = L.N[i - n0];
+  } else {
+    r.e = L.Ef[i];
+    r.n = L.Nf[i];
+    r.ne = L.NEf[i];
+    r.nw = L.NWf[i];
+    if (x > 0) r.w = L.Ef[i - 1];
+    if (y > 0) {
+      r.s = L.Nf[i - n0];
+      if (x > 0) r.sw = L.NEf[i - n0 - 1];
+      if (x < L.m) r.se = L.NWf[i - n0 + 1];
+    }
   }
   return r;
 }
 
-__device__ __forceinline__ double dot_smem(const S9& a, const double* v, int i, int n0, int x, int y, int m) {
+// Σ of the off-diagonal couplings times v: axis neighbours from va, diagonal neighbours from vd
+__device__ __forceinline__ double dot_smem(const S9& a, const double* va, const double* vd, int i, int n0, int x,
+                                           int y, int m) {
   double s = 0.0;
-  if (x > 0) s += a.w * v[i - 1];
-  if (x < m) s += a.e * v[i + 1];
+  if (x > 0) s += a.w * va[i - 1];
+  if (x < m) s += a.e * va[i + 1];
   if (y > 0) {
-    s += a.s * v[i - n0];
-    if (x > 0) s += a.sw * v[i - n0 - 1];
-    if (x < m) s += a.se * v[i - n0 + 1];
+    s += a.s * va[i - n0];
+    if (x > 0) s += a.sw * vd[i - n0 - 1];
+    if (x < m) s += a.se * vd[i - n0 + 1];
   }
   if (y < m) {
-    s += a.n * v[i + n0];
-    if (x > 0) s += a.nw * v[i + n0 - 1];
-    if (x < m) s += a.ne * v[i + n0 + 1];
+    s += a.n * va[i + n0];
+    if (x > 0) s += a.nw * vd[i + n0 - 1];
+    if (x < m) s += a.ne * vd[i + n0 + 1];
   }
   return s;
 }
 
-// V(1,1) on levels 0..nlev−1 of `lev`: input lev[0].r, output lev[0].t
-__device__ void vcycle_smem(SLev* lev, int nlev, const double* Ainv, int bc, int opdep) {
+// Block sum with one barrier: warp sums → sh[parity][warp] → every thread adds them in warp order
+// (deterministic). Consecutive calls alternate the buffer, so no second barrier is needed.
+struct BlockSum {
+  double (*sh)[32];
+  int parity = 0;
+  __device__ double operator()(double v) {
+    v = warp_sum(v);
+    double* s = sh[parity];
+    parity ^= 1;
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += s[w];
+    return t;
+  }
+};
+
+// reciprocal diagonals and edge-node transfer weights of levels 0 … nlev−2 (once per solve / call)
+__device__ void prepare_levels(const SLev* lev, int nlev, int bc, int opdep) {
   for (int l = 0; l + 1 < nlev; ++l) {
     const SLev& F = lev[l];
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
-      const int y = i / F.n0, x = i - y * F.n0;
-      F.z[i] = is_red(x, y) ? F.r[i] / F.C[i] : 0.0;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
-      const int y = i / F.n0, x = i - y * F.n0;
-      if (is_red(x, y)) continue;
-      const S9 a = row_smem(F, x, y);
+    for_nodes(F.N_, [&](int i) {
+      int x, y;
+      node_xy(F, i, x, y);
+      F.iC[i] = rcp64(F.C[i]);
+      const bool ox = x & 1, oy = y & 1;
+      if (ox == oy) return;
+      double a0, a1;
+      edge_w(row_smem(F, i, x, y), ox, opdep != 0, is_dir(bc, F.m, x, y), false, false, a0, a1);
+      F.w0[i] = (float)a0;
+      F.w1[i] = (float)a1;
+    });
+  }
+  __syncthreads();
+}
+
+// V(1,1) on levels 0..nlev−1 of `lev`: input lev[0].r, output lev[0].t
+__device__ void vcycle_smem(const SLev* lev, int nlev, const double* Ainv, int bc) {
+  for (int l = 0; l + 1 < nlev; ++l) {
+    const SLev& F = lev[l];
+    const int n0 = F.n0, m = F.m;
+    // red z = r/C; black z = (r − Σ_axis a·z_red)/C with the red neighbours formed in place
+    for_nodes(F.N_, [&](int i) {
+      int x, y;
+      node_xy(F, i, x, y);
+      const double ri = F.r[i], ic = F.iC[i];
+      if (is_red(x, y)) {
+        F.z[i] = ri * ic;
+        return;
+      }
+      const S9 a = row_smem(F, i, x, y);
       double s = 0.0;
-      if (x > 0) s += a.w * F.z[i - 1];
-      if (x < F.m) s += a.e * F.z[i + 1];
-      if (y > 0) s += a.s * F.z[i - F.n0];
-      if (y < F.m) s += a.n * F.z[i + F.n0];
-      F.z[i] = (F.r[i] - s) / a.c;
-    }
+      if (x > 0) s += a.w * (F.r[i - 1] * F.iC[i - 1]);
+      if (x < m) s += a.e * (F.r[i + 1] * F.iC[i + 1]);
+      if (y > 0) s += a.s * (F.r[i - n0] * F.iC[i - n0]);
+      if (y < m) s += a.n * (F.r[i + n0] * F.iC[i + n0]);
+      F.z[i] = (ri - s) * ic;
+    });
     __syncthreads();
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
-      const int y = i / F.n0, x = i - y * F.n0;
-      const S9 a = row_smem(F, x, y);
-      F.t[i] = F.r[i] - (a.c * F.z[i] + dot_smem(a, F.z, i, F.n0, x, y, F.m));
-    }
+    for_nodes(F.N_, [&](int i) {
+      int x, y;
+      node_xy(F, i, x, y);
+      const S9 a = row_smem(F, i, x, y);
+      F.t[i] = F.r[i] - (a.c * F.z[i] + dot_smem(a, F.z, F.z, i, n0, x, y, m));
+    });
     __syncthreads();
     const SLev& C = lev[l + 1];
-    const int mcl = F.m / 2;
-    for (int ic = threadIdx.x; ic < C.N_; ic += blockDim.x) {
-      const int J = ic / C.n0, I = ic - J * C.n0;
+    const int mcl = m / 2;
+    for_nodes(C.N_, [&](int ic) {
+      int I, J;
+      node_xy(C, ic, I, J);
       double acc = 0.0;
       if (!is_dir(bc, C.m, I, J)) {
-        const int x = 2 * I, y = 2 * J;
-        auto T = [&](int xx, int yy) { return F.t[yy * F.n0 + xx]; };
-        acc = T(x, y);
-        for (int s = -1; s <= 1; s += 2) {
-          if (x + s >= 0 && x + s <= F.m) {
-            double w0, w1;
-            edge_w(row_smem(F, x + s, y), true, opdep != 0, is_dir(bc, F.m, x + s, y), false, false, w0, w1);
-            acc += (s > 0 ? w0 : w1) * T(x + s, y);
-          }
-          if (y + s >= 0 && y + s <= F.m) {
-            double w0, w1;
-            edge_w(row_smem(F, x, y + s), false, opdep != 0, is_dir(bc, F.m, x, y + s), false, false, w0, w1);
-            acc += (s > 0 ? w0 : w1) * T(x, y + s);
-          }
-        }
-        if (I < mcl && J < mcl) acc += F.pw[0][J * mcl + I] * T(x + 1, y + 1);
-        if (I > 0 && J < mcl) acc += F.pw[1][J * mcl + I - 1] * T(x - 1, y + 1);
-        if (I < mcl && J > 0) acc += F.pw[2][(J - 1) * mcl + I] * T(x + 1, y - 1);
-        if (I > 0 && J > 0) acc += F.pw[3][(J - 1) * mcl + I - 1] * T(x - 1, y - 1);
+        const int x = 2 * I, y = 2 * J, i = y * n0 + x;
+        acc = F.t[i];
+        if (x < m) acc += F.w0[i + 1] * F.t[i + 1];
+        if (x > 0) acc += F.w1[i - 1] * F.t[i - 1];
+        if (y < m) acc += F.w0[i + n0] * F.t[i + n0];
+        if (y > 0) acc += F.w1[i - n0] * F.t[i - n0];
+        if (I < mcl && J < mcl) acc += F.pw[0][J * mcl + I] * F.t[i + n0 + 1];
+        if (I > 0 && J < mcl) acc += F.pw[1][J * mcl + I - 1] * F.t[i + n0 - 1];
+        if (I < mcl && J > 0) acc += F.pw[2][(J - 1) * mcl + I] * F.t[i - n0 + 1];
+        if (I > 0 && J > 0) acc += F.pw[3][(J - 1) * mcl + I - 1] * F.t[i - n0 - 1];
       }
       C.r[ic] = acc;
-    }
+    });
     __syncthreads();
   }
   {  // coarsest: t = A⁻¹ r
@@ -2559,161 +2624,173 @@ __device__ void vcycle_smem(SLev* lev, int nlev, const double* Ainv, int bc, int
   for (int l = nlev - 2; l >= 0; --l) {
     const SLev& F = lev[l];
     const SLev& C = lev[l + 1];
-    const int mcl = F.m / 2;
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {
-      const int y = i / F.n0, x = i - y * F.n0;
-      auto ZC = [&](int I, int J) { return C.t[J * C.n0 + I]; };
+    const int n0 = F.n0, m = F.m, mcl = m / 2, cn0 = C.n0;
+    for_nodes(F.N_, [&](int i) {
+      int x, y;
+      node_xy(F, i, x, y);
       const int ox = x & 1, oy = y & 1;
+      const double* zc = C.t + (y >> 1) * cn0 + (x >> 1);
       double v;
       if (!ox && !oy) {
-        v = ZC(x >> 1, y >> 1);
+        v = zc[0];
       } else if (ox && oy) {
-        const int I = x >> 1, J = y >> 1, cell = J * mcl + I;
-        v = F.pw[0][cell] * ZC(I, J) + F.pw[1][cell] * ZC(I + 1, J) + F.pw[2][cell] * ZC(I, J + 1) +
-            F.pw[3][cell] * ZC(I + 1, J + 1);
+        const int cell = (y >> 1) * mcl + (x >> 1);
+        v = F.pw[0][cell] * zc[0] + F.pw[1][cell] * zc[1] + F.pw[2][cell] * zc[cn0] + F.pw[3][cell] * zc[cn0 + 1];
       } else {
-        double w0, w1;
-        const bool horiz = ox != 0;
-        edge_w(row_smem(F, x, y), horiz, opdep != 0, is_dir(bc, F.m, x, y), false, false, w0, w1);
-        v = horiz ? w0 * ZC(x >> 1, y >> 1) + w1 * ZC((x >> 1) + 1, y >> 1)
-                  : w0 * ZC(x >> 1, y >> 1) + w1 * ZC(x >> 1, (y >> 1) + 1);
+        v = F.w0[i] * zc[0] + F.w1[i] * zc[ox ? 1 : cn0];
       }
       F.z[i] += v;
-    }
+    });
     __syncthreads();
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {  // black: reads z, writes t
-      const int y = i / F.n0, x = i - y * F.n0;
-      if (is_red(x, y)) continue;
-      const S9 a = row_smem(F, x, y);
-      F.t[i] = (F.r[i] - dot_smem(a, F.z, i, F.n0, x, y, F.m)) / a.c;
-    }
+    for_nodes(F.N_, [&](int i) {  // black: reads z, writes t
+      int x, y;
+      node_xy(F, i, x, y);
+      if (is_red(x, y)) return;
+      const S9 a = row_smem(F, i, x, y);
+      F.t[i] = (F.r[i] - dot_smem(a, F.z, F.z, i, n0, x, y, m)) * F.iC[i];
+    });
     __syncthreads();
-    for (int i = threadIdx.x; i < F.N_; i += blockDim.x) {  // red: new black (t), old red (z)
-      const int y = i / F.n0, x = i - y * F.n0;
-      if (!is_red(x, y)) continue;
-      const S9 a = row_smem(F, x, y);
-      const int n0 = F.n0, m = F.m;
-      double s = 0.0;
-      if (x > 0) s += a.w * F.t[i - 1];
-      if (x < m) s += a.e * F.t[i + 1];
-      if (y > 0) {
-        s += a.s * F.t[i - n0];
-        if (x > 0) s += a.sw * F.z[i - n0 - 1];
-        if (x < m) s += a.se * F.z[i - n0 + 1];
-      }
-      if (y < m) {
-        s += a.n * F.t[i + n0];
-        if (x > 0) s += a.nw * F.z[i + n0 - 1];
-        if (x < m) s += a.ne * F.z[i + n0 + 1];
-      }
-      F.t[i] = (F.r[i] - s) / a.c;
-    }
+    for_nodes(F.N_, [&](int i) {  // red: new black (t) on the axes, old red (z) on the diagonals
+      int x, y;
+      node_xy(F, i, x, y);
+      if (!is_red(x, y)) return;
+      const S9 a = row_smem(F, i, x, y);
+      F.t[i] = (F.r[i] - dot_smem(a, F.t, F.z, i, n0, x, y, m)) * F.iC[i];
+    });
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ double block_sum_s(double v) {
-  __shared__ double sh[32];
-  const double t = block_sum(v, sh);
-  __shared__ double res;
-  if (threadIdx.x == 0) res = t;
-  __syncthreads();
-  return res;
+// Shared-memory layout of a hierarchy m_top, m_top/2, … (nlev levels); level 0 is 5-point fp64 when
+// five_point0. All fp64 arrays first, then the fp32 ones. The coarsest level only holds r, t (its
+// solve is the precomputed inverse). Entries of level g: fp64 and fp32 counts.
+__host__ __device__ inline void level_counts(int g, bool last, bool p5, int& n64, int& n32) {
+  const int N = (g + 1) * (g + 1), mcl = g / 2;
+  n64 = last ? 2 * N : (p5 ? 7 * N : 5 * N);                    // r, t | z, C, iC | E, N
+  n32 = last ? 0 : (p5 ? 0 : 4 * N) + 2 * N + 4 * mcl * mcl;    // E, N, NE, NW | w0, w1 | pw
 }
-
-// Carve a hierarchy m_top, m_top/2, … (nlev levels) from shared memory; level 0 is 5-point when
-// five_point0 (no NE/NW). Returns the first free address.
-__device__ double* carve_levels(SLev* lev, double* cur, int m_top, int nlev, bool five_point0) {
+__host__ __device__ inline void hier_counts(int m_top, int nlev, bool five_point0, size_t& n64, size_t& n32) {
+  n64 = n32 = 0;
   int g = m_top;
-  for (int l = 0; l < nlev; ++l) {
-    const int n0 = g + 1, N = n0 * n0, mcl = g / 2;
-    SLev L;
-    L.m = g;
-    L.n0 = n0;
-    L.N_ = N;
-    L.C = cur; cur += N;
-    L.E = cur; cur += N;
-    L.N = cur; cur += N;
-    if (l == 0 && five_point0) {
-      L.NE = L.NW = nullptr;
-    } else {
-      L.NE = cur; cur += N;
-      L.NW = cur; cur += N;
+  for (int l = 0; l < nlev; ++l, g /= 2) {
+    int a, b;
+    level_counts(g, l + 1 == nlev, l == 0 && five_point0, a, b);
+    n64 += (size_t)a;
+    n32 += (size_t)b;
+  }
+}
+
+// Carve the hierarchy from shared memory: thread 0 fills the level structs (shared), every thread
+// gets the first free address.
+__device__ double* carve_levels(SLev* lev, double* base, int m_top, int nlev, bool five_point0) {
+  size_t n64, n32;
+  hier_counts(m_top, nlev, five_point0, n64, n32);
+  if (threadIdx.x == 0) {
+    double* c64 = base;
+    float* c32 = reinterpret_cast<float*>(base + n64);
+    int g = m_top;
+    for (int l = 0; l < nlev; ++l, g /= 2) {
+      const int N = (g + 1) * (g + 1), mcl = g / 2;
+      auto d = [&] { double* p = c64; c64 += N; return p; };
+      auto f = [&](int n) { float* p = c32; c32 += n; return p; };
+      SLev L{};
+      L.m = g;
+      L.n0 = g + 1;
+      L.N_ = N;
+      L.inv_n0 = 1.0f / (float)(g + 1);
+      L.r = d();
+      L.t = d();
+      if (l + 1 < nlev) {
+        L.z = d();
+        L.C = d();
+        L.iC = d();
+        if (l == 0 && five_point0) {
+          L.E = d();
+          L.N = d();
+        } else {
+          L.Ef = f(N);
+          L.Nf = f(N);
+          L.NEf = f(N);
+          L.NWf = f(N);
+        }
+        L.w0 = f(N);
+        L.w1 = f(N);
+        for (int q = 0; q < 4; ++q) L.pw[q] = f(mcl * mcl);
+      }
+      lev[l] = L;
     }
-    L.r = cur; cur += N;
-    L.z = cur; cur += N;
-    L.t = cur; cur += N;
-    for (int q = 0; q < 4; ++q) {
-      L.pw[q] = cur;
-      if (l + 1 < nlev) cur += mcl * mcl;
-    }
-    if (threadIdx.x == 0) lev[l] = L;
-    g /= 2;
   }
   __syncthreads();
-  return cur;
+  return base + n64 + (n32 + 1) / 2;
 }
 
-size_t hier_smem_doubles(int m_top, int nlev, bool five_point0) {
-  size_t tot = 0;
-  int g = m_top, nc = 0;
-  for (int l = 0; l < nlev; ++l) {
-    const size_t N = (size_t)(g + 1) * (g + 1), mcl = g / 2;
-    tot += N * ((l == 0 && five_point0) ? 6 : 8) + ((l + 1 < nlev) ? 4 * mcl * mcl : 0);
-    nc = (int)N;
-    g /= 2;
-  }
-  return tot + (size_t)nc * nc;  // + coarsest inverse
+size_t hier_smem_bytes(int m_top, int nlev, bool five_point0) {
+  size_t n64, n32;
+  hier_counts(m_top, nlev, five_point0, n64, n32);
+  int nc = m_top >> (nlev - 1);
+  nc = (nc + 1) * (nc + 1);
+  return sizeof(double) * (n64 + (n32 + 1) / 2 + (size_t)nc * nc);  // + coarsest inverse
 }
 
-// Load a stored level (operator + centre weights) of sample b into shared memory.
-__device__ void load_level(const SLev& L, const SolverLevelDev& G, int b, bool has_pw) {
+constexpr size_t kMaxCtaSmem = 227 * 1024 - 2048;  // dynamic shared memory a CTA-resident hierarchy may take
+
+// threads per CTA: the smallest warp multiple with SM_KMAX·T ≥ (m+1)²
+inline int small_threads(int m) {
+  const int N = (m + 1) * (m + 1);
+  int t = ((N + SM_KMAX - 1) / SM_KMAX + 31) / 32 * 32;
+  if (const char* e = std::getenv("OSC_SMALL_T")) t = std::max(t, std::atoi(e) / 32 * 32);
+  return std::min(std::max(t, 64), 1024);
+}
+
+// Load a stored 9-point level (operator + centre weights) of sample b into shared memory.
+__device__ void load_level(const SLev& L, const SolverLevelDev& G, int b, bool has_coarse) {
+  if (!has_coarse) return;  // the coarsest level is solved by its inverse
   const int64_t off = (int64_t)b * L.N_;
-  for (int i = threadIdx.x; i < L.N_; i += blockDim.x) {
+  for_nodes(L.N_, [&](int i) {
     L.C[i] = __ldg(G.C + off + i);
-    L.E[i] = __ldg(G.E + off + i);
-    L.N[i] = __ldg(G.N + off + i);
-    L.NE[i] = __ldg(G.NE + off + i);
-    L.NW[i] = __ldg(G.NW + off + i);
-  }
-  if (has_pw) {
-    const int mcl = L.m / 2;
-    const int64_t co = (int64_t)b * mcl * mcl;
-    for (int q = 0; q < 4; ++q)
-      for (int i = threadIdx.x; i < mcl * mcl; i += blockDim.x) L.pw[q][i] = __ldg(G.pw[q] + co + i);
-  }
+    L.Ef[i] = __ldg(G.E + off + i);
+    L.Nf[i] = __ldg(G.N + off + i);
+    L.NEf[i] = __ldg(G.NE + off + i);
+    L.NWf[i] = __ldg(G.NW + off + i);
+  });
+  const int mcl = L.m / 2;
+  const int64_t co = (int64_t)b * mcl * mcl;
+  for (int q = 0; q < 4; ++q)
+    for_nodes(mcl * mcl, [&](int i) { L.pw[q][i] = __ldg(G.pw[q] + co + i); });
 }
 
 // Whole PCG of one sample per CTA (m ≤ 32): level 0 from k, coarse levels + transfers + coarsest
 // inverse from the global setup (prow / rap / factor kernels), the same algorithm and stopping
 // rule as the multi-kernel path, one launch per batch.
-__global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev, int bc, int opdep, int forcing,
-                                                               double fval, double tol, int max_iter_factor,
-                                                               const double* __restrict__ kin, HierDev H,
-                                                               const double* __restrict__ chol,
-                                                               double* __restrict__ uout, int* flags,
-                                                               double* scal) {
+__global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int bc, int opdep, int forcing,
+                                                         double fval, double tol, int max_iter_factor,
+                                                         const double* __restrict__ kin, HierDev H,
+                                                         const double* __restrict__ chol,
+                                                         double* __restrict__ uout, int* flags,
+                                                         double* scal) {
   extern __shared__ double smem[];
-  __shared__ SLev lev[12];
+  __shared__ double sum_sh[2][32];
+  __shared__ SLev lev[6];  // m ≤ 32: at most 32, 16, 8, 4 (or an odd tail)
+  BlockSum bsum{sum_sh};
   const int b = blockIdx.x;
   const int N0 = (m0 + 1) * (m0 + 1);
   const double* k0 = kin + (int64_t)b * N0;
-  double* u = uout + (int64_t)b * N0;
   double* p = smem;
   double* Ainv = carve_levels(lev, smem + N0, m0, nlev, true);
-  const SLev L0 = lev[0];
-  const int m = m0;
-  for (int i = threadIdx.x; i < N0; i += blockDim.x) {  // level-0 5-point rows from k
-    const int y = i / L0.n0, x = i - y * L0.n0;
+  const SLev& L0 = lev[0];
+  const int m = m0, n0 = m0 + 1;
+  for_nodes(N0, [&](int i) {  // level-0 5-point rows from k
+    int x, y;
+    node_xy(L0, i, x, y);
     const S9 a = row_k(k0, m + 1, 1, m, bc, x, y);
     L0.C[i] = a.c;
     L0.E[i] = a.e;
     L0.N[i] = a.n;
-  }
-  if (nlev > 1) {
+  });
+  {
     const int mcl = m / 2;
     for (int q = 0; q < 4; ++q)
-      for (int i = threadIdx.x; i < mcl * mcl; i += blockDim.x) L0.pw[q][i] = __ldg(H.lev[0].pw[q] + (int64_t)b * mcl * mcl + i);
+      for_nodes(mcl * mcl, [&](int i) { L0.pw[q][i] = __ldg(H.lev[0].pw[q] + (int64_t)b * mcl * mcl + i); });
   }
   for (int l = 1; l < nlev; ++l) load_level(lev[l], H.lev[l], b, l + 1 < nlev);
   {
@@ -2722,15 +2799,22 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
     for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Ainv[i] = X[i];
   }
   __syncthreads();
-  // PCG init (fem.cpp:335-365): u = lift, r = b − A u
+  prepare_levels(lev, nlev, bc, opdep);
+  // PCG init (fem.cpp:335-365): u = lift, r = b − A u; u of this thread's nodes stays in registers
+  double ureg[SM_KMAX];
   double bb = 0.0, rr0 = 0.0;
-  for (int i = threadIdx.x; i < N0; i += blockDim.x) {
-    const int y = i / L0.n0, x = i - y * L0.n0;
+#pragma unroll
+  for (int k = 0; k < SM_KMAX; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    ureg[k] = 0.0;
+    if (i >= N0) continue;
+    int x, y;
+    node_xy(L0, i, x, y);
     const double gs = (bc == OSC_BC_FLOWCELL && x == 0) ? 1.0 : 0.0;
     double bi;
     if (is_dir(bc, m, x, y)) {
       bi = gs;
-      u[i] = gs;
+      ureg[k] = gs;
       L0.r[i] = 0.0;
     } else {
       const int tri = 2 * (x < m && y < m) + (x > 0 && y < m) + 2 * (x > 0 && y > 0) + (x < m && y > 0);
@@ -2742,62 +2826,76 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
                                  (y > 0 ? (K(0, y - 1) + K(1, y) + K(0, y)) / 3.0 : 0.0));
         bi -= e * 1.0;
       }
-      u[i] = 0.0;
       L0.r[i] = bi;
       rr0 += bi * bi;
     }
     bb += bi * bi;
   }
-  const double bnorm = sqrt(block_sum_s(bb));
-  double rel = sqrt(block_sum_s(rr0)) / bnorm;
+  const double bnorm = sqrt(bsum(bb));
+  double rel = sqrt(bsum(rr0)) / bnorm;
   int it = 0, status = 0;
   const int64_t cap64 = (int64_t)max_iter_factor * N0;
   const int cap = (int)(cap64 < 0x7fffffff ? cap64 : 0x7fffffff);
   if (rel > tol) {
-    vcycle_smem(lev, nlev, Ainv, bc, opdep);
+    __syncthreads();  // r complete before the first cycle reads neighbours
+    vcycle_smem(lev, nlev, Ainv, bc);
     double rz = 0.0;
-    for (int i = threadIdx.x; i < N0; i += blockDim.x) {
+    for_nodes(N0, [&](int i) {
       p[i] = L0.t[i];
       rz += L0.r[i] * L0.t[i];
-    }
-    rz = block_sum_s(rz);
+    });
+    rz = bsum(rz);  // its barrier also publishes p
     for (;;) {
       if (it >= cap) {
         status = OSC_ERR_SOLVER;
         break;
       }
       ++it;
+      double ap[SM_KMAX];
       double pap = 0.0;
-      for (int i = threadIdx.x; i < N0; i += blockDim.x) {
-        const int y = i / L0.n0, x = i - y * L0.n0;
-        const S9 a = row_smem(L0, x, y);
-        pap += p[i] * (a.c * p[i] + dot_smem(a, p, i, L0.n0, x, y, m));
+#pragma unroll
+      for (int k = 0; k < SM_KMAX; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        ap[k] = 0.0;
+        if (i >= N0) continue;
+        int x, y;
+        node_xy(L0, i, x, y);
+        const S9 a = row_smem(L0, i, x, y);
+        ap[k] = a.c * p[i] + dot_smem(a, p, p, i, n0, x, y, m);
+        pap += p[i] * ap[k];
       }
-      const double alpha = rz / block_sum_s(pap);
+      const double alpha = rz / bsum(pap);
       double rr = 0.0;
-      for (int i = threadIdx.x; i < N0; i += blockDim.x) {
-        const int y = i / L0.n0, x = i - y * L0.n0;
-        const S9 a = row_smem(L0, x, y);
-        u[i] = fma(alpha, p[i], u[i]);
-        const double rn = fma(-alpha, a.c * p[i] + dot_smem(a, p, i, L0.n0, x, y, m), L0.r[i]);
+#pragma unroll
+      for (int k = 0; k < SM_KMAX; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        if (i >= N0) continue;
+        ureg[k] = fma(alpha, p[i], ureg[k]);
+        const double rn = fma(-alpha, ap[k], L0.r[i]);
         L0.r[i] = rn;
         rr += rn * rn;
       }
-      rel = sqrt(block_sum_s(rr)) / bnorm;
+      rel = sqrt(bsum(rr)) / bnorm;  // barrier: r complete
       if (rel <= tol) break;
       if (!isfinite(rel)) {
         status = OSC_ERR_SOLVER;
         break;
       }
-      vcycle_smem(lev, nlev, Ainv, bc, opdep);
+      vcycle_smem(lev, nlev, Ainv, bc);
       double rzn = 0.0;
-      for (int i = threadIdx.x; i < N0; i += blockDim.x) rzn += L0.r[i] * L0.t[i];
-      rzn = block_sum_s(rzn);
+      for_nodes(N0, [&](int i) { rzn += L0.r[i] * L0.t[i]; });
+      rzn = bsum(rzn);
       const double beta = rzn / rz;
       rz = rzn;
-      for (int i = threadIdx.x; i < N0; i += blockDim.x) p[i] = fma(beta, p[i], L0.t[i]);
+      for_nodes(N0, [&](int i) { p[i] = fma(beta, p[i], L0.t[i]); });
       __syncthreads();
     }
+  }
+  double* u = uout + (int64_t)b * N0;
+#pragma unroll
+  for (int k = 0; k < SM_KMAX; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < N0) u[i] = ureg[k];
   }
   if (threadIdx.x == 0) {
     flags[b * F_NFLAGS + F_ACTIVE] = 0;
@@ -2809,19 +2907,18 @@ __global__ void __launch_bounds__(SM_THREADS) small_pcg_kernel(int m0, int nlev,
 }
 
 size_t small_smem_bytes(int m, int nlev) {
-  return sizeof(double) * ((size_t)(m + 1) * (m + 1) + hier_smem_doubles(m, nlev, true)) + 64;
+  return sizeof(double) * (size_t)(m + 1) * (m + 1) + hier_smem_bytes(m, nlev, true) + 64;
 }
 
 // CTA-resident tail of the V-cycle (levels ls … nlev−1, m_ls ≤ 32) inside large solves: the
 // coarsest levels are launch/latency-bound as separate kernels (≈ 20 µs each whatever their size).
-constexpr int SUB_THREADS = 256;
-__global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int nlev, int bc, int opdep, HierDev H,
-                                                                 const double* __restrict__ r_ls,
-                                                                 double* __restrict__ z_out,
-                                                                 const double* __restrict__ chol,
-                                                                 const int* flags) {
+__global__ void __launch_bounds__(1024) sub_vcycle_kernel(int m_ls, int nlev, int bc, int opdep, HierDev H,
+                                                          const double* __restrict__ r_ls,
+                                                          double* __restrict__ z_out,
+                                                          const double* __restrict__ chol,
+                                                          const int* flags) {
   extern __shared__ double smem[];
-  __shared__ SLev lev[12];
+  __shared__ SLev lev[6];
   const int b = blockIdx.x;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
   const int N_ls = (m_ls + 1) * (m_ls + 1);
@@ -2833,14 +2930,15 @@ __global__ void __launch_bounds__(SUB_THREADS) sub_vcycle_kernel(int m_ls, int n
     for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Ainv[i] = X[i];
   }
   const double* rb = r_ls + (int64_t)b * N_ls;
-  for (int i = threadIdx.x; i < N_ls; i += blockDim.x) lev[0].r[i] = rb[i];
+  for_nodes(N_ls, [&](int i) { lev[0].r[i] = rb[i]; });
   __syncthreads();
-  vcycle_smem(lev, nlev, Ainv, bc, opdep);
+  prepare_levels(lev, nlev, bc, opdep);
+  vcycle_smem(lev, nlev, Ainv, bc);
   double* zb = z_out + (int64_t)b * N_ls;
-  for (int i = threadIdx.x; i < N_ls; i += blockDim.x) zb[i] = lev[0].t[i];
+  for_nodes(N_ls, [&](int i) { zb[i] = lev[0].t[i]; });
 }
 
-size_t sub_smem_bytes(int m_ls, int nlev) { return sizeof(double) * hier_smem_doubles(m_ls, nlev, false); }
+size_t sub_smem_bytes(int m_ls, int nlev) { return hier_smem_bytes(m_ls, nlev, false) + 64; }
 
 __global__ void mark_active_failed_kernel(int B, int* flags) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -3174,7 +3272,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
   }
   int ls = w.nlev - 1;
   for (int l = 1; l < w.nlev - 1; ++l)
-    if (w.lev[l].m <= 32) {
+    if (w.lev[l].m <= 32 && sub_smem_bytes(w.lev[l].m, w.nlev - l) <= kMaxCtaSmem) {
       ls = l;
       break;
     }
@@ -3201,7 +3299,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
     const size_t sm = sub_smem_bytes(S.m, nl);
     smem_attr(sub_vcycle_kernel, sm);
     KScope ks(ctx, "mg_sub_vcycle");
-    sub_vcycle_kernel<<<B, SUB_THREADS, sm, st>>>(S.m, nl, bc, w.opdep, hier_of(w, ls), S.r, S.z2, w.chol,
+    sub_vcycle_kernel<<<B, small_threads(S.m), sm, st>>>(S.m, nl, bc, w.opdep, hier_of(w, ls), S.r, S.z2, w.chol,
                                                   w.flags);
   } else {
     const SolverLevel& C = w.lev[w.nlev - 1];
@@ -3425,13 +3523,13 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
   const Geo g0 = geo_of(L0);
   w.r_cur = L0.r;
   mg_setup(ctx, prob, B);
-  if (w.m <= 32 && w.nlev > 1 && w.hist_cap == 0) {
+  if (w.m <= 32 && w.nlev > 1 && w.hist_cap == 0 && small_smem_bytes(w.m, w.nlev) <= kMaxCtaSmem) {
     // whole solve CTA-resident (one CTA per sample, one launch); a kept residual history takes the
     // streaming path below
     const size_t sm = small_smem_bytes(w.m, w.nlev);
     smem_attr(small_pcg_kernel, sm);
     KScope ks(ctx, "small_pcg");
-    small_pcg_kernel<<<B, SM_THREADS, sm, st>>>(w.m, w.nlev, bc, w.opdep, prob->forcing, prob->forcing_value,
+    small_pcg_kernel<<<B, small_threads(w.m), sm, st>>>(w.m, w.nlev, bc, w.opdep, prob->forcing, prob->forcing_value,
                                                prob->tol, prob->max_iter_factor, L0.k, hier_of(w, 0), w.chol,
                                                w.u, w.flags, w.scal);
     OSC_CUDA(cudaGetLastError());

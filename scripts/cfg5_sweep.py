@@ -13,7 +13,9 @@ reports converged = false, as the reference does.
 GPU-routed run with IDENTICAL options, on the rows the CPU finishes in minutes — finest grid capped
 at 256², L2-norm QoI (the pristine reference has no flux QoI) — with N_ℓ compared level by level.
 
-usage: python scripts/cfg5_sweep.py [eps,eps,...] [--no-cpu]
+Each sweep row also runs the GPU-resident driver (osc_mlmc_adaptive, csrc/driver.cpp) on the same options.
+
+usage: python scripts/cfg5_sweep.py [eps,eps,...] [--no-cpu] [--no-driver]
 """
 import json
 import math
@@ -25,12 +27,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2306_13493_b200 as P  # noqa: E402
 from paper_2306_13493_b200 import estimators as E  # noqa: E402
+from paper_2306_13493_b200 import mlmc as M  # noqa: E402
 
 api = P.api
 ctx = api.default_context(0)
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 eps_list = [float(x) for x in (args[0].split(",") if args else ["1e-2", "3e-3", "1e-3", "3e-4"])]
 with_cpu = "--no-cpu" not in sys.argv
+with_driver = "--no-driver" not in sys.argv
 rows, beside = [], []
 
 
@@ -55,7 +59,19 @@ for lam in (0.03, 0.01):
             rep = E.mlmc_estimate(problem, options(variant, l_max), h0, eps)
             ctx.synchronize()
             wall = time.perf_counter() - t0
-            row = dict(lam=lam, eps=eps, variant=variant, h0=h0, wall_s=wall, estimate=rep.estimate,
+            # the GPU-resident driver (osc_mlmc_adaptive): levels of a pass drawn at the same time, levels
+            # created on the device (no host sort of the n = 4096 spectrum), moments as device sums
+            drv = None
+            if with_driver:
+                t0 = time.perf_counter()
+                d = M.mlmc_adaptive(problem, options(variant, l_max), h0, eps)
+                ctx.synchronize()
+                dw = time.perf_counter() - t0
+                drv = dict(wall_s=dw, setup_s=d.setup_s, draw_s=d.draw_s, waves=d.waves, n=[l.n for l in d.levels],
+                           estimate=d.estimate, sampling_error=d.sampling_error, bias=d.bias_estimate,
+                           converged=d.converged, same_n=[l.n for l in d.levels] == [l.n for l in rep.levels],
+                           samples_per_s=sum(l.n for l in d.levels) / dw)
+            row = dict(lam=lam, eps=eps, variant=variant, h0=h0, wall_s=wall, estimate=rep.estimate, driver=drv,
                        level_setup="device" if setup else "reference",
                        sampling_error=rep.sampling_error, bias=rep.bias_estimate, converged=rep.converged,
                        levels=len(rep.levels), n=[l.n for l in rep.levels], cost_model=rep.total_cost_model,

@@ -172,14 +172,17 @@ class ClockSampler:
             time.sleep(0.02)
 
     def mark(self):
-        """Start of the timed region: only rows sampled from here on are reported."""
-        self.rows = []
+        """Start of the timed region: rows sampled from here on are the ones reported. A timed region
+        shorter than the 200 ms sampling period (the few-ms steps of the small configs) may end before a
+        row arrives: stop() then reports the rows of the last second BEFORE the mark, i.e. of the
+        warm-up steps that ran back to back into the timed region, and says so in `window`."""
+        self.t_mark = time.perf_counter()
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append(parts + [time.perf_counter()])
 
     def stop(self):
         if not self.proc:
@@ -190,12 +193,21 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.thread.join(timeout=2)
+        t_mark = getattr(self, "t_mark", 0.0)
+        window = "timed region"
+        rows = [r for r in self.rows if r[6] >= t_mark]
+        if not rows:
+            rows = [r for r in self.rows if r[6] >= t_mark - 1.0]
+            window = "warm-up steps under load within 1 s before the timed region (region shorter than the sampling period)"
+        self.rows = rows
+        self.window = window
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "window": self.window}
 
 
 # ---- reference (CPU) arm --------------------------------------------------------------------------
@@ -413,6 +425,10 @@ def main():
     # W warm-up steps, continued until at least 0.4 s have been spent warming up: an idle B200 sits at
     # 120 MHz and the few-ms steps of the small configs would otherwise be timed on ramping clocks
     # (config 1 measured 94k or 140k samples/s depending on it)
+    # the clock sampler starts before the warm-up: nvidia-smi's NVML start-up (hundreds of ms) then
+    # overlaps the warm-up instead of leaving the GPU idle (and down-clocking) right before the timed region
+    clocks = ClockSampler(local)
+    clocks.start()
     t_warm = time.perf_counter()
     w = 0
     while w < args.warmup - 1 or (time.perf_counter() - t_warm < 0.4 and w < 500):
@@ -449,9 +465,15 @@ def main():
     ctx.reset_stats()
     iters_total[:] = [0, 0]
     launches0 = ctx.launch_count
-    clocks = ClockSampler(local)
-    clocks.start()
-    clocks.wait_ready()
+    if not clocks.rows:  # (long steps: the sampler had the whole warm-up; short ones: keep the GPU busy meanwhile)
+        t_w = time.perf_counter()
+        while not clocks.rows and clocks.proc and clocks.proc.poll() is None and time.perf_counter() - t_w < 10.0:
+            step(2_000_000)
+    if graph_loop:
+        step(2_000_001)  # back-to-back into the timed region
+    ctx.reset_stats()
+    iters_total[:] = [0, 0]
+    launches0 = ctx.launch_count
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -777,14 +799,15 @@ def run_ce_only(args, W, api, ctx, torch, dist, rank, world, local):
         idx0 = (k * world + rank) * B
         api._check(lib.osc_ce_sample(lev.h, None, 1, W["ell"], idx0, B, flags, out.data_ptr(), None))
 
-    for w in range(args.warmup):
-        step(1_000_000 + w)
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_w, w = time.perf_counter(), 0
+    while w < args.warmup or (not clocks.rows and clocks.proc and clocks.proc.poll() is None and time.perf_counter() - t_w < 10.0):
+        step(1_000_000 + w)  # the sampler's NVML start-up overlaps the warm-up (the GPU never idles before the timed region)
+        w += 1
     ctx.set_profiling(True)
     ctx.reset_stats()
     launches0 = ctx.launch_count
-    clocks = ClockSampler(local)
-    clocks.start()
-    clocks.wait_ready()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()

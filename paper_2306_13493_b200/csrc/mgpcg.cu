@@ -2446,12 +2446,20 @@ struct HierDev {
 //   - residual t = r − A z, restricted with Pᵀ;
 //   - recursion, then z += P z_c;
 //   - post-smoother black → red, into t.
-// Each level's output is in its t. These kernels are bound by barrier and dependent-latency chains,
-// not by bandwidth, so everything an iteration would recompute is formed once per solve: the
-// reciprocal diagonals and the edge-node transfer weights (fp32; restriction and prolongation read
-// the same stored value, so the cycle stays symmetric); the red pre-sweep is folded into the black
-// one (z starts at 0, a black node's red neighbours are r/C); a thread owns at most SM_KMAX nodes
-// per level (u of the PCG stays in registers); reductions cost one barrier.
+// Each level's output is in its t. These kernels are bound by instruction issue, barriers and
+// dependent-latency chains, not by bandwidth (ncu: 1 % of DRAM), so:
+//   * everything an iteration would recompute is formed once per solve — the reciprocal diagonals and
+//     the edge-node transfer weights (fp32; restriction and prolongation read the same stored value,
+//     so the cycle stays symmetric);
+//   * the stencil sums are branch-free: every array is preceded (and each level followed) by n0 + 1
+//     zeros and the couplings that point outside the grid are stored as exact zeros, so a node reads
+//     its eight neighbours unconditionally (a row end reads the neighbouring row's end node through
+//     a zero coupling) and never needs its (x, y);
+//   * m is even on every level with a coarser one, so n0 is odd and node i is red exactly when i is
+//     even: the coloured sweeps run over packed indices;
+//   * the red pre-sweep is folded into the black one (z starts at 0, a black node's red neighbours
+//     are r/C); a thread owns at most SM_KMAX nodes per level (u of the PCG stays in registers);
+//     reductions cost one barrier; the CTA is sized to the grid (7 CTAs per SM at 16², 2 at 32²).
 constexpr int SM_KMAX = 3;
 
 struct SLev {
@@ -2471,8 +2479,16 @@ __device__ __forceinline__ void node_xy(const SLev& L, int i, int& x, int& y) {
 }
 
 // body(i) for the nodes i < N owned by this thread (i = tid + k·T, k < SM_KMAX; SM_KMAX·T ≥ N)
+// (a rolled loop: these kernels are instruction-cache bound — ncu: 33 % of the stall samples were
+// "no instruction" with the three-fold unrolled bodies — so code size counts more than loop overhead)
 template <class F>
 __device__ __forceinline__ void for_nodes(int N, F&& body) {
+#pragma unroll 1
+  for (int i = threadIdx.x; i < N; i += blockDim.x) body(i);
+}
+// unrolled variant for the global-memory loads (their latencies overlap across the thread's nodes)
+template <class F>
+__device__ __forceinline__ void for_nodes_unrolled(int N, F&& body) {
 #pragma unroll
   for (int k = 0; k < SM_KMAX; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
@@ -2480,47 +2496,38 @@ __device__ __forceinline__ void for_nodes(int N, F&& body) {
   }
 }
 
-__device__ __forceinline__ S9 row_smem(const SLev& L, int i, int x, int y) {
+// Σ of node i's off-diagonal couplings times v (axis neighbours from va, diagonal ones from vd).
+// W, S, SW, SE are the neighbours' E, N, NE, NW. No bounds tests: zero pads and zero outward couplings.
+__device__ __forceinline__ double offdiag(const SLev& L, const double* va, const double* vd, int i) {
+  const int n0 = L.n0;
+  if (L.E) return L.E[i - 1] * va[i - 1] + L.E[i] * va[i + 1] + L.N[i - n0] * va[i - n0] + L.N[i] * va[i + n0];
+  double s = L.Ef[i - 1] * va[i - 1] + L.Ef[i] * va[i + 1] + L.Nf[i - n0] * va[i - n0] + L.Nf[i] * va[i + n0];
+  s += L.NEf[i - n0 - 1] * vd[i - n0 - 1] + L.NWf[i - n0 + 1] * vd[i - n0 + 1];
+  s += L.NWf[i] * vd[i + n0 - 1] + L.NEf[i] * vd[i + n0 + 1];
+  return s;
+}
+
+// the full row (setup only: transfer weights)
+__device__ __forceinline__ S9 row_smem(const SLev& L, int i) {
   S9 r{0, 0, 0, 0, 0, 0, 0, 0, 0};
   const int n0 = L.n0;
   r.c = L.C[i];
   if (L.E) {
     r.e = L.E[i];
     r.n = L.N[i];
-    if (x > 0) r.w = L.E[i - 1];
-    if (y > 0) r.s = L.N[i - n0];
+    r.w = L.E[i - 1];
+    r.s = L.N[i - n0];
   } else {
     r.e = L.Ef[i];
     r.n = L.Nf[i];
     r.ne = L.NEf[i];
     r.nw = L.NWf[i];
-    if (x > 0) r.w = L.Ef[i - 1];
-    if (y > 0) {
-      r.s = L.Nf[i - n0];
-      if (x > 0) r.sw = L.NEf[i - n0 - 1];
-      if (x < L.m) r.se = L.NWf[i - n0 + 1];
-    }
+    r.w = L.Ef[i - 1];
+    r.s = L.Nf[i - n0];
+    r.sw = L.NEf[i - n0 - 1];
+    r.se = L.NWf[i - n0 + 1];
   }
   return r;
-}
-
-// Σ of the off-diagonal couplings times v: axis neighbours from va, diagonal neighbours from vd
-__device__ __forceinline__ double dot_smem(const S9& a, const double* va, const double* vd, int i, int n0, int x,
-                                           int y, int m) {
-  double s = 0.0;
-  if (x > 0) s += a.w * va[i - 1];
-  if (x < m) s += a.e * va[i + 1];
-  if (y > 0) {
-    s += a.s * va[i - n0];
-    if (x > 0) s += a.sw * vd[i - n0 - 1];
-    if (x < m) s += a.se * vd[i - n0 + 1];
-  }
-  if (y < m) {
-    s += a.n * va[i + n0];
-    if (x > 0) s += a.nw * vd[i + n0 - 1];
-    if (x < m) s += a.ne * vd[i + n0 + 1];
-  }
-  return s;
 }
 
 // Block sum with one barrier: warp sums → sh[parity][warp] → every thread adds them in warp order
@@ -2552,7 +2559,7 @@ __device__ void prepare_levels(const SLev* lev, int nlev, int bc, int opdep) {
       const bool ox = x & 1, oy = y & 1;
       if (ox == oy) return;
       double a0, a1;
-      edge_w(row_smem(F, i, x, y), ox, opdep != 0, is_dir(bc, F.m, x, y), false, false, a0, a1);
+      edge_w(row_smem(F, i), ox, opdep != 0, is_dir(bc, F.m, x, y), false, false, a0, a1);
       F.w0[i] = (float)a0;
       F.w1[i] = (float)a1;
     });
@@ -2565,30 +2572,32 @@ __device__ void vcycle_smem(const SLev* lev, int nlev, const double* Ainv, int b
   for (int l = 0; l + 1 < nlev; ++l) {
     const SLev& F = lev[l];
     const int n0 = F.n0, m = F.m;
+    const int n_red = (F.N_ + 1) / 2, n_black = F.N_ / 2;
+    const bool five = F.E != nullptr;
     // red z = r/C; black z = (r − Σ_axis a·z_red)/C with the red neighbours formed in place
-    for_nodes(F.N_, [&](int i) {
-      int x, y;
-      node_xy(F, i, x, y);
-      const double ri = F.r[i], ic = F.iC[i];
-      if (is_red(x, y)) {
-        F.z[i] = ri * ic;
-        return;
-      }
-      const S9 a = row_smem(F, i, x, y);
-      double s = 0.0;
-      if (x > 0) s += a.w * (F.r[i - 1] * F.iC[i - 1]);
-      if (x < m) s += a.e * (F.r[i + 1] * F.iC[i + 1]);
-      if (y > 0) s += a.s * (F.r[i - n0] * F.iC[i - n0]);
-      if (y < m) s += a.n * (F.r[i + n0] * F.iC[i + n0]);
-      F.z[i] = (ri - s) * ic;
+    for_nodes(n_red, [&](int j) { F.z[2 * j] = F.r[2 * j] * F.iC[2 * j]; });
+    for_nodes(n_black, [&](int j) {
+      const int i = 2 * j + 1;
+      double s;
+      if (five)
+        s = F.E[i - 1] * (F.r[i - 1] * F.iC[i - 1]) + F.E[i] * (F.r[i + 1] * F.iC[i + 1]) +
+            F.N[i - n0] * (F.r[i - n0] * F.iC[i - n0]) + F.N[i] * (F.r[i + n0] * F.iC[i + n0]);
+      else
+        s = F.Ef[i - 1] * (F.r[i - 1] * F.iC[i - 1]) + F.Ef[i] * (F.r[i + 1] * F.iC[i + 1]) +
+            F.Nf[i - n0] * (F.r[i - n0] * F.iC[i - n0]) + F.Nf[i] * (F.r[i + n0] * F.iC[i + n0]);
+      F.z[i] = (F.r[i] - s) * F.iC[i];
     });
     __syncthreads();
-    for_nodes(F.N_, [&](int i) {
-      int x, y;
-      node_xy(F, i, x, y);
-      const S9 a = row_smem(F, i, x, y);
-      F.t[i] = F.r[i] - (a.c * F.z[i] + dot_smem(a, F.z, F.z, i, n0, x, y, m));
-    });
+    // residual t = r − A z. On a 5-point level the black rows were just solved exactly (their
+    // neighbours are all red), so their residual is rounding noise: only the red rows are formed and
+    // the restriction below leaves the black (edge-node) terms out.
+    if (five)
+      for_nodes(n_red, [&](int j) {
+        const int i = 2 * j;
+        F.t[i] = F.r[i] - (F.C[i] * F.z[i] + offdiag(F, F.z, F.z, i));
+      });
+    else
+      for_nodes(F.N_, [&](int i) { F.t[i] = F.r[i] - (F.C[i] * F.z[i] + offdiag(F, F.z, F.z, i)); });
     __syncthreads();
     const SLev& C = lev[l + 1];
     const int mcl = m / 2;
@@ -2599,10 +2608,12 @@ __device__ void vcycle_smem(const SLev* lev, int nlev, const double* Ainv, int b
       if (!is_dir(bc, C.m, I, J)) {
         const int x = 2 * I, y = 2 * J, i = y * n0 + x;
         acc = F.t[i];
-        if (x < m) acc += F.w0[i + 1] * F.t[i + 1];
-        if (x > 0) acc += F.w1[i - 1] * F.t[i - 1];
-        if (y < m) acc += F.w0[i + n0] * F.t[i + n0];
-        if (y > 0) acc += F.w1[i - n0] * F.t[i - n0];
+        if (!five) {
+          if (x < m) acc += F.w0[i + 1] * F.t[i + 1];
+          if (x > 0) acc += F.w1[i - 1] * F.t[i - 1];
+          if (y < m) acc += F.w0[i + n0] * F.t[i + n0];
+          if (y > 0) acc += F.w1[i - n0] * F.t[i - n0];
+        }
         if (I < mcl && J < mcl) acc += F.pw[0][J * mcl + I] * F.t[i + n0 + 1];
         if (I > 0 && J < mcl) acc += F.pw[1][J * mcl + I - 1] * F.t[i + n0 - 1];
         if (I < mcl && J > 0) acc += F.pw[2][(J - 1) * mcl + I] * F.t[i - n0 + 1];
@@ -2612,19 +2623,23 @@ __device__ void vcycle_smem(const SLev* lev, int nlev, const double* Ainv, int b
     });
     __syncthreads();
   }
-  {  // coarsest: t = A⁻¹ r
+  {  // coarsest: t = A⁻¹ r, one warp per row (lanes over the columns, shuffle sum): every other warp
+     // of the CTA waits at the barrier below, so the chain is kept short. The inverse stays in global
+     // memory (L1/L2-resident).
     const SLev& C = lev[nlev - 1];
-    for (int i = threadIdx.x; i < C.N_; i += blockDim.x) {
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5, nc = C.N_;
+    for (int i = threadIdx.x >> 5; i < nc; i += nw) {
       double v = 0.0;
-      for (int j = 0; j < C.N_; ++j) v = fma(Ainv[i * C.N_ + j], C.r[j], v);
-      C.t[i] = v;
+      for (int j = lane; j < nc; j += 32) v = fma(__ldg(Ainv + i * nc + j), C.r[j], v);
+      v = warp_sum(v);
+      if (lane == 0) C.t[i] = v;
     }
     __syncthreads();
   }
   for (int l = nlev - 2; l >= 0; --l) {
     const SLev& F = lev[l];
     const SLev& C = lev[l + 1];
-    const int n0 = F.n0, m = F.m, mcl = m / 2, cn0 = C.n0;
+    const int mcl = F.m / 2, cn0 = C.n0;
     for_nodes(F.N_, [&](int i) {
       int x, y;
       node_xy(F, i, x, y);
@@ -2642,32 +2657,29 @@ __device__ void vcycle_smem(const SLev* lev, int nlev, const double* Ainv, int b
       F.z[i] += v;
     });
     __syncthreads();
-    for_nodes(F.N_, [&](int i) {  // black: reads z, writes t
-      int x, y;
-      node_xy(F, i, x, y);
-      if (is_red(x, y)) return;
-      const S9 a = row_smem(F, i, x, y);
-      F.t[i] = (F.r[i] - dot_smem(a, F.z, F.z, i, n0, x, y, m)) * F.iC[i];
+    for_nodes(F.N_ / 2, [&](int j) {  // black (odd i): reads z, writes t
+      const int i = 2 * j + 1;
+      F.t[i] = (F.r[i] - offdiag(F, F.z, F.z, i)) * F.iC[i];
     });
     __syncthreads();
-    for_nodes(F.N_, [&](int i) {  // red: new black (t) on the axes, old red (z) on the diagonals
-      int x, y;
-      node_xy(F, i, x, y);
-      if (!is_red(x, y)) return;
-      const S9 a = row_smem(F, i, x, y);
-      F.t[i] = (F.r[i] - dot_smem(a, F.t, F.z, i, n0, x, y, m)) * F.iC[i];
+    for_nodes((F.N_ + 1) / 2, [&](int j) {  // red (even i): new black (t) on the axes, old red (z) on the diagonals
+      const int i = 2 * j;
+      F.t[i] = (F.r[i] - offdiag(F, F.t, F.z, i)) * F.iC[i];
     });
     __syncthreads();
   }
 }
 
 // Shared-memory layout of a hierarchy m_top, m_top/2, … (nlev levels); level 0 is 5-point fp64 when
-// five_point0. All fp64 arrays first, then the fp32 ones. The coarsest level only holds r, t (its
-// solve is the precomputed inverse). Entries of level g: fp64 and fp32 counts.
+// five_point0. All fp64 arrays first, then the fp32 ones; every array has a zero pad of n0 + 1
+// entries in front, every level one behind its last array (the zero-pad / zero-coupling contract of
+// offdiag). The coarsest level only holds r, t (its solve is the precomputed inverse).
 __host__ __device__ inline void level_counts(int g, bool last, bool p5, int& n64, int& n32) {
-  const int N = (g + 1) * (g + 1), mcl = g / 2;
-  n64 = last ? 2 * N : (p5 ? 7 * N : 5 * N);                    // r, t | z, C, iC | E, N
-  n32 = last ? 0 : (p5 ? 0 : 4 * N) + 2 * N + 4 * mcl * mcl;    // E, N, NE, NW | w0, w1 | pw
+  const int N = (g + 1) * (g + 1), mcl = g / 2, pad = g + 2;
+  const int a64 = last ? 2 : (p5 ? 7 : 5);      // r, t | z, C, iC | E, N
+  const int a32 = last ? 0 : (p5 ? 2 : 6);      // E, N, NE, NW | w0, w1
+  n64 = a64 * (N + pad) + pad;
+  n32 = last ? 0 : a32 * (N + pad) + pad + 4 * mcl * mcl;  // + pw
 }
 __host__ __device__ inline void hier_counts(int m_top, int nlev, bool five_point0, size_t& n64, size_t& n32) {
   n64 = n32 = 0;
@@ -2680,8 +2692,8 @@ __host__ __device__ inline void hier_counts(int m_top, int nlev, bool five_point
   }
 }
 
-// Carve the hierarchy from shared memory: thread 0 fills the level structs (shared), every thread
-// gets the first free address.
+// Carve the hierarchy from (zeroed) shared memory: thread 0 fills the level structs (shared), every
+// thread gets the first free address.
 __device__ double* carve_levels(SLev* lev, double* base, int m_top, int nlev, bool five_point0) {
   size_t n64, n32;
   hier_counts(m_top, nlev, five_point0, n64, n32);
@@ -2690,9 +2702,9 @@ __device__ double* carve_levels(SLev* lev, double* base, int m_top, int nlev, bo
     float* c32 = reinterpret_cast<float*>(base + n64);
     int g = m_top;
     for (int l = 0; l < nlev; ++l, g /= 2) {
-      const int N = (g + 1) * (g + 1), mcl = g / 2;
-      auto d = [&] { double* p = c64; c64 += N; return p; };
-      auto f = [&](int n) { float* p = c32; c32 += n; return p; };
+      const int N = (g + 1) * (g + 1), mcl = g / 2, pad = g + 2;
+      auto d = [&] { double* p = c64 + pad; c64 += pad + N; return p; };
+      auto f = [&] { float* p = c32 + pad; c32 += pad + N; return p; };
       SLev L{};
       L.m = g;
       L.n0 = g + 1;
@@ -2708,15 +2720,20 @@ __device__ double* carve_levels(SLev* lev, double* base, int m_top, int nlev, bo
           L.E = d();
           L.N = d();
         } else {
-          L.Ef = f(N);
-          L.Nf = f(N);
-          L.NEf = f(N);
-          L.NWf = f(N);
+          L.Ef = f();
+          L.Nf = f();
+          L.NEf = f();
+          L.NWf = f();
         }
-        L.w0 = f(N);
-        L.w1 = f(N);
-        for (int q = 0; q < 4; ++q) L.pw[q] = f(mcl * mcl);
+        L.w0 = f();
+        L.w1 = f();
+        c32 += pad;
+        for (int q = 0; q < 4; ++q) {
+          L.pw[q] = c32;
+          c32 += mcl * mcl;
+        }
       }
+      c64 += pad;
       lev[l] = L;
     }
   }
@@ -2727,9 +2744,7 @@ __device__ double* carve_levels(SLev* lev, double* base, int m_top, int nlev, bo
 size_t hier_smem_bytes(int m_top, int nlev, bool five_point0) {
   size_t n64, n32;
   hier_counts(m_top, nlev, five_point0, n64, n32);
-  int nc = m_top >> (nlev - 1);
-  nc = (nc + 1) * (nc + 1);
-  return sizeof(double) * (n64 + (n32 + 1) / 2 + (size_t)nc * nc);  // + coarsest inverse
+  return sizeof(double) * (n64 + (n32 + 1) / 2);
 }
 
 constexpr size_t kMaxCtaSmem = 227 * 1024 - 2048;  // dynamic shared memory a CTA-resident hierarchy may take
@@ -2737,21 +2752,29 @@ constexpr size_t kMaxCtaSmem = 227 * 1024 - 2048;  // dynamic shared memory a CT
 // threads per CTA: the smallest warp multiple with SM_KMAX·T ≥ (m+1)²
 inline int small_threads(int m) {
   const int N = (m + 1) * (m + 1);
-  int t = ((N + SM_KMAX - 1) / SM_KMAX + 31) / 32 * 32;
-  if (const char* e = std::getenv("OSC_SMALL_T")) t = std::max(t, std::atoi(e) / 32 * 32);
+  const int t = ((N + SM_KMAX - 1) / SM_KMAX + 31) / 32 * 32;
   return std::min(std::max(t, 64), 1024);
 }
 
-// Load a stored 9-point level (operator + centre weights) of sample b into shared memory.
+__device__ __forceinline__ void zero_smem(double* smem, int n_doubles) {
+  for (int i = threadIdx.x; i < n_doubles; i += blockDim.x) smem[i] = 0.0;
+  __syncthreads();
+}
+
+// Load a stored 9-point level (operator + centre weights) of sample b into shared memory; couplings
+// that point outside the grid are stored as zeros (offdiag's contract).
 __device__ void load_level(const SLev& L, const SolverLevelDev& G, int b, bool has_coarse) {
   if (!has_coarse) return;  // the coarsest level is solved by its inverse
   const int64_t off = (int64_t)b * L.N_;
-  for_nodes(L.N_, [&](int i) {
+  for_nodes_unrolled(L.N_, [&](int i) {
+    int x, y;
+    node_xy(L, i, x, y);
+    const bool xm = x == L.m, ym = y == L.m;
     L.C[i] = __ldg(G.C + off + i);
-    L.Ef[i] = __ldg(G.E + off + i);
-    L.Nf[i] = __ldg(G.N + off + i);
-    L.NEf[i] = __ldg(G.NE + off + i);
-    L.NWf[i] = __ldg(G.NW + off + i);
+    L.Ef[i] = xm ? 0.f : __ldg(G.E + off + i);
+    L.Nf[i] = ym ? 0.f : __ldg(G.N + off + i);
+    L.NEf[i] = (xm || ym) ? 0.f : __ldg(G.NE + off + i);
+    L.NWf[i] = (x == 0 || ym) ? 0.f : __ldg(G.NW + off + i);
   });
   const int mcl = L.m / 2;
   const int64_t co = (int64_t)b * mcl * mcl;
@@ -2767,7 +2790,7 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
                                                          const double* __restrict__ kin, HierDev H,
                                                          const double* __restrict__ chol,
                                                          double* __restrict__ uout, int* flags,
-                                                         double* scal) {
+                                                         double* scal, int smem_doubles) {
   extern __shared__ double smem[];
   __shared__ double sum_sh[2][32];
   __shared__ SLev lev[6];  // m ≤ 32: at most 32, 16, 8, 4 (or an odd tail)
@@ -2775,11 +2798,12 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
   const int b = blockIdx.x;
   const int N0 = (m0 + 1) * (m0 + 1);
   const double* k0 = kin + (int64_t)b * N0;
-  double* p = smem;
-  double* Ainv = carve_levels(lev, smem + N0, m0, nlev, true);
+  zero_smem(smem, smem_doubles);
+  double* p = smem + m0 + 2;  // padded like the level arrays (its back pad is the first level array's front pad)
+  carve_levels(lev, p + N0, m0, nlev, true);
   const SLev& L0 = lev[0];
-  const int m = m0, n0 = m0 + 1;
-  for_nodes(N0, [&](int i) {  // level-0 5-point rows from k
+  const int m = m0;
+  for_nodes(N0, [&](int i) {  // level-0 5-point rows from k (outward and eliminated couplings are zeros)
     int x, y;
     node_xy(L0, i, x, y);
     const S9 a = row_k(k0, m + 1, 1, m, bc, x, y);
@@ -2793,11 +2817,8 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
       for_nodes(mcl * mcl, [&](int i) { L0.pw[q][i] = __ldg(H.lev[0].pw[q] + (int64_t)b * mcl * mcl + i); });
   }
   for (int l = 1; l < nlev; ++l) load_level(lev[l], H.lev[l], b, l + 1 < nlev);
-  {
-    const int nc = lev[nlev - 1].N_;
-    const double* X = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
-    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Ainv[i] = X[i];
-  }
+  const int nc = lev[nlev - 1].N_;
+  const double* Ainv = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
   __syncthreads();
   prepare_levels(lev, nlev, bc, opdep);
   // PCG init (fem.cpp:335-365): u = lift, r = b − A u; u of this thread's nodes stays in registers
@@ -2837,15 +2858,16 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
   const int64_t cap64 = (int64_t)max_iter_factor * N0;
   const int cap = (int)(cap64 < 0x7fffffff ? cap64 : 0x7fffffff);
   if (rel > tol) {
-    __syncthreads();  // r complete before the first cycle reads neighbours
-    vcycle_smem(lev, nlev, Ainv, bc);
-    double rz = 0.0;
-    for_nodes(N0, [&](int i) {
-      p[i] = L0.t[i];
-      rz += L0.r[i] * L0.t[i];
-    });
-    rz = bsum(rz);  // its barrier also publishes p
-    for (;;) {
+    double rz = 1.0;
+    for (;;) {  // one call site of the V-cycle (code size)
+      vcycle_smem(lev, nlev, Ainv, bc);
+      double rzn = 0.0;
+      for_nodes(N0, [&](int i) { rzn += L0.r[i] * L0.t[i]; });
+      rzn = bsum(rzn);
+      const double beta = it == 0 ? 0.0 : rzn / rz;
+      rz = rzn;
+      for_nodes(N0, [&](int i) { p[i] = fma(beta, p[i], L0.t[i]); });
+      __syncthreads();
       if (it >= cap) {
         status = OSC_ERR_SOLVER;
         break;
@@ -2858,10 +2880,7 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
         const int i = threadIdx.x + k * blockDim.x;
         ap[k] = 0.0;
         if (i >= N0) continue;
-        int x, y;
-        node_xy(L0, i, x, y);
-        const S9 a = row_smem(L0, i, x, y);
-        ap[k] = a.c * p[i] + dot_smem(a, p, p, i, n0, x, y, m);
+        ap[k] = L0.C[i] * p[i] + offdiag(L0, p, p, i);
         pap += p[i] * ap[k];
       }
       const double alpha = rz / bsum(pap);
@@ -2881,14 +2900,6 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
         status = OSC_ERR_SOLVER;
         break;
       }
-      vcycle_smem(lev, nlev, Ainv, bc);
-      double rzn = 0.0;
-      for_nodes(N0, [&](int i) { rzn += L0.r[i] * L0.t[i]; });
-      rzn = bsum(rzn);
-      const double beta = rzn / rz;
-      rz = rzn;
-      for_nodes(N0, [&](int i) { p[i] = fma(beta, p[i], L0.t[i]); });
-      __syncthreads();
     }
   }
   double* u = uout + (int64_t)b * N0;
@@ -2907,7 +2918,7 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
 }
 
 size_t small_smem_bytes(int m, int nlev) {
-  return sizeof(double) * (size_t)(m + 1) * (m + 1) + hier_smem_bytes(m, nlev, true) + 64;
+  return sizeof(double) * ((size_t)(m + 1) * (m + 1) + m + 2) + hier_smem_bytes(m, nlev, true);
 }
 
 // CTA-resident tail of the V-cycle (levels ls … nlev−1, m_ls ≤ 32) inside large solves: the
@@ -2916,21 +2927,19 @@ __global__ void __launch_bounds__(1024) sub_vcycle_kernel(int m_ls, int nlev, in
                                                           const double* __restrict__ r_ls,
                                                           double* __restrict__ z_out,
                                                           const double* __restrict__ chol,
-                                                          const int* flags) {
+                                                          const int* flags, int smem_doubles) {
   extern __shared__ double smem[];
   __shared__ SLev lev[6];
   const int b = blockIdx.x;
   if (!flags[b * F_NFLAGS + F_ACTIVE]) return;
   const int N_ls = (m_ls + 1) * (m_ls + 1);
-  double* Ainv = carve_levels(lev, smem, m_ls, nlev, false);
+  zero_smem(smem, smem_doubles);
+  carve_levels(lev, smem, m_ls, nlev, false);
   for (int l = 0; l < nlev; ++l) load_level(lev[l], H.lev[l], b, l + 1 < nlev);
-  {
-    const int nc = lev[nlev - 1].N_;
-    const double* X = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
-    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Ainv[i] = X[i];
-  }
+  const int nc = lev[nlev - 1].N_;
+  const double* Ainv = chol + (int64_t)b * 2 * nc * nc + (int64_t)nc * nc;
   const double* rb = r_ls + (int64_t)b * N_ls;
-  for_nodes(N_ls, [&](int i) { lev[0].r[i] = rb[i]; });
+  for_nodes_unrolled(N_ls, [&](int i) { lev[0].r[i] = rb[i]; });
   __syncthreads();
   prepare_levels(lev, nlev, bc, opdep);
   vcycle_smem(lev, nlev, Ainv, bc);
@@ -2938,7 +2947,7 @@ __global__ void __launch_bounds__(1024) sub_vcycle_kernel(int m_ls, int nlev, in
   for_nodes(N_ls, [&](int i) { zb[i] = lev[0].t[i]; });
 }
 
-size_t sub_smem_bytes(int m_ls, int nlev) { return hier_smem_bytes(m_ls, nlev, false) + 64; }
+size_t sub_smem_bytes(int m_ls, int nlev) { return hier_smem_bytes(m_ls, nlev, false); }
 
 __global__ void mark_active_failed_kernel(int B, int* flags) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -3300,7 +3309,7 @@ void vcycle(Ctx* ctx, int bc, int B) {
     smem_attr(sub_vcycle_kernel, sm);
     KScope ks(ctx, "mg_sub_vcycle");
     sub_vcycle_kernel<<<B, small_threads(S.m), sm, st>>>(S.m, nl, bc, w.opdep, hier_of(w, ls), S.r, S.z2, w.chol,
-                                                  w.flags);
+                                                         w.flags, (int)(sm / sizeof(double)));
   } else {
     const SolverLevel& C = w.lev[w.nlev - 1];
     coarsest_solve(ctx, B, C.r, C.z2);
@@ -3531,7 +3540,7 @@ void solver_run(Ctx* ctx, const osc_problem* prob, int B, const double* uc_guess
     KScope ks(ctx, "small_pcg");
     small_pcg_kernel<<<B, small_threads(w.m), sm, st>>>(w.m, w.nlev, bc, w.opdep, prob->forcing, prob->forcing_value,
                                                prob->tol, prob->max_iter_factor, L0.k, hier_of(w, 0), w.chol,
-                                               w.u, w.flags, w.scal);
+                                               w.u, w.flags, w.scal, (int)(sm / sizeof(double)));
     OSC_CUDA(cudaGetLastError());
     return;
   }

@@ -1,6 +1,6 @@
 # Round measurement set (gpurun -- 'bash scripts/measure.sh TAG [parts]'); outputs in gpurun_out/.
-# parts: any of  tests bench ref cfgs mlmc launches ncu   (default: all)
-TAG=${1:-x}; PARTS=${2:-"tests bench ref cfgs mlmc launches ncu"}  # + cesplit
+# parts: any of  tests bench ref cfgs mlmc levels launches ncu   (default: all)   + cesplit cfg5
+TAG=${1:-x}; PARTS=${2:-"tests bench ref cfgs mlmc levels launches ncu"}
 O=gpurun_out
 has() { case " $PARTS " in *" $1 "*) return 0;; esac; return 1; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv
@@ -29,6 +29,18 @@ PY
 fi
 if has mlmc; then
   timeout 900 python bench.py --config 3 --mlmc > $O/${TAG}_mlmc.json 2> $O/${TAG}_mlmc.err; echo "mlmc rc=$?"; head -c 800 $O/${TAG}_mlmc.json; echo
+fi
+if has levels; then
+  # kernel-class shares of config 3's small levels + an ncu capture of the CTA-resident solver (16^2)
+  timeout 600 python scripts/level_breakdown.py 0,1,2,3 > $O/${TAG}_levels.json 2> $O/${TAG}_levels.err; echo "levels rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:small_pcg -s 3 -c 1 -o $O/${TAG}_small_pcg16 python scripts/level_breakdown.py 0 > $O/${TAG}_ncu_small.log 2>&1; tail -1 $O/${TAG}_ncu_small.log
+  python scripts/ncu_summary.py $O/${TAG}_small_pcg16.ncu-rep 8 > $O/${TAG}_small_pcg16_ncu.txt 2>&1
+  python scripts/ncu_stalls.py $O/${TAG}_small_pcg16.ncu-rep >> $O/${TAG}_small_pcg16_ncu.txt 2>&1
+  python scripts/ncu_lines.py $O/${TAG}_small_pcg16.ncu-rep 20 >> $O/${TAG}_small_pcg16_ncu.txt 2>&1
+  [ -n "$KEEP_REP" ] || rm -f $O/${TAG}_small_pcg16.ncu-rep
+fi
+if has cfg5; then
+  timeout 2400 python scripts/cfg5_sweep.py > $O/${TAG}_cfg5.log 2> $O/${TAG}_cfg5.err; echo "cfg5 rc=$?"; cp $O/cfg5_sweep.json $O/${TAG}_cfg5_sweep.json
 fi
 CMD="python bench.py --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-e2e"
 if has launches; then

@@ -148,8 +148,14 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 200):
+        # One nvidia-smi query costs the process ≈ 50 ms of stalled launches / synchronisations (NVML and
+        # the CUDA driver share a lock): invisible in the 190 ms steps of config 4 (the recipe's 200 ms
+        # period), but a third of a step on the host-polled 256² level of config 3 (15.8k samples/s with one
+        # query inside the timed region, 20.9k without) — the small workloads sample once per second, so
+        # their short timed regions are normally reported from the warm-up window (see mark()).
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
 
@@ -157,7 +163,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -174,7 +180,7 @@ class ClockSampler:
     def mark(self):
         """Start of the timed region: rows sampled from here on are the ones reported. A timed region
         shorter than the 200 ms sampling period (the few-ms steps of the small configs) may end before a
-        row arrives: stop() then reports the rows of the last second BEFORE the mark, i.e. of the
+        row arrives: stop() then reports the rows of the last two seconds BEFORE the mark, i.e. of the
         warm-up steps that ran back to back into the timed region, and says so in `window`."""
         self.t_mark = time.perf_counter()
 
@@ -197,8 +203,8 @@ class ClockSampler:
         window = "timed region"
         rows = [r for r in self.rows if r[6] >= t_mark]
         if not rows:
-            rows = [r for r in self.rows if r[6] >= t_mark - 1.0]
-            window = "warm-up steps under load within 1 s before the timed region (region shorter than the sampling period)"
+            rows = [r for r in self.rows if r[6] >= t_mark - 2.0]
+            window = "warm-up steps under load within 2 s before the timed region (region shorter than the sampling period)"
         self.rows = rows
         self.window = window
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -427,7 +433,7 @@ def main():
     # (config 1 measured 94k or 140k samples/s depending on it)
     # the clock sampler starts before the warm-up: nvidia-smi's NVML start-up (hundreds of ms) then
     # overlaps the warm-up instead of leaving the GPU idle (and down-clocking) right before the timed region
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, 200 if m >= 1024 else 1000)
     clocks.start()
     t_warm = time.perf_counter()
     w = 0

@@ -171,26 +171,33 @@ struct Driver {
       if (e) std::rethrow_exception(e);
   }
 
-  // Equal shares of each device's free memory for the batch workspaces of the active levels
-  // (N_ℓ · bytes per sample is roughly level-independent under the MLMC allocation). Contexts are
-  // replaced so that workspaces grown under an older, larger share return to the pool.
+  static size_t held_bytes(const Ctx* c) {
+    return c->ce_inter.bytes + c->xi_dev.bytes + c->fields_fine.bytes + c->fields_coarse.bytes + c->solver.mem.bytes +
+           c->out_q.bytes + c->out_i.bytes + c->retry_k.bytes + c->retry_q.bytes;
+  }
+
+  // Equal shares of each device's memory for the batch workspaces of the active levels (under the MLMC
+  // allocation N_ℓ · bytes per sample is roughly level-independent). A context whose workspaces have
+  // grown beyond the new share is replaced, so that memory returns to the pool; the others keep their
+  // workspaces (and their instantiated PCG-loop graphs) and only get the new budget.
   void rebalance() {
-    for (auto& L : levels)
-      for (int g = 0; g < G(); ++g) {
-        OSC_CUDA(cudaSetDevice(devices[g]));
-        L->launches_gone += L->ctx[g]->launches;
-        osc_ctx* fresh = nullptr;
-        if (int rc = osc_ctx_create(devices[g], &fresh)) throw Error(rc, osc_last_error());
-        osc_ctx_destroy(L->ctx[g]);
-        L->ctx[g] = fresh;
-        L->lev[g]->ctx = fresh;
-      }
     for (int g = 0; g < G(); ++g) {
       OSC_CUDA(cudaSetDevice(devices[g]));
-      size_t fr = 0, tot = 0;
+      size_t fr = 0, tot = 0, held = 0;
       OSC_CUDA(cudaMemGetInfo(&fr, &tot));
-      const size_t share = (size_t)(0.85 * (double)fr / (double)levels.size());
-      for (auto& L : levels) osc_ctx_set_mem_budget(L->ctx[g], std::max<size_t>(share, (size_t)64 << 20));
+      for (auto& L : levels) held += held_bytes(L->ctx[g]);
+      const size_t share = std::max<size_t>((size_t)(0.85 * (double)(fr + held) / (double)levels.size()), (size_t)64 << 20);
+      for (auto& L : levels) {
+        if (held_bytes(L->ctx[g]) > share) {
+          L->launches_gone += L->ctx[g]->launches;
+          osc_ctx* fresh = nullptr;
+          if (int rc = osc_ctx_create(devices[g], &fresh)) throw Error(rc, osc_last_error());
+          osc_ctx_destroy(L->ctx[g]);
+          L->ctx[g] = fresh;
+          L->lev[g]->ctx = fresh;
+        }
+        osc_ctx_set_mem_budget(L->ctx[g], share);
+      }
     }
   }
 

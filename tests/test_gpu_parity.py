@@ -196,6 +196,31 @@ def test_solve_vs_oracle(P, ctx, port, m, bc, coarse_op):
             assert abs(q[b] - qo) <= QOI_TOL * max(abs(qo), 1e-12), (kind, b, q[b], qo)
 
 
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("m", [6, 12, 16, 20, 24, 28, 30, 48, 96])
+def test_solve_cta_resident_grids(P, ctx, port, m, bc):
+    """The shared-memory multigrid (whole solves with m ≤ 32, the V-cycle tail below 32² of larger ones)
+    on grids that are not powers of two: 6 → 3, 12 → 6 → 3, 20 → 10 → 5, 24 → … → 3, 28 → 14 → 7,
+    30 → 15 (a 256-node coarsest level, its inverse read from global memory), 48 and 96 (streaming
+    top levels over a 24 → 12 → 6 → 3 tail). Its zero-padded, branch-free layout and the packed
+    red/black sweeps rely on odd row lengths on every level with a coarser one. QoIs against the port."""
+    api = P.api
+    rng = np.random.default_rng(3 * m + bc)
+    Z = np.cumsum(np.cumsum(rng.standard_normal((5, m + 1, m + 1)) * 0.2, axis=1), axis=2)
+    Z = ((Z - Z.mean()) / Z.std() * 1.4).reshape(5, -1)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1, 1), bc=api.BC(bc))
+    u, it, _ = api.assemble_and_solve(m, Z, prob, ctx=ctx)
+    assert np.all(it > 0) and np.all(it < 60)
+    for kind in (0, 1, 2, 3):
+        prob.qoi = api.QoiSpec(api.QoiKind(kind))
+        q = api.evaluate_qoi(m, u, prob, Z=Z, ctx=ctx)
+        for b in range(5):
+            uo, ito, rc, _ = port.solve(m, Z[b], bc=bc)
+            assert rc == 0
+            qo = port.qoi(m, uo, bc=bc, qoi=kind, Z=Z[b])
+            assert abs(q[b] - qo) <= QOI_TOL * max(abs(qo), 1e-12), (kind, b, q[b], qo)
+
+
 @pytest.mark.parametrize("m,bc", [(33, 0), (33, 1), (66, 0), (70, 1), (132, 0)])
 def test_solve_odd_coarsest_grids(P, ctx, port, m, bc):
     """Grids whose coarsening stops above 1089 nodes (m = 2^j·c, odd c ≥ 33): the reference

@@ -322,7 +322,7 @@ struct Driver {
   void refresh(const std::vector<Job>& jobs) {
     const size_t nl = levels.size();
     std::vector<double> sums(8 * nl, 0.0);
-    if (G() == 1) {
+    if (!group) {
       for (const Job& j : jobs) {
         double out[7];
         if (int rc = osc_level_sums_read(j.L->lev[0], out)) throw Error(rc, osc_last_error());
@@ -402,7 +402,10 @@ void run(int n_devices, const int* devs, const osc_problem& prob, const osc_mlmc
   } else {
     for (int i = 0; i < n_devices; ++i) d.devices.push_back(devs ? devs[i] : i);
   }
-  if (d.G() > 1) {
+  // several devices: NCCL communicators + one staging context per device (OSC_MLMC_FORCE_GROUP=1 takes
+  // this path on a single device too, so the collective path can be exercised on a one-GPU box)
+  const char* force = std::getenv("OSC_MLMC_FORCE_GROUP");
+  if (d.G() > 1 || (force && force[0] == '1')) {
     if (int rc = osc_group_create(d.G(), d.devices.data(), &d.group)) throw Error(rc, osc_last_error());
     d.stage.resize((size_t)d.G());
   }

@@ -812,7 +812,6 @@ __global__ void __launch_bounds__(32) coarse_band_solve_kernel(int n0, int B, co
 // diagonal neighbours), so every sweep is a parallel, deterministic pass; the V-cycle stays
 // symmetric (pre red→black, post black→red) and CG-valid. From z = 0 the pre-smoother's diagonal
 // terms vanish: red z = r/C, black z = (r − Σ_WENS a z_red)/C.
-__device__ __forceinline__ bool is_red(int x, int y) { return ((x + y) & 1) == 0; }
 
 // ---- PCG init: u = lift (or the nested-iteration guess), r = b − A u, ‖b‖, ‖r‖ -------------------
 // One thread per column marching INIT_RY rows, so a CTA covers NT × INIT_RY nodes and does one

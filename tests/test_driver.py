@@ -191,3 +191,18 @@ def test_level_sums_reshift(P, ctx):
     assert s[0] == 40 and s[5] == ky and s[6] == kq
     assert abs(s[2] - want[2]) <= 1e-12 * want[2] and abs(s[4] - want[4]) <= 1e-10 * want[4]
     assert abs(s[1]) <= 1e-13 * np.abs(y).sum() and abs(s[3]) <= 1e-13 * np.abs(q).sum()
+
+
+@pytest.mark.gpu
+def test_driver_collective_path_on_one_device(P, ctx, monkeypatch):
+    """The several-device path of the driver (per-device staging of all levels' sums + one NCCL all-reduce
+    per wave) on the one visible device: same decisions and bit-identical moments as the direct read."""
+    from paper_2306_13493_b200 import mlmc
+    prob, opt = _opts(P, lam=0.1, seed=7, pilot_n=30, l_max=3)
+    a = mlmc.mlmc_adaptive(prob, opt, 1 / 8, 4e-3, 2, devices=[0])
+    monkeypatch.setenv("OSC_MLMC_FORCE_GROUP", "1")
+    b = mlmc.mlmc_adaptive(prob, opt, 1 / 8, 4e-3, 2, devices=[0])
+    assert [l.n for l in a.levels] == [l.n for l in b.levels] and a.waves == b.waves
+    assert [l.mean_y for l in a.levels] == [l.mean_y for l in b.levels]
+    assert [l.var_y for l in a.levels] == [l.var_y for l in b.levels]
+    assert a.estimate == b.estimate

@@ -706,20 +706,24 @@ def cfg3_per_level(args, api, ctx, torch, lib, hbm):
             step(1_000_000 + w)
             w += 1
         ctx.synchronize()
+        # a batch of the small levels takes 4–40 ms: at least 0.25 s of batches (and at least args.steps),
+        # so that one host hiccup does not move the level's rate by a third
+        n_steps = max(args.steps, min(200, int(0.25 * w / max(time.perf_counter() - t_warm, 1e-3)) + 1))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         its = [0, 0]
         e0.record(stream)
-        for kk in range(args.steps):
+        for kk in range(n_steps):
             step(kk)
             its[0] += int(itf.sum())
             its[1] += int(itc.sum())
         e1.record(stream)
         ctx.synchronize()
         ms = e0.elapsed_time(e1)
-        rate = args.steps * B / (ms / 1000.0)
-        Wl = dict(m=m, batch=B, coupled=ell > 0, it=(its[0] / (args.steps * B), its[1] / (args.steps * B)))
+        rate = n_steps * B / (ms / 1000.0)
+        Wl = dict(m=m, batch=B, coupled=ell > 0, it=(its[0] / (n_steps * B), its[1] / (n_steps * B)))
         b_meas = algorithmic_bytes_per_sample(Wl, plan.op.n)
         out[str(ell)] = {"grid": f"{m}^2" + (f"/{m // 2}^2" if ell else ""), "samples_per_s": rate, "batch": B,
+                         "batches_timed": n_steps,
                          "smoothed": bool(k), "mean_iters": [round(x, 2) for x in Wl["it"]],
                          "roofline_frac_at_measured_iters": rate / (hbm * 1e9 / b_meas),
                          "non_converged_sample_indices": failed}

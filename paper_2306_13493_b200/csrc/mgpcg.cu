@@ -622,8 +622,8 @@ __global__ void __launch_bounds__(NT) rediscretize_kernel(const double* __restri
 
 // Coarsest operator (stored 9-point rows) and its explicit inverse, one warp per sample. The
 // reference factors the coarsest matrix by dense Cholesky (fem.cpp:255-272) and back-substitutes
-// per V-cycle (:274-286); here the SPD matrix is inverted once per solve by Gauss–Jordan (lane i
-// owns row i of [A | I]), so every coarsest solve is one warp matvec. n ≤ 32 uses this path.
+// per V-cycle (:274-286); here the SPD matrix is inverted once per solve by in-place Gauss–Jordan (lane i
+// owns row i), so every coarsest solve is one warp matvec. n ≤ 32 uses this path.
 constexpr int CF_WARPS = 2;
 // Row i of the coarsest operator: the stored level, or — when the whole grid is the coarsest level
 // (k0 != null) — the exact fp64 P1 row rebuilt from k, so that single-level solves keep the exact
@@ -650,30 +650,37 @@ __device__ __forceinline__ void dense_row(const L9& L, int64_t off, int i, doubl
 
 __global__ void __launch_bounds__(32 * CF_WARPS) coarse_factor_warp_kernel(L9 L, int B, double* __restrict__ chol,
                                                                            const double* __restrict__ k0, int bc) {
-  __shared__ double aug[CF_WARPS][32][65];  // row i: A(i, 0..n−1) | I(i, 0..n−1), padded
+  __shared__ double mat[CF_WARPS][32][33];  // row i of A, inverted in place (odd pitch: conflict-free columns)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * CF_WARPS + w;
   if (b >= B) return;
   const int n = (int)L.Nn;
-  double(*A)[65] = aug[w];
+  double(*A)[33] = mat[w];
   if (lane < n) {
-    for (int j = 0; j < 2 * n; ++j) A[lane][j] = (j == n + lane) ? 1.0 : 0.0;
+    for (int j = 0; j < n; ++j) A[lane][j] = 0.0;
     dense_row(L, (int64_t)b * n, lane, A[lane], n, k0, bc);
   }
   __syncwarp();
+  // In-place Gauss–Jordan (no pivoting: A is SPD): after pivot c, column c holds the c-th column of the
+  // running inverse. Per pivot every row does n updates (the augmented [A | I] form did 2n − c).
   for (int c = 0; c < n; ++c) {
     const double inv_p = 1.0 / A[c][c];
-    const double f = (lane < n && lane != c) ? A[lane][c] * inv_p : 0.0;
+    const bool other = lane < n && lane != c;
+    const double f = other ? A[lane][c] * inv_p : 0.0;
     __syncwarp();
-    if (lane < n && lane != c)
-      for (int j = c; j < 2 * n; ++j) A[lane][j] = fma(-f, A[c][j], A[lane][j]);
+    if (other) {
+      for (int j = 0; j < n; ++j) A[lane][j] = fma(-f, A[c][j], A[lane][j]);
+      A[lane][c] = -f;
+    }
     __syncwarp();
-    if (lane == c)
-      for (int j = c; j < 2 * n; ++j) A[c][j] *= inv_p;
+    if (lane == c) {
+      for (int j = 0; j < n; ++j) A[c][j] *= inv_p;
+      A[c][c] = inv_p;
+    }
     __syncwarp();
   }
   double* X = chol + (int64_t)b * 2 * n * n + (int64_t)n * n;
-  for (int idx = lane; idx < n * n; idx += 32) X[idx] = A[idx / n][n + idx % n];
+  for (int idx = lane; idx < n * n; idx += 32) X[idx] = A[idx / n][idx % n];
 }
 
 // Dense Cholesky + explicit inverse of the coarsest operator, one thread per sample (n > 32).
@@ -2777,8 +2784,10 @@ __device__ void load_level(const SLev& L, const SolverLevelDev& G, int b, bool h
   });
   const int mcl = L.m / 2;
   const int64_t co = (int64_t)b * mcl * mcl;
-  for (int q = 0; q < 4; ++q)
-    for_nodes(mcl * mcl, [&](int i) { L.pw[q][i] = __ldg(G.pw[q] + co + i); });
+  for_nodes_unrolled(mcl * mcl, [&](int i) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) L.pw[q][i] = __ldg(G.pw[q] + co + i);
+  });
 }
 
 // Whole PCG of one sample per CTA (m ≤ 32): level 0 from k, coarse levels + transfers + coarsest
@@ -2812,8 +2821,10 @@ __global__ void __launch_bounds__(1024) small_pcg_kernel(int m0, int nlev, int b
   });
   {
     const int mcl = m / 2;
-    for (int q = 0; q < 4; ++q)
-      for_nodes(mcl * mcl, [&](int i) { L0.pw[q][i] = __ldg(H.lev[0].pw[q] + (int64_t)b * mcl * mcl + i); });
+    for_nodes_unrolled(mcl * mcl, [&](int i) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) L0.pw[q][i] = __ldg(H.lev[0].pw[q] + (int64_t)b * mcl * mcl + i);
+    });
   }
   for (int l = 1; l < nlev; ++l) load_level(lev[l], H.lev[l], b, l + 1 < nlev);
   const int nc = lev[nlev - 1].N_;

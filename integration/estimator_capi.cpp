@@ -15,6 +15,10 @@
 
 using namespace oscfield;
 
+namespace oscfield {
+MlmcReport mlmc_estimate_gpu(const ProblemSpec& problem, const EstimatorOptions& opt, double h0, double eps,
+                             int initial_levels, int n_gpus);
+}
 extern "C" int oscfield_gpu_configure(int n_gpus, const int* devices, int bc, int qoi);
 extern "C" int oscfield_gpu_set_setup(int mode);
 
@@ -149,6 +153,12 @@ extern "C" {
 
 int oscgpu_mlmc_estimate(const oscgpu_opts* o, double h0, double eps, int initial_levels, oscgpu_report* out) {
   return guard([&] { fill(mlmc_estimate(problem_of(*o), options_of(*o), h0, eps, initial_levels), out); });
+}
+
+// the same estimate on the GPU-resident driver (mlmc_estimate_gpu, oscfield_gpu_seams.cpp)
+int oscgpu_mlmc_estimate_resident(const oscgpu_opts* o, double h0, double eps, int initial_levels, int n_gpus,
+                                  oscgpu_report* out) {
+  return guard([&] { fill(mlmc_estimate_gpu(problem_of(*o), options_of(*o), h0, eps, initial_levels, n_gpus), out); });
 }
 
 int oscgpu_mc_estimate(const oscgpu_opts* o, double eps, double fixed_h /* <= 0: none */, oscgpu_report* out) {

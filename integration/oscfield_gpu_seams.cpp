@@ -14,6 +14,7 @@
 // osc_group over n devices: each batch is cut into contiguous per-device chunks (the chunking of
 // parallel_samples, estimators.cpp:32-63), one host thread per GPU, slot i = sample i on any count.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <map>
@@ -29,6 +30,8 @@
 namespace oscfield {
 EmbeddingOperator build_operator_routed(const GridSpec& grid, const CovarianceModel& model,
                                         const BuildOptions& options);
+MlmcReport mlmc_estimate_gpu(const ProblemSpec& problem, const EstimatorOptions& opt, double h0, double eps,
+                             int initial_levels = 1, int n_gpus = 0);
 namespace {
 
 // cap of the residual history a SolverError carries (the failing slot is re-solved with it kept)
@@ -281,6 +284,95 @@ void run_level_samples(LevelPlan& plan, const GridSpec* coarse_grid, bool trunca
                        std::int64_t to, std::vector<LevelDraw>& draws) {
   draws.resize(static_cast<std::size_t>(to));  // run_level_samples' own contract (estimators.cpp:69)
   run_level_draws(plan, coarse_grid, truncate_fine, truncate_coarse, problem, opt, from, to, draws);
+}
+
+// mlmc_estimate (estimators.hpp; estimators.cpp:414-418) on the GPU-resident driver
+// (osc_mlmc_adaptive, include/oscfield_b200.h): same arguments and report type as the reference's
+// mlmc_estimate, so a caller switches by name. All levels of an allocation pass draw concurrently and
+// the level moments stay in HBM; the levels' spectra come from the routed build_operator (the
+// reference's own by default, so truncation masks match the CPU reference bit for bit; modes 1 / 2 of
+// oscfield_gpu_set_setup hand the driver this repo's host spectrum or let it build them on the
+// device). n_gpus = 0 draws on the calling thread's device, n > 0 over devices 0..n-1.
+namespace {
+struct SpectrumSource {
+  const CovarianceModel* model;
+};
+extern "C" int oscfield_gpu_spectrum_cb(void* user, int m, int* J, std::int64_t* s, double** eig) {
+  try {
+    const auto* src = static_cast<const SpectrumSource*>(user);
+    const EmbeddingOperator op = build_operator_routed(GridSpec::square(m), *src->model, BuildOptions{});
+    *J = op.padding()[0];
+    *s = op.s();
+    *eig = static_cast<double*>(std::malloc(sizeof(double) * static_cast<std::size_t>(op.s())));
+    if (!*eig) return 1;
+    const auto ev = op.eigenvalues();
+    for (std::int64_t i = 0; i < op.s(); ++i) (*eig)[i] = ev[static_cast<std::size_t>(i)];
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+}  // namespace
+
+MlmcReport mlmc_estimate_gpu(const ProblemSpec& problem, const EstimatorOptions& opt, double h0, double eps,
+                             int initial_levels, int n_gpus) {
+  GroupState& gs = group_state();
+  const osc_problem p = problem_of(problem, opt, gs);
+  const CovarianceModel& model = problem.model;
+  osc_mlmc_options o{};
+  o.family = model.family() == CovFamily::Matern ? OSC_COV_MATERN : OSC_COV_SEPARABLE_EXP;
+  o.sigma2 = model.sigma2();
+  o.lambda = model.lambda();
+  o.nu_or_p = o.family == OSC_COV_MATERN ? model.nu() : model.p_norm();
+  o.h0 = h0;
+  o.eps = eps;
+  o.initial_levels = initial_levels;
+  o.l_max = opt.l_max;
+  o.allow_extension = 1;
+  o.seed = opt.seed;
+  o.pilot_n = opt.pilot_n;
+  o.gamma_model = opt.gamma_model;
+  o.alpha = opt.alpha;
+  o.c_alpha = opt.c_alpha;
+  o.c_ratio = opt.c_ratio;
+  o.c_alpha_tilde_ratio = opt.c_alpha_tilde_ratio;
+  o.smoothing = opt.smoothing == SmoothingRule::Off            ? OSC_SMOOTHING_OFF
+                : opt.smoothing == SmoothingRule::HalfSpectrum ? OSC_SMOOTHING_HALF_SPECTRUM
+                                                               : OSC_SMOOTHING_ADAPTIVE;
+  o.use_coarse_s = opt.smoothing_use_coarse_s ? 1 : 0;
+  o.lstar_only = opt.smoothing_lstar_only ? 1 : 0;
+  o.concurrent_levels = 1;
+  static const int env_mode = env_int("OSC_SEAM_SETUP", 0);
+  const int mode = gs.setup_mode >= 0 ? gs.setup_mode : env_mode;
+  SpectrumSource src{&model};
+  if (mode != 2) {  // 2: the driver's own device level setup
+    o.spectrum = oscfield_gpu_spectrum_cb;
+    o.spectrum_user = &src;
+  }
+  osc_mlmc_report r{};
+  if (int rc = osc_mlmc_adaptive(n_gpus, nullptr, &p, &o, &r)) raise(rc);
+  MlmcReport rep;
+  rep.estimate = r.estimate;
+  rep.bias_estimate = r.bias_estimate;
+  rep.sampling_error = r.sampling_error;
+  rep.total_cost_model = r.total_cost_model;
+  rep.total_cost_wall = r.total_cost_wall;
+  rep.converged = r.converged != 0;
+  rep.message = r.message;
+  for (int i = 0; i < r.n_levels; ++i) {
+    LevelStats l;
+    l.n = r.n[i];
+    l.mean_y = r.mean_y[i];
+    l.var_y = r.var_y[i];
+    l.mean_q = r.mean_q[i];
+    l.var_q = r.var_q[i];
+    l.cost_wall_per_sample = r.wall_per_sample[i];
+    l.cost_model_per_sample = std::pow(r.h[i], -opt.gamma_model);
+    l.n_real = r.n_real[i];
+    rep.levels.push_back(l);
+    rep.level_h.push_back(r.h[i]);
+  }
+  return rep;
 }
 
 }  // namespace oscfield

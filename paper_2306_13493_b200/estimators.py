@@ -90,6 +90,8 @@ def lib() -> C.CDLL:
         L.oscgpu_configure.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_int]
         L.oscgpu_set_setup.argtypes = [C.c_int]
         L.oscgpu_mlmc_estimate.argtypes = [C.POINTER(_Opts), C.c_double, C.c_double, C.c_int, C.POINTER(_Report)]
+        L.oscgpu_mlmc_estimate_resident.argtypes = [C.POINTER(_Opts), C.c_double, C.c_double, C.c_int, C.c_int,
+                                                    C.POINTER(_Report)]
         L.oscgpu_mc_estimate.argtypes = [C.POINTER(_Opts), C.c_double, C.c_double, C.POINTER(_Report)]
         L.oscgpu_mc_estimate_fixed_n.argtypes = [C.POINTER(_Opts), C.c_int, C.c_int64, C.POINTER(_Report)]
         L.oscgpu_coarsest_level_bound.restype = C.c_double
@@ -163,6 +165,17 @@ def mlmc_estimate(problem: ProblemSpec, opt: EstimatorOptions, h0: float, eps: f
     _configure(problem, n_gpus)
     o = _opts(problem, opt)
     return _run(lib().oscgpu_mlmc_estimate, C.byref(o), float(h0), float(eps), int(initial_levels))
+
+
+def mlmc_estimate_resident(problem: ProblemSpec, opt: EstimatorOptions, h0: float, eps: float,
+                           initial_levels: int = 1, n_gpus: int = 0) -> MlmcReport:
+    """oscfield::mlmc_estimate_gpu (integration/oscfield_gpu_seams.cpp): the reference's ProblemSpec /
+    EstimatorOptions / MlmcReport around the GPU-resident driver osc_mlmc_adaptive, with the levels'
+    spectra from the routed build_operator (set_setup)."""
+    _configure(problem, 0)
+    o = _opts(problem, opt)
+    return _run(lib().oscgpu_mlmc_estimate_resident, C.byref(o), float(h0), float(eps), int(initial_levels),
+                int(n_gpus))
 
 
 def mc_estimate(problem: ProblemSpec, opt: EstimatorOptions, eps: float, fixed_h: Optional[float] = None,

@@ -206,3 +206,25 @@ def test_driver_collective_path_on_one_device(P, ctx, monkeypatch):
     assert [l.mean_y for l in a.levels] == [l.mean_y for l in b.levels]
     assert [l.var_y for l in a.levels] == [l.var_y for l in b.levels]
     assert a.estimate == b.estimate
+
+
+def test_driver_struct_layout_matches_header(P, tmp_path):
+    """The ctypes mirrors of osc_mlmc_options / osc_mlmc_report / osc_problem have the C layout of
+    include/oscfield_b200.h (sizes and the offsets of the last fields), checked with the C compiler."""
+    import ctypes as C
+    import subprocess
+    from paper_2306_13493_b200 import _lib, mlmc
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "oscfield_b200.h"\n'
+        'int main(void) { printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(osc_mlmc_options), '
+        'offsetof(osc_mlmc_options, spectrum_user), offsetof(osc_mlmc_options, seed), sizeof(osc_mlmc_report), '
+        'offsetof(osc_mlmc_report, message), offsetof(osc_mlmc_report, wall_per_sample), sizeof(osc_problem)); '
+        'return 0; }\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(_lib.ROOT) + "/include", "-o", str(exe), str(src)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [C.sizeof(mlmc.Options), mlmc.Options.spectrum_user.offset, mlmc.Options.seed.offset,
+            C.sizeof(mlmc.Report), mlmc.Report.message.offset, mlmc.Report.wall_per_sample.offset,
+            C.sizeof(_lib.Problem)]
+    assert got == want, (got, want)

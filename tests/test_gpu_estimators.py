@@ -141,3 +141,24 @@ def test_solver_error_carries_history_through_reference(P, E):
         E.mc_estimate_fixed_n(prob, opt, 8, 4)
     h = ei.value.residual_history
     assert h is not None and len(h) >= 1 and np.all(np.isfinite(h)) and h[0] > 1e-10
+
+
+def test_mlmc_estimate_gpu_drop_in(P, E, ref):
+    """oscfield::mlmc_estimate_gpu — the reference's mlmc_estimate signature and report around the
+    GPU-resident driver, spectra from the reference's own build_operator: under config 3's rule
+    (smoothed coarse levels, whose truncation masks depend on the spectrum's bits) it takes the CPU
+    reference's decisions and reproduces its level moments."""
+    import os
+    from oracle import oracle as O
+    api = P.api
+    lam, h0, eps, pilot, l_max = 0.01, 1.0 / 16, 1e-2, 50, 4
+    opts = O.RefOpts.make(family=O.SEP_EXP, sigma2=1.0, lam=lam, nu_or_p=1.0, seed=1, pilot_n=pilot,
+                          threads=os.cpu_count() or 1, l_max=l_max, smoothing=2, lstar_only=1, qoi_kind=0)
+    cpu = ref.mlmc(opts, h0, eps, 1)
+    prob = api.ProblemSpec(api.CovarianceModel.separable_exponential(1.0, lam), api.QoiSpec(api.QoiKind.Point))
+    opt = api.EstimatorOptions(seed=1, pilot_n=pilot, l_max=l_max, smoothing=api.SmoothingRule.Adaptive,
+                               smoothing_lstar_only=True)
+    gpu = E.mlmc_estimate_resident(prob, opt, h0, eps, 1)
+    _same_report(gpu, cpu)
+    routed = E.mlmc_estimate(prob, opt, h0, eps, 1)
+    assert [l.n for l in routed.levels] == [l.n for l in gpu.levels]

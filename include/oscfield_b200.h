@@ -314,7 +314,8 @@ enum { OSC_SMOOTHING_OFF = 0, OSC_SMOOTHING_HALF_SPECTRUM = 1, OSC_SMOOTHING_ADA
 
 /* Optional source of a level's eigenvalues (OSC1 files, the reference's build_operator, …): fills J, s
  * and a malloc'd array of s = (2(m+J))² eigenvalues that the driver releases with free(). Non-zero
- * return = failure (reported as OSC_ERR_EMBEDDING). */
+ * return = failure (reported as OSC_ERR_EMBEDDING). Called once per level, always from the thread that
+ * called osc_mlmc_adaptive (it need not be re-entrant). */
 typedef int (*osc_spectrum_fn)(void* user, int m, int* J, int64_t* s, double** eigenvalues);
 
 typedef struct {

@@ -233,6 +233,26 @@ struct Driver {
       levels.push_back(std::move(L));
     }
     const int nl = last - first + 1;
+    // caller-supplied spectra: one call per level, from this thread only (the callback may be a host
+    // setup that is not re-entrant), shared by the level's devices
+    struct Spectrum {
+      int J = 0;
+      int64_t s = 0;
+      double* eig = nullptr;
+    };
+    std::vector<Spectrum> spectra((size_t)nl);
+    struct FreeAll {
+      std::vector<Spectrum>& v;
+      ~FreeAll() {
+        for (auto& sp : v) std::free(sp.eig);
+      }
+    } free_all{spectra};
+    if (opt.spectrum)
+      for (int i = 0; i < nl; ++i) {
+        Spectrum& sp = spectra[(size_t)i];
+        if (opt.spectrum(opt.spectrum_user, levels[base + (size_t)i]->m, &sp.J, &sp.s, &sp.eig) != 0 || !sp.eig)
+          throw Error(OSC_ERR_EMBEDDING, "osc_mlmc: the spectrum callback failed");
+      }
     // setup of the new levels: all (level, device) pairs at once, each on its own stream
     fan_out(nl * G(), !opt.concurrent_levels, [&](int j) {
       LevelRun& L = *levels[base + (size_t)(j / G())];
@@ -240,15 +260,9 @@ struct Driver {
       OSC_CUDA(cudaSetDevice(devices[g]));
       if (int rc = osc_ctx_create(devices[g], &L.ctx[g])) throw Error(rc, osc_last_error());
       if (opt.spectrum) {
-        int J = 0;
-        int64_t s = 0;
-        double* eig = nullptr;
-        if (opt.spectrum(opt.spectrum_user, L.m, &J, &s, &eig) != 0 || !eig)
-          throw Error(OSC_ERR_EMBEDDING, "osc_mlmc: the spectrum callback failed");
-        const int64_t k = k_trunc_rule(opt, L.h, J, s);
-        const int rc = osc_level_create(L.ctx[g], L.m, J, eig, k, &L.lev[g]);
-        std::free(eig);
-        if (rc) throw Error(rc, osc_last_error());
+        const Spectrum& sp = spectra[(size_t)(j / G())];
+        const int64_t k = k_trunc_rule(opt, L.h, sp.J, sp.s);
+        if (int rc = osc_level_create(L.ctx[g], L.m, sp.J, sp.eig, k, &L.lev[g])) throw Error(rc, osc_last_error());
       } else {
         if (int rc = osc_level_create_device(L.ctx[g], L.m, opt.family, opt.sigma2, opt.lambda, opt.nu_or_p, nullptr,
                                              0, 0.0, 0, &L.lev[g]))

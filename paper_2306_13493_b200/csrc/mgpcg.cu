@@ -2467,6 +2467,7 @@ struct HierDev {
 //     are r/C); a thread owns at most SM_KMAX nodes per level (u of the PCG stays in registers);
 //     reductions cost one barrier; the CTA is sized to the grid (7 CTAs per SM at 16², 2 at 32²).
 constexpr int SM_KMAX = 3;
+constexpr int SM_CSPLIT = 4;  // threads per row of the coarsest solve
 
 struct SLev {
   double *C, *iC;              // diagonal and its reciprocal
@@ -2629,16 +2630,25 @@ __device__ void vcycle_smem(const SLev* lev, int nlev, const double* Ainv, int b
     });
     __syncthreads();
   }
-  {  // coarsest: t = A⁻¹ r, one warp per row (lanes over the columns, shuffle sum): every other warp
-     // of the CTA waits at the barrier below, so the chain is kept short. The inverse stays in global
-     // memory (L1/L2-resident).
+  {  // coarsest: t = A⁻¹ r. Every other warp waits for this solve, so its dependent chain is kept short
+     // without spending a warp per row: SM_CSPLIT threads per row each sum every SM_CSPLIT-th column
+     // (A⁻¹ is symmetric: read by columns, coalesced over the rows; it stays in global memory,
+     // L1/L2-resident), the partial sums meet in shared memory.
     const SLev& C = lev[nlev - 1];
-    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5, nc = C.N_;
-    for (int i = threadIdx.x >> 5; i < nc; i += nw) {
+    const int nc = C.N_;
+    double* part = C.z;  // SM_CSPLIT × nc
+    for (int idx = threadIdx.x; idx < SM_CSPLIT * nc; idx += blockDim.x) {
+      const int p = idx / nc, i = idx - p * nc;
       double v = 0.0;
-      for (int j = lane; j < nc; j += 32) v = fma(__ldg(Ainv + i * nc + j), C.r[j], v);
-      v = warp_sum(v);
-      if (lane == 0) C.t[i] = v;
+      for (int j = p; j < nc; j += SM_CSPLIT) v = fma(__ldg(Ainv + j * nc + i), C.r[j], v);
+      part[idx] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      double v = part[i];
+#pragma unroll
+      for (int p = 1; p < SM_CSPLIT; ++p) v += part[p * nc + i];
+      C.t[i] = v;
     }
     __syncthreads();
   }
@@ -2684,7 +2694,7 @@ __host__ __device__ inline void level_counts(int g, bool last, bool p5, int& n64
   const int N = (g + 1) * (g + 1), mcl = g / 2, pad = g + 2;
   const int a64 = last ? 2 : (p5 ? 7 : 5);      // r, t | z, C, iC | E, N
   const int a32 = last ? 0 : (p5 ? 2 : 6);      // E, N, NE, NW | w0, w1
-  n64 = a64 * (N + pad) + pad;
+  n64 = a64 * (N + pad) + pad + (last ? SM_CSPLIT * N : 0);     // + the coarsest solve's partial sums
   n32 = last ? 0 : a32 * (N + pad) + pad + 4 * mcl * mcl;  // + pw
 }
 __host__ __device__ inline void hier_counts(int m_top, int nlev, bool five_point0, size_t& n64, size_t& n32) {
@@ -2718,6 +2728,10 @@ __device__ double* carve_levels(SLev* lev, double* base, int m_top, int nlev, bo
       L.inv_n0 = 1.0f / (float)(g + 1);
       L.r = d();
       L.t = d();
+      if (l + 1 == nlev) {
+        L.z = c64;  // partial sums of the coarsest solve (SM_CSPLIT × N)
+        c64 += SM_CSPLIT * N;
+      }
       if (l + 1 < nlev) {
         L.z = d();
         L.C = d();

@@ -410,9 +410,23 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
     double* sK = sP + 4 * GP_W * GP_H;
     const double* kb = k0 + (int64_t)b * F.Nn;
     const int kx = ax - 1, ky = ay - 1;
-    for (int i = tid; i < GK_W * GK_H; i += GT_THREADS) {
-      const int lx = i % GK_W, ly = i / GK_W, x = kx + lx, y = ky + ly;
-      sK[i] = ((unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0) ? __ldg(kb + (int64_t)y * n0 + x) : 0.0;
+    {  // all of a thread's k loads are issued before the first is stored (the rolled load → store loop
+       // serialised eight DRAM latencies: a quarter of this kernel's stall samples)
+      constexpr int NKQ = (GK_W * GK_H + GT_THREADS - 1) / GT_THREADS;
+      double kv[NKQ];
+#pragma unroll
+      for (int q = 0; q < NKQ; ++q) {
+        const int i = tid + q * GT_THREADS;
+        const int lx = i % GK_W, ly = i / GK_W, x = kx + lx, y = ky + ly;
+        kv[q] = (i < GK_W * GK_H && (unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0)
+                    ? __ldg(kb + (int64_t)y * n0 + x)
+                    : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < NKQ; ++q) {
+        const int i = tid + q * GT_THREADS;
+        if (i < GK_W * GK_H) sK[i] = kv[q];
+      }
     }
     __syncthreads();
     // level-0 rows (row_k, stride 1) of the raw region from the staged k
@@ -456,7 +470,8 @@ __device__ __forceinline__ void galerkin_tile_body(const double* __restrict__ k0
   } else {
     const int64_t off = (int64_t)b * F.Nn;
     const float* src[4] = {F.E + off, F.N + off, F.NE + off, F.NW + off};
-    for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {
+#pragma unroll 2
+    for (int i = tid; i < GA_W * GA_H; i += GT_THREADS) {  // two nodes' ten loads in flight per thread
       const int lx = i % GA_W, ly = i / GA_W, x = ax + lx, y = ay + ly;
       const bool in = INT || ((unsigned)x < (unsigned)n0 && (unsigned)y < (unsigned)n0);
       const int64_t o = (int64_t)y * n0 + x;
